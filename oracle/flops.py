@@ -1,0 +1,48 @@
+"""FLOP and communication-byte model of one layer (TEST INFRASTRUCTURE).
+
+* SPEC.md:298 forward FLOPs (non-causal, MHA + FFN): (8 b s h^2 + 4 b s^2 h) + 16 b s h^2
+  -> exactly 2^30 at C1 (h = 256, s = 512, b = 1).
+* Model FLOPs per token, causal (SURVEY O-7, the roofline numerator of bench.py):
+    fwd  2 (3h^2 + h^2 + 2hF) + 2 s h       (= 24 h^2 + 2 s h at F = 4h)
+    bwd  2 x fwd                            (dX and dW GEMMs; dQ, dK, dV)
+    total 72 h^2 + 6 s h at F = 4h
+* Comm bytes per rank per layer fwd+bwd (O-7), payload (P-1)/P x full.
+
+Pins: C1 value 2^30; the 4x / 2x scaling under s-doubling; the
+matmul shapes actually executed by oracle.layer (tests/test_oracle_flops.py);
+the comm bytes equal the simulated grid's comm log (tests/test_oracle_strategies.py).
+"""
+from __future__ import annotations
+
+
+def spec_fwd_flops_noncausal(h, s, b=1):
+    return (8 * b * s * h * h + 4 * b * s * s * h) + 16 * b * s * h * h
+
+
+def layer_flops_per_token(h, s, ffn=None, causal=True):
+    """Model FLOPs per token for fwd+bwd of one layer."""
+    f = 4 * h if ffn is None else ffn
+    lin = 2 * (3 * h * h + h * h + 2 * h * f)
+    att = (2 if causal else 4) * s * h
+    return 3 * (lin + att)
+
+
+def layer_flops(h, s, ffn=None, causal=True, b=1):
+    return layer_flops_per_token(h, s, ffn, causal) * s * b
+
+
+def comm_bytes(pi, h, s, P, ffn=None, b=1):
+    """Bytes each rank sends per layer (fwd + bwd), payload convention SPEC.md:109."""
+    f = 4 * h if ffn is None else ffn
+    if P == 1:
+        return 0
+    fr = (P - 1) / P
+    act = s * b * h * 2
+    ar = 2 * fr * 2 * h * 4
+    if pi == 0 or pi == 2:   # TS / METP (same bytes, c x more messages)
+        return int(round(10 * fr * act + ar))
+    if pi == 1:
+        a2a = 2 * fr * (s // P) * b * (3 * h + h) * 2
+        wb = 4 * h * h + 2 * h * f
+        return int(round(a2a + fr * wb * (2 + 2 + 4) + ar))
+    raise KeyError(pi)

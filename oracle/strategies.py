@@ -1,0 +1,424 @@
+"""Per-strategy sharded simulations of one layer, fwd + bwd, fp64 (TEST INFRASTRUCTURE).
+
+Each function f_{pi} maps spec-layout input shards + spec-layout weight shards
+to spec-layout output shards on a simulated Grid (Eqs. 7-8, PAPER.md:228-232;
+"identical parameter lists ... and return types").  The
+dataflows are those of SURVEY §8(c) O-5 / DESIGN.md:
+
+  MegatronTS: AllGather on s before MHA / FFN, column-
+      parallel QKV / FC1, row-parallel proj / FC2, ReduceScatter after.
+  UlyssesZ   (R-12): ZeRO3-style AllGather of the weight
+      shards, All-to-All sequence->heads around attention and back.
+  METP       (R-11 "R-METP"): the TS dataflow split into
+      c waves (wave k = local rows [k s/(Pc), (k+1) s/(Pc)) of every shard),
+      per-wave AG / RS, attention over the full position-ordered Q/K/V (a
+      query-chunk x KV-chunk loop), FFN intermediates recomputed in backward.
+
+Every saved activation is registered in the grid's memory ledger with its
+device byte size (bf16 = 2 B, fp32 statistics = 4 B) and the backward reads
+ONLY registered tensors, so the ledger is an honest recount of what must be
+kept between forward and backward (pin for oracle/memory.py).
+
+Pins: every strategy at every P in {1, 2, 4, 8} reproduces layer.layer_fwd /
+layer_bwd to <= 1e-12 (north_star); switched chains equal the
+L-layer unsharded stack; comm-log multisets match the
+documented signature.  METP's true external schedule is
+"parity unpinned" beyond that invariant.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
+                    rmsnorm, rmsnorm_bwd)
+
+TS, UZ, METP = 0, 1, 2
+NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
+
+
+class Cfg:
+    def __init__(self, h, n, ffn, causal=True, eps=EPS, theta=ROPE_THETA, metp_chunks=None):
+        self.h, self.n, self.ffn = h, n, ffn
+        self.causal, self.eps, self.theta = causal, eps, theta
+        self.metp_chunks = metp_chunks
+
+
+def _save(grid, r, saved, name, arr, bpe):
+    saved[name] = arr
+    saved.setdefault("_ids", []).append(grid.track(r, arr.size * bpe, "saved"))
+
+
+def _release(grid, saved):
+    for hid in saved.pop("_ids", []):
+        grid.release(hid)
+
+
+def _apply_norm(x, r, g):
+    """Recompute u = x r g from the saved input and rstd (no new statistics)."""
+    return x * r[..., None] * g
+
+
+def _zero_grads(W):
+    p = len(W["w_qkv_t"])
+    return {k: [np.zeros_like(a) for a in W[src]] for k, src in
+            [("dw_qkv_t", "w_qkv_t"), ("dw_proj", "w_proj"), ("dw_in_t", "w_in_t"),
+             ("dw_out", "w_out"), ("dg1", "g1"), ("dg2", "g2")]} | {"_p": p}
+
+
+# ------------------------------------------------------------------ MegatronTS
+def ts_fwd(grid, xs, W, cfg):
+    P = grid.p
+    s = xs[0].shape[0] * P
+    nl = cfg.n // P
+    pos = np.arange(s)
+    saved = [dict() for _ in range(P)]
+    u, r1 = [], []
+    for r in range(P):
+        ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
+        u.append(ur)
+        r1.append(rr)
+    U = grid.all_gather(u)                                         # AG(u)
+    qkv = [U[r] @ W["w_qkv_t"][r].T for r in range(P)]             # column-parallel Eq. 1
+    att = [mha_core_fwd(qkv[r], nl, pos, cfg.causal, cfg.theta) for r in range(P)]
+    opart = [att[r][0] @ W["w_proj"][r] for r in range(P)]        # row-parallel Eq. 3
+    o = grid.reduce_scatter(opart)                                 # RS(o)
+    x1 = [xs[r] + o[r] for r in range(P)]
+    v, r2 = [], []
+    for r in range(P):
+        vr, _, rr = rmsnorm(x1[r], W["g2"][r], cfg.eps)
+        v.append(vr)
+        r2.append(rr)
+    V = grid.all_gather(v)                                         # AG(v)
+    hpre = [V[r] @ W["w_in_t"][r].T for r in range(P)]
+    zpart = [gelu(hpre[r]) @ W["w_out"][r] for r in range(P)]
+    z = grid.reduce_scatter(zpart)                                 # RS(z)
+    y = [x1[r] + z[r] for r in range(P)]
+    for r in range(P):
+        sv = saved[r]
+        _save(grid, r, sv, "x", xs[r], 2)
+        _save(grid, r, sv, "r1", r1[r], 4)
+        _save(grid, r, sv, "qkv", qkv[r], 2)
+        _save(grid, r, sv, "a", att[r][0], 2)
+        _save(grid, r, sv, "lse", att[r][1], 4)
+        _save(grid, r, sv, "x1", x1[r], 2)
+        _save(grid, r, sv, "r2", r2[r], 4)
+        _save(grid, r, sv, "h", hpre[r], 2)
+    return y, saved, dict(o=o, z=z)
+
+
+def ts_bwd(grid, dys, saved, W, cfg, grads):
+    P = grid.p
+    s = dys[0].shape[0] * P
+    nl = cfg.n // P
+    pos = np.arange(s)
+    sv = saved
+    dZ = grid.all_gather(dys)                                      # AG(dz)
+    v = [_apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r]) for r in range(P)]
+    V = grid.all_gather(v)                                         # AG(v) re-gather
+    dvpart = []
+    for r in range(P):
+        hp = sv[r]["h"]
+        dg = dZ[r] @ W["w_out"][r].T
+        dh = dg * gelu_grad(hp)
+        grads["dw_out"][r] += np.einsum("sbf,sbh->fh", gelu(hp), dZ[r])
+        grads["dw_in_t"][r] += np.einsum("sbf,sbh->fh", dh, V[r])
+        dvpart.append(dh @ W["w_in_t"][r])
+    dv = grid.reduce_scatter(dvpart)                               # RS(dv)
+    dx1, dg2 = [], []
+    for r in range(P):
+        xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
+        d, dgr = rmsnorm_bwd(dv[r], xhat2, sv[r]["r2"], W["g2"][r])
+        dx1.append(dys[r] + d)
+        dg2.append(dgr)
+    dX1 = grid.all_gather(dx1)                                     # AG(dx1)
+    u = [_apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r]) for r in range(P)]
+    dqkv = []
+    for r in range(P):
+        da = dX1[r] @ W["w_proj"][r].T
+        grads["dw_proj"][r] += np.einsum("sbi,sbj->ij", sv[r]["a"], dX1[r])
+        dqkv.append(mha_core_bwd(da, sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, pos,
+                                 cfg.causal, cfg.theta))
+    U = grid.all_gather(u)                                         # AG(u) re-gather
+    dupart = []
+    for r in range(P):
+        grads["dw_qkv_t"][r] += np.einsum("sbj,sbh->jh", dqkv[r], U[r])
+        dupart.append(dqkv[r] @ W["w_qkv_t"][r])
+    du = grid.reduce_scatter(dupart)                               # RS(du)
+    dx, dg1 = [], []
+    for r in range(P):
+        xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
+        d, dgr = rmsnorm_bwd(du[r], xhat1, sv[r]["r1"], W["g1"][r])
+        dx.append(dx1[r] + d)
+        dg1.append(dgr)
+    _finish_dgamma(grid, grads, dg1, dg2)
+    for r in range(P):
+        _release(grid, sv[r])
+    return dx
+
+
+def _finish_dgamma(grid, grads, dg1, dg2):
+    P = grid.p
+    cat = grid.all_reduce([np.concatenate([dg1[r], dg2[r]]) for r in range(P)])  # AR(dg1||dg2)
+    hh = dg1[0].shape[0]
+    for r in range(P):
+        grads["dg1"][r] += cat[r][:hh]
+        grads["dg2"][r] += cat[r][hh:]
+
+
+# ------------------------------------------------------------------ UlyssesZ
+def _gather_weights(grid, W):
+    return dict(
+        w_qkv_t=grid.all_gather(W["w_qkv_t"]),   # rows: head-group-major [g0 Q,K,V | g1 ...]
+        w_proj=grid.all_gather(W["w_proj"]),
+        w_in_t=grid.all_gather(W["w_in_t"]),
+        w_out=grid.all_gather(W["w_out"]),
+    )
+
+
+def uz_fwd(grid, xs, W, cfg):
+    P = grid.p
+    sl = xs[0].shape[0]
+    s = sl * P
+    nl = cfg.n // P
+    Wf = _gather_weights(grid, W)                                  # 4 x AG(W)
+    saved = [dict() for _ in range(P)]
+    u, r1, qkv_loc = [], [], []
+    for r in range(P):
+        ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
+        u.append(ur)
+        r1.append(rr)
+        qkv_loc.append(ur @ Wf["w_qkv_t"][r].T)     # [s/P, b, 3h], head-group-major columns
+    # A2A seq -> heads: send column block j (3h/P wide) to rank j, concat along s
+    qkv = grid.all_to_all(qkv_loc, split_axis=2, concat_axis=0)
+    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta) for r in range(P)]
+    # A2A heads -> seq: send row block j (s/P rows) to rank j, concat along columns
+    afull = grid.all_to_all([att[r][0] for r in range(P)], split_axis=0, concat_axis=2)
+    o = [afull[r] @ Wf["w_proj"][r] for r in range(P)]
+    x1 = [xs[r] + o[r] for r in range(P)]
+    y, z = [], []
+    for r in range(P):
+        vr, _, rr = rmsnorm(x1[r], W["g2"][r], cfg.eps)
+        hp = vr @ Wf["w_in_t"][r].T
+        zr = gelu(hp) @ Wf["w_out"][r]
+        z.append(zr)
+        y.append(x1[r] + zr)
+        sv = saved[r]
+        _save(grid, r, sv, "x", xs[r], 2)
+        _save(grid, r, sv, "r1", r1[r], 4)
+        _save(grid, r, sv, "qkv", qkv[r], 2)
+        _save(grid, r, sv, "a", att[r][0], 2)
+        _save(grid, r, sv, "lse", att[r][1], 4)
+        _save(grid, r, sv, "afull", afull[r], 2)
+        _save(grid, r, sv, "x1", x1[r], 2)
+        _save(grid, r, sv, "r2", rr, 4)
+        _save(grid, r, sv, "h", hp, 2)
+    return y, saved, dict(o=o, z=z)
+
+
+def uz_bwd(grid, dys, saved, W, cfg, grads):
+    P = grid.p
+    sl = dys[0].shape[0]
+    s = sl * P
+    nl = cfg.n // P
+    sv = saved
+    Wf = _gather_weights(grid, W)                                  # 4 x AG(W) again
+    dwo, dwi, dwp, dwq = [], [], [], []
+    dx1, dg2, dafull = [], [], []
+    for r in range(P):
+        hp = sv[r]["h"]
+        v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
+        dg = dys[r] @ Wf["w_out"][r].T
+        dh = dg * gelu_grad(hp)
+        dwo.append(np.einsum("sbf,sbh->fh", gelu(hp), dys[r]))
+        dwi.append(np.einsum("sbf,sbh->fh", dh, v))
+        dv = dh @ Wf["w_in_t"][r]
+        xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
+        d, dgr = rmsnorm_bwd(dv, xhat2, sv[r]["r2"], W["g2"][r])
+        dx1.append(dys[r] + d)
+        dg2.append(dgr)
+        dafull.append(dx1[r] @ Wf["w_proj"][r].T)
+        dwp.append(np.einsum("sbi,sbj->ij", sv[r]["afull"], dx1[r]))
+    # A2A(dO): seq -> heads (column block j to rank j)
+    da = grid.all_to_all(dafull, split_axis=2, concat_axis=0)
+    dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
+                         cfg.causal, cfg.theta) for r in range(P)]
+    # A2A(dQKV): heads -> seq (row block j to rank j, concat along columns)
+    dqkv_loc = grid.all_to_all(dqkv, split_axis=0, concat_axis=2)
+    dx, dg1 = [], []
+    for r in range(P):
+        u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
+        dwq.append(np.einsum("sbj,sbh->jh", dqkv_loc[r], u))
+        du = dqkv_loc[r] @ Wf["w_qkv_t"][r]
+        xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
+        d, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
+        dx.append(dx1[r] + d)
+        dg1.append(dgr)
+    # ZeRO3: reduce-scatter full local dW (fp32) into spec shards
+    for key, full in (("dw_qkv_t", dwq), ("dw_proj", dwp), ("dw_in_t", dwi), ("dw_out", dwo)):
+        part = grid.reduce_scatter(full, axis=0, bpe=4)
+        for r in range(P):
+            grads[key][r] += part[r]
+    _finish_dgamma(grid, grads, dg1, dg2)
+    for r in range(P):
+        _release(grid, sv[r])
+    return dx
+
+
+# ------------------------------------------------------------------ METP (R-METP)
+def _wave_rows(sl, c, k):
+    w = sl // c
+    return slice(k * w, (k + 1) * w)
+
+
+def _wave_positions(P, sl, c, k):
+    """Global positions of the AG'd wave-k rows, rank-major: r' s/P + k s/(Pc) + j."""
+    w = sl // c
+    return np.concatenate([r * sl + k * w + np.arange(w) for r in range(P)])
+
+
+def metp_chunks(cfg, P):
+    return cfg.metp_chunks if cfg.metp_chunks else P
+
+
+def metp_fwd(grid, xs, W, cfg):
+    P = grid.p
+    sl = xs[0].shape[0]
+    s = sl * P
+    nl = cfg.n // P
+    c = metp_chunks(cfg, P)
+    if sl % c:
+        raise ValueError(f"s/P={sl} not divisible by metp_chunks={c} (SPEC.md:184)")
+    hq = 3 * cfg.h // P
+    b = xs[0].shape[1]
+    saved = [dict() for _ in range(P)]
+    u, r1 = [], []
+    for r in range(P):
+        ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
+        u.append(ur)
+        r1.append(rr)
+    qkv = [np.zeros((s, b, hq)) for _ in range(P)]     # full-s, position-ordered
+    for k in range(c):
+        rows = _wave_rows(sl, c, k)
+        Uw = grid.all_gather([u[r][rows] for r in range(P)])       # AG(u) wave k
+        posw = _wave_positions(P, sl, c, k)
+        for r in range(P):
+            qkv[r][posw] = Uw[r] @ W["w_qkv_t"][r].T
+    # attention over the full sequence (query-chunk x KV-chunk two-level loop)
+    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta) for r in range(P)]
+    o = [np.zeros_like(xs[r]) for r in range(P)]
+    for k in range(c):
+        rows = _wave_rows(sl, c, k)
+        posw = _wave_positions(P, sl, c, k)
+        ow = grid.reduce_scatter([att[r][0][posw] @ W["w_proj"][r] for r in range(P)])  # RS(o)
+        for r in range(P):
+            o[r][rows] = ow[r]
+    x1 = [xs[r] + o[r] for r in range(P)]
+    v, r2 = [], []
+    for r in range(P):
+        vr, _, rr = rmsnorm(x1[r], W["g2"][r], cfg.eps)
+        v.append(vr)
+        r2.append(rr)
+    z = [np.zeros_like(xs[r]) for r in range(P)]
+    for k in range(c):
+        rows = _wave_rows(sl, c, k)
+        Vw = grid.all_gather([v[r][rows] for r in range(P)])       # AG(v) wave k
+        zw = grid.reduce_scatter([gelu(Vw[r] @ W["w_in_t"][r].T) @ W["w_out"][r]
+                                  for r in range(P)])             # RS(z) wave k
+        for r in range(P):
+            z[r][rows] = zw[r]
+    y = [x1[r] + z[r] for r in range(P)]
+    for r in range(P):
+        sv = saved[r]
+        _save(grid, r, sv, "x", xs[r], 2)
+        _save(grid, r, sv, "r1", r1[r], 4)
+        _save(grid, r, sv, "qkv", qkv[r], 2)
+        _save(grid, r, sv, "a", att[r][0], 2)
+        _save(grid, r, sv, "lse", att[r][1], 4)
+        _save(grid, r, sv, "x1", x1[r], 2)
+        _save(grid, r, sv, "r2", r2[r], 4)
+    return y, saved, dict(o=o, z=z)
+
+
+def metp_bwd(grid, dys, saved, W, cfg, grads):
+    P = grid.p
+    sl = dys[0].shape[0]
+    s = sl * P
+    nl = cfg.n // P
+    c = metp_chunks(cfg, P)
+    sv = saved
+    dx1 = [np.zeros_like(d) for d in dys]
+    dg2 = [np.zeros(cfg.h) for _ in range(P)]
+    for k in range(c):   # FFN backward, recomputing v, H, G per wave
+        rows = _wave_rows(sl, c, k)
+        dZw = grid.all_gather([dys[r][rows] for r in range(P)])    # AG(dz) wave k
+        vloc = [_apply_norm(sv[r]["x1"][rows], sv[r]["r2"][rows], W["g2"][r]) for r in range(P)]
+        Vw = grid.all_gather(vloc)                                 # AG(v) wave k
+        dvpart = []
+        for r in range(P):
+            hp = Vw[r] @ W["w_in_t"][r].T
+            dg = dZw[r] @ W["w_out"][r].T
+            dh = dg * gelu_grad(hp)
+            grads["dw_out"][r] += np.einsum("sbf,sbh->fh", gelu(hp), dZw[r])
+            grads["dw_in_t"][r] += np.einsum("sbf,sbh->fh", dh, Vw[r])
+            dvpart.append(dh @ W["w_in_t"][r])
+        dvw = grid.reduce_scatter(dvpart)                          # RS(dv) wave k
+        for r in range(P):
+            xhat2 = sv[r]["x1"][rows] * sv[r]["r2"][rows][..., None]
+            d, dgr = rmsnorm_bwd(dvw[r], xhat2, sv[r]["r2"][rows], W["g2"][r])
+            dx1[r][rows] = dys[r][rows] + d
+            dg2[r] += dgr
+    hl = cfg.h // P
+    b = dys[0].shape[1]
+    da = [np.zeros((s, b, hl)) for _ in range(P)]
+    for k in range(c):   # projection backward per wave
+        rows = _wave_rows(sl, c, k)
+        posw = _wave_positions(P, sl, c, k)
+        dX1w = grid.all_gather([dx1[r][rows] for r in range(P)])   # AG(dx1) wave k
+        for r in range(P):
+            da[r][posw] = dX1w[r] @ W["w_proj"][r].T
+            grads["dw_proj"][r] += np.einsum("sbi,sbj->ij", sv[r]["a"][posw], dX1w[r])
+    dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
+                         cfg.causal, cfg.theta) for r in range(P)]
+    dx = [np.zeros_like(d) for d in dys]
+    dg1 = [np.zeros(cfg.h) for _ in range(P)]
+    for k in range(c):   # QKV backward per wave
+        rows = _wave_rows(sl, c, k)
+        posw = _wave_positions(P, sl, c, k)
+        uloc = [_apply_norm(sv[r]["x"][rows], sv[r]["r1"][rows], W["g1"][r]) for r in range(P)]
+        Uw = grid.all_gather(uloc)                                 # AG(u) wave k
+        dupart = []
+        for r in range(P):
+            grads["dw_qkv_t"][r] += np.einsum("sbj,sbh->jh", dqkv[r][posw], Uw[r])
+            dupart.append(dqkv[r][posw] @ W["w_qkv_t"][r])
+        duw = grid.reduce_scatter(dupart)                          # RS(du) wave k
+        for r in range(P):
+            xhat1 = sv[r]["x"][rows] * sv[r]["r1"][rows][..., None]
+            d, dgr = rmsnorm_bwd(duw[r], xhat1, sv[r]["r1"][rows], W["g1"][r])
+            dx[r][rows] = dx1[r][rows] + d
+            dg1[r] += dgr
+    _finish_dgamma(grid, grads, dg1, dg2)
+    for r in range(P):
+        _release(grid, sv[r])
+    return dx
+
+
+REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd)}
+
+
+def layer_fwd(pi, grid, xs, W, cfg):
+    """Registry lookup f_pi — the uniform signature."""
+    if pi not in REGISTRY:
+        raise KeyError(f"unknown strategy {pi} (SPEC.md:244)")
+    return REGISTRY[pi][0](grid, xs, W, cfg)
+
+
+def layer_bwd(pi, grid, dys, saved, W, cfg, grads):
+    if pi not in REGISTRY:
+        raise KeyError(f"unknown strategy {pi} (SPEC.md:244)")
+    return REGISTRY[pi][1](grid, dys, saved, W, cfg, grads)
+
+
+def new_grads(W):
+    g = _zero_grads(W)
+    g.pop("_p")
+    return g

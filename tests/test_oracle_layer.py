@@ -1,0 +1,175 @@
+"""Pins for oracle/layer.py against what the paper and mathematics fix."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layer as L
+from synth import layer_inputs
+
+
+def _inputs(h=16, n=2, ffn=64, s=8, b=1, seed=3):
+    d = layer_inputs(h, n, ffn, s, b, seed=seed)
+    return d
+
+
+def test_attention_single_token_is_v():
+    # s = 1 => softmax over one key is 1, attention output = V
+    rng = np.random.default_rng(0)
+    q, k, v = rng.normal(size=(3, 1, 8))
+    a, lse = L.attention_fwd(q, k, v)
+    assert np.array_equal(a, v)
+    assert np.isclose(lse[0], float(q[0] @ k[0]) / math.sqrt(8))
+
+
+def test_attention_identical_keys_is_causal_prefix_mean():
+    # identical keys => constant scores => uniform weights over the causal prefix,
+    # A_t = mean(V[0..t]) and LSE_t = log(t+1) + q_t.k / sqrt(d) (closed form)
+    rng = np.random.default_rng(1)
+    s, d = 13, 8
+    q = rng.normal(size=(s, d))
+    k = np.tile(rng.normal(size=(1, d)), (s, 1))
+    v = rng.normal(size=(s, d))
+    a, lse = L.attention_fwd(q, k, v, causal=True, block=4)
+    for t in range(s):
+        assert np.allclose(a[t], v[: t + 1].mean(axis=0), atol=1e-13)
+        assert np.isclose(lse[t], math.log(t + 1) + q[t] @ k[0] / math.sqrt(d), atol=1e-13)
+    a2, _ = L.attention_fwd(q, k, v, causal=False)
+    assert np.allclose(a2, np.tile(v.mean(axis=0), (s, 1)), atol=1e-13)
+
+
+def test_attention_naive_loops():
+    # a hand-rolled loop oracle on s <= 4 agrees to 1e-12
+    rng = np.random.default_rng(2)
+    s, d = 4, 6
+    q, k, v = rng.normal(size=(3, s, d))
+    a, _ = L.attention_fwd(q, k, v, causal=True, block=2)
+    for t in range(s):
+        w = [math.exp(sum(q[t, j] * k[u, j] for j in range(d)) / math.sqrt(d)) for u in range(t + 1)]
+        z = sum(w)
+        for j in range(d):
+            ref = sum(w[u] * v[u, j] for u in range(t + 1)) / z
+            assert abs(a[t, j] - ref) < 1e-12
+
+
+def test_rope_identity_at_zero_and_relative():
+    d = 16
+    rng = np.random.default_rng(4)
+    x = rng.normal(size=(1, d))
+    c, s = L.rope_cos_sin([0], d)
+    assert np.array_equal(L.rope_apply(x, c, s), x)
+    # q.k after RoPE depends only on the position difference (rotation property)
+    q, k = rng.normal(size=(2, 1, d))
+    def dot(tq, tk):
+        cq, sq = L.rope_cos_sin([tq], d)
+        ck, sk = L.rope_cos_sin([tk], d)
+        return float(L.rope_apply(q, cq, sq)[0] @ L.rope_apply(k, ck, sk)[0])
+    assert np.isclose(dot(7, 3), dot(1007, 1003), atol=1e-9)
+    assert np.isclose(dot(5, 5), float(q[0] @ k[0]), atol=1e-12)
+    # complex view: pair (x_k, x_{k+d/2}) is multiplied by exp(i t theta^(-2k/d))
+    t = 11
+    c1, s1 = L.rope_cos_sin([t], d)
+    r = L.rope_apply(x, c1, s1)[0]
+    for kk in range(d // 2):
+        z = complex(x[0, kk], x[0, kk + d // 2]) * np.exp(1j * t * 10000.0 ** (-2 * kk / d))
+        assert np.isclose(r[kk], z.real) and np.isclose(r[kk + d // 2], z.imag)
+    # backward is the transpose rotation: <R x, y> == <x, R^T y>
+    y = rng.normal(size=(1, d))
+    assert np.isclose(float(L.rope_apply(x, c1, s1)[0] @ y[0]),
+                      float(x[0] @ L.rope_apply_t(y, c1, s1)[0]))
+
+
+def test_rmsnorm_and_gelu_closed_forms():
+    from scipy.stats import norm
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(5, 1, 32)) * 3
+    u, xhat, r = L.rmsnorm(x, np.ones(32), eps=0.0)
+    assert np.allclose(np.mean(u * u, axis=-1), 1.0)
+    u2, _, _ = L.rmsnorm(7.0 * x, np.ones(32), eps=0.0)   # scale invariance
+    assert np.allclose(u, u2)
+    z = np.linspace(-6, 6, 101)
+    assert np.allclose(L.gelu(z), z * norm.cdf(z), atol=1e-15)
+    assert np.allclose(L.gelu_grad(z), norm.cdf(z) + z * norm.pdf(z), atol=1e-14)
+
+
+def test_zero_w_in_gives_zero_z():
+    # W_in = 0 => Z = GELU(0) W_out = 0 and Y = X1
+    d = _inputs()
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], np.zeros_like(d["w_in"]), d["w_out"],
+                       d["g1"], d["g2"], n=2)
+    assert np.array_equal(c["z"], np.zeros_like(c["z"]))
+    assert np.array_equal(y, c["x1"])
+
+
+def _torch_layer(x, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True, eps=1e-5):
+    """Independent torch fp64 implementation from library routines
+    (F.rms_norm, F.scaled_dot_product_attention, F.gelu)."""
+    import torch.nn.functional as F
+    s, b, h = x.shape
+    d = h // n
+    def norm(t, g):
+        return F.rms_norm(t, (h,), g, eps=eps)
+    u = norm(x, g1)
+    qkv = u @ w_qkv
+    q, k, v = qkv.split(h, dim=-1)
+    def heads(t):
+        return t.reshape(s, b, n, d).permute(1, 2, 0, 3)
+    q, k, v = heads(q), heads(k), heads(v)
+    pos = torch.arange(s, dtype=torch.float64)
+    inv = 10000.0 ** (-2 * torch.arange(d // 2, dtype=torch.float64) / d)
+    ang = pos[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], -1)
+    sin = torch.cat([ang.sin(), ang.sin()], -1)
+    def rot(t):
+        t1, t2 = t[..., : d // 2], t[..., d // 2:]
+        return t * cos + torch.cat([-t2, t1], -1) * sin
+    a = F.scaled_dot_product_attention(rot(q), rot(k), v, is_causal=causal)
+    a = a.permute(2, 0, 1, 3).reshape(s, b, h)
+    x1 = x + a @ w_proj
+    y = x1 + F.gelu(norm(x1, g2) @ w_in) @ w_out
+    return y
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("b", [1, 2])
+def test_layer_fwd_bwd_vs_torch_autograd(causal, b):
+    d = _inputs(h=16, n=4, ffn=48, s=9, b=b, seed=7)
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"],
+                       n=4, causal=causal)
+    g = L.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"],
+                    n=4, causal=causal)
+    names = ["x", "w_qkv", "w_proj", "w_in", "w_out", "g1", "g2"]
+    tt = {k: torch.tensor(d[k], dtype=torch.float64, requires_grad=True) for k in names}
+    yt = _torch_layer(*(tt[k] for k in names), n=4, causal=causal)
+    assert np.allclose(yt.detach().numpy(), y, rtol=1e-12, atol=1e-12)
+    yt.backward(torch.tensor(d["dy"]))
+    for k, gk in [("x", "dx"), ("w_qkv", "dw_qkv"), ("w_proj", "dw_proj"), ("w_in", "dw_in"),
+                  ("w_out", "dw_out"), ("g1", "dg1"), ("g2", "dg2")]:
+        ref = tt[k].grad.numpy()
+        err = np.linalg.norm(ref - g[gk]) / np.linalg.norm(ref)
+        assert err < 1e-12, (k, err)
+
+
+def test_layer_bwd_finite_differences():
+    d = _inputs(h=8, n=2, ffn=16, s=5, b=1, seed=11)
+    args = dict(n=2)
+    def loss(dd):
+        y, _ = L.layer_fwd(dd["x"], dd["w_qkv"], dd["w_proj"], dd["w_in"], dd["w_out"], dd["g1"],
+                           dd["g2"], **args)
+        return float(np.sum(y * d["dy"]))
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **args)
+    g = L.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **args)
+    rng = np.random.default_rng(0)
+    eps = 1e-6
+    for key, gkey in [("x", "dx"), ("w_qkv", "dw_qkv"), ("w_proj", "dw_proj"), ("w_in", "dw_in"),
+                      ("w_out", "dw_out"), ("g1", "dg1"), ("g2", "dg2")]:
+        for _ in range(3):
+            idx = tuple(rng.integers(0, n) for n in d[key].shape)
+            dp = {k: v.copy() for k, v in d.items()}
+            dm = {k: v.copy() for k, v in d.items()}
+            dp[key][idx] += eps
+            dm[key][idx] -= eps
+            fd = (loss(dp) - loss(dm)) / (2 * eps)
+            an = g[gkey][idx]
+            assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (key, idx, fd, an)
