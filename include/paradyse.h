@@ -1,0 +1,231 @@
+/* paradyse.h — C ABI of the B200-native ParaDySe hot path (arXiv 2511.13198).
+ *
+ * The calls follow the paper's statement of the problem:
+ *   - pds_plan(seq_len) -> layer-wise strategy vector Pi* (Eqs. 5-6, PAPER.md:112-116,
+ *     Algorithm 1, cost model Eq. 9);
+ *   - pds_layer_fwd / pds_layer_bwd(strategy, shard): one Transformer layer
+ *     f_{pi,MHA} then f_{pi,FFN} (Eqs. 7-8) over the unified
+ *     boundary layout of Table 2's "Specification" row.
+ *
+ * Conventions (all calls):
+ *   - Every call returns pds_status (0 = OK).  No exception crosses the ABI.  On
+ *     error, pds_last_error() returns a thread-local message naming the offending
+ *     argument / axis / value.
+ *   - Device pointers are plain CUDA device addresses (the caller owns them, e.g.
+ *     torch tensors passed by data_ptr).  Host pointers are marked "host".
+ *   - Streams are cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *     device work of a call is enqueued on that stream; calls do not synchronise
+ *     the host unless stated.
+ *   - Dtypes: activations / weights bf16; weight gradients fp32, ACCUMULATED (+=).
+ *   - Boundary activation layout: [s/P, b, h] row-major bf16, rank r holding
+ *     global positions [r*s/P, (r+1)*s/P) (reading R-10).  This build supports
+ *     b = 1 (other b -> PDS_ENOTIMPL).
+ *   - Weight shards (spec layout, reading R-9), rank r of P, n heads, d = h/n, F = ffn:
+ *       w_qkv_t [3h/P, h]  rows: Q rows of head group r (heads [r n/P, (r+1) n/P)),
+ *                          then its K rows, then its V rows  ((3h/p x h)^T of Table 2)
+ *       w_proj  [h/P, h]   rows [r h/P, (r+1) h/P) of W_proj
+ *       w_in_t  [F/P, h]   rows [r F/P, (r+1) F/P) of W_in^T   ((4h/p x h)^T)
+ *       w_out   [F/P, h]   rows [r F/P, (r+1) F/P) of W_out
+ *       g1, g2  [h]        RMSNorm gains, replicated
+ *   - Divisibility (P | s, P | n, 128 | s/P, metp_chunks | s/P) is a hard error
+ *     (PDS_EDIVISIBILITY), never padded: the caller pads (reading R-15).
+ */
+#ifndef PARADYSE_H
+#define PARADYSE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PDS_OK = 0,
+  PDS_EINVAL = -1,         /* bad argument (NULL pointer, L = 0, P = 0, ...)           */
+  PDS_EDIVISIBILITY = -2,  /* s, n or chunk count not divisible as required            */
+  PDS_ESTRATEGY = -3,      /* unknown / disabled strategy id                           */
+  PDS_ENOMEM = -4,         /* device allocation failed (cudaErrorMemoryAllocation)     */
+  PDS_ECUDA = -5,          /* any other CUDA error                                     */
+  PDS_ENCCL = -6,          /* NCCL error                                               */
+  PDS_ESTATE = -7,         /* call order / state error (e.g. bwd strategy != fwd)      */
+  PDS_ENOCOSTS = -8,       /* pds_plan without a loaded cost bundle                    */
+  PDS_ENOTIMPL = -9        /* feature outside this build (e.g. b > 1)                  */
+} pds_status;
+
+/* Strategy ids, stored as uint8_t in plans. */
+typedef enum {
+  PDS_MEGATRON_TS = 0,     /* Megatron-LM TP+SP                    */
+  PDS_ULYSSES_Z = 1,       /* DeepSpeed Ulysses + ZeRO3 weight gathering*/
+  PDS_METP = 2             /* METP-style chunked, memory-bounded (R-11)  */
+} pds_strategy;
+#define PDS_N_STRATEGIES 3
+
+/* pds_plan flags */
+#define PDS_PLAN_INFEASIBLE 1u  /* no plan satisfies Eq. 6; least-memory fallback returned */
+#define PDS_PLAN_CACHED 2u      /* served from the (b, s) dictionary D     */
+#define PDS_PLAN_EARLY 4u       /* early termination (R-18)             */
+#define PDS_PLAN_SMOOTHED 8u    /* previous plan retained by gamma-smoothing (R-19)       */
+
+/* Model configuration C = (h, n, L) plus the north_star additions. */
+typedef struct {
+  int32_t h;              /* hidden size                                     */
+  int32_t n_heads;        /* attention heads n (d = h / n, d in {64, 128})   */
+  int32_t ffn;            /* FFN width F (4h in the paper, Eq. 4)            */
+  int32_t n_layers;       /* L                                               */
+  int32_t batch;          /* b (must be 1 in this build)                     */
+  float norm_eps;         /* RMSNorm epsilon (1e-5, R-2)                     */
+  double rope_theta;      /* RoPE base (10000, R-3)                          */
+  int32_t causal;         /* 1 = causal mask (north_star), 0 = none          */
+  int32_t metp_chunks;    /* METP wave count c (0 -> P)                      */
+  int32_t metp_recompute; /* 0 = recompute FFN intermediates in bwd (R-11)   */
+} pds_model;
+
+typedef struct pds_ctx pds_ctx;     /* opaque: rank, P, comm, streams, arenas, costs, plan cache */
+typedef struct pds_group pds_group; /* opaque: in-process loopback group (P virtual ranks on    */
+                                    /* one device; used by single-GPU multi-rank parity tests) */
+typedef struct pds_saved pds_saved; /* opaque: one layer's saved activations (ctx-owned)        */
+
+/* Spec-layout weight shards (bf16, device) and their fp32 gradients (device, +=). */
+typedef struct { const void *w_qkv_t, *w_proj, *w_in_t, *w_out, *g1, *g2; } pds_weights;
+typedef struct { void *dw_qkv_t, *dw_proj, *dw_in_t, *dw_out, *dg1, *dg2; } pds_grads;
+
+/* ------------------------------------------------------------------ context */
+/* Writes a 128-byte NCCL unique id (host) — rank 0 calls this and broadcasts it
+ * (e.g. via torch.distributed) before every rank calls pds_create. */
+pds_status pds_nccl_unique_id(void* out128);
+
+/* Create the per-rank context on `device`.  P = 1: no communicator.  P > 1:
+ * nccl_unique_id (host, 128 B) must be the same on all ranks; the NCCL
+ * communicator is created collectively (blocks until all ranks join). */
+pds_status pds_create(const pds_model* model, int32_t P, int32_t rank, int32_t device,
+                      const void* nccl_unique_id, pds_ctx** out);
+
+/* Loopback: P virtual ranks in one process on one device; rank r's calls must run
+ * on their own host thread (collectives rendezvous on a host barrier). */
+pds_status pds_group_create(int32_t P, pds_group** out);
+pds_status pds_group_destroy(pds_group* g);
+pds_status pds_create_loopback(const pds_model* model, pds_group* g, int32_t rank,
+                               int32_t device, pds_ctx** out);
+pds_status pds_destroy(pds_ctx* ctx);
+
+/* Optional: pre-allocate workspace for sequences up to max_seq_len (global) for the
+ * strategies in strategy_mask (bit i = strategy i); otherwise grown on demand. */
+pds_status pds_reserve(pds_ctx* ctx, int64_t max_seq_len, uint32_t strategy_mask);
+
+/* ------------------------------------------------------------------ planner (host only) */
+/* Load a calibrated cost bundle (text, "pds_bundle 1" format, see DESIGN.md §Cost
+ * bundle): per strategy an exported random forest (RF, interpolation) and an AIC-
+ * selected polynomial (PR, extrapolation) for T_pi(s), plus s_profile_max (Eq. 9). */
+pds_status pds_load_costs(pds_ctx* ctx, const char* bundle_path);
+/* Device capacity (bytes) the plan must stay strictly below (Eq. 6) and the
+ * smoothing ratio gamma.  Defaults: cudaMemGetInfo total minus
+ * the reserve in the bundle; gamma = 0. */
+pds_status pds_set_capacity(pds_ctx* ctx, double capacity_bytes, double gamma);
+/* Enable / disable strategies (bit mask; default: all). */
+pds_status pds_set_enabled(pds_ctx* ctx, uint32_t strategy_mask);
+
+/* Pi*(b, s): writes L strategy ids to strategy_out (host, L bytes) — always a full
+ * plan (totality); *flags_out (nullable) gets PDS_PLAN_* bits.
+ * T_pi(s) from the bundle (Eq. 9), M_pi(s) from pds_mem_bytes (exact model),
+ * Algorithm 1 with the readings R-17..R-24, dictionary D keyed by (b, s). */
+pds_status pds_plan(pds_ctx* ctx, int64_t seq_len, uint8_t* strategy_out, int32_t L,
+                    uint32_t* flags_out);
+
+/* Stateless Algorithm 1 on explicit per-layer costs (host arrays of n_strat):
+ * t_layer[i], m_layer[i] for strategy i, enabled[i] in {0,1}; feasibility is
+ * sum m < capacity (strict).  prev_plan (nullable, L bytes) enables smoothing with
+ * gamma.  counters_out (nullable, 3 x int64): layer memory checks, candidate plans
+ * generated, cache hits (always 0 here).  Bit-exact contract with the oracle. */
+pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_layer, const double* m_layer,
+                       const uint8_t* enabled, double capacity, double gamma,
+                       const uint8_t* prev_plan, uint8_t* strategy_out, uint32_t* flags_out,
+                       int64_t* counters_out);
+
+/* T_pi(s) and M_pi(s) for every strategy (host arrays of PDS_N_STRATEGIES);
+ * branch_out (nullable, host int32[3]): 0 = RF, 1 = PR. */
+pds_status pds_cost_eval(pds_ctx* ctx, int64_t seq_len, double* t_layer, double* m_layer,
+                         int32_t* branch_out);
+
+/* Exact per-rank memory model of this implementation:
+ * saved activations per layer, the strategy's workspace peak, and the persistent
+ * bytes per layer (bf16 weight shards + fp32 gradient shards).  Host only. */
+pds_status pds_mem_bytes(const pds_model* model, int32_t P, uint8_t strategy, int64_t seq_len,
+                         int64_t* saved_per_layer, int64_t* transient_peak,
+                         int64_t* persistent_per_layer);
+
+/* ------------------------------------------------------------------ the layer */
+/* y = f_{pi,FFN}(f_{pi,MHA}(x)) with residuals and pre-norms,
+ * x, y: local [s/P, b, h] bf16 shards of a length-seq_len global sequence.
+ * *saved receives the layer's saved activations (ctx arena, LIFO across layers);
+ * pass saved = NULL for a forward-only call.  x must stay valid until the
+ * matching bwd (it is referenced, not copied). */
+pds_status pds_layer_fwd(pds_ctx* ctx, uint8_t strategy, int64_t seq_len, const void* x,
+                         const pds_weights* w, void* y, pds_saved** saved, void* stream);
+/* dx = VJP of the layer at dy; weight gradients accumulated (+=) into g (fp32).
+ * `strategy` must equal the forward's (else PDS_ESTATE).  Consumes `saved`. */
+pds_status pds_layer_bwd(pds_ctx* ctx, uint8_t strategy, const void* dy, pds_saved* saved,
+                         const pds_weights* w, const pds_grads* g, void* dx, void* stream);
+/* Release a saved set without running backward. */
+pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
+/* Debug taps: the next pds_layer_fwd also writes the sublayer deltas O (attention
+ * block output) and Z (FFN output), local [s/P, b, h] bf16 (reading R-34).  NULL
+ * pointers disable. */
+pds_status pds_debug_taps(pds_ctx* ctx, void* o_out, void* z_out);
+
+/* ------------------------------------------------------------------ measurement */
+/* Per-kernel-class device timing with CUDA events on the launching stream.
+ * Classes: 0 GEMM, 1 attention fwd, 2 attention bwd, 3 norm/elementwise,
+ * 4 collectives.  read: total ms, launches, algorithmic flops and bytes. */
+pds_status pds_profile_enable(pds_ctx* ctx, int32_t on);
+pds_status pds_profile_read(pds_ctx* ctx, int32_t klass, double* ms, int64_t* launches,
+                            double* flops, double* bytes);
+pds_status pds_profile_reset(pds_ctx* ctx);
+
+/* ------------------------------------------------------------------ kernel-level entry points
+ * Per-stage parity (fp32-accumulate path, reading R-14).  Device pointers, stream-
+ * ordered, no context needed. */
+/* C[M,N] (op)= A * B^T with A [M][K] (a_mn = 0) or [K][M] (a_mn = 1), B [N][K]
+ * (b_mn = 0) or [K][N] (b_mn = 1); epi: 0 bf16 store, 1 fp32 +=, 2 fp32 store,
+ * 3 GELU (C = H bf16, aux_out = GELU(H)), 4 dGELU (aux_in = H; C = acc * GELU'(H),
+ * aux_out = GELU(H)). */
+pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
+                      int32_t b_mn, int32_t M, int32_t N, int32_t K, void* C, int64_t ldc,
+                      int32_t epi, const void* aux_in, void* aux_out, int64_t ld_aux,
+                      void* stream);
+/* QKV GEMM with fused RoPE on the Q and K columns: C [M, N] where columns form
+ * groups of 3*hq ([Q | K | V], hq = heads*d); row r has global position
+ * (r / seg) * seg_stride + seg_base + r % seg.  rope: [positions][d/2] float2. */
+pds_status pds_k_gemm_rope(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                           int32_t N, int32_t K, void* C, int64_t ldc, const void* rope,
+                           int32_t d, int32_t hq, int64_t seg, int64_t seg_stride,
+                           int64_t seg_base, void* stream);
+/* cos/sin table [n_pos][d/2] (float2), angles t * theta^(-2k/d) formed and
+ * range-reduced in fp64 (reading R-3). */
+pds_status pds_k_rope_table(void* table, int64_t n_pos, int32_t d, double theta, void* stream);
+/* RMSNorm forward over rows of h: if residual != NULL, x1 = x + residual is
+ * written to x1_out and normalised; u = g * x1 * rstd; rstd fp32 [rows]. */
+pds_status pds_k_rmsnorm_fwd(const void* x, const void* residual, const void* g, int64_t rows,
+                             int32_t h, float eps, void* x1_out, void* u_out, void* rstd_out,
+                             void* stream);
+/* RMSNorm backward: dx = r (a - xhat mean(a xhat)) (+ dres if != NULL), a = du g;
+ * dg_partial fp32 [gridrows][h] reduced into dg (fp32 [h], +=). */
+pds_status pds_k_rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g,
+                             const void* dres, int64_t rows, int32_t h, void* dx, void* dg,
+                             void* stream);
+/* Causal (or full) attention forward over qkv [s][ld] laid out [Q | K | V] blocks
+ * of heads*d: out [s][ld_out] (head i at column i*d), lse fp32 [heads][s]. */
+pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
+                          int32_t causal, void* out, int64_t ld_out, void* lse, void* stream);
+/* Attention backward: dqkv [s][ld] (pre-RoPE positions handled by caller), from
+ * qkv (post-RoPE Q, K), out, lse, dout. */
+pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                          const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
+                          int32_t causal, void* dqkv, void* stream);
+
+const char* pds_last_error(void);
+const char* pds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARADYSE_H */

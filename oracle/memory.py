@@ -44,33 +44,38 @@ def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
     raise KeyError(pi)
 
 
-def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
-    """Workspace bytes of the CUDA path's buffer plan, per rank.
+def _al(x):
+    return (x + 255) // 256 * 256
 
-    Buffers (bf16 unless noted), with u = one [s/P, b, h] activation:
-      TS   fwd: gather P u, partial P u, G (F/h) P?  -> see formulas below
-    The plan is written as max(fwd, bwd) of the live-buffer maxima.
-    """
-    u, l, lam = units(h, n, s, P, b)
-    f = ffn // h
-    sl_rows = s // P
+
+def _norm_bwd_grid(rows):
+    return min((rows + 3) // 4, 592)
+
+
+def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
+    """Workspace bytes per rank of the CUDA path's buffer plan,
+    each buffer rounded up to 256 B.  Written out from the plan table, not shared
+    with the library (tests compare it with pds_mem_bytes)."""
+    sl = s // P
+    u = sl * b * h * 2
+    lam = (n // P) * s * b * 4
+    hl, Fl = h // P, ffn // P
+    small = _al(2 * h * 4)
     if pi == TS:
-        fwd = 2 * P * u + f * u + 2 * u
-        bwd = P * u + 2 * f * u + 5 * u + 2 * P * u
-        return max(fwd, bwd)
-    if pi == UZ:
-        wfull = (4 * h * h + 2 * h * ffn) * 2
-        dwfull = max(3 * h * h, h * h, h * ffn) * 4
-        fwd = wfull + 3 * u + 2 * u + f * u * 2
-        bwd = wfull + dwfull + 2 * f * u + 6 * u + 3 * u
-        return max(fwd, bwd)
-    if pi == METP:
+        bufs = [s * h * 2, s * h * 2, s * Fl * 2, s * Fl * 2, lam, _norm_bwd_grid(sl) * h * 4]
+    elif pi == UZ:
+        bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
+                u, 3 * u, 3 * u, sl * ffn * 2, sl * ffn * 2, 3 * u, 3 * u, u, lam,
+                _norm_bwd_grid(sl) * h * 4]
+    elif pi == METP:
         c = metp_chunks or P
-        w = P * u // c
-        fwd = 3 * w + f * w + 2 * u
-        bwd = 3 * w + 3 * f * w + 5 * u + 2 * u
-        return max(fwd, bwd)
-    raise KeyError(pi)
+        w = sl // c
+        uw = w * h * 2
+        bufs = [u, u, P * uw, P * uw, P * uw, P * w * Fl * 2, P * w * Fl * 2, P * w * Fl * 2,
+                s * hl * 2, s * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4]
+    else:
+        raise KeyError(pi)
+    return sum(_al(x) for x in bufs) + small
 
 
 def layer_bytes(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):

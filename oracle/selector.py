@@ -144,11 +144,14 @@ def alg1(L, t, m, enabled, cap, cache=None, key=None, literal=False, ctr=None):
     return result, infeasible
 
 
-def smooth(plan, prev, t, m, cap, gamma):
-    """Smoothing (R-19): retain prev if feasible and within gamma."""
+def smooth(plan, prev, t, m, cap, gamma, enabled=None):
+    """Smoothing (R-19): retain prev if feasible and within gamma.
+    A previous plan using a strategy that is no longer enabled is never retained."""
     if prev is None or len(prev) != len(plan):
         return plan, False
     if list(prev) == list(plan):
+        return plan, False
+    if enabled is not None and any(p not in enabled for p in prev):
         return plan, False
     if feasible(prev, m, cap) and plan_time(prev, t) <= (1.0 + gamma) * plan_time(plan, t):
         return list(prev), True

@@ -1,0 +1,297 @@
+"""ctypes binding of include/paradyse.h (same names, argument marshalling only).
+
+Device buffers are passed as integer device addresses (e.g. ``tensor.data_ptr()``)
+and streams as ``torch.cuda.Stream.cuda_stream`` integers; torch is plumbing
+(memory, streams, process groups), never on the compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libparadyse.so")
+
+TS, UZ, METP = 0, 1, 2
+STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
+
+STATUS = {0: "PDS_OK", -1: "PDS_EINVAL", -2: "PDS_EDIVISIBILITY", -3: "PDS_ESTRATEGY", -4: "PDS_ENOMEM",
+          -5: "PDS_ECUDA", -6: "PDS_ENCCL", -7: "PDS_ESTATE", -8: "PDS_ENOCOSTS", -9: "PDS_ENOTIMPL"}
+PLAN_INFEASIBLE, PLAN_CACHED, PLAN_EARLY, PLAN_SMOOTHED = 1, 2, 4, 8
+
+
+class PdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Model(C.Structure):
+    _fields_ = [("h", C.c_int32), ("n_heads", C.c_int32), ("ffn", C.c_int32), ("n_layers", C.c_int32),
+                ("batch", C.c_int32), ("norm_eps", C.c_float), ("rope_theta", C.c_double),
+                ("causal", C.c_int32), ("metp_chunks", C.c_int32), ("metp_recompute", C.c_int32)]
+
+
+class _Weights(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")]
+
+
+class _Grads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")]
+
+
+@dataclass
+class Model:
+    h: int
+    n_heads: int
+    ffn: int
+    n_layers: int = 1
+    batch: int = 1
+    norm_eps: float = 1e-5
+    rope_theta: float = 10000.0
+    causal: int = 1
+    metp_chunks: int = 0
+    metp_recompute: int = 0
+
+    def c(self):
+        return _Model(self.h, self.n_heads, self.ffn, self.n_layers, self.batch, self.norm_eps,
+                      self.rope_theta, self.causal, self.metp_chunks, self.metp_recompute)
+
+
+@dataclass
+class Weights:
+    w_qkv_t: int
+    w_proj: int
+    w_in_t: int
+    w_out: int
+    g1: int
+    g2: int
+
+    def c(self):
+        return _Weights(self.w_qkv_t, self.w_proj, self.w_in_t, self.w_out, self.g1, self.g2)
+
+
+@dataclass
+class Grads:
+    dw_qkv_t: int
+    dw_proj: int
+    dw_in_t: int
+    dw_out: int
+    dg1: int
+    dg2: int
+
+    def c(self):
+        return _Grads(self.dw_qkv_t, self.dw_proj, self.dw_in_t, self.dw_out, self.dg1, self.dg2)
+
+
+_lib = None
+
+_SIGS = {
+    "pds_nccl_unique_id": [C.c_void_p],
+    "pds_create": [C.POINTER(_Model), C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)],
+    "pds_group_create": [C.c_int32, C.POINTER(C.c_void_p)],
+    "pds_group_destroy": [C.c_void_p],
+    "pds_create_loopback": [C.POINTER(_Model), C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)],
+    "pds_destroy": [C.c_void_p],
+    "pds_reserve": [C.c_void_p, C.c_int64, C.c_uint32],
+    "pds_load_costs": [C.c_void_p, C.c_char_p],
+    "pds_set_capacity": [C.c_void_p, C.c_double, C.c_double],
+    "pds_set_enabled": [C.c_void_p, C.c_uint32],
+    "pds_plan": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.POINTER(C.c_uint32)],
+    "pds_plan_ex": [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                    C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p],
+    "pds_cost_eval": [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_mem_bytes": [C.POINTER(_Model), C.c_int32, C.c_uint8, C.c_int64, C.POINTER(C.c_int64),
+                      C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+    "pds_layer_fwd": [C.c_void_p, C.c_uint8, C.c_int64, C.c_void_p, C.POINTER(_Weights), C.c_void_p,
+                      C.POINTER(C.c_void_p), C.c_void_p],
+    "pds_layer_bwd": [C.c_void_p, C.c_uint8, C.c_void_p, C.c_void_p, C.POINTER(_Weights),
+                      C.POINTER(_Grads), C.c_void_p, C.c_void_p],
+    "pds_saved_release": [C.c_void_p, C.c_void_p],
+    "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_profile_enable": [C.c_void_p, C.c_int32],
+    "pds_profile_read": [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                         C.POINTER(C.c_double), C.POINTER(C.c_double)],
+    "pds_profile_reset": [C.c_void_p],
+    "pds_k_gemm": [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                   C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "pds_k_gemm_rope": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                        C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                        C.c_int64, C.c_void_p],
+    "pds_k_rope_table": [C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p],
+    "pds_k_rmsnorm_fwd": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_float, C.c_void_p,
+                          C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_k_rmsnorm_bwd": [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                          C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_k_attn_fwd": [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                       C.c_int64, C.c_void_p, C.c_void_p],
+    "pds_k_attn_bwd": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
+                       C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
+    "pds_last_error": [],
+    "pds_version": [],
+}
+
+
+def lib():
+    """Load libparadyse.so; raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run __graft_entry__.build() "
+                              "(python paper_2511_13198_b200/build.py). There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_char_p if name in ("pds_last_error", "pds_version") else C.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        raise PdsError(rc, lib().pds_last_error().decode())
+    return rc
+
+
+def call(name, *args):
+    return check(getattr(lib(), name)(*args))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    call("pds_nccl_unique_id", buf)
+    return buf.raw
+
+
+def mem_bytes(model: Model, P: int, strategy: int, s: int):
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    call("pds_mem_bytes", C.byref(model.c()), P, strategy, s, C.byref(a), C.byref(b), C.byref(c))
+    return a.value, b.value, c.value
+
+
+def plan_ex(L, t, m, enabled, capacity, gamma=0.0, prev=None, counters=False):
+    n = len(t)
+    ta = (C.c_double * n)(*t)
+    ma = (C.c_double * n)(*m)
+    ea = (C.c_uint8 * n)(*[1 if e else 0 for e in enabled])
+    out = (C.c_uint8 * L)()
+    pv = (C.c_uint8 * L)(*prev) if prev is not None else None
+    flags = C.c_uint32()
+    ctr = (C.c_int64 * 3)()
+    call("pds_plan_ex", L, n, ta, ma, ea, capacity, gamma, pv, out, C.byref(flags), ctr)
+    res = list(out), flags.value
+    return (res + (list(ctr),)) if counters else res
+
+
+class Group:
+    """In-process loopback group: P virtual ranks on one device (single-GPU multi-rank tests)."""
+
+    def __init__(self, P):
+        h = C.c_void_p()
+        call("pds_group_create", P, C.byref(h))
+        self.h = h
+        self.P = P
+
+    def close(self):
+        if self.h:
+            lib().pds_group_destroy(self.h)
+            self.h = None
+
+
+class Context:
+    def __init__(self, model: Model, P=1, rank=0, device=0, uid: bytes | None = None, group: Group | None = None):
+        self.model, self.P, self.rank = model, P, rank
+        h = C.c_void_p()
+        self._m = model.c()
+        if group is not None:
+            call("pds_create_loopback", C.byref(self._m), group.h, rank, device, C.byref(h))
+        else:
+            ub = C.create_string_buffer(uid, 128) if uid else None
+            call("pds_create", C.byref(self._m), P, rank, device, ub, C.byref(h))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().pds_destroy(self.h)
+            self.h = None
+
+    def reserve(self, max_seq_len, mask=0x7):
+        call("pds_reserve", self.h, max_seq_len, mask)
+
+    def load_costs(self, path):
+        call("pds_load_costs", self.h, path.encode())
+
+    def set_capacity(self, cap, gamma=0.0):
+        call("pds_set_capacity", self.h, cap, gamma)
+
+    def set_enabled(self, mask):
+        call("pds_set_enabled", self.h, mask)
+
+    def plan(self, s, L):
+        out = (C.c_uint8 * L)()
+        fl = C.c_uint32()
+        call("pds_plan", self.h, s, out, L, C.byref(fl))
+        return list(out), fl.value
+
+    def cost_eval(self, s):
+        t = (C.c_double * 3)()
+        m = (C.c_double * 3)()
+        b = (C.c_int32 * 3)()
+        call("pds_cost_eval", self.h, s, t, m, b)
+        return list(t), list(m), list(b)
+
+    def layer_fwd(self, strategy, s, x, w: Weights, y, stream=0, keep=True):
+        sv = C.c_void_p()
+        call("pds_layer_fwd", self.h, strategy, s, x, C.byref(w.c()), y, C.byref(sv) if keep else None, stream)
+        return sv if keep else None
+
+    def layer_bwd(self, strategy, dy, saved, w: Weights, g: Grads, dx, stream=0):
+        call("pds_layer_bwd", self.h, strategy, dy, saved, C.byref(w.c()), C.byref(g.c()), dx, stream)
+
+    def saved_release(self, saved):
+        call("pds_saved_release", self.h, saved)
+
+    def debug_taps(self, o=None, z=None):
+        call("pds_debug_taps", self.h, o, z)
+
+    def profile(self, on=True):
+        call("pds_profile_enable", self.h, 1 if on else 0)
+
+    def profile_read(self, klass):
+        ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        call("pds_profile_read", self.h, klass, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by))
+        return dict(ms=ms.value, launches=n.value, flops=fl.value, bytes=by.value)
+
+    def profile_reset(self):
+        call("pds_profile_reset", self.h)
+
+
+# ------------------------------------------------------------------ kernel-level entry points
+def k_gemm(A, lda, a_mn, B, ldb, b_mn, M, N, K, Cp, ldc, epi=0, aux_in=None, aux_out=None, ld_aux=0, stream=0):
+    call("pds_k_gemm", A, lda, a_mn, B, ldb, b_mn, M, N, K, Cp, ldc, epi, aux_in, aux_out, ld_aux, stream)
+
+
+def k_gemm_rope(A, lda, B, ldb, M, N, K, Cp, ldc, rope, d, hq, seg=0, seg_stride=0, seg_base=0, stream=0):
+    call("pds_k_gemm_rope", A, lda, B, ldb, M, N, K, Cp, ldc, rope, d, hq, seg, seg_stride, seg_base, stream)
+
+
+def k_rope_table(t, n_pos, d, theta=10000.0, stream=0):
+    call("pds_k_rope_table", t, n_pos, d, theta, stream)
+
+
+def k_rmsnorm_fwd(x, res, g, rows, h, eps, x1, u, rstd, stream=0):
+    call("pds_k_rmsnorm_fwd", x, res, g, rows, h, eps, x1, u, rstd, stream)
+
+
+def k_rmsnorm_bwd(du, x, rstd, g, dres, rows, h, dx, dg, stream=0):
+    call("pds_k_rmsnorm_bwd", du, x, rstd, g, dres, rows, h, dx, dg, stream)
+
+
+def k_attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, stream=0):
+    call("pds_k_attn_fwd", qkv, ld, s, heads, d, causal, out, ld_out, lse, stream)
+
+
+def k_attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream=0):
+    call("pds_k_attn_bwd", qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream)

@@ -1,0 +1,101 @@
+// Kernel-level C-ABI entry points (per-stage parity) and the
+// NCCL unique-id helper.  Thin argument checks + launch; no context.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "internal.hpp"
+#include "kernels/gemm.cuh"
+#include "kernels/kernels.hpp"
+
+using namespace pds;
+
+static pds_status rc2s(int rc, const char* what) {
+  if (rc == 0) return PDS_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString((cudaError_t)rc));
+  return rc == (int)cudaErrorMemoryAllocation ? PDS_ENOMEM : (rc == (int)cudaErrorInvalidValue ? PDS_EINVAL : PDS_ECUDA);
+}
+
+extern "C" pds_status pds_nccl_unique_id(void* out128) {
+  if (!out128) PDS_FAIL(PDS_EINVAL, "NULL out");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) PDS_FAIL(PDS_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const void* B, int64_t ldb,
+                                 int32_t b_mn, int32_t M, int32_t N, int32_t K, void* C, int64_t ldc,
+                                 int32_t epi, const void* aux_in, void* aux_out, int64_t ld_aux, void* stream) {
+  if (!A || !B || !C) PDS_FAIL(PDS_EINVAL, "NULL operand");
+  if (epi < 0 || epi > EPI_DGELU) PDS_FAIL(PDS_EINVAL, "bad epilogue");
+  if ((epi == EPI_GELU && !aux_out) || (epi == EPI_DGELU && (!aux_in || !aux_out)))
+    PDS_FAIL(PDS_EINVAL, "GELU epilogues need aux buffers");
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.a_mn = a_mn; g.B = B; g.ldb = ldb; g.b_mn = b_mn;
+  g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc; g.epi = epi;
+  g.aux_in = aux_in; g.aux_out = aux_out; g.ld_aux = ld_aux;
+  return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm");
+}
+
+extern "C" pds_status pds_k_gemm_rope(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                                      int32_t N, int32_t K, void* C, int64_t ldc, const void* rope, int32_t d,
+                                      int32_t hq, int64_t seg, int64_t seg_stride, int64_t seg_base,
+                                      void* stream) {
+  if (!A || !B || !C || !rope) PDS_FAIL(PDS_EINVAL, "NULL operand");
+  if (hq <= 0 || N % (3 * hq)) PDS_FAIL(PDS_EINVAL, "N must be a multiple of 3*hq");
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.epi = EPI_ROPE; g.rope = reinterpret_cast<const float2*>(rope); g.rope_d = d; g.rope_hq = hq;
+  g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
+  return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm_rope");
+}
+
+extern "C" pds_status pds_k_rope_table(void* table, int64_t n_pos, int32_t d, double theta, void* stream) {
+  if (!table || n_pos <= 0 || d <= 0 || d % 2) PDS_FAIL(PDS_EINVAL, "bad rope table args");
+  return rc2s(rope_table(table, n_pos, d, theta, static_cast<cudaStream_t>(stream)), "pds_k_rope_table");
+}
+
+extern "C" pds_status pds_k_rmsnorm_fwd(const void* x, const void* residual, const void* g, int64_t rows,
+                                        int32_t h, float eps, void* x1_out, void* u_out, void* rstd_out,
+                                        void* stream) {
+  if (!x || !g || !u_out || !rstd_out || (residual && !x1_out)) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(rmsnorm_fwd(x, residual, g, rows, h, eps, x1_out, u_out, rstd_out, static_cast<cudaStream_t>(stream)),
+              "pds_k_rmsnorm_fwd");
+}
+
+extern "C" pds_status pds_k_rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g,
+                                        const void* dres, int64_t rows, int32_t h, void* dx, void* dg,
+                                        void* stream) {
+  if (!du || !x || !rstd || !g || !dx || !dg) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* part = nullptr;
+  PDS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)rmsnorm_bwd_grid(rows) * h * 4, st));
+  pds_status r = rc2s(rmsnorm_bwd(du, x, rstd, g, dres, rows, h, dx, part, static_cast<float*>(dg), st),
+                      "pds_k_rmsnorm_bwd");
+  cudaFreeAsync(part, st);
+  return r;
+}
+
+extern "C" pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
+                                     int32_t causal, void* out, int64_t ld_out, void* lse, void* stream) {
+  if (!qkv || !out || !lse) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, static_cast<cudaStream_t>(stream)),
+              "pds_k_attn_fwd");
+}
+
+extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                                     const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
+                                     int32_t causal, void* dqkv, void* stream) {
+  if (!qkv || !out || !lse || !dout || !dqkv) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* dd = nullptr;
+  PDS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dd), (size_t)heads * s * 4, st));
+  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st),
+                      "pds_k_attn_bwd");
+  cudaFreeAsync(dd, st);
+  return r;
+}

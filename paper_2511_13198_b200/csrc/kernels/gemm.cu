@@ -1,0 +1,445 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+// The dense contractions of the layer (Eqs. 1, 3, 4 and their
+// gradients) all run here:  C[M,N] = A[M,K] * B[N,K]^T, bf16 operands staged by
+// TMA (SWIZZLE_128B) into a STAGES-deep shared-memory ring, one elected thread
+// issuing tcgen05.mma (M = 128, N = BN, K = 16) into a double-buffered TMEM
+// accumulator, and four epilogue warps draining TMEM with tcgen05.ld while the
+// next tile accumulates.
+//
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      MMA issuer   (one elected lane)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue (TMEM lanes 32*(warp%4) .. +31, one output row per thread)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace pds {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int GROUP_M = 16;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct EpiParams {
+  int M, N;
+  void* C;
+  int64_t ldc;
+  int epi;
+  int blk_w;
+  int64_t blk_stride;
+  const __nv_bfloat16* aux_in;
+  __nv_bfloat16* aux_out;
+  int64_t ld_aux;
+  const float2* rope;
+  int rope_d, rope_hq;
+  int64_t seg, seg_stride, seg_base;
+  int64_t c_seg, c_stride, c_base;
+};
+
+struct RowMap {
+  int64_t seg, stride, base;
+  __device__ __forceinline__ int map(int r) const {
+    return (int)((r / seg) * stride + base + (r % seg));
+  }
+};
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+  return cdf + x * pdf;
+}
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int& nb) {
+  const int band = t / (GROUP_M * nt);
+  const int first = band * GROUP_M;
+  const int gm = min(GROUP_M, mt - first);
+  const int idx = t - band * GROUP_M * nt;
+  mb = first + idx % gm;
+  nb = idx / gm;
+}
+
+// store 32 consecutive bf16 values of one row
+__device__ __forceinline__ void store_row32_bf16(__nv_bfloat16* dst, const float* v, int valid) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q * 8 < valid) {
+      uint4 w;
+      w.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+      w.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+      w.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+      w.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+      d4[q] = w;
+    }
+  }
+}
+__device__ __forceinline__ void load_row32_bf16(const __nv_bfloat16* src, float* v, int valid) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (q * 8 < valid) w = s4[q];
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(b[e]);
+      v[q * 8 + 2 * e] = f.x;
+      v[q * 8 + 2 * e + 1] = f.y;
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t out_offset(const EpiParams& p, int row_l, int col) {
+  const int64_t row = (row_l / p.c_seg) * p.c_stride + p.c_base + (row_l % p.c_seg);
+  if (p.blk_w > 0) {
+    const int blk = col / p.blk_w;
+    return (int64_t)blk * p.blk_stride + (int64_t)row * p.ldc + (col - blk * p.blk_w);
+  }
+  return (int64_t)row * p.ldc + col;
+}
+
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, RowMap amap, RowMap bmap, EpiParams ep) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int mt = (M + BM - 1) / BM;
+  const int nt = (N + BN - 1) / BN;
+  const int ntiles = mt * nt;
+  const int nkb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, mt, nt, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) {
+            const int kr = amap.map(k0);
+            tma_load_2d(sa, &tmA, &full_bar[stage], m0, kr);
+            tma_load_2d(sa + 8192, &tmA, &full_bar[stage], m0 + 64, kr);
+          } else {
+            tma_load_2d(sa, &tmA, &full_bar[stage], k0, amap.map(m0));
+          }
+          if (B_MN) {
+            const int kr = bmap.map(k0);
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(sb + i * 8192, &tmB, &full_bar[stage], n0 + 64 * i, kr);
+          } else {
+            tma_load_2d(sb, &tmB, &full_bar[stage], k0, bmap.map(n0));
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad, bd;
+            if (A_MN) ad = umma_desc_sw128(sa + k * 2048, 8192, 1024);
+            else      ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+            if (B_MN) bd = umma_desc_sw128(sb + k * 2048, 8192, 1024);
+            else      bd = umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (kb == nkb - 1) umma_commit(&tfull_bar[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, mt, nt, mb, nb);
+      const int m0 = mb * BM, n0 = nb * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < M;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (ep.epi == EPI_ROPE) {
+        const int d = ep.rope_d, d2 = d >> 1;
+        int64_t pos = 0;
+        if (row_ok) {
+          const int64_t r = row;
+          pos = (r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg);
+        }
+        for (int hs = 0; hs < BN; hs += d) {
+          for (int j0 = 0; j0 < d2; j0 += 32) {
+            uint32_t r1[32], r2[32];
+            tmem_ld32(tbase + hs + j0, r1);
+            tmem_ld32(tbase + hs + j0 + d2, r2);
+            tmem_ld_wait();
+            const int c1 = n0 + hs + j0;
+            if (row_ok && c1 < N) {
+            float v1[32], v2[32];
+            const int within = (n0 + hs) % (3 * ep.rope_hq);
+            if (within < 2 * ep.rope_hq) {
+              const float2* cs = ep.rope + pos * d2 + j0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float2 c = cs[i];
+                const float a = __uint_as_float(r1[i]), b = __uint_as_float(r2[i]);
+                v1[i] = a * c.x - b * c.y;
+                v2[i] = a * c.y + b * c.x;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                v1[i] = __uint_as_float(r1[i]);
+                v2[i] = __uint_as_float(r2[i]);
+              }
+            }
+            __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C);
+            store_row32_bf16(C + out_offset(ep, row, c1), v1, 32);
+            store_row32_bf16(C + out_offset(ep, row, c1 + d2), v2, 32);
+            }
+            __syncwarp();
+          }
+        }
+      } else {
+        for (int cc = 0; cc < BN; cc += 32) {
+          uint32_t r[32];
+          tmem_ld32(tbase + cc, r);
+          tmem_ld_wait();
+          const int col = n0 + cc;
+          if (row_ok && col < N) {
+          const int valid = min(32, N - col);
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (ep.epi == EPI_BF16) {
+            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                             valid);
+          } else if (ep.epi == EPI_F32_ACC || ep.epi == EPI_F32) {
+            float4* c4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + out_offset(ep, row, col));
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              if (e * 4 < valid) {
+                float4 o = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+                if (ep.epi == EPI_F32_ACC) {
+                  const float4 old = c4[e];
+                  o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+                }
+                c4[e] = o;
+              }
+            }
+          } else if (ep.epi == EPI_GELU) {
+            float g[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) g[i] = gelu_f(bf16_round(v[i]));
+            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                             valid);
+            store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+          } else if (ep.epi == EPI_DGELU) {
+            float hh[32], g[32];
+            load_row32_bf16(ep.aux_in + (int64_t)row * ep.ld_aux + col, hh, valid);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              g[i] = gelu_f(hh[i]);
+              v[i] = v[i] * gelu_grad_f(hh[i]);
+            }
+            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                             valid);
+            store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+          }
+          }
+          __syncwarp();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner (contiguous) dim `inner`, outer dim `outer`, row stride in elements
+static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t ld, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+int gemm_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, int A_MN, int B_MN>
+static int launch_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  CUtensorMap ta, tb;
+  int rc;
+  const int64_t a_rows = g.a_rows > 0 ? g.a_rows : (A_MN ? g.K : g.M);
+  const int64_t b_rows = g.b_rows > 0 ? g.b_rows : (B_MN ? g.K : g.N);
+  if (A_MN) rc = make_map(&ta, g.A, g.M, a_rows, g.lda, 64, 64);
+  else      rc = make_map(&ta, g.A, g.K, a_rows, g.lda, 64, BM);
+  if (rc) return rc;
+  if (B_MN) rc = make_map(&tb, g.B, g.N, b_rows, g.ldb, 64, 64);
+  else      rc = make_map(&tb, g.B, g.K, b_rows, g.ldb, 64, BN);
+  if (rc) return rc;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr_set = true;
+  }
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
+  RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
+  RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
+  kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep);
+  return (int)cudaGetLastError();
+}
+
+int gemm_launch(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
+  if (g.N % 8 || (g.blk_w % 32)) return (int)cudaErrorInvalidValue;
+  EpiParams ep;
+  ep.M = g.M; ep.N = g.N; ep.C = g.C; ep.ldc = g.ldc; ep.epi = g.epi;
+  ep.blk_w = g.blk_w; ep.blk_stride = g.blk_stride;
+  ep.aux_in = reinterpret_cast<const __nv_bfloat16*>(g.aux_in);
+  ep.aux_out = reinterpret_cast<__nv_bfloat16*>(g.aux_out);
+  ep.ld_aux = g.ld_aux;
+  ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq;
+  ep.seg = g.seg > 0 ? g.seg : (int64_t)1 << 40;
+  ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;
+  ep.c_seg = g.c_seg > 0 ? g.c_seg : (int64_t)1 << 40;
+  ep.c_stride = g.c_stride; ep.c_base = g.c_base;
+  // a tile must not straddle a remap segment
+  if (g.a_seg > 0 && g.a_seg % (g.a_mn ? 64 : BM)) return (int)cudaErrorInvalidValue;
+  if (g.b_seg > 0 && g.b_seg % (g.b_mn ? 64 : 256)) return (int)cudaErrorInvalidValue;
+  // BN = 256 when N is large enough to fill the machine, else 128 (more tiles)
+  const int64_t tiles256 = (int64_t)((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
+  bool use256 = (g.N % 256 == 0 || g.N > 1024) && tiles256 >= gemm_num_sms();
+  if (g.epi == EPI_ROPE && (g.rope_d % 64 || 128 % g.rope_d)) return (int)cudaErrorInvalidValue;
+  const int key = (use256 ? 4 : 0) | (g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0);
+  switch (key) {
+    case 0: return launch_t<128, 0, 0>(g, ep, st);
+    case 1: return launch_t<128, 0, 1>(g, ep, st);
+    case 2: return launch_t<128, 1, 0>(g, ep, st);
+    case 3: return launch_t<128, 1, 1>(g, ep, st);
+    case 4: return launch_t<256, 0, 0>(g, ep, st);
+    case 5: return launch_t<256, 0, 1>(g, ep, st);
+    case 6: return launch_t<256, 1, 0>(g, ep, st);
+    default: return launch_t<256, 1, 1>(g, ep, st);
+  }
+}
+
+}  // namespace pds

@@ -1,0 +1,62 @@
+// Host-visible description of the tcgen05 GEMM and its fused epilogues.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pds {
+
+// C[M,N] (op)= A[M,K] * B[N,K]^T   with fp32 accumulation in TMEM.
+//   A K-major : A stored [M][K] (row stride lda elements)
+//   A MN-major: A stored [K][M] (row stride lda)      -- i.e. C = A_stored^T * ...
+//   B K-major : B stored [N][K] (row stride ldb)
+//   B MN-major: B stored [K][N] (row stride ldb)
+enum GemmEpi : int {
+  EPI_BF16 = 0,      // C bf16 = acc
+  EPI_F32_ACC = 1,   // C fp32 += acc            (weight gradients)
+  EPI_F32 = 2,       // C fp32 = acc
+  EPI_GELU = 3,      // C bf16 = H = acc ; aux_out bf16 = GELU(bf16(H))
+  EPI_DGELU = 4,     // aux_in = H (bf16): C bf16 = acc * GELU'(H) ; aux_out bf16 = GELU(H)
+  EPI_ROPE = 5,      // C bf16 = acc with RoPE applied to the Q/K columns
+};
+
+struct GemmArgs {
+  const void* A = nullptr;
+  int64_t lda = 0;
+  int a_mn = 0;
+  const void* B = nullptr;
+  int64_t ldb = 0;
+  int b_mn = 0;
+  int M = 0, N = 0, K = 0;
+  void* C = nullptr;
+  int64_t ldc = 0;
+  int epi = EPI_BF16;
+  // output column blocking (Ulysses pack): column c goes to
+  //   C + (c / blk_w) * blk_stride + row * ldc + (c % blk_w)     (blk_w = 0: off)
+  int blk_w = 0;
+  int64_t blk_stride = 0;
+  // GELU / dGELU aux tensors, same [M, N] indexing (row stride ld_aux)
+  const void* aux_in = nullptr;
+  void* aux_out = nullptr;
+  int64_t ld_aux = 0;
+  // RoPE: columns laid out in groups of 3*hq = [Q | K | V] (hq = heads * d);
+  // position of row r: (r / seg) * seg_stride + seg_base + (r % seg)
+  const float2* rope = nullptr;   // [positions][d/2] (cos, sin)
+  int rope_d = 0;
+  int rope_hq = 0;
+  int64_t seg = 0, seg_stride = 0, seg_base = 0;
+  // Row remaps of the STORED matrices (seg = 0: identity): logical row r lives at
+  // storage row (r / seg) * stride + base + r % seg.  For A/B this is the TMA outer
+  // coordinate (a tile never crosses a segment: seg % tile rows == 0); for C the
+  // output row.  Used by METP waves to read / write position-ordered buffers.
+  int64_t a_seg = 0, a_stride = 0, a_base = 0;
+  int64_t b_seg = 0, b_stride = 0, b_base = 0;
+  int64_t c_seg = 0, c_stride = 0, c_base = 0;
+  // storage row counts of A / B when remapped (0: the logical extent)
+  int64_t a_rows = 0, b_rows = 0;
+};
+
+// returns 0 on success, a cudaError_t value otherwise
+int gemm_launch(const GemmArgs& g, cudaStream_t st);
+int gemm_num_sms();
+
+}  // namespace pds

@@ -1,0 +1,24 @@
+// Launchers of the non-GEMM kernels (all return 0 or a cudaError_t value).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pds {
+int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
+             void* lse, cudaStream_t st);
+int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
+             int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st);
+int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps, void* x1_out,
+                void* u_out, void* rstd, cudaStream_t st);
+int rmsnorm_bwd_grid(int64_t rows);
+int rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g, const void* dres, int64_t rows,
+                int h, void* dx, float* dg_part, float* dg, cudaStream_t st);
+int apply_norm(const void* x, const void* rstd, const void* g, int64_t rows, int h, void* u, cudaStream_t st);
+int add_bf16(const void* a, const void* b, void* c, int64_t n, cudaStream_t st);
+int add_f32(const void* a, void* acc, int64_t n, cudaStream_t st);
+int sum_bf16_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st);
+int sum_f32_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st);
+int rope_table(void* t, int64_t n_pos, int d, double theta, cudaStream_t st);
+// dst[t][j*cw + c] = src[j][t][c]  (A2A receive buffer -> row-major columns), bf16
+int unpack_blocks(const void* src, int P, int64_t rows, int64_t cw, void* dst, int64_t ld_dst, cudaStream_t st);
+}  // namespace pds

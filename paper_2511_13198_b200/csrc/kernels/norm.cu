@@ -1,0 +1,362 @@
+// HBM-bound elementwise kernels of the layer: fused residual-add + RMSNorm
+// forward / backward (reading R-2: pre-norm Llama block, fp32 statistics),
+// the RoPE cos/sin table (reading R-3: angles formed in fp64), recompute of a
+// normalised activation from its saved input + rstd, and bf16 add / copy.
+//
+// One warp per row, 16-byte vector loads/stores (8 bf16 per lane per vector),
+// warp-shuffle row reductions; VPL = h / 256 vectors per lane kept in registers
+// so every byte is read once.  Algorithmic bytes per element: fwd 8 B with a
+// residual (x, res in; x1, u out), bwd 8 B (du, x, dres in; dx out).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace pds {
+
+__device__ __forceinline__ void unpack8(const uint4& w, float* f) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __bfloat1622float2(b[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint4 w;
+  uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+    u[e] = *reinterpret_cast<uint32_t*>(&v);
+  }
+  return w;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  return v;
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(128)
+    rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
+                       const __nv_bfloat16* __restrict__ g, int64_t rows, int h, float eps,
+                       __nv_bfloat16* __restrict__ x1_out, __nv_bfloat16* __restrict__ u_out,
+                       float* __restrict__ rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
+  float v[VPL][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + i * 32;
+    unpack8(__ldcs(xr + c), v[i]);
+    if (res) {
+      float r[8];
+      unpack8(__ldcs(reinterpret_cast<const uint4*>(res + row * h) + c), r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[i][e] = __bfloat162float(__float2bfloat16_rn(v[i][e] + r[e]));
+      reinterpret_cast<uint4*>(x1_out + row * h)[c] = pack8(v[i]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += v[i][e] * v[i][e];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)h + eps);
+  if (lane == 0) rstd_out[row] = r;
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + i * 32;
+    float gg[8], o[8];
+    unpack8(__ldg(gr + c), gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = v[i][e] * r * gg[e];
+    reinterpret_cast<uint4*>(u_out + row * h)[c] = pack8(o);
+  }
+}
+
+// dx = r (a - xhat mean(a xhat)) + dres, a = du g ; dg_part[block][h] += du xhat
+template <int VPL>
+__global__ void __launch_bounds__(128)
+    rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ du, const __nv_bfloat16* __restrict__ x,
+                       const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ g,
+                       const __nv_bfloat16* __restrict__ dres, int64_t rows, int h,
+                       __nv_bfloat16* __restrict__ dx, float* __restrict__ dg_part) {
+  extern __shared__ float sdg[];
+  for (int i = threadIdx.x; i < h; i += blockDim.x) sdg[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+  for (int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5); row < rows;
+       row += (int64_t)gridDim.x * 4) {
+    const float r = rstd[row];
+    uint4 xr[VPL], dr8[VPL];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + i * 32;
+      xr[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * h) + c);
+      dr8[i] = __ldcs(reinterpret_cast<const uint4*>(du + row * h) + c);
+    }
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + i * 32;
+      float xh[8], d8[8], gg[8];
+      unpack8(xr[i], xh);
+      unpack8(dr8[i], d8);
+      unpack8(__ldg(gr + c), gg);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xh[e] *= r;
+        dot += d8[e] * gg[e] * xh[e];
+        atomicAdd(&sdg[c * 8 + e], d8[e] * xh[e]);
+      }
+    }
+    dot = warp_sum(dot) / (float)h;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = lane + i * 32;
+      float xh[8], d8[8], gg[8], o[8], dr[8];
+      unpack8(xr[i], xh);
+      unpack8(dr8[i], d8);
+      unpack8(__ldg(gr + c), gg);
+      if (dres) unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + row * h) + c), dr);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        o[e] = r * (d8[e] * gg[e] - xh[e] * r * dot) + (dres ? dr[e] : 0.f);
+      reinterpret_cast<uint4*>(dx + row * h)[c] = pack8(o);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < h; i += blockDim.x) dg_part[(int64_t)blockIdx.x * h + i] = sdg[i];
+}
+
+__global__ void reduce_rows_add_kernel(const float* __restrict__ part, int nparts, int h,
+                                       float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  float acc = 0.f;
+  for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * h + i];
+  out[i] += acc;
+}
+
+// u = x * rstd * g  (recompute of a normalised activation from saved x, rstd)
+template <int VPL>
+__global__ void __launch_bounds__(128)
+    apply_norm_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ rstd,
+                      const __nv_bfloat16* __restrict__ g, int64_t rows, int h,
+                      __nv_bfloat16* __restrict__ u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float r = rstd[row];
+  const uint4* gr = reinterpret_cast<const uint4*>(g);
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int c = lane + i * 32;
+    float v[8], gg[8];
+    unpack8(__ldcs(reinterpret_cast<const uint4*>(x + row * h) + c), v);
+    unpack8(__ldg(gr + c), gg);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = v[e] * r * gg[e];
+    reinterpret_cast<uint4*>(u + row * h)[c] = pack8(v);
+  }
+}
+
+__global__ void add_bf16_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                                uint4* __restrict__ c, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float x[8], y[8];
+    unpack8(__ldcs(a + i), x);
+    unpack8(__ldcs(b + i), y);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] += y[e];
+    c[i] = pack8(x);
+  }
+}
+
+// sum of P buffers (loopback reduce-scatter / all-reduce), fp32 accumulation in rank order
+struct Ptrs8 {
+  const void* p[8];
+};
+__global__ void sum_bf16_kernel(Ptrs8 srcs, int P, uint4* __restrict__ dst, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[8], t[8];
+    unpack8(reinterpret_cast<const uint4*>(srcs.p[0])[i], acc);
+    for (int p = 1; p < P; ++p) {
+      unpack8(reinterpret_cast<const uint4*>(srcs.p[p])[i], t);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += t[e];
+    }
+    dst[i] = pack8(acc);
+  }
+}
+__global__ void sum_f32_kernel(Ptrs8 srcs, int P, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = reinterpret_cast<const float*>(srcs.p[0])[i];
+    for (int p = 1; p < P; ++p) acc += reinterpret_cast<const float*>(srcs.p[p])[i];
+    dst[i] = acc;
+  }
+}
+__global__ void add_f32_kernel(const float4* __restrict__ a, float4* __restrict__ acc, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 x = acc[i];
+    const float4 y = a[i];
+    x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+    acc[i] = x;
+  }
+}
+
+// dst[t][j*cw + c] = src[j][t][c]; 16-byte vectors (cw % 8 == 0)
+__global__ void unpack_blocks_kernel(const uint4* __restrict__ src, int P, int64_t rows, int64_t cw8,
+                                     uint4* __restrict__ dst, int64_t ld8) {
+  const int64_t n = (int64_t)P * rows * cw8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % cw8;
+    const int64_t t = (i / cw8) % rows;
+    const int64_t j = i / (cw8 * rows);
+    dst[t * ld8 + j * cw8 + c] = __ldcs(src + i);
+  }
+}
+
+__global__ void rope_table_kernel(float2* __restrict__ t, int64_t n_pos, int d, double theta) {
+  const int d2 = d / 2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pos * d2) return;
+  const int64_t pos = i / d2;
+  const int k = (int)(i % d2);
+  const double inv = pow(theta, -2.0 * (double)k / (double)d);
+  const double ang = (double)pos * inv;        // fp64 angle, fp64 range reduction in sincos
+  double s, c;
+  sincos(ang, &s, &c);
+  t[i] = make_float2((float)c, (float)s);
+}
+
+// ------------------------------------------------------------------ launchers
+#define PDS_UNPACK(...) __VA_ARGS__
+#define PDS_VPL_DISPATCH(h, KERN, LAUNCH, ARGS)                 \
+  switch ((h) / 256) {                                         \
+    case 1: KERN<1><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
+    case 2: KERN<2><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
+    case 4: KERN<4><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
+    case 8: KERN<8><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
+    case 16: KERN<16><<<PDS_UNPACK LAUNCH>>> ARGS; break;      \
+    default: return (int)cudaErrorInvalidValue;                \
+  }
+
+static bool h_ok(int h) {
+  const int v = h / 256;
+  return h % 256 == 0 && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16);
+}
+
+int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps,
+                void* x1_out, void* u_out, void* rstd, cudaStream_t st) {
+  if (!h_ok(h)) return (int)cudaErrorInvalidValue;
+  if (rows <= 0) return 0;
+  const unsigned grid = (unsigned)((rows + 3) / 4);
+  auto X = reinterpret_cast<const __nv_bfloat16*>(x);
+  auto R = reinterpret_cast<const __nv_bfloat16*>(res);
+  auto G = reinterpret_cast<const __nv_bfloat16*>(g);
+  auto X1 = reinterpret_cast<__nv_bfloat16*>(x1_out);
+  auto U = reinterpret_cast<__nv_bfloat16*>(u_out);
+  auto RS = reinterpret_cast<float*>(rstd);
+  PDS_VPL_DISPATCH(h, rmsnorm_fwd_kernel, (grid, 128, 0, st), (X, R, G, rows, h, eps, X1, U, RS));
+  return (int)cudaGetLastError();
+}
+
+int rmsnorm_bwd_grid(int64_t rows) {
+  int64_t b = (rows + 3) / 4;
+  return (int)(b < 592 ? b : 592);
+}
+
+// dg_part: fp32 scratch [rmsnorm_bwd_grid(rows)][h]; dg (fp32 [h]) += reduced partials
+int rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g, const void* dres,
+                int64_t rows, int h, void* dx, float* dg_part, float* dg, cudaStream_t st) {
+  if (!h_ok(h)) return (int)cudaErrorInvalidValue;
+  if (rows <= 0) return 0;
+  const int grid = rmsnorm_bwd_grid(rows);
+  auto DU = reinterpret_cast<const __nv_bfloat16*>(du);
+  auto X = reinterpret_cast<const __nv_bfloat16*>(x);
+  auto RS = reinterpret_cast<const float*>(rstd);
+  auto G = reinterpret_cast<const __nv_bfloat16*>(g);
+  auto DR = reinterpret_cast<const __nv_bfloat16*>(dres);
+  auto DX = reinterpret_cast<__nv_bfloat16*>(dx);
+  const size_t smem = (size_t)h * sizeof(float);
+  PDS_VPL_DISPATCH(h, rmsnorm_bwd_kernel, (grid, 128, smem, st), (DU, X, RS, G, DR, rows, h, DX, dg_part));
+  reduce_rows_add_kernel<<<(h + 255) / 256, 256, 0, st>>>(dg_part, grid, h, dg);
+  return (int)cudaGetLastError();
+}
+
+int apply_norm(const void* x, const void* rstd, const void* g, int64_t rows, int h, void* u,
+               cudaStream_t st) {
+  if (!h_ok(h)) return (int)cudaErrorInvalidValue;
+  if (rows <= 0) return 0;
+  const unsigned grid = (unsigned)((rows + 3) / 4);
+  auto X = reinterpret_cast<const __nv_bfloat16*>(x);
+  auto RS = reinterpret_cast<const float*>(rstd);
+  auto G = reinterpret_cast<const __nv_bfloat16*>(g);
+  auto U = reinterpret_cast<__nv_bfloat16*>(u);
+  PDS_VPL_DISPATCH(h, apply_norm_kernel, (grid, 128, 0, st), (X, RS, G, rows, h, U));
+  return (int)cudaGetLastError();
+}
+
+static unsigned ew_grid(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return (unsigned)(b < 148 * 16 ? b : 148 * 16);
+}
+
+int add_bf16(const void* a, const void* b, void* c, int64_t n, cudaStream_t st) {
+  if (n % 8) return (int)cudaErrorInvalidValue;
+  add_bf16_kernel<<<ew_grid(n / 8), 256, 0, st>>>(reinterpret_cast<const uint4*>(a),
+                                                  reinterpret_cast<const uint4*>(b),
+                                                  reinterpret_cast<uint4*>(c), n / 8);
+  return (int)cudaGetLastError();
+}
+int sum_bf16_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st) {
+  if (n % 8 || P > 8) return (int)cudaErrorInvalidValue;
+  Ptrs8 p{};
+  for (int i = 0; i < P; ++i) p.p[i] = srcs[i];
+  sum_bf16_kernel<<<ew_grid(n / 8), 256, 0, st>>>(p, P, reinterpret_cast<uint4*>(dst), n / 8);
+  return (int)cudaGetLastError();
+}
+int sum_f32_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st) {
+  if (P > 8) return (int)cudaErrorInvalidValue;
+  Ptrs8 p{};
+  for (int i = 0; i < P; ++i) p.p[i] = srcs[i];
+  sum_f32_kernel<<<ew_grid(n), 256, 0, st>>>(p, P, reinterpret_cast<float*>(dst), n);
+  return (int)cudaGetLastError();
+}
+int add_f32(const void* a, void* acc, int64_t n, cudaStream_t st) {
+  if (n % 4) return (int)cudaErrorInvalidValue;
+  add_f32_kernel<<<ew_grid(n / 4), 256, 0, st>>>(reinterpret_cast<const float4*>(a),
+                                                 reinterpret_cast<float4*>(acc), n / 4);
+  return (int)cudaGetLastError();
+}
+
+int unpack_blocks(const void* src, int P, int64_t rows, int64_t cw, void* dst, int64_t ld_dst,
+                  cudaStream_t st) {
+  if (cw % 8 || ld_dst % 8) return (int)cudaErrorInvalidValue;
+  const int64_t n = (int64_t)P * rows * cw / 8;
+  unpack_blocks_kernel<<<ew_grid(n), 256, 0, st>>>(reinterpret_cast<const uint4*>(src), P, rows, cw / 8,
+                                                   reinterpret_cast<uint4*>(dst), ld_dst / 8);
+  return (int)cudaGetLastError();
+}
+
+int rope_table(void* t, int64_t n_pos, int d, double theta, cudaStream_t st) {
+  const int64_t n = n_pos * (d / 2);
+  rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(reinterpret_cast<float2*>(t), n_pos,
+                                                                  d, theta);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace pds

@@ -1,0 +1,874 @@
+// The switchable functional parallelism library:
+// one Transformer layer f_{pi,FFN} o f_{pi,MHA} per strategy pi, forward and
+// backward, over the unified boundary layout [s/P, b, h] (Table 2 spec row,
+// PAPER.md:139).  Every strategy consumes and produces the same layout, so a
+// layer-wise switch is a different function pointer, never a redistribution
+// (PAPER.md:45, 224, 294).
+//
+//   MegatronTS  AG(s) -> column-parallel QKV(+RoPE) / FC1(+GELU) -> row-parallel
+//               proj / FC2 -> RS(s)
+//   UlyssesZ    AG(weights, ZeRO3) -> local QKV packed per head group -> A2A
+//               seq->heads -> attention -> A2A heads->seq
+//   METP        the TS dataflow in c waves of s/(Pc) rows per rank, per-wave AG/RS,
+//               GEMMs reading / writing position-ordered buffers through TMA row
+//               remaps (no gather copies), FFN recomputed in bwd  (R-11)
+//
+// Readings R-1..R-36 of DESIGN.md; buffer plan in planner.cpp (make_plan).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "comm.hpp"
+#include "internal.hpp"
+#include "kernels/gemm.cuh"
+#include "kernels/kernels.hpp"
+
+using namespace pds;
+
+struct ProfRec {
+  int klass;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
+struct pds_saved {
+  int strategy;
+  int64_t s;
+  const void* x;
+  char* mem;
+  int64_t bytes;
+  BufPlan plan;
+  char* at(const char* n) const { return mem + plan.saved_off(n); }
+};
+
+struct pds_group {
+  LoopGroup g;
+};
+
+struct pds_ctx {
+  pds_model m{};
+  int P = 1, rank = 0, device = 0;
+  Comm* comm = nullptr;
+  // rope table (float2 [rope_pos][d/2])
+  void* rope = nullptr;
+  int64_t rope_pos = 0;
+  // workspace
+  char* ws = nullptr;
+  int64_t ws_cap = 0;
+  // saved arena: cached blocks by size
+  std::multimap<int64_t, char*> free_blocks;
+  int64_t saved_live = 0;
+  // planner
+  Bundle bundle;
+  double capacity = 0, gamma = 0;
+  uint32_t enabled = 0x7;
+  std::map<std::pair<int, int64_t>, std::pair<std::vector<uint8_t>, bool>> cache;
+  std::vector<uint8_t> prev;
+  // debug taps
+  void* tap_o = nullptr;
+  void* tap_z = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double acc_ms[5] = {0}, acc_flops[5] = {0}, acc_bytes[5] = {0};
+  int64_t acc_n[5] = {0};
+
+  ~pds_ctx() {
+    for (auto& r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    if (ws) cudaFree(ws);
+    if (rope) cudaFree(rope);
+    delete comm;
+  }
+  cudaEvent_t ev() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+
+enum { K_GEMM = 0, K_ATTN_F = 1, K_ATTN_B = 2, K_NORM = 3, K_COMM = 4 };
+
+struct Prof {
+  pds_ctx* c;
+  cudaStream_t st;
+  int k;
+  double fl, by;
+  cudaEvent_t a = nullptr;
+  Prof(pds_ctx* c_, cudaStream_t s_, int k_, double f_, double b_) : c(c_), st(s_), k(k_), fl(f_), by(b_) {
+    if (c->prof) {
+      a = c->ev();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Prof() {
+    if (a) {
+      cudaEvent_t b = c->ev();
+      cudaEventRecord(b, st);
+      c->pending.push_back(ProfRec{k, a, b, fl, by});
+    }
+  }
+};
+
+pds_status kerr(int rc, const char* what) {
+  if (rc == 0) return PDS_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString((cudaError_t)rc));
+  return rc == (int)cudaErrorMemoryAllocation ? PDS_ENOMEM : PDS_ECUDA;
+}
+
+struct Exec {
+  pds_ctx* c;
+  cudaStream_t st;
+  const pds_model& m;
+  int P, r;
+  int64_t s, sl, h, F, nl, d, hl, Fl;
+  Exec(pds_ctx* c_, cudaStream_t st_, int64_t s_)
+      : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), s(s_), sl(s_ / c_->P), h(c_->m.h), F(c_->m.ffn),
+        nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
+
+  pds_status gemm(GemmArgs g) {
+    Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 0);
+    return kerr(gemm_launch(g, st), "gemm");
+  }
+  // C[M,N] = A * B^T helpers
+  static GemmArgs G(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int64_t M,
+                    int64_t N, int64_t K, void* C, int64_t ldc, int epi = EPI_BF16) {
+    GemmArgs g;
+    g.A = A; g.lda = lda; g.a_mn = a_mn; g.B = B; g.ldb = ldb; g.b_mn = b_mn;
+    g.M = (int)M; g.N = (int)N; g.K = (int)K; g.C = C; g.ldc = ldc; g.epi = epi;
+    return g;
+  }
+  GemmArgs rope(GemmArgs g, int64_t hq, int64_t seg, int64_t seg_stride, int64_t seg_base) {
+    g.epi = EPI_ROPE;
+    g.rope = reinterpret_cast<const float2*>(c->rope);
+    g.rope_d = (int)d;
+    g.rope_hq = (int)hq;
+    g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
+    return g;
+  }
+  pds_status norm_fwd(const void* x, const void* res, const void* g, int64_t rows, void* x1, void* u, void* rstd) {
+    Prof p(c, st, K_NORM, 0, (double)rows * h * (res ? 8 : 4) + rows * 4);
+    return kerr(rmsnorm_fwd(x, res, g, rows, (int)h, m.norm_eps, x1, u, rstd, st), "rmsnorm_fwd");
+  }
+  pds_status norm_bwd(const void* du, const void* x, const void* rstd, const void* g, const void* dres,
+                      int64_t rows, void* dx, float* dgp, float* dg) {
+    Prof p(c, st, K_NORM, 0, (double)rows * h * (dres ? 8 : 6));
+    return kerr(rmsnorm_bwd(du, x, rstd, g, dres, rows, (int)h, dx, dgp, dg, st), "rmsnorm_bwd");
+  }
+  pds_status apply(const void* x, const void* rstd, const void* g, int64_t rows, void* u) {
+    Prof p(c, st, K_NORM, 0, (double)rows * h * 4);
+    return kerr(apply_norm(x, rstd, g, rows, (int)h, u, st), "apply_norm");
+  }
+  pds_status add(const void* a, const void* b, void* out, int64_t n) {
+    Prof p(c, st, K_NORM, 0, (double)n * 6);
+    return kerr(add_bf16(a, b, out, n, st), "add_bf16");
+  }
+  pds_status attn_f(const void* qkv, void* out, void* lse) {
+    const double fl = 4.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
+    Prof p(c, st, K_ATTN_F, fl, 0);
+    return kerr(attn_fwd(qkv, 3 * hl, (int)s, (int)nl, (int)d, m.causal, out, hl, lse, st), "attn_fwd");
+  }
+  pds_status attn_b(const void* qkv, const void* out, const void* lse, const void* dout, void* dqkv, float* dd) {
+    const double fl = 10.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
+    Prof p(c, st, K_ATTN_B, fl, 0);
+    return kerr(attn_bwd(qkv, 3 * hl, out, hl, lse, dout, (int)s, (int)nl, (int)d, m.causal, dqkv, c->rope, dd, st),
+                "attn_bwd");
+  }
+  // collectives
+  pds_status ag(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
+    Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
+    return c->comm->all_gather(send, recv, count, dt, st);
+  }
+  pds_status rs(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
+    Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
+    return c->comm->reduce_scatter(send, recv, count, dt, st);
+  }
+  pds_status a2a(const void* send, void* recv, int64_t count) {
+    Prof p(c, st, K_COMM, 0, (double)count * 2 * (P - 1));
+    return c->comm->all_to_all(send, recv, count, DT_BF16, st);
+  }
+  pds_status dgamma(float* dgl, const pds_grads* g) {
+    {
+      Prof p(c, st, K_COMM, 0, 2.0 * h * 4 * 2 * (P - 1));
+      PDS_TRY(c->comm->all_reduce(dgl, 2 * h, DT_F32, st));
+    }
+    PDS_TRY(kerr(add_f32(dgl, g->dg1, h, st), "add_f32"));
+    return kerr(add_f32(dgl + h, g->dg2, h, st), "add_f32");
+  }
+  pds_status tap(void* dst, const void* src, int64_t n) {
+    if (!dst) return PDS_OK;
+    PDS_CUDA(cudaMemcpyAsync(dst, src, n * 2, cudaMemcpyDeviceToDevice, st));
+    return PDS_OK;
+  }
+};
+
+#define B16(p) (reinterpret_cast<char*>(p))
+
+// ================================================================== MegatronTS
+pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
+  const BufPlan& bp = sv->plan;
+  char* gather = ws + bp.ws_off("gather");
+  char* partial = ws + bp.ws_off("partial");
+  char* f0 = ws + bp.ws_off("f0");
+  const int64_t slot = e.r * e.sl * e.h * 2;
+  PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, gather + slot, sv->at("rstd1")));
+  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u)
+  PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
+                        e.hl, 0, 0, 0)));                                                // Eq. 1 + RoPE
+  PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));                          // Eq. 2
+  PDS_TRY(e.gemm(Exec::G(sv->at("a"), e.hl, 0, w->w_proj, e.h, 1, e.s, e.h, e.hl, partial, e.h)));  // Eq. 3
+  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(o)
+  PDS_TRY(e.tap(e.c->tap_o, partial + slot, e.sl * e.h));
+  PDS_TRY(e.norm_fwd(x, partial + slot, w->g2, e.sl, sv->at("x1"), gather + slot, sv->at("rstd2")));
+  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(v)
+  GemmArgs fc1 = Exec::G(gather, e.h, 0, w->w_in_t, e.h, 0, e.s, e.Fl, e.h, sv->at("h"), e.Fl, EPI_GELU);
+  fc1.aux_out = f0; fc1.ld_aux = e.Fl;
+  PDS_TRY(e.gemm(fc1));                                                                 // Eq. 4 (GELU)
+  PDS_TRY(e.gemm(Exec::G(f0, e.Fl, 0, w->w_out, e.h, 1, e.s, e.h, e.Fl, partial, e.h)));
+  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(z)
+  PDS_TRY(e.tap(e.c->tap_z, partial + slot, e.sl * e.h));
+  return e.add(sv->at("x1"), partial + slot, y, e.sl * e.h);
+}
+
+pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
+                  char* ws) {
+  const BufPlan& bp = sv->plan;
+  char* gather = ws + bp.ws_off("gather");
+  char* partial = ws + bp.ws_off("partial");
+  char* f0 = ws + bp.ws_off("f0");
+  char* f1 = ws + bp.ws_off("f1");
+  float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
+  float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
+  float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  const int64_t slot = e.r * e.sl * e.h * 2;
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  PDS_TRY(e.ag(dy, gather, e.sl * e.h));                                                // AG(dz)
+  GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
+  dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.Fl;
+  PDS_TRY(e.gemm(dgel));                                                                // dH, G
+  PDS_TRY(e.gemm(Exec::G(f0, e.Fl, 1, gather, e.h, 1, e.Fl, e.h, e.s, g->dw_out, e.h, EPI_F32_ACC)));
+  PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, gather + slot));
+  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(v) re-gather
+  PDS_TRY(e.gemm(Exec::G(f1, e.Fl, 1, gather, e.h, 1, e.Fl, e.h, e.s, g->dw_in_t, e.h, EPI_F32_ACC)));
+  PDS_TRY(e.gemm(Exec::G(f1, e.Fl, 0, w->w_in_t, e.h, 1, e.s, e.h, e.Fl, partial, e.h)));
+  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(dv)
+  PDS_TRY(e.norm_bwd(partial + slot, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
+  PDS_TRY(e.ag(dx, gather, e.sl * e.h));                                                // AG(dx1)
+  PDS_TRY(e.gemm(Exec::G(gather, e.h, 0, w->w_proj, e.h, 0, e.s, e.hl, e.h, f1, e.hl)));  // dA
+  PDS_TRY(e.gemm(Exec::G(sv->at("a"), e.hl, 1, gather, e.h, 1, e.hl, e.h, e.s, g->dw_proj, e.h, EPI_F32_ACC)));
+  PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), f1, f0, dd));            // dQKV (RoPE^T)
+  PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, gather + slot));
+  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u) re-gather
+  PDS_TRY(e.gemm(Exec::G(f0, 3 * e.hl, 1, gather, e.h, 1, 3 * e.hl, e.h, e.s, g->dw_qkv_t, e.h, EPI_F32_ACC)));
+  PDS_TRY(e.gemm(Exec::G(f0, 3 * e.hl, 0, w->w_qkv_t, e.h, 1, e.s, e.h, 3 * e.hl, partial, e.h)));
+  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(du)
+  PDS_TRY(e.norm_bwd(partial + slot, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
+  return e.dgamma(dgl, g);
+}
+
+// ================================================================== UlyssesZ
+pds_status uz_gather_w(Exec& e, const pds_weights* w, char* ws, const BufPlan& bp) {
+  PDS_TRY(e.ag(w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));   // ZeRO3: rows contiguous
+  PDS_TRY(e.ag(w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
+  PDS_TRY(e.ag(w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
+  return e.ag(w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h);
+}
+
+pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
+  const BufPlan& bp = sv->plan;
+  PDS_TRY(uz_gather_w(e, w, ws, bp));
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* u1 = ws + bp.ws_off("u1");
+  char* s1 = ws + bp.ws_off("s1");
+  char* r1 = ws + bp.ws_off("r1");
+  char* f0 = ws + bp.ws_off("f0");
+  PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
+  // local QKV for all heads, head-group-major columns, written straight into the A2A
+  // send layout [P][s/P][3h/P]; RoPE at global positions r*s/P + t
+  GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, 3 * e.h, e.h, s1, 3 * e.hl), e.hl, 0, 0, e.r * e.sl);
+  q.blk_w = (int)(3 * e.hl);
+  q.blk_stride = e.sl * 3 * e.hl;
+  PDS_TRY(e.gemm(q));
+  PDS_TRY(e.a2a(s1, sv->at("qkv"), e.sl * 3 * e.hl));                                  // A2A seq -> heads
+  PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));
+  PDS_TRY(e.a2a(sv->at("a"), r1, e.sl * e.hl));                                        // A2A heads -> seq
+  {
+    Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * e.h);
+    PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, e.hl, sv->at("afull"), e.h, e.st), "unpack"));
+  }
+  PDS_TRY(e.gemm(Exec::G(sv->at("afull"), e.h, 0, wproj, e.h, 1, e.sl, e.h, e.h, u1, e.h)));  // O
+  PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
+  PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), s1, sv->at("rstd2")));
+  GemmArgs fc1 = Exec::G(s1, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
+  fc1.aux_out = f0; fc1.ld_aux = e.F;
+  PDS_TRY(e.gemm(fc1));
+  PDS_TRY(e.gemm(Exec::G(f0, e.F, 0, wout, e.h, 1, e.sl, e.h, e.F, u1, e.h)));          // Z
+  PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * e.h));
+  return e.add(sv->at("x1"), u1, y, e.sl * e.h);
+}
+
+pds_status uz_dw(Exec& e, char* dw, int64_t rows_full, void* grad) {
+  // ZeRO3: reduce-scatter the full local fp32 dW into spec shards, then accumulate
+  const int64_t cnt = rows_full / e.P * e.h;
+  char* mine = dw + e.r * cnt * 4;
+  PDS_TRY(e.rs(dw, mine, cnt, DT_F32));
+  return kerr(add_f32(mine, grad, cnt, e.st), "add_f32");
+}
+
+pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
+                  char* ws) {
+  const BufPlan& bp = sv->plan;
+  PDS_TRY(uz_gather_w(e, w, ws, bp));
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* dw = ws + bp.ws_off("dw");
+  char* u1 = ws + bp.ws_off("u1");
+  char* s1 = ws + bp.ws_off("s1");
+  char* r1 = ws + bp.ws_off("r1");
+  char* f0 = ws + bp.ws_off("f0");
+  char* f1 = ws + bp.ws_off("f1");
+  char* x3 = ws + bp.ws_off("x3");
+  char* x4 = ws + bp.ws_off("x4");
+  char* v2 = ws + bp.ws_off("v2");
+  float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
+  float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
+  float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
+  dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.F;
+  PDS_TRY(e.gemm(dgel));
+  PDS_TRY(e.gemm(Exec::G(f0, e.F, 1, dy, e.h, 1, e.F, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
+  PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
+  PDS_TRY(e.gemm(Exec::G(f1, e.F, 1, u1, e.h, 1, e.F, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(e.gemm(Exec::G(f1, e.F, 0, win, e.h, 1, e.sl, e.h, e.F, v2, e.h)));
+  PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
+  GemmArgs dafull = Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, s1, e.hl);
+  dafull.blk_w = (int)e.hl;
+  dafull.blk_stride = e.sl * e.hl;
+  PDS_TRY(e.gemm(dafull));                                                              // packed for A2A
+  PDS_TRY(e.gemm(Exec::G(sv->at("afull"), e.h, 1, dx, e.h, 1, e.h, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
+  PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                                 // A2A(dO)
+  PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), r1, x3, dd));
+  PDS_TRY(e.a2a(x3, r1, e.sl * 3 * e.hl));                                             // A2A(dQKV)
+  {
+    Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * 3 * e.h);
+    PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, 3 * e.hl, x4, 3 * e.h, e.st), "unpack"));
+  }
+  PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
+  PDS_TRY(e.gemm(Exec::G(x4, 3 * e.h, 1, u1, e.h, 1, 3 * e.h, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(uz_dw(e, dw, 3 * e.h, g->dw_qkv_t));
+  PDS_TRY(e.gemm(Exec::G(x4, 3 * e.h, 0, wqkv, e.h, 1, e.sl, e.h, 3 * e.h, v2, e.h)));
+  PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
+  return e.dgamma(dgl, g);
+}
+
+// ================================================================== METP (R-METP)
+int64_t metp_c(const Exec& e) { return e.m.metp_chunks > 0 ? e.m.metp_chunks : e.P; }
+
+pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
+  const BufPlan& bp = sv->plan;
+  const int64_t c = metp_c(e), wr = e.sl / c, W = e.P * wr;   // wave rows per rank / gathered
+  char* ul = ws + bp.ws_off("ul");
+  char* vl = ws + bp.ws_off("vl");
+  char* wg = ws + bp.ws_off("wg");
+  char* pw = ws + bp.ws_off("pw");
+  char* hw = ws + bp.ws_off("hw");
+  char* gw = ws + bp.ws_off("gw");
+  const int64_t row = e.h * 2;
+  const int64_t slot = e.r * wr * e.h * 2;
+  const char* xb = static_cast<const char*>(x);
+  PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, ul, sv->at("rstd1")));
+  for (int64_t k = 0; k < c; ++k) {   // QKV waves: rows land at their global positions
+    PDS_TRY(e.ag(ul + k * wr * row, wg, wr * e.h));
+    GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
+                        e.hl, wr, e.sl, k * wr);
+    q.c_seg = wr; q.c_stride = e.sl; q.c_base = k * wr;
+    PDS_TRY(e.gemm(q));
+  }
+  PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));  // query-chunk x KV-chunk loop
+  for (int64_t k = 0; k < c; ++k) {   // projection waves
+    GemmArgs pj = Exec::G(sv->at("a"), e.hl, 0, w->w_proj, e.h, 1, W, e.h, e.hl, pw, e.h);
+    pj.a_seg = wr; pj.a_stride = e.sl; pj.a_base = k * wr; pj.a_rows = e.s;
+    PDS_TRY(e.gemm(pj));
+    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
+    if (e.c->tap_o) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_o) + k * wr * row, pw + slot, wr * e.h));
+    PDS_TRY(e.norm_fwd(xb + k * wr * row, pw + slot, w->g2, wr, sv->at("x1") + k * wr * row, vl + k * wr * row,
+                       sv->at("rstd2") + k * wr * 4));
+  }
+  for (int64_t k = 0; k < c; ++k) {   // FFN waves
+    PDS_TRY(e.ag(vl + k * wr * row, wg, wr * e.h));
+    GemmArgs fc1 = Exec::G(wg, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
+    fc1.aux_out = gw; fc1.ld_aux = e.Fl;
+    PDS_TRY(e.gemm(fc1));
+    PDS_TRY(e.gemm(Exec::G(gw, e.Fl, 0, w->w_out, e.h, 1, W, e.h, e.Fl, pw, e.h)));
+    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
+    if (e.c->tap_z) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_z) + k * wr * row, pw + slot, wr * e.h));
+    PDS_TRY(e.add(sv->at("x1") + k * wr * row, pw + slot, static_cast<char*>(y) + k * wr * row, wr * e.h));
+  }
+  return PDS_OK;
+}
+
+pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
+                    char* ws) {
+  const BufPlan& bp = sv->plan;
+  const int64_t c = metp_c(e), wr = e.sl / c, W = e.P * wr;
+  char* ul = ws + bp.ws_off("ul");
+  char* vl = ws + bp.ws_off("vl");
+  char* wg = ws + bp.ws_off("wg");
+  char* wg2 = ws + bp.ws_off("wg2");
+  char* pw = ws + bp.ws_off("pw");
+  char* hw = ws + bp.ws_off("hw");
+  char* gw = ws + bp.ws_off("gw");
+  char* dhw = ws + bp.ws_off("dhw");
+  char* da = ws + bp.ws_off("da");
+  char* dqkv = ws + bp.ws_off("dqkv");
+  float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
+  float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
+  float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  const int64_t row = e.h * 2;
+  const int64_t slot = e.r * wr * e.h * 2;
+  const char* dyb = static_cast<const char*>(dy);
+  const char* xb = static_cast<const char*>(sv->x);
+  char* dxb = static_cast<char*>(dx);
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  for (int64_t k = 0; k < c; ++k) {   // FFN backward waves, recomputing v, H, G
+    const int64_t o = k * wr;
+    PDS_TRY(e.ag(dyb + o * row, wg, wr * e.h));                                         // AG(dz)
+    PDS_TRY(e.apply(sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, wr, vl));
+    PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                    // AG(v)
+    PDS_TRY(e.gemm(Exec::G(wg2, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl)));   // H recompute
+    GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.Fl, EPI_DGELU);
+    dgel.aux_in = hw; dgel.aux_out = gw; dgel.ld_aux = e.Fl;
+    PDS_TRY(e.gemm(dgel));
+    PDS_TRY(e.gemm(Exec::G(gw, e.Fl, 1, wg, e.h, 1, e.Fl, e.h, W, g->dw_out, e.h, EPI_F32_ACC)));
+    PDS_TRY(e.gemm(Exec::G(dhw, e.Fl, 1, wg2, e.h, 1, e.Fl, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC)));
+    PDS_TRY(e.gemm(Exec::G(dhw, e.Fl, 0, w->w_in_t, e.h, 1, W, e.h, e.Fl, pw, e.h)));
+    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(dv)
+    PDS_TRY(e.norm_bwd(pw + slot, sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, dyb + o * row, wr,
+                       dxb + o * row, dgp, dgl + e.h));
+  }
+  for (int64_t k = 0; k < c; ++k) {   // projection backward waves
+    const int64_t o = k * wr;
+    PDS_TRY(e.ag(dxb + o * row, wg, wr * e.h));                                          // AG(dx1)
+    GemmArgs dA = Exec::G(wg, e.h, 0, w->w_proj, e.h, 0, W, e.hl, e.h, da, e.hl);
+    dA.c_seg = wr; dA.c_stride = e.sl; dA.c_base = o;
+    PDS_TRY(e.gemm(dA));
+    GemmArgs dwp = Exec::G(sv->at("a"), e.hl, 1, wg, e.h, 1, e.hl, e.h, W, g->dw_proj, e.h, EPI_F32_ACC);
+    dwp.a_seg = wr; dwp.a_stride = e.sl; dwp.a_base = o; dwp.a_rows = e.s;
+    PDS_TRY(e.gemm(dwp));
+  }
+  PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), da, dqkv, dd));
+  for (int64_t k = 0; k < c; ++k) {   // QKV backward waves
+    const int64_t o = k * wr;
+    PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
+    PDS_TRY(e.ag(ul, wg, wr * e.h));                                                     // AG(u)
+    GemmArgs dwq = Exec::G(dqkv, 3 * e.hl, 1, wg, e.h, 1, 3 * e.hl, e.h, W, g->dw_qkv_t, e.h, EPI_F32_ACC);
+    dwq.a_seg = wr; dwq.a_stride = e.sl; dwq.a_base = o; dwq.a_rows = e.s;
+    PDS_TRY(e.gemm(dwq));
+    GemmArgs du = Exec::G(dqkv, 3 * e.hl, 0, w->w_qkv_t, e.h, 1, W, e.h, 3 * e.hl, pw, e.h);
+    du.a_seg = wr; du.a_stride = e.sl; du.a_base = o; du.a_rows = e.s;
+    PDS_TRY(e.gemm(du));
+    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(du)
+    PDS_TRY(e.norm_bwd(pw + slot, xb + o * row, sv->at("rstd1") + o * 4, w->g1, dxb + o * row, wr, dxb + o * row,
+                       dgp, dgl));
+  }
+  return e.dgamma(dgl, g);
+}
+
+// ------------------------------------------------------------------ ctx helpers
+pds_status ensure_ws(pds_ctx* c, int64_t bytes, cudaStream_t st) {
+  if (bytes <= c->ws_cap) return PDS_OK;
+  PDS_CUDA(cudaStreamSynchronize(st));
+  if (c->ws) PDS_CUDA(cudaFree(c->ws));
+  c->ws = nullptr;
+  c->ws_cap = 0;
+  PDS_CUDA(cudaMalloc(&c->ws, bytes));
+  c->ws_cap = bytes;
+  return PDS_OK;
+}
+
+pds_status ensure_rope(pds_ctx* c, int64_t s, cudaStream_t st) {
+  if (s <= c->rope_pos) return PDS_OK;
+  const int64_t d = c->m.h / c->m.n_heads;
+  const int64_t n = std::max<int64_t>(s, 2 * c->rope_pos);
+  PDS_CUDA(cudaStreamSynchronize(st));
+  if (c->rope) PDS_CUDA(cudaFree(c->rope));
+  c->rope = nullptr;
+  PDS_CUDA(cudaMalloc(&c->rope, n * (d / 2) * 8));
+  c->rope_pos = n;
+  return kerr(rope_table(c->rope, n, (int)d, c->m.rope_theta, st), "rope_table");
+}
+
+pds_status alloc_saved(pds_ctx* c, int64_t bytes, char** out) {
+  auto it = c->free_blocks.find(bytes);
+  if (it != c->free_blocks.end()) {
+    *out = it->second;
+    c->free_blocks.erase(it);
+    return PDS_OK;
+  }
+  cudaError_t e = cudaMalloc(out, bytes);
+  if (e == cudaErrorMemoryAllocation && !c->free_blocks.empty()) {
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    for (auto& kv : c->free_blocks) cudaFree(kv.second);
+    c->free_blocks.clear();
+    e = cudaMalloc(out, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(std::string("saved arena cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? PDS_ENOMEM : PDS_ECUDA;
+  }
+  return PDS_OK;
+}
+
+pds_status check_layer(pds_ctx* c, uint8_t strategy, int64_t s) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (strategy >= PDS_N_STRATEGIES) PDS_FAIL(PDS_ESTRATEGY, "unknown strategy id " + std::to_string(strategy));
+  return PDS_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" pds_status pds_nccl_unique_id(void* out128);
+
+static pds_status ctx_common(pds_ctx* c, const pds_model* m, int P, int rank, int device) {
+  if (!m) PDS_FAIL(PDS_EINVAL, "NULL model");
+  if (P < 1 || P > 8) PDS_FAIL(PDS_EINVAL, "P must be in [1, 8]");
+  if (rank < 0 || rank >= P) PDS_FAIL(PDS_EINVAL, "rank out of range");
+  c->m = *m;
+  if (c->m.norm_eps <= 0) c->m.norm_eps = 1e-5f;
+  if (c->m.rope_theta <= 0) c->m.rope_theta = 10000.0;
+  c->P = P;
+  c->rank = rank;
+  c->device = device;
+  BufPlan probe;
+  PDS_TRY(make_plan(c->m, P, PDS_MEGATRON_TS, (int64_t)128 * P, &probe));   // validates dims
+  PDS_CUDA(cudaSetDevice(device));
+  size_t fr = 0, tot = 0;
+  PDS_CUDA(cudaMemGetInfo(&fr, &tot));
+  c->capacity = (double)tot;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_create(const pds_model* model, int32_t P, int32_t rank, int32_t device,
+                                 const void* nccl_unique_id, pds_ctx** out) {
+  if (!out) PDS_FAIL(PDS_EINVAL, "NULL out");
+  std::unique_ptr<pds_ctx> c(new pds_ctx());
+  PDS_TRY(ctx_common(c.get(), model, P, rank, device));
+  if (P == 1) {
+    c->comm = make_self_comm();
+  } else {
+    if (!nccl_unique_id) PDS_FAIL(PDS_EINVAL, "P > 1 needs an NCCL unique id");
+    pds_status st = PDS_OK;
+    c->comm = make_nccl_comm(P, rank, nccl_unique_id, &st);
+    if (st != PDS_OK) return st;
+  }
+  *out = c.release();
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_group_create(int32_t P, pds_group** out) {
+  if (!out || P < 1 || P > 8) PDS_FAIL(PDS_EINVAL, "pds_group_create: bad args");
+  pds_group* g = new pds_group();
+  g->g.P = P;
+  g->g.ptr.assign(P, nullptr);
+  g->g.ready.resize(P);
+  g->g.done.resize(P);
+  for (int i = 0; i < P; ++i) {
+    cudaEventCreateWithFlags(&g->g.ready[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->g.done[i], cudaEventDisableTiming);
+  }
+  *out = g;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_group_destroy(pds_group* g) {
+  if (!g) return PDS_OK;
+  for (auto e : g->g.ready) cudaEventDestroy(e);
+  for (auto e : g->g.done) cudaEventDestroy(e);
+  delete g;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_create_loopback(const pds_model* model, pds_group* g, int32_t rank, int32_t device,
+                                          pds_ctx** out) {
+  if (!out || !g) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  std::unique_ptr<pds_ctx> c(new pds_ctx());
+  PDS_TRY(ctx_common(c.get(), model, g->g.P, rank, device));
+  pds_status st = PDS_OK;
+  c->comm = g->g.P == 1 ? make_self_comm() : make_loop_comm(&g->g, rank, &st);
+  if (st != PDS_OK) return st;
+  *out = c.release();
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_destroy(pds_ctx* c) {
+  if (!c) return PDS_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  delete c;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_reserve(pds_ctx* c, int64_t max_seq_len, uint32_t mask) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  int64_t need = 0;
+  for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
+    if (!(mask >> i & 1)) continue;
+    BufPlan bp;
+    PDS_TRY(make_plan(c->m, c->P, i, max_seq_len, &bp));
+    need = std::max(need, bp.ws_bytes);
+  }
+  PDS_CUDA(cudaSetDevice(c->device));
+  PDS_TRY(ensure_ws(c, need, 0));
+  return ensure_rope(c, max_seq_len, 0);
+}
+
+extern "C" pds_status pds_debug_taps(pds_ctx* c, void* o_out, void* z_out) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  c->tap_o = o_out;
+  c->tap_z = z_out;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_len, const void* x,
+                                    const pds_weights* w, void* y, pds_saved** saved, void* stream) {
+  PDS_TRY(check_layer(c, strategy, seq_len));
+  if (!x || !w || !y) PDS_FAIL(PDS_EINVAL, "NULL x / w / y");
+  if (!w->w_qkv_t || !w->w_proj || !w->w_in_t || !w->w_out || !w->g1 || !w->g2)
+    PDS_FAIL(PDS_EINVAL, "NULL weight pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  BufPlan bp;
+  PDS_TRY(make_plan(c->m, c->P, strategy, seq_len, &bp));
+  PDS_CUDA(cudaSetDevice(c->device));
+  PDS_TRY(ensure_ws(c, bp.ws_bytes, st));
+  PDS_TRY(ensure_rope(c, seq_len, st));
+  std::unique_ptr<pds_saved> sv(new pds_saved());
+  sv->strategy = strategy;
+  sv->s = seq_len;
+  sv->x = x;
+  sv->plan = bp;
+  sv->bytes = bp.saved_bytes;
+  PDS_TRY(alloc_saved(c, bp.saved_bytes, &sv->mem));
+  Exec e(c, st, seq_len);
+  pds_status rc;
+  switch (strategy) {
+    case PDS_MEGATRON_TS: rc = ts_fwd(e, x, w, y, sv.get(), c->ws); break;
+    case PDS_ULYSSES_Z: rc = uz_fwd(e, x, w, y, sv.get(), c->ws); break;
+    default: rc = metp_fwd(e, x, w, y, sv.get(), c->ws); break;
+  }
+  c->tap_o = c->tap_z = nullptr;
+  if (rc != PDS_OK || !saved) {
+    c->free_blocks.emplace(sv->bytes, sv->mem);
+    return rc;
+  }
+  c->saved_live += sv->bytes;
+  *saved = sv.release();
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy, pds_saved* saved,
+                                    const pds_weights* w, const pds_grads* g, void* dx, void* stream) {
+  PDS_TRY(check_layer(c, strategy, saved ? saved->s : 0));
+  if (!dy || !saved || !w || !g || !dx) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  if (!g->dw_qkv_t || !g->dw_proj || !g->dw_in_t || !g->dw_out || !g->dg1 || !g->dg2)
+    PDS_FAIL(PDS_EINVAL, "NULL gradient pointer");
+  if (saved->strategy != strategy)
+    PDS_FAIL(PDS_ESTATE, "bwd strategy " + std::to_string(strategy) + " != fwd strategy " +
+                             std::to_string(saved->strategy));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PDS_CUDA(cudaSetDevice(c->device));
+  PDS_TRY(ensure_ws(c, saved->plan.ws_bytes, st));
+  Exec e(c, st, saved->s);
+  pds_status rc;
+  switch (strategy) {
+    case PDS_MEGATRON_TS: rc = ts_bwd(e, dy, saved, w, g, dx, c->ws); break;
+    case PDS_ULYSSES_Z: rc = uz_bwd(e, dy, saved, w, g, dx, c->ws); break;
+    default: rc = metp_bwd(e, dy, saved, w, g, dx, c->ws); break;
+  }
+  c->saved_live -= saved->bytes;
+  c->free_blocks.emplace(saved->bytes, saved->mem);
+  delete saved;
+  return rc;
+}
+
+extern "C" pds_status pds_saved_release(pds_ctx* c, pds_saved* saved) {
+  if (!c || !saved) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  c->saved_live -= saved->bytes;
+  c->free_blocks.emplace(saved->bytes, saved->mem);
+  delete saved;
+  return PDS_OK;
+}
+
+// ------------------------------------------------------------------ planner with ctx
+extern "C" pds_status pds_load_costs(pds_ctx* c, const char* path) {
+  if (!c || !path) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  Bundle b;
+  PDS_TRY(load_bundle(path, &b));
+  if (b.P != c->P || b.h != c->m.h || b.n != c->m.n_heads || b.ffn != c->m.ffn)
+    PDS_FAIL(PDS_EINVAL, "bundle (P, h, n, ffn) does not match the context");
+  c->bundle = b;
+  c->cache.clear();
+  c->prev.clear();
+  c->capacity = b.capacity > 0 ? b.capacity - b.reserve : c->capacity;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_set_capacity(pds_ctx* c, double capacity, double gamma) {
+  if (!c || capacity <= 0 || gamma < 0 || gamma >= 1) PDS_FAIL(PDS_EINVAL, "bad capacity / gamma");
+  c->capacity = capacity;
+  c->gamma = gamma;
+  c->cache.clear();
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_set_enabled(pds_ctx* c, uint32_t mask) {
+  if (!c || !(mask & 0x7)) PDS_FAIL(PDS_EINVAL, "empty strategy mask");
+  c->enabled = mask & 0x7;
+  c->cache.clear();
+  c->prev.clear();
+  return PDS_OK;
+}
+
+// T_pi(s) from the bundle (Eq. 9) and M_pi(s) = persistent + saved bytes of one
+// layer (exact plan); *headroom = max workspace over the enabled strategies
+// (reading R-22: Eq. 6 keeps its additive per-layer form, transients are one
+// plan-independent term subtracted from the capacity).
+static pds_status costs(pds_ctx* c, int64_t s, double* t, double* mm, int* branch, double* headroom) {
+  if (!c->bundle.loaded) PDS_FAIL(PDS_ENOCOSTS, "no cost bundle loaded (pds_load_costs)");
+  double trans = 0;
+  for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
+    t[i] = c->bundle.strat[i].present ? bundle_time(c->bundle, i, s, branch ? &branch[i] : nullptr) : 1e300;
+    int64_t saved = 0, tr = 0, pers = 0;
+    pds_status rc = pds_mem_bytes(&c->m, c->P, (uint8_t)i, s, &saved, &tr, &pers);
+    if (rc != PDS_OK) {
+      mm[i] = 1e300;
+      continue;
+    }
+    mm[i] = (double)(saved + pers);
+    if ((c->enabled >> i & 1) && c->bundle.strat[i].present) trans = std::max(trans, (double)tr);
+  }
+  if (headroom) *headroom = trans;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_cost_eval(pds_ctx* c, int64_t s, double* t_layer, double* m_layer, int32_t* branch) {
+  if (!c || !t_layer || !m_layer) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  double t[PDS_N_STRATEGIES], mm[PDS_N_STRATEGIES];
+  int br[PDS_N_STRATEGIES] = {0, 0, 0};
+  PDS_TRY(costs(c, s, t, mm, br, nullptr));
+  for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
+    t_layer[i] = t[i];
+    m_layer[i] = mm[i];
+    if (branch) branch[i] = br[i];
+  }
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_plan(pds_ctx* c, int64_t s, uint8_t* out, int32_t L, uint32_t* flags_out) {
+  if (!c || !out) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  if (L <= 0) PDS_FAIL(PDS_EINVAL, "L must be >= 1");
+  uint32_t flags = 0;
+  std::vector<uint8_t> plan;
+  double t[PDS_N_STRATEGIES], mm[PDS_N_STRATEGIES], head = 0;
+  const auto key = std::make_pair(c->m.batch, s);
+  auto it = c->cache.find(key);
+  bool need_costs = true;
+  if (it != c->cache.end() && (int)it->second.first.size() == L) {
+    plan = it->second.first;
+    flags |= PDS_PLAN_CACHED | (it->second.second ? PDS_PLAN_INFEASIBLE : 0u);
+  } else {
+    PDS_TRY(costs(c, s, t, mm, nullptr, &head));
+    need_costs = false;
+    uint8_t en[PDS_N_STRATEGIES];
+    for (int i = 0; i < PDS_N_STRATEGIES; ++i) en[i] = (c->enabled >> i & 1) && c->bundle.strat[i].present && mm[i] < 1e299;
+    const double cap = c->capacity - head;
+    bool inf = false, early = false;
+    bool any = false;
+    for (int i = 0; i < PDS_N_STRATEGIES; ++i) any |= en[i] != 0;
+    if (!any) PDS_FAIL(PDS_ESTRATEGY, "no enabled strategy is valid at this seq_len");
+    alg1(L, PDS_N_STRATEGIES, t, mm, en, cap, plan, &inf, &early, nullptr);
+    flags |= (inf ? PDS_PLAN_INFEASIBLE : 0u) | (early ? PDS_PLAN_EARLY : 0u);
+    c->cache[key] = std::make_pair(plan, inf);
+  }
+  if (c->gamma > 0 && (int)c->prev.size() == L && c->prev != plan) {
+    if (need_costs) PDS_TRY(costs(c, s, t, mm, nullptr, &head));
+    bool valid = true;
+    for (uint8_t p : c->prev) valid &= (c->enabled >> p & 1) && mm[p] < 1e299;
+    const double cap = c->capacity - head;
+    if (valid && plan_feasible(c->prev.data(), L, mm, cap, nullptr) &&
+        plan_time(c->prev.data(), L, t) <= (1.0 + c->gamma) * plan_time(plan.data(), L, t)) {
+      plan = c->prev;
+      flags |= PDS_PLAN_SMOOTHED;
+      flags &= ~PDS_PLAN_INFEASIBLE;
+    }
+  }
+  c->prev = plan;
+  std::memcpy(out, plan.data(), (size_t)L);
+  if (flags_out) *flags_out = flags;
+  return PDS_OK;
+}
+
+// ------------------------------------------------------------------ profiling
+extern "C" pds_status pds_profile_enable(pds_ctx* c, int32_t on) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  c->prof = on != 0;
+  return PDS_OK;
+}
+
+static void drain(pds_ctx* c) {
+  for (auto& r : c->pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    c->acc_ms[r.klass] += ms;
+    c->acc_n[r.klass] += 1;
+    c->acc_flops[r.klass] += r.flops;
+    c->acc_bytes[r.klass] += r.bytes;
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->pending.clear();
+}
+
+extern "C" pds_status pds_profile_read(pds_ctx* c, int32_t k, double* ms, int64_t* n, double* flops, double* bytes) {
+  if (!c || k < 0 || k > 4) PDS_FAIL(PDS_EINVAL, "bad profile class");
+  drain(c);
+  if (ms) *ms = c->acc_ms[k];
+  if (n) *n = c->acc_n[k];
+  if (flops) *flops = c->acc_flops[k];
+  if (bytes) *bytes = c->acc_bytes[k];
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_profile_reset(pds_ctx* c) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  drain(c);
+  for (int k = 0; k < 5; ++k) c->acc_ms[k] = c->acc_flops[k] = c->acc_bytes[k] = 0, c->acc_n[k] = 0;
+  return PDS_OK;
+}

@@ -1,0 +1,371 @@
+// Host planner: Algorithm 1, the hybrid cost model of Eq. 9
+// evaluated from an exported random forest + AIC polynomial,
+// and the exact memory plan behind Eq. 6.
+//
+// Readings: R-17 inner-loop reset, R-18 early return of [P0] x L,
+// R-19 gamma-smoothing against the previous plan, R-20 Pareto prune + sort by
+// (t, m, id), R-23 strict "<", R-24 ties: first candidate in generation order.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+
+#include "internal.hpp"
+
+namespace pds {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+// ------------------------------------------------------------------ Algorithm 1
+bool plan_feasible(const uint8_t* plan, int L, const double* m, double cap, Alg1Counters* c) {
+  double acc = 0.0;
+  for (int l = 0; l < L; ++l) {
+    acc += m[plan[l]];
+    if (c) c->layer_checks++;
+    if (acc >= cap) return false;  // OOM short-circuit
+  }
+  return acc < cap;
+}
+
+double plan_time(const uint8_t* plan, int L, const double* t) {
+  double acc = 0.0;
+  for (int l = 0; l < L; ++l) acc += t[plan[l]];
+  return acc;
+}
+
+// pop_useless (line 1): Pareto prune, sort ascending by (t, m, id)
+static std::vector<int> prune_sort(int n, const double* t, const double* m, const uint8_t* en) {
+  std::vector<int> keep;
+  for (int a = 0; a < n; ++a) {
+    if (!en[a]) continue;
+    bool dominated = false;
+    for (int b = 0; b < n && !dominated; ++b) {
+      if (b == a || !en[b]) continue;
+      if (t[b] <= t[a] && m[b] <= m[a] && (t[b] < t[a] || m[b] < m[a])) dominated = true;
+    }
+    if (!dominated) keep.push_back(a);
+  }
+  std::sort(keep.begin(), keep.end(), [&](int a, int b) {
+    if (t[a] != t[b]) return t[a] < t[b];
+    if (m[a] != m[b]) return m[a] < m[b];
+    return a < b;
+  });
+  return keep;
+}
+
+void alg1(int L, int n, const double* t, const double* m, const uint8_t* enabled, double cap,
+          std::vector<uint8_t>& out, bool* infeasible, bool* early, Alg1Counters* c) {
+  std::vector<int> P = prune_sort(n, t, m, enabled);
+  *infeasible = false;
+  *early = false;
+  out.assign(L, 0);
+  std::vector<uint8_t> s(L), best;
+  double best_t = 0.0;
+  bool have = false;
+  for (size_t i = 0; i < P.size(); ++i) {
+    std::fill(s.begin(), s.end(), (uint8_t)P[i]);          // line 7
+    if (c) c->plans++;
+    const bool ok = plan_feasible(s.data(), L, m, cap, c);
+    if (i == 0 && ok) {                                     // lines 8-10 (R-18)
+      out = s;
+      *early = true;
+      return;
+    }
+    if (ok) {                                               // line 12
+      const double tp = plan_time(s.data(), L, t);
+      if (!have || tp < best_t) { best = s; best_t = tp; have = true; }
+    } else {
+      for (size_t k = i + 1; k < P.size(); ++k) {           // lines 14-20
+        std::fill(s.begin(), s.end(), (uint8_t)P[i]);       // R-17 reset
+        for (int l = 0; l < L; ++l) {
+          // pop the first element, append P[k] (a left shift of the window)
+          std::memmove(s.data(), s.data() + 1, (size_t)(L - 1));
+          s[L - 1] = (uint8_t)P[k];
+          if (c) c->plans++;
+          if (plan_feasible(s.data(), L, m, cap, c)) {
+            const double tp = plan_time(s.data(), L, t);
+            if (!have || tp < best_t) { best = s; best_t = tp; have = true; }
+          }
+        }
+      }
+    }
+  }
+  if (have) {                                               // line 25
+    out = best;
+  } else {                                                  // line 27
+    int least = P[0];
+    for (int a : P)
+      if (m[a] < m[least] || (m[a] == m[least] && a < least)) least = a;
+    std::fill(out.begin(), out.end(), (uint8_t)least);
+    *infeasible = true;
+  }
+}
+
+// ------------------------------------------------------------------ cost bundle (Eq. 9)
+pds_status load_bundle(const char* path, Bundle* b) {
+  std::ifstream f(path);
+  if (!f) PDS_FAIL(PDS_EINVAL, std::string("pds_load_costs: cannot open ") + path);
+  std::string tok;
+  auto expect = [&](const char* w) -> bool {
+    if (!(f >> tok) || tok != w) {
+      set_error(std::string("pds_load_costs: expected '") + w + "', got '" + tok + "'");
+      return false;
+    }
+    return true;
+  };
+  Bundle nb;
+  int ver = 0;
+  if (!expect("pds_bundle") || !(f >> ver) || ver != 1) PDS_FAIL(PDS_EINVAL, "pds_load_costs: bad header");
+  if (!expect("P") || !(f >> nb.P) || !expect("h") || !(f >> nb.h) || !expect("n") || !(f >> nb.n) ||
+      !expect("ffn") || !(f >> nb.ffn) || !expect("L") || !(f >> nb.L) || !expect("capacity") ||
+      !(f >> nb.capacity) || !expect("reserve") || !(f >> nb.reserve))
+    return PDS_EINVAL;
+  if (!expect("norm")) return PDS_EINVAL;
+  for (int i = 0; i < 4; ++i) f >> nb.norm[i][0] >> nb.norm[i][1];
+  int ns = 0;
+  if (!expect("n_strat") || !(f >> ns)) return PDS_EINVAL;
+  for (int i = 0; i < ns; ++i) {
+    int sid = -1;
+    if (!expect("strategy") || !(f >> sid) || sid < 0 || sid >= PDS_N_STRATEGIES)
+      PDS_FAIL(PDS_EINVAL, "pds_load_costs: bad strategy id");
+    StratCost& sc = nb.strat[sid];
+    sc.present = true;
+    if (!expect("s_profile_max") || !(f >> sc.s_profile_max)) return PDS_EINVAL;
+    if (!expect("poly") || !(f >> sc.poly_deg >> sc.poly_scale)) return PDS_EINVAL;
+    sc.poly_coef.resize(sc.poly_deg + 1);
+    for (auto& v : sc.poly_coef) f >> v;
+    int nt = 0;
+    if (!expect("trees") || !(f >> nt)) return PDS_EINVAL;
+    sc.trees.resize(nt);
+    for (auto& tr : sc.trees) {
+      int nn = 0;
+      if (!expect("tree") || !(f >> nn)) return PDS_EINVAL;
+      tr.feature.resize(nn); tr.left.resize(nn); tr.right.resize(nn);
+      tr.threshold.resize(nn); tr.value.resize(nn);
+      for (int k = 0; k < nn; ++k)
+        f >> tr.feature[k] >> tr.threshold[k] >> tr.left[k] >> tr.right[k] >> tr.value[k];
+    }
+  }
+  if (!expect("end")) return PDS_EINVAL;
+  if (f.fail()) PDS_FAIL(PDS_EINVAL, "pds_load_costs: parse error");
+  nb.loaded = true;
+  *b = nb;
+  return PDS_OK;
+}
+
+// feature vector: one-hot over the strategies present (reading R-25) + normalised h, n, L, s
+static double feat(const Bundle& b, int strategy, int64_t s, int idx) {
+  int nen = 0, pos = -1;
+  for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
+    if (!b.strat[i].present) continue;
+    if (i == strategy) pos = nen;
+    ++nen;
+  }
+  if (idx < nen) return idx == pos ? 1.0 : 0.0;
+  const double raw[4] = {(double)b.h, (double)b.n, (double)b.L, (double)s};
+  const int j = idx - nen;
+  const double lo = b.norm[j][0], hi = b.norm[j][1];
+  return hi == lo ? 0.0 : (raw[j] - lo) / (hi - lo);
+}
+
+double bundle_time(const Bundle& b, int strategy, int64_t s, int* branch) {
+  const StratCost& sc = b.strat[strategy];
+  if ((double)s <= sc.s_profile_max) {       // RF: interpolation
+    if (branch) *branch = 0;
+    double acc = 0.0;
+    for (const Tree& tr : sc.trees) {
+      int node = 0;
+      while (tr.left[node] >= 0) {
+        node = feat(b, strategy, s, tr.feature[node]) <= tr.threshold[node] ? tr.left[node] : tr.right[node];
+      }
+      acc += tr.value[node];
+    }
+    return acc / (double)sc.trees.size();
+  }
+  if (branch) *branch = 1;                    // PR: extrapolation
+  const double x = (double)s / sc.poly_scale;
+  double acc = 0.0;
+  for (double c : sc.poly_coef) acc = acc * x + c;
+  return acc;
+}
+
+// ------------------------------------------------------------------ memory plan
+int64_t BufPlan::off(const std::vector<Region>& v, const char* n) const {
+  for (const auto& r : v)
+    if (std::strcmp(r.name, n) == 0) return r.off;
+  return -1;
+}
+
+static void push(std::vector<Region>& v, int64_t& tot, const char* n, int64_t bytes) {
+  v.push_back(Region{n, bytes, tot});
+  tot += al(bytes);
+}
+
+int64_t persistent_bytes(const pds_model& m, int P) {
+  const int64_t h = m.h, F = m.ffn;
+  return (4 * h * h + 2 * h * F) / P * (2 + 4) + 2 * h * (2 + 4);
+}
+
+pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan* out) {
+  if (P < 1) PDS_FAIL(PDS_EINVAL, "P must be >= 1");
+  if (m.h <= 0 || m.n_heads <= 0 || m.ffn <= 0) PDS_FAIL(PDS_EINVAL, "model dims must be positive");
+  if (m.batch != 1) PDS_FAIL(PDS_ENOTIMPL, "batch != 1 is not supported in this build");
+  if (m.h % m.n_heads) PDS_FAIL(PDS_EDIVISIBILITY, "h not divisible by n_heads");
+  const int64_t d = m.h / m.n_heads;
+  if (d != 64 && d != 128) PDS_FAIL(PDS_ENOTIMPL, "head dim must be 64 or 128");
+  if (m.h % 256) PDS_FAIL(PDS_ENOTIMPL, "h must be a multiple of 256");
+  if (s <= 0 || s % P) PDS_FAIL(PDS_EDIVISIBILITY, "seq_len=" + std::to_string(s) + " not divisible by P=" + std::to_string(P));
+  if (m.n_heads % P) PDS_FAIL(PDS_EDIVISIBILITY, "n_heads=" + std::to_string(m.n_heads) + " not divisible by P=" + std::to_string(P));
+  if (m.ffn % P || (m.ffn / P) % 64) PDS_FAIL(PDS_EDIVISIBILITY, "ffn/P must be a multiple of 64");
+  const int64_t sl = s / P;
+  if (sl % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/P=" + std::to_string(sl) + " must be a multiple of 128 (caller pads, R-15)");
+  const int64_t h = m.h, F = m.ffn, nl = m.n_heads / P, hl = h / P, Fl = F / P;
+  const int64_t u = sl * h * 2, lam = nl * s * 4, ell = sl * 4;
+  BufPlan p;
+  int64_t ts = 0, tw = 0;
+  const int64_t dgp = (int64_t)rmsnorm_bwd_grid(sl) * h * 4;
+  switch (strategy) {
+    case PDS_MEGATRON_TS:
+      push(p.saved, ts, "rstd1", ell);
+      push(p.saved, ts, "qkv", s * 3 * hl * 2);
+      push(p.saved, ts, "a", s * hl * 2);
+      push(p.saved, ts, "lse", lam);
+      push(p.saved, ts, "x1", u);
+      push(p.saved, ts, "rstd2", ell);
+      push(p.saved, ts, "h", s * Fl * 2);
+      push(p.ws, tw, "gather", s * h * 2);
+      push(p.ws, tw, "partial", s * h * 2);
+      push(p.ws, tw, "f0", s * Fl * 2);
+      push(p.ws, tw, "f1", s * Fl * 2);
+      push(p.ws, tw, "dd", lam);
+      push(p.ws, tw, "dgp", dgp);
+      push(p.ws, tw, "dgl", 2 * h * 4);
+      break;
+    case PDS_ULYSSES_Z: {
+      push(p.saved, ts, "rstd1", ell);
+      push(p.saved, ts, "qkv", s * 3 * hl * 2);
+      push(p.saved, ts, "a", s * hl * 2);
+      push(p.saved, ts, "lse", lam);
+      push(p.saved, ts, "afull", u);
+      push(p.saved, ts, "x1", u);
+      push(p.saved, ts, "rstd2", ell);
+      push(p.saved, ts, "h", sl * F * 2);
+      push(p.ws, tw, "wqkv", 3 * h * h * 2);
+      push(p.ws, tw, "wproj", h * h * 2);
+      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "wout", F * h * 2);
+      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "u1", u);
+      push(p.ws, tw, "s1", 3 * u);
+      push(p.ws, tw, "r1", 3 * u);
+      push(p.ws, tw, "f0", sl * F * 2);
+      push(p.ws, tw, "f1", sl * F * 2);
+      push(p.ws, tw, "x3", 3 * u);
+      push(p.ws, tw, "x4", 3 * u);
+      push(p.ws, tw, "v2", u);
+      push(p.ws, tw, "dd", lam);
+      push(p.ws, tw, "dgp", dgp);
+      push(p.ws, tw, "dgl", 2 * h * 4);
+      break;
+    }
+    case PDS_METP: {
+      const int64_t c = m.metp_chunks > 0 ? m.metp_chunks : P;
+      if (sl % c) PDS_FAIL(PDS_EDIVISIBILITY, "s/P not divisible by metp_chunks");
+      const int64_t w = sl / c;
+      if (w % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/(P*metp_chunks)=" + std::to_string(w) + " must be a multiple of 128");
+      if (m.metp_recompute != 0) PDS_FAIL(PDS_ENOTIMPL, "metp_recompute=full is not implemented");
+      const int64_t uw = w * h * 2;
+      push(p.saved, ts, "rstd1", ell);
+      push(p.saved, ts, "qkv", s * 3 * hl * 2);
+      push(p.saved, ts, "a", s * hl * 2);
+      push(p.saved, ts, "lse", lam);
+      push(p.saved, ts, "x1", u);
+      push(p.saved, ts, "rstd2", ell);
+      push(p.ws, tw, "ul", u);
+      push(p.ws, tw, "vl", u);
+      push(p.ws, tw, "wg", P * uw);
+      push(p.ws, tw, "wg2", P * uw);
+      push(p.ws, tw, "pw", P * uw);
+      push(p.ws, tw, "hw", P * w * Fl * 2);
+      push(p.ws, tw, "gw", P * w * Fl * 2);
+      push(p.ws, tw, "dhw", P * w * Fl * 2);
+      push(p.ws, tw, "da", s * hl * 2);
+      push(p.ws, tw, "dqkv", s * 3 * hl * 2);
+      push(p.ws, tw, "dd", lam);
+      push(p.ws, tw, "dgp", (int64_t)rmsnorm_bwd_grid(w) * h * 4);
+      push(p.ws, tw, "dgl", 2 * h * 4);
+      break;
+    }
+    default:
+      PDS_FAIL(PDS_ESTRATEGY, "unknown strategy id " + std::to_string(strategy));
+  }
+  p.saved_bytes = ts;
+  p.ws_bytes = tw;
+  *out = p;
+  return PDS_OK;
+}
+
+}  // namespace pds
+
+// ------------------------------------------------------------------ C ABI (host only)
+using namespace pds;
+
+extern "C" const char* pds_last_error(void) { return g_err.c_str(); }
+extern "C" const char* pds_version(void) { return "paradyse-b200 0.1 (sm_100a)"; }
+
+extern "C" pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_layer,
+                                  const double* m_layer, const uint8_t* enabled, double capacity,
+                                  double gamma, const uint8_t* prev_plan, uint8_t* strategy_out,
+                                  uint32_t* flags_out, int64_t* counters_out) {
+  if (L <= 0) PDS_FAIL(PDS_EINVAL, "L must be >= 1 (SPEC.md:394)");
+  if (n_strat <= 0 || n_strat > 255) PDS_FAIL(PDS_EINVAL, "n_strat out of range");
+  if (!t_layer || !m_layer || !enabled || !strategy_out) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  bool any = false;
+  for (int i = 0; i < n_strat; ++i) any |= enabled[i] != 0;
+  if (!any) PDS_FAIL(PDS_ESTRATEGY, "no enabled strategy");
+  Alg1Counters c;
+  std::vector<uint8_t> out;
+  bool inf = false, early = false;
+  alg1(L, n_strat, t_layer, m_layer, enabled, capacity, out, &inf, &early, &c);
+  uint32_t flags = (inf ? PDS_PLAN_INFEASIBLE : 0u) | (early ? PDS_PLAN_EARLY : 0u);
+  if (prev_plan) {
+    bool valid = true, same = true;
+    for (int l = 0; l < L; ++l) {
+      if (prev_plan[l] >= n_strat || !enabled[prev_plan[l]]) valid = false;
+      else if (prev_plan[l] != out[l]) same = false;
+    }
+    if (valid && !same && plan_feasible(prev_plan, L, m_layer, capacity, nullptr) &&
+        plan_time(prev_plan, L, t_layer) <= (1.0 + gamma) * plan_time(out.data(), L, t_layer)) {
+      std::memcpy(out.data(), prev_plan, (size_t)L);
+      flags |= PDS_PLAN_SMOOTHED;
+      flags &= ~PDS_PLAN_INFEASIBLE;
+    }
+  }
+  std::memcpy(strategy_out, out.data(), (size_t)L);
+  if (flags_out) *flags_out = flags;
+  if (counters_out) {
+    counters_out[0] = c.layer_checks;
+    counters_out[1] = c.plans;
+    counters_out[2] = c.cache_hits;
+  }
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_mem_bytes(const pds_model* model, int32_t P, uint8_t strategy,
+                                    int64_t seq_len, int64_t* saved_per_layer,
+                                    int64_t* transient_peak, int64_t* persistent_per_layer) {
+  if (!model) PDS_FAIL(PDS_EINVAL, "NULL model");
+  BufPlan p;
+  PDS_TRY(make_plan(*model, P, strategy, seq_len, &p));
+  // saved per layer = ctx-owned saved arena + the retained layer input x (caller-owned)
+  const int64_t x_bytes = seq_len / P * model->batch * model->h * 2;
+  if (saved_per_layer) *saved_per_layer = p.saved_bytes + x_bytes;
+  if (transient_peak) *transient_peak = p.ws_bytes;
+  if (persistent_per_layer) *persistent_per_layer = persistent_bytes(*model, P);
+  return PDS_OK;
+}

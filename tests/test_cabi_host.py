@@ -1,0 +1,101 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/paradyse.h
+declares, and its host-only logic (Algorithm 1, memory plan, cost bundle) agrees
+bit-exactly with the oracle.  No GPU compute is called."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import memory as OM
+from oracle import selector as OA
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2511_13198_b200 import binding
+    binding.lib()
+    return binding
+
+
+def test_exports_every_declared_symbol(B):
+    hdr = open(os.path.join(ROOT, "include", "paradyse.h")).read()
+    names = set(re.findall(r"^\s*(?:pds_status|const char\*)\s+(pds_\w+)\s*\(", hdr, re.M))
+    assert len(names) >= 30
+    L = ctypes.CDLL(B.LIB_PATH)
+    for n in sorted(names):
+        assert hasattr(L, n), n
+    assert B.lib().pds_version().decode().startswith("paradyse-b200")
+
+
+def test_plan_ex_bit_exact_vs_oracle(B):
+    rng = np.random.default_rng(0)
+    n_inf = n_early = 0
+    for trial in range(4000):
+        k = int(rng.integers(1, 6))
+        L = int(rng.choice([1, 2, 3, 5, 8, 32]))
+        t = [float(v) for v in rng.random(k)]
+        m = [float(v) for v in rng.random(k)]
+        if trial % 7 == 0:                       # exact ties
+            t[-1] = t[0]
+        en = [bool(e) for e in (rng.random(k) < 0.85)]
+        if not any(en):
+            en[0] = True
+        cap = float(rng.random() * L * 0.9 + 1e-3)
+        enabled = [i for i in range(k) if en[i]]
+        plan, flags, ctr = B.plan_ex(L, t, m, en, cap, counters=True)
+        ctr_o = OA.Counters()
+        ref, inf = OA.alg1(L, dict(enumerate(t)), dict(enumerate(m)), enabled, cap, ctr=ctr_o)
+        assert plan == ref, (trial, k, L, t, m, en, cap)
+        assert bool(flags & B.PLAN_INFEASIBLE) == inf
+        assert ctr[0] == ctr_o.layer_checks and ctr[1] == ctr_o.plans
+        n_inf += inf
+        n_early += bool(flags & B.PLAN_EARLY)
+        # smoothing against a random previous plan
+        prev = [int(rng.choice(enabled)) for _ in range(L)]
+        g = float(rng.choice([0.0, 0.05, 0.3]))
+        p2, f2 = B.plan_ex(L, t, m, en, cap, gamma=g, prev=prev)
+        r2, kept = OA.smooth(ref, prev, dict(enumerate(t)), dict(enumerate(m)), cap, g, enabled)
+        assert p2 == r2 and bool(f2 & B.PLAN_SMOOTHED) == kept
+    assert n_inf > 50 and n_early > 50
+
+
+def test_plan_ex_worked_examples(B):
+    assert B.plan_ex(3, [1.0, 2.0], [10.0, 4.0], [1, 1], 25.0)[0] == [0, 0, 1]
+    assert B.plan_ex(2, [0.0, 2.9, 3.0], [10.0, 6.0, 0.0], [1, 1, 1], 11.0)[0] == [0, 2]   # R-17
+    plan, fl = B.plan_ex(3, [1.0, 2.0], [10.0, 5.0], [1, 1], 1.0)
+    assert plan == [1, 1, 1] and fl & B.PLAN_INFEASIBLE
+    with pytest.raises(B.PdsError) as e:
+        B.plan_ex(0, [1.0], [1.0], [1], 1.0)
+    assert e.value.code == -1
+
+
+@pytest.mark.parametrize("cfg", [(256, 4, 1024, 512, 2), (4096, 32, 16384, 32768, 8), (4096, 32, 16384, 4096, 1),
+                                 (4096, 32, 16384, 638976, 8), (1024, 8, 4096, 1024, 4)])
+def test_mem_bytes_vs_oracle(B, cfg):
+    h, n, F, s, P = cfg
+    m = B.Model(h=h, n_heads=n, ffn=F)
+    for pi in (0, 1, 2):
+        c = P
+        if pi == 2 and (s // P) % c == 0 and (s // P // c) % 128:
+            continue
+        saved, tr, pers = B.mem_bytes(m, P, pi, s)
+        assert saved == OM.saved(pi, h, n, F, s, P), (pi, cfg)
+        assert pers == OM.persistent(h, F, P)
+        assert tr == OM.transient(pi, h, n, F, s, P), (pi, cfg)
+
+
+def test_mem_bytes_errors(B):
+    m = B.Model(h=256, n_heads=4, ffn=1024)
+    with pytest.raises(B.PdsError) as e:
+        B.mem_bytes(m, 2, 0, 500)                    # P does not divide s (hard error, R-15)
+    assert e.value.code == -2
+    with pytest.raises(B.PdsError) as e:
+        B.mem_bytes(m, 2, 9, 512)
+    assert e.value.code == -3
+    with pytest.raises(B.PdsError) as e:
+        B.mem_bytes(B.Model(h=256, n_heads=4, ffn=1024, batch=2), 2, 0, 512)
+    assert e.value.code == -9

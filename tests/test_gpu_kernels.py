@@ -1,0 +1,186 @@
+"""Per-kernel parity on B200 against the oracle (fp32-accumulate path, reading R-14).
+
+Each kernel is fed bf16 inputs; the oracle computes the same stage in fp64 from
+those exact inputs.  Tolerances (relative L2, written per check): fp32 outputs
+2e-3 (north_star "fp32-accumulate path"), bf16 outputs 1e-2.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layer as OL
+from synth import normal, round_bf16
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2511_13198_b200 import binding as B
+    from tests.gpu_util import dev_bf16, dev_f32, host, rel, stream
+
+
+def _mat(seed, tid, shape, std=1.0):
+    return normal(seed, tid, shape, std=std)
+
+
+GEMM_SHAPES = [(256, 384, 256), (200, 392, 200), (128, 128, 64), (1024, 768, 512), (4096, 4096, 512),
+               (344, 1536, 4096)]
+
+
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+@pytest.mark.parametrize("shape", GEMM_SHAPES)
+def test_gemm_f32(a_mn, b_mn, shape):
+    M, N, K = shape
+    A = _mat(1, 1, (M, K), std=1 / math.sqrt(K))
+    Bm = _mat(1, 2, (N, K))
+    ref = A @ Bm.T
+    a_st = A.T.copy() if a_mn else A
+    b_st = Bm.T.copy() if b_mn else Bm
+    ta, tb = dev_bf16(a_st), dev_bf16(b_st)
+    out = torch.zeros(M, N, dtype=torch.float32, device="cuda")
+    B.k_gemm(ta.data_ptr(), a_st.shape[1], a_mn, tb.data_ptr(), b_st.shape[1], b_mn, M, N, K,
+             out.data_ptr(), N, 2, stream=stream())
+    torch.cuda.synchronize()
+    assert rel(host(out), ref) < 2e-3
+    # fp32 accumulate epilogue: C += A B^T
+    B.k_gemm(ta.data_ptr(), a_st.shape[1], a_mn, tb.data_ptr(), b_st.shape[1], b_mn, M, N, K,
+             out.data_ptr(), N, 1, stream=stream())
+    torch.cuda.synchronize()
+    assert rel(host(out), 2 * ref) < 2e-3
+
+
+def test_gemm_bf16_and_gelu_epilogues():
+    M, N, K = 384, 512, 256
+    A = _mat(2, 1, (M, K), std=1 / math.sqrt(K))
+    W = _mat(2, 2, (N, K))
+    ref = A @ W.T
+    ta, tw = dev_bf16(A), dev_bf16(W)
+    c = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    g = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm(ta.data_ptr(), K, 0, tw.data_ptr(), K, 0, M, N, K, c.data_ptr(), N, 0, stream=stream())
+    torch.cuda.synchronize()
+    assert rel(host(c), ref) < 1e-2
+    B.k_gemm(ta.data_ptr(), K, 0, tw.data_ptr(), K, 0, M, N, K, c.data_ptr(), N, 3, None, g.data_ptr(), N,
+             stream=stream())
+    torch.cuda.synchronize()
+    hb = host(c)
+    assert rel(hb, ref) < 1e-2
+    assert rel(host(g), OL.gelu(hb)) < 1e-2           # G = GELU(bf16(H))
+    # dGELU: C = acc * GELU'(H), aux_out = GELU(H)
+    dg = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    g2 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm(ta.data_ptr(), K, 0, tw.data_ptr(), K, 0, M, N, K, dg.data_ptr(), N, 4, c.data_ptr(),
+             g2.data_ptr(), N, stream=stream())
+    torch.cuda.synchronize()
+    assert rel(host(dg), ref * OL.gelu_grad(hb)) < 1e-2
+    assert rel(host(g2), OL.gelu(hb)) < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_rope_table_and_gemm_rope(d):
+    n_pos = 2048
+    t = torch.empty(n_pos, d // 2, 2, dtype=torch.float32, device="cuda")
+    B.k_rope_table(t.data_ptr(), n_pos, d, 10000.0, stream())
+    torch.cuda.synchronize()
+    cos, sin = OL.rope_cos_sin(np.arange(n_pos), d)
+    tt = t.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(tt[..., 0] - cos)) < 1e-7 and np.max(np.abs(tt[..., 1] - sin)) < 1e-7
+    # large positions: fp64 angle formation keeps the table exact (R-3)
+    big = 638976
+    tb = torch.empty(big, d // 2, 2, dtype=torch.float32, device="cuda")
+    B.k_rope_table(tb.data_ptr(), big, d, 10000.0, stream())
+    torch.cuda.synchronize()
+    c2, s2 = OL.rope_cos_sin(np.arange(big - 4, big), d)
+    last = tb[-4:].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(last[..., 0] - c2)) < 1e-7 and np.max(np.abs(last[..., 1] - s2)) < 1e-7
+    # QKV GEMM with fused RoPE; two head groups (Ulysses packing order), rows offset
+    heads = 2
+    hq = heads * d
+    N = 2 * 3 * hq
+    M, K = 256, 256
+    base = 1000
+    A = _mat(3, 1, (M, K), std=1 / math.sqrt(K))
+    W = _mat(3, 2, (N, K))
+    ref = A @ W.T
+    cs, sn = OL.rope_cos_sin(base + np.arange(M), d)
+    exp = ref.copy()
+    for grp in range(2):
+        for blk in range(2):   # Q and K blocks rotate, V does not
+            for hh in range(heads):
+                c0 = grp * 3 * hq + blk * hq + hh * d
+                exp[:, c0:c0 + d] = OL.rope_apply(ref[:, c0:c0 + d], cs, sn)
+    ta, tw = dev_bf16(A), dev_bf16(W)
+    c = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm_rope(ta.data_ptr(), K, tw.data_ptr(), K, M, N, K, c.data_ptr(), N, t.data_ptr(), d, hq, 0, 0,
+                  base, stream())
+    torch.cuda.synchronize()
+    assert rel(host(c), exp) < 1e-2
+
+
+@pytest.mark.parametrize("h", [256, 4096])
+def test_rmsnorm_fwd_bwd(h):
+    rows = 300
+    x = _mat(4, 1, (rows, h))
+    r = _mat(4, 2, (rows, h))
+    g = normal(4, 3, (h,), std=0.1, mean=1.0)
+    du = _mat(4, 4, (rows, h))
+    tx, tr, tg, tdu = dev_bf16(x), dev_bf16(r), dev_bf16(g), dev_bf16(du)
+    x1 = torch.empty(rows, h, dtype=torch.bfloat16, device="cuda")
+    u = torch.empty(rows, h, dtype=torch.bfloat16, device="cuda")
+    rstd = torch.empty(rows, dtype=torch.float32, device="cuda")
+    B.k_rmsnorm_fwd(tx.data_ptr(), tr.data_ptr(), tg.data_ptr(), rows, h, 1e-5, x1.data_ptr(), u.data_ptr(),
+                    rstd.data_ptr(), stream())
+    torch.cuda.synchronize()
+    x1r = round_bf16(x + r)
+    assert np.array_equal(host(x1), x1r)
+    uref, xhat, rref = OL.rmsnorm(x1r, g)
+    assert rel(host(rstd), rref) < 2e-3
+    assert rel(host(u), uref) < 1e-2
+    dx = torch.empty(rows, h, dtype=torch.bfloat16, device="cuda")
+    dg = torch.zeros(h, dtype=torch.float32, device="cuda")
+    B.k_rmsnorm_bwd(tdu.data_ptr(), x1.data_ptr(), rstd.data_ptr(), tg.data_ptr(), tr.data_ptr(), rows, h,
+                    dx.data_ptr(), dg.data_ptr(), stream())
+    torch.cuda.synchronize()
+    dxr, dgr = OL.rmsnorm_bwd(du, xhat, rref, g)
+    assert rel(host(dx), dxr + r) < 1e-2
+    assert rel(host(dg), dgr) < 2e-3
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [1, 0])
+@pytest.mark.parametrize("s", [256, 640])
+def test_attention_fwd_bwd(d, causal, s):
+    heads = 2
+    hq = heads * d
+    qkv = _mat(5 + d, 1, (s, 3 * hq))
+    dout = _mat(5 + d, 2, (s, hq))
+    tq, tdo = dev_bf16(qkv), dev_bf16(dout)
+    out = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+    B.k_attn_fwd(tq.data_ptr(), 3 * hq, s, heads, d, causal, out.data_ptr(), hq, lse.data_ptr(), stream())
+    torch.cuda.synchronize()
+    o_gpu = host(out)
+    for hh in range(heads):
+        q = qkv[:, hh * d:(hh + 1) * d]
+        k = qkv[:, hq + hh * d:hq + (hh + 1) * d]
+        v = qkv[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d]
+        a, l = OL.attention_fwd(q, k, v, causal=bool(causal))
+        assert rel(o_gpu[:, hh * d:(hh + 1) * d], a) < 1e-2
+        assert rel(host(lse)[hh], l) < 2e-3
+    dqkv = torch.empty(s, 3 * hq, dtype=torch.bfloat16, device="cuda")
+    B.k_attn_bwd(tq.data_ptr(), 3 * hq, out.data_ptr(), hq, lse.data_ptr(), tdo.data_ptr(), s, heads, d, causal,
+                 dqkv.data_ptr(), stream())
+    torch.cuda.synchronize()
+    g = host(dqkv)
+    for hh in range(heads):
+        q = qkv[:, hh * d:(hh + 1) * d]
+        k = qkv[:, hq + hh * d:hq + (hh + 1) * d]
+        v = qkv[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d]
+        _, l = OL.attention_fwd(q, k, v, causal=bool(causal))
+        dq, dk, dv = OL.attention_bwd(q, k, v, o_gpu[:, hh * d:(hh + 1) * d], l,
+                                      dout[:, hh * d:(hh + 1) * d], causal=bool(causal))
+        assert rel(g[:, hh * d:(hh + 1) * d], dq) < 1e-2
+        assert rel(g[:, hq + hh * d:hq + (hh + 1) * d], dk) < 1e-2
+        assert rel(g[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d], dv) < 1e-2

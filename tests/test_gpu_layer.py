@@ -1,0 +1,187 @@
+"""Whole-layer parity on B200: every strategy at P = 1 (real context) and P = 2, 4
+(loopback group: P virtual ranks, one host thread each, on one GPU) against the
+fp64 oracle (north_star: "every strategy ... matches the CPU oracle").
+
+bf16 path tolerance (north_star): relative L2 <= 1e-2 on Y, the sublayer deltas
+O and Z (R-34), dX, dX - dY, every weight gradient and dgamma; shard indexing is
+checked per rank against the oracle's rank-r slice.
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layer as OL
+from oracle import shard as OS
+from synth import layer_inputs
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2511_13198_b200 import binding as B
+    from tests.gpu_util import dev_bf16, host, rel
+
+TOL = 1e-2
+
+
+class Rank:
+    """Device buffers of one (virtual) rank."""
+
+    def __init__(self, W, r, x, dy):
+        self.w = {k: dev_bf16(W[k][r]) for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")}
+        self.g = {k: torch.zeros(W[src][r].shape, dtype=torch.float32, device="cuda")
+                  for k, src in (("dw_qkv_t", "w_qkv_t"), ("dw_proj", "w_proj"), ("dw_in_t", "w_in_t"),
+                                 ("dw_out", "w_out"), ("dg1", "g1"), ("dg2", "g2"))}
+        self.x = dev_bf16(x.reshape(x.shape[0], -1))
+        self.dy = dev_bf16(dy.reshape(dy.shape[0], -1))
+        self.y = torch.empty_like(self.x)
+        self.dx = torch.empty_like(self.x)
+        self.o = torch.empty_like(self.x)
+        self.z = torch.empty_like(self.x)
+
+    def weights(self):
+        return B.Weights(*(self.w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
+
+    def grads(self):
+        return B.Grads(*(self.g[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
+
+
+def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True):
+    """Run an L-layer stack (plan pi_list) on P loopback ranks; returns per-rank outputs."""
+    grp = B.Group(P)
+    errs = []
+    outs = [None] * P
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                ctx = B.Context(model, group=grp, rank=r)
+                xs = dev_bf16(x_shards[r].reshape(x_shards[r].shape[0], -1))
+                acts = [xs]
+                saves = []
+                for li, pi in enumerate(pi_list):
+                    R = ranks_per_layer[li][r]
+                    if taps:
+                        ctx.debug_taps(R.o.data_ptr(), R.z.data_ptr())
+                    y = torch.empty_like(xs)
+                    sv = ctx.layer_fwd(pi, x_shards[r].shape[0] * P, acts[-1].data_ptr(), R.weights(), y.data_ptr(),
+                                       st.cuda_stream)
+                    acts.append(y)
+                    saves.append(sv)
+                d = dev_bf16(dy_shards[r].reshape(dy_shards[r].shape[0], -1))
+                for li in reversed(range(len(pi_list))):
+                    R = ranks_per_layer[li][r]
+                    dx = torch.empty_like(d)
+                    ctx.layer_bwd(pi_list[li], d.data_ptr(), saves[li], R.weights(), R.grads(), dx.data_ptr(),
+                                  st.cuda_stream)
+                    d = dx
+                st.synchronize()
+                outs[r] = (host(acts[-1]), host(d))
+                ctx.close()
+        except Exception as e:  # surfaced in the main thread
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    grp.close()
+    if errs:
+        raise errs[0]
+    return outs
+
+
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0):
+    d = layer_inputs(h, n, F, s, 1, seed=seed)
+    y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
+    g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
+    W = OS.shard_weights(d, n, P)
+    xs = OS.shard_act(d["x"], P)
+    dys = OS.shard_act(d["dy"], P)
+    ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
+    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks)
+    outs = run_ranks(model, P, [pi], [ranks], xs, dys)
+    y = np.concatenate([o[0] for o in outs])[:, None, :]
+    dx = np.concatenate([o[1] for o in outs])[:, None, :]
+    o = np.concatenate([host(R.o) for R in ranks])[:, None, :]
+    z = np.concatenate([host(R.z) for R in ranks])[:, None, :]
+    res = dict(y=rel(y, y_ref), o=rel(o, c["o"]), z=rel(z, c["z"]), dx=rel(dx, g_ref["dx"]),
+               dxmdy=rel(dx - d["dy"], g_ref["dx"] - d["dy"]))
+    gsh = {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g}
+    dense = OS.unshard_grads(gsh, n)
+    for k in ("dw_qkv", "dw_proj", "dw_in", "dw_out", "dg1", "dg2"):
+        res[k] = rel(dense[k], g_ref[k])
+    # shard indexing: rank r's gradient shard vs the oracle's rank-r slice (O-4)
+    ref_sh = OS.shard_weights(dict(w_qkv=g_ref["dw_qkv"], w_proj=g_ref["dw_proj"], w_in=g_ref["dw_in"],
+                                   w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P)
+    for r in range(P):
+        res[f"qkv_shard{r}"] = rel(gsh["dw_qkv_t"][r], ref_sh["w_qkv_t"][r])
+        res[f"y_shard{r}"] = rel(outs[r][0], y_ref[r * (s // P):(r + 1) * (s // P), 0])
+    bad = {k: v for k, v in res.items() if not v < TOL}
+    assert not bad, (pi, P, bad, res)
+    return res
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_layer_p1_c1(pi):
+    # C1 shapes (h=256, n=4, d=64, F=1024, s=512), P = 1: every strategy degenerates
+    _check_layer(pi, 1, 256, 4, 1024, 512)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_layer_p2_c1(pi):
+    # C1 at P = 2 (the configs[0] case), METP with c = 2 waves
+    _check_layer(pi, 2, 256, 4, 1024, 512)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_layer_p4_d128(pi):
+    # d = 128 heads, P = 4, METP c = 2 waves of 128 rows per rank
+    _check_layer(pi, 4, 1024, 8, 4096, 1024, chunks=2)
+
+
+def test_switched_chain_p2():
+    # a 4-layer stack with a switched plan; boundary tensors pass unchanged (R-31)
+    P, h, n, F, s = 2, 256, 4, 1024, 512
+    plan = [2, 0, 1, 2]
+    layers = [layer_inputs(h, n, F, s, 1, seed=5, layer=i) for i in range(4)]
+    yd = layers[0]["x"]
+    caches = []
+    for L in layers:
+        yd, cc = OL.layer_fwd(yd, L["w_qkv"], L["w_proj"], L["w_in"], L["w_out"], L["g1"], L["g2"], n=n)
+        caches.append(cc)
+    dd = layers[0]["dy"]
+    for i in reversed(range(4)):
+        L = layers[i]
+        dd = OL.layer_bwd(dd, caches[i], L["w_qkv"], L["w_proj"], L["w_in"], L["w_out"], L["g1"], L["g2"],
+                          n=n)["dx"]
+    xs = OS.shard_act(layers[0]["x"], P)
+    dys = OS.shard_act(layers[0]["dy"], P)
+    rpl = []
+    for i in range(4):
+        W = OS.shard_weights(layers[i], n, P)
+        rpl.append([Rank(W, r, xs[r], dys[r]) for r in range(P)])
+    outs = run_ranks(B.Model(h=h, n_heads=n, ffn=F), P, plan, rpl, xs, dys, taps=False)
+    y = np.concatenate([o[0] for o in outs])[:, None, :]
+    dx = np.concatenate([o[1] for o in outs])[:, None, :]
+    assert rel(y, yd) < TOL
+    assert rel(dx, dd) < TOL
+    assert rel(dx - layers[0]["dy"], dd - layers[0]["dy"]) < TOL
+
+
+def test_layer_errors():
+    m = B.Model(h=256, n_heads=4, ffn=1024)
+    ctx = B.Context(m)
+    x = torch.zeros(384, 256, dtype=torch.bfloat16, device="cuda")
+    w = B.Weights(*([x.data_ptr()] * 6))
+    with pytest.raises(B.PdsError) as e:
+        ctx.layer_fwd(7, 384, x.data_ptr(), w, x.data_ptr())
+    assert e.value.code == -3
+    with pytest.raises(B.PdsError) as e:
+        ctx.layer_fwd(0, 200, x.data_ptr(), w, x.data_ptr())      # s/P not a multiple of 128
+    assert e.value.code == -2
+    ctx.close()
