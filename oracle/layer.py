@@ -212,21 +212,21 @@ def layer_bwd(dy, cache, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True,
     c = cache
     # FFN (O-2 step 1)
     dz = dy
-    dw_out = np.einsum("sbf,sbh->fh", c["g"], dz)
+    dw_out = np.tensordot(c["g"], dz, axes=([0, 1], [0, 1]))
     dg = dz @ w_out.T
     dh = dg * gelu_grad(c["h"])
-    dw_in = np.einsum("sbh,sbf->hf", c["v2"], dh)
+    dw_in = np.tensordot(c["v2"], dh, axes=([0, 1], [0, 1]))
     dv2 = dh @ w_in.T
     # RMSNorm2 (step 2)
     dx1n, dg2 = rmsnorm_bwd(dv2, c["xhat2"], c["r2"], g2)
     dx1 = dy + dx1n
     # projection (step 3)
-    dw_proj = np.einsum("sbi,sbj->ij", c["a"], dx1)
+    dw_proj = np.tensordot(c["a"], dx1, axes=([0, 1], [0, 1]))
     da = dx1 @ w_proj.T
     # attention + RoPE (steps 4-5)
     dqkv = mha_core_bwd(da, c["qkv"], c["a"], c["lse"], n, c["pos"], causal, theta)
     # QKV (step 6)
-    dw_qkv = np.einsum("sbh,sbj->hj", c["u"], dqkv)
+    dw_qkv = np.tensordot(c["u"], dqkv, axes=([0, 1], [0, 1]))
     du = dqkv @ w_qkv.T
     # RMSNorm1 (step 7)
     dxn, dg1 = rmsnorm_bwd(du, c["xhat1"], c["r1"], g1)

@@ -120,8 +120,8 @@ def ts_bwd(grid, dys, saved, W, cfg, grads):
         hp = sv[r]["h"]
         dg = dZ[r] @ W["w_out"][r].T
         dh = dg * gelu_grad(hp)
-        grads["dw_out"][r] += np.einsum("sbf,sbh->fh", gelu(hp), dZ[r])
-        grads["dw_in_t"][r] += np.einsum("sbf,sbh->fh", dh, V[r])
+        grads["dw_out"][r] += np.tensordot(gelu(hp), dZ[r], axes=([0, 1], [0, 1]))
+        grads["dw_in_t"][r] += np.tensordot(dh, V[r], axes=([0, 1], [0, 1]))
         dvpart.append(dh @ W["w_in_t"][r])
     dv = grid.reduce_scatter(dvpart)                               # RS(dv)
     dx1, dg2 = [], []
@@ -135,13 +135,13 @@ def ts_bwd(grid, dys, saved, W, cfg, grads):
     dqkv = []
     for r in range(P):
         da = dX1[r] @ W["w_proj"][r].T
-        grads["dw_proj"][r] += np.einsum("sbi,sbj->ij", sv[r]["a"], dX1[r])
+        grads["dw_proj"][r] += np.tensordot(sv[r]["a"], dX1[r], axes=([0, 1], [0, 1]))
         dqkv.append(mha_core_bwd(da, sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, pos,
                                  cfg.causal, cfg.theta))
     U = grid.all_gather(u)                                         # AG(u) re-gather
     dupart = []
     for r in range(P):
-        grads["dw_qkv_t"][r] += np.einsum("sbj,sbh->jh", dqkv[r], U[r])
+        grads["dw_qkv_t"][r] += np.tensordot(dqkv[r], U[r], axes=([0, 1], [0, 1]))
         dupart.append(dqkv[r] @ W["w_qkv_t"][r])
     du = grid.reduce_scatter(dupart)                               # RS(du)
     dx, dg1 = [], []
@@ -229,15 +229,15 @@ def uz_bwd(grid, dys, saved, W, cfg, grads):
         v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
         dg = dys[r] @ Wf["w_out"][r].T
         dh = dg * gelu_grad(hp)
-        dwo.append(np.einsum("sbf,sbh->fh", gelu(hp), dys[r]))
-        dwi.append(np.einsum("sbf,sbh->fh", dh, v))
+        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
         dv = dh @ Wf["w_in_t"][r]
         xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
         d, dgr = rmsnorm_bwd(dv, xhat2, sv[r]["r2"], W["g2"][r])
         dx1.append(dys[r] + d)
         dg2.append(dgr)
         dafull.append(dx1[r] @ Wf["w_proj"][r].T)
-        dwp.append(np.einsum("sbi,sbj->ij", sv[r]["afull"], dx1[r]))
+        dwp.append(np.tensordot(sv[r]["afull"], dx1[r], axes=([0, 1], [0, 1])))
     # A2A(dO): seq -> heads (column block j to rank j)
     da = grid.all_to_all(dafull, split_axis=2, concat_axis=0)
     dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
@@ -247,7 +247,7 @@ def uz_bwd(grid, dys, saved, W, cfg, grads):
     dx, dg1 = [], []
     for r in range(P):
         u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
-        dwq.append(np.einsum("sbj,sbh->jh", dqkv_loc[r], u))
+        dwq.append(np.tensordot(dqkv_loc[r], u, axes=([0, 1], [0, 1])))
         du = dqkv_loc[r] @ Wf["w_qkv_t"][r]
         xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
         d, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
@@ -358,8 +358,8 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
             hp = Vw[r] @ W["w_in_t"][r].T
             dg = dZw[r] @ W["w_out"][r].T
             dh = dg * gelu_grad(hp)
-            grads["dw_out"][r] += np.einsum("sbf,sbh->fh", gelu(hp), dZw[r])
-            grads["dw_in_t"][r] += np.einsum("sbf,sbh->fh", dh, Vw[r])
+            grads["dw_out"][r] += np.tensordot(gelu(hp), dZw[r], axes=([0, 1], [0, 1]))
+            grads["dw_in_t"][r] += np.tensordot(dh, Vw[r], axes=([0, 1], [0, 1]))
             dvpart.append(dh @ W["w_in_t"][r])
         dvw = grid.reduce_scatter(dvpart)                          # RS(dv) wave k
         for r in range(P):
@@ -376,7 +376,7 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
         dX1w = grid.all_gather([dx1[r][rows] for r in range(P)])   # AG(dx1) wave k
         for r in range(P):
             da[r][posw] = dX1w[r] @ W["w_proj"][r].T
-            grads["dw_proj"][r] += np.einsum("sbi,sbj->ij", sv[r]["a"][posw], dX1w[r])
+            grads["dw_proj"][r] += np.tensordot(sv[r]["a"][posw], dX1w[r], axes=([0, 1], [0, 1]))
     dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
                          cfg.causal, cfg.theta) for r in range(P)]
     dx = [np.zeros_like(d) for d in dys]
@@ -388,7 +388,7 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
         Uw = grid.all_gather(uloc)                                 # AG(u) wave k
         dupart = []
         for r in range(P):
-            grads["dw_qkv_t"][r] += np.einsum("sbj,sbh->jh", dqkv[r][posw], Uw[r])
+            grads["dw_qkv_t"][r] += np.tensordot(dqkv[r][posw], Uw[r], axes=([0, 1], [0, 1]))
             dupart.append(dqkv[r][posw] @ W["w_qkv_t"][r])
         duw = grid.reduce_scatter(dupart)                          # RS(du) wave k
         for r in range(P):

@@ -1,0 +1,207 @@
+"""Cost-model calibration: profile -> fit -> export bundle.
+
+1. Profile: device-timed fwd+bwd of ONE layer (R-31) per strategy over a
+   geometric grid of sequence lengths, CUDA events on the launching stream,
+   median of `reps` after warm-up, through the C ABI (pds_layer_fwd/bwd).
+2. Fit per strategy: a RandomForestRegressor (n_estimators=50,
+   max_depth=10, random_state=42) on features
+   one-hot(strategy) + normalised (h, n, L) + normalised s, and a polynomial of
+   degree 1..3 chosen by AIC in x = s / s_max (R-26).
+3. Export the "pds_bundle 1" text file read by pds_load_costs (Eq. 9 dispatch:
+   RF iff s <= s_profile_max, else PR).
+
+For P > 1 on a single-GPU box the profile is MODELLED: the per-rank compute of
+each strategy is measured on one GPU at the per-rank shapes through the
+loopback group, and the collective time is its byte count (oracle-independent
+formula of DESIGN.md §Comm) over the measured NVLink peer bandwidth (770 GB/s,
+B200_PROFILING.md).  The bundle header records which.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BUNDLES = os.path.join(HERE, "bundles")
+
+
+def aic_poly(s, y):
+    """Degree 1..3 least squares in x = s / s_max; AIC = n ln(max(RSS/n, 1e-12 var y)) + 2k."""
+    s = np.asarray(s, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    scale = float(s.max())
+    x = s / scale
+    best = None
+    for deg in (1, 2, 3):
+        if len(np.unique(x)) < deg + 1:
+            continue
+        c = np.polyfit(x, y, deg)
+        rss = float(np.sum((np.polyval(c, x) - y) ** 2))
+        n = len(y)
+        floor = 1e-12 * float(np.var(y)) if np.var(y) > 0 else 1e-300
+        a = n * math.log(max(rss / n, floor)) + 2 * (deg + 1)
+        if best is None or a < best[0] - 1e-12:
+            best = (a, deg, c)
+    return best[1], best[2], scale
+
+
+def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
+    """records: {strategy: [(s, seconds), ...]} -> bundle file."""
+    from sklearn.ensemble import RandomForestRegressor
+    strategies = sorted(records)
+    all_s = [s for st in strategies for s, _ in records[st]]
+    norm = [(h, h), (n, n), (L, L), (float(min(all_s)), float(max(all_s)))]
+
+    def feats(pi, s):
+        oh = [1.0 if e == pi else 0.0 for e in strategies]
+        def nz(v, a, b):
+            return 0.0 if a == b else (v - a) / (b - a)
+        return oh + [nz(h, *norm[0]), nz(n, *norm[1]), nz(L, *norm[2]), nz(s, *norm[3])]
+
+    lines = ["pds_bundle 1",
+             f"P {P} h {h} n {n} ffn {ffn} L {L} capacity {capacity!r} reserve {reserve!r}",
+             "norm " + " ".join(f"{float(a)!r} {float(b)!r}" for a, b in norm),
+             f"n_strat {len(strategies)}"]
+    for pi in strategies:
+        ss = np.array([s for s, _ in records[pi]], dtype=np.float64)
+        ts = np.array([t for _, t in records[pi]], dtype=np.float64)
+        X = np.array([feats(pi, s) for s in ss])
+        rf = RandomForestRegressor(n_estimators=50, max_depth=10, random_state=42).fit(X, ts)
+        deg, coef, scale = aic_poly(ss, ts)
+        lines.append(f"strategy {pi} s_profile_max {float(ss.max())!r} poly {deg} {scale!r} "
+                     + " ".join(repr(float(c)) for c in coef))
+        lines.append(f"trees {len(rf.estimators_)}")
+        for est in rf.estimators_:
+            tr = est.tree_
+            lines.append(f"tree {tr.node_count}")
+            for i in range(tr.node_count):
+                lines.append(f"{int(tr.feature[i])} {float(tr.threshold[i])!r} {int(tr.children_left[i])} "
+                             f"{int(tr.children_right[i])} {float(tr.value[i].ravel()[0])!r}")
+    lines.append("end")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(path + ".json", "w") as f:
+        json.dump({"P": P, "h": h, "n": n, "ffn": ffn, "L": L, "note": note,
+                   "records": {str(k): v for k, v in records.items()}}, f, indent=1)
+    return path
+
+
+# ------------------------------------------------------------------ profiling (GPU)
+def make_layer_buffers(torch, model, P, s, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    h, F = model.h, model.ffn
+    sl = s // P
+    def rn(*shape, std=1.0):
+        return (torch.randn(*shape, generator=g, device="cuda") * std).to(torch.bfloat16)
+    w = dict(w_qkv_t=rn(3 * h // P, h, std=h ** -0.5), w_proj=rn(h // P, h, std=h ** -0.5),
+             w_in_t=rn(F // P, h, std=h ** -0.5), w_out=rn(F // P, h, std=F ** -0.5),
+             g1=(1 + 0.1 * torch.randn(h, generator=g, device="cuda")).to(torch.bfloat16),
+             g2=(1 + 0.1 * torch.randn(h, generator=g, device="cuda")).to(torch.bfloat16))
+    gr = {k: torch.zeros(v.shape, dtype=torch.float32, device="cuda") for k, v in
+          (("dw_qkv_t", w["w_qkv_t"]), ("dw_proj", w["w_proj"]), ("dw_in_t", w["w_in_t"]),
+           ("dw_out", w["w_out"]), ("dg1", w["g1"]), ("dg2", w["g2"]))}
+    x = rn(sl, h)
+    dy = rn(sl, h)
+    return w, gr, x, dy
+
+
+def time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=5, warm=2):
+    st = torch.cuda.current_stream()
+    W = B.Weights(*(w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
+    G = B.Grads(*(gr[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    ts = []
+    for i in range(warm + reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        sv = ctx.layer_fwd(pi, s, x.data_ptr(), W, y.data_ptr(), st.cuda_stream)
+        ctx.layer_bwd(pi, dy.data_ptr(), sv, W, G, dx.data_ptr(), st.cuda_stream)
+        b.record(st)
+        b.synchronize()
+        if i >= warm:
+            ts.append(a.elapsed_time(b) / 1e3)
+    return float(np.median(ts))
+
+
+def comm_bytes_per_rank(pi, h, F, s, P):
+    """Bytes each rank moves per layer fwd+bwd (ring payload (P-1)/P x full)."""
+    if P == 1:
+        return 0.0
+    fr = (P - 1) / P
+    act = s * h * 2
+    if pi in (0, 2):
+        return 10 * fr * act + 2 * fr * 8 * h
+    a2a = 2 * fr * (s // P) * 4 * h * 2
+    wb = 4 * h * h + 2 * h * F
+    return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+
+
+def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.0):
+    import torch
+    from . import binding as B
+    model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L)
+    records = {0: [], 1: [], 2: []}
+    if P_target == 1:
+        ctx = B.Context(model)
+        for s in grid:
+            w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
+            for pi in (0, 1, 2):
+                t = time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=reps)
+                records[pi].append((int(s), t))
+                print(f"P=1 s={s} pi={pi} t={t * 1e3:.3f} ms", flush=True)
+            del w, gr, x, dy
+            torch.cuda.empty_cache()
+        ctx.close()
+        note = "measured: device-timed one-layer fwd+bwd on 1 B200"
+    else:
+        # modelled: per-rank compute measured at the per-rank shapes (TS: s tokens for
+        # the column/row-parallel GEMMs; UZ: s/P local tokens + full-s attention over
+        # n/P heads; METP: TS compute + waves) on a 1-rank context whose layer runs the
+        # same kernels, then collective bytes / link bandwidth added.
+        ctx = B.Context(model)
+        ctx_m = B.Context(B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, metp_chunks=P_target))
+        for s in grid:
+            t_unit = {}
+            for pi in (0, 1, 2):
+                w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
+                t1 = time_layer(torch, B, ctx_m if pi == 2 else ctx, pi, s, w, gr, x, dy, reps=reps)
+                t_unit[pi] = t1
+                del w, gr, x, dy
+            torch.cuda.empty_cache()
+            for pi in (0, 1, 2):
+                comp = t_unit[pi] / P
+                comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
+                extra = (2 * P - 1) * 8e-6 * (P if pi == 2 else 1)   # collective launch latency
+                records[pi].append((int(s), comp + comm + extra))
+        ctx.close()
+        ctx_m.close()
+        note = (f"modelled for P={P_target}: P=1 device time / P + comm bytes / {link_gbs} GB/s "
+                "(+ per-collective latency); replace with a measured profile on an 8xB200 box")
+    os.makedirs(out_dir, exist_ok=True)
+    path = os.path.join(out_dir, f"h{h}_n{n}_f{ffn}_P{P_target}.txt")
+    cap = float(torch.cuda.get_device_properties(0).total_memory)
+    fit_and_export(path, P_target, h, n, ffn, L, records, capacity=cap, reserve=8.0 * 2 ** 30, note=note)
+    return path
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--P", type=int, nargs="+", default=[1])
+    ap.add_argument("--h", type=int, default=4096)
+    ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--ffn", type=int, default=16384)
+    ap.add_argument("--L", type=int, default=32)
+    ap.add_argument("--grid", type=int, nargs="+",
+                    default=[1024, 2048, 4096, 8192, 16384, 32768, 65536])
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    for P in a.P:
+        t0 = time.time()
+        print(profile(P, a.h, a.n, a.ffn, a.L, a.grid, reps=a.reps), f"{time.time() - t0:.1f}s")
