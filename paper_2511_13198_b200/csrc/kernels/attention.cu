@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace pds {
 
@@ -547,8 +548,12 @@ static int fwd_t(const void* qkv, int64_t ld, int s, int heads, int causal, void
   return (int)cudaGetLastError();
 }
 
-int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out,
-             int64_t ld_out, void* lse, cudaStream_t st) {
+int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
+                void* lse, cudaStream_t st);
+
+// warp-level mma.sync FA2 forward (round-1 baseline, kept for A/B: PDS_ATTN_FWD=sync)
+int attn_fwd_sync(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out,
+                  int64_t ld_out, void* lse, cudaStream_t st) {
   if (s % 128) return (int)cudaErrorInvalidValue;
   if (d == 128) return fwd_t<128>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
   if (d == 64) return fwd_t<64>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
@@ -586,14 +591,42 @@ static int bwd_t(const void* qkv, int64_t ld, const void* out, int64_t ld_out, c
   return (int)cudaGetLastError();
 }
 
+int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out,
+             int64_t ld_out, void* lse, cudaStream_t st) {
+  static const bool use_sync = [] {
+    const char* e = getenv("PDS_ATTN_FWD");
+    return e && e[0] == 's';
+  }();
+  if (use_sync) return attn_fwd_sync(qkv, ld, s, heads, d, causal, out, ld_out, lse, st);
+  return attn_fwd_tc(qkv, ld, s, heads, d, causal, out, ld_out, lse, st);
+}
+
+int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st);
+
 // Dd: fp32 scratch [heads][s]
-int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
+int attn_bwd_sync(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
              const void* dout, int s, int heads, int d, int causal, void* dqkv, const void* rope,
              float* Dd, cudaStream_t st) {
   if (s % 128) return (int)cudaErrorInvalidValue;
   if (d == 128) return bwd_t<128>(qkv, ld, out, ld_out, lse, dout, s, heads, causal, dqkv, rope, Dd, st);
   if (d == 64) return bwd_t<64>(qkv, ld, out, ld_out, lse, dout, s, heads, causal, dqkv, rope, Dd, st);
   return (int)cudaErrorInvalidValue;
+}
+
+int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
+             const void* dout, int s, int heads, int d, int causal, void* dqkv, const void* rope,
+             float* Dd, cudaStream_t st) {
+  static const bool use_sync = [] {
+    const char* e = getenv("PDS_ATTN_BWD");
+    return e && e[0] == 's';
+  }();
+  if (use_sync) return attn_bwd_sync(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, rope, Dd, st);
+  if (s % 128) return (int)cudaErrorInvalidValue;
+  attn_bwd_dot_kernel<<<(s * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), s, heads,
+                                                          d, Dd);
+  return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st);
 }
 
 }  // namespace pds

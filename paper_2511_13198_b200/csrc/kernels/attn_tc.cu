@@ -1,0 +1,814 @@
+// tcgen05 / TMEM causal flash attention (Eq. 2; causal R-1) for
+// sm_100a.  One CTA per (128-query block, head):
+//
+//   warp 0      TMA producer: Q once, then K_j / V_j (128 keys) into a 2-stage ring
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered TMEM
+//               S (128 x 128 fp32), then O += P_j V_j into TMEM O (128 x d fp32)
+//   warp 2      TMEM allocator (512 columns: S0, S1, O)
+//   warps 4..7  softmax: thread t owns query row t (= TMEM lane t); two TMEM passes
+//               over S_j (row max, then exp2 / row sum / bf16 P into shared memory in
+//               the UMMA K-major SWIZZLE_128B layout); O is rescaled in TMEM only
+//               when the running max grows by more than 2^8 (exact: l and O always
+//               use the same stale max).  Epilogue: O / l -> bf16, LSE (natural log).
+//
+// Operand layouts (all SWIZZLE_128B, TMA boxes of 64 columns x 128 rows of the
+// [s][3*heads*d] QKV buffer): Q and K are K-major (K = d), V is MN-major (N = d,
+// K = keys), P is K-major (K = keys) written by the softmax warps.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ptx.cuh"
+
+namespace pds {
+
+namespace attn_tc {
+
+constexpr int BM = 128;  // queries per CTA
+constexpr int BN = 128;  // keys per block
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+template <int D>
+struct Cfg {
+  static constexpr int ATOMS = D / 64;                 // 64-column atoms per row
+  static constexpr int TILE = 128 * D * 2;             // one [128][D] bf16 tile
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = TILE;                   // 2 stages of K
+  static constexpr int V_OFF = K_OFF + 2 * TILE;       // 2 stages of V
+  static constexpr int P_OFF = V_OFF + 2 * TILE;       // P [128][128] bf16
+  static constexpr int BAR_OFF = P_OFF + 128 * 128 * 2;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int S_COL = 0;                      // S buffers at columns 0, 128
+  static constexpr int O_COL = 256;
+};
+
+}  // namespace attn_tc
+
+using namespace attn_tc;
+
+// K-major SW128 descriptor of k-step kk (16 elements) in a [rows][64*atoms] tile whose
+// 64-column atoms are `atom` bytes apart (rows * 128)
+__device__ __forceinline__ uint64_t kmaj_desc(uint32_t tile, int kk, uint32_t atom = 16384) {
+  return umma_desc_sw128(tile + (kk >> 2) * atom + (kk & 3) * 32, 16, 1024);
+}
+// MN-major SW128 descriptor: the tile's rows are K, 64-wide MN groups `atom` bytes
+// apart (LBO), k-step kk = 16 rows (2 x 8-row groups, SBO = 1024)
+__device__ __forceinline__ uint64_t mnmaj_desc(uint32_t tile, int kk, uint32_t atom = 16384) {
+  return umma_desc_sw128(tile + kk * 2048, atom, 1024);
+}
+
+// 16-byte chunk store into a K-major SW128 tile: row r, 16-byte chunk c of atom a
+__device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, int a, int c, uint4 v) {
+  *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int heads, int causal,
+                       __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
+                       float scale_log2) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;    // [2]
+  uint64_t* kv_empty = bar + 3;   // [2]
+  uint64_t* s_full = bar + 5;     // [2]
+  uint64_t* s_empty = bar + 7;    // [2]
+  uint64_t* p_full = bar + 9;
+  uint64_t* pv_done = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / BM;
+  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int head = blockIdx.y;
+  const int hq = heads * D;
+  const int q0 = qb * BM;
+  const int nkv = causal ? qb + 1 : s / BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // Q: D/64 boxes of [128 rows][64 cols]
+      mbar_arrive_expect_tx(q_full, C::TILE);
+      for (int a = 0; a < C::ATOMS; ++a)
+        tma_load_2d(sm + C::Q_OFF + a * 16384, &tm, q_full, head * D + a * 64, q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
+        for (int a = 0; a < C::ATOMS; ++a) {
+          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], hq + head * D + a * 64, j * BN);
+          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], 2 * hq + head * D + a * 64,
+                      j * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, BN, 0, 0);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1);
+    const uint32_t sq = smem_u32(sm + C::Q_OFF);
+    const uint32_t sp = smem_u32(sm + C::P_OFF);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int j) {
+      const int st = j & 1;
+      mbar_wait(&kv_full[st], (j >> 1) & 1);
+      if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = smem_u32(sm + C::K_OFF + st * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(tmem + C::S_COL + st * BN, kmaj_desc(sq, kk), kmaj_desc(sk, kk), idesc_s, kk > 0);
+        umma_commit(&s_full[st]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nkv; ++j) {
+      if (j + 1 < nkv) issue_s(j + 1);
+      mbar_wait(p_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sv = smem_u32(sm + C::V_OFF + (j & 1) * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          umma_f16(tmem + C::O_COL, kmaj_desc(sp, kk), mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
+        umma_commit(pv_done);
+        umma_commit(&kv_empty[j & 1]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int t = q * 32 + lane;             // query row within the block = TMEM lane
+    const int row = q0 + t;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    float m_used = -INFINITY, l = 0.f;
+    uint8_t* P = sm + C::P_OFF;
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sbase = lane_base + C::S_COL + st * BN;
+      const bool diag = causal && (j == qb);
+      const int k0 = j * BN;
+      // pass 1: row max
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(sbase + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float v = __uint_as_float(r[i]);
+          if (diag && k0 + c * 32 + i > row) v = -INFINITY;
+          mx = fmaxf(mx, v);
+        }
+      }
+      const float m_new = mx * scale_log2;
+      // wait until PV_{j-1} has finished reading P and accumulating O
+      if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
+      tc_fence_after();
+      const bool need = m_new > m_used + 8.0f;
+      if (__any_sync(0xffffffff, need) && j > 0) {
+        const float f = need ? exp2f(m_used - m_new) : 1.0f;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(lane_base + C::O_COL + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+          uint32_t (&lo)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
+          uint32_t (&hi)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[16]);
+          tmem_st16(lane_base + C::O_COL + c * 32, lo);
+          tmem_st16(lane_base + C::O_COL + c * 32 + 16, hi);
+        }
+        tmem_st_wait();
+        if (need) l *= f;
+      }
+      if (need) m_used = m_new;
+      // pass 2: p = exp2(s * scale_log2 - m_used), row sum, bf16 P into shared memory
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(sbase + c * 32, r);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
+          float p0 = exp2f(fmaf(v0, scale_log2, -m_used));
+          float p1 = exp2f(fmaf(v1, scale_log2, -m_used));
+          if (diag) {
+            if (k0 + c * 32 + i > row) p0 = 0.f;
+            if (k0 + c * 32 + i + 1 > row) p1 = 0.f;
+          }
+          rs += p0 + p1;
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
+        // 32 keys = 4 chunks of 8 in atom (c >> 1), chunks (c & 1) * 4 .. + 3
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int cc = (c & 1) * 4 + e;
+          uint8_t* dst = P + (c >> 1) * 16384 + t * 128 + ((cc ^ (t & 7)) << 4);
+          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
+      }
+      l += rs;
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_empty[st]);
+        mbar_arrive(p_full);
+      }
+    }
+    // epilogue
+    mbar_wait(pv_done, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    __nv_bfloat16* o = out + (int64_t)row * ld_out + head * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + C::O_COL + c * 32, r);
+      tmem_ld_wait();
+      uint4* d4 = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        d4[e] = make_uint4(pack_bf16(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
+                           pack_bf16(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
+                           pack_bf16(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
+                           pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+      }
+    }
+    lse[(int64_t)head * s + row] = (m_used + log2f(l)) * LN2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ================================================================== backward
+// RoPE^T + scale on one accumulator row held as chunk pairs (cols c*32.. and c*32 + D/2..)
+template <int D>
+__device__ __forceinline__ void rope_t_rows(float* a, float* b, const float2* rope, int64_t pos, int k0, float sc) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float x = a[i] * sc, y = b[i] * sc;
+    if (rope) {
+      const float2 cs = rope[pos * (D / 2) + k0 + i];
+      const float nx = x * cs.x + y * cs.y;
+      y = -x * cs.y + y * cs.x;
+      x = nx;
+    }
+    a[i] = x;
+    b[i] = y;
+  }
+}
+
+__device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float* v) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    d4[e] = make_uint4(pack_bf16(v[8 * e], v[8 * e + 1]), pack_bf16(v[8 * e + 2], v[8 * e + 3]),
+                       pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
+}
+
+// ---------------------------------------------------------------- dK / dV
+// CTA = (128-key block, head); loop over 64-query blocks.  Thread t of warps 4..7
+// owns key row t: S^T = K Q^T and dP^T = V dO^T land in TMEM (double-buffered),
+// P^T = exp2(S^T scale - lse), dS^T = P^T (dP^T - D) go to shared memory (K-major,
+// K = queries) and feed dV += P^T dO, dK += dS^T Q (dO, Q read MN-major from the
+// same tiles).  dK gets the softmax scale and RoPE^T in the epilogue.
+template <int D>
+struct BwdKVCfg {
+  static constexpr int KT = 128 * D * 2;     // K or V tile [128][D]
+  static constexpr int QT = 64 * D * 2;      // Q or dO tile [64][D]
+  static constexpr int K_OFF = 0, V_OFF = KT;
+  static constexpr int Q_OFF = 2 * KT;       // [2]
+  static constexpr int O_OFF = Q_OFF + 2 * QT;   // dO [2]
+  static constexpr int P_OFF = O_OFF + 2 * QT;   // P^T [2][128][64]
+  static constexpr int S_OFF = P_OFF + 2 * 16384;  // dS^T [2]
+  static constexpr int L_OFF = S_OFF + 2 * 16384;  // lse [2][64], D [2][64] floats
+  static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
+                            const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
+                            const float* __restrict__ Dd, int s, int heads, int causal,
+                            __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
+                            float scale, float scale_log2) {
+  using C = BwdKVCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;     // [2]
+  uint64_t* q_empty = bar + 3;    // [2]
+  uint64_t* st_full = bar + 5;    // [2]
+  uint64_t* st_empty = bar + 7;   // [2]
+  uint64_t* p_full = bar + 9;     // [2]
+  uint64_t* pd_done = bar + 11;   // [2]
+  uint64_t* fin = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, head = blockIdx.y;
+  const int hq = heads * D;
+  const int k0 = kb * 128;
+  const int qstart = causal ? k0 / 64 : 0;
+  const int nq = s / 64 - qstart;
+  constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tkv);
+    tma_prefetch(&tq);
+    tma_prefetch(&tdo);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pd_done[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::KT);
+      for (int a = 0; a < D / 64; ++a) {
+        tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, hq + head * D + a * 64, k0);
+        tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, 2 * hq + head * D + a * 64, k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int b = i & 1, q0 = (qstart + i) * 64;
+        if (i >= 2) mbar_wait(&q_empty[b], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[b], 2 * C::QT + 2 * 256);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::Q_OFF + b * C::QT + a * 8192, &tq, &q_full[b], head * D + a * 64, q0);
+          tma_load_2d(sm + C::O_OFF + b * C::QT + a * 8192, &tdo, &q_full[b], head * D + a * 64, q0);
+        }
+        bulk_load(sm + C::L_OFF + b * 256, lse + (int64_t)head * s + q0, 256, &q_full[b]);
+        bulk_load(sm + C::L_OFF + 512 + b * 256, Dd + (int64_t)head * s + q0, 256, &q_full[b]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_st = umma_idesc_bf16(128, 64, 0, 0);
+    constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
+    const uint32_t sk = smem_u32(sm + C::K_OFF), sv = smem_u32(sm + C::V_OFF);
+    mbar_wait(kv_full, 0);
+    auto dkdv = [&](int i) {
+      const int b = i & 1;
+      mbar_wait(&p_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
+        const uint32_t sp = smem_u32(sm + C::P_OFF + b * 16384), ss = smem_u32(sm + C::S_OFF + b * 16384);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_f16(tmem + DV_COL, kmaj_desc(sp, kk), mnmaj_desc(so, kk, 8192), idesc_acc, (i | kk) != 0);
+          umma_f16(tmem + DK_COL, kmaj_desc(ss, kk), mnmaj_desc(sq, kk, 8192), idesc_acc, (i | kk) != 0);
+        }
+        umma_commit(&pd_done[b]);
+        umma_commit(&q_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int i = 0; i < nq; ++i) {
+      const int b = i & 1;
+      mbar_wait(&q_full[b], (i >> 1) & 1);
+      if (i >= 2) mbar_wait(&st_empty[b], ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16(tmem + ST_COL + b * 64, kmaj_desc(sk, kk), kmaj_desc(sq, kk, 8192), idesc_st, kk > 0);
+          umma_f16(tmem + DP_COL + b * 64, kmaj_desc(sv, kk), kmaj_desc(so, kk, 8192), idesc_st, kk > 0);
+        }
+        umma_commit(&st_full[b]);
+      }
+      __syncwarp();
+      if (i >= 1) dkdv(i - 1);
+    }
+    dkdv(nq - 1);
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int key = k0 + t;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    for (int i = 0; i < nq; ++i) {
+      const int b = i & 1, q0 = (qstart + i) * 64;
+      mbar_wait(&st_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      const float* L = reinterpret_cast<const float*>(sm + C::L_OFF + b * 256);
+      const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + 512 + b * 256);
+      const bool mask = causal && (q0 < k0 + 128);
+      uint32_t pk[2][16], dk[2][16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(lb + ST_COL + b * 64 + c * 32, sr);
+        tmem_ld32(lb + DP_COL + b * 64 + c * 32, dr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -L[c * 32 + e] * LOG2E));
+          float p1 = exp2f(fmaf(__uint_as_float(sr[e + 1]), scale_log2, -L[c * 32 + e + 1] * LOG2E));
+          if (mask) {
+            if (key > q0 + c * 32 + e) p0 = 0.f;
+            if (key > q0 + c * 32 + e + 1) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dr[e]) - Dv[c * 32 + e]);
+          const float d1 = p1 * (__uint_as_float(dr[e + 1]) - Dv[c * 32 + e + 1]);
+          pk[c][e >> 1] = pack_bf16(p0, p1);
+          dk[c][e >> 1] = pack_bf16(d0, d1);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[b]);
+      if (i >= 2) mbar_wait(&pd_done[b], ((i >> 1) - 1) & 1);
+      uint8_t* PT = sm + C::P_OFF + b * 16384;
+      uint8_t* ST = sm + C::S_OFF + b * 16384;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          st_sw128(PT, 16384, t, 0, c * 4 + e, make_uint4(pk[c][4 * e], pk[c][4 * e + 1], pk[c][4 * e + 2], pk[c][4 * e + 3]));
+          st_sw128(ST, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
+        }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+    }
+    // epilogue: dK (scale, RoPE^T), dV
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(lb + DK_COL + c * 32, ra);
+      tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
+      tmem_ld_wait();
+      float a[32], bb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
+      rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+      store32_bf16(rowp + hq + c * 32, a);
+      store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+    }
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(lb + DV_COL + c * 32, r);
+      tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      store32_bf16(rowp + 2 * hq + c * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------- dQ
+// CTA = (128-query block, head); loop over 64-key blocks: S = Q K^T, dP = dO V^T
+// in TMEM (double-buffered); dS = P (dP - D) -> shared memory (K-major, K = keys);
+// dQ += dS K (K read MN-major) accumulates in TMEM; epilogue scale + RoPE^T.
+template <int D>
+struct BwdQCfg {
+  static constexpr int QT = 128 * D * 2;    // Q or dO [128][D]
+  static constexpr int KT = 64 * D * 2;     // K or V [64][D]
+  static constexpr int Q_OFF = 0, O_OFF = QT;
+  static constexpr int K_OFF = 2 * QT;      // [2]
+  static constexpr int V_OFF = K_OFF + 2 * KT;  // [2]
+  static constexpr int S_OFF = V_OFF + 2 * KT;  // dS [2][128][64]
+  static constexpr int L_OFF = S_OFF + 2 * 16384;   // lse [128], D [128]
+  static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
+                          const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
+                          const float* __restrict__ Dd, int s, int heads, int causal,
+                          __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
+                          float scale, float scale_log2) {
+  using C = BwdQCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;    // [2]
+  uint64_t* kv_empty = bar + 3;   // [2]
+  uint64_t* sd_full = bar + 5;    // [2]
+  uint64_t* sd_empty = bar + 7;   // [2]
+  uint64_t* ds_full = bar + 9;    // [2]
+  uint64_t* dq_done = bar + 11;   // [2]
+  uint64_t* fin = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / 128;
+  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int head = blockIdx.y;
+  const int hq = heads * D;
+  const int q0 = qb * 128;
+  const int nkv = causal ? (q0 + 128) / 64 : s / 64;
+  constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tdo);
+    tma_prefetch(&tkv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_empty[i], 4);
+      mbar_init(&ds_full[i], 4);
+      mbar_init(&dq_done[i], 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, 2 * C::QT + 2 * 512);
+      for (int a = 0; a < D / 64; ++a) {
+        tma_load_2d(sm + C::Q_OFF + a * 16384, &tq, q_full, head * D + a * 64, q0);
+        tma_load_2d(sm + C::O_OFF + a * 16384, &tdo, q_full, head * D + a * 64, q0);
+      }
+      bulk_load(sm + C::L_OFF, lse + (int64_t)head * s + q0, 512, q_full);
+      bulk_load(sm + C::L_OFF + 512, Dd + (int64_t)head * s + q0, 512, q_full);
+      for (int j = 0; j < nkv; ++j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[b], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
+          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
+    const uint32_t sq = smem_u32(sm + C::Q_OFF), so = smem_u32(sm + C::O_OFF);
+    mbar_wait(q_full, 0);
+    auto dq = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&ds_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sd = smem_u32(sm + C::S_OFF + b * 16384), sk = smem_u32(sm + C::K_OFF + b * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16(tmem + DQ_COL, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
+        umma_commit(&dq_done[b]);
+        umma_commit(&kv_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1;
+      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      if (j >= 2) mbar_wait(&sd_empty[b], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = smem_u32(sm + C::K_OFF + b * C::KT), sv = smem_u32(sm + C::V_OFF + b * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16(tmem + S_COL + b * 64, kmaj_desc(sq, kk), kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
+          umma_f16(tmem + DP_COL + b * 64, kmaj_desc(so, kk), kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
+        }
+        umma_commit(&sd_full[b]);
+      }
+      __syncwarp();
+      if (j >= 1) dq(j - 1);
+    }
+    dq(nkv - 1);
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int row = q0 + t;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    mbar_wait(q_full, 0);
+    const float l2 = reinterpret_cast<const float*>(sm + C::L_OFF)[t] * LOG2E;
+    const float dd = reinterpret_cast<const float*>(sm + C::L_OFF + 512)[t];
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1, k0 = j * 64;
+      mbar_wait(&sd_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const bool mask = causal && (k0 + 63 > q0);
+      uint32_t dk[2][16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(lb + S_COL + b * 64 + c * 32, sr);
+        tmem_ld32(lb + DP_COL + b * 64 + c * 32, dr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -l2));
+          float p1 = exp2f(fmaf(__uint_as_float(sr[e + 1]), scale_log2, -l2));
+          if (mask) {
+            if (k0 + c * 32 + e > row) p0 = 0.f;
+            if (k0 + c * 32 + e + 1 > row) p1 = 0.f;
+          }
+          dk[c][e >> 1] = pack_bf16(p0 * (__uint_as_float(dr[e]) - dd), p1 * (__uint_as_float(dr[e + 1]) - dd));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_empty[b]);
+      if (j >= 2) mbar_wait(&dq_done[b], ((j >> 1) - 1) & 1);
+      uint8_t* DS = sm + C::S_OFF + b * 16384;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          st_sw128(DS, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[b]);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(lb + DQ_COL + c * 32, ra);
+      tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
+      tmem_ld_wait();
+      float a[32], bb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
+      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
+      store32_bf16(rowp + c * 32, a);
+      store32_bf16(rowp + c * 32 + D / 2, bb);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                  uint32_t box_rows = 128) {
+  auto enc = encode_fn();
+  if (!enc) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+template <int D>
+static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, void* out, int64_t ld_out,
+                    void* lse, cudaStream_t st) {
+  CUtensorMap tm;
+  int rc = make_map_rows(&tm, qkv, (uint64_t)3 * heads * D, (uint64_t)s, (uint64_t)ld);
+  if (rc) return rc;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
+    once = true;
+  }
+  const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
+  attn_fwd_tc_kernel<D><<<dim3(s / BM, heads), 256, Cfg<D>::SMEM, st>>>(
+      tm, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
+      scale_log2);
+  return (int)cudaGetLastError();
+}
+
+int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
+                void* lse, cudaStream_t st) {
+  if (s % 128 || (ld % 8)) return (int)cudaErrorInvalidValue;
+  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
+  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace pds
+
+namespace pds {
+template <int D>
+static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                    int s, int heads, int causal, void* dqkv, const void* rope, cudaStream_t st) {
+  const uint64_t cols = (uint64_t)3 * heads * D;
+  CUtensorMap kv128, q64, do64, q128, do128, kv64;
+  int rc = make_map_rows(&kv128, qkv, cols, s, ld, 128);
+  rc |= make_map_rows(&q64, qkv, cols, s, ld, 64);
+  rc |= make_map_rows(&do64, dout, (uint64_t)heads * D, s, ld_out, 64);
+  rc |= make_map_rows(&q128, qkv, cols, s, ld, 128);
+  rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, s, ld_out, 128);
+  rc |= make_map_rows(&kv64, qkv, cols, s, ld, 64);
+  if (rc) return (int)cudaErrorInvalidValue;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKVCfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQCfg<D>::SMEM);
+    once = true;
+  }
+  const float scale = 1.0f / sqrtf((float)D);
+  const float scale_log2 = scale * LOG2E;
+  attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdKVCfg<D>::SMEM, st>>>(
+      kv128, q64, do64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+      reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  attn_bwd_dq_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdQCfg<D>::SMEM, st>>>(
+      q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+      reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  return (int)cudaGetLastError();
+}
+
+// dQ, dK, dV into dqkv (same [s][ld] layout as qkv); Dd = rowsum(dO o O) precomputed
+int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st) {
+  if (s % 128 || ld % 8 || ld_out % 8) return (int)cudaErrorInvalidValue;
+  if (d == 128) return bwd_tc_t<128>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, st);
+  if (d == 64) return bwd_tc_t<64>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, st);
+  return (int)cudaErrorInvalidValue;
+}
+}  // namespace pds
