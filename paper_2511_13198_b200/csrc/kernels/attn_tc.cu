@@ -27,7 +27,7 @@ namespace pds {
 
 namespace attn_tc {
 
-constexpr int BM = 128;  // queries per CTA
+[[maybe_unused]] constexpr int BM = 128;  // queries per tile
 constexpr int BN = 128;  // keys per block
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -66,31 +66,48 @@ __device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, in
   *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
 }
 
+// Forward, two 128-row query tiles per CTA (rows [q0, q0+128) and [q0+128, q0+256))
+// sharing every K/V tile.  TMEM: S0 | S1 | O0 | O1 (128 columns each).  MMA order per
+// KV block j:  PV0_{j-1}? ... S0_j, S1_j, PV0_j, S0_{j+1}, PV1_j, S1_{j+1}, ...  so the
+// softmax of one tile overlaps the other tile's MMAs.  P_t is written back as packed
+// bf16 into the first 64 columns of S_t and consumed with the A operand in TMEM;
+// because tcgen05 MMAs of one thread execute in issue order, S_t(j+1) (issued after
+// PV_t(j)) completing implies PV_t(j) completed, so the softmax may rescale O_t and
+// overwrite P_t as soon as S_t(j+1) is ready.
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+struct Fwd2Cfg {
+  static constexpr int TILE = 128 * D * 2;
+  static constexpr int Q_OFF = 0;                 // Q0, Q1
+  static constexpr int K_OFF = 2 * TILE;          // [2 stages]
+  static constexpr int V_OFF = K_OFF + 2 * TILE;  // [2 stages]
+  static constexpr int BAR_OFF = V_OFF + 2 * TILE;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int heads, int causal,
                        __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
                        float scale_log2) {
-  using C = Cfg<D>;
+  using C = Fwd2Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
   uint64_t* q_full = bar + 0;
   uint64_t* kv_full = bar + 1;    // [2]
   uint64_t* kv_empty = bar + 3;   // [2]
-  uint64_t* s_full = bar + 5;     // [2]
-  uint64_t* s_empty = bar + 7;    // [2]
-  uint64_t* p_full = bar + 9;
-  uint64_t* pv_done = bar + 10;
+  uint64_t* s_full = bar + 5;     // [2] per tile
+  uint64_t* p_full = bar + 7;     // [2] per tile
+  uint64_t* o_done = bar + 9;     // [2] per tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = s / BM;
+  const int nqb = (s + 255) / 256;
   const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int head = blockIdx.y;
   const int hq = heads * D;
-  const int q0 = qb * BM;
-  const int nkv = causal ? qb + 1 : s / BN;
+  const int q0 = qb * 256;
+  const int nkv = causal ? min(s, q0 + 256) / BN : s / BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
@@ -99,10 +116,9 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -113,15 +129,15 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      // Q: D/64 boxes of [128 rows][64 cols]
-      mbar_arrive_expect_tx(q_full, C::TILE);
-      for (int a = 0; a < C::ATOMS; ++a)
-        tma_load_2d(sm + C::Q_OFF + a * 16384, &tm, q_full, head * D + a * 64, q0);
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < D / 64; ++a)
+          tma_load_2d(sm + C::Q_OFF + t * C::TILE + a * 16384, &tm, q_full, head * D + a * 64, q0 + 128 * t);
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
-        for (int a = 0; a < C::ATOMS; ++a) {
+        for (int a = 0; a < D / 64; ++a) {
           tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], hq + head * D + a * 64, j * BN);
           tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], 2 * hq + head * D + a * 64,
                       j * BN);
@@ -132,145 +148,139 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, BN, 0, 0);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1);
     const uint32_t sq = smem_u32(sm + C::Q_OFF);
-    const uint32_t sp = smem_u32(sm + C::P_OFF);
     mbar_wait(q_full, 0);
-    auto issue_s = [&](int j) {
-      const int st = j & 1;
-      mbar_wait(&kv_full[st], (j >> 1) & 1);
-      if (j >= 2) mbar_wait(&s_empty[st], ((j >> 1) - 1) & 1);
-      tc_fence_after();
+    auto issue_s = [&](int t, int j) {
       if (elect_one()) {
-        const uint32_t sk = smem_u32(sm + C::K_OFF + st * C::TILE);
+        const uint32_t sk = smem_u32(sm + C::K_OFF + (j & 1) * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16(tmem + C::S_COL + st * BN, kmaj_desc(sq, kk), kmaj_desc(sk, kk), idesc_s, kk > 0);
-        umma_commit(&s_full[st]);
+          umma_f16(tmem + t * 128, kmaj_desc(sq + t * C::TILE, kk), kmaj_desc(sk, kk), idesc_s, kk > 0);
+        umma_commit(&s_full[t]);
       }
       __syncwarp();
     };
-    issue_s(0);
-    for (int j = 0; j < nkv; ++j) {
-      if (j + 1 < nkv) issue_s(j + 1);
-      mbar_wait(p_full, j & 1);
+    auto issue_pv = [&](int t, int j) {
+      mbar_wait(&p_full[t], j & 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sv = smem_u32(sm + C::V_OFF + (j & 1) * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          umma_f16(tmem + C::O_COL, kmaj_desc(sp, kk), mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
-        umma_commit(pv_done);
-        umma_commit(&kv_empty[j & 1]);
+          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
       }
+      __syncwarp();
+    };
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < nkv; ++j) {
+      issue_pv(0, j);
+      if (j + 1 < nkv) {
+        mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);
+      } else if (elect_one()) {
+        umma_commit(&o_done[0]);
+      }
+      __syncwarp();
+      issue_pv(1, j);
+      if (elect_one()) umma_commit(&kv_empty[j & 1]);
+      __syncwarp();
+      if (j + 1 < nkv) issue_s(1, j + 1);
+      else if (elect_one()) umma_commit(&o_done[1]);
       __syncwarp();
     }
   } else if (warp >= 4) {
+    const int tile = (warp - 4) >> 2;        // 0: warps 4-7, 1: warps 8-11
     const int q = warp & 3;
-    const int t = q * 32 + lane;             // query row within the block = TMEM lane
-    const int row = q0 + t;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int tr = q * 32 + lane;            // row within the tile = TMEM lane
+    const int row = q0 + tile * 128 + tr;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t s_col = tile * 128, o_col = 256 + tile * 128;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* P = sm + C::P_OFF;
     for (int j = 0; j < nkv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[tile], j & 1);
       tc_fence_after();
-      const uint32_t sbase = lane_base + C::S_COL + st * BN;
-      const bool diag = causal && (j == qb);
       const int k0 = j * BN;
-      // pass 1: row max
+      const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
       float mx = -INFINITY;
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(sbase + c * 32, r);
+        tmem_ld32(lb + s_col + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           float v = __uint_as_float(r[i]);
-          if (diag && k0 + c * 32 + i > row) v = -INFINITY;
+          if (mask && k0 + c * 32 + i > row) v = -INFINITY;
           mx = fmaxf(mx, v);
         }
       }
       const float m_new = mx * scale_log2;
-      // wait until PV_{j-1} has finished reading P and accumulating O
-      if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
-      tc_fence_after();
       const bool need = m_new > m_used + 8.0f;
-      if (__any_sync(0xffffffff, need) && j > 0) {
+      if (j > 0 && __any_sync(0xffffffff, need)) {
         const float f = need ? exp2f(m_used - m_new) : 1.0f;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
-          tmem_ld32(lane_base + C::O_COL + c * 32, r);
+          tmem_ld32(lb + o_col + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-          uint32_t (&lo)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[0]);
-          uint32_t (&hi)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[16]);
-          tmem_st16(lane_base + C::O_COL + c * 32, lo);
-          tmem_st16(lane_base + C::O_COL + c * 32 + 16, hi);
+          tmem_st16(lb + o_col + c * 32, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+          tmem_st16(lb + o_col + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
         }
-        tmem_st_wait();
         if (need) l *= f;
       }
       if (need) m_used = m_new;
-      // pass 2: p = exp2(s * scale_log2 - m_used), row sum, bf16 P into shared memory
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(sbase + c * 32, r);
+        tmem_ld32(lb + s_col + c * 32, r);
         tmem_ld_wait();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float v0 = __uint_as_float(r[i]), v1 = __uint_as_float(r[i + 1]);
-          float p0 = exp2f(fmaf(v0, scale_log2, -m_used));
-          float p1 = exp2f(fmaf(v1, scale_log2, -m_used));
-          if (diag) {
+          float p0 = exp2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_used));
+          float p1 = exp2f(fmaf(__uint_as_float(r[i + 1]), scale_log2, -m_used));
+          if (mask) {
             if (k0 + c * 32 + i > row) p0 = 0.f;
             if (k0 + c * 32 + i + 1 > row) p1 = 0.f;
           }
           rs += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
-        // 32 keys = 4 chunks of 8 in atom (c >> 1), chunks (c & 1) * 4 .. + 3
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int cc = (c & 1) * 4 + e;
-          uint8_t* dst = P + (c >> 1) * 16384 + t * 128 + ((cc ^ (t & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-        }
+        tmem_st16(lb + s_col + c * 16, pk);     // P chunk c -> packed bf16 columns 16c..16c+15
       }
       l += rs;
+      tmem_st_wait();
       tc_fence_before();
-      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[st]);
-        mbar_arrive(p_full);
-      }
+      if (lane == 0) mbar_arrive(&p_full[tile]);
     }
-    // epilogue
-    mbar_wait(pv_done, (nkv - 1) & 1);
+    mbar_wait(&o_done[tile], 0);
     tc_fence_after();
     const float inv = 1.0f / l;
+    const bool ok = row < s;
     __nv_bfloat16* o = out + (int64_t)row * ld_out + head * D;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t r[32];
-      tmem_ld32(lane_base + C::O_COL + c * 32, r);
+      tmem_ld32(lb + o_col + c * 32, r);
       tmem_ld_wait();
-      uint4* d4 = reinterpret_cast<uint4*>(o + c * 32);
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(o + c * 32);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        d4[e] = make_uint4(pack_bf16(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
-                           pack_bf16(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
-                           pack_bf16(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
-                           pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+        for (int e = 0; e < 4; ++e)
+          d4[e] = make_uint4(pack_bf16(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
       }
     }
-    lse[(int64_t)head * s + row] = (m_used + log2f(l)) * LN2;
+    if (ok) lse[(int64_t)head * s + row] = (m_used + log2f(l)) * LN2;
   }
   tc_fence_before();
   __syncthreads();
@@ -753,11 +763,11 @@ static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, v
   if (rc) return rc;
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
     once = true;
   }
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
-  attn_fwd_tc_kernel<D><<<dim3(s / BM, heads), 256, Cfg<D>::SMEM, st>>>(
+  attn_fwd_tc_kernel<D><<<dim3((s + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
       tm, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
       scale_log2);
   return (int)cudaGetLastError();
