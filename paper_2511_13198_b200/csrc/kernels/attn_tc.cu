@@ -61,6 +61,19 @@ __device__ __forceinline__ uint64_t mnmaj_desc(uint32_t tile, int kk, uint32_t a
   return umma_desc_sw128(tile + kk * 2048, atom, 1024);
 }
 
+// 2^x for x <= 0 on the FMA pipe (Cody-Waite split + degree-3 minimax on [-0.5, 0.5],
+// max relative error 7.5e-5 — far below the bf16 rounding of P).  Used for a share of
+// the softmax exponentials so the MUFU (ex2) unit is not the bottleneck.
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;             // 1.5 * 2^23: round to nearest integer
+  const float f = x - (t - 12582912.0f);       // [-0.5, 0.5]
+  float p = fmaf(0.05517161f, f, 0.24261112f);
+  p = fmaf(p, f, 0.693261f);
+  p = fmaf(p, f, 0.99992807f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // 16-byte chunk store into a K-major SW128 tile: row r, 16-byte chunk c of atom a
 __device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, int a, int c, uint4 v) {
   *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
@@ -204,19 +217,26 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const int k0 = j * BN;
       const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
-      float mx = -INFINITY;
+      // pass 1: row max with 8 independent accumulators, two TMEM loads per wait
+      float mxa[8];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
+      for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < BN / 32; c += 2) {
+        uint32_t r[32], r2[32];
         tmem_ld32(lb + s_col + c * 32, r);
+        tmem_ld32(lb + s_col + c * 32 + 32, r2);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(r[i]);
+          float v = __uint_as_float(r[i]), w = __uint_as_float(r2[i]);
           if (mask && k0 + c * 32 + i > row) v = -INFINITY;
-          mx = fmaxf(mx, v);
+          if (mask && k0 + c * 32 + 32 + i > row) w = -INFINITY;
+          mxa[i & 7] = fmaxf(mxa[i & 7], fmaxf(v, w));
         }
       }
+      const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                             fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
       const float m_new = mx * scale_log2;
       const bool need = m_new > m_used + 8.0f;
       if (j > 0 && __any_sync(0xffffffff, need)) {
@@ -234,27 +254,36 @@ __global__ void __launch_bounds__(384, 1)
         if (need) l *= f;
       }
       if (need) m_used = m_new;
-      float rs = 0.f;
+      // pass 2: p = exp2(s scale - m), 4 independent row-sum accumulators
+      float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+      const float neg_m = -m_used;
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
+      for (int c = 0; c < BN / 32; c += 2) {
+        uint32_t r[32], r2[32];
         tmem_ld32(lb + s_col + c * 32, r);
+        tmem_ld32(lb + s_col + c * 32 + 32, r2);
         tmem_ld_wait();
-        uint32_t pk[16];
+        uint32_t pk[16], pk2[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          float p0 = exp2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_used));
-          float p1 = exp2f(fmaf(__uint_as_float(r[i + 1]), scale_log2, -m_used));
+          float p0 = exp2f(fmaf(__uint_as_float(r[i]), scale_log2, neg_m));
+          float p1 = exp2f(fmaf(__uint_as_float(r[i + 1]), scale_log2, neg_m));
+          float p2 = exp2f(fmaf(__uint_as_float(r2[i]), scale_log2, neg_m));
+          float p3 = exp2_fma(fmaf(__uint_as_float(r2[i + 1]), scale_log2, neg_m));
           if (mask) {
             if (k0 + c * 32 + i > row) p0 = 0.f;
             if (k0 + c * 32 + i + 1 > row) p1 = 0.f;
+            if (k0 + c * 32 + 32 + i > row) p2 = 0.f;
+            if (k0 + c * 32 + 32 + i + 1 > row) p3 = 0.f;
           }
-          rs += p0 + p1;
+          rsa[(i >> 1) & 3] += (p0 + p1) + (p2 + p3);
           pk[i >> 1] = pack_bf16(p0, p1);
+          pk2[i >> 1] = pack_bf16(p2, p3);
         }
         tmem_st16(lb + s_col + c * 16, pk);     // P chunk c -> packed bf16 columns 16c..16c+15
+        tmem_st16(lb + s_col + c * 16 + 16, pk2);
       }
-      l += rs;
+      l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -469,7 +498,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -L[c * 32 + e] * LOG2E));
-          float p1 = exp2f(fmaf(__uint_as_float(sr[e + 1]), scale_log2, -L[c * 32 + e + 1] * LOG2E));
+          const float x1 = fmaf(__uint_as_float(sr[e + 1]), scale_log2, -L[c * 32 + e + 1] * LOG2E);
+          float p1 = exp2f(x1);
           if (mask) {
             if (key > q0 + c * 32 + e) p0 = 0.f;
             if (key > q0 + c * 32 + e + 1) p1 = 0.f;
@@ -682,7 +712,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -l2));
-          float p1 = exp2f(fmaf(__uint_as_float(sr[e + 1]), scale_log2, -l2));
+          const float x1 = fmaf(__uint_as_float(sr[e + 1]), scale_log2, -l2);
+          float p1 = exp2f(x1);
           if (mask) {
             if (k0 + c * 32 + e > row) p0 = 0.f;
             if (k0 + c * 32 + e + 1 > row) p1 = 0.f;

@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "gemm.cuh"
 #include "ptx.cuh"
@@ -119,6 +122,104 @@ __device__ __forceinline__ int64_t out_offset(const EpiParams& p, int row_l, int
     return (int64_t)blk * p.blk_stride + (int64_t)row * p.ldc + (col - blk * p.blk_w);
   }
   return (int64_t)row * p.ldc + col;
+}
+
+// Drain one accumulator tile (this thread's row, BN columns at TMEM address tbase)
+// through the fused epilogue.  Called by the four epilogue warps (warp-collective
+// tcgen05.ld, so every lane executes every load).
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbase, int row, bool row_ok,
+                                              int n0, int N) {
+  if (ep.epi == EPI_ROPE) {
+    const int d = ep.rope_d, d2 = d >> 1;
+    int64_t pos = 0;
+    if (row_ok) {
+      const int64_t r = row;
+      pos = (r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg);
+    }
+    for (int hs = 0; hs < BN; hs += d) {
+      for (int j0 = 0; j0 < d2; j0 += 32) {
+        uint32_t r1[32], r2[32];
+        tmem_ld32(tbase + hs + j0, r1);
+        tmem_ld32(tbase + hs + j0 + d2, r2);
+        tmem_ld_wait();
+        const int c1 = n0 + hs + j0;
+        if (row_ok && c1 < N) {
+        float v1[32], v2[32];
+        const int within = (n0 + hs) % (3 * ep.rope_hq);
+        if (within < 2 * ep.rope_hq) {
+          const float2* cs = ep.rope + pos * d2 + j0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 c = cs[i];
+            const float a = __uint_as_float(r1[i]), b = __uint_as_float(r2[i]);
+            v1[i] = a * c.x - b * c.y;
+            v2[i] = a * c.y + b * c.x;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v1[i] = __uint_as_float(r1[i]);
+            v2[i] = __uint_as_float(r2[i]);
+          }
+        }
+        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C);
+        store_row32_bf16(C + out_offset(ep, row, c1), v1, 32);
+        store_row32_bf16(C + out_offset(ep, row, c1 + d2), v2, 32);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    for (int cc = 0; cc < BN; cc += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + cc, r);
+      tmem_ld_wait();
+      const int col = n0 + cc;
+      if (row_ok && col < N) {
+      const int valid = min(32, N - col);
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      if (ep.epi == EPI_BF16) {
+        store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                         valid);
+      } else if (ep.epi == EPI_F32_ACC || ep.epi == EPI_F32) {
+        float4* c4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + out_offset(ep, row, col));
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e * 4 < valid) {
+            float4 o = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+            if (ep.epi == EPI_F32_ACC) {
+              const float4 old = c4[e];
+              o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+            }
+            c4[e] = o;
+          }
+        }
+      } else if (ep.epi == EPI_GELU) {
+        float g[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) g[i] = gelu_f(bf16_round(v[i]));
+        store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                         valid);
+        store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+      } else if (ep.epi == EPI_DGELU) {
+        float hh[32], g[32];
+        load_row32_bf16(ep.aux_in + (int64_t)row * ep.ld_aux + col, hh, valid);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          g[i] = gelu_f(hh[i]);
+          v[i] = v[i] * gelu_grad_f(hh[i]);
+        }
+        store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
+                         valid);
+        store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+      }
+      }
+      __syncwarp();
+    }
+  }
 }
 
 template <int BN, int A_MN, int B_MN>
@@ -240,96 +341,7 @@ __global__ void __launch_bounds__(256, 1)
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (ep.epi == EPI_ROPE) {
-        const int d = ep.rope_d, d2 = d >> 1;
-        int64_t pos = 0;
-        if (row_ok) {
-          const int64_t r = row;
-          pos = (r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg);
-        }
-        for (int hs = 0; hs < BN; hs += d) {
-          for (int j0 = 0; j0 < d2; j0 += 32) {
-            uint32_t r1[32], r2[32];
-            tmem_ld32(tbase + hs + j0, r1);
-            tmem_ld32(tbase + hs + j0 + d2, r2);
-            tmem_ld_wait();
-            const int c1 = n0 + hs + j0;
-            if (row_ok && c1 < N) {
-            float v1[32], v2[32];
-            const int within = (n0 + hs) % (3 * ep.rope_hq);
-            if (within < 2 * ep.rope_hq) {
-              const float2* cs = ep.rope + pos * d2 + j0;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float2 c = cs[i];
-                const float a = __uint_as_float(r1[i]), b = __uint_as_float(r2[i]);
-                v1[i] = a * c.x - b * c.y;
-                v2[i] = a * c.y + b * c.x;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                v1[i] = __uint_as_float(r1[i]);
-                v2[i] = __uint_as_float(r2[i]);
-              }
-            }
-            __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C);
-            store_row32_bf16(C + out_offset(ep, row, c1), v1, 32);
-            store_row32_bf16(C + out_offset(ep, row, c1 + d2), v2, 32);
-            }
-            __syncwarp();
-          }
-        }
-      } else {
-        for (int cc = 0; cc < BN; cc += 32) {
-          uint32_t r[32];
-          tmem_ld32(tbase + cc, r);
-          tmem_ld_wait();
-          const int col = n0 + cc;
-          if (row_ok && col < N) {
-          const int valid = min(32, N - col);
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (ep.epi == EPI_BF16) {
-            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
-                             valid);
-          } else if (ep.epi == EPI_F32_ACC || ep.epi == EPI_F32) {
-            float4* c4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.C) + out_offset(ep, row, col));
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              if (e * 4 < valid) {
-                float4 o = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-                if (ep.epi == EPI_F32_ACC) {
-                  const float4 old = c4[e];
-                  o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-                }
-                c4[e] = o;
-              }
-            }
-          } else if (ep.epi == EPI_GELU) {
-            float g[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) g[i] = gelu_f(bf16_round(v[i]));
-            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
-                             valid);
-            store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
-          } else if (ep.epi == EPI_DGELU) {
-            float hh[32], g[32];
-            load_row32_bf16(ep.aux_in + (int64_t)row * ep.ld_aux + col, hh, valid);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              g[i] = gelu_f(hh[i]);
-              v[i] = v[i] * gelu_grad_f(hh[i]);
-            }
-            store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
-                             valid);
-            store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
-          }
-          }
-          __syncwarp();
-        }
-      }
+      epilogue_tile<BN>(ep, tbase, row, row_ok, n0, N);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -341,6 +353,149 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with one
+// tcgen05.mma (M = 256, N = 256, K = 16) issued by the leader.  Each CTA stages only
+// its half of A (128 rows) and its half of B (128 rows of N) per k-block, so every SM
+// reads 32 KB per stage instead of 48 KB for the same MMA work; each CTA's TMEM holds
+// its 128 rows of the accumulator and its own epilogue warps drain them.
+template <int A_MN, int B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm2_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int M, int N, int K, RowMap amap, RowMap bmap, EpiParams ep) {
+  constexpr int STAGES = 6;
+  constexpr int HALF = 128 * BK * 2;           // 16 KB: one operand half per stage
+  constexpr int STAGE = 2 * HALF;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int mt = (M + 255) / 256;
+  const int nt = (N + 255) / 256;
+  const int ntiles = mt * nt;
+  const int nkb = (K + BK - 1) / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        int mb, nb;
+        tile_coords(t, mt, nt, mb, nb);
+        const int m0 = mb * 256 + rank * 128, n0 = nb * 256 + rank * 128;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE;
+          uint8_t* sb = sa + HALF;
+          const uint32_t fb = mapa_u32(&full_bar[stage], 0);    // the leader's barrier
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE);
+          const int k0 = kb * BK;
+          if (A_MN) {
+            const int kr = amap.map(k0);
+            tma_load_2d_2sm(sa, &tmA, fb, m0, kr);
+            tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, kr);
+          } else {
+            tma_load_2d_2sm(sa, &tmA, fb, k0, amap.map(m0));
+          }
+          if (B_MN) {
+            const int kr = bmap.map(k0);
+            tma_load_2d_2sm(sb, &tmB, fb, n0, kr);
+            tma_load_2d_2sm(sb + 8192, &tmB, fb, n0 + 64, kr);
+          } else {
+            tma_load_2d_2sm(sb, &tmB, fb, k0, bmap.map(n0));
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, 256, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * STAGE);
+            const uint32_t sb = sa + HALF;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              uint64_t ad, bd;
+              if (A_MN) ad = umma_desc_sw128(sa + k * 2048, 8192, 1024);
+              else      ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+              if (B_MN) bd = umma_desc_sw128(sb + k * 2048, 8192, 1024);
+              else      bd = umma_desc_sw128(sb + k * 32, 16, 1024);
+              umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+            umma_commit_2sm_mc(&empty_bar[stage], 0x3);
+            if (kb == nkb - 1) umma_commit_2sm_mc(&tfull_bar[acc], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      int mb, nb;
+      tile_coords(t, mt, nt, mb, nb);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + rank * 128 + q * 32 + lane;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+      epilogue_tile<256>(ep, tbase, row, row < M, nb * 256, N);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_u32(&tempty_bar[acc], 0));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, 512);
   }
 }
 
@@ -408,6 +563,41 @@ static int launch_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
+template <int A_MN, int B_MN>
+static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
+  constexpr int SMEM = 6 * 32768 + 1024 + 256;
+  CUtensorMap ta, tb;
+  int rc;
+  const int64_t a_rows = g.a_rows > 0 ? g.a_rows : (A_MN ? g.K : g.M);
+  const int64_t b_rows = g.b_rows > 0 ? g.b_rows : (B_MN ? g.K : g.N);
+  if (A_MN) rc = make_map(&ta, g.A, g.M, a_rows, g.lda, 64, 64);
+  else      rc = make_map(&ta, g.A, g.K, a_rows, g.lda, 64, 128);
+  if (rc) return rc;
+  if (B_MN) rc = make_map(&tb, g.B, g.N, b_rows, g.ldb, 64, 64);
+  else      rc = make_map(&tb, g.B, g.K, b_rows, g.ldb, 64, 128);
+  if (rc) return rc;
+  auto kern = gemm2_tc_kernel<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr_set = true;
+  }
+  const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const int ncl = std::min(tiles, gemm_num_sms() / 2);
+  RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
+  RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
+  kern<<<2 * ncl, 256, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep);
+  return (int)cudaGetLastError();
+}
+
+static int pair_mode() {
+  static int v = [] {
+    const char* e = getenv("PDS_GEMM_PAIR");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return 0;
   if (g.N % 8 || (g.blk_w % 32)) return (int)cudaErrorInvalidValue;
@@ -429,6 +619,18 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   const int64_t tiles256 = (int64_t)((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
   bool use256 = (g.N % 256 == 0 || g.N > 1024) && tiles256 >= gemm_num_sms();
   if (g.epi == EPI_ROPE && (g.rope_d % 64 || 128 % g.rope_d)) return (int)cudaErrorInvalidValue;
+  const int64_t pair_tiles = (int64_t)((g.M + 255) / 256) * ((g.N + 255) / 256);
+  const bool pair_ok = pair_mode() && g.M >= 256 && (g.N % 256 == 0 || g.N > 1024) &&
+                       pair_tiles >= gemm_num_sms() / 2 && (g.a_seg == 0 || g.a_seg % 128 == 0) &&
+                       (g.b_seg == 0 || g.b_seg % 128 == 0);
+  if (pair_ok) {
+    switch ((g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0)) {
+      case 0: return launch2_t<0, 0>(g, ep, st);
+      case 1: return launch2_t<0, 1>(g, ep, st);
+      case 2: return launch2_t<1, 0>(g, ep, st);
+      default: return launch2_t<1, 1>(g, ep, st);
+    }
+  }
   const int key = (use256 ? 4 : 0) | (g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0);
   switch (key) {
     case 0: return launch_t<128, 0, 0>(g, ep, st);

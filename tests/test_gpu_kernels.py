@@ -25,7 +25,7 @@ def _mat(seed, tid, shape, std=1.0):
 
 
 GEMM_SHAPES = [(256, 384, 256), (200, 392, 200), (128, 128, 64), (1024, 768, 512), (4096, 4096, 512),
-               (344, 1536, 4096)]
+               (344, 1536, 4096), (2368, 2048, 320), (4096, 1536, 4096)]
 
 
 @pytest.mark.parametrize("a_mn", [0, 1])
