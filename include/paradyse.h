@@ -112,6 +112,10 @@ pds_status pds_destroy(pds_ctx* ctx);
  * strategies in strategy_mask (bit i = strategy i); otherwise grown on demand. */
 pds_status pds_reserve(pds_ctx* ctx, int64_t max_seq_len, uint32_t strategy_mask);
 
+/* Free the context's cached device memory (idle saved-arena blocks, workspace) so a
+ * following call starts from an empty pool.  Live pds_saved sets are untouched. */
+pds_status pds_release_cache(pds_ctx* ctx);
+
 /* ------------------------------------------------------------------ planner (host only) */
 /* Load a calibrated cost bundle (text, "pds_bundle 1" format, see DESIGN.md §Cost
  * bundle): per strategy an exported random forest (RF, interpolation) and an AIC-

@@ -95,6 +95,7 @@ _SIGS = {
     "pds_create_loopback": [C.POINTER(_Model), C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)],
     "pds_destroy": [C.c_void_p],
     "pds_reserve": [C.c_void_p, C.c_int64, C.c_uint32],
+    "pds_release_cache": [C.c_void_p],
     "pds_load_costs": [C.c_void_p, C.c_char_p],
     "pds_set_capacity": [C.c_void_p, C.c_double, C.c_double],
     "pds_set_enabled": [C.c_void_p, C.c_uint32],
@@ -219,6 +220,9 @@ class Context:
 
     def reserve(self, max_seq_len, mask=0x7):
         call("pds_reserve", self.h, max_seq_len, mask)
+
+    def release_cache(self):
+        call("pds_release_cache", self.h)
 
     def load_costs(self, path):
         call("pds_load_costs", self.h, path.encode())

@@ -87,10 +87,11 @@ __global__ void __launch_bounds__(128)
                        const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ g,
                        const __nv_bfloat16* __restrict__ dres, int64_t rows, int h,
                        __nv_bfloat16* __restrict__ dx, float* __restrict__ dg_part) {
-  extern __shared__ float sdg[];
-  for (int i = threadIdx.x; i < h; i += blockDim.x) sdg[i] = 0.f;
+  extern __shared__ float sdg_all[];   // [4 warps][h]
+  for (int i = threadIdx.x; i < 4 * h; i += blockDim.x) sdg_all[i] = 0.f;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  float* sdg = sdg_all + (threadIdx.x >> 5) * h;
   const uint4* gr = reinterpret_cast<const uint4*>(g);
   for (int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5); row < rows;
        row += (int64_t)gridDim.x * 4) {
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(128)
       for (int e = 0; e < 8; ++e) {
         xh[e] *= r;
         dot += d8[e] * gg[e] * xh[e];
-        atomicAdd(&sdg[c * 8 + e], d8[e] * xh[e]);
+        sdg[c * 8 + e] += d8[e] * xh[e];
       }
     }
     dot = warp_sum(dot) / (float)h;
@@ -133,16 +134,27 @@ __global__ void __launch_bounds__(128)
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < h; i += blockDim.x) dg_part[(int64_t)blockIdx.x * h + i] = sdg[i];
+  for (int i = threadIdx.x; i < h; i += blockDim.x)
+    dg_part[(int64_t)blockIdx.x * h + i] = sdg_all[i] + sdg_all[h + i] + sdg_all[2 * h + i] + sdg_all[3 * h + i];
 }
 
-__global__ void reduce_rows_add_kernel(const float* __restrict__ part, int nparts, int h,
-                                       float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= h) return;
+// out[i] += sum_p part[p][i]: 32 columns per block, 8 row groups, smem tree
+__global__ void __launch_bounds__(256)
+    reduce_rows_add_kernel(const float* __restrict__ part, int nparts, int h, float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int g = threadIdx.x >> 5;
   float acc = 0.f;
-  for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * h + i];
-  out[i] += acc;
+  if (c < h)
+    for (int p = g; p < nparts; p += 8) acc += part[(int64_t)p * h + c];
+  red[g][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (g == 0 && c < h) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][threadIdx.x];
+    out[c] += t;
+  }
 }
 
 // u = x * rstd * g  (recompute of a normalised activation from saved x, rstd)
@@ -291,9 +303,14 @@ int rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g, 
   auto G = reinterpret_cast<const __nv_bfloat16*>(g);
   auto DR = reinterpret_cast<const __nv_bfloat16*>(dres);
   auto DX = reinterpret_cast<__nv_bfloat16*>(dx);
-  const size_t smem = (size_t)h * sizeof(float);
+  const size_t smem = (size_t)4 * h * sizeof(float);
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(rmsnorm_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4096 * 4);
+    once = true;
+  }
   PDS_VPL_DISPATCH(h, rmsnorm_bwd_kernel, (grid, 128, smem, st), (DU, X, RS, G, DR, rows, h, DX, dg_part));
-  reduce_rows_add_kernel<<<(h + 255) / 256, 256, 0, st>>>(dg_part, grid, h, dg);
+  reduce_rows_add_kernel<<<(h + 31) / 32, 256, 0, st>>>(dg_part, grid, h, dg);
   return (int)cudaGetLastError();
 }
 

@@ -649,6 +649,18 @@ extern "C" pds_status pds_reserve(pds_ctx* c, int64_t max_seq_len, uint32_t mask
   return ensure_rope(c, max_seq_len, 0);
 }
 
+extern "C" pds_status pds_release_cache(pds_ctx* c) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  PDS_CUDA(cudaSetDevice(c->device));
+  PDS_CUDA(cudaDeviceSynchronize());
+  for (auto& kv : c->free_blocks) cudaFree(kv.second);
+  c->free_blocks.clear();
+  if (c->ws) cudaFree(c->ws);
+  c->ws = nullptr;
+  c->ws_cap = 0;
+  return PDS_OK;
+}
+
 extern "C" pds_status pds_debug_taps(pds_ctx* c, void* o_out, void* z_out) {
   if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
   c->tap_o = o_out;
