@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ptx.cuh"
 
@@ -760,6 +761,219 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ---------------------------------------------------------------- dQ, two query tiles
+// CTA = (256 queries = tiles 0 and 1, head); 64-key blocks staged once for both tiles.
+// TMEM per tile t: S_t (64) | dP_t (64) | dQ_t (128) at column 256 t.  MMA order per
+// block j: S/dP_0(j), S/dP_1(j), dQ_0(j), S/dP_0(j+1), dQ_1(j), S/dP_1(j+1), ... so one
+// tile's elementwise pass overlaps the other tile's MMAs.  Because one thread's
+// tcgen05 MMAs execute in order, S_t(j+1) completing implies dQ_t(j) finished reading
+// dS_t, so the elementwise warps may overwrite dS_t as soon as S_t(j+1) is ready.
+template <int D>
+struct BwdQ2Cfg {
+  static constexpr int QT = 128 * D * 2;
+  static constexpr int KT = 64 * D * 2;
+  static constexpr int Q_OFF = 0;               // Q0, Q1
+  static constexpr int O_OFF = 2 * QT;          // dO0, dO1
+  static constexpr int K_OFF = 4 * QT;          // [2 stages]
+  static constexpr int V_OFF = K_OFF + 2 * KT;  // [2 stages]
+  static constexpr int S_OFF = V_OFF + 2 * KT;  // dS_0, dS_1 [128][64]
+  static constexpr int BAR_OFF = S_OFF + 2 * 16384;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq2_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
+                           const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
+                           const float* __restrict__ Dd, int s, int heads, int causal,
+                           __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
+                           float scale, float scale_log2) {
+  using C = BwdQ2Cfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;    // [2]
+  uint64_t* kv_empty = bar + 3;   // [2]
+  uint64_t* sd_full = bar + 5;    // [2] per tile
+  uint64_t* ds_full = bar + 7;    // [2] per tile
+  uint64_t* fin = bar + 9;        // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = (s + 255) / 256;
+  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int head = blockIdx.y;
+  const int hq = heads * D;
+  const int q0 = qb * 256;
+  const int nk[2] = {causal ? min(s, q0 + 128) / 64 : s / 64, causal ? min(s, q0 + 256) / 64 : s / 64};
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tdo);
+    tma_prefetch(&tkv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ds_full[i], 4);
+      mbar_init(&fin[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, 4 * C::QT);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::Q_OFF + t * C::QT + a * 16384, &tq, q_full, head * D + a * 64, q0 + 128 * t);
+          tma_load_2d(sm + C::O_OFF + t * C::QT + a * 16384, &tdo, q_full, head * D + a * 64, q0 + 128 * t);
+        }
+      for (int j = 0; j < nk[1]; ++j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(&kv_empty[b], ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
+          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
+    mbar_wait(q_full, 0);
+    int kv_ready = -1;
+    auto need_kv = [&](int j) {
+      if (kv_ready < j) {
+        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        kv_ready = j;
+      }
+    };
+    auto issue_sd = [&](int t, int j) {
+      need_kv(j);
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(sm + C::Q_OFF + t * C::QT), so = smem_u32(sm + C::O_OFF + t * C::QT);
+        const uint32_t sk = smem_u32(sm + C::K_OFF + (j & 1) * C::KT), sv = smem_u32(sm + C::V_OFF + (j & 1) * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16(tmem + t * 256, kmaj_desc(sq, kk), kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
+          umma_f16(tmem + t * 256 + 64, kmaj_desc(so, kk), kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
+        }
+        umma_commit(&sd_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_dq = [&](int t, int j) {
+      mbar_wait(&ds_full[t], j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sd = smem_u32(sm + C::S_OFF + t * 16384), sk = smem_u32(sm + C::K_OFF + (j & 1) * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16(tmem + t * 256 + 128, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
+      }
+      __syncwarp();
+    };
+    if (nk[0] > 0) issue_sd(0, 0);
+    issue_sd(1, 0);
+    for (int j = 0; j < nk[1]; ++j) {
+      if (j < nk[0]) {
+        issue_dq(0, j);
+        if (j + 1 < nk[0]) issue_sd(0, j + 1);
+        else if (elect_one()) umma_commit(&fin[0]);
+        __syncwarp();
+      }
+      issue_dq(1, j);
+      if (elect_one()) umma_commit(&kv_empty[j & 1]);
+      __syncwarp();
+      if (j + 1 < nk[1]) issue_sd(1, j + 1);
+      else if (elect_one()) umma_commit(&fin[1]);
+      __syncwarp();
+    }
+    if (nk[0] == 0 && elect_one()) umma_commit(&fin[0]);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int tile = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int row = q0 + tile * 128 + t;
+    const bool ok = row < s;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + tile * 256;
+    const float l2 = ok ? lse[(int64_t)head * s + row] * LOG2E : 0.f;
+    const float dd = ok ? Dd[(int64_t)head * s + row] : 0.f;
+    uint8_t* DS = sm + C::S_OFF + tile * 16384;
+    for (int j = 0; j < nk[tile]; ++j) {
+      const int k0 = j * 64;
+      mbar_wait(&sd_full[tile], j & 1);
+      tc_fence_after();
+      const bool mask = causal && (k0 + 63 > q0 + tile * 128);
+      uint32_t sr[32], dr[32], sr2[32], dr2[32];
+      tmem_ld32(lb + 0, sr);
+      tmem_ld32(lb + 64, dr);
+      tmem_ld32(lb + 32, sr2);
+      tmem_ld32(lb + 96, dr2);
+      tmem_ld_wait();
+      uint32_t dk[2][16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float s0 = __uint_as_float(c ? sr2[e] : sr[e]), s1 = __uint_as_float(c ? sr2[e + 1] : sr[e + 1]);
+          const float g0 = __uint_as_float(c ? dr2[e] : dr[e]), g1 = __uint_as_float(c ? dr2[e + 1] : dr[e + 1]);
+          float p0 = exp2f(fmaf(s0, scale_log2, -l2));
+          float p1 = exp2f(fmaf(s1, scale_log2, -l2));
+          if (mask) {
+            if (k0 + c * 32 + e > row) p0 = 0.f;
+            if (k0 + c * 32 + e + 1 > row) p1 = 0.f;
+          }
+          dk[c][e >> 1] = pack_bf16(p0 * (g0 - dd), p1 * (g1 - dd));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          st_sw128(DS, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[tile]);
+    }
+    mbar_wait(&fin[tile], 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(lb + 128 + c * 32, ra);
+      tmem_ld32(lb + 128 + c * 32 + D / 2, rb);
+      tmem_ld_wait();
+      float a[32], bb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
+      if (ok) {
+        rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
+        store32_bf16(rowp + c * 32, a);
+        store32_bf16(rowp + c * 32 + D / 2, bb);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -831,6 +1045,7 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   if (!once) {
     cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKVCfg<D>::SMEM);
     cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQCfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dq2_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ2Cfg<D>::SMEM);
     once = true;
   }
   const float scale = 1.0f / sqrtf((float)D);
@@ -838,9 +1053,18 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdKVCfg<D>::SMEM, st>>>(
       kv128, q64, do64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
       reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
-  attn_bwd_dq_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdQCfg<D>::SMEM, st>>>(
-      q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-      reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  static const bool dq1 = [] {
+    const char* e = getenv("PDS_ATTN_DQ");
+    return e && e[0] == '1';
+  }();
+  if (dq1)
+    attn_bwd_dq_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdQCfg<D>::SMEM, st>>>(
+        q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  else
+    attn_bwd_dq2_tc_kernel<D><<<dim3((s + 255) / 256, heads), 384, BwdQ2Cfg<D>::SMEM, st>>>(
+        q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
   return (int)cudaGetLastError();
 }
 

@@ -68,6 +68,10 @@ def main():
         for s in lens:
             if fixed is None:
                 plan, flags = ctx.plan(s, a.L)
+                if flags & B.PLAN_INFEASIBLE:      # proactive OOM prediction
+                    oom_at = s
+                    recs.append({"s": s, "oom": True, "predicted": True})
+                    break
             else:
                 plan, flags = [fixed] * a.L, 0
             try:
