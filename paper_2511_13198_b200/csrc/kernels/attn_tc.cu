@@ -62,6 +62,13 @@ __device__ __forceinline__ uint64_t mnmaj_desc(uint32_t tile, int kk, uint32_t a
   return umma_desc_sw128(tile + kk * 2048, atom, 1024);
 }
 
+// 2^x on the MUFU unit, flush-to-zero (P is rounded to bf16 anyway)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // 2^x for x <= 0 on the FMA pipe (Cody-Waite split + degree-3 minimax on [-0.5, 0.5],
 // max relative error 7.5e-5 — far below the bf16 rounding of P).  Used for a share of
 // the softmax exponentials so the MUFU (ex2) unit is not the bottleneck.
@@ -218,30 +225,31 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const int k0 = j * BN;
       const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
-      // pass 1: row max with 8 independent accumulators, two TMEM loads per wait
-      float mxa[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mxa[i] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < BN / 32; c += 2) {
-        uint32_t r[32], r2[32];
-        tmem_ld32(lb + s_col + c * 32, r);
-        tmem_ld32(lb + s_col + c * 32 + 32, r2);
+      // pass 1: row max; 16-column TMEM loads software-pipelined (next chunk in flight)
+      float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      {
+        uint32_t cur[16], nxt[16];
+        tmem_ld16(lb + s_col, cur);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float v = __uint_as_float(r[i]), w = __uint_as_float(r2[i]);
-          if (mask && k0 + c * 32 + i > row) v = -INFINITY;
-          if (mask && k0 + c * 32 + 32 + i > row) w = -INFINITY;
-          mxa[i & 7] = fmaxf(mxa[i & 7], fmaxf(v, w));
+        for (int c = 0; c < BN / 16; ++c) {
+          if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float v = __uint_as_float(cur[i]);
+            if (mask && k0 + c * 16 + i > row) v = -INFINITY;
+            mxa[i & 3] = fmaxf(mxa[i & 3], v);
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
         }
       }
-      const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
-                             fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
+      const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
       const float m_new = mx * scale_log2;
       const bool need = m_new > m_used + 8.0f;
       if (j > 0 && __any_sync(0xffffffff, need)) {
-        const float f = need ? exp2f(m_used - m_new) : 1.0f;
+        const float f = need ? ex2(m_used - m_new) : 1.0f;
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           uint32_t r[32];
@@ -255,34 +263,36 @@ __global__ void __launch_bounds__(384, 1)
         if (need) l *= f;
       }
       if (need) m_used = m_new;
-      // pass 2: p = exp2(s scale - m), 4 independent row-sum accumulators
+      // pass 2: p = exp2(s scale - m) (1 in 4 on the FMA pipe), bf16-packed P written
+      // back into the consumed S columns (chunk c of 16 keys -> 8 packed columns at 8c)
       float rsa[4] = {0.f, 0.f, 0.f, 0.f};
       const float neg_m = -m_used;
-#pragma unroll
-      for (int c = 0; c < BN / 32; c += 2) {
-        uint32_t r[32], r2[32];
-        tmem_ld32(lb + s_col + c * 32, r);
-        tmem_ld32(lb + s_col + c * 32 + 32, r2);
+      {
+        uint32_t cur[16], nxt[16];
+        tmem_ld16(lb + s_col, cur);
         tmem_ld_wait();
-        uint32_t pk[16], pk2[16];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = exp2f(fmaf(__uint_as_float(r[i]), scale_log2, neg_m));
-          float p1 = exp2f(fmaf(__uint_as_float(r[i + 1]), scale_log2, neg_m));
-          float p2 = exp2f(fmaf(__uint_as_float(r2[i]), scale_log2, neg_m));
-          float p3 = exp2_fma(fmaf(__uint_as_float(r2[i + 1]), scale_log2, neg_m));
-          if (mask) {
-            if (k0 + c * 32 + i > row) p0 = 0.f;
-            if (k0 + c * 32 + i + 1 > row) p1 = 0.f;
-            if (k0 + c * 32 + 32 + i > row) p2 = 0.f;
-            if (k0 + c * 32 + 32 + i + 1 > row) p3 = 0.f;
+        for (int c = 0; c < BN / 16; ++c) {
+          if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const float x0 = fmaf(__uint_as_float(cur[i]), scale_log2, neg_m);
+            const float x1 = fmaf(__uint_as_float(cur[i + 1]), scale_log2, neg_m);
+            float p0 = ex2(x0);
+            float p1 = (i & 2) ? exp2_fma(x1) : ex2(x1);
+            if (mask) {
+              if (k0 + c * 16 + i > row) p0 = 0.f;
+              if (k0 + c * 16 + i + 1 > row) p1 = 0.f;
+            }
+            rsa[(i >> 1) & 3] += p0 + p1;
+            pk[i >> 1] = pack_bf16(p0, p1);
           }
-          rsa[(i >> 1) & 3] += (p0 + p1) + (p2 + p3);
-          pk[i >> 1] = pack_bf16(p0, p1);
-          pk2[i >> 1] = pack_bf16(p2, p3);
+          tmem_st8(lb + s_col + c * 8, pk);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
         }
-        tmem_st16(lb + s_col + c * 16, pk);     // P chunk c -> packed bf16 columns 16c..16c+15
-        tmem_st16(lb + s_col + c * 16 + 16, pk2);
       }
       l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
       tmem_st_wait();
@@ -490,25 +500,34 @@ __global__ void __launch_bounds__(256, 1)
       const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + 512 + b * 256);
       const bool mask = causal && (q0 < k0 + 128);
       uint32_t pk[2][16], dk[2][16];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(lb + ST_COL + b * 64 + c * 32, sr);
-        tmem_ld32(lb + DP_COL + b * 64 + c * 32, dr);
+      {
+        uint32_t cs[16], cd[16], ns[16], nd[16];
+        tmem_ld16(lb + ST_COL + b * 64, cs);
+        tmem_ld16(lb + DP_COL + b * 64, cd);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -L[c * 32 + e] * LOG2E));
-          const float x1 = fmaf(__uint_as_float(sr[e + 1]), scale_log2, -L[c * 32 + e + 1] * LOG2E);
-          float p1 = exp2f(x1);
-          if (mask) {
-            if (key > q0 + c * 32 + e) p0 = 0.f;
-            if (key > q0 + c * 32 + e + 1) p1 = 0.f;
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) {
+            tmem_ld16(lb + ST_COL + b * 64 + (c + 1) * 16, ns);
+            tmem_ld16(lb + DP_COL + b * 64 + (c + 1) * 16, nd);
           }
-          const float d0 = p0 * (__uint_as_float(dr[e]) - Dv[c * 32 + e]);
-          const float d1 = p1 * (__uint_as_float(dr[e + 1]) - Dv[c * 32 + e + 1]);
-          pk[c][e >> 1] = pack_bf16(p0, p1);
-          dk[c][e >> 1] = pack_bf16(d0, d1);
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const int qi = c * 16 + e;
+            float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -L[qi] * LOG2E));
+            float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -L[qi + 1] * LOG2E));
+            if (mask) {
+              if (key > q0 + qi) p0 = 0.f;
+              if (key > q0 + qi + 1) p1 = 0.f;
+            }
+            const float d0 = p0 * (__uint_as_float(cd[e]) - Dv[qi]);
+            const float d1 = p1 * (__uint_as_float(cd[e + 1]) - Dv[qi + 1]);
+            pk[c >> 1][(c & 1) * 8 + (e >> 1)] = pack_bf16(p0, p1);
+            dk[c >> 1][(c & 1) * 8 + (e >> 1)] = pack_bf16(d0, d1);
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) { cs[i] = ns[i]; cd[i] = nd[i]; }
         }
       }
       tc_fence_before();
@@ -712,9 +731,9 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          float p0 = exp2f(fmaf(__uint_as_float(sr[e]), scale_log2, -l2));
+          float p0 = ex2(fmaf(__uint_as_float(sr[e]), scale_log2, -l2));
           const float x1 = fmaf(__uint_as_float(sr[e + 1]), scale_log2, -l2);
-          float p1 = exp2f(x1);
+          float p1 = ex2(x1);
           if (mask) {
             if (k0 + c * 32 + e > row) p0 = 0.f;
             if (k0 + c * 32 + e + 1 > row) p1 = 0.f;
@@ -915,26 +934,33 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&sd_full[tile], j & 1);
       tc_fence_after();
       const bool mask = causal && (k0 + 63 > q0 + tile * 128);
-      uint32_t sr[32], dr[32], sr2[32], dr2[32];
-      tmem_ld32(lb + 0, sr);
-      tmem_ld32(lb + 64, dr);
-      tmem_ld32(lb + 32, sr2);
-      tmem_ld32(lb + 96, dr2);
-      tmem_ld_wait();
+      // S and dP rows in 16-key chunks, next chunk's loads in flight while processing
       uint32_t dk[2][16];
+      {
+        uint32_t cs[16], cd[16], ns[16], nd[16];
+        tmem_ld16(lb + 0, cs);
+        tmem_ld16(lb + 64, cd);
+        tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float s0 = __uint_as_float(c ? sr2[e] : sr[e]), s1 = __uint_as_float(c ? sr2[e + 1] : sr[e + 1]);
-          const float g0 = __uint_as_float(c ? dr2[e] : dr[e]), g1 = __uint_as_float(c ? dr2[e + 1] : dr[e + 1]);
-          float p0 = exp2f(fmaf(s0, scale_log2, -l2));
-          float p1 = exp2f(fmaf(s1, scale_log2, -l2));
-          if (mask) {
-            if (k0 + c * 32 + e > row) p0 = 0.f;
-            if (k0 + c * 32 + e + 1 > row) p1 = 0.f;
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) {
+            tmem_ld16(lb + (c + 1) * 16, ns);
+            tmem_ld16(lb + 64 + (c + 1) * 16, nd);
           }
-          dk[c][e >> 1] = pack_bf16(p0 * (g0 - dd), p1 * (g1 - dd));
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -l2));
+            float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -l2));
+            if (mask) {
+              if (k0 + c * 16 + e > row) p0 = 0.f;
+              if (k0 + c * 16 + e + 1 > row) p1 = 0.f;
+            }
+            dk[c >> 1][(c & 1) * 8 + (e >> 1)] =
+                pack_bf16(p0 * (__uint_as_float(cd[e]) - dd), p1 * (__uint_as_float(cd[e + 1]) - dd));
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) { cs[i] = ns[i]; cd[i] = nd[i]; }
         }
       }
 #pragma unroll
