@@ -62,17 +62,19 @@ def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
     hl, Fl = h // P, ffn // P
     small = _al(2 * h * 4)
     if pi == TS:
-        bufs = [s * h * 2, s * h * 2, s * Fl * 2, s * Fl * 2, lam, _norm_bwd_grid(sl) * h * 4]
+        bufs = [s * h * 2, s * h * 2, s * Fl * 2, s * Fl * 2, lam, _norm_bwd_grid(sl) * h * 4,
+                max(Fl, 3 * hl) * s * 2, h * s * 2, h * max(Fl, 3 * hl) * 2]
     elif pi == UZ:
         bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
                 u, 3 * u, 3 * u, sl * ffn * 2, sl * ffn * 2, 3 * u, 3 * u, u, lam,
-                _norm_bwd_grid(sl) * h * 4]
+                _norm_bwd_grid(sl) * h * 4, max(ffn, 3 * h) * sl * 2, h * sl * 2, h * max(ffn, 3 * h) * 2]
     elif pi == METP:
         c = metp_chunks or P
         w = sl // c
         uw = w * h * 2
         bufs = [u, u, P * uw, P * uw, P * uw, P * w * Fl * 2, P * w * Fl * 2, P * w * Fl * 2,
-                s * hl * 2, s * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4]
+                s * hl * 2, s * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4,
+                max(Fl, 3 * hl) * P * w * 2, h * P * w * 2, h * max(Fl, 3 * hl) * 2]
     else:
         raise KeyError(pi)
     return sum(_al(x) for x in bufs) + small

@@ -420,17 +420,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           const uint32_t fb = mapa_u32(&full_bar[stage], 0);    // the leader's barrier
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE);
           const int k0 = kb * BK;
-          if (A_MN) {
-            const int kr = amap.map(k0);
-            tma_load_2d_2sm(sa, &tmA, fb, m0, kr);
-            tma_load_2d_2sm(sa + 8192, &tmA, fb, m0 + 64, kr);
+          if (A_MN) {   // one 3-D box = both 64-wide MN groups (dims: elem, K row, MN group)
+            tma_load_3d_2sm(sa, &tmA, fb, 0, amap.map(k0), m0 >> 6);
           } else {
             tma_load_2d_2sm(sa, &tmA, fb, k0, amap.map(m0));
           }
           if (B_MN) {
-            const int kr = bmap.map(k0);
-            tma_load_2d_2sm(sb, &tmB, fb, n0, kr);
-            tma_load_2d_2sm(sb + 8192, &tmB, fb, n0 + 64, kr);
+            tma_load_3d_2sm(sb, &tmB, fb, 0, bmap.map(k0), n0 >> 6);
           } else {
             tma_load_2d_2sm(sb, &tmB, fb, k0, bmap.map(n0));
           }
@@ -526,6 +522,20 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// 3-D view of an MN-major operand: (64 elements, K rows, MN/64 groups), box (64, 64, 2)
+static int make_map_mn3(CUtensorMap* m, const void* base, uint64_t mn, uint64_t rows, uint64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[3] = {64, rows, mn / 64};
+  cuuint64_t strides[2] = {ld * 2, 128};
+  cuuint32_t box[3] = {64, 64, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
 int gemm_num_sms() {
   static int n = 0;
   if (!n) {
@@ -570,10 +580,10 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   int rc;
   const int64_t a_rows = g.a_rows > 0 ? g.a_rows : (A_MN ? g.K : g.M);
   const int64_t b_rows = g.b_rows > 0 ? g.b_rows : (B_MN ? g.K : g.N);
-  if (A_MN) rc = make_map(&ta, g.A, g.M, a_rows, g.lda, 64, 64);
+  if (A_MN) rc = make_map_mn3(&ta, g.A, g.M, a_rows, g.lda);
   else      rc = make_map(&ta, g.A, g.K, a_rows, g.lda, 64, 128);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&tb, g.B, g.N, b_rows, g.ldb, 64, 64);
+  if (B_MN) rc = make_map_mn3(&tb, g.B, g.N, b_rows, g.ldb);
   else      rc = make_map(&tb, g.B, g.K, b_rows, g.ldb, 64, 128);
   if (rc) return rc;
   auto kern = gemm2_tc_kernel<A_MN, B_MN>;
@@ -622,6 +632,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   const int64_t pair_tiles = (int64_t)((g.M + 255) / 256) * ((g.N + 255) / 256);
   const bool pair_ok = pair_mode() && g.M >= 256 && (g.N % 256 == 0 || g.N > 1024) &&
                        pair_tiles >= gemm_num_sms() / 2 && (g.a_seg == 0 || g.a_seg % 128 == 0) &&
+                       (!g.a_mn || g.M % 64 == 0) && (!g.b_mn || g.N % 64 == 0) &&
                        (g.b_seg == 0 || g.b_seg % 128 == 0);
   if (pair_ok) {
     switch ((g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0)) {

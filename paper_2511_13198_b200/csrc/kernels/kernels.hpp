@@ -18,6 +18,9 @@ int add_bf16(const void* a, const void* b, void* c, int64_t n, cudaStream_t st);
 int add_f32(const void* a, void* acc, int64_t n, cudaStream_t st);
 int sum_bf16_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st);
 int sum_f32_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st);
+// dst[c][r] = src[map(r)][c], map(r) = (r / seg) * stride + base + r % seg (seg = 0: identity)
+int transpose_bf16(const void* src, int64_t ld_src, int64_t rows, int64_t cols, void* dst, int64_t ld_dst,
+                   int64_t seg, int64_t stride, int64_t base, cudaStream_t st);
 int rope_table(void* t, int64_t n_pos, int d, double theta, cudaStream_t st);
 // dst[t][j*cw + c] = src[j][t][c]  (A2A receive buffer -> row-major columns), bf16
 int unpack_blocks(const void* src, int P, int64_t rows, int64_t cw, void* dst, int64_t ld_dst, cudaStream_t st);

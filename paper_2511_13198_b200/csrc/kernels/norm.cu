@@ -241,6 +241,50 @@ __global__ void unpack_blocks_kernel(const uint4* __restrict__ src, int P, int64
   }
 }
 
+// dst[c][r] = src[map(r)][c] for r < rows, c < cols (bf16); 64 x 64 tiles through
+// shared memory, 16-byte global loads and stores.  map(r) = (r / seg) * stride + base + r % seg
+// (METP waves read position-ordered buffers).  HBM-bound: 4 B per element.
+__global__ void __launch_bounds__(256)
+    transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
+                          uint16_t* __restrict__ dst, int64_t ld_dst, int64_t seg, int64_t stride, int64_t base) {
+  // 64 x 64 tile as 32-bit words (column pairs), row stride 33 words: the 16-byte
+  // loads are stored as 4 conflict-free 32-bit words; the transposed reads hit <= 2
+  // banks per word; two output vectors per thread are assembled with byte permutes.
+  __shared__ uint32_t tile[64][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int h2 = 0; h2 < 2; ++h2) {
+    const int rr = (t >> 3) + 32 * h2, v = t & 7;
+    const int64_t r = r0 + rr;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (r < rows && c0 + v * 8 < cols) {
+      const int64_t sr = (r / seg) * stride + base + (r % seg);
+      x = __ldcs(reinterpret_cast<const uint4*>(src + sr * ld_src + c0 + v * 8));
+    }
+    tile[rr][v * 4 + 0] = x.x;
+    tile[rr][v * 4 + 1] = x.y;
+    tile[rr][v * 4 + 2] = x.z;
+    tile[rr][v * 4 + 3] = x.w;
+  }
+  __syncthreads();
+  // thread -> column pair cp (dst rows c0 + 2cp, +1), source rows rb*8 .. +7
+  const int cp = t >> 3, rb = t & 7;
+  uint32_t w[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[i] = tile[rb * 8 + i][cp];
+  uint4 lo, hi;
+  lo.x = __byte_perm(w[0], w[1], 0x5410); hi.x = __byte_perm(w[0], w[1], 0x7632);
+  lo.y = __byte_perm(w[2], w[3], 0x5410); hi.y = __byte_perm(w[2], w[3], 0x7632);
+  lo.z = __byte_perm(w[4], w[5], 0x5410); hi.z = __byte_perm(w[4], w[5], 0x7632);
+  lo.w = __byte_perm(w[6], w[7], 0x5410); hi.w = __byte_perm(w[6], w[7], 0x7632);
+  const int64_t c = c0 + 2 * cp, rr0 = r0 + rb * 8;
+  if (rr0 < rows) {
+    if (c < cols) *reinterpret_cast<uint4*>(dst + c * ld_dst + rr0) = lo;
+    if (c + 1 < cols) *reinterpret_cast<uint4*>(dst + (c + 1) * ld_dst + rr0) = hi;
+  }
+}
+
 __global__ void rope_table_kernel(float2* __restrict__ t, int64_t n_pos, int d, double theta) {
   const int d2 = d / 2;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -366,6 +410,17 @@ int unpack_blocks(const void* src, int P, int64_t rows, int64_t cw, void* dst, i
   const int64_t n = (int64_t)P * rows * cw / 8;
   unpack_blocks_kernel<<<ew_grid(n), 256, 0, st>>>(reinterpret_cast<const uint4*>(src), P, rows, cw / 8,
                                                    reinterpret_cast<uint4*>(dst), ld_dst / 8);
+  return (int)cudaGetLastError();
+}
+
+int transpose_bf16(const void* src, int64_t ld_src, int64_t rows, int64_t cols, void* dst, int64_t ld_dst,
+                   int64_t seg, int64_t stride, int64_t base, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if (rows % 8 || cols % 8 || ld_src % 8 || ld_dst % 8) return (int)cudaErrorInvalidValue;
+  dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
+  transpose_bf16_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(src), ld_src, rows, cols,
+                                               reinterpret_cast<uint16_t*>(dst), ld_dst,
+                                               seg > 0 ? seg : ((int64_t)1 << 40), stride, base);
   return (int)cudaGetLastError();
 }
 

@@ -219,19 +219,55 @@ struct Exec {
 
 #define B16(p) (reinterpret_cast<char*>(p))
 
+// Every GEMM is issued TN (both operands K-major), the layout the tcgen05 GEMM runs
+// at full rate: weight operands that the math needs MN-major are transposed into
+// `wt` per call (weights are small), and the token-major activations of the dW
+// GEMMs (contraction over tokens) into `ta` / `tb`.
+struct TN {
+  Exec& e;
+  char *ta, *tb, *wt;
+  // C[M,N] (+)= A[M,K] B[N,K]^T with both operands K-major
+  pds_status mm(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M, int64_t N, int64_t K, void* C,
+                int64_t ldc, int epi = EPI_BF16) {
+    return e.gemm(Exec::G(A, lda, 0, B, ldb, 0, M, N, K, C, ldc, epi));
+  }
+  // X [rows][cols] (rows optionally remapped) -> dst [cols][rows]
+  pds_status tr(const void* X, int64_t ldx, int64_t rows, int64_t cols, void* dst, int64_t seg = 0,
+                int64_t stride = 0, int64_t base = 0) {
+    Prof p(e.c, e.st, K_NORM, 0, 4.0 * rows * cols);
+    return kerr(transpose_bf16(X, ldx, rows, cols, dst, rows, seg, stride, base, e.st), "transpose");
+  }
+  // C[M,N] += Xa^T Xb over T tokens: Xa [T][M], Xb [T][N] token-major (dW GEMM)
+  pds_status dw(const void* Xa, int64_t lda, const void* Xb, int64_t ldb, int64_t T, int64_t M, int64_t N, void* C,
+                int epi = EPI_F32_ACC, int64_t seg = 0, int64_t stride = 0, int64_t base = 0) {
+    PDS_TRY(tr(Xa, lda, T, M, ta, seg, stride, base));
+    PDS_TRY(tr(Xb, ldb, T, N, tb));
+    return mm(ta, T, tb, T, M, N, T, C, N, epi);
+  }
+  // C[M,N] = X[M,K] W[K,N] for a weight stored [K][N]: transpose W into wt [N][K]
+  pds_status xw(const void* X, int64_t ldx, const void* W, int64_t ldw, int64_t M, int64_t N, int64_t K, void* C,
+                int64_t ldc, int64_t aseg = 0, int64_t astride = 0, int64_t abase = 0, int64_t arows = 0) {
+    PDS_TRY(tr(W, ldw, K, N, wt));
+    GemmArgs g = Exec::G(X, ldx, 0, wt, K, 0, M, N, K, C, ldc);
+    g.a_seg = aseg; g.a_stride = astride; g.a_base = abase; g.a_rows = arows;
+    return e.gemm(g);
+  }
+};
+
 // ================================================================== MegatronTS
 pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
   const BufPlan& bp = sv->plan;
   char* gather = ws + bp.ws_off("gather");
   char* partial = ws + bp.ws_off("partial");
   char* f0 = ws + bp.ws_off("f0");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   const int64_t slot = e.r * e.sl * e.h * 2;
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, gather + slot, sv->at("rstd1")));
   PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u)
   PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
                         e.hl, 0, 0, 0)));                                                // Eq. 1 + RoPE
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));                          // Eq. 2
-  PDS_TRY(e.gemm(Exec::G(sv->at("a"), e.hl, 0, w->w_proj, e.h, 1, e.s, e.h, e.hl, partial, e.h)));  // Eq. 3
+  PDS_TRY(tn.xw(sv->at("a"), e.hl, w->w_proj, e.h, e.s, e.h, e.hl, partial, e.h));      // Eq. 3
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(o)
   PDS_TRY(e.tap(e.c->tap_o, partial + slot, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, partial + slot, w->g2, e.sl, sv->at("x1"), gather + slot, sv->at("rstd2")));
@@ -239,7 +275,7 @@ pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   GemmArgs fc1 = Exec::G(gather, e.h, 0, w->w_in_t, e.h, 0, e.s, e.Fl, e.h, sv->at("h"), e.Fl, EPI_GELU);
   fc1.aux_out = f0; fc1.ld_aux = e.Fl;
   PDS_TRY(e.gemm(fc1));                                                                 // Eq. 4 (GELU)
-  PDS_TRY(e.gemm(Exec::G(f0, e.Fl, 0, w->w_out, e.h, 1, e.s, e.h, e.Fl, partial, e.h)));
+  PDS_TRY(tn.xw(f0, e.Fl, w->w_out, e.h, e.s, e.h, e.Fl, partial, e.h));
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(z)
   PDS_TRY(e.tap(e.c->tap_z, partial + slot, e.sl * e.h));
   return e.add(sv->at("x1"), partial + slot, y, e.sl * e.h);
@@ -255,27 +291,28 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
   float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
   float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   const int64_t slot = e.r * e.sl * e.h * 2;
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
   PDS_TRY(e.ag(dy, gather, e.sl * e.h));                                                // AG(dz)
   GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
   dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.Fl;
   PDS_TRY(e.gemm(dgel));                                                                // dH, G
-  PDS_TRY(e.gemm(Exec::G(f0, e.Fl, 1, gather, e.h, 1, e.Fl, e.h, e.s, g->dw_out, e.h, EPI_F32_ACC)));
+  PDS_TRY(tn.dw(f0, e.Fl, gather, e.h, e.s, e.Fl, e.h, g->dw_out));                      // dW_out += G^T dZ
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, gather + slot));
   PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(v) re-gather
-  PDS_TRY(e.gemm(Exec::G(f1, e.Fl, 1, gather, e.h, 1, e.Fl, e.h, e.s, g->dw_in_t, e.h, EPI_F32_ACC)));
-  PDS_TRY(e.gemm(Exec::G(f1, e.Fl, 0, w->w_in_t, e.h, 1, e.s, e.h, e.Fl, partial, e.h)));
+  PDS_TRY(tn.dw(f1, e.Fl, gather, e.h, e.s, e.Fl, e.h, g->dw_in_t));                     // dW_in^T += dH^T V
+  PDS_TRY(tn.xw(f1, e.Fl, w->w_in_t, e.h, e.s, e.h, e.Fl, partial, e.h));               // dV = dH W_in^T
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(dv)
   PDS_TRY(e.norm_bwd(partial + slot, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
   PDS_TRY(e.ag(dx, gather, e.sl * e.h));                                                // AG(dx1)
-  PDS_TRY(e.gemm(Exec::G(gather, e.h, 0, w->w_proj, e.h, 0, e.s, e.hl, e.h, f1, e.hl)));  // dA
-  PDS_TRY(e.gemm(Exec::G(sv->at("a"), e.hl, 1, gather, e.h, 1, e.hl, e.h, e.s, g->dw_proj, e.h, EPI_F32_ACC)));
+  PDS_TRY(tn.mm(gather, e.h, w->w_proj, e.h, e.s, e.hl, e.h, f1, e.hl));                 // dA
+  PDS_TRY(tn.dw(sv->at("a"), e.hl, gather, e.h, e.s, e.hl, e.h, g->dw_proj));            // dW_proj += A^T dX1
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), f1, f0, dd));            // dQKV (RoPE^T)
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, gather + slot));
   PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u) re-gather
-  PDS_TRY(e.gemm(Exec::G(f0, 3 * e.hl, 1, gather, e.h, 1, 3 * e.hl, e.h, e.s, g->dw_qkv_t, e.h, EPI_F32_ACC)));
-  PDS_TRY(e.gemm(Exec::G(f0, 3 * e.hl, 0, w->w_qkv_t, e.h, 1, e.s, e.h, 3 * e.hl, partial, e.h)));
+  PDS_TRY(tn.dw(f0, 3 * e.hl, gather, e.h, e.s, 3 * e.hl, e.h, g->dw_qkv_t));           // dW_qkv^T += dQKV^T U
+  PDS_TRY(tn.xw(f0, 3 * e.hl, w->w_qkv_t, e.h, e.s, e.h, 3 * e.hl, partial, e.h));      // dU = dQKV W_qkv^T
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(du)
   PDS_TRY(e.norm_bwd(partial + slot, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
@@ -300,6 +337,7 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   char* s1 = ws + bp.ws_off("s1");
   char* r1 = ws + bp.ws_off("r1");
   char* f0 = ws + bp.ws_off("f0");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
   // local QKV for all heads, head-group-major columns, written straight into the A2A
   // send layout [P][s/P][3h/P]; RoPE at global positions r*s/P + t
@@ -314,13 +352,13 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
     Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * e.h);
     PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, e.hl, sv->at("afull"), e.h, e.st), "unpack"));
   }
-  PDS_TRY(e.gemm(Exec::G(sv->at("afull"), e.h, 0, wproj, e.h, 1, e.sl, e.h, e.h, u1, e.h)));  // O
+  PDS_TRY(tn.xw(sv->at("afull"), e.h, wproj, e.h, e.sl, e.h, e.h, u1, e.h));          // O
   PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), s1, sv->at("rstd2")));
   GemmArgs fc1 = Exec::G(s1, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
-  PDS_TRY(e.gemm(Exec::G(f0, e.F, 0, wout, e.h, 1, e.sl, e.h, e.F, u1, e.h)));          // Z
+  PDS_TRY(tn.xw(f0, e.F, wout, e.h, e.sl, e.h, e.F, u1, e.h));                          // Z
   PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * e.h));
   return e.add(sv->at("x1"), u1, y, e.sl * e.h);
 }
@@ -353,22 +391,23 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
   float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
   float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
   GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
   dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.F;
   PDS_TRY(e.gemm(dgel));
-  PDS_TRY(e.gemm(Exec::G(f0, e.F, 1, dy, e.h, 1, e.F, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(tn.dw(f0, e.F, dy, e.h, e.sl, e.F, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
-  PDS_TRY(e.gemm(Exec::G(f1, e.F, 1, u1, e.h, 1, e.F, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(tn.dw(f1, e.F, u1, e.h, e.sl, e.F, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
-  PDS_TRY(e.gemm(Exec::G(f1, e.F, 0, win, e.h, 1, e.sl, e.h, e.F, v2, e.h)));
+  PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
   GemmArgs dafull = Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, s1, e.hl);
   dafull.blk_w = (int)e.hl;
   dafull.blk_stride = e.sl * e.hl;
   PDS_TRY(e.gemm(dafull));                                                              // packed for A2A
-  PDS_TRY(e.gemm(Exec::G(sv->at("afull"), e.h, 1, dx, e.h, 1, e.h, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(tn.dw(sv->at("afull"), e.h, dx, e.h, e.sl, e.h, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
   PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                                 // A2A(dO)
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), r1, x3, dd));
@@ -378,9 +417,9 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, 3 * e.hl, x4, 3 * e.h, e.st), "unpack"));
   }
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
-  PDS_TRY(e.gemm(Exec::G(x4, 3 * e.h, 1, u1, e.h, 1, 3 * e.h, e.h, e.sl, dw, e.h, EPI_F32)));
+  PDS_TRY(tn.dw(x4, 3 * e.h, u1, e.h, e.sl, 3 * e.h, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, 3 * e.h, g->dw_qkv_t));
-  PDS_TRY(e.gemm(Exec::G(x4, 3 * e.h, 0, wqkv, e.h, 1, e.sl, e.h, 3 * e.h, v2, e.h)));
+  PDS_TRY(tn.xw(x4, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -397,6 +436,8 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   char* pw = ws + bp.ws_off("pw");
   char* hw = ws + bp.ws_off("hw");
   char* gw = ws + bp.ws_off("gw");
+  char* wt = ws + bp.ws_off("wt");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), wt};
   const int64_t row = e.h * 2;
   const int64_t slot = e.r * wr * e.h * 2;
   const char* xb = static_cast<const char*>(x);
@@ -409,8 +450,9 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
     PDS_TRY(e.gemm(q));
   }
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));  // query-chunk x KV-chunk loop
-  for (int64_t k = 0; k < c; ++k) {   // projection waves
-    GemmArgs pj = Exec::G(sv->at("a"), e.hl, 0, w->w_proj, e.h, 1, W, e.h, e.hl, pw, e.h);
+  PDS_TRY(tn.tr(w->w_proj, e.h, e.hl, e.h, wt));                 // W_proj^T, reused by every wave
+  for (int64_t k = 0; k < c; ++k) {   // projection waves (A rows read through the TMA row remap)
+    GemmArgs pj = Exec::G(sv->at("a"), e.hl, 0, wt, e.hl, 0, W, e.h, e.hl, pw, e.h);
     pj.a_seg = wr; pj.a_stride = e.sl; pj.a_base = k * wr; pj.a_rows = e.s;
     PDS_TRY(e.gemm(pj));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
@@ -418,12 +460,13 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
     PDS_TRY(e.norm_fwd(xb + k * wr * row, pw + slot, w->g2, wr, sv->at("x1") + k * wr * row, vl + k * wr * row,
                        sv->at("rstd2") + k * wr * 4));
   }
+  PDS_TRY(tn.tr(w->w_out, e.h, e.Fl, e.h, wt));                  // W_out^T, reused by every wave
   for (int64_t k = 0; k < c; ++k) {   // FFN waves
     PDS_TRY(e.ag(vl + k * wr * row, wg, wr * e.h));
     GemmArgs fc1 = Exec::G(wg, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
     fc1.aux_out = gw; fc1.ld_aux = e.Fl;
     PDS_TRY(e.gemm(fc1));
-    PDS_TRY(e.gemm(Exec::G(gw, e.Fl, 0, w->w_out, e.h, 1, W, e.h, e.Fl, pw, e.h)));
+    PDS_TRY(tn.mm(gw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
     if (e.c->tap_z) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_z) + k * wr * row, pw + slot, wr * e.h));
     PDS_TRY(e.add(sv->at("x1") + k * wr * row, pw + slot, static_cast<char*>(y) + k * wr * row, wr * e.h));
@@ -445,27 +488,30 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
   char* dhw = ws + bp.ws_off("dhw");
   char* da = ws + bp.ws_off("da");
   char* dqkv = ws + bp.ws_off("dqkv");
+  char* wt = ws + bp.ws_off("wt");
   float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
   float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
   float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), wt};
   const int64_t row = e.h * 2;
   const int64_t slot = e.r * wr * e.h * 2;
   const char* dyb = static_cast<const char*>(dy);
   const char* xb = static_cast<const char*>(sv->x);
   char* dxb = static_cast<char*>(dx);
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  PDS_TRY(tn.tr(w->w_in_t, e.h, e.Fl, e.h, wt));                 // W_in (= (W_in^T)^T) for dV, every wave
   for (int64_t k = 0; k < c; ++k) {   // FFN backward waves, recomputing v, H, G
     const int64_t o = k * wr;
     PDS_TRY(e.ag(dyb + o * row, wg, wr * e.h));                                         // AG(dz)
     PDS_TRY(e.apply(sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, wr, vl));
     PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                    // AG(v)
-    PDS_TRY(e.gemm(Exec::G(wg2, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl)));   // H recompute
+    PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                   // H recompute
     GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.Fl, EPI_DGELU);
     dgel.aux_in = hw; dgel.aux_out = gw; dgel.ld_aux = e.Fl;
     PDS_TRY(e.gemm(dgel));
-    PDS_TRY(e.gemm(Exec::G(gw, e.Fl, 1, wg, e.h, 1, e.Fl, e.h, W, g->dw_out, e.h, EPI_F32_ACC)));
-    PDS_TRY(e.gemm(Exec::G(dhw, e.Fl, 1, wg2, e.h, 1, e.Fl, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC)));
-    PDS_TRY(e.gemm(Exec::G(dhw, e.Fl, 0, w->w_in_t, e.h, 1, W, e.h, e.Fl, pw, e.h)));
+    PDS_TRY(tn.dw(gw, e.Fl, wg, e.h, W, e.Fl, e.h, g->dw_out));
+    PDS_TRY(tn.dw(dhw, e.Fl, wg2, e.h, W, e.Fl, e.h, g->dw_in_t));
+    PDS_TRY(tn.mm(dhw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(dv)
     PDS_TRY(e.norm_bwd(pw + slot, sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, dyb + o * row, wr,
                        dxb + o * row, dgp, dgl + e.h));
@@ -476,19 +522,16 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     GemmArgs dA = Exec::G(wg, e.h, 0, w->w_proj, e.h, 0, W, e.hl, e.h, da, e.hl);
     dA.c_seg = wr; dA.c_stride = e.sl; dA.c_base = o;
     PDS_TRY(e.gemm(dA));
-    GemmArgs dwp = Exec::G(sv->at("a"), e.hl, 1, wg, e.h, 1, e.hl, e.h, W, g->dw_proj, e.h, EPI_F32_ACC);
-    dwp.a_seg = wr; dwp.a_stride = e.sl; dwp.a_base = o; dwp.a_rows = e.s;
-    PDS_TRY(e.gemm(dwp));
+    PDS_TRY(tn.dw(sv->at("a"), e.hl, wg, e.h, W, e.hl, e.h, g->dw_proj, EPI_F32_ACC, wr, e.sl, o));
   }
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), da, dqkv, dd));
+  PDS_TRY(tn.tr(w->w_qkv_t, e.h, 3 * e.hl, e.h, wt));            // W_qkv for dU, every wave
   for (int64_t k = 0; k < c; ++k) {   // QKV backward waves
     const int64_t o = k * wr;
     PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
     PDS_TRY(e.ag(ul, wg, wr * e.h));                                                     // AG(u)
-    GemmArgs dwq = Exec::G(dqkv, 3 * e.hl, 1, wg, e.h, 1, 3 * e.hl, e.h, W, g->dw_qkv_t, e.h, EPI_F32_ACC);
-    dwq.a_seg = wr; dwq.a_stride = e.sl; dwq.a_base = o; dwq.a_rows = e.s;
-    PDS_TRY(e.gemm(dwq));
-    GemmArgs du = Exec::G(dqkv, 3 * e.hl, 0, w->w_qkv_t, e.h, 1, W, e.h, 3 * e.hl, pw, e.h);
+    PDS_TRY(tn.dw(dqkv, 3 * e.hl, wg, e.h, W, 3 * e.hl, e.h, g->dw_qkv_t, EPI_F32_ACC, wr, e.sl, o));
+    GemmArgs du = Exec::G(dqkv, 3 * e.hl, 0, wt, 3 * e.hl, 0, W, e.h, 3 * e.hl, pw, e.h);
     du.a_seg = wr; du.a_stride = e.sl; du.a_base = o; du.a_rows = e.s;
     PDS_TRY(e.gemm(du));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(du)

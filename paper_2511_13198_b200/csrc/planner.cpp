@@ -245,6 +245,9 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
+      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * s * 2);   // transposed operands (all GEMMs TN)
+      push(p.ws, tw, "tb", h * s * 2);
+      push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
       break;
     case PDS_ULYSSES_Z: {
       push(p.saved, ts, "rstd1", ell);
@@ -271,6 +274,9 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
+      push(p.ws, tw, "ta", std::max(F, 3 * h) * sl * 2);
+      push(p.ws, tw, "tb", h * sl * 2);
+      push(p.ws, tw, "wt", h * std::max(F, 3 * h) * 2);
       break;
     }
     case PDS_METP: {
@@ -299,6 +305,9 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", (int64_t)rmsnorm_bwd_grid(w) * h * 4);
       push(p.ws, tw, "dgl", 2 * h * 4);
+      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * w * 2);
+      push(p.ws, tw, "tb", h * P * w * 2);
+      push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
       break;
     }
     default:

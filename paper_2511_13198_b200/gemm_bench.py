@@ -21,12 +21,16 @@ def main():
     ap.add_argument("--s", type=int, default=16384)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--probe", action="store_true")
     a = ap.parse_args()
     s, h, F = a.s, 4096, 16384
     shapes = [("QKV", s, 3 * h, h, 0, 0, 0), ("proj", s, h, h, 0, 1, 0), ("FC1", s, F, h, 0, 0, 3),
               ("FC2", s, h, F, 0, 1, 0), ("dG", s, F, h, 0, 0, 4), ("dW_out", F, h, s, 1, 1, 1),
               ("dW_in", F, h, s, 1, 1, 1), ("dV2", s, h, F, 0, 1, 0), ("dA", s, h, h, 0, 0, 0),
               ("dW_proj", h, h, s, 1, 1, 1), ("dW_qkv", 3 * h, h, s, 1, 1, 1), ("dU", s, h, 3 * h, 0, 1, 0)]
+    if a.probe:   # isolate operand majors from the epilogue
+        shapes = [("TN_bf16", F, h, s, 0, 0, 0), ("TN_f32acc", F, h, s, 0, 0, 1), ("MM_bf16", F, h, s, 1, 1, 0),
+                  ("MM_f32acc", F, h, s, 1, 1, 1), ("NT_bf16", F, h, s, 0, 1, 0), ("MT_bf16", F, h, s, 1, 0, 0)]
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
     res = {}
