@@ -22,6 +22,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace pds {
@@ -225,6 +227,8 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const int k0 = j * BN;
       const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
+      auto block = [&](auto mask_c) {
+        constexpr bool MASK = decltype(mask_c)::value;
       // pass 1: row max; 16-column TMEM loads software-pipelined (next chunk in flight)
       float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       {
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float v = __uint_as_float(cur[i]);
-            if (mask && k0 + c * 16 + i > row) v = -INFINITY;
+            if (MASK && k0 + c * 16 + i > row) v = -INFINITY;
             mxa[i & 3] = fmaxf(mxa[i & 3], v);
           }
           tmem_ld_wait();
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(384, 1)
             const float x1 = fmaf(__uint_as_float(cur[i + 1]), scale_log2, neg_m);
             float p0 = ex2(x0);
             float p1 = (i & 2) ? exp2_fma(x1) : ex2(x1);
-            if (mask) {
+            if (MASK) {
               if (k0 + c * 16 + i > row) p0 = 0.f;
               if (k0 + c * 16 + i + 1 > row) p1 = 0.f;
             }
@@ -294,7 +298,10 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
         }
       }
-      l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+      };
+      if (mask) block(std::true_type{});
+      else block(std::false_type{});
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -377,7 +384,7 @@ struct BwdKVCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                             const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                             const float* __restrict__ Dd, int s, int heads, int causal,
@@ -413,8 +420,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&st_empty[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pd_done[i], 1);
     }
     mbar_init(fin, 1);
@@ -488,6 +495,8 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) umma_commit(fin);
     __syncwarp();
   } else if (warp >= 4) {
+    // two warpgroups: wg owns query columns [32 wg, 32 wg + 32) of every key row
+    const int wg = (warp - 4) >> 2;
     const int q = warp & 3;
     const int t = q * 32 + lane;
     const int key = k0 + t;
@@ -499,21 +508,22 @@ __global__ void __launch_bounds__(256, 1)
       const float* L = reinterpret_cast<const float*>(sm + C::L_OFF + b * 256);
       const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + 512 + b * 256);
       const bool mask = causal && (q0 < k0 + 128);
-      uint32_t pk[2][16], dk[2][16];
+      uint32_t pk[16], dk[16];
       {
         uint32_t cs[16], cd[16], ns[16], nd[16];
-        tmem_ld16(lb + ST_COL + b * 64, cs);
-        tmem_ld16(lb + DP_COL + b * 64, cd);
+        const uint32_t c0 = b * 64 + wg * 32;
+        tmem_ld16(lb + ST_COL + c0, cs);
+        tmem_ld16(lb + DP_COL + c0, cd);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < 3) {
-            tmem_ld16(lb + ST_COL + b * 64 + (c + 1) * 16, ns);
-            tmem_ld16(lb + DP_COL + b * 64 + (c + 1) * 16, nd);
+        for (int c = 0; c < 2; ++c) {
+          if (c == 0) {
+            tmem_ld16(lb + ST_COL + c0 + 16, ns);
+            tmem_ld16(lb + DP_COL + c0 + 16, nd);
           }
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
-            const int qi = c * 16 + e;
+            const int qi = wg * 32 + c * 16 + e;
             float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -L[qi] * LOG2E));
             float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -L[qi + 1] * LOG2E));
             if (mask) {
@@ -522,57 +532,60 @@ __global__ void __launch_bounds__(256, 1)
             }
             const float d0 = p0 * (__uint_as_float(cd[e]) - Dv[qi]);
             const float d1 = p1 * (__uint_as_float(cd[e + 1]) - Dv[qi + 1]);
-            pk[c >> 1][(c & 1) * 8 + (e >> 1)] = pack_bf16(p0, p1);
-            dk[c >> 1][(c & 1) * 8 + (e >> 1)] = pack_bf16(d0, d1);
+            pk[c * 8 + (e >> 1)] = pack_bf16(p0, p1);
+            dk[c * 8 + (e >> 1)] = pack_bf16(d0, d1);
           }
-          tmem_ld_wait();
+          if (c == 0) {
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) { cs[i] = ns[i]; cd[i] = nd[i]; }
+            for (int j = 0; j < 16; ++j) { cs[j] = ns[j]; cd[j] = nd[j]; }
+          }
         }
       }
-      tc_fence_before();
+            tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&st_empty[b]);
       if (i >= 2) mbar_wait(&pd_done[b], ((i >> 1) - 1) & 1);
       uint8_t* PT = sm + C::P_OFF + b * 16384;
       uint8_t* ST = sm + C::S_OFF + b * 16384;
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          st_sw128(PT, 16384, t, 0, c * 4 + e, make_uint4(pk[c][4 * e], pk[c][4 * e + 1], pk[c][4 * e + 2], pk[c][4 * e + 3]));
-          st_sw128(ST, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
-        }
+      for (int e = 0; e < 4; ++e) {
+        st_sw128(PT, 16384, t, 0, wg * 4 + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
+        st_sw128(ST, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
     }
-    // epilogue: dK (scale, RoPE^T), dV
+    // epilogue: warpgroup 0 drains dK (scale, RoPE^T), warpgroup 1 drains dV
     mbar_wait(fin, 0);
     tc_fence_after();
     __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
+    if (wg == 0) {
 #pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t ra[32], rb[32];
-      tmem_ld32(lb + DK_COL + c * 32, ra);
-      tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
-      tmem_ld_wait();
-      float a[32], bb[32];
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(lb + DK_COL + c * 32, ra);
+        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
+        tmem_ld_wait();
+        float a[32], bb[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
-      rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
-      store32_bf16(rowp + hq + c * 32, a);
-      store32_bf16(rowp + hq + c * 32 + D / 2, bb);
-    }
+        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
+        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+        store32_bf16(rowp + hq + c * 32, a);
+        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+      }
+    } else {
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(lb + DV_COL + c * 32, r);
-      tmem_ld_wait();
-      float v[32];
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(lb + DV_COL + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      store32_bf16(rowp + 2 * hq + c * 32, v);
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        store32_bf16(rowp + 2 * hq + c * 32, v);
+      }
     }
   }
   tc_fence_before();
@@ -934,8 +947,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&sd_full[tile], j & 1);
       tc_fence_after();
       const bool mask = causal && (k0 + 63 > q0 + tile * 128);
-      // S and dP rows in 16-key chunks, next chunk's loads in flight while processing
       uint32_t dk[2][16];
+      // S and dP rows in 16-key chunks, next chunk's loads in flight while processing
       {
         uint32_t cs[16], cd[16], ns[16], nd[16];
         tmem_ld16(lb + 0, cs);
@@ -963,7 +976,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; ++i) { cs[i] = ns[i]; cd[i] = nd[i]; }
         }
       }
-#pragma unroll
+      #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
@@ -1076,7 +1089,7 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   }
   const float scale = 1.0f / sqrtf((float)D);
   const float scale_log2 = scale * LOG2E;
-  attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdKVCfg<D>::SMEM, st>>>(
+  attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 384, BwdKVCfg<D>::SMEM, st>>>(
       kv128, q64, do64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
       reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
   static const bool dq1 = [] {
