@@ -1013,6 +1013,424 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ================================================================== backward v3
+// The fixed operand of each backward MMA lives in TMEM (A operand from TMEM), so
+// the tensor core reads only the streaming operand from shared memory:
+//   dK/dV kernel: K and V of the CTA's 128 keys are packed into TMEM once; per 64-query
+//     block S^T = K Q^T and dP^T = V dO^T read only Q / dO from shared memory.
+//   dQ kernel: Q and dO of the CTA's 128 queries are packed into TMEM once; per
+//     64-key block S = Q K^T and dP = dO V^T read only K / V from shared memory.
+// Packing: lane = row, 32-bit column c holds elements (2c, 2c+1) of the K dimension.
+
+// thread-row load of 128 bf16 (D = 128) or 64 (D = 64) values into TMEM columns [col, col + D/2)
+template <int D>
+__device__ __forceinline__ void row_to_tmem(uint32_t lb, uint32_t col, const __nv_bfloat16* src, bool ok) {
+#pragma unroll
+  for (int c = 0; c < D / 64; ++c) {
+    uint32_t r[32];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + c * 64);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = ok ? __ldg(s4 + q) : make_uint4(0, 0, 0, 0);
+      r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+    }
+    tmem_st32(lb + col + c * 32, r);
+  }
+}
+
+template <int D>
+struct BwdKV3Cfg {
+  static constexpr int QT = 64 * D * 2;      // Q or dO tile [64][D]
+  static constexpr int NST = 3;              // query-block stages
+  static constexpr int Q_OFF = 0;            // [NST]
+  static constexpr int O_OFF = NST * QT;     // [NST]
+  static constexpr int P_OFF = 2 * NST * QT; // P^T [2][128][64]
+  static constexpr int S_OFF = P_OFF + 2 * 16384;
+  static constexpr int L_OFF = S_OFF + 2 * 16384;   // lse / D [NST][64] each
+  static constexpr int BAR_OFF = L_OFF + 2 * NST * 256;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv3_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __grid_constant__ CUtensorMap tq,
+                          const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
+                          const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
+                          const float2* __restrict__ rope, float scale, float scale_log2) {
+  using C = BwdKV3Cfg<D>;
+  constexpr int NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;              // [NST]
+  uint64_t* q_empty = bar + NST;           // [NST]
+  uint64_t* st_full = bar + 2 * NST;
+  uint64_t* st_empty = bar + 2 * NST + 1;
+  uint64_t* p_full = bar + 2 * NST + 2;    // [2]
+  uint64_t* pd_done = bar + 2 * NST + 4;   // [2]
+  uint64_t* kv_ready = bar + 2 * NST + 6;
+  uint64_t* fin = bar + 2 * NST + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, head = blockIdx.y;
+  const int hq = heads * D;
+  const int k0 = kb * 128;
+  const int qstart = causal ? k0 / 64 : 0;
+  const int nq = s / 64 - qstart;
+  constexpr int K_COL = 0, V_COL = 64, ST_COL = 128, DP_COL = 192, DV_COL = 256, DK_COL = 384;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tdo);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(st_full, 1);
+    mbar_init(st_empty, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pd_done[i], 1);
+    }
+    mbar_init(kv_ready, 8);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int i = 0; i < nq; ++i) {
+        const int b = i % NST, q0 = (qstart + i) * 64;
+        if (i >= NST) mbar_wait(&q_empty[b], ((i / NST) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[b], 2 * C::QT + 2 * 256);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::Q_OFF + b * C::QT + a * 8192, &tq, &q_full[b], head * D + a * 64, q0);
+          tma_load_2d(sm + C::O_OFF + b * C::QT + a * 8192, &tdo, &q_full[b], head * D + a * 64, q0);
+        }
+        bulk_load(sm + C::L_OFF + b * 256, lse + (int64_t)head * s + q0, 256, &q_full[b]);
+        bulk_load(sm + C::L_OFF + NST * 256 + b * 256, Dd + (int64_t)head * s + q0, 256, &q_full[b]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_st = umma_idesc_bf16(128, 64, 0, 0);
+    constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
+    mbar_wait(kv_ready, 0);
+    tc_fence_after();
+    auto dkdv = [&](int i) {
+      const int b = i % NST, pb = i & 1;
+      mbar_wait(&p_full[pb], (i >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
+        const uint32_t sp = smem_u32(sm + C::P_OFF + pb * 16384), ss = smem_u32(sm + C::S_OFF + pb * 16384);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_f16(tmem + DV_COL, kmaj_desc(sp, kk), mnmaj_desc(so, kk, 8192), idesc_acc, (i | kk) != 0);
+          umma_f16(tmem + DK_COL, kmaj_desc(ss, kk), mnmaj_desc(sq, kk, 8192), idesc_acc, (i | kk) != 0);
+        }
+        umma_commit(&pd_done[pb]);
+        umma_commit(&q_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int i = 0; i < nq; ++i) {
+      const int b = i % NST;
+      mbar_wait(&q_full[b], (i / NST) & 1);
+      if (i >= 1) mbar_wait(st_empty, (i - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16_ts(tmem + ST_COL, tmem + K_COL + kk * 8, kmaj_desc(sq, kk, 8192), idesc_st, kk > 0);
+          umma_f16_ts(tmem + DP_COL, tmem + V_COL + kk * 8, kmaj_desc(so, kk, 8192), idesc_st, kk > 0);
+        }
+        umma_commit(st_full);
+      }
+      __syncwarp();
+      if (i >= 1) dkdv(i - 1);
+    }
+    dkdv(nq - 1);
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int key = k0 + t;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    // K (warpgroup 0) / V (warpgroup 1) rows -> TMEM A operands
+    row_to_tmem<D>(lb, wg ? V_COL : K_COL, qkv + (int64_t)key * ld + (wg ? 2 * hq : hq) + head * D, key < s);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(kv_ready);
+    for (int i = 0; i < nq; ++i) {
+      const int b = i % NST, pb = i & 1, q0 = (qstart + i) * 64;
+      mbar_wait(st_full, i & 1);
+      tc_fence_after();
+      const float* L = reinterpret_cast<const float*>(sm + C::L_OFF + b * 256);
+      const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + NST * 256 + b * 256);
+      const bool mask = causal && (q0 < k0 + 128);
+      uint32_t cs[32], cd[32];
+      tmem_ld32(lb + ST_COL + wg * 32, cs);
+      tmem_ld32(lb + DP_COL + wg * 32, cd);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(st_empty);
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const int qi = wg * 32 + e;
+        float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -L[qi] * LOG2E));
+        float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -L[qi + 1] * LOG2E));
+        if (mask) {
+          if (key > q0 + qi) p0 = 0.f;
+          if (key > q0 + qi + 1) p1 = 0.f;
+        }
+        pk[e >> 1] = pack_bf16(p0, p1);
+        dk[e >> 1] = pack_bf16(p0 * (__uint_as_float(cd[e]) - Dv[qi]), p1 * (__uint_as_float(cd[e + 1]) - Dv[qi + 1]));
+      }
+      if (i >= 2) mbar_wait(&pd_done[pb], ((i >> 1) - 1) & 1);
+      uint8_t* PT = sm + C::P_OFF + pb * 16384;
+      uint8_t* ST = sm + C::S_OFF + pb * 16384;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        st_sw128(PT, 16384, t, 0, wg * 4 + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
+        st_sw128(ST, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
+    if (wg == 0) {
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(lb + DK_COL + c * 32, ra);
+        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
+        tmem_ld_wait();
+        float a[32], bb[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
+        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+        store32_bf16(rowp + hq + c * 32, a);
+        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(lb + DV_COL + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        store32_bf16(rowp + 2 * hq + c * 32, v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct BwdQ3Cfg {
+  static constexpr int KT = 64 * D * 2;     // K or V [64][D]
+  static constexpr int NST = 3;
+  static constexpr int K_OFF = 0;           // [NST]
+  static constexpr int V_OFF = NST * KT;    // [NST]
+  static constexpr int S_OFF = 2 * NST * KT;   // dS [2][128][64]
+  static constexpr int BAR_OFF = S_OFF + 2 * 16384;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq3_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
+                        int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
+                        const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
+                        const float2* __restrict__ rope, float scale, float scale_log2) {
+  using C = BwdQ3Cfg<D>;
+  constexpr int NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* kv_full = bar + 0;            // [NST]
+  uint64_t* kv_empty = bar + NST;         // [NST]
+  uint64_t* sd_full = bar + 2 * NST;      // [2]
+  uint64_t* sd_empty = bar + 2 * NST + 2; // [2]
+  uint64_t* ds_full = bar + 2 * NST + 4;  // [2]
+  uint64_t* dq_done = bar + 2 * NST + 6;  // [2]
+  uint64_t* q_ready = bar + 2 * NST + 8;
+  uint64_t* fin = bar + 2 * NST + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 10);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / 128;
+  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int head = blockIdx.y;
+  const int hq = heads * D;
+  const int q0 = qb * 128;
+  const int nkv = causal ? (q0 + 128) / 64 : s / 64;
+  constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tkv);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_empty[i], 8);
+      mbar_init(&ds_full[i], 8);
+      mbar_init(&dq_done[i], 1);
+    }
+    mbar_init(q_ready, 8);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int j = 0; j < nkv; ++j) {
+        const int b = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
+          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    auto dq = [&](int j) {
+      const int b = j % NST, sb = j & 1;
+      mbar_wait(&ds_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sd = smem_u32(sm + C::S_OFF + sb * 16384), sk = smem_u32(sm + C::K_OFF + b * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16(tmem + DQ_COL, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
+        umma_commit(&dq_done[sb]);
+        umma_commit(&kv_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j % NST, sb = j & 1;
+      mbar_wait(&kv_full[b], (j / NST) & 1);
+      if (j >= 2) mbar_wait(&sd_empty[sb], ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = smem_u32(sm + C::K_OFF + b * C::KT), sv = smem_u32(sm + C::V_OFF + b * C::KT);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16_ts(tmem + S_COL + sb * 64, tmem + Q_COL + kk * 8, kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
+          umma_f16_ts(tmem + DP_COL + sb * 64, tmem + O_COL + kk * 8, kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
+        }
+        umma_commit(&sd_full[sb]);
+      }
+      __syncwarp();
+      if (j >= 1) dq(j - 1);
+    }
+    dq(nkv - 1);
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;          // key columns [32 wg, 32 wg + 32) of each block
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int row = q0 + t;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    if (wg == 0) row_to_tmem<D>(lb, Q_COL, qkv + (int64_t)row * ld + head * D, true);
+    else row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_ready);
+    const float l2 = lse[(int64_t)head * s + row] * LOG2E;
+    const float dd = Dd[(int64_t)head * s + row];
+    for (int j = 0; j < nkv; ++j) {
+      const int sb = j & 1, k0 = j * 64;
+      mbar_wait(&sd_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      const bool mask = causal && (k0 + 63 > q0);
+      uint32_t cs[32], cd[32];
+      tmem_ld32(lb + S_COL + sb * 64 + wg * 32, cs);
+      tmem_ld32(lb + DP_COL + sb * 64 + wg * 32, cd);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_empty[sb]);
+      uint32_t dk[16];
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -l2));
+        float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -l2));
+        if (mask) {
+          if (k0 + wg * 32 + e > row) p0 = 0.f;
+          if (k0 + wg * 32 + e + 1 > row) p1 = 0.f;
+        }
+        dk[e >> 1] = pack_bf16(p0 * (__uint_as_float(cd[e]) - dd), p1 * (__uint_as_float(cd[e + 1]) - dd));
+      }
+      if (j >= 2) mbar_wait(&dq_done[sb], ((j >> 1) - 1) & 1);
+      uint8_t* DS = sm + C::S_OFF + sb * 16384;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        st_sw128(DS, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[sb]);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
+    // warpgroup w drains the RoPE pair chunk c = w (D = 128) / both halves (D = 64, wg 0)
+    for (int c = wg; c < D / 64; c += 2) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(lb + DQ_COL + c * 32, ra);
+      tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
+      tmem_ld_wait();
+      float a[32], bb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
+      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
+      store32_bf16(rowp + c * 32, a);
+      store32_bf16(rowp + c * 32 + D / 2, bb);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1089,6 +1507,27 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   }
   const float scale = 1.0f / sqrtf((float)D);
   const float scale_log2 = scale * LOG2E;
+  static const int bwdv = [] {
+    const char* e = getenv("PDS_ATTN_BWDV");
+    return e ? atoi(e) : 3;
+  }();
+  if (bwdv >= 3) {
+    static bool once3 = false;
+    if (!once3) {
+      cudaFuncSetAttribute(attn_bwd_dkdv3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV3Cfg<D>::SMEM);
+      cudaFuncSetAttribute(attn_bwd_dq3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ3Cfg<D>::SMEM);
+      once3 = true;
+    }
+    attn_bwd_dkdv3_kernel<D><<<dim3(s / 128, heads), 384, BwdKV3Cfg<D>::SMEM, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, q64, do64, reinterpret_cast<const float*>(lse), Dd, s,
+        heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv), reinterpret_cast<const float2*>(rope), scale,
+        scale_log2);
+    attn_bwd_dq3_kernel<D><<<dim3(s / 128, heads), 384, BwdQ3Cfg<D>::SMEM, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out,
+        kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
+        reinterpret_cast<const float2*>(rope), scale, scale_log2);
+    return (int)cudaGetLastError();
+  }
   attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 384, BwdKVCfg<D>::SMEM, st>>>(
       kv128, q64, do64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
       reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
