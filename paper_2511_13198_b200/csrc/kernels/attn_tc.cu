@@ -1431,6 +1431,486 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ============================================================ backward v4
+// 128 x 128 blocks everywhere (every MMA has N = 128: the N = 64 MMAs of v3 run at
+// 2/3 of the tensor peak, tools/mma_probe.cu).  The elementwise results P^T / dS^T
+// (dK/dV kernel) and dS (dQ kernel) are written back into TMEM as packed bf16 and
+// used as the A operand of the next MMA, so no shared-memory round trip and no
+// generic->async proxy fence sits on the critical path.  Two elementwise
+// warpgroups split the 128 columns of a block: warpgroup w owns columns
+// [64w, 64w + 64) and writes its packed half into TMEM columns [64w, 64w + 32) of
+// the same region, so the A operand's k-step kk lives at column acol(kk).
+__device__ __forceinline__ uint32_t acol(int kk) { return (kk & 3) * 8 + (kk >> 2) * 64; }
+
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+// exponentials of one 64-column half: e % 4 == 3 on the FMA pipe, the rest on MUFU
+__device__ __forceinline__ float ex2_mix(float x, int e) { return (e & 3) == 3 ? exp2_fma(x) : ex2(x); }
+
+template <int D>
+struct BwdKV4Cfg {
+  static constexpr int T = 128 * D * 2;      // one [128][D] bf16 tile
+  static constexpr int NST = D == 128 ? 2 : 3;
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = T;
+  static constexpr int Q_OFF = 2 * T;        // [NST]
+  static constexpr int O_OFF = Q_OFF + NST * T;
+  static constexpr int L_OFF = O_OFF + NST * T;    // lse [NST][128], then D [NST][128]
+  static constexpr int BAR_OFF = L_OFF + 2 * NST * 512;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+// dK / dV.  CTA = (128-key block kb, head); loop over 128-query blocks i.
+//   MMA order:  S^T_0 dP^T_0 | dV_0 S^T_1 | dK_0 dP^T_1 | dV_1 S^T_2 | dK_1 dP^T_2 ...
+//   S^T = K Q^T (TMEM cols 0..127), dP^T = V dO^T (cols 128..255),
+//   P^T (bf16) overwrites S^T, dS^T = P^T (dP^T - D) overwrites dP^T;
+//   dV += P^T dO (cols 256..), dK += dS^T Q (cols 256 + D..).
+// A later MMA that overwrites a region is issued after the MMA that reads it, and
+// tcgen05 MMAs of one thread execute in order.
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkdv4_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
+                          const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
+                          const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
+                          int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2) {
+  using C = BwdKV4Cfg<D>;
+  constexpr int NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;             // [NST]
+  uint64_t* q_empty = bar + NST;          // [NST]
+  uint64_t* kv_full = bar + 2 * NST;
+  uint64_t* s_full = bar + 2 * NST + 1;
+  uint64_t* dp_full = bar + 2 * NST + 2;
+  uint64_t* p_full = bar + 2 * NST + 3;
+  uint64_t* ds_full = bar + 2 * NST + 4;
+  uint64_t* fin = bar + 2 * NST + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 6);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, head = blockIdx.y;
+  const int hq = heads * D;
+  const int k0 = kb * 128;
+  const int qstart = causal ? kb : 0;
+  const int nq = s / 128 - qstart;
+  constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tkv);
+    tma_prefetch(&tq);
+    tma_prefetch(&tdo);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(kv_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(ds_full, 8);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::T);
+      for (int a = 0; a < D / 64; ++a) {
+        tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, hq + head * D + a * 64, k0);
+        tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, 2 * hq + head * D + a * 64, k0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int b = i % NST, q0 = (qstart + i) * 128;
+        if (i >= NST) mbar_wait(&q_empty[b], ((i / NST) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[b], 2 * C::T + 1024);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::Q_OFF + b * C::T + a * 16384, &tq, &q_full[b], head * D + a * 64, q0);
+          tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &q_full[b], head * D + a * 64, q0);
+        }
+        bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)head * s + q0, 512, &q_full[b]);
+        bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)head * s + q0, 512, &q_full[b]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
+    const uint32_t sk = smem_u32(sm + C::K_OFF), sv = smem_u32(sm + C::V_OFF);
+    auto qtile = [&](int i) { return smem_u32(sm + C::Q_OFF + (i % NST) * C::T); };
+    auto otile = [&](int i) { return smem_u32(sm + C::O_OFF + (i % NST) * C::T); };
+    auto issue_s = [&](int i) {
+      mbar_wait(&q_full[i % NST], (i / NST) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = qtile(i);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(tmem + ST_COL, kmaj_desc(sk, kk), kmaj_desc(sq, kk), idesc_s, kk > 0);
+        umma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int i) {
+      if (elect_one()) {
+        const uint32_t so = otile(i);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(tmem + DP_COL, kmaj_desc(sv, kk), kmaj_desc(so, kk), idesc_s, kk > 0);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    issue_s(0);
+    issue_dp(0);
+    for (int i = 0; i < nq; ++i) {
+      mbar_wait(p_full, i & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t so = otile(i);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
+      }
+      __syncwarp();
+      if (i + 1 < nq) issue_s(i + 1);
+      mbar_wait(ds_full, i & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = qtile(i);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16_ts(tmem + DK_COL, tmem + DP_COL + acol(kk), mnmaj_desc(sq, kk), idesc_acc, (i | kk) != 0);
+        umma_commit(&q_empty[i % NST]);
+      }
+      __syncwarp();
+      if (i + 1 < nq) issue_dp(i + 1);
+    }
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;          // query columns [64 wg, 64 wg + 64)
+    const int q = warp & 3;
+    const int t = q * 32 + lane;             // key row (TMEM lane)
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t c_s = lb + ST_COL + 64 * wg, c_d = lb + DP_COL + 64 * wg;
+    for (int i = 0; i < nq; ++i) {
+      const int b = i % NST;
+      const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * 256;
+      const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * 256;
+      const bool diag = causal && i == 0;
+      float p[64];
+      {
+        uint32_t sa[32], sb[32];
+        mbar_wait(s_full, i & 1);
+        tc_fence_after();
+        tmem_ld32(c_s, sa);
+        tmem_ld32(c_s + 32, sb);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          const float4 L = lds4(lsm + e * 4);
+          const float l[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float sv = __uint_as_float(e + u < 32 ? sa[e + u] : sb[e + u - 32]);
+            p[e + u] = ex2_mix(fmaf(sv, scale_log2, -l[u] * LOG2E), u);
+          }
+        }
+        if (diag) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (t > 64 * wg + e) p[e] = 0.f;
+        }
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(p[2 * e], p[2 * e + 1]);
+        tmem_st32(c_s, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      {
+        mbar_wait(dp_full, i & 1);
+        tc_fence_after();
+        uint32_t pk[32];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t dv[32];
+          tmem_ld32(c_d + 32 * h, dv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 Dq = lds4(dsm + (32 * h + e) * 4);
+            const float dq[4] = {Dq.x, Dq.y, Dq.z, Dq.w};
+            pk[16 * h + e / 2] = pack_bf16(p[32 * h + e] * (__uint_as_float(dv[e]) - dq[0]),
+                                           p[32 * h + e + 1] * (__uint_as_float(dv[e + 1]) - dq[1]));
+            pk[16 * h + e / 2 + 1] = pack_bf16(p[32 * h + e + 2] * (__uint_as_float(dv[e + 2]) - dq[2]),
+                                               p[32 * h + e + 3] * (__uint_as_float(dv[e + 3]) - dq[3]));
+          }
+        }
+        tmem_st32(c_d, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ds_full);
+      }
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const int key = k0 + t;
+    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
+    if (wg == 0) {
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(lb + DK_COL + c * 32, ra);
+        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
+        tmem_ld_wait();
+        float a[32], bb[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
+        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+        store32_bf16(rowp + hq + c * 32, a);
+        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(lb + DV_COL + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        store32_bf16(rowp + 2 * hq + c * 32, v);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+struct BwdQ4Cfg {
+  static constexpr int T = 128 * D * 2;     // K or V [128][D]
+  static constexpr int NST = D == 128 ? 3 : 4;
+  static constexpr int K_OFF = 0;           // [NST]
+  static constexpr int V_OFF = NST * T;     // [NST]
+  static constexpr int BAR_OFF = 2 * NST * T;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+// dQ.  CTA = (128-query block, head); loop over 128-key blocks j.  Q, dO (the fixed
+// A operands) live in TMEM; S = Q K^T (cols 128..255), dP = dO V^T (cols 256..383),
+// dS = P (dP - D) overwrites dP as packed bf16, dQ += dS K (cols 384..).
+//   MMA order:  S_0 dP_0 | S_1 | dQ_0 dP_1 | S_2 | dQ_1 dP_2 ...
+// S_{j+1} is issued as soon as the elementwise warps have read S_j.
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq4_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
+                        int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
+                        const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
+                        const float2* __restrict__ rope, float scale, float scale_log2) {
+  using C = BwdQ4Cfg<D>;
+  constexpr int NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* kv_full = bar + 0;            // [NST]
+  uint64_t* kv_empty = bar + NST;         // [NST]
+  uint64_t* s_full = bar + 2 * NST;
+  uint64_t* s_free = bar + 2 * NST + 1;
+  uint64_t* dp_full = bar + 2 * NST + 2;
+  uint64_t* ds_full = bar + 2 * NST + 3;
+  uint64_t* q_ready = bar + 2 * NST + 4;
+  uint64_t* fin = bar + 2 * NST + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 6);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / 128;
+  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int head = blockIdx.y;
+  const int hq = heads * D;
+  const int q0 = qb * 128;
+  const int nkv = causal ? qb + 1 : nqb;
+  constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tkv);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(q_ready, 8);
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int j = 0; j < nkv; ++j) {
+        const int b = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
+        mbar_arrive_expect_tx(&kv_full[b], 2 * C::T);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], hq + head * D + a * 64, j * 128);
+          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
+    auto ktile = [&](int j) { return smem_u32(sm + C::K_OFF + (j % NST) * C::T); };
+    auto vtile = [&](int j) { return smem_u32(sm + C::V_OFF + (j % NST) * C::T); };
+    auto issue_s = [&](int j) {
+      mbar_wait(&kv_full[j % NST], (j / NST) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = ktile(j);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ts(tmem + S_COL, tmem + Q_COL + kk * 8, kmaj_desc(sk, kk), idesc_s, kk > 0);
+        umma_commit(s_full);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int j) {
+      if (elect_one()) {
+        const uint32_t sv = vtile(j);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16_ts(tmem + DP_COL, tmem + O_COL + kk * 8, kmaj_desc(sv, kk), idesc_s, kk > 0);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    issue_s(0);
+    issue_dp(0);
+    for (int j = 0; j < nkv; ++j) {
+      if (j + 1 < nkv) {
+        mbar_wait(s_free, j & 1);
+        tc_fence_after();
+        issue_s(j + 1);
+      }
+      mbar_wait(ds_full, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = ktile(j);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol(kk), mnmaj_desc(sk, kk), idesc_q, (j | kk) != 0);
+        umma_commit(&kv_empty[j % NST]);
+      }
+      __syncwarp();
+      if (j + 1 < nkv) issue_dp(j + 1);
+    }
+    if (elect_one()) umma_commit(fin);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) >> 2;          // key columns [64 wg, 64 wg + 64) of each block
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const int row = q0 + t;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    if (wg == 0) row_to_tmem<D>(lb, Q_COL, qkv + (int64_t)row * ld + head * D, true);
+    else row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_ready);
+    const float nl2 = -lse[(int64_t)head * s + row] * LOG2E;
+    const float dd = Dd[(int64_t)head * s + row];
+    const uint32_t c_s = lb + S_COL + 64 * wg, c_d = lb + DP_COL + 64 * wg;
+    for (int j = 0; j < nkv; ++j) {
+      const bool diag = causal && j == nkv - 1;
+      float p[64];
+      {
+        uint32_t sa[32], sb[32];
+        mbar_wait(s_full, j & 1);
+        tc_fence_after();
+        tmem_ld32(c_s, sa);
+        tmem_ld32(c_s + 32, sb);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
+#pragma unroll
+        for (int e = 0; e < 64; ++e)
+          p[e] = ex2_mix(fmaf(__uint_as_float(e < 32 ? sa[e] : sb[e - 32]), scale_log2, nl2), e);
+        if (diag) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e)
+            if (64 * wg + e > t) p[e] = 0.f;
+        }
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      uint32_t pk[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t dv[32];
+        tmem_ld32(c_d + 32 * h, dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2)
+          pk[16 * h + e / 2] = pack_bf16(p[32 * h + e] * (__uint_as_float(dv[e]) - dd),
+                                         p[32 * h + e + 1] * (__uint_as_float(dv[e + 1]) - dd));
+      }
+      tmem_st32(c_d, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
+    for (int c = wg; c < D / 64; c += 2) {
+      uint32_t ra[32], rb[32];
+      tmem_ld32(lb + DQ_COL + c * 32, ra);
+      tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
+      tmem_ld_wait();
+      float a[32], bb[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
+      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
+      store32_bf16(rowp + c * 32, a);
+      store32_bf16(rowp + c * 32 + D / 2, bb);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1509,8 +1989,24 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   const float scale_log2 = scale * LOG2E;
   static const int bwdv = [] {
     const char* e = getenv("PDS_ATTN_BWDV");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 4;
   }();
+  if (bwdv >= 4) {
+    static bool once4 = false;
+    if (!once4) {
+      cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
+      cudaFuncSetAttribute(attn_bwd_dq4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
+      once4 = true;
+    }
+    attn_bwd_dkdv4_kernel<D><<<dim3(s / 128, heads), 384, BwdKV4Cfg<D>::SMEM, st>>>(
+        kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+    attn_bwd_dq4_kernel<D><<<dim3(s / 128, heads), 384, BwdQ4Cfg<D>::SMEM, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out,
+        kv128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
+        reinterpret_cast<const float2*>(rope), scale, scale_log2);
+    return (int)cudaGetLastError();
+  }
   if (bwdv >= 3) {
     static bool once3 = false;
     if (!once3) {
