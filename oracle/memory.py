@@ -49,7 +49,7 @@ def _al(x):
 
 
 def _norm_bwd_grid(rows):
-    return min((rows + 3) // 4, 592)
+    return min((rows + 3) // 4, 444)   # 148 SMs x 3 resident 256-thread blocks
 
 
 def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):

@@ -1,19 +1,24 @@
 // tcgen05 / TMEM causal flash attention (Eq. 2; causal R-1) for
-// sm_100a.  One CTA per (128-query block, head):
+// sm_100a, forward and backward.  Every kernel: warp 0 = TMA producer, warp 1 = the
+// single-thread MMA issuer, warp 2 = TMEM allocator (512 columns), warps 4..11 =
+// two elementwise warpgroups (thread = TMEM lane = one row of the 128-row tile).
 //
-//   warp 0      TMA producer: Q once, then K_j / V_j (128 keys) into a 2-stage ring
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered TMEM
-//               S (128 x 128 fp32), then O += P_j V_j into TMEM O (128 x d fp32)
-//   warp 2      TMEM allocator (512 columns: S0, S1, O)
-//   warps 4..7  softmax: thread t owns query row t (= TMEM lane t); two TMEM passes
-//               over S_j (row max, then exp2 / row sum / bf16 P into shared memory in
-//               the UMMA K-major SWIZZLE_128B layout); O is rescaled in TMEM only
-//               when the running max grows by more than 2^8 (exact: l and O always
-//               use the same stale max).  Epilogue: O / l -> bf16, LSE (natural log).
+//   attn_fwd_tc_kernel     CTA = two 128-query tiles x one head; S = Q K^T per
+//                          128-key block into TMEM, online softmax with lazy
+//                          rescale, P written back into TMEM (packed bf16) and
+//                          used as the A operand of O += P V.
+//   attn_bwd_dkdv4_kernel  CTA = 128 keys x one head, loop over 128-query blocks:
+//                          S^T, dP^T in TMEM; P^T, dS^T written back into TMEM
+//                          as A operands of dV += P^T dO, dK += dS^T Q.
+//   attn_bwd_dq4_kernel    CTA = 128 queries x one head (Q, dO resident in TMEM as
+//                          A operands), loop over 128-key blocks: S, dP, dS into
+//                          TMEM, dQ += dS K.
+// dQ and dK leave through RoPE^T (gradients w.r.t. the pre-rotation Q, K) and the
+// softmax scale; D = rowsum(dO o O) comes from attn_bwd_dot_kernel (attention.cu).
 //
-// Operand layouts (all SWIZZLE_128B, TMA boxes of 64 columns x 128 rows of the
-// [s][3*heads*d] QKV buffer): Q and K are K-major (K = d), V is MN-major (N = d,
-// K = keys), P is K-major (K = keys) written by the softmax warps.
+// Operand layouts: every smem tile is a TMA box of 64 columns x 128 rows of the
+// row-major [s][3*heads*d] QKV (or [s][heads*d] dO) buffer, SWIZZLE_128B; a tile is
+// read K-major when the contraction runs over d and MN-major when it runs over rows.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -35,19 +40,6 @@ constexpr int BN = 128;  // keys per block
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-template <int D>
-struct Cfg {
-  static constexpr int ATOMS = D / 64;                 // 64-column atoms per row
-  static constexpr int TILE = 128 * D * 2;             // one [128][D] bf16 tile
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = TILE;                   // 2 stages of K
-  static constexpr int V_OFF = K_OFF + 2 * TILE;       // 2 stages of V
-  static constexpr int P_OFF = V_OFF + 2 * TILE;       // P [128][128] bf16
-  static constexpr int BAR_OFF = P_OFF + 128 * 128 * 2;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr int S_COL = 0;                      // S buffers at columns 0, 128
-  static constexpr int O_COL = 256;
-};
 
 }  // namespace attn_tc
 
@@ -363,666 +355,6 @@ __device__ __forceinline__ void store32_bf16(__nv_bfloat16* dst, const float* v)
                        pack_bf16(v[8 * e + 4], v[8 * e + 5]), pack_bf16(v[8 * e + 6], v[8 * e + 7]));
 }
 
-// ---------------------------------------------------------------- dK / dV
-// CTA = (128-key block, head); loop over 64-query blocks.  Thread t of warps 4..7
-// owns key row t: S^T = K Q^T and dP^T = V dO^T land in TMEM (double-buffered),
-// P^T = exp2(S^T scale - lse), dS^T = P^T (dP^T - D) go to shared memory (K-major,
-// K = queries) and feed dV += P^T dO, dK += dS^T Q (dO, Q read MN-major from the
-// same tiles).  dK gets the softmax scale and RoPE^T in the epilogue.
-template <int D>
-struct BwdKVCfg {
-  static constexpr int KT = 128 * D * 2;     // K or V tile [128][D]
-  static constexpr int QT = 64 * D * 2;      // Q or dO tile [64][D]
-  static constexpr int K_OFF = 0, V_OFF = KT;
-  static constexpr int Q_OFF = 2 * KT;       // [2]
-  static constexpr int O_OFF = Q_OFF + 2 * QT;   // dO [2]
-  static constexpr int P_OFF = O_OFF + 2 * QT;   // P^T [2][128][64]
-  static constexpr int S_OFF = P_OFF + 2 * 16384;  // dS^T [2]
-  static constexpr int L_OFF = S_OFF + 2 * 16384;  // lse [2][64], D [2][64] floats
-  static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
-                            const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
-                            const float* __restrict__ Dd, int s, int heads, int causal,
-                            __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
-                            float scale, float scale_log2) {
-  using C = BwdKVCfg<D>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;     // [2]
-  uint64_t* q_empty = bar + 3;    // [2]
-  uint64_t* st_full = bar + 5;    // [2]
-  uint64_t* st_empty = bar + 7;   // [2]
-  uint64_t* p_full = bar + 9;     // [2]
-  uint64_t* pd_done = bar + 11;   // [2]
-  uint64_t* fin = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, head = blockIdx.y;
-  const int hq = heads * D;
-  const int k0 = kb * 128;
-  const int qstart = causal ? k0 / 64 : 0;
-  const int nq = s / 64 - qstart;
-  constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tkv);
-    tma_prefetch(&tq);
-    tma_prefetch(&tdo);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-      mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 8);
-      mbar_init(&p_full[i], 8);
-      mbar_init(&pd_done[i], 1);
-    }
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      mbar_arrive_expect_tx(kv_full, 2 * C::KT);
-      for (int a = 0; a < D / 64; ++a) {
-        tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, hq + head * D + a * 64, k0);
-        tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, 2 * hq + head * D + a * 64, k0);
-      }
-      for (int i = 0; i < nq; ++i) {
-        const int b = i & 1, q0 = (qstart + i) * 64;
-        if (i >= 2) mbar_wait(&q_empty[b], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[b], 2 * C::QT + 2 * 256);
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::Q_OFF + b * C::QT + a * 8192, &tq, &q_full[b], head * D + a * 64, q0);
-          tma_load_2d(sm + C::O_OFF + b * C::QT + a * 8192, &tdo, &q_full[b], head * D + a * 64, q0);
-        }
-        bulk_load(sm + C::L_OFF + b * 256, lse + (int64_t)head * s + q0, 256, &q_full[b]);
-        bulk_load(sm + C::L_OFF + 512 + b * 256, Dd + (int64_t)head * s + q0, 256, &q_full[b]);
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_st = umma_idesc_bf16(128, 64, 0, 0);
-    constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
-    const uint32_t sk = smem_u32(sm + C::K_OFF), sv = smem_u32(sm + C::V_OFF);
-    mbar_wait(kv_full, 0);
-    auto dkdv = [&](int i) {
-      const int b = i & 1;
-      mbar_wait(&p_full[b], (i >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
-        const uint32_t sp = smem_u32(sm + C::P_OFF + b * 16384), ss = smem_u32(sm + C::S_OFF + b * 16384);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          umma_f16(tmem + DV_COL, kmaj_desc(sp, kk), mnmaj_desc(so, kk, 8192), idesc_acc, (i | kk) != 0);
-          umma_f16(tmem + DK_COL, kmaj_desc(ss, kk), mnmaj_desc(sq, kk, 8192), idesc_acc, (i | kk) != 0);
-        }
-        umma_commit(&pd_done[b]);
-        umma_commit(&q_empty[b]);
-      }
-      __syncwarp();
-    };
-    for (int i = 0; i < nq; ++i) {
-      const int b = i & 1;
-      mbar_wait(&q_full[b], (i >> 1) & 1);
-      if (i >= 2) mbar_wait(&st_empty[b], ((i >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + ST_COL + b * 64, kmaj_desc(sk, kk), kmaj_desc(sq, kk, 8192), idesc_st, kk > 0);
-          umma_f16(tmem + DP_COL + b * 64, kmaj_desc(sv, kk), kmaj_desc(so, kk, 8192), idesc_st, kk > 0);
-        }
-        umma_commit(&st_full[b]);
-      }
-      __syncwarp();
-      if (i >= 1) dkdv(i - 1);
-    }
-    dkdv(nq - 1);
-    if (elect_one()) umma_commit(fin);
-    __syncwarp();
-  } else if (warp >= 4) {
-    // two warpgroups: wg owns query columns [32 wg, 32 wg + 32) of every key row
-    const int wg = (warp - 4) >> 2;
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const int key = k0 + t;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    for (int i = 0; i < nq; ++i) {
-      const int b = i & 1, q0 = (qstart + i) * 64;
-      mbar_wait(&st_full[b], (i >> 1) & 1);
-      tc_fence_after();
-      const float* L = reinterpret_cast<const float*>(sm + C::L_OFF + b * 256);
-      const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + 512 + b * 256);
-      const bool mask = causal && (q0 < k0 + 128);
-      uint32_t pk[16], dk[16];
-      {
-        uint32_t cs[16], cd[16], ns[16], nd[16];
-        const uint32_t c0 = b * 64 + wg * 32;
-        tmem_ld16(lb + ST_COL + c0, cs);
-        tmem_ld16(lb + DP_COL + c0, cd);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          if (c == 0) {
-            tmem_ld16(lb + ST_COL + c0 + 16, ns);
-            tmem_ld16(lb + DP_COL + c0 + 16, nd);
-          }
-#pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            const int qi = wg * 32 + c * 16 + e;
-            float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -L[qi] * LOG2E));
-            float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -L[qi + 1] * LOG2E));
-            if (mask) {
-              if (key > q0 + qi) p0 = 0.f;
-              if (key > q0 + qi + 1) p1 = 0.f;
-            }
-            const float d0 = p0 * (__uint_as_float(cd[e]) - Dv[qi]);
-            const float d1 = p1 * (__uint_as_float(cd[e + 1]) - Dv[qi + 1]);
-            pk[c * 8 + (e >> 1)] = pack_bf16(p0, p1);
-            dk[c * 8 + (e >> 1)] = pack_bf16(d0, d1);
-          }
-          if (c == 0) {
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) { cs[j] = ns[j]; cd[j] = nd[j]; }
-          }
-        }
-      }
-            tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[b]);
-      if (i >= 2) mbar_wait(&pd_done[b], ((i >> 1) - 1) & 1);
-      uint8_t* PT = sm + C::P_OFF + b * 16384;
-      uint8_t* ST = sm + C::S_OFF + b * 16384;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        st_sw128(PT, 16384, t, 0, wg * 4 + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
-        st_sw128(ST, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-    }
-    // epilogue: warpgroup 0 drains dK (scale, RoPE^T), warpgroup 1 drains dV
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
-    if (wg == 0) {
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t ra[32], rb[32];
-        tmem_ld32(lb + DK_COL + c * 32, ra);
-        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
-        tmem_ld_wait();
-        float a[32], bb[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
-        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
-        store32_bf16(rowp + hq + c * 32, a);
-        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(lb + DV_COL + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        store32_bf16(rowp + 2 * hq + c * 32, v);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ---------------------------------------------------------------- dQ
-// CTA = (128-query block, head); loop over 64-key blocks: S = Q K^T, dP = dO V^T
-// in TMEM (double-buffered); dS = P (dP - D) -> shared memory (K-major, K = keys);
-// dQ += dS K (K read MN-major) accumulates in TMEM; epilogue scale + RoPE^T.
-template <int D>
-struct BwdQCfg {
-  static constexpr int QT = 128 * D * 2;    // Q or dO [128][D]
-  static constexpr int KT = 64 * D * 2;     // K or V [64][D]
-  static constexpr int Q_OFF = 0, O_OFF = QT;
-  static constexpr int K_OFF = 2 * QT;      // [2]
-  static constexpr int V_OFF = K_OFF + 2 * KT;  // [2]
-  static constexpr int S_OFF = V_OFF + 2 * KT;  // dS [2][128][64]
-  static constexpr int L_OFF = S_OFF + 2 * 16384;   // lse [128], D [128]
-  static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(256, 1)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                          const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
-                          const float* __restrict__ Dd, int s, int heads, int causal,
-                          __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
-                          float scale, float scale_log2) {
-  using C = BwdQCfg<D>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;    // [2]
-  uint64_t* kv_empty = bar + 3;   // [2]
-  uint64_t* sd_full = bar + 5;    // [2]
-  uint64_t* sd_empty = bar + 7;   // [2]
-  uint64_t* ds_full = bar + 9;    // [2]
-  uint64_t* dq_done = bar + 11;   // [2]
-  uint64_t* fin = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = s / 128;
-  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
-  const int head = blockIdx.y;
-  const int hq = heads * D;
-  const int q0 = qb * 128;
-  const int nkv = causal ? (q0 + 128) / 64 : s / 64;
-  constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tq);
-    tma_prefetch(&tdo);
-    tma_prefetch(&tkv);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&sd_empty[i], 4);
-      mbar_init(&ds_full[i], 4);
-      mbar_init(&dq_done[i], 1);
-    }
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, 2 * C::QT + 2 * 512);
-      for (int a = 0; a < D / 64; ++a) {
-        tma_load_2d(sm + C::Q_OFF + a * 16384, &tq, q_full, head * D + a * 64, q0);
-        tma_load_2d(sm + C::O_OFF + a * 16384, &tdo, q_full, head * D + a * 64, q0);
-      }
-      bulk_load(sm + C::L_OFF, lse + (int64_t)head * s + q0, 512, q_full);
-      bulk_load(sm + C::L_OFF + 512, Dd + (int64_t)head * s + q0, 512, q_full);
-      for (int j = 0; j < nkv; ++j) {
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[b], ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
-          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
-    const uint32_t sq = smem_u32(sm + C::Q_OFF), so = smem_u32(sm + C::O_OFF);
-    mbar_wait(q_full, 0);
-    auto dq = [&](int j) {
-      const int b = j & 1;
-      mbar_wait(&ds_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sd = smem_u32(sm + C::S_OFF + b * 16384), sk = smem_u32(sm + C::K_OFF + b * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16(tmem + DQ_COL, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
-        umma_commit(&dq_done[b]);
-        umma_commit(&kv_empty[b]);
-      }
-      __syncwarp();
-    };
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      mbar_wait(&kv_full[b], (j >> 1) & 1);
-      if (j >= 2) mbar_wait(&sd_empty[b], ((j >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sk = smem_u32(sm + C::K_OFF + b * C::KT), sv = smem_u32(sm + C::V_OFF + b * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + S_COL + b * 64, kmaj_desc(sq, kk), kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
-          umma_f16(tmem + DP_COL + b * 64, kmaj_desc(so, kk), kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
-        }
-        umma_commit(&sd_full[b]);
-      }
-      __syncwarp();
-      if (j >= 1) dq(j - 1);
-    }
-    dq(nkv - 1);
-    if (elect_one()) umma_commit(fin);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const int row = q0 + t;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    mbar_wait(q_full, 0);
-    const float l2 = reinterpret_cast<const float*>(sm + C::L_OFF)[t] * LOG2E;
-    const float dd = reinterpret_cast<const float*>(sm + C::L_OFF + 512)[t];
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1, k0 = j * 64;
-      mbar_wait(&sd_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      const bool mask = causal && (k0 + 63 > q0);
-      uint32_t dk[2][16];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(lb + S_COL + b * 64 + c * 32, sr);
-        tmem_ld32(lb + DP_COL + b * 64 + c * 32, dr);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(sr[e]), scale_log2, -l2));
-          const float x1 = fmaf(__uint_as_float(sr[e + 1]), scale_log2, -l2);
-          float p1 = ex2(x1);
-          if (mask) {
-            if (k0 + c * 32 + e > row) p0 = 0.f;
-            if (k0 + c * 32 + e + 1 > row) p1 = 0.f;
-          }
-          dk[c][e >> 1] = pack_bf16(p0 * (__uint_as_float(dr[e]) - dd), p1 * (__uint_as_float(dr[e + 1]) - dd));
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sd_empty[b]);
-      if (j >= 2) mbar_wait(&dq_done[b], ((j >> 1) - 1) & 1);
-      uint8_t* DS = sm + C::S_OFF + b * 16384;
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          st_sw128(DS, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[b]);
-    }
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
-#pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t ra[32], rb[32];
-      tmem_ld32(lb + DQ_COL + c * 32, ra);
-      tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
-      tmem_ld_wait();
-      float a[32], bb[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
-      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
-      store32_bf16(rowp + c * 32, a);
-      store32_bf16(rowp + c * 32 + D / 2, bb);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ---------------------------------------------------------------- dQ, two query tiles
-// CTA = (256 queries = tiles 0 and 1, head); 64-key blocks staged once for both tiles.
-// TMEM per tile t: S_t (64) | dP_t (64) | dQ_t (128) at column 256 t.  MMA order per
-// block j: S/dP_0(j), S/dP_1(j), dQ_0(j), S/dP_0(j+1), dQ_1(j), S/dP_1(j+1), ... so one
-// tile's elementwise pass overlaps the other tile's MMAs.  Because one thread's
-// tcgen05 MMAs execute in order, S_t(j+1) completing implies dQ_t(j) finished reading
-// dS_t, so the elementwise warps may overwrite dS_t as soon as S_t(j+1) is ready.
-template <int D>
-struct BwdQ2Cfg {
-  static constexpr int QT = 128 * D * 2;
-  static constexpr int KT = 64 * D * 2;
-  static constexpr int Q_OFF = 0;               // Q0, Q1
-  static constexpr int O_OFF = 2 * QT;          // dO0, dO1
-  static constexpr int K_OFF = 4 * QT;          // [2 stages]
-  static constexpr int V_OFF = K_OFF + 2 * KT;  // [2 stages]
-  static constexpr int S_OFF = V_OFF + 2 * KT;  // dS_0, dS_1 [128][64]
-  static constexpr int BAR_OFF = S_OFF + 2 * 16384;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq2_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo,
-                           const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
-                           const float* __restrict__ Dd, int s, int heads, int causal,
-                           __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope,
-                           float scale, float scale_log2) {
-  using C = BwdQ2Cfg<D>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;    // [2]
-  uint64_t* kv_empty = bar + 3;   // [2]
-  uint64_t* sd_full = bar + 5;    // [2] per tile
-  uint64_t* ds_full = bar + 7;    // [2] per tile
-  uint64_t* fin = bar + 9;        // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (s + 255) / 256;
-  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
-  const int head = blockIdx.y;
-  const int hq = heads * D;
-  const int q0 = qb * 256;
-  const int nk[2] = {causal ? min(s, q0 + 128) / 64 : s / 64, causal ? min(s, q0 + 256) / 64 : s / 64};
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tq);
-    tma_prefetch(&tdo);
-    tma_prefetch(&tkv);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&ds_full[i], 4);
-      mbar_init(&fin[i], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, 4 * C::QT);
-      for (int t = 0; t < 2; ++t)
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::Q_OFF + t * C::QT + a * 16384, &tq, q_full, head * D + a * 64, q0 + 128 * t);
-          tma_load_2d(sm + C::O_OFF + t * C::QT + a * 16384, &tdo, q_full, head * D + a * 64, q0 + 128 * t);
-        }
-      for (int j = 0; j < nk[1]; ++j) {
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(&kv_empty[b], ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
-          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
-    mbar_wait(q_full, 0);
-    int kv_ready = -1;
-    auto need_kv = [&](int j) {
-      if (kv_ready < j) {
-        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
-        tc_fence_after();
-        kv_ready = j;
-      }
-    };
-    auto issue_sd = [&](int t, int j) {
-      need_kv(j);
-      if (elect_one()) {
-        const uint32_t sq = smem_u32(sm + C::Q_OFF + t * C::QT), so = smem_u32(sm + C::O_OFF + t * C::QT);
-        const uint32_t sk = smem_u32(sm + C::K_OFF + (j & 1) * C::KT), sv = smem_u32(sm + C::V_OFF + (j & 1) * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + t * 256, kmaj_desc(sq, kk), kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
-          umma_f16(tmem + t * 256 + 64, kmaj_desc(so, kk), kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
-        }
-        umma_commit(&sd_full[t]);
-      }
-      __syncwarp();
-    };
-    auto issue_dq = [&](int t, int j) {
-      mbar_wait(&ds_full[t], j & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sd = smem_u32(sm + C::S_OFF + t * 16384), sk = smem_u32(sm + C::K_OFF + (j & 1) * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16(tmem + t * 256 + 128, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
-      }
-      __syncwarp();
-    };
-    if (nk[0] > 0) issue_sd(0, 0);
-    issue_sd(1, 0);
-    for (int j = 0; j < nk[1]; ++j) {
-      if (j < nk[0]) {
-        issue_dq(0, j);
-        if (j + 1 < nk[0]) issue_sd(0, j + 1);
-        else if (elect_one()) umma_commit(&fin[0]);
-        __syncwarp();
-      }
-      issue_dq(1, j);
-      if (elect_one()) umma_commit(&kv_empty[j & 1]);
-      __syncwarp();
-      if (j + 1 < nk[1]) issue_sd(1, j + 1);
-      else if (elect_one()) umma_commit(&fin[1]);
-      __syncwarp();
-    }
-    if (nk[0] == 0 && elect_one()) umma_commit(&fin[0]);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int tile = (warp - 4) >> 2;
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const int row = q0 + tile * 128 + t;
-    const bool ok = row < s;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + tile * 256;
-    const float l2 = ok ? lse[(int64_t)head * s + row] * LOG2E : 0.f;
-    const float dd = ok ? Dd[(int64_t)head * s + row] : 0.f;
-    uint8_t* DS = sm + C::S_OFF + tile * 16384;
-    for (int j = 0; j < nk[tile]; ++j) {
-      const int k0 = j * 64;
-      mbar_wait(&sd_full[tile], j & 1);
-      tc_fence_after();
-      const bool mask = causal && (k0 + 63 > q0 + tile * 128);
-      uint32_t dk[2][16];
-      // S and dP rows in 16-key chunks, next chunk's loads in flight while processing
-      {
-        uint32_t cs[16], cd[16], ns[16], nd[16];
-        tmem_ld16(lb + 0, cs);
-        tmem_ld16(lb + 64, cd);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < 3) {
-            tmem_ld16(lb + (c + 1) * 16, ns);
-            tmem_ld16(lb + 64 + (c + 1) * 16, nd);
-          }
-#pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -l2));
-            float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -l2));
-            if (mask) {
-              if (k0 + c * 16 + e > row) p0 = 0.f;
-              if (k0 + c * 16 + e + 1 > row) p1 = 0.f;
-            }
-            dk[c >> 1][(c & 1) * 8 + (e >> 1)] =
-                pack_bf16(p0 * (__uint_as_float(cd[e]) - dd), p1 * (__uint_as_float(cd[e + 1]) - dd));
-          }
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) { cs[i] = ns[i]; cd[i] = nd[i]; }
-        }
-      }
-      #pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          st_sw128(DS, 16384, t, 0, c * 4 + e, make_uint4(dk[c][4 * e], dk[c][4 * e + 1], dk[c][4 * e + 2], dk[c][4 * e + 3]));
-      tc_fence_before();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[tile]);
-    }
-    mbar_wait(&fin[tile], 0);
-    tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
-#pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t ra[32], rb[32];
-      tmem_ld32(lb + 128 + c * 32, ra);
-      tmem_ld32(lb + 128 + c * 32 + D / 2, rb);
-      tmem_ld_wait();
-      float a[32], bb[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
-      if (ok) {
-        rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
-        store32_bf16(rowp + c * 32, a);
-        store32_bf16(rowp + c * 32 + D / 2, bb);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-// ================================================================== backward v3
-// The fixed operand of each backward MMA lives in TMEM (A operand from TMEM), so
-// the tensor core reads only the streaming operand from shared memory:
-//   dK/dV kernel: K and V of the CTA's 128 keys are packed into TMEM once; per 64-query
-//     block S^T = K Q^T and dP^T = V dO^T read only Q / dO from shared memory.
-//   dQ kernel: Q and dO of the CTA's 128 queries are packed into TMEM once; per
-//     64-key block S = Q K^T and dP = dO V^T read only K / V from shared memory.
-// Packing: lane = row, 32-bit column c holds elements (2c, 2c+1) of the K dimension.
-
-// thread-row load of 128 bf16 (D = 128) or 64 (D = 64) values into TMEM columns [col, col + D/2)
 template <int D>
 __device__ __forceinline__ void row_to_tmem(uint32_t lb, uint32_t col, const __nv_bfloat16* src, bool ok) {
 #pragma unroll
@@ -1038,402 +370,9 @@ __device__ __forceinline__ void row_to_tmem(uint32_t lb, uint32_t col, const __n
   }
 }
 
-template <int D>
-struct BwdKV3Cfg {
-  static constexpr int QT = 64 * D * 2;      // Q or dO tile [64][D]
-  static constexpr int NST = 3;              // query-block stages
-  static constexpr int Q_OFF = 0;            // [NST]
-  static constexpr int O_OFF = NST * QT;     // [NST]
-  static constexpr int P_OFF = 2 * NST * QT; // P^T [2][128][64]
-  static constexpr int S_OFF = P_OFF + 2 * 16384;
-  static constexpr int L_OFF = S_OFF + 2 * 16384;   // lse / D [NST][64] each
-  static constexpr int BAR_OFF = L_OFF + 2 * NST * 256;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkdv3_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __grid_constant__ CUtensorMap tq,
-                          const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
-                          const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
-                          const float2* __restrict__ rope, float scale, float scale_log2) {
-  using C = BwdKV3Cfg<D>;
-  constexpr int NST = C::NST;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* q_full = bar + 0;              // [NST]
-  uint64_t* q_empty = bar + NST;           // [NST]
-  uint64_t* st_full = bar + 2 * NST;
-  uint64_t* st_empty = bar + 2 * NST + 1;
-  uint64_t* p_full = bar + 2 * NST + 2;    // [2]
-  uint64_t* pd_done = bar + 2 * NST + 4;   // [2]
-  uint64_t* kv_ready = bar + 2 * NST + 6;
-  uint64_t* fin = bar + 2 * NST + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 8);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, head = blockIdx.y;
-  const int hq = heads * D;
-  const int k0 = kb * 128;
-  const int qstart = causal ? k0 / 64 : 0;
-  const int nq = s / 64 - qstart;
-  constexpr int K_COL = 0, V_COL = 64, ST_COL = 128, DP_COL = 192, DV_COL = 256, DK_COL = 384;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tq);
-    tma_prefetch(&tdo);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-    }
-    mbar_init(st_full, 1);
-    mbar_init(st_empty, 8);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&p_full[i], 8);
-      mbar_init(&pd_done[i], 1);
-    }
-    mbar_init(kv_ready, 8);
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      for (int i = 0; i < nq; ++i) {
-        const int b = i % NST, q0 = (qstart + i) * 64;
-        if (i >= NST) mbar_wait(&q_empty[b], ((i / NST) - 1) & 1);
-        mbar_arrive_expect_tx(&q_full[b], 2 * C::QT + 2 * 256);
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::Q_OFF + b * C::QT + a * 8192, &tq, &q_full[b], head * D + a * 64, q0);
-          tma_load_2d(sm + C::O_OFF + b * C::QT + a * 8192, &tdo, &q_full[b], head * D + a * 64, q0);
-        }
-        bulk_load(sm + C::L_OFF + b * 256, lse + (int64_t)head * s + q0, 256, &q_full[b]);
-        bulk_load(sm + C::L_OFF + NST * 256 + b * 256, Dd + (int64_t)head * s + q0, 256, &q_full[b]);
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_st = umma_idesc_bf16(128, 64, 0, 0);
-    constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
-    mbar_wait(kv_ready, 0);
-    tc_fence_after();
-    auto dkdv = [&](int i) {
-      const int b = i % NST, pb = i & 1;
-      mbar_wait(&p_full[pb], (i >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
-        const uint32_t sp = smem_u32(sm + C::P_OFF + pb * 16384), ss = smem_u32(sm + C::S_OFF + pb * 16384);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          umma_f16(tmem + DV_COL, kmaj_desc(sp, kk), mnmaj_desc(so, kk, 8192), idesc_acc, (i | kk) != 0);
-          umma_f16(tmem + DK_COL, kmaj_desc(ss, kk), mnmaj_desc(sq, kk, 8192), idesc_acc, (i | kk) != 0);
-        }
-        umma_commit(&pd_done[pb]);
-        umma_commit(&q_empty[b]);
-      }
-      __syncwarp();
-    };
-    for (int i = 0; i < nq; ++i) {
-      const int b = i % NST;
-      mbar_wait(&q_full[b], (i / NST) & 1);
-      if (i >= 1) mbar_wait(st_empty, (i - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sq = smem_u32(sm + C::Q_OFF + b * C::QT), so = smem_u32(sm + C::O_OFF + b * C::QT);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16_ts(tmem + ST_COL, tmem + K_COL + kk * 8, kmaj_desc(sq, kk, 8192), idesc_st, kk > 0);
-          umma_f16_ts(tmem + DP_COL, tmem + V_COL + kk * 8, kmaj_desc(so, kk, 8192), idesc_st, kk > 0);
-        }
-        umma_commit(st_full);
-      }
-      __syncwarp();
-      if (i >= 1) dkdv(i - 1);
-    }
-    dkdv(nq - 1);
-    if (elect_one()) umma_commit(fin);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const int key = k0 + t;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    // K (warpgroup 0) / V (warpgroup 1) rows -> TMEM A operands
-    row_to_tmem<D>(lb, wg ? V_COL : K_COL, qkv + (int64_t)key * ld + (wg ? 2 * hq : hq) + head * D, key < s);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(kv_ready);
-    for (int i = 0; i < nq; ++i) {
-      const int b = i % NST, pb = i & 1, q0 = (qstart + i) * 64;
-      mbar_wait(st_full, i & 1);
-      tc_fence_after();
-      const float* L = reinterpret_cast<const float*>(sm + C::L_OFF + b * 256);
-      const float* Dv = reinterpret_cast<const float*>(sm + C::L_OFF + NST * 256 + b * 256);
-      const bool mask = causal && (q0 < k0 + 128);
-      uint32_t cs[32], cd[32];
-      tmem_ld32(lb + ST_COL + wg * 32, cs);
-      tmem_ld32(lb + DP_COL + wg * 32, cd);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(st_empty);
-      uint32_t pk[16], dk[16];
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        const int qi = wg * 32 + e;
-        float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -L[qi] * LOG2E));
-        float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -L[qi + 1] * LOG2E));
-        if (mask) {
-          if (key > q0 + qi) p0 = 0.f;
-          if (key > q0 + qi + 1) p1 = 0.f;
-        }
-        pk[e >> 1] = pack_bf16(p0, p1);
-        dk[e >> 1] = pack_bf16(p0 * (__uint_as_float(cd[e]) - Dv[qi]), p1 * (__uint_as_float(cd[e + 1]) - Dv[qi + 1]));
-      }
-      if (i >= 2) mbar_wait(&pd_done[pb], ((i >> 1) - 1) & 1);
-      uint8_t* PT = sm + C::P_OFF + pb * 16384;
-      uint8_t* ST = sm + C::S_OFF + pb * 16384;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        st_sw128(PT, 16384, t, 0, wg * 4 + e, make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]));
-        st_sw128(ST, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[pb]);
-    }
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
-    if (wg == 0) {
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t ra[32], rb[32];
-        tmem_ld32(lb + DK_COL + c * 32, ra);
-        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
-        tmem_ld_wait();
-        float a[32], bb[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
-        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
-        store32_bf16(rowp + hq + c * 32, a);
-        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(lb + DV_COL + c * 32, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        store32_bf16(rowp + 2 * hq + c * 32, v);
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-template <int D>
-struct BwdQ3Cfg {
-  static constexpr int KT = 64 * D * 2;     // K or V [64][D]
-  static constexpr int NST = 3;
-  static constexpr int K_OFF = 0;           // [NST]
-  static constexpr int V_OFF = NST * KT;    // [NST]
-  static constexpr int S_OFF = 2 * NST * KT;   // dS [2][128][64]
-  static constexpr int BAR_OFF = S_OFF + 2 * 16384;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq3_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
-                        int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
-                        const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
-                        const float2* __restrict__ rope, float scale, float scale_log2) {
-  using C = BwdQ3Cfg<D>;
-  constexpr int NST = C::NST;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
-  uint64_t* kv_full = bar + 0;            // [NST]
-  uint64_t* kv_empty = bar + NST;         // [NST]
-  uint64_t* sd_full = bar + 2 * NST;      // [2]
-  uint64_t* sd_empty = bar + 2 * NST + 2; // [2]
-  uint64_t* ds_full = bar + 2 * NST + 4;  // [2]
-  uint64_t* dq_done = bar + 2 * NST + 6;  // [2]
-  uint64_t* q_ready = bar + 2 * NST + 8;
-  uint64_t* fin = bar + 2 * NST + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 10);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = s / 128;
-  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
-  const int head = blockIdx.y;
-  const int hq = heads * D;
-  const int q0 = qb * 128;
-  const int nkv = causal ? (q0 + 128) / 64 : s / 64;
-  constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tkv);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&sd_empty[i], 8);
-      mbar_init(&ds_full[i], 8);
-      mbar_init(&dq_done[i], 1);
-    }
-    mbar_init(q_ready, 8);
-    mbar_init(fin, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      for (int j = 0; j < nkv; ++j) {
-        const int b = j % NST;
-        if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
-        mbar_arrive_expect_tx(&kv_full[b], 2 * C::KT);
-        for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], hq + head * D + a * 64, j * 64);
-          tma_load_2d(sm + C::V_OFF + b * C::KT + a * 8192, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 64);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 64, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(128, D, 0, 1);
-    mbar_wait(q_ready, 0);
-    tc_fence_after();
-    auto dq = [&](int j) {
-      const int b = j % NST, sb = j & 1;
-      mbar_wait(&ds_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sd = smem_u32(sm + C::S_OFF + sb * 16384), sk = smem_u32(sm + C::K_OFF + b * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16(tmem + DQ_COL, kmaj_desc(sd, kk), mnmaj_desc(sk, kk, 8192), idesc_q, (j | kk) != 0);
-        umma_commit(&dq_done[sb]);
-        umma_commit(&kv_empty[b]);
-      }
-      __syncwarp();
-    };
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j % NST, sb = j & 1;
-      mbar_wait(&kv_full[b], (j / NST) & 1);
-      if (j >= 2) mbar_wait(&sd_empty[sb], ((j >> 1) - 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sk = smem_u32(sm + C::K_OFF + b * C::KT), sv = smem_u32(sm + C::V_OFF + b * C::KT);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16_ts(tmem + S_COL + sb * 64, tmem + Q_COL + kk * 8, kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
-          umma_f16_ts(tmem + DP_COL + sb * 64, tmem + O_COL + kk * 8, kmaj_desc(sv, kk, 8192), idesc_s, kk > 0);
-        }
-        umma_commit(&sd_full[sb]);
-      }
-      __syncwarp();
-      if (j >= 1) dq(j - 1);
-    }
-    dq(nkv - 1);
-    if (elect_one()) umma_commit(fin);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;          // key columns [32 wg, 32 wg + 32) of each block
-    const int q = warp & 3;
-    const int t = q * 32 + lane;
-    const int row = q0 + t;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    if (wg == 0) row_to_tmem<D>(lb, Q_COL, qkv + (int64_t)row * ld + head * D, true);
-    else row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(q_ready);
-    const float l2 = lse[(int64_t)head * s + row] * LOG2E;
-    const float dd = Dd[(int64_t)head * s + row];
-    for (int j = 0; j < nkv; ++j) {
-      const int sb = j & 1, k0 = j * 64;
-      mbar_wait(&sd_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      const bool mask = causal && (k0 + 63 > q0);
-      uint32_t cs[32], cd[32];
-      tmem_ld32(lb + S_COL + sb * 64 + wg * 32, cs);
-      tmem_ld32(lb + DP_COL + sb * 64 + wg * 32, cd);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sd_empty[sb]);
-      uint32_t dk[16];
-#pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        float p0 = ex2(fmaf(__uint_as_float(cs[e]), scale_log2, -l2));
-        float p1 = ex2(fmaf(__uint_as_float(cs[e + 1]), scale_log2, -l2));
-        if (mask) {
-          if (k0 + wg * 32 + e > row) p0 = 0.f;
-          if (k0 + wg * 32 + e + 1 > row) p1 = 0.f;
-        }
-        dk[e >> 1] = pack_bf16(p0 * (__uint_as_float(cd[e]) - dd), p1 * (__uint_as_float(cd[e + 1]) - dd));
-      }
-      if (j >= 2) mbar_wait(&dq_done[sb], ((j >> 1) - 1) & 1);
-      uint8_t* DS = sm + C::S_OFF + sb * 16384;
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        st_sw128(DS, 16384, t, 0, wg * 4 + e, make_uint4(dk[4 * e], dk[4 * e + 1], dk[4 * e + 2], dk[4 * e + 3]));
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[sb]);
-    }
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
-    // warpgroup w drains the RoPE pair chunk c = w (D = 128) / both halves (D = 64, wg 0)
-    for (int c = wg; c < D / 64; c += 2) {
-      uint32_t ra[32], rb[32];
-      tmem_ld32(lb + DQ_COL + c * 32, ra);
-      tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
-      tmem_ld_wait();
-      float a[32], bb[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
-      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
-      store32_bf16(rowp + c * 32, a);
-      store32_bf16(rowp + c * 32 + D / 2, bb);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 // ============================================================ backward v4
-// 128 x 128 blocks everywhere (every MMA has N = 128: the N = 64 MMAs of v3 run at
-// 2/3 of the tensor peak, tools/mma_probe.cu).  The elementwise results P^T / dS^T
+// 128 x 128 blocks everywhere: every MMA has N = 128 (tcgen05 MMAs with N = 64 run
+// at 2/3 of the tensor peak, tools/mma_probe.cu).  The elementwise results P^T / dS^T
 // (dK/dV kernel) and dS (dQ kernel) are written back into TMEM as packed bf16 and
 // used as the A operand of the next MMA, so no shared-memory round trip and no
 // generic->async proxy fence sits on the critical path.  Two elementwise
@@ -1970,75 +909,26 @@ template <int D>
 static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
                     int s, int heads, int causal, void* dqkv, const void* rope, cudaStream_t st) {
   const uint64_t cols = (uint64_t)3 * heads * D;
-  CUtensorMap kv128, q64, do64, q128, do128, kv64;
+  CUtensorMap kv128, do128;
   int rc = make_map_rows(&kv128, qkv, cols, s, ld, 128);
-  rc |= make_map_rows(&q64, qkv, cols, s, ld, 64);
-  rc |= make_map_rows(&do64, dout, (uint64_t)heads * D, s, ld_out, 64);
-  rc |= make_map_rows(&q128, qkv, cols, s, ld, 128);
   rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, s, ld_out, 128);
-  rc |= make_map_rows(&kv64, qkv, cols, s, ld, 64);
   if (rc) return (int)cudaErrorInvalidValue;
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKVCfg<D>::SMEM);
-    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQCfg<D>::SMEM);
-    cudaFuncSetAttribute(attn_bwd_dq2_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ2Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dq4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
     once = true;
   }
   const float scale = 1.0f / sqrtf((float)D);
   const float scale_log2 = scale * LOG2E;
-  static const int bwdv = [] {
-    const char* e = getenv("PDS_ATTN_BWDV");
-    return e ? atoi(e) : 4;
-  }();
-  if (bwdv >= 4) {
-    static bool once4 = false;
-    if (!once4) {
-      cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
-      cudaFuncSetAttribute(attn_bwd_dq4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
-      once4 = true;
-    }
-    attn_bwd_dkdv4_kernel<D><<<dim3(s / 128, heads), 384, BwdKV4Cfg<D>::SMEM, st>>>(
-        kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
-    attn_bwd_dq4_kernel<D><<<dim3(s / 128, heads), 384, BwdQ4Cfg<D>::SMEM, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out,
-        kv128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2);
-    return (int)cudaGetLastError();
-  }
-  if (bwdv >= 3) {
-    static bool once3 = false;
-    if (!once3) {
-      cudaFuncSetAttribute(attn_bwd_dkdv3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV3Cfg<D>::SMEM);
-      cudaFuncSetAttribute(attn_bwd_dq3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ3Cfg<D>::SMEM);
-      once3 = true;
-    }
-    attn_bwd_dkdv3_kernel<D><<<dim3(s / 128, heads), 384, BwdKV3Cfg<D>::SMEM, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, q64, do64, reinterpret_cast<const float*>(lse), Dd, s,
-        heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv), reinterpret_cast<const float2*>(rope), scale,
-        scale_log2);
-    attn_bwd_dq3_kernel<D><<<dim3(s / 128, heads), 384, BwdQ3Cfg<D>::SMEM, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out,
-        kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2);
-    return (int)cudaGetLastError();
-  }
-  attn_bwd_dkdv_tc_kernel<D><<<dim3(s / 128, heads), 384, BwdKVCfg<D>::SMEM, st>>>(
-      kv128, q64, do64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+  // the Q map is the K/V map (same buffer, same box): only the column offset differs
+  attn_bwd_dkdv4_kernel<D><<<dim3(s / 128, heads), 384, BwdKV4Cfg<D>::SMEM, st>>>(
+      kv128, kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
       reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
-  static const bool dq1 = [] {
-    const char* e = getenv("PDS_ATTN_DQ");
-    return e && e[0] == '1';
-  }();
-  if (dq1)
-    attn_bwd_dq_tc_kernel<D><<<dim3(s / 128, heads), 256, BwdQCfg<D>::SMEM, st>>>(
-        q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
-  else
-    attn_bwd_dq2_tc_kernel<D><<<dim3((s + 255) / 256, heads), 384, BwdQ2Cfg<D>::SMEM, st>>>(
-        q128, do128, kv64, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  attn_bwd_dq4_kernel<D><<<dim3(s / 128, heads), 384, BwdQ4Cfg<D>::SMEM, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
+      reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
+      reinterpret_cast<const float2*>(rope), scale, scale_log2);
   return (int)cudaGetLastError();
 }
 

@@ -3,9 +3,8 @@
 // the RoPE cos/sin table (reading R-3: angles formed in fp64), recompute of a
 // normalised activation from its saved input + rstd, and bf16 add / copy.
 //
-// One warp per row, 16-byte vector loads/stores (8 bf16 per lane per vector),
-// warp-shuffle row reductions; VPL = h / 256 vectors per lane kept in registers
-// so every byte is read once.  Algorithmic bytes per element: fwd 8 B with a
+// Norm kernels: one block per row (fwd) / grid-stride rows (bwd), 16-byte vector
+// loads/stores, each byte read once; the other kernels: one warp per row.  Algorithmic bytes per element: fwd 8 B with a
 // residual (x, res in; x1, u out), bwd 8 B (du, x, dres in; dx out).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -39,103 +38,134 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-template <int VPL>
-__global__ void __launch_bounds__(128)
+// Block-per-row layout for the two norm kernels: NT = min(h / 8, 256) threads, each
+// owning VPT = h / (8 NT) 16-byte vectors of the row (8 bf16 columns per vector), so
+// a row is one fully coalesced pass and the only cross-thread step is the row sum
+// (warp shuffle + one shared-memory exchange).
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < nw; ++w) t += red[w];
+  return t;
+}
+
+template <int VPT>
+__global__ void __launch_bounds__(256)
     rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
                        const __nv_bfloat16* __restrict__ g, int64_t rows, int h, float eps,
                        __nv_bfloat16* __restrict__ x1_out, __nv_bfloat16* __restrict__ u_out,
                        float* __restrict__ rstd_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
-  float v[VPL][8];
+  const uint4* rr = reinterpret_cast<const uint4*>(res + row * h);
+  uint4 w[VPT], rw[VPT];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = threadIdx.x + k * blockDim.x;
+    w[k] = __ldcs(xr + c);
+    if (res) rw[k] = __ldcs(rr + c);
+  }
   float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = lane + i * 32;
-    unpack8(__ldcs(xr + c), v[i]);
+  for (int k = 0; k < VPT; ++k) {
+    const int c = threadIdx.x + k * blockDim.x;
+    float v[8];
+    unpack8(w[k], v);
     if (res) {
       float r[8];
-      unpack8(__ldcs(reinterpret_cast<const uint4*>(res + row * h) + c), r);
+      unpack8(rw[k], r);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[i][e] = __bfloat162float(__float2bfloat16_rn(v[i][e] + r[e]));
-      reinterpret_cast<uint4*>(x1_out + row * h)[c] = pack8(v[i]);
+      for (int e = 0; e < 8; ++e) v[e] += r[e];
+      w[k] = pack8(v);                         // x1 = bf16(x + res)
+      unpack8(w[k], v);
+      reinterpret_cast<uint4*>(x1_out + row * h)[c] = w[k];
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ss += v[i][e] * v[i][e];
+    for (int e = 0; e < 8; ++e) ss += v[e] * v[e];
   }
-  ss = warp_sum(ss);
+  ss = block_sum(ss, red);
   const float r = rsqrtf(ss / (float)h + eps);
-  if (lane == 0) rstd_out[row] = r;
+  if (threadIdx.x == 0) rstd_out[row] = r;
   const uint4* gr = reinterpret_cast<const uint4*>(g);
 #pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = lane + i * 32;
-    float gg[8], o[8];
+  for (int k = 0; k < VPT; ++k) {
+    const int c = threadIdx.x + k * blockDim.x;
+    float v[8], gg[8], o[8];
+    unpack8(w[k], v);
     unpack8(__ldg(gr + c), gg);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = v[i][e] * r * gg[e];
+    for (int e = 0; e < 8; ++e) o[e] = v[e] * r * gg[e];
     reinterpret_cast<uint4*>(u_out + row * h)[c] = pack8(o);
   }
 }
 
-// dx = r (a - xhat mean(a xhat)) + dres, a = du g ; dg_part[block][h] += du xhat
-template <int VPL>
-__global__ void __launch_bounds__(128)
+// dx = r (a - xhat mean(a xhat)) + dres, a = du g, xhat = x r;  dg_part[block][:] =
+// sum over the block's rows of du xhat (each thread keeps its columns' partials in
+// registers across the grid-stride row loop).
+template <int VPT>
+__global__ void __launch_bounds__(256, 3)
     rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ du, const __nv_bfloat16* __restrict__ x,
                        const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ g,
                        const __nv_bfloat16* __restrict__ dres, int64_t rows, int h,
                        __nv_bfloat16* __restrict__ dx, float* __restrict__ dg_part) {
-  extern __shared__ float sdg_all[];   // [4 warps][h]
-  for (int i = threadIdx.x; i < 4 * h; i += blockDim.x) sdg_all[i] = 0.f;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  float* sdg = sdg_all + (threadIdx.x >> 5) * h;
-  const uint4* gr = reinterpret_cast<const uint4*>(g);
-  for (int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5); row < rows;
-       row += (int64_t)gridDim.x * 4) {
+  __shared__ float red[2][8];
+  uint4 gw[VPT];
+  float dga[VPT][8];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    gw[k] = __ldg(reinterpret_cast<const uint4*>(g) + threadIdx.x + k * blockDim.x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) dga[k][e] = 0.f;
+  }
+  int par = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1) {
     const float r = rstd[row];
-    uint4 xr[VPL], dr8[VPL];
+    uint4 xw[VPT], dw[VPT], rw[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      xw[k] = __ldcs(reinterpret_cast<const uint4*>(x + row * h) + c);
+      dw[k] = __ldcs(reinterpret_cast<const uint4*>(du + row * h) + c);
+      if (dres) rw[k] = __ldcs(reinterpret_cast<const uint4*>(dres + row * h) + c);
+    }
     float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      const int c = lane + i * 32;
-      xr[i] = __ldcs(reinterpret_cast<const uint4*>(x + row * h) + c);
-      dr8[i] = __ldcs(reinterpret_cast<const uint4*>(du + row * h) + c);
-    }
-#pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      const int c = lane + i * 32;
+    for (int k = 0; k < VPT; ++k) {
       float xh[8], d8[8], gg[8];
-      unpack8(xr[i], xh);
-      unpack8(dr8[i], d8);
-      unpack8(__ldg(gr + c), gg);
+      unpack8(xw[k], xh);
+      unpack8(dw[k], d8);
+      unpack8(gw[k], gg);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         xh[e] *= r;
         dot += d8[e] * gg[e] * xh[e];
-        sdg[c * 8 + e] += d8[e] * xh[e];
+        dga[k][e] += d8[e] * xh[e];
       }
     }
-    dot = warp_sum(dot) / (float)h;
+    dot = block_sum(dot, red[par]) / (float)h;
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) {
-      const int c = lane + i * 32;
-      float xh[8], d8[8], gg[8], o[8], dr[8];
-      unpack8(xr[i], xh);
-      unpack8(dr8[i], d8);
-      unpack8(__ldg(gr + c), gg);
-      if (dres) unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + row * h) + c), dr);
+    for (int k = 0; k < VPT; ++k) {
+      const int c = threadIdx.x + k * blockDim.x;
+      float xh[8], d8[8], dr[8], o[8], gg[8];
+      unpack8(xw[k], xh);
+      unpack8(dw[k], d8);
+      unpack8(gw[k], gg);
+      if (dres) unpack8(rw[k], dr);
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        o[e] = r * (d8[e] * gg[e] - xh[e] * r * dot) + (dres ? dr[e] : 0.f);
+      for (int e = 0; e < 8; ++e) o[e] = r * (d8[e] * gg[e] - xh[e] * r * dot) + (dres ? dr[e] : 0.f);
       reinterpret_cast<uint4*>(dx + row * h)[c] = pack8(o);
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < h; i += blockDim.x)
-    dg_part[(int64_t)blockIdx.x * h + i] = sdg_all[i] + sdg_all[h + i] + sdg_all[2 * h + i] + sdg_all[3 * h + i];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    float4* o = reinterpret_cast<float4*>(dg_part + (int64_t)blockIdx.x * h + 8 * (threadIdx.x + k * blockDim.x));
+    o[0] = make_float4(dga[k][0], dga[k][1], dga[k][2], dga[k][3]);
+    o[1] = make_float4(dga[k][4], dga[k][5], dga[k][6], dga[k][7]);
+  }
 }
 
 // out[i] += sum_p part[p][i]: 32 columns per block, 8 row groups, smem tree
@@ -247,41 +277,51 @@ __global__ void unpack_blocks_kernel(const uint4* __restrict__ src, int P, int64
 __global__ void __launch_bounds__(256)
     transpose_bf16_kernel(const uint16_t* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
                           uint16_t* __restrict__ dst, int64_t ld_dst, int64_t seg, int64_t stride, int64_t base) {
-  // 64 x 64 tile as 32-bit words (column pairs), row stride 33 words: the 16-byte
-  // loads are stored as 4 conflict-free 32-bit words; the transposed reads hit <= 2
-  // banks per word; two output vectors per thread are assembled with byte permutes.
-  __shared__ uint32_t tile[64][33];
-  const int64_t r0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 64;
+  // Two 64 x 64 tiles (source rows r0 .. r0 + 127) as 32-bit words (column pairs), row
+  // stride 33 words: the 16-byte loads are stored as 4 conflict-free 32-bit words; the
+  // transposed reads hit <= 2 banks per word; two output vectors per thread are
+  // assembled with byte permutes.  All four loads of a thread are issued first.
+  __shared__ uint32_t tile[128][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
   const int t = threadIdx.x;
+  const bool remap = seg < rows;
+  uint4 x[4];
 #pragma unroll
-  for (int h2 = 0; h2 < 2; ++h2) {
-    const int rr = (t >> 3) + 32 * h2, v = t & 7;
+  for (int h4 = 0; h4 < 4; ++h4) {
+    const int rr = (t >> 3) + 32 * h4, v = t & 7;
     const int64_t r = r0 + rr;
-    uint4 x = make_uint4(0, 0, 0, 0);
+    x[h4] = make_uint4(0, 0, 0, 0);
     if (r < rows && c0 + v * 8 < cols) {
-      const int64_t sr = (r / seg) * stride + base + (r % seg);
-      x = __ldcs(reinterpret_cast<const uint4*>(src + sr * ld_src + c0 + v * 8));
+      const int64_t sr = remap ? (r / seg) * stride + base + (r % seg) : r;
+      x[h4] = __ldcs(reinterpret_cast<const uint4*>(src + sr * ld_src + c0 + v * 8));
     }
-    tile[rr][v * 4 + 0] = x.x;
-    tile[rr][v * 4 + 1] = x.y;
-    tile[rr][v * 4 + 2] = x.z;
-    tile[rr][v * 4 + 3] = x.w;
+  }
+#pragma unroll
+  for (int h4 = 0; h4 < 4; ++h4) {
+    const int rr = (t >> 3) + 32 * h4, v = t & 7;
+    tile[rr][v * 4 + 0] = x[h4].x;
+    tile[rr][v * 4 + 1] = x[h4].y;
+    tile[rr][v * 4 + 2] = x[h4].z;
+    tile[rr][v * 4 + 3] = x[h4].w;
   }
   __syncthreads();
-  // thread -> column pair cp (dst rows c0 + 2cp, +1), source rows rb*8 .. +7
+  // thread -> column pair cp (dst rows c0 + 2cp, +1), source rows rb*8 .. +7 of each half
   const int cp = t >> 3, rb = t & 7;
-  uint32_t w[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w[i] = tile[rb * 8 + i][cp];
-  uint4 lo, hi;
-  lo.x = __byte_perm(w[0], w[1], 0x5410); hi.x = __byte_perm(w[0], w[1], 0x7632);
-  lo.y = __byte_perm(w[2], w[3], 0x5410); hi.y = __byte_perm(w[2], w[3], 0x7632);
-  lo.z = __byte_perm(w[4], w[5], 0x5410); hi.z = __byte_perm(w[4], w[5], 0x7632);
-  lo.w = __byte_perm(w[6], w[7], 0x5410); hi.w = __byte_perm(w[6], w[7], 0x7632);
-  const int64_t c = c0 + 2 * cp, rr0 = r0 + rb * 8;
-  if (rr0 < rows) {
-    if (c < cols) *reinterpret_cast<uint4*>(dst + c * ld_dst + rr0) = lo;
-    if (c + 1 < cols) *reinterpret_cast<uint4*>(dst + (c + 1) * ld_dst + rr0) = hi;
+  for (int half = 0; half < 2; ++half) {
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = tile[half * 64 + rb * 8 + i][cp];
+    uint4 lo, hi;
+    lo.x = __byte_perm(w[0], w[1], 0x5410); hi.x = __byte_perm(w[0], w[1], 0x7632);
+    lo.y = __byte_perm(w[2], w[3], 0x5410); hi.y = __byte_perm(w[2], w[3], 0x7632);
+    lo.z = __byte_perm(w[4], w[5], 0x5410); hi.z = __byte_perm(w[4], w[5], 0x7632);
+    lo.w = __byte_perm(w[6], w[7], 0x5410); hi.w = __byte_perm(w[6], w[7], 0x7632);
+    const int64_t c = c0 + 2 * cp, rr0 = r0 + half * 64 + rb * 8;
+    if (rr0 < rows) {
+      if (c < cols) *reinterpret_cast<uint4*>(dst + c * ld_dst + rr0) = lo;
+      if (c + 1 < cols) *reinterpret_cast<uint4*>(dst + (c + 1) * ld_dst + rr0) = hi;
+    }
   }
 }
 
@@ -326,13 +366,17 @@ int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int
   auto X1 = reinterpret_cast<__nv_bfloat16*>(x1_out);
   auto U = reinterpret_cast<__nv_bfloat16*>(u_out);
   auto RS = reinterpret_cast<float*>(rstd);
-  PDS_VPL_DISPATCH(h, rmsnorm_fwd_kernel, (grid, 128, 0, st), (X, R, G, rows, h, eps, X1, U, RS));
+  const int nt = h / 8 < 256 ? h / 8 : 256;
+  if (h / 8 / nt == 2)
+    rmsnorm_fwd_kernel<2><<<(unsigned)rows, nt, 0, st>>>(X, R, G, rows, h, eps, X1, U, RS);
+  else
+    rmsnorm_fwd_kernel<1><<<(unsigned)rows, nt, 0, st>>>(X, R, G, rows, h, eps, X1, U, RS);
   return (int)cudaGetLastError();
 }
 
 int rmsnorm_bwd_grid(int64_t rows) {
   int64_t b = (rows + 3) / 4;
-  return (int)(b < 592 ? b : 592);
+  return (int)(b < 444 ? b : 444);   // 148 SMs x 3 resident blocks (all resident: one wave)
 }
 
 // dg_part: fp32 scratch [rmsnorm_bwd_grid(rows)][h]; dg (fp32 [h]) += reduced partials
@@ -347,13 +391,11 @@ int rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g, 
   auto G = reinterpret_cast<const __nv_bfloat16*>(g);
   auto DR = reinterpret_cast<const __nv_bfloat16*>(dres);
   auto DX = reinterpret_cast<__nv_bfloat16*>(dx);
-  const size_t smem = (size_t)4 * h * sizeof(float);
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(rmsnorm_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4096 * 4);
-    once = true;
-  }
-  PDS_VPL_DISPATCH(h, rmsnorm_bwd_kernel, (grid, 128, smem, st), (DU, X, RS, G, DR, rows, h, DX, dg_part));
+  const int nt = h / 8 < 256 ? h / 8 : 256;
+  if (h / 8 / nt == 2)
+    rmsnorm_bwd_kernel<2><<<grid, nt, 0, st>>>(DU, X, RS, G, DR, rows, h, DX, dg_part);
+  else
+    rmsnorm_bwd_kernel<1><<<grid, nt, 0, st>>>(DU, X, RS, G, DR, rows, h, DX, dg_part);
   reduce_rows_add_kernel<<<(h + 31) / 32, 256, 0, st>>>(dg_part, grid, h, dg);
   return (int)cudaGetLastError();
 }
@@ -417,7 +459,7 @@ int transpose_bf16(const void* src, int64_t ld_src, int64_t rows, int64_t cols, 
                    int64_t seg, int64_t stride, int64_t base, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return 0;
   if (rows % 8 || cols % 8 || ld_src % 8 || ld_dst % 8) return (int)cudaErrorInvalidValue;
-  dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64));
+  dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((rows + 127) / 128));
   transpose_bf16_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint16_t*>(src), ld_src, rows, cols,
                                                reinterpret_cast<uint16_t*>(dst), ld_dst,
                                                seg > 0 ? seg : ((int64_t)1 << 40), stride, base);
