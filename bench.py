@@ -178,16 +178,18 @@ def main():
 
     plans = {}
 
-    def step(s, timed_events=None):
-        b = bufs[s]
+    def choose(s):
         if args.strategy >= 0:
-            pi = args.strategy
-        elif have_bundle:
+            return args.strategy
+        if have_bundle:
             plan, _ = ctx.plan(s, L_STACK)
             plans[s] = plan
-            pi = plan[0]
-        else:
-            pi = 0
+            return plan[0]
+        return 0
+
+    def step(s, timed_events=None):
+        b = bufs[s]
+        pi = choose(s)
         sv = ctx.layer_fwd(pi, s, b["x"].data_ptr(), b["W"], b["y"].data_ptr(), st.cuda_stream)
         ctx.layer_bwd(pi, b["dy"].data_ptr(), sv, b["W"], b["G"], b["dx"].data_ptr(), st.cuda_stream)
         return pi
@@ -233,7 +235,8 @@ def main():
     tokens = sum(args.seqs) * args.steps
     value = tokens / (total_ms / 1e3)
 
-    # end-to-end through the C ABI with HOST buffers (pinned), copies inside the timed region
+    # end-to-end through the C ABI with HOST buffers (pinned): pds_layer_step_host uploads x, dy and
+    # downloads y, dx inside the timed region (dy / y transfers overlap the fwd / bwd)
     host = {s: dict(x=bufs[s]["x"].cpu().pin_memory(), dy=bufs[s]["dy"].cpu().pin_memory(),
                     y=torch.empty_like(bufs[s]["x"], device="cpu").pin_memory(),
                     dx=torch.empty_like(bufs[s]["x"], device="cpu").pin_memory()) for s in args.seqs}
@@ -246,11 +249,10 @@ def main():
             a = torch.cuda.Event(enable_timing=True)
             e = torch.cuda.Event(enable_timing=True)
             a.record(st)
-            bufs[s]["x"].copy_(host[s]["x"], non_blocking=True)
-            bufs[s]["dy"].copy_(host[s]["dy"], non_blocking=True)
-            step(s)
-            host[s]["y"].copy_(bufs[s]["y"], non_blocking=True)
-            host[s]["dx"].copy_(bufs[s]["dx"], non_blocking=True)
+            b, hb = bufs[s], host[s]
+            pi = choose(s)
+            ctx.layer_step_host(pi, s, hb["x"].data_ptr(), hb["dy"].data_ptr(), b["W"], b["G"],
+                                hb["y"].data_ptr(), hb["dx"].data_ptr(), st.cuda_stream)
             e.record(st)
             e.synchronize()
             e2e_ms += a.elapsed_time(e)

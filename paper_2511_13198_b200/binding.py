@@ -109,6 +109,8 @@ _SIGS = {
                       C.POINTER(C.c_void_p), C.c_void_p],
     "pds_layer_bwd": [C.c_void_p, C.c_uint8, C.c_void_p, C.c_void_p, C.POINTER(_Weights),
                       C.POINTER(_Grads), C.c_void_p, C.c_void_p],
+    "pds_layer_step_host": [C.c_void_p, C.c_uint8, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(_Weights),
+                            C.POINTER(_Grads), C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_saved_release": [C.c_void_p, C.c_void_p],
     "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
@@ -253,6 +255,12 @@ class Context:
 
     def layer_bwd(self, strategy, dy, saved, w: Weights, g: Grads, dx, stream=0):
         call("pds_layer_bwd", self.h, strategy, dy, saved, C.byref(w.c()), C.byref(g.c()), dx, stream)
+
+    def layer_step_host(self, strategy, seq_len, x_host, dy_host, w: Weights, g: Grads, y_host, dx_host,
+                        stream=0):
+        """One layer fwd + bwd on HOST buffers (pinned host pointers); pds_layer_step_host."""
+        call("pds_layer_step_host", self.h, strategy, seq_len, x_host, dy_host, C.byref(w.c()), C.byref(g.c()),
+             y_host, dx_host, stream)
 
     def saved_release(self, saved):
         call("pds_saved_release", self.h, saved)

@@ -76,6 +76,47 @@ __device__ __forceinline__ float exp2_fma(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Packed fp32 pair arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): one instruction per
+// two elements for the softmax / dS elementwise work, which is issue-bound.
+struct f2 { float x, y; };
+__device__ __forceinline__ uint64_t f2u(f2 a) {
+  return (uint64_t)__float_as_uint(a.x) | ((uint64_t)__float_as_uint(a.y) << 32);
+}
+__device__ __forceinline__ f2 u2f(uint64_t v) { return f2{__uint_as_float((uint32_t)v), __uint_as_float((uint32_t)(v >> 32))}; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+  return u2f(d);
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+  return u2f(d);
+}
+// exp2_fma on a pair: the same Cody-Waite split and polynomial with packed arithmetic
+__device__ __forceinline__ f2 exp2_fma2(f2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const f2 big{12582912.0f, 12582912.0f};
+  const f2 t = add2(x, big);
+  const f2 f = sub2(x, sub2(t, big));
+  f2 p = fma2(f2{0.05517161f, 0.05517161f}, f, f2{0.24261112f, 0.24261112f});
+  p = fma2(p, f, f2{0.693261f, 0.693261f});
+  p = fma2(p, f, f2{0.99992807f, 0.99992807f});
+  return f2{__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+            __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23))};
+}
+
 // 16-byte chunk store into a K-major SW128 tile: row r, 16-byte chunk c of atom a
 __device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, int a, int c, uint4 v) {
   *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
@@ -261,8 +302,8 @@ __global__ void __launch_bounds__(384, 1)
       if (need) m_used = m_new;
       // pass 2: p = exp2(s scale - m) (1 in 4 on the FMA pipe), bf16-packed P written
       // back into the consumed S columns (chunk c of 16 keys -> 8 packed columns at 8c)
-      float rsa[4] = {0.f, 0.f, 0.f, 0.f};
-      const float neg_m = -m_used;
+      f2 rs2[2] = {f2{0.f, 0.f}, f2{0.f, 0.f}};
+      const f2 nm2{-m_used, -m_used}, sl2{scale_log2, scale_log2};
       {
         uint32_t cur[16], nxt[16];
         tmem_ld16(lb + s_col, cur);
@@ -273,16 +314,20 @@ __global__ void __launch_bounds__(384, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const float x0 = fmaf(__uint_as_float(cur[i]), scale_log2, neg_m);
-            const float x1 = fmaf(__uint_as_float(cur[i + 1]), scale_log2, neg_m);
-            float p0 = ex2(x0);
-            float p1 = (i & 2) ? exp2_fma(x1) : ex2(x1);
-            if (MASK) {
-              if (k0 + c * 16 + i > row) p0 = 0.f;
-              if (k0 + c * 16 + i + 1 > row) p1 = 0.f;
+            const f2 x = fma2(f2{__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])}, sl2, nm2);
+            f2 p;
+            if ((i & 6) == 6) {
+              p = exp2_fma2(x);                  // 1 pair in 4 on the FMA pipe
+            } else {
+              p.x = ex2(x.x);
+              p.y = ex2(x.y);
             }
-            rsa[(i >> 1) & 3] += p0 + p1;
-            pk[i >> 1] = pack_bf16(p0, p1);
+            if (MASK) {
+              if (k0 + c * 16 + i > row) p.x = 0.f;
+              if (k0 + c * 16 + i + 1 > row) p.y = 0.f;
+            }
+            rs2[(i >> 1) & 1] = add2(rs2[(i >> 1) & 1], p);
+            pk[i >> 1] = pack_bf16(p.x, p.y);
           }
           tmem_st8(lb + s_col + c * 8, pk);
           tmem_ld_wait();
@@ -290,7 +335,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
         }
       }
-        l += (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+        const f2 rs = add2(rs2[0], rs2[1]);
+        l += rs.x + rs.y;
       };
       if (mask) block(std::true_type{});
       else block(std::false_type{});
@@ -386,9 +432,6 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
-
-// exponentials of one 64-column half: e % 4 == 3 on the FMA pipe, the rest on MUFU
-__device__ __forceinline__ float ex2_mix(float x, int e) { return (e & 3) == 3 ? exp2_fma(x) : ex2(x); }
 
 template <int D>
 struct BwdKV4Cfg {
@@ -554,14 +597,25 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(c_s, sa);
         tmem_ld32(c_s + 32, sb);
         tmem_ld_wait();
+        const f2 sl2{scale_log2, scale_log2}, nlog2e{-LOG2E, -LOG2E};
 #pragma unroll
         for (int e = 0; e < 64; e += 4) {
           const float4 L = lds4(lsm + e * 4);
-          const float l[4] = {L.x, L.y, L.z, L.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float sv = __uint_as_float(e + u < 32 ? sa[e + u] : sb[e + u - 32]);
-            p[e + u] = ex2_mix(fmaf(sv, scale_log2, -l[u] * LOG2E), u);
+          for (int u = 0; u < 4; u += 2) {
+            const f2 sv{__uint_as_float(e + u < 32 ? sa[e + u] : sb[e + u - 32]),
+                        __uint_as_float(e + u + 1 < 32 ? sa[e + u + 1] : sb[e + u + 1 - 32])};
+            const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
+            const f2 x = fma2(sv, sl2, nl);
+            f2 pp;
+            if (((e + u) & 6) == 6) {
+              pp = exp2_fma2(x);                 // 1 pair in 4 on the FMA pipe
+            } else {
+              pp.x = ex2(x.x);
+              pp.y = ex2(x.y);
+            }
+            p[e + u] = pp.x;
+            p[e + u + 1] = pp.y;
           }
         }
         if (diag) {
@@ -590,11 +644,12 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const float4 Dq = lds4(dsm + (32 * h + e) * 4);
-            const float dq[4] = {Dq.x, Dq.y, Dq.z, Dq.w};
-            pk[16 * h + e / 2] = pack_bf16(p[32 * h + e] * (__uint_as_float(dv[e]) - dq[0]),
-                                           p[32 * h + e + 1] * (__uint_as_float(dv[e + 1]) - dq[1]));
-            pk[16 * h + e / 2 + 1] = pack_bf16(p[32 * h + e + 2] * (__uint_as_float(dv[e + 2]) - dq[2]),
-                                               p[32 * h + e + 3] * (__uint_as_float(dv[e + 3]) - dq[3]));
+            const f2 d0 = mul2(f2{p[32 * h + e], p[32 * h + e + 1]},
+                               sub2(f2{__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])}, f2{Dq.x, Dq.y}));
+            const f2 d1 = mul2(f2{p[32 * h + e + 2], p[32 * h + e + 3]},
+                               sub2(f2{__uint_as_float(dv[e + 2]), __uint_as_float(dv[e + 3])}, f2{Dq.z, Dq.w}));
+            pk[16 * h + e / 2] = pack_bf16(d0.x, d0.y);
+            pk[16 * h + e / 2 + 1] = pack_bf16(d1.x, d1.y);
           }
         }
         tmem_st32(c_d, pk);
@@ -798,9 +853,21 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
+        const f2 sl2{scale_log2, scale_log2}, nl{nl2, nl2};
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          p[e] = ex2_mix(fmaf(__uint_as_float(e < 32 ? sa[e] : sb[e - 32]), scale_log2, nl2), e);
+        for (int e = 0; e < 64; e += 2) {
+          const f2 x = fma2(f2{__uint_as_float(e < 32 ? sa[e] : sb[e - 32]),
+                               __uint_as_float(e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32])}, sl2, nl);
+          f2 pp;
+          if ((e & 6) == 6) {
+            pp = exp2_fma2(x);                   // 1 pair in 4 on the FMA pipe
+          } else {
+            pp.x = ex2(x.x);
+            pp.y = ex2(x.y);
+          }
+          p[e] = pp.x;
+          p[e + 1] = pp.y;
+        }
         if (diag) {
 #pragma unroll
           for (int e = 0; e < 64; ++e)
@@ -816,9 +883,11 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(c_d + 32 * h, dv);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; e += 2)
-          pk[16 * h + e / 2] = pack_bf16(p[32 * h + e] * (__uint_as_float(dv[e]) - dd),
-                                         p[32 * h + e + 1] * (__uint_as_float(dv[e + 1]) - dd));
+        for (int e = 0; e < 32; e += 2) {
+          const f2 d = mul2(f2{p[32 * h + e], p[32 * h + e + 1]},
+                            sub2(f2{__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])}, f2{dd, dd}));
+          pk[16 * h + e / 2] = pack_bf16(d.x, d.y);
+        }
       }
       tmem_st32(c_d, pk);
       tmem_st_wait();

@@ -73,6 +73,11 @@ struct pds_ctx {
   // debug taps
   void* tap_o = nullptr;
   void* tap_z = nullptr;
+  // host-buffer step (pds_layer_step_host): device staging for x, dy, y, dx + copy stream
+  char* stage = nullptr;
+  int64_t stage_cap = 0;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_y = nullptr, ev_dy = nullptr, ev_ycopied = nullptr;
   // profiling
   bool prof = false;
   std::vector<ProfRec> pending;
@@ -86,6 +91,10 @@ struct pds_ctx {
     for (auto& kv : free_blocks) cudaFree(kv.second);
     if (ws) cudaFree(ws);
     if (rope) cudaFree(rope);
+    if (stage) cudaFree(stage);
+    for (cudaEvent_t e : {ev_start, ev_y, ev_dy, ev_ycopied})
+      if (e) cudaEventDestroy(e);
+    if (copy_st) cudaStreamDestroy(copy_st);
     delete comm;
   }
   cudaEvent_t ev() {
@@ -701,6 +710,9 @@ extern "C" pds_status pds_release_cache(pds_ctx* c) {
   if (c->ws) cudaFree(c->ws);
   c->ws = nullptr;
   c->ws_cap = 0;
+  if (c->stage) cudaFree(c->stage);
+  c->stage = nullptr;
+  c->stage_cap = 0;
   return PDS_OK;
 }
 
@@ -770,6 +782,58 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
   c->free_blocks.emplace(saved->bytes, saved->mem);
   delete saved;
   return rc;
+}
+
+// One layer fwd + bwd with HOST activations: x and dy are copied in, y and dx copied
+// out by the library.  The dy upload runs on a copy stream during the forward and
+// the y download during the backward; only the x upload and the dx download are
+// exposed.  Host buffers should be pinned (pageable memory works, without overlap).
+extern "C" pds_status pds_layer_step_host(pds_ctx* c, uint8_t strategy, int64_t seq_len, const void* x_host,
+                                          const void* dy_host, const pds_weights* w, const pds_grads* g,
+                                          void* y_host, void* dx_host, void* stream) {
+  PDS_TRY(check_layer(c, strategy, seq_len));
+  if (!x_host || !dy_host || !y_host || !dx_host) PDS_FAIL(PDS_EINVAL, "NULL host buffer");
+  if (seq_len <= 0 || seq_len % c->P) PDS_FAIL(PDS_EDIVISIBILITY, "seq_len not divisible by P");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PDS_CUDA(cudaSetDevice(c->device));
+  const int64_t nb = seq_len / c->P * c->m.h * 2;       // one local [s/P, b, h] bf16 activation
+  const int64_t slot = (nb + 255) / 256 * 256;
+  if (!c->copy_st) {
+    PDS_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_start, &c->ev_y, &c->ev_dy, &c->ev_ycopied})
+      PDS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  if (c->stage_cap < 4 * slot) {
+    PDS_CUDA(cudaStreamSynchronize(st));
+    PDS_CUDA(cudaStreamSynchronize(c->copy_st));
+    if (c->stage) PDS_CUDA(cudaFree(c->stage));
+    c->stage = nullptr;
+    c->stage_cap = 0;
+    cudaError_t e = cudaMalloc(&c->stage, 4 * slot);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      PDS_FAIL(e == cudaErrorMemoryAllocation ? PDS_ENOMEM : PDS_ECUDA,
+               std::string("staging cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    c->stage_cap = 4 * slot;
+  }
+  char *x = c->stage, *dy = c->stage + slot, *y = c->stage + 2 * slot, *dx = c->stage + 3 * slot;
+  PDS_CUDA(cudaEventRecord(c->ev_start, st));                       // previous step fully ordered
+  PDS_CUDA(cudaStreamWaitEvent(c->copy_st, c->ev_start, 0));
+  PDS_CUDA(cudaMemcpyAsync(dy, dy_host, nb, cudaMemcpyHostToDevice, c->copy_st));
+  PDS_CUDA(cudaEventRecord(c->ev_dy, c->copy_st));
+  PDS_CUDA(cudaMemcpyAsync(x, x_host, nb, cudaMemcpyHostToDevice, st));
+  pds_saved* sv = nullptr;
+  PDS_TRY(pds_layer_fwd(c, strategy, seq_len, x, w, y, &sv, stream));
+  PDS_CUDA(cudaEventRecord(c->ev_y, st));
+  PDS_CUDA(cudaStreamWaitEvent(c->copy_st, c->ev_y, 0));
+  PDS_CUDA(cudaMemcpyAsync(y_host, y, nb, cudaMemcpyDeviceToHost, c->copy_st));
+  PDS_CUDA(cudaEventRecord(c->ev_ycopied, c->copy_st));
+  PDS_CUDA(cudaStreamWaitEvent(st, c->ev_dy, 0));
+  PDS_TRY(pds_layer_bwd(c, strategy, dy, sv, w, g, dx, stream));
+  PDS_CUDA(cudaMemcpyAsync(dx_host, dx, nb, cudaMemcpyDeviceToHost, st));
+  PDS_CUDA(cudaStreamWaitEvent(st, c->ev_ycopied, 0));               // the step ends on `stream`
+  return PDS_OK;
 }
 
 extern "C" pds_status pds_saved_release(pds_ctx* c, pds_saved* saved) {

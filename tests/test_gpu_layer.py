@@ -185,3 +185,32 @@ def test_layer_errors():
         ctx.layer_fwd(0, 200, x.data_ptr(), w, x.data_ptr())      # s/P not a multiple of 128
     assert e.value.code == -2
     ctx.close()
+
+
+@pytest.mark.parametrize("pi", [0, 2])
+def test_step_host(pi):
+    """pds_layer_step_host (host x, dy in; host y, dx out; copies overlapped on a copy
+    stream) equals the device-pointer fwd + bwd bit for bit and the oracle within TOL."""
+    h, n, F, s = 256, 4, 1024, 512
+    d = layer_inputs(h, n, F, s, 1, seed=3)
+    y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
+    g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
+    W = OS.shard_weights(d, n, 1)
+    R1 = Rank(W, 0, d["x"], d["dy"])
+    R2 = Rank(W, 0, d["x"], d["dy"])
+    ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F))
+    st = torch.cuda.current_stream()
+    sv = ctx.layer_fwd(pi, s, R1.x.data_ptr(), R1.weights(), R1.y.data_ptr(), st.cuda_stream)
+    ctx.layer_bwd(pi, R1.dy.data_ptr(), sv, R1.weights(), R1.grads(), R1.dx.data_ptr(), st.cuda_stream)
+    xh, dyh = R2.x.cpu().pin_memory(), R2.dy.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    dxh = torch.empty_like(xh).pin_memory()
+    ctx.layer_step_host(pi, s, xh.data_ptr(), dyh.data_ptr(), R2.weights(), R2.grads(), yh.data_ptr(),
+                        dxh.data_ptr(), st.cuda_stream)
+    st.synchronize()
+    assert torch.equal(yh, R1.y.cpu()) and torch.equal(dxh, R1.dx.cpu())
+    for k in R1.g:
+        assert torch.equal(R1.g[k], R2.g[k]), k
+    assert rel(host(yh)[:, None, :], y_ref) < TOL
+    assert rel(host(dxh)[:, None, :], g_ref["dx"]) < TOL
+    ctx.close()
