@@ -293,10 +293,13 @@ def main():
         "clocks": clk.summary(),
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (tcgen05)", "achieved": gemm_tf,
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (gemm2_tc_kernel CTA pair / gemm_tc_kernel)",
+                     "achieved": gemm_tf,
                      "peak": sustained, "unit": "TFLOP/s", "frac": gemm_tf / sustained,
                      "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
-                     "traffic": traffic, "launches": g["launches"], "gemm_ms": g["ms"],
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": g["bytes"] / g["launches"] if g["launches"] else None,
+                     "launches": g["launches"], "gemm_ms": g["ms"],
                      "step_share": g["ms"] / total_ms if total_ms else None,
                      "attn_fwd_tflops": attn[1], "attn_bwd_tflops": attn[2],
                      "norm_ms": prof[3]["ms"], "norm_gbs": (prof[3]["bytes"] / (prof[3]["ms"] / 1e3) / 1e9

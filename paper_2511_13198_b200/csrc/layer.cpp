@@ -151,7 +151,12 @@ struct Exec {
         nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
 
   pds_status gemm(GemmArgs g) {
-    Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 0);
+    // algorithmic bytes: A and B once, C by epilogue (fp32 += reads and writes; GELU /
+    // dGELU add the bf16 aux streams)
+    const double mn = (double)g.M * g.N;
+    const double cb = g.epi == EPI_F32_ACC ? 8.0 : g.epi == EPI_F32 ? 4.0 : g.epi == EPI_GELU ? 4.0
+                    : g.epi == EPI_DGELU ? 6.0 : 2.0;
+    Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M + g.N) * g.K + cb * mn);
     return kerr(gemm_launch(g, st), "gemm");
   }
   // C[M,N] = A * B^T helpers
