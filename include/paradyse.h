@@ -130,18 +130,22 @@ pds_status pds_set_enabled(pds_ctx* ctx, uint32_t strategy_mask);
 
 /* Pi*(b, s): writes L strategy ids to strategy_out (host, L bytes) — always a full
  * plan (totality); *flags_out (nullable) gets PDS_PLAN_* bits.
- * T_pi(s) from the bundle (Eq. 9), M_pi(s) from pds_mem_bytes (exact model),
- * Algorithm 1 with the readings R-17..R-24, dictionary D keyed by (b, s). */
+ * T_pi(s) from the bundle (Eq. 9), M_pi(s) from pds_mem_bytes (exact model: saved
+ * + persistent per layer, plus the plan's largest workspace, R-22), Algorithm 1
+ * with the readings R-17..R-24, dictionary D keyed by (b, s). */
 pds_status pds_plan(pds_ctx* ctx, int64_t seq_len, uint8_t* strategy_out, int32_t L,
                     uint32_t* flags_out);
 
 /* Stateless Algorithm 1 on explicit per-layer costs (host arrays of n_strat):
- * t_layer[i], m_layer[i] for strategy i, enabled[i] in {0,1}; feasibility is
- * sum m < capacity (strict).  prev_plan (nullable, L bytes) enables smoothing with
- * gamma.  counters_out (nullable, 3 x int64): layer memory checks, candidate plans
+ * t_layer[i], m_layer[i] for strategy i, w_layer[i] (nullable) the strategy's
+ * workspace, enabled[i] in {0,1}; a plan is feasible iff
+ * sum_l m[pi_l] + max_l w[pi_l] < capacity (strict; Eq. 6 with reading R-22: one
+ * workspace per plan, reused by every layer; w_layer = NULL gives the paper's
+ * sum m < capacity).  prev_plan (nullable, L bytes) enables smoothing with gamma.
+ * counters_out (nullable, 3 x int64): layer memory checks, candidate plans
  * generated, cache hits (always 0 here).  Bit-exact contract with the oracle. */
 pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_layer, const double* m_layer,
-                       const uint8_t* enabled, double capacity, double gamma,
+                       const double* w_layer, const uint8_t* enabled, double capacity, double gamma,
                        const uint8_t* prev_plan, uint8_t* strategy_out, uint32_t* flags_out,
                        int64_t* counters_out);
 

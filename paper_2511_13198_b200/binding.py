@@ -11,7 +11,7 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparadyse.so")
+LIB_PATH = os.environ.get("PDS_LIB") or os.path.join(HERE, "libparadyse.so")   # PDS_LIB: A/B builds
 
 TS, UZ, METP = 0, 1, 2
 STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
@@ -100,8 +100,8 @@ _SIGS = {
     "pds_set_capacity": [C.c_void_p, C.c_double, C.c_double],
     "pds_set_enabled": [C.c_void_p, C.c_uint32],
     "pds_plan": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.POINTER(C.c_uint32)],
-    "pds_plan_ex": [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double,
-                    C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p],
+    "pds_plan_ex": [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                    C.c_double, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p],
     "pds_cost_eval": [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_mem_bytes": [C.POINTER(_Model), C.c_int32, C.c_uint8, C.c_int64, C.POINTER(C.c_int64),
                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
@@ -174,16 +174,17 @@ def mem_bytes(model: Model, P: int, strategy: int, s: int):
     return a.value, b.value, c.value
 
 
-def plan_ex(L, t, m, enabled, capacity, gamma=0.0, prev=None, counters=False):
+def plan_ex(L, t, m, enabled, capacity, gamma=0.0, prev=None, counters=False, w=None):
     n = len(t)
     ta = (C.c_double * n)(*t)
     ma = (C.c_double * n)(*m)
+    wa = (C.c_double * n)(*w) if w is not None else None
     ea = (C.c_uint8 * n)(*[1 if e else 0 for e in enabled])
     out = (C.c_uint8 * L)()
     pv = (C.c_uint8 * L)(*prev) if prev is not None else None
     flags = C.c_uint32()
     ctr = (C.c_int64 * 3)()
-    call("pds_plan_ex", L, n, ta, ma, ea, capacity, gamma, pv, out, C.byref(flags), ctr)
+    call("pds_plan_ex", L, n, ta, ma, wa, ea, capacity, gamma, pv, out, C.byref(flags), ctr)
     res = list(out), flags.value
     return (res + (list(ctr),)) if counters else res
 

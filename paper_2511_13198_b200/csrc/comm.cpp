@@ -45,8 +45,26 @@ static ncclDataType_t nt(DType dt) { return dt == DT_BF16 ? ncclBfloat16 : ncclF
 
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
+  NcclComm* side_ = nullptr;
   ~NcclComm() override {
+    delete side_;
     if (comm) ncclCommDestroy(comm);
+  }
+  Comm* side(pds_status* st) override {
+    if (!side_) {
+      ncclComm_t c2 = nullptr;
+      ncclResult_t r = ncclCommSplit(comm, 0, rank, &c2, nullptr);
+      if (r != ncclSuccess) {
+        set_error(std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+        *st = PDS_ENCCL;
+        return nullptr;
+      }
+      side_ = new NcclComm();
+      side_->P = P;
+      side_->rank = rank;
+      side_->comm = c2;
+    }
+    return side_;
   }
   pds_status all_gather(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     PDS_NCCL(ncclAllGather(send, recv, (size_t)count, nt(dt), comm, st));

@@ -29,6 +29,11 @@ struct Comm {
   virtual pds_status all_reduce(void* buf, int64_t count, DType dt, cudaStream_t st) = 0;
   // recv[j][count] <- send_j[rank][count]  (chunk `rank` of every source j)
   virtual pds_status all_to_all(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) = 0;
+  // A communicator for collectives issued on a second stream concurrently with this
+  // one's (NCCL: a split of the same ranks, so two in-flight collectives never share
+  // one communicator; loopback / self: the same object).  Collective: every rank
+  // calls it at the same point of the program.
+  virtual Comm* side(pds_status* st) { return this; }
 };
 
 Comm* make_nccl_comm(int P, int rank, const void* uid, pds_status* st);

@@ -64,9 +64,11 @@ struct Alg1Counters {
   int64_t layer_checks = 0, plans = 0, cache_hits = 0;
 };
 // Algorithm 1 on explicit costs; returns infeasible flag via *infeasible
-void alg1(int L, int n, const double* t, const double* m, const uint8_t* enabled, double cap,
+// w: per-strategy workspace bytes (one workspace per plan: max over its strategies,
+// reading R-22); NULL = none
+void alg1(int L, int n, const double* t, const double* m, const double* w, const uint8_t* enabled, double cap,
           std::vector<uint8_t>& out, bool* infeasible, bool* early, Alg1Counters* c);
-bool plan_feasible(const uint8_t* plan, int L, const double* m, double cap, Alg1Counters* c);
+bool plan_feasible(const uint8_t* plan, int L, const double* m, const double* w, double cap, Alg1Counters* c);
 double plan_time(const uint8_t* plan, int L, const double* t);
 
 // ------------------------------------------------------------------ cost bundle

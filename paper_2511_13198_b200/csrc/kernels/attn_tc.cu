@@ -117,6 +117,14 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
             __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23))};
 }
 
+// Which element pairs take exp2 on the FMA pipe: bit (pair index mod 8) of the mask.
+// 0x88 = 1 pair in 4 (25 %).  MUFU ex2 runs 16 / clk / SM, the FFMA2 emulation costs
+// issue slots instead; the best split depends on the kernel's other work.
+#ifndef PDS_EMU_MASK
+#define PDS_EMU_MASK 0x88
+#endif
+__host__ __device__ constexpr bool emu_pair(int pair) { return (PDS_EMU_MASK >> (pair & 7)) & 1; }
+
 // 16-byte chunk store into a K-major SW128 tile: row r, 16-byte chunk c of atom a
 __device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, int a, int c, uint4 v) {
   *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
@@ -316,8 +324,8 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; i += 2) {
             const f2 x = fma2(f2{__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])}, sl2, nm2);
             f2 p;
-            if ((i & 6) == 6) {
-              p = exp2_fma2(x);                  // 1 pair in 4 on the FMA pipe
+            if (emu_pair(i >> 1)) {
+              p = exp2_fma2(x);                  // share of the pairs on the FMA pipe
             } else {
               p.x = ex2(x.x);
               p.y = ex2(x.y);
@@ -608,8 +616,8 @@ __global__ void __launch_bounds__(384, 1)
             const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
             const f2 x = fma2(sv, sl2, nl);
             f2 pp;
-            if (((e + u) & 6) == 6) {
-              pp = exp2_fma2(x);                 // 1 pair in 4 on the FMA pipe
+            if (emu_pair((e + u) >> 1)) {
+              pp = exp2_fma2(x);                 // share of the pairs on the FMA pipe
             } else {
               pp.x = ex2(x.x);
               pp.y = ex2(x.y);
@@ -859,8 +867,8 @@ __global__ void __launch_bounds__(384, 1)
           const f2 x = fma2(f2{__uint_as_float(e < 32 ? sa[e] : sb[e - 32]),
                                __uint_as_float(e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32])}, sl2, nl);
           f2 pp;
-          if ((e & 6) == 6) {
-            pp = exp2_fma2(x);                   // 1 pair in 4 on the FMA pipe
+          if (emu_pair(e >> 1)) {
+            pp = exp2_fma2(x);                   // share of the pairs on the FMA pipe
           } else {
             pp.x = ex2(x.x);
             pp.y = ex2(x.y);

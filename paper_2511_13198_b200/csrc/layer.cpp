@@ -77,6 +77,9 @@ struct pds_ctx {
   char* stage = nullptr;
   int64_t stage_cap = 0;
   cudaStream_t copy_st = nullptr;
+  // side stream for collectives overlapped with compute (METP wave prefetch)
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> sync_pool;
   cudaEvent_t ev_start = nullptr, ev_y = nullptr, ev_dy = nullptr, ev_ycopied = nullptr;
   // profiling
   bool prof = false;
@@ -95,6 +98,8 @@ struct pds_ctx {
     for (cudaEvent_t e : {ev_start, ev_y, ev_dy, ev_ycopied})
       if (e) cudaEventDestroy(e);
     if (copy_st) cudaStreamDestroy(copy_st);
+    if (comm_st) cudaStreamDestroy(comm_st);
+    for (auto e : sync_pool) cudaEventDestroy(e);
     delete comm;
   }
   cudaEvent_t ev() {
@@ -207,6 +212,33 @@ struct Exec {
   pds_status ag(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
     Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
     return c->comm->all_gather(send, recv, count, dt, st);
+  }
+  // all_gather on another stream (the caller orders it with link())
+  pds_status ag_on(cudaStream_t s2, const void* send, void* recv, int64_t count) {
+    pds_status rc = PDS_OK;
+    Comm* cm = s2 == st ? c->comm : c->comm->side(&rc);
+    if (!cm) return rc;
+    Prof p(c, s2, K_COMM, 0, (double)count * 2 * (P - 1));
+    return cm->all_gather(send, recv, count, DT_BF16, s2);
+  }
+  cudaStream_t comm_stream() {
+    if (!c->comm_st) cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking);
+    return c->comm_st;
+  }
+  // `to` waits for everything enqueued on `from` so far
+  pds_status link(cudaStream_t from, cudaStream_t to) {
+    if (from == to) return PDS_OK;
+    cudaEvent_t ev;
+    if (c->sync_pool.empty()) {
+      PDS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    } else {
+      ev = c->sync_pool.back();
+      c->sync_pool.pop_back();
+    }
+    PDS_CUDA(cudaEventRecord(ev, from));
+    PDS_CUDA(cudaStreamWaitEvent(to, ev, 0));
+    c->sync_pool.push_back(ev);       // the wait captured this record; the event may be reused
+    return PDS_OK;
   }
   pds_status rs(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
     Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
@@ -455,14 +487,29 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   const int64_t row = e.h * 2;
   const int64_t slot = e.r * wr * e.h * 2;
   const char* xb = static_cast<const char*>(x);
+  // Wave gathers run on a side stream one wave ahead of the GEMMs ("asynchronous
+  // ring-based execution"): AG(k+1) into one of two buffers while the
+  // GEMM of wave k reads the other.  At P = 1 the gathers are identities.
+  char* gb[2] = {wg, ws + bp.ws_off("wg2")};
+  const cudaStream_t cs = e.P > 1 ? e.comm_stream() : e.st;
+  auto waves = [&](const char* src, auto&& gemm_wave) -> pds_status {
+    PDS_TRY(e.link(e.st, cs));                                   // src rows are ready
+    PDS_TRY(e.ag_on(cs, src, gb[0], wr * e.h));
+    for (int64_t k = 0; k < c; ++k) {
+      PDS_TRY(e.link(cs, e.st));                                 // wave k gathered
+      if (k + 1 < c) PDS_TRY(e.ag_on(cs, src + (k + 1) * wr * row, gb[(k + 1) & 1], wr * e.h));
+      PDS_TRY(gemm_wave(k, gb[k & 1]));
+      if (k + 2 < c) PDS_TRY(e.link(e.st, cs));                  // buffer k & 1 free again
+    }
+    return PDS_OK;
+  };
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, ul, sv->at("rstd1")));
-  for (int64_t k = 0; k < c; ++k) {   // QKV waves: rows land at their global positions
-    PDS_TRY(e.ag(ul + k * wr * row, wg, wr * e.h));
-    GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
+  PDS_TRY(waves(ul, [&](int64_t k, char* buf) -> pds_status {   // QKV waves: rows land at global positions
+    GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
                         e.hl, wr, e.sl, k * wr);
     q.c_seg = wr; q.c_stride = e.sl; q.c_base = k * wr;
-    PDS_TRY(e.gemm(q));
-  }
+    return e.gemm(q);
+  }));
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));  // query-chunk x KV-chunk loop
   PDS_TRY(tn.tr(w->w_proj, e.h, e.hl, e.h, wt));                 // W_proj^T, reused by every wave
   for (int64_t k = 0; k < c; ++k) {   // projection waves (A rows read through the TMA row remap)
@@ -475,17 +522,15 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
                        sv->at("rstd2") + k * wr * 4));
   }
   PDS_TRY(tn.tr(w->w_out, e.h, e.Fl, e.h, wt));                  // W_out^T, reused by every wave
-  for (int64_t k = 0; k < c; ++k) {   // FFN waves
-    PDS_TRY(e.ag(vl + k * wr * row, wg, wr * e.h));
-    GemmArgs fc1 = Exec::G(wg, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
+  return waves(vl, [&](int64_t k, char* buf) -> pds_status {     // FFN waves
+    GemmArgs fc1 = Exec::G(buf, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
     fc1.aux_out = gw; fc1.ld_aux = e.Fl;
     PDS_TRY(e.gemm(fc1));
     PDS_TRY(tn.mm(gw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
     if (e.c->tap_z) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_z) + k * wr * row, pw + slot, wr * e.h));
-    PDS_TRY(e.add(sv->at("x1") + k * wr * row, pw + slot, static_cast<char*>(y) + k * wr * row, wr * e.h));
-  }
-  return PDS_OK;
+    return e.add(sv->at("x1") + k * wr * row, pw + slot, static_cast<char*>(y) + k * wr * row, wr * e.h);
+  });
 }
 
 pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
@@ -880,24 +925,21 @@ extern "C" pds_status pds_set_enabled(pds_ctx* c, uint32_t mask) {
 }
 
 // T_pi(s) from the bundle (Eq. 9) and M_pi(s) = persistent + saved bytes of one
-// layer (exact plan); *headroom = max workspace over the enabled strategies
-// (reading R-22: Eq. 6 keeps its additive per-layer form, transients are one
-// plan-independent term subtracted from the capacity).
-static pds_status costs(pds_ctx* c, int64_t s, double* t, double* mm, int* branch, double* headroom) {
+// layer (exact plan); w = its workspace (one per plan, reading R-22)
+static pds_status costs(pds_ctx* c, int64_t s, double* t, double* mm, int* branch, double* w) {
   if (!c->bundle.loaded) PDS_FAIL(PDS_ENOCOSTS, "no cost bundle loaded (pds_load_costs)");
-  double trans = 0;
   for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
     t[i] = c->bundle.strat[i].present ? bundle_time(c->bundle, i, s, branch ? &branch[i] : nullptr) : 1e300;
     int64_t saved = 0, tr = 0, pers = 0;
     pds_status rc = pds_mem_bytes(&c->m, c->P, (uint8_t)i, s, &saved, &tr, &pers);
     if (rc != PDS_OK) {
       mm[i] = 1e300;
+      if (w) w[i] = 1e300;
       continue;
     }
     mm[i] = (double)(saved + pers);
-    if ((c->enabled >> i & 1) && c->bundle.strat[i].present) trans = std::max(trans, (double)tr);
+    if (w) w[i] = (double)tr;
   }
-  if (headroom) *headroom = trans;
   return PDS_OK;
 }
 
@@ -919,7 +961,7 @@ extern "C" pds_status pds_plan(pds_ctx* c, int64_t s, uint8_t* out, int32_t L, u
   if (L <= 0) PDS_FAIL(PDS_EINVAL, "L must be >= 1");
   uint32_t flags = 0;
   std::vector<uint8_t> plan;
-  double t[PDS_N_STRATEGIES], mm[PDS_N_STRATEGIES], head = 0;
+  double t[PDS_N_STRATEGIES], mm[PDS_N_STRATEGIES], ws[PDS_N_STRATEGIES];
   const auto key = std::make_pair(c->m.batch, s);
   auto it = c->cache.find(key);
   bool need_costs = true;
@@ -927,25 +969,25 @@ extern "C" pds_status pds_plan(pds_ctx* c, int64_t s, uint8_t* out, int32_t L, u
     plan = it->second.first;
     flags |= PDS_PLAN_CACHED | (it->second.second ? PDS_PLAN_INFEASIBLE : 0u);
   } else {
-    PDS_TRY(costs(c, s, t, mm, nullptr, &head));
+    PDS_TRY(costs(c, s, t, mm, nullptr, ws));
     need_costs = false;
     uint8_t en[PDS_N_STRATEGIES];
     for (int i = 0; i < PDS_N_STRATEGIES; ++i) en[i] = (c->enabled >> i & 1) && c->bundle.strat[i].present && mm[i] < 1e299;
-    const double cap = c->capacity - head;
+    const double cap = c->capacity;
     bool inf = false, early = false;
     bool any = false;
     for (int i = 0; i < PDS_N_STRATEGIES; ++i) any |= en[i] != 0;
     if (!any) PDS_FAIL(PDS_ESTRATEGY, "no enabled strategy is valid at this seq_len");
-    alg1(L, PDS_N_STRATEGIES, t, mm, en, cap, plan, &inf, &early, nullptr);
+    alg1(L, PDS_N_STRATEGIES, t, mm, ws, en, cap, plan, &inf, &early, nullptr);
     flags |= (inf ? PDS_PLAN_INFEASIBLE : 0u) | (early ? PDS_PLAN_EARLY : 0u);
     c->cache[key] = std::make_pair(plan, inf);
   }
   if (c->gamma > 0 && (int)c->prev.size() == L && c->prev != plan) {
-    if (need_costs) PDS_TRY(costs(c, s, t, mm, nullptr, &head));
+    if (need_costs) PDS_TRY(costs(c, s, t, mm, nullptr, ws));
     bool valid = true;
     for (uint8_t p : c->prev) valid &= (c->enabled >> p & 1) && mm[p] < 1e299;
-    const double cap = c->capacity - head;
-    if (valid && plan_feasible(c->prev.data(), L, mm, cap, nullptr) &&
+    const double cap = c->capacity;
+    if (valid && plan_feasible(c->prev.data(), L, mm, ws, cap, nullptr) &&
         plan_time(c->prev.data(), L, t) <= (1.0 + c->gamma) * plan_time(plan.data(), L, t)) {
       plan = c->prev;
       flags |= PDS_PLAN_SMOOTHED;

@@ -22,14 +22,16 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
 // ------------------------------------------------------------------ Algorithm 1
-bool plan_feasible(const uint8_t* plan, int L, const double* m, double cap, Alg1Counters* c) {
-  double acc = 0.0;
+// Eq. 6 with reading R-22: sum_l m[pi_l] + max_l w[pi_l] < cap (w = NULL: all zero)
+bool plan_feasible(const uint8_t* plan, int L, const double* m, const double* w, double cap, Alg1Counters* c) {
+  double acc = 0.0, ws = 0.0;
   for (int l = 0; l < L; ++l) {
     acc += m[plan[l]];
+    if (w) ws = std::max(ws, w[plan[l]]);
     if (c) c->layer_checks++;
-    if (acc >= cap) return false;  // OOM short-circuit
+    if (acc + ws >= cap) return false;  // OOM short-circuit
   }
-  return acc < cap;
+  return acc + ws < cap;
 }
 
 double plan_time(const uint8_t* plan, int L, const double* t) {
@@ -38,15 +40,17 @@ double plan_time(const uint8_t* plan, int L, const double* t) {
   return acc;
 }
 
-// pop_useless (line 1): Pareto prune, sort ascending by (t, m, id)
-static std::vector<int> prune_sort(int n, const double* t, const double* m, const uint8_t* en) {
+// pop_useless (line 1): Pareto prune on (t, m, w), sort ascending by (t, m, id)
+static std::vector<int> prune_sort(int n, const double* t, const double* m, const double* w, const uint8_t* en) {
+  auto W = [&](int a) { return w ? w[a] : 0.0; };
   std::vector<int> keep;
   for (int a = 0; a < n; ++a) {
     if (!en[a]) continue;
     bool dominated = false;
     for (int b = 0; b < n && !dominated; ++b) {
       if (b == a || !en[b]) continue;
-      if (t[b] <= t[a] && m[b] <= m[a] && (t[b] < t[a] || m[b] < m[a])) dominated = true;
+      if (t[b] <= t[a] && m[b] <= m[a] && W(b) <= W(a) && (t[b] < t[a] || m[b] < m[a] || W(b) < W(a)))
+        dominated = true;
     }
     if (!dominated) keep.push_back(a);
   }
@@ -58,9 +62,9 @@ static std::vector<int> prune_sort(int n, const double* t, const double* m, cons
   return keep;
 }
 
-void alg1(int L, int n, const double* t, const double* m, const uint8_t* enabled, double cap,
+void alg1(int L, int n, const double* t, const double* m, const double* w, const uint8_t* enabled, double cap,
           std::vector<uint8_t>& out, bool* infeasible, bool* early, Alg1Counters* c) {
-  std::vector<int> P = prune_sort(n, t, m, enabled);
+  std::vector<int> P = prune_sort(n, t, m, w, enabled);
   *infeasible = false;
   *early = false;
   out.assign(L, 0);
@@ -70,7 +74,7 @@ void alg1(int L, int n, const double* t, const double* m, const uint8_t* enabled
   for (size_t i = 0; i < P.size(); ++i) {
     std::fill(s.begin(), s.end(), (uint8_t)P[i]);          // line 7
     if (c) c->plans++;
-    const bool ok = plan_feasible(s.data(), L, m, cap, c);
+    const bool ok = plan_feasible(s.data(), L, m, w, cap, c);
     if (i == 0 && ok) {                                     // lines 8-10 (R-18)
       out = s;
       *early = true;
@@ -87,7 +91,7 @@ void alg1(int L, int n, const double* t, const double* m, const uint8_t* enabled
           std::memmove(s.data(), s.data() + 1, (size_t)(L - 1));
           s[L - 1] = (uint8_t)P[k];
           if (c) c->plans++;
-          if (plan_feasible(s.data(), L, m, cap, c)) {
+          if (plan_feasible(s.data(), L, m, w, cap, c)) {
             const double tp = plan_time(s.data(), L, t);
             if (!have || tp < best_t) { best = s; best_t = tp; have = true; }
           }
@@ -328,7 +332,7 @@ extern "C" const char* pds_last_error(void) { return g_err.c_str(); }
 extern "C" const char* pds_version(void) { return "paradyse-b200 0.1 (sm_100a)"; }
 
 extern "C" pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_layer,
-                                  const double* m_layer, const uint8_t* enabled, double capacity,
+                                  const double* m_layer, const double* w_layer, const uint8_t* enabled, double capacity,
                                   double gamma, const uint8_t* prev_plan, uint8_t* strategy_out,
                                   uint32_t* flags_out, int64_t* counters_out) {
   if (L <= 0) PDS_FAIL(PDS_EINVAL, "L must be >= 1 (SPEC.md:394)");
@@ -340,7 +344,7 @@ extern "C" pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_la
   Alg1Counters c;
   std::vector<uint8_t> out;
   bool inf = false, early = false;
-  alg1(L, n_strat, t_layer, m_layer, enabled, capacity, out, &inf, &early, &c);
+  alg1(L, n_strat, t_layer, m_layer, w_layer, enabled, capacity, out, &inf, &early, &c);
   uint32_t flags = (inf ? PDS_PLAN_INFEASIBLE : 0u) | (early ? PDS_PLAN_EARLY : 0u);
   if (prev_plan) {
     bool valid = true, same = true;
@@ -348,7 +352,7 @@ extern "C" pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_la
       if (prev_plan[l] >= n_strat || !enabled[prev_plan[l]]) valid = false;
       else if (prev_plan[l] != out[l]) same = false;
     }
-    if (valid && !same && plan_feasible(prev_plan, L, m_layer, capacity, nullptr) &&
+    if (valid && !same && plan_feasible(prev_plan, L, m_layer, w_layer, capacity, nullptr) &&
         plan_time(prev_plan, L, t_layer) <= (1.0 + gamma) * plan_time(out.data(), L, t_layer)) {
       std::memcpy(out.data(), prev_plan, (size_t)L);
       flags |= PDS_PLAN_SMOOTHED;

@@ -30,8 +30,11 @@ def predicted_bytes(B, model, P, plan, s):
     return tot, ws
 
 
-def run_stack(torch, B, ctx, model, plan, s, layers, timed=True):
-    """fwd through len(plan) layers then bwd; returns seconds or raises PdsError."""
+def run_stack(torch, B, ctx, model, plan, s, layers, timed=True, release=True):
+    """fwd through len(plan) layers then bwd; returns seconds or raises PdsError.
+    release=False keeps the library's workspace and cached saved blocks (the saved
+    arena frees its cache and retries when cudaMalloc fails, so this never causes a
+    false OOM)."""
     st = torch.cuda.current_stream()
     h = model.h
     acts = [torch.randn(s, h, device="cuda", dtype=torch.bfloat16)]
@@ -61,7 +64,8 @@ def run_stack(torch, B, ctx, model, plan, s, layers, timed=True):
                 ctx.saved_release(sv)
         del acts
         torch.cuda.synchronize()
-        ctx.release_cache()
+        if release:
+            ctx.release_cache()
         torch.cuda.empty_cache()
 
 

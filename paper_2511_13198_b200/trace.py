@@ -1,20 +1,38 @@
-"""Dynamic-length training trace (configs[4]; the protocol of Figure 3).
+"""Dynamic-length training trace (configs[4]; the protocol of Figure 3)
+and the ablation harness of Table 5.
 
 Lengths are drawn from a Table 3 histogram (readings R-29/R-30),
 padded to a multiple of 128·P (R-15), curriculum-sorted short to long
 (PAPER.md:336), and each sequence runs forward + backward through an L-layer
 stack with the plan pds_plan returns for its length (adaptive), or with a fixed
 uniform plan (static baselines).  Records per sequence: s, plan, device time,
-OOM.  A static strategy's curve ends at its first OOM ("curve
-termination indicates OOM failure").  Per Table 3 bucket: sum tokens / sum time.
+OOM.  A run ends at its first OOM ("curve termination indicates OOM
+failure"); the adaptive planner stops *before* running when Eq. 6 has no
+feasible plan (proactive OOM prediction).
+
+--ablation runs ParaDySe (full) = all strategies, RF + PR cost model, smoothing
+gamma = 0.05, and the variants w/o MegatronTS, w/o UlyssesZ, w/o
+METP (strategy set), w/o RF (PR everywhere: the bundle's s_profile_max set to 0,
+Eq. 9), w/o Smoothing (gamma = 0), and reports Table 5's columns:
+  Seq_len   = largest length trained before OOM,
+  Time      = cumulative device time of the variant,
+  Time_full = cumulative time of ParaDySe (full) up to that Seq_len,
+  Saving    = (Time - Time_full) / Time.
+MegatronCZ is not in this build's strategy set.  Switching
+statistics per run: plan changes between consecutive sequences and strategy
+boundaries inside the plans.  --switch-cost measures a mixed plan's stack time
+against the per-layer times of short uniform stacks at the same length.
 
   python -m paper_2511_13198_b200.trace --dataset grch38 --n 48 --L 32 --out profiles/t.json
+  python -m paper_2511_13198_b200.trace --ablation --out profiles/ablation.json
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import re
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -28,6 +46,79 @@ def bucket_of(s):
     return len(BUCKET_EDGES) - 2
 
 
+def pr_only_bundle(path):
+    """Copy of a cost bundle whose Eq. 9 branch always takes the polynomial (w/o RF)."""
+    txt = open(path).read()
+    txt = re.sub(r"s_profile_max [0-9.eE+-]+", "s_profile_max 0.0", txt)
+    fd, out = tempfile.mkstemp(suffix=".txt")
+    with os.fdopen(fd, "w") as f:
+        f.write(txt)
+    return out
+
+
+def switches(recs):
+    plans = [r["plan"] for r in recs if "plan" in r]
+    between = sum(1 for a, b in zip(plans, plans[1:]) if a != b)
+    inside = sum(sum(1 for x, y in zip(p, p[1:]) if x != y) for p in plans)
+    return {"plan_changes_between_sequences": between, "strategy_boundaries_inside_plans": inside}
+
+
+def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None):
+    from .frontier import run_stack
+    recs, cum, oom_at = [], 0.0, None
+    for s in lens:
+        if fixed is None:
+            plan, flags = ctx.plan(s, L)
+            if flags & B.PLAN_INFEASIBLE:      # proactive OOM prediction (PAPER.md:410)
+                oom_at = s
+                recs.append({"s": s, "oom": True, "predicted": True})
+                break
+        else:
+            plan, flags = [fixed] * L, 0
+        try:
+            t = run_stack(torch, B, ctx, model, plan, s, layers)
+        except (B.PdsError, torch.OutOfMemoryError):
+            oom_at = s
+            recs.append({"s": s, "oom": True})
+            break
+        cum += t
+        recs.append({"s": s, "plan": "".join("TUM"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
+    per_bucket = {}
+    for r in recs:
+        if r.get("oom"):
+            continue
+        b = bucket_of(r["s"])
+        tok, sec = per_bucket.get(b, (0, 0.0))
+        per_bucket[b] = (tok + r["s"] * L, sec + r["seconds"])
+    return {"records": recs, "cumulative_s": cum, "oom_at": oom_at,
+            "max_s_trained": max([r["s"] for r in recs if not r.get("oom")] + [0]),
+            "tokens_per_s_per_layer_by_bucket": {str(k): v[0] / v[1] for k, v in per_bucket.items()},
+            "switching": switches(recs)}
+
+
+def time_full_at(full, s_max):
+    t = 0.0
+    for r in full["records"]:
+        if r.get("oom") or r["s"] > s_max:
+            break
+        t = r["cum"]
+    return t
+
+
+def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
+    """Stack time of a mixed plan vs sum of per-layer times from short uniform stacks."""
+    from .frontier import run_stack
+    per_layer = {}
+    for pi in sorted(set(plan)):
+        t = run_stack(torch, B, ctx, model, [pi] * n_short, s, layers)
+        per_layer[pi] = t / n_short
+    t_mixed = run_stack(torch, B, ctx, model, plan, s, layers)
+    pred = sum(per_layer[p] for p in plan)
+    return {"s": s, "plan": "".join("TUM"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
+            "overhead": t_mixed / pred - 1.0,
+            "per_layer_s": {"TUM"[k]: v for k, v in per_layer.items()}}
+
+
 def main():
     import sys
     sys.path.insert(0, ROOT)
@@ -35,7 +126,6 @@ def main():
     from synth import pad_to, sample_lengths
     from . import binding as B
     from .calibrate import make_layer_buffers
-    from .frontier import run_stack
     ap = argparse.ArgumentParser()
     ap.add_argument("--dataset", default="grch38")
     ap.add_argument("--n", type=int, default=48)
@@ -43,14 +133,14 @@ def main():
     ap.add_argument("--cap-s", type=int, default=131072, help="truncate sampled lengths (1 GPU)")
     ap.add_argument("--reserve-gb", type=float, default=4.0)
     ap.add_argument("--gamma", type=float, default=0.0)
+    ap.add_argument("--ablation", action="store_true")
+    ap.add_argument("--switch-cost", action="store_true")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     H, N, F, P = 4096, 32, 16384, 1
     model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)
-    ctx = B.Context(model)
-    ctx.load_costs(os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt"))
-    layers = []
-    keep = []
+    bundle = os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt")
+    layers, keep = [], []
     for li in range(a.L):
         w, gr, _, _ = make_layer_buffers(torch, model, P, 128, seed=li)
         keep.append((w, gr))
@@ -59,42 +149,61 @@ def main():
     torch.cuda.synchronize()
     free, total = torch.cuda.mem_get_info()
     pers = a.L * B.mem_bytes(model, P, 0, 1024)[2]
-    ctx.set_capacity(float(free) - a.reserve_gb * 2 ** 30 + pers, max(a.gamma, 0.0) if a.gamma > 0 else 1e-9)
+    cap = float(free) - a.reserve_gb * 2 ** 30 + pers
     lens = sample_lengths(a.dataset, a.n, seed=42)
     lens = sorted(min(int(pad_to(int(x), 128 * P)), a.cap_s) for x in lens)   # curriculum
-    out = {"dataset": a.dataset, "n": a.n, "L": a.L, "P": P, "gamma": a.gamma, "lengths": lens, "runs": {}}
-    for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1)):
-        recs, cum, oom_at = [], 0.0, None
-        for s in lens:
-            if fixed is None:
-                plan, flags = ctx.plan(s, a.L)
-                if flags & B.PLAN_INFEASIBLE:      # proactive OOM prediction
-                    oom_at = s
-                    recs.append({"s": s, "oom": True, "predicted": True})
-                    break
-            else:
-                plan, flags = [fixed] * a.L, 0
-            try:
-                t = run_stack(torch, B, ctx, model, plan, s, layers)
-            except (B.PdsError, torch.OutOfMemoryError) as e:
-                oom_at = s
-                recs.append({"s": s, "oom": True})
+    out = {"dataset": a.dataset, "n": a.n, "L": a.L, "P": P, "lengths": lens, "capacity_for_plan": cap, "runs": {}}
+
+    def context(mask=0x7, gamma=0.0, pr_only=False):
+        ctx = B.Context(model)
+        ctx.load_costs(pr_only_bundle(bundle) if pr_only else bundle)
+        ctx.set_enabled(mask)
+        ctx.set_capacity(cap, gamma if gamma > 0 else 1e-9)
+        return ctx
+
+    if a.ablation:
+        variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=0x6, gamma=0.05)),
+                    ("w/o UlyssesZ", dict(mask=0x5, gamma=0.05)), ("w/o METP", dict(mask=0x3, gamma=0.05)),
+                    ("w/o RF", dict(gamma=0.05, pr_only=True)), ("w/o Smoothing", dict(gamma=0.0))]
+        out["gamma_full"] = 0.05
+        for name, kw in variants:
+            ctx = context(**kw)
+            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L)
+            ctx.close()
+            r = out["runs"][name]
+            print(name, "cum %.1fs" % r["cumulative_s"], "max_s", r["max_s_trained"], r["switching"], flush=True)
+        full = out["runs"]["ParaDySe (full)"]
+        table = []
+        for name, _ in variants:
+            r = out["runs"][name]
+            tf = time_full_at(full, r["max_s_trained"])
+            table.append({"framework": name, "seq_len": r["max_s_trained"], "time_s": r["cumulative_s"],
+                          "time_full_s": tf,
+                          "saving": None if name.endswith("(full)") or r["cumulative_s"] == 0
+                          else (r["cumulative_s"] - tf) / r["cumulative_s"]})
+        out["table5"] = table
+        for row in table:
+            print(row, flush=True)
+    else:
+        for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1)):
+            ctx = context(mask=0x7 if fixed is None else 1 << fixed, gamma=a.gamma)
+            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, fixed)
+            ctx.close()
+            r = out["runs"][name]
+            print(name, "cum %.1fs" % r["cumulative_s"], "oom_at", r["oom_at"], "max_s", r["max_s_trained"],
+                  flush=True)
+    if a.switch_cost:
+        ctx = context()
+        mixed = None
+        for s in reversed(lens):
+            plan, flags = ctx.plan(s, a.L)
+            if not flags & B.PLAN_INFEASIBLE and len(set(plan)) > 1:
+                mixed = (s, plan)
                 break
-            cum += t
-            recs.append({"s": s, "plan": "".join("TUM"[p] for p in plan), "seconds": t, "cum": cum,
-                         "flags": flags})
-        per_bucket = {}
-        for r in recs:
-            if r.get("oom"):
-                continue
-            b = bucket_of(r["s"])
-            tok, sec = per_bucket.get(b, (0, 0.0))
-            per_bucket[b] = (tok + r["s"] * a.L, sec + r["seconds"])
-        out["runs"][name] = {"records": recs, "cumulative_s": cum, "oom_at": oom_at,
-                             "max_s_trained": max([r["s"] for r in recs if not r.get("oom")] + [0]),
-                             "tokens_per_s_per_layer_by_bucket": {str(k): v[0] / v[1] for k, v in per_bucket.items()}}
-        print(name, "cum %.1fs" % cum, "oom_at", oom_at, "max_s", out["runs"][name]["max_s_trained"], flush=True)
-    ctx.close()
+        if mixed:
+            out["switch_cost"] = switch_cost(torch, B, ctx, model, mixed[0], mixed[1], layers)
+            print("switch cost", out["switch_cost"], flush=True)
+        ctx.close()
     if a.out:
         with open(a.out, "w") as f:
             json.dump(out, f, indent=1)

@@ -46,9 +46,12 @@ def test_plan_ex_bit_exact_vs_oracle(B):
             en[0] = True
         cap = float(rng.random() * L * 0.9 + 1e-3)
         enabled = [i for i in range(k) if en[i]]
-        plan, flags, ctr = B.plan_ex(L, t, m, en, cap, counters=True)
+        # per-strategy workspace (reading R-22) in half of the trials
+        w = [float(v) for v in rng.random(k) * 0.5] if trial % 2 else None
+        wd = dict(enumerate(w)) if w is not None else None
+        plan, flags, ctr = B.plan_ex(L, t, m, en, cap, counters=True, w=w)
         ctr_o = OA.Counters()
-        ref, inf = OA.alg1(L, dict(enumerate(t)), dict(enumerate(m)), enabled, cap, ctr=ctr_o)
+        ref, inf = OA.alg1(L, dict(enumerate(t)), dict(enumerate(m)), enabled, cap, ctr=ctr_o, w=wd)
         assert plan == ref, (trial, k, L, t, m, en, cap)
         assert bool(flags & B.PLAN_INFEASIBLE) == inf
         assert ctr[0] == ctr_o.layer_checks and ctr[1] == ctr_o.plans
@@ -57,8 +60,8 @@ def test_plan_ex_bit_exact_vs_oracle(B):
         # smoothing against a random previous plan
         prev = [int(rng.choice(enabled)) for _ in range(L)]
         g = float(rng.choice([0.0, 0.05, 0.3]))
-        p2, f2 = B.plan_ex(L, t, m, en, cap, gamma=g, prev=prev)
-        r2, kept = OA.smooth(ref, prev, dict(enumerate(t)), dict(enumerate(m)), cap, g, enabled)
+        p2, f2 = B.plan_ex(L, t, m, en, cap, gamma=g, prev=prev, w=w)
+        r2, kept = OA.smooth(ref, prev, dict(enumerate(t)), dict(enumerate(m)), cap, g, enabled, w=wd)
         assert p2 == r2 and bool(f2 & B.PLAN_SMOOTHED) == kept
     assert n_inf > 50 and n_early > 50
 

@@ -154,3 +154,39 @@ def test_heuristic_gap_example():
     plan, _ = A.alg1(3, t, m, [0, 1, 2], 16.5)
     assert A.plan_time(plan, t) == 5.0
     assert A.brute_force(3, t, m, [0, 1, 2], 16.5)[0] == 4.0
+
+
+def test_workspace_reading_two_strategies_equal_brute_force():
+    # R-22: one workspace per plan (max over its strategies).  Feasibility stays
+    # permutation invariant, so |P| = 2 prefix mixes still cover every multiset
+    rng = np.random.default_rng(11)
+    n_feas = 0
+    for _ in range(500):
+        L = int(rng.integers(1, 7))
+        t = {0: float(rng.random()), 1: float(rng.random())}
+        m = {0: float(rng.random()), 1: float(rng.random())}
+        w = {0: float(rng.random()), 1: float(rng.random())}
+        cap = float(rng.random() * L + 0.5)
+        plan, inf = A.alg1(L, t, m, [0, 1], cap, w=w)
+        bf = A.brute_force(L, t, m, [0, 1], cap, w=w)
+        ms = A.multiset_best(L, t, m, [0, 1], cap, w=w)
+        assert (bf is None) == (ms is None)
+        if bf is None:
+            assert inf
+            continue
+        n_feas += 1
+        assert abs(A.plan_time(plan, t) - bf[0]) < 1e-12 and abs(ms[0] - bf[0]) < 1e-12
+        assert A.plan_mem(plan, m) + max(w[p] for p in plan) < cap
+    assert n_feas > 100
+
+
+def test_workspace_reading_example():
+    # A fast strategy with a huge workspace (UZ-like) must not shrink the budget of
+    # plans that do not use it: T (t 1, m 4, w 1), U (t 1.1, m 4.5, w 10), M (t 2, m 2, w 1)
+    t, m, w = {0: 1.0, 1: 1.1, 2: 2.0}, {0: 4.0, 1: 4.5, 2: 2.0}, {0: 1.0, 1: 10.0, 2: 1.0}
+    # cap 13: [T,T,T] = 12 + 1 = 13 (not < 13); [T,T,M] = 10 + 1 < 13 -> feasible
+    plan, inf = A.alg1(3, t, m, [0, 1, 2], 13.0, w=w)
+    assert not inf and sorted(plan) == [0, 0, 2]
+    # the enabled-max reading (cap - max w = 3) would have found nothing feasible
+    plan2, inf2 = A.alg1(3, t, m, [0, 1, 2], 13.0 - 10.0)
+    assert inf2
