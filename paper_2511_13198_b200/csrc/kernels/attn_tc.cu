@@ -1,7 +1,8 @@
 // tcgen05 / TMEM causal flash attention (Eq. 2; causal R-1) for
 // sm_100a, forward and backward.  Every kernel: warp 0 = TMA producer, warp 1 = the
-// single-thread MMA issuer, warp 2 = TMEM allocator (512 columns), warps 4..11 =
-// two elementwise warpgroups (thread = TMEM lane = one row of the 128-row tile).
+// single-thread MMA issuer, warp 2 = TMEM allocator (512 columns), warps 4.. =
+// elementwise warpgroups (thread = TMEM lane = one row of the 128-row tile; two
+// warpgroups in the forward and dQ kernels, four in dK/dV, splitting the columns).
 //
 //   attn_fwd_tc_kernel     CTA = two 128-query tiles x one head; S = Q K^T per
 //                          128-key block into TMEM, online softmax with lazy
@@ -433,7 +434,13 @@ __device__ __forceinline__ void row_to_tmem(uint32_t lb, uint32_t col, const __n
 // warpgroups split the 128 columns of a block: warpgroup w owns columns
 // [64w, 64w + 64) and writes its packed half into TMEM columns [64w, 64w + 32) of
 // the same region, so the A operand's k-step kk lives at column acol(kk).
-__device__ __forceinline__ uint32_t acol(int kk) { return (kk & 3) * 8 + (kk >> 2) * 64; }
+// (warpgroup w of NWG owns CW = 128 / NWG columns and writes their packed half into
+// columns [CW w, CW w + CW / 2))
+template <int NWG>
+__device__ __forceinline__ uint32_t acol(int kk) {
+  constexpr int CW = 128 / NWG, KPW = CW / 16;    // k-steps (16 columns) per warpgroup
+  return (kk / KPW) * CW + (kk % KPW) * 8;
+}
 
 __device__ __forceinline__ float4 lds4(uint32_t addr) {
   float4 v;
@@ -461,8 +468,8 @@ struct BwdKV4Cfg {
 //   dV += P^T dO (cols 256..), dK += dS^T Q (cols 256 + D..).
 // A later MMA that overwrites a region is issued after the MMA that reads it, and
 // tcgen05 MMAs of one thread execute in order.
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int NWG>
+__global__ void __launch_bounds__(128 + 128 * NWG, 1)
     attn_bwd_dkdv4_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                           const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
@@ -500,8 +507,8 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(kv_full, 1);
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_full, 8);
-    mbar_init(ds_full, 8);
+    mbar_init(p_full, 4 * NWG);
+    mbar_init(ds_full, 4 * NWG);
     mbar_init(fin, 1);
     fence_barrier_init();
   }
@@ -568,7 +575,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t so = otile(i);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
+          umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
       }
       __syncwarp();
       if (i + 1 < nq) issue_s(i + 1);
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t sq = qtile(i);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + DK_COL, tmem + DP_COL + acol(kk), mnmaj_desc(sq, kk), idesc_acc, (i | kk) != 0);
+          umma_f16_ts(tmem + DK_COL, tmem + DP_COL + acol<NWG>(kk), mnmaj_desc(sq, kk), idesc_acc, (i | kk) != 0);
         umma_commit(&q_empty[i % NST]);
       }
       __syncwarp();
@@ -587,32 +594,33 @@ __global__ void __launch_bounds__(384, 1)
     if (elect_one()) umma_commit(fin);
     __syncwarp();
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;          // query columns [64 wg, 64 wg + 64)
+    constexpr int CW = 128 / NWG;             // query columns per warpgroup
+    const int wg = (warp - 4) >> 2;          // query columns [CW wg, CW wg + CW)
     const int q = warp & 3;
     const int t = q * 32 + lane;             // key row (TMEM lane)
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t c_s = lb + ST_COL + 64 * wg, c_d = lb + DP_COL + 64 * wg;
+    const uint32_t c_s = lb + ST_COL + CW * wg, c_d = lb + DP_COL + CW * wg;
     for (int i = 0; i < nq; ++i) {
       const int b = i % NST;
-      const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * 256;
-      const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * 256;
+      const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * CW * 4;
+      const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * CW * 4;
       const bool diag = causal && i == 0;
-      float p[64];
+      float p[CW];
       {
-        uint32_t sa[32], sb[32];
+        uint32_t sr[CW / 32][32];
         mbar_wait(s_full, i & 1);
         tc_fence_after();
-        tmem_ld32(c_s, sa);
-        tmem_ld32(c_s + 32, sb);
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h) tmem_ld32(c_s + 32 * h, sr[h]);
         tmem_ld_wait();
         const f2 sl2{scale_log2, scale_log2}, nlog2e{-LOG2E, -LOG2E};
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {
+        for (int e = 0; e < CW; e += 4) {
           const float4 L = lds4(lsm + e * 4);
 #pragma unroll
           for (int u = 0; u < 4; u += 2) {
-            const f2 sv{__uint_as_float(e + u < 32 ? sa[e + u] : sb[e + u - 32]),
-                        __uint_as_float(e + u + 1 < 32 ? sa[e + u + 1] : sb[e + u + 1 - 32])};
+            const f2 sv{__uint_as_float(sr[(e + u) / 32][(e + u) % 32]),
+                        __uint_as_float(sr[(e + u + 1) / 32][(e + u + 1) % 32])};
             const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
             const f2 x = fma2(sv, sl2, nl);
             f2 pp;
@@ -628,13 +636,17 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (diag) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (t > 64 * wg + e) p[e] = 0.f;
+          for (int e = 0; e < CW; ++e)
+            if (t > CW * wg + e) p[e] = 0.f;
         }
-        uint32_t pk[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) pk[e] = pack_bf16(p[2 * e], p[2 * e + 1]);
-        tmem_st32(c_s, pk);
+        for (int h = 0; h < CW / 64 + (CW < 64); ++h) {   // 32 packed columns per store
+          uint32_t pk[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) pk[e] = (64 * h + 2 * e < CW) ? pack_bf16(p[64 * h + 2 * e], p[64 * h + 2 * e + 1]) : 0u;
+          if (CW >= 64) tmem_st32(c_s + 32 * h, pk);
+          else tmem_st16(c_s, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -643,9 +655,9 @@ __global__ void __launch_bounds__(384, 1)
       {
         mbar_wait(dp_full, i & 1);
         tc_fence_after();
-        uint32_t pk[32];
+        uint32_t pk[CW / 2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < CW / 32; ++h) {
           uint32_t dv[32];
           tmem_ld32(c_d + 32 * h, dv);
           tmem_ld_wait();
@@ -660,7 +672,8 @@ __global__ void __launch_bounds__(384, 1)
             pk[16 * h + e / 2 + 1] = pack_bf16(d1.x, d1.y);
           }
         }
-        tmem_st32(c_d, pk);
+        if (CW == 64) tmem_st32(c_d, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        else tmem_st16(c_d, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -671,9 +684,10 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const int key = k0 + t;
     __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
-    if (wg == 0) {
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
+    // epilogue tasks: D/64 RoPE^T chunk pairs of dK, then D/32 chunks of dV
+    for (int task = wg; task < D / 64 + D / 32; task += NWG) {
+      if (task < D / 64) {
+        const int c = task;
         uint32_t ra[32], rb[32];
         tmem_ld32(lb + DK_COL + c * 32, ra);
         tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
@@ -684,10 +698,8 @@ __global__ void __launch_bounds__(384, 1)
         rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
         store32_bf16(rowp + hq + c * 32, a);
         store32_bf16(rowp + hq + c * 32 + D / 2, bb);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      } else {
+        const int c = task - D / 64;
         uint32_t r[32];
         tmem_ld32(lb + DV_COL + c * 32, r);
         tmem_ld_wait();
@@ -721,8 +733,8 @@ struct BwdQ4Cfg {
 // dS = P (dP - D) overwrites dP as packed bf16, dQ += dS K (cols 384..).
 //   MMA order:  S_0 dP_0 | S_1 | dQ_0 dP_1 | S_2 | dQ_1 dP_2 ...
 // S_{j+1} is issued as soon as the elementwise warps have read S_j.
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int NWG>
+__global__ void __launch_bounds__(128 + 128 * NWG, 1)
     attn_bwd_dq4_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
                         int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
                         const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
@@ -757,9 +769,9 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&kv_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 8);
+    mbar_init(s_free, 4 * NWG);
     mbar_init(dp_full, 1);
-    mbar_init(ds_full, 8);
+    mbar_init(ds_full, 4 * NWG);
     mbar_init(q_ready, 8);
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t sk = ktile(j);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol(kk), mnmaj_desc(sk, kk), idesc_q, (j | kk) != 0);
+          umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol<NWG>(kk), mnmaj_desc(sk, kk), idesc_q, (j | kk) != 0);
         umma_commit(&kv_empty[j % NST]);
       }
       __syncwarp();
@@ -834,38 +846,41 @@ __global__ void __launch_bounds__(384, 1)
     if (elect_one()) umma_commit(fin);
     __syncwarp();
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;          // key columns [64 wg, 64 wg + 64) of each block
+    constexpr int CW = 128 / NWG;             // key columns per warpgroup
+    const int wg = (warp - 4) >> 2;          // key columns [CW wg, CW wg + CW) of each block
     const int q = warp & 3;
     const int t = q * 32 + lane;
     const int row = q0 + t;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     if (wg == 0) row_to_tmem<D>(lb, Q_COL, qkv + (int64_t)row * ld + head * D, true);
-    else row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(q_ready);
+    else if (wg == 1) row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
+    if (wg < 2) {
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
     const float nl2 = -lse[(int64_t)head * s + row] * LOG2E;
     const float dd = Dd[(int64_t)head * s + row];
-    const uint32_t c_s = lb + S_COL + 64 * wg, c_d = lb + DP_COL + 64 * wg;
+    const uint32_t c_s = lb + S_COL + CW * wg, c_d = lb + DP_COL + CW * wg;
     for (int j = 0; j < nkv; ++j) {
       const bool diag = causal && j == nkv - 1;
-      float p[64];
+      float p[CW];
       {
-        uint32_t sa[32], sb[32];
+        uint32_t sr[CW / 32][32];
         mbar_wait(s_full, j & 1);
         tc_fence_after();
-        tmem_ld32(c_s, sa);
-        tmem_ld32(c_s + 32, sb);
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h) tmem_ld32(c_s + 32 * h, sr[h]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
         const f2 sl2{scale_log2, scale_log2}, nl{nl2, nl2};
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
-          const f2 x = fma2(f2{__uint_as_float(e < 32 ? sa[e] : sb[e - 32]),
-                               __uint_as_float(e + 1 < 32 ? sa[e + 1] : sb[e + 1 - 32])}, sl2, nl);
+        for (int e = 0; e < CW; e += 2) {
+          const f2 x = fma2(f2{__uint_as_float(sr[e / 32][e % 32]), __uint_as_float(sr[(e + 1) / 32][(e + 1) % 32])},
+                            sl2, nl);
           f2 pp;
           if (emu_pair(e >> 1)) {
             pp = exp2_fma2(x);                   // share of the pairs on the FMA pipe
@@ -878,15 +893,15 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (diag) {
 #pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (64 * wg + e > t) p[e] = 0.f;
+          for (int e = 0; e < CW; ++e)
+            if (CW * wg + e > t) p[e] = 0.f;
         }
       }
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
-      uint32_t pk[32];
+      uint32_t pk[CW / 2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < CW / 32; ++h) {
         uint32_t dv[32];
         tmem_ld32(c_d + 32 * h, dv);
         tmem_ld_wait();
@@ -897,7 +912,8 @@ __global__ void __launch_bounds__(384, 1)
           pk[16 * h + e / 2] = pack_bf16(d.x, d.y);
         }
       }
-      tmem_st32(c_d, pk);
+      if (CW == 64) tmem_st32(c_d, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      else tmem_st16(c_d, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -906,7 +922,7 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(fin, 0);
     tc_fence_after();
     __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
-    for (int c = wg; c < D / 64; c += 2) {
+    for (int c = wg; c < D / 64; c += NWG) {
       uint32_t ra[32], rb[32];
       tmem_ld32(lb + DQ_COL + c * 32, ra);
       tmem_ld32(lb + DQ_COL + c * 32 + D / 2, rb);
@@ -990,22 +1006,41 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   int rc = make_map_rows(&kv128, qkv, cols, s, ld, 128);
   rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, s, ld_out, 128);
   if (rc) return (int)cudaErrorInvalidValue;
+  // Elementwise warpgroups per CTA, measured under fixed clocks (ncu --clock-control
+  // base, s = 16384): dK/dV 4 (4766 us vs 4792 with 2), dQ 2 (3408 us vs 3484 with 4).
+  // PDS_BWD_NWG=2|4 forces both (A/B).
+  static const int force = [] {
+    const char* e = getenv("PDS_BWD_NWG");
+    return e ? atoi(e) : 0;
+  }();
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
-    cudaFuncSetAttribute(attn_bwd_dq4_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dq4_kernel<D, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dkdv4_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdKV4Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_bwd_dq4_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, BwdQ4Cfg<D>::SMEM);
     once = true;
   }
   const float scale = 1.0f / sqrtf((float)D);
   const float scale_log2 = scale * LOG2E;
-  // the Q map is the K/V map (same buffer, same box): only the column offset differs
-  attn_bwd_dkdv4_kernel<D><<<dim3(s / 128, heads), 384, BwdKV4Cfg<D>::SMEM, st>>>(
-      kv128, kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-      reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
-  attn_bwd_dq4_kernel<D><<<dim3(s / 128, heads), 384, BwdQ4Cfg<D>::SMEM, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
-      reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-      reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  auto dkdv = [&](auto nw) {
+    constexpr int NW = decltype(nw)::value;
+    // the Q map is the K/V map (same buffer, same box): only the column offset differs
+    attn_bwd_dkdv4_kernel<D, NW><<<dim3(s / 128, heads), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
+        kv128, kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  };
+  auto dq = [&](auto nw) {
+    constexpr int NW = decltype(nw)::value;
+    attn_bwd_dq4_kernel<D, NW><<<dim3(s / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
+        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
+        reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
+        reinterpret_cast<const float2*>(rope), scale, scale_log2);
+  };
+  if (force == 2) dkdv(std::integral_constant<int, 2>{});
+  else dkdv(std::integral_constant<int, 4>{});
+  if (force == 4) dq(std::integral_constant<int, 4>{});
+  else dq(std::integral_constant<int, 2>{});
   return (int)cudaGetLastError();
 }
 

@@ -31,7 +31,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "{\n"
       ".reg .pred p;\n"
       "LAB_WAIT:\n"
+#ifdef PDS_WAIT_NOHINT
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n"
+#endif
       "@p bra.uni DONE;\n"
       "bra.uni LAB_WAIT;\n"
       "DONE:\n"

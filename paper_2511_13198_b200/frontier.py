@@ -64,9 +64,9 @@ def run_stack(torch, B, ctx, model, plan, s, layers, timed=True, release=True):
                 ctx.saved_release(sv)
         del acts
         torch.cuda.synchronize()
-        if release:
+        if release:                 # keep both caches for an immediate rerun at the same length
             ctx.release_cache()
-        torch.cuda.empty_cache()
+            torch.cuda.empty_cache()
 
 
 def main():

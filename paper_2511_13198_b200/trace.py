@@ -63,8 +63,21 @@ def switches(recs):
     return {"plan_changes_between_sequences": between, "strategy_boundaries_inside_plans": inside}
 
 
-def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None):
+def measure(torch, B, ctx, model, plan, s, layers, memo):
+    """Device time of one fwd + bwd of the stack under `plan` at length s: an untimed
+    warm-up pass (allocations of the saved arena / workspace at this length), then
+    the timed pass.  Memoised on (s, plan): variants that choose the same plan for
+    the same length share one measurement, so ablation deltas are not clock noise."""
     from .frontier import run_stack
+    key = (s, tuple(plan))
+    if key not in memo:
+        run_stack(torch, B, ctx, model, plan, s, layers, release=False)
+        memo[key] = run_stack(torch, B, ctx, model, plan, s, layers)
+    return memo[key]
+
+
+def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None, memo=None):
+    memo = {} if memo is None else memo
     recs, cum, oom_at = [], 0.0, None
     for s in lens:
         if fixed is None:
@@ -76,8 +89,10 @@ def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None):
         else:
             plan, flags = [fixed] * L, 0
         try:
-            t = run_stack(torch, B, ctx, model, plan, s, layers)
+            t = measure(torch, B, ctx, model, plan, s, layers, memo)
         except (B.PdsError, torch.OutOfMemoryError):
+            ctx.release_cache()
+            torch.cuda.empty_cache()
             oom_at = s
             recs.append({"s": s, "oom": True})
             break
@@ -161,14 +176,16 @@ def main():
         ctx.set_capacity(cap, gamma if gamma > 0 else 1e-9)
         return ctx
 
+    out["timing"] = "per (s, plan): one untimed warm-up pass, then one timed fwd + bwd of the stack (memoised)"
     if a.ablation:
         variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=0x6, gamma=0.05)),
                     ("w/o UlyssesZ", dict(mask=0x5, gamma=0.05)), ("w/o METP", dict(mask=0x3, gamma=0.05)),
                     ("w/o RF", dict(gamma=0.05, pr_only=True)), ("w/o Smoothing", dict(gamma=0.0))]
         out["gamma_full"] = 0.05
+        memo = {}
         for name, kw in variants:
             ctx = context(**kw)
-            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L)
+            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, memo=memo)
             ctx.close()
             r = out["runs"][name]
             print(name, "cum %.1fs" % r["cumulative_s"], "max_s", r["max_s_trained"], r["switching"], flush=True)

@@ -184,3 +184,42 @@ def test_attention_fwd_bwd(d, causal, s):
         assert rel(g[:, hh * d:(hh + 1) * d], dq) < 1e-2
         assert rel(g[:, hq + hh * d:hq + (hh + 1) * d], dk) < 1e-2
         assert rel(g[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d], dv) < 1e-2
+
+
+_NWG_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2511_13198_b200 import binding as B
+s, heads, d = 640, 2, 128
+hq = heads * d
+g = torch.Generator().manual_seed(3)
+qkv = (torch.randn(s, 3 * hq, generator=g) * 0.5).to(torch.bfloat16).cuda()
+dout = torch.randn(s, hq, generator=g).to(torch.bfloat16).cuda()
+out = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+dqkv = torch.empty_like(qkv)
+B.k_attn_fwd(qkv.data_ptr(), 3 * hq, s, heads, d, 1, out.data_ptr(), hq, lse.data_ptr(), 0)
+B.k_attn_bwd(qkv.data_ptr(), 3 * hq, out.data_ptr(), hq, lse.data_ptr(), dout.data_ptr(), s, heads, d, 1,
+             dqkv.data_ptr(), 0)
+torch.cuda.synchronize()
+np.save(sys.argv[2], dqkv.view(torch.int16).cpu().numpy())
+"""
+
+
+def test_attention_bwd_warpgroup_variants_bitwise(tmp_path):
+    """dK/dV and dQ kernels with 2 or 4 elementwise warpgroups (PDS_BWD_NWG) run the
+    same MMAs in the same order on the same per-element arithmetic: bit-identical."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for v in ("", "2", "4"):
+        f = tmp_path / f"dqkv{v or 'default'}.npy"
+        env = dict(os.environ)
+        env.pop("PDS_BWD_NWG", None)
+        if v:
+            env["PDS_BWD_NWG"] = v
+        subprocess.run([sys.executable, "-c", _NWG_SCRIPT, root, str(f)], check=True, env=env, timeout=300)
+        outs[v] = np.load(f)
+    assert np.array_equal(outs[""], outs["2"]) and np.array_equal(outs[""], outs["4"])
