@@ -94,9 +94,11 @@ typedef struct { void *dw_qkv_t, *dw_proj, *dw_in_t, *dw_out, *dg1, *dg2; } pds_
  * (e.g. via torch.distributed) before every rank calls pds_create. */
 pds_status pds_nccl_unique_id(void* out128);
 
-/* Create the per-rank context on `device`.  P = 1: no communicator.  P > 1:
- * nccl_unique_id (host, 128 B) must be the same on all ranks; the NCCL
- * communicator is created collectively (blocks until all ranks join). */
+/* Create the per-rank context on `device`.  P = 1 and nccl_unique_id = NULL: no
+ * communicator (collectives are identities).  Otherwise nccl_unique_id (host, 128 B)
+ * must be the same on all ranks and the NCCL communicator is created collectively
+ * (blocks until all ranks join); P = 1 with an id gives a one-rank NCCL
+ * communicator, which runs the NCCL code path on a single GPU. */
 pds_status pds_create(const pds_model* model, int32_t P, int32_t rank, int32_t device,
                       const void* nccl_unique_id, pds_ctx** out);
 

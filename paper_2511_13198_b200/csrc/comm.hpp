@@ -34,6 +34,8 @@ struct Comm {
   // one communicator; loopback / self: the same object).  Collective: every rank
   // calls it at the same point of the program.
   virtual Comm* side(pds_status* st) { return this; }
+  // true when every collective is an identity (one rank, no library)
+  virtual bool trivial() const { return false; }
 };
 
 Comm* make_nccl_comm(int P, int rank, const void* uid, pds_status* st);

@@ -225,6 +225,24 @@ struct Exec {
     if (!c->comm_st) cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking);
     return c->comm_st;
   }
+  // an event marking everything enqueued on `s` so far; consume it with wait()
+  cudaEvent_t mark(cudaStream_t s) {
+    cudaEvent_t ev;
+    if (c->sync_pool.empty()) {
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    } else {
+      ev = c->sync_pool.back();
+      c->sync_pool.pop_back();
+    }
+    cudaEventRecord(ev, s);
+    return ev;
+  }
+  pds_status wait(cudaStream_t s, cudaEvent_t ev) {
+    PDS_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    c->sync_pool.push_back(ev);
+    return PDS_OK;
+  }
+  cudaStream_t side_stream() { return c->comm->trivial() ? st : comm_stream(); }
   // `to` waits for everything enqueued on `from` so far
   pds_status link(cudaStream_t from, cudaStream_t to) {
     if (from == to) return PDS_OK;
@@ -365,16 +383,19 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
 }
 
 // ================================================================== UlyssesZ
-pds_status uz_gather_w(Exec& e, const pds_weights* w, char* ws, const BufPlan& bp) {
-  PDS_TRY(e.ag(w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));   // ZeRO3: rows contiguous
-  PDS_TRY(e.ag(w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
-  PDS_TRY(e.ag(w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
-  return e.ag(w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h);
-}
-
+// ZeRO3 weight gathers (rows contiguous).  The first weight a pass needs
+// is gathered on the compute stream; the others are prefetched on the side stream
+// while the compute stream works, each consumed through its own event.
 pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
   const BufPlan& bp = sv->plan;
-  PDS_TRY(uz_gather_w(e, w, ws, bp));
+  const cudaStream_t cs = e.side_stream();
+  PDS_TRY(e.link(e.st, cs));                 // gather buffers free (previous layer done with them)
+  PDS_TRY(e.ag(w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h));
+  cudaEvent_t ev_ffn = e.mark(cs);
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
@@ -398,9 +419,11 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
     Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * e.h);
     PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, e.hl, sv->at("afull"), e.h, e.st), "unpack"));
   }
+  PDS_TRY(e.wait(e.st, ev_proj));
   PDS_TRY(tn.xw(sv->at("afull"), e.h, wproj, e.h, e.sl, e.h, e.h, u1, e.h));          // O
   PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), s1, sv->at("rstd2")));
+  PDS_TRY(e.wait(e.st, ev_ffn));
   GemmArgs fc1 = Exec::G(s1, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
@@ -420,7 +443,15 @@ pds_status uz_dw(Exec& e, char* dw, int64_t rows_full, void* grad) {
 pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
                   char* ws) {
   const BufPlan& bp = sv->plan;
-  PDS_TRY(uz_gather_w(e, w, ws, bp));
+  const cudaStream_t cs = e.side_stream();
+  PDS_TRY(e.link(e.st, cs));
+  PDS_TRY(e.ag(w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
+  cudaEvent_t ev_in = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));
+  cudaEvent_t ev_qkv = e.mark(cs);
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
@@ -447,8 +478,10 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
   PDS_TRY(tn.dw(f1, e.F, u1, e.h, e.sl, e.F, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(e.wait(e.st, ev_in));
   PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
+  PDS_TRY(e.wait(e.st, ev_proj));
   GemmArgs dafull = Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, s1, e.hl);
   dafull.blk_w = (int)e.hl;
   dafull.blk_stride = e.sl * e.hl;
@@ -465,6 +498,7 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
   PDS_TRY(tn.dw(x4, 3 * e.h, u1, e.h, e.sl, 3 * e.h, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, 3 * e.h, g->dw_qkv_t));
+  PDS_TRY(e.wait(e.st, ev_qkv));
   PDS_TRY(tn.xw(x4, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
@@ -491,7 +525,7 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   // ring-based execution"): AG(k+1) into one of two buffers while the
   // GEMM of wave k reads the other.  At P = 1 the gathers are identities.
   char* gb[2] = {wg, ws + bp.ws_off("wg2")};
-  const cudaStream_t cs = e.P > 1 ? e.comm_stream() : e.st;
+  const cudaStream_t cs = e.c->comm->trivial() ? e.st : e.comm_stream();
   auto waves = [&](const char* src, auto&& gemm_wave) -> pds_status {
     PDS_TRY(e.link(e.st, cs));                                   // src rows are ready
     PDS_TRY(e.ag_on(cs, src, gb[0], wr * e.h));
@@ -682,9 +716,9 @@ extern "C" pds_status pds_create(const pds_model* model, int32_t P, int32_t rank
   if (!out) PDS_FAIL(PDS_EINVAL, "NULL out");
   std::unique_ptr<pds_ctx> c(new pds_ctx());
   PDS_TRY(ctx_common(c.get(), model, P, rank, device));
-  if (P == 1) {
+  if (P == 1 && !nccl_unique_id) {
     c->comm = make_self_comm();
-  } else {
+  } else {       // P = 1 with an id: a one-rank NCCL communicator (exercises the NCCL path)
     if (!nccl_unique_id) PDS_FAIL(PDS_EINVAL, "P > 1 needs an NCCL unique id");
     pds_status st = PDS_OK;
     c->comm = make_nccl_comm(P, rank, nccl_unique_id, &st);

@@ -121,13 +121,14 @@ def time_full_at(full, s_max):
 
 
 def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
-    """Stack time of a mixed plan vs sum of per-layer times from short uniform stacks."""
-    from .frontier import run_stack
+    """Stack time of a mixed plan vs sum of per-layer times from short uniform stacks
+    (every stack warmed up once at this length, then timed)."""
+    memo = {}
     per_layer = {}
     for pi in sorted(set(plan)):
-        t = run_stack(torch, B, ctx, model, [pi] * n_short, s, layers)
+        t = measure(torch, B, ctx, model, [pi] * n_short, s, layers, memo)
         per_layer[pi] = t / n_short
-    t_mixed = run_stack(torch, B, ctx, model, plan, s, layers)
+    t_mixed = measure(torch, B, ctx, model, plan, s, layers, memo)
     pred = sum(per_layer[p] for p in plan)
     return {"s": s, "plan": "".join("TUM"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
             "overhead": t_mixed / pred - 1.0,
@@ -202,9 +203,10 @@ def main():
         for row in table:
             print(row, flush=True)
     else:
+        memo = {}
         for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1)):
             ctx = context(mask=0x7 if fixed is None else 1 << fixed, gamma=a.gamma)
-            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, fixed)
+            out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, fixed, memo=memo)
             ctx.close()
             r = out["runs"][name]
             print(name, "cum %.1fs" % r["cumulative_s"], "oom_at", r["oom_at"], "max_s", r["max_s_trained"],

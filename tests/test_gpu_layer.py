@@ -214,3 +214,29 @@ def test_step_host(pi):
     assert rel(host(yh)[:, None, :], y_ref) < TOL
     assert rel(host(dxh)[:, None, :], g_ref["dx"]) < TOL
     ctx.close()
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_nccl_one_rank_equals_self(pi):
+    """The NCCL backend (a one-rank communicator: pds_create with P = 1 and a unique
+    id) runs every collective of the strategy, METP's side-stream wave gathers on a
+    split communicator included (c = 2 waves), and must reproduce the no-communicator
+    context bit for bit."""
+    h, n, F, s = 256, 4, 1024, 512
+    d = layer_inputs(h, n, F, s, 1, seed=9)
+    W = OS.shard_weights(d, n, 1)
+    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=2)
+    res = []
+    for uid in (None, B.nccl_unique_id()):
+        R = Rank(W, 0, d["x"], d["dy"])
+        ctx = B.Context(model, P=1, rank=0, device=0, uid=uid)
+        st = torch.cuda.current_stream()
+        sv = ctx.layer_fwd(pi, s, R.x.data_ptr(), R.weights(), R.y.data_ptr(), st.cuda_stream)
+        ctx.layer_bwd(pi, R.dy.data_ptr(), sv, R.weights(), R.grads(), R.dx.data_ptr(), st.cuda_stream)
+        st.synchronize()
+        res.append(R)
+        ctx.close()
+    a, b = res
+    assert torch.equal(a.y, b.y) and torch.equal(a.dx, b.dx)
+    for k in a.g:
+        assert torch.equal(a.g[k], b.g[k]), k
