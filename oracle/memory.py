@@ -64,6 +64,9 @@ def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
     if pi == TS:
         bufs = [s * h * 2, s * h * 2, s * Fl * 2, s * Fl * 2, lam, _norm_bwd_grid(sl) * h * 4,
                 max(Fl, 3 * hl) * s * 2, h * s * 2, h * max(Fl, 3 * hl) * 2]
+        if P > 1:
+            bufs.append(s * h * 2)      # second gather buffer: bwd re-gathers prefetched
+
     elif pi == UZ:
         bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
                 u, 3 * u, 3 * u, sl * ffn * 2, sl * ffn * 2, 3 * u, 3 * u, u, lam,

@@ -1,5 +1,6 @@
 // Internal declarations of the ParaDySe C-ABI library (not part of the ABI).
 #pragma once
+#include <cstring>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,6 +52,11 @@ struct BufPlan {
   int64_t off(const std::vector<Region>& v, const char* n) const;
   int64_t saved_off(const char* n) const { return off(saved, n); }
   int64_t ws_off(const char* n) const { return off(ws, n); }
+  bool has_ws(const char* n) const {
+    for (const Region& r : ws)
+      if (std::strcmp(r.name, n) == 0) return true;
+    return false;
+  }
 };
 
 int rmsnorm_bwd_grid(int64_t rows);

@@ -358,14 +358,37 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   const int64_t slot = e.r * e.sl * e.h * 2;
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  // P > 1: the re-gathers of v and u (for dW_in and dW_qkv) go into a second gather
+  // buffer on the side stream, overlapping the dG / dW_out GEMMs resp. the attention
+  // backward; P = 1 keeps one buffer and program order (the gathers are identities).
+  const bool pre = bp.has_ws("gather2");
+  char* g2 = pre ? ws + bp.ws_off("gather2") : gather;
+  const cudaStream_t cs = pre ? e.side_stream() : e.st;
+  cudaEvent_t ev_v = nullptr, ev_u = nullptr;
+  if (pre) {
+    PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, g2 + slot));
+    PDS_TRY(e.link(e.st, cs));
+    PDS_TRY(e.ag_on(cs, g2 + slot, g2, e.sl * e.h));                                  // AG(v) re-gather
+    ev_v = e.mark(cs);
+  }
   PDS_TRY(e.ag(dy, gather, e.sl * e.h));                                                // AG(dz)
   GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
   dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.Fl;
   PDS_TRY(e.gemm(dgel));                                                                // dH, G
   PDS_TRY(tn.dw(f0, e.Fl, gather, e.h, e.s, e.Fl, e.h, g->dw_out));                      // dW_out += G^T dZ
-  PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, gather + slot));
-  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(v) re-gather
-  PDS_TRY(tn.dw(f1, e.Fl, gather, e.h, e.s, e.Fl, e.h, g->dw_in_t));                     // dW_in^T += dH^T V
+  if (pre) {
+    PDS_TRY(e.wait(e.st, ev_v));
+  } else {
+    PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, gather + slot));
+    PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(v) re-gather
+  }
+  PDS_TRY(tn.dw(f1, e.Fl, g2, e.h, e.s, e.Fl, e.h, g->dw_in_t));                         // dW_in^T += dH^T V
+  if (pre) {
+    PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, g2 + slot));
+    PDS_TRY(e.link(e.st, cs));
+    PDS_TRY(e.ag_on(cs, g2 + slot, g2, e.sl * e.h));                                  // AG(u) re-gather
+    ev_u = e.mark(cs);
+  }
   PDS_TRY(tn.xw(f1, e.Fl, w->w_in_t, e.h, e.s, e.h, e.Fl, partial, e.h));               // dV = dH W_in^T
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(dv)
   PDS_TRY(e.norm_bwd(partial + slot, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
@@ -373,9 +396,13 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(tn.mm(gather, e.h, w->w_proj, e.h, e.s, e.hl, e.h, f1, e.hl));                 // dA
   PDS_TRY(tn.dw(sv->at("a"), e.hl, gather, e.h, e.s, e.hl, e.h, g->dw_proj));            // dW_proj += A^T dX1
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), f1, f0, dd));            // dQKV (RoPE^T)
-  PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, gather + slot));
-  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u) re-gather
-  PDS_TRY(tn.dw(f0, 3 * e.hl, gather, e.h, e.s, 3 * e.hl, e.h, g->dw_qkv_t));           // dW_qkv^T += dQKV^T U
+  if (pre) {
+    PDS_TRY(e.wait(e.st, ev_u));
+  } else {
+    PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, gather + slot));
+    PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(u) re-gather
+  }
+  PDS_TRY(tn.dw(f0, 3 * e.hl, g2, e.h, e.s, 3 * e.hl, e.h, g->dw_qkv_t));               // dW_qkv^T += dQKV^T U
   PDS_TRY(tn.xw(f0, 3 * e.hl, w->w_qkv_t, e.h, e.s, e.h, 3 * e.hl, partial, e.h));      // dU = dQKV W_qkv^T
   PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(du)
   PDS_TRY(e.norm_bwd(partial + slot, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));

@@ -252,6 +252,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * s * 2);   // transposed operands (all GEMMs TN)
       push(p.ws, tw, "tb", h * s * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      if (P > 1) push(p.ws, tw, "gather2", s * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
       push(p.saved, ts, "rstd1", ell);
