@@ -54,6 +54,9 @@ struct EpiParams {
   int rope_d, rope_hq;
   int64_t seg, seg_stride, seg_base;
   int64_t c_seg, c_stride, c_base;
+  __nv_bfloat16* c_t;      // transposed copies (dGELU epilogue): [N][ld_t]
+  __nv_bfloat16* aux_t;
+  int64_t ld_t;
 };
 
 struct RowMap {
@@ -82,6 +85,15 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int&
   const int idx = t - band * GROUP_M * nt;
   mb = first + idx % gm;
   nb = idx / gm;
+}
+
+// transposed store: element (row, col + i) -> dst[(col + i) * ld + row]; the 32 lanes
+// of a warp hold 32 consecutive rows, so each column is one 64-byte segment
+__device__ __forceinline__ void store_col32_bf16(__nv_bfloat16* dst, int64_t ld, int row, int col, const float* v,
+                                                 int valid) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < valid) dst[(int64_t)(col + i) * ld + row] = __float2bfloat16_rn(v[i]);
 }
 
 // store 32 consecutive bf16 values of one row
@@ -214,7 +226,9 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
         }
         store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
                          valid);
-        store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+        if (ep.aux_out) store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+        if (ep.c_t) store_col32_bf16(ep.c_t, ep.ld_t, row, col, v, valid);
+        if (ep.aux_t) store_col32_bf16(ep.aux_t, ep.ld_t, row, col, g, valid);
       }
       }
       __syncwarp();
@@ -617,6 +631,9 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.aux_in = reinterpret_cast<const __nv_bfloat16*>(g.aux_in);
   ep.aux_out = reinterpret_cast<__nv_bfloat16*>(g.aux_out);
   ep.ld_aux = g.ld_aux;
+  ep.c_t = reinterpret_cast<__nv_bfloat16*>(g.c_t);
+  ep.aux_t = reinterpret_cast<__nv_bfloat16*>(g.aux_t);
+  ep.ld_t = g.ld_t;
   ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq;
   ep.seg = g.seg > 0 ? g.seg : (int64_t)1 << 40;
   ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;

@@ -53,6 +53,12 @@ struct GemmArgs {
   int64_t c_seg = 0, c_stride = 0, c_base = 0;
   // storage row counts of A / B when remapped (0: the logical extent)
   int64_t a_rows = 0, b_rows = 0;
+  // EPI_DGELU only: transposed bf16 copies of C (dH^T) and of the aux output (G^T),
+  // [N][ld_t] (element (r, c) at c * ld_t + r); aux_out may then be NULL.  They feed
+  // the dW GEMMs, which take both operands K-major (K = tokens).
+  void* c_t = nullptr;
+  void* aux_t = nullptr;
+  int64_t ld_t = 0;
 };
 
 // returns 0 on success, a cudaError_t value otherwise

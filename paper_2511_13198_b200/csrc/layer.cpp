@@ -372,17 +372,22 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     ev_v = e.mark(cs);
   }
   PDS_TRY(e.ag(dy, gather, e.sl * e.h));                                                // AG(dz)
+  // dH (row-major, for dV) plus the two operands the dW GEMMs need K-major, straight
+  // from the epilogue: dH^T into f0, G^T into ta (G itself is never stored)
   GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.Fl;
-  PDS_TRY(e.gemm(dgel));                                                                // dH, G
-  PDS_TRY(tn.dw(f0, e.Fl, gather, e.h, e.s, e.Fl, e.h, g->dw_out));                      // dW_out += G^T dZ
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.Fl;
+  dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.s;
+  PDS_TRY(e.gemm(dgel));                                                                // dH, dH^T, G^T
+  PDS_TRY(tn.tr(gather, e.h, e.s, e.h, tn.tb));
+  PDS_TRY(tn.mm(tn.ta, e.s, tn.tb, e.s, e.Fl, e.h, e.s, g->dw_out, e.h, EPI_F32_ACC));     // dW_out += G^T dZ
   if (pre) {
     PDS_TRY(e.wait(e.st, ev_v));
   } else {
     PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, gather + slot));
     PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(v) re-gather
   }
-  PDS_TRY(tn.dw(f1, e.Fl, g2, e.h, e.s, e.Fl, e.h, g->dw_in_t));                         // dW_in^T += dH^T V
+  PDS_TRY(tn.tr(g2, e.h, e.s, e.h, tn.tb));
+  PDS_TRY(tn.mm(f0, e.s, tn.tb, e.s, e.Fl, e.h, e.s, g->dw_in_t, e.h, EPI_F32_ACC));      // dW_in^T += dH^T V
   if (pre) {
     PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, g2 + slot));
     PDS_TRY(e.link(e.st, cs));
@@ -498,12 +503,15 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
   GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.aux_out = f0; dgel.ld_aux = e.F;
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;                                 // G^T, dH^T
   PDS_TRY(e.gemm(dgel));
-  PDS_TRY(tn.dw(f0, e.F, dy, e.h, e.sl, e.F, e.h, dw, EPI_F32));
+  PDS_TRY(tn.tr(dy, e.h, e.sl, e.h, tn.tb));
+  PDS_TRY(tn.mm(tn.ta, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));           // dW_out (full, local)
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
-  PDS_TRY(tn.dw(f1, e.F, u1, e.h, e.sl, e.F, e.h, dw, EPI_F32));
+  PDS_TRY(tn.tr(u1, e.h, e.sl, e.h, tn.tb));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));              // dW_in^T (full, local)
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
   PDS_TRY(e.wait(e.st, ev_in));
   PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
@@ -627,10 +635,13 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                    // AG(v)
     PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                   // H recompute
     GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.Fl, EPI_DGELU);
-    dgel.aux_in = hw; dgel.aux_out = gw; dgel.ld_aux = e.Fl;
+    dgel.aux_in = hw; dgel.ld_aux = e.Fl;
+    dgel.aux_t = tn.ta; dgel.c_t = gw; dgel.ld_t = W;                                  // G^T, dH^T
     PDS_TRY(e.gemm(dgel));
-    PDS_TRY(tn.dw(gw, e.Fl, wg, e.h, W, e.Fl, e.h, g->dw_out));
-    PDS_TRY(tn.dw(dhw, e.Fl, wg2, e.h, W, e.Fl, e.h, g->dw_in_t));
+    PDS_TRY(tn.tr(wg, e.h, W, e.h, tn.tb));
+    PDS_TRY(tn.mm(tn.ta, W, tn.tb, W, e.Fl, e.h, W, g->dw_out, e.h, EPI_F32_ACC));      // dW_out += G^T dZ
+    PDS_TRY(tn.tr(wg2, e.h, W, e.h, tn.tb));
+    PDS_TRY(tn.mm(gw, W, tn.tb, W, e.Fl, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC));        // dW_in^T += dH^T V
     PDS_TRY(tn.mm(dhw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
     PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(dv)
     PDS_TRY(e.norm_bwd(pw + slot, sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, dyb + o * row, wr,
