@@ -69,11 +69,6 @@ struct RowMap {
 __device__ __forceinline__ float gelu_f(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
-__device__ __forceinline__ float gelu_grad_f(float x) {
-  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
-  return cdf + x * pdf;
-}
 __device__ __forceinline__ float bf16_round(float x) {
   return __bfloat162float(__float2bfloat16_rn(x));
 }
@@ -220,9 +215,12 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
         float hh[32], g[32];
         load_row32_bf16(ep.aux_in + (int64_t)row * ep.ld_aux + col, hh, valid);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          g[i] = gelu_f(hh[i]);
-          v[i] = v[i] * gelu_grad_f(hh[i]);
+        for (int i = 0; i < 32; ++i) {        // one erf per element: G = x Phi, G' = Phi + x phi
+          const float x = hh[i];
+          const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+          const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+          g[i] = x * cdf;
+          v[i] = v[i] * (cdf + x * pdf);
         }
         store_row32_bf16(reinterpret_cast<__nv_bfloat16*>(ep.C) + out_offset(ep, row, col), v,
                          valid);
@@ -377,7 +375,7 @@ __global__ void __launch_bounds__(256, 1)
 // reads 32 KB per stage instead of 48 KB for the same MMA work; each CTA's TMEM holds
 // its 128 rows of the accumulator and its own epilogue warps drain them.
 template <int A_MN, int B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     int M, int N, int K, RowMap amap, RowMap bmap, EpiParams ep) {
   constexpr int STAGES = 6;
@@ -409,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 8);
+      mbar_init(&tempty_bar[i], 16);      // 8 epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -484,7 +482,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
+    // two epilogue warpgroups, one per 128-column half of the accumulator, so heavy
+    // epilogues (dGELU with transposed copies, RoPE) stay under the mainloop time
     const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < ntiles; t += ncl) {
@@ -493,8 +494,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + rank * 128 + q * 32 + lane;
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
-      epilogue_tile<256>(ep, tbase, row, row < M, nb * 256, N);
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + half * 128;
+      epilogue_tile<128>(ep, tbase, row, row < M, nb * 256 + half * 128, N);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_u32(&tempty_bar[acc], 0));
@@ -610,7 +611,7 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   const int ncl = std::min(tiles, gemm_num_sms() / 2);
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
-  kern<<<2 * ncl, 256, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep);
+  kern<<<2 * ncl, 384, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep);
   return (int)cudaGetLastError();
 }
 
