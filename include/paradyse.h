@@ -177,16 +177,21 @@ pds_status pds_layer_bwd(pds_ctx* ctx, uint8_t strategy, const void* dy, pds_sav
                          const pds_weights* w, const pds_grads* g, void* dx, void* stream);
 /* End-to-end step with HOST activations (the call a user without device buffers
  * makes): x_host, dy_host (host, [s/P, b, h] bf16) are uploaded into library-owned
- * staging, one layer fwd + bwd runs as pds_layer_fwd / pds_layer_bwd, and y_host,
- * dx_host (host, same layout) receive the results; weight gradients are accumulated
- * into g as in pds_layer_bwd.  The dy upload overlaps the forward and the y download
- * the backward (copy stream inside the context); all work is complete when
- * `stream` reaches the end of the call.  Host buffers should be page-locked for the
- * overlap.  Errors: as pds_layer_fwd / pds_layer_bwd; staging allocation failure ->
- * PDS_ENOMEM. */
+ * staging, one layer fwd + bwd runs as pds_layer_fwd / pds_layer_bwd on `stream`,
+ * and y_host, dx_host (host, same layout) receive the results; weight gradients are
+ * accumulated into g as in pds_layer_bwd.  Asynchronous: uploads and downloads run
+ * on context-owned copy streams and consecutive calls alternate between two staging
+ * sets, so a call's transfers overlap the neighbouring calls' compute.  Host buffers
+ * must be page-locked for the overlap and must stay untouched until
+ * pds_host_drain(ctx, stream) has been enqueued and `stream` has reached it; the
+ * compute of every call is ordered on `stream`.  Errors: as pds_layer_fwd /
+ * pds_layer_bwd; staging allocation failure -> PDS_ENOMEM. */
 pds_status pds_layer_step_host(pds_ctx* ctx, uint8_t strategy, int64_t seq_len, const void* x_host,
                                const void* dy_host, const pds_weights* w, const pds_grads* g,
                                void* y_host, void* dx_host, void* stream);
+/* Orders `stream` after every transfer of the pds_layer_step_host calls issued so
+ * far (after it, synchronising `stream` makes all y_host / dx_host valid). */
+pds_status pds_host_drain(pds_ctx* ctx, void* stream);
 /* Release a saved set without running backward. */
 pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
 /* Debug taps: the next pds_layer_fwd also writes the sublayer deltas O (attention

@@ -111,6 +111,7 @@ _SIGS = {
                       C.POINTER(_Grads), C.c_void_p, C.c_void_p],
     "pds_layer_step_host": [C.c_void_p, C.c_uint8, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(_Weights),
                             C.POINTER(_Grads), C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_host_drain": [C.c_void_p, C.c_void_p],
     "pds_saved_release": [C.c_void_p, C.c_void_p],
     "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
@@ -145,6 +146,8 @@ def lib():
                               "(python paper_2511_13198_b200/build.py). There is no CPU fallback.")
         L = C.CDLL(LIB_PATH)
         for name, args in _SIGS.items():
+            if os.environ.get("PDS_LIB") and not hasattr(L, name):
+                continue                  # an older A/B build may lack newer entry points
             f = getattr(L, name)
             f.argtypes = args
             f.restype = C.c_char_p if name in ("pds_last_error", "pds_version") else C.c_int
@@ -259,9 +262,14 @@ class Context:
 
     def layer_step_host(self, strategy, seq_len, x_host, dy_host, w: Weights, g: Grads, y_host, dx_host,
                         stream=0):
-        """One layer fwd + bwd on HOST buffers (pinned host pointers); pds_layer_step_host."""
+        """One layer fwd + bwd on HOST buffers (pinned host pointers), asynchronous;
+        results valid after host_drain(stream) and a sync.  pds_layer_step_host."""
         call("pds_layer_step_host", self.h, strategy, seq_len, x_host, dy_host, C.byref(w.c()), C.byref(g.c()),
              y_host, dx_host, stream)
+
+    def host_drain(self, stream=0):
+        """Orders `stream` after all pds_layer_step_host transfers (pds_host_drain)."""
+        call("pds_host_drain", self.h, stream)
 
     def saved_release(self, saved):
         call("pds_saved_release", self.h, saved)

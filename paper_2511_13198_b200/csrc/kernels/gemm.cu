@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(256, 1)
 template <int A_MN, int B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    int M, int N, int K, RowMap amap, RowMap bmap, EpiParams ep, int group_m, int l2mode) {
+                    int M, int N, int K, RowMap amap, RowMap bmap, EpiParams ep, int group_m) {
   constexpr int STAGES = 6;
   constexpr int HALF = 128 * BK * 2;           // 16 KB: one operand half per stage
   constexpr int STAGE = 2 * HALF;
@@ -439,12 +439,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      // L2 policies for the operand streams (l2mode bits: 1 A evict_last, 2 B evict_first,
-      // 4 B evict_last, 8 A evict_first)
-      const uint64_t pol_a = (l2mode & 1) ? l2_policy_evict_last()
-                           : (l2mode & 8) ? l2_policy_evict_first() : l2_policy_evict_normal();
-      const uint64_t pol_b = (l2mode & 2) ? l2_policy_evict_first()
-                           : (l2mode & 4) ? l2_policy_evict_last() : l2_policy_evict_normal();
       for (int t = cid; t < ntiles; t += ncl) {
         int mb, nb;
         tile_coords(t, mt, nt, mb, nb, group_m);
@@ -458,15 +452,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const int k0 = kb * BK;
           if (A_MN) {   // one 3-D box = both 64-wide MN groups (dims: elem, K row, MN group)
             tma_load_3d_2sm(sa, &tmA, fb, 0, amap.map(k0), m0 >> 6);
-          } else if (l2mode) {
-            tma_load_2d_2sm_hint(sa, &tmA, fb, k0, amap.map(m0), pol_a);
           } else {
             tma_load_2d_2sm(sa, &tmA, fb, k0, amap.map(m0));
           }
           if (B_MN) {
             tma_load_3d_2sm(sb, &tmB, fb, 0, bmap.map(k0), n0 >> 6);
-          } else if (l2mode) {
-            tma_load_2d_2sm_hint(sb, &tmB, fb, k0, bmap.map(n0), pol_b);
           } else {
             tma_load_2d_2sm(sb, &tmB, fb, k0, bmap.map(n0));
           }
@@ -640,9 +630,8 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
   static const int env_gm = [] { const char* e = getenv("PDS_GEMM_GM"); return e ? atoi(e) : 0; }();
-  static const int env_l2 = [] { const char* e = getenv("PDS_GEMM_L2"); return e ? atoi(e) : 0; }();
   const int group_m = env_gm > 0 ? env_gm : GROUP_M;
-  kern<<<2 * ncl, 384, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep, group_m, env_l2);
+  kern<<<2 * ncl, 384, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep, group_m);
   return (int)cudaGetLastError();
 }
 

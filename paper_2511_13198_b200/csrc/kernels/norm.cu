@@ -359,7 +359,6 @@ int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int
                 void* x1_out, void* u_out, void* rstd, cudaStream_t st) {
   if (!h_ok(h)) return (int)cudaErrorInvalidValue;
   if (rows <= 0) return 0;
-  const unsigned grid = (unsigned)((rows + 3) / 4);
   auto X = reinterpret_cast<const __nv_bfloat16*>(x);
   auto R = reinterpret_cast<const __nv_bfloat16*>(res);
   auto G = reinterpret_cast<const __nv_bfloat16*>(g);

@@ -73,14 +73,17 @@ struct pds_ctx {
   // debug taps
   void* tap_o = nullptr;
   void* tap_z = nullptr;
-  // host-buffer step (pds_layer_step_host): device staging for x, dy, y, dx + copy stream
+  // host-buffer steps (pds_layer_step_host): two staging sets of x, dy, y, dx used by
+  // alternate calls, an upload and a download stream
   char* stage = nullptr;
-  int64_t stage_cap = 0;
-  cudaStream_t copy_st = nullptr;
+  int64_t stage_cap = 0;       // bytes of one set
+  int stage_next = 0;
+  bool stage_used[2] = {false, false};
+  cudaStream_t up_st = nullptr, down_st = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_y = nullptr, ev_dx = nullptr;
   // side stream for collectives overlapped with compute (METP wave prefetch)
   cudaStream_t comm_st = nullptr;
   std::vector<cudaEvent_t> sync_pool;
-  cudaEvent_t ev_start = nullptr, ev_y = nullptr, ev_dy = nullptr, ev_ycopied = nullptr;
   // profiling
   bool prof = false;
   std::vector<ProfRec> pending;
@@ -95,9 +98,10 @@ struct pds_ctx {
     if (ws) cudaFree(ws);
     if (rope) cudaFree(rope);
     if (stage) cudaFree(stage);
-    for (cudaEvent_t e : {ev_start, ev_y, ev_dy, ev_ycopied})
+    for (cudaEvent_t e : {ev_in[0], ev_in[1], ev_done[0], ev_done[1], ev_y, ev_dx})
       if (e) cudaEventDestroy(e);
-    if (copy_st) cudaStreamDestroy(copy_st);
+    if (up_st) cudaStreamDestroy(up_st);
+    if (down_st) cudaStreamDestroy(down_st);
     if (comm_st) cudaStreamDestroy(comm_st);
     for (auto e : sync_pool) cudaEventDestroy(e);
     delete comm;
@@ -835,6 +839,7 @@ extern "C" pds_status pds_release_cache(pds_ctx* c) {
   if (c->stage) cudaFree(c->stage);
   c->stage = nullptr;
   c->stage_cap = 0;
+  c->stage_used[0] = c->stage_used[1] = false;
   return PDS_OK;
 }
 
@@ -906,10 +911,11 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
   return rc;
 }
 
-// One layer fwd + bwd with HOST activations: x and dy are copied in, y and dx copied
-// out by the library.  The dy upload runs on a copy stream during the forward and
-// the y download during the backward; only the x upload and the dx download are
-// exposed.  Host buffers should be pinned (pageable memory works, without overlap).
+// One layer fwd + bwd with HOST activations.  Uploads run on an upload stream, the
+// y / dx downloads on a download stream, and consecutive calls alternate between two
+// staging sets, so call k+1's uploads overlap call k's compute and call k's
+// downloads overlap call k+1's compute.  pds_host_drain orders `stream` after every
+// outstanding download.
 extern "C" pds_status pds_layer_step_host(pds_ctx* c, uint8_t strategy, int64_t seq_len, const void* x_host,
                                           const void* dy_host, const pds_weights* w, const pds_grads* g,
                                           void* y_host, void* dx_host, void* stream) {
@@ -920,18 +926,19 @@ extern "C" pds_status pds_layer_step_host(pds_ctx* c, uint8_t strategy, int64_t 
   PDS_CUDA(cudaSetDevice(c->device));
   const int64_t nb = seq_len / c->P * c->m.h * 2;       // one local [s/P, b, h] bf16 activation
   const int64_t slot = (nb + 255) / 256 * 256;
-  if (!c->copy_st) {
-    PDS_CUDA(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&c->ev_start, &c->ev_y, &c->ev_dy, &c->ev_ycopied})
+  if (!c->up_st) {
+    PDS_CUDA(cudaStreamCreateWithFlags(&c->up_st, cudaStreamNonBlocking));
+    PDS_CUDA(cudaStreamCreateWithFlags(&c->down_st, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_in[0], &c->ev_in[1], &c->ev_done[0], &c->ev_done[1], &c->ev_y, &c->ev_dx})
       PDS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   if (c->stage_cap < 4 * slot) {
-    PDS_CUDA(cudaStreamSynchronize(st));
-    PDS_CUDA(cudaStreamSynchronize(c->copy_st));
+    PDS_CUDA(cudaDeviceSynchronize());                   // every outstanding step is done with the old sets
     if (c->stage) PDS_CUDA(cudaFree(c->stage));
     c->stage = nullptr;
     c->stage_cap = 0;
-    cudaError_t e = cudaMalloc(&c->stage, 4 * slot);
+    c->stage_used[0] = c->stage_used[1] = false;
+    cudaError_t e = cudaMalloc(&c->stage, 2 * 4 * slot);
     if (e != cudaSuccess) {
       cudaGetLastError();
       PDS_FAIL(e == cudaErrorMemoryAllocation ? PDS_ENOMEM : PDS_ECUDA,
@@ -939,22 +946,38 @@ extern "C" pds_status pds_layer_step_host(pds_ctx* c, uint8_t strategy, int64_t 
     }
     c->stage_cap = 4 * slot;
   }
-  char *x = c->stage, *dy = c->stage + slot, *y = c->stage + 2 * slot, *dx = c->stage + 3 * slot;
-  PDS_CUDA(cudaEventRecord(c->ev_start, st));                       // previous step fully ordered
-  PDS_CUDA(cudaStreamWaitEvent(c->copy_st, c->ev_start, 0));
-  PDS_CUDA(cudaMemcpyAsync(dy, dy_host, nb, cudaMemcpyHostToDevice, c->copy_st));
-  PDS_CUDA(cudaEventRecord(c->ev_dy, c->copy_st));
-  PDS_CUDA(cudaMemcpyAsync(x, x_host, nb, cudaMemcpyHostToDevice, st));
+  const int b = c->stage_next;
+  c->stage_next ^= 1;
+  char* base = c->stage + b * c->stage_cap;
+  char *x = base, *dy = base + slot, *y = base + 2 * slot, *dx = base + 3 * slot;
+  // uploads: set b is free once the call that last used it has downloaded dx
+  if (c->stage_used[b]) PDS_CUDA(cudaStreamWaitEvent(c->up_st, c->ev_done[b], 0));
+  PDS_CUDA(cudaMemcpyAsync(x, x_host, nb, cudaMemcpyHostToDevice, c->up_st));
+  PDS_CUDA(cudaMemcpyAsync(dy, dy_host, nb, cudaMemcpyHostToDevice, c->up_st));
+  PDS_CUDA(cudaEventRecord(c->ev_in[b], c->up_st));
+  PDS_CUDA(cudaStreamWaitEvent(st, c->ev_in[b], 0));
   pds_saved* sv = nullptr;
   PDS_TRY(pds_layer_fwd(c, strategy, seq_len, x, w, y, &sv, stream));
   PDS_CUDA(cudaEventRecord(c->ev_y, st));
-  PDS_CUDA(cudaStreamWaitEvent(c->copy_st, c->ev_y, 0));
-  PDS_CUDA(cudaMemcpyAsync(y_host, y, nb, cudaMemcpyDeviceToHost, c->copy_st));
-  PDS_CUDA(cudaEventRecord(c->ev_ycopied, c->copy_st));
-  PDS_CUDA(cudaStreamWaitEvent(st, c->ev_dy, 0));
+  PDS_CUDA(cudaStreamWaitEvent(c->down_st, c->ev_y, 0));
+  PDS_CUDA(cudaMemcpyAsync(y_host, y, nb, cudaMemcpyDeviceToHost, c->down_st));
   PDS_TRY(pds_layer_bwd(c, strategy, dy, sv, w, g, dx, stream));
-  PDS_CUDA(cudaMemcpyAsync(dx_host, dx, nb, cudaMemcpyDeviceToHost, st));
-  PDS_CUDA(cudaStreamWaitEvent(st, c->ev_ycopied, 0));               // the step ends on `stream`
+  PDS_CUDA(cudaEventRecord(c->ev_dx, st));
+  PDS_CUDA(cudaStreamWaitEvent(c->down_st, c->ev_dx, 0));
+  PDS_CUDA(cudaMemcpyAsync(dx_host, dx, nb, cudaMemcpyDeviceToHost, c->down_st));
+  PDS_CUDA(cudaEventRecord(c->ev_done[b], c->down_st));
+  c->stage_used[b] = true;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_host_drain(pds_ctx* c, void* stream) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (!c->down_st) return PDS_OK;
+  cudaEvent_t ev;
+  PDS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  PDS_CUDA(cudaEventRecord(ev, c->down_st));
+  PDS_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ev, 0));
+  PDS_CUDA(cudaEventDestroy(ev));
   return PDS_OK;
 }
 

@@ -207,7 +207,15 @@ def test_step_host(pi):
     dxh = torch.empty_like(xh).pin_memory()
     ctx.layer_step_host(pi, s, xh.data_ptr(), dyh.data_ptr(), R2.weights(), R2.grads(), yh.data_ptr(),
                         dxh.data_ptr(), st.cuda_stream)
+    # a second, pipelined call on the other staging set with its own host buffers
+    R3 = Rank(W, 0, d["x"], d["dy"])
+    yh3 = torch.empty_like(xh).pin_memory()
+    dxh3 = torch.empty_like(xh).pin_memory()
+    ctx.layer_step_host(pi, s, xh.data_ptr(), dyh.data_ptr(), R3.weights(), R3.grads(), yh3.data_ptr(),
+                        dxh3.data_ptr(), st.cuda_stream)
+    ctx.host_drain(st.cuda_stream)
     st.synchronize()
+    assert torch.equal(yh3, yh) and torch.equal(dxh3, dxh)
     assert torch.equal(yh, R1.y.cpu()) and torch.equal(dxh, R1.dx.cpu())
     for k in R1.g:
         assert torch.equal(R1.g[k], R2.g[k]), k
