@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = bar + 5;     // [2] per tile
   uint64_t* p_full = bar + 7;     // [2] per tile
   uint64_t* o_done = bar + 9;     // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* p_half = bar + 12;    // [2] per tile: P columns of keys 0..63 written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (s + 255) / 256;
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
+      mbar_init(&p_half[i], 4);
       mbar_init(&o_done[i], 1);
     }
     fence_barrier_init();
@@ -224,14 +226,24 @@ __global__ void __launch_bounds__(384, 1)
       }
       __syncwarp();
     };
+    // O_t += P_t V in two halves of keys: the first as soon as the softmax has written
+    // P for keys 0..63, overlapping the exponentials of keys 64..127
     auto issue_pv = [&](int t, int j) {
+      const uint32_t sv = smem_u32(sm + C::V_OFF + (j & 1) * C::TILE);
+      mbar_wait(&p_half[t], j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < BN / 32; ++kk)
+          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
+      }
+      __syncwarp();
       mbar_wait(&p_full[t], j & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sv = smem_u32(sm + C::V_OFF + (j & 1) * C::TILE);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
+        for (int kk = BN / 32; kk < BN / 16; ++kk)
+          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, 1);
       }
       __syncwarp();
     };
@@ -339,6 +351,12 @@ __global__ void __launch_bounds__(384, 1)
             pk[i >> 1] = pack_bf16(p.x, p.y);
           }
           tmem_st8(lb + s_col + c * 8, pk);
+          if (c == BN / 32 - 1) {             // P of keys 0..63 complete: release the first PV half
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_half[tile]);
+          }
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
