@@ -82,13 +82,15 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_baseline(sample_s=1024):
+def cpu_baseline(sample_s=1024, d=None):
     """The fp64 oracle, as it stands, on this host's cores: one 7B layer fwd+bwd at
-    s = sample_s (a bounded sample of the workload), tokens/s = s / seconds."""
+    s = sample_s (a bounded sample of the workload), tokens/s = s / seconds.
+    `d` = pre-generated inputs (the seeded generator is not part of the timing)."""
     import numpy as np
     from oracle import layer as OL
     from synth import layer_inputs
-    d = layer_inputs(H, N_HEADS, FFN, sample_s, 1, seed=42)
+    if d is None:
+        d = layer_inputs(H, N_HEADS, FFN, sample_s, 1, seed=42)
     t0 = time.perf_counter()
     y, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=N_HEADS)
     OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=N_HEADS)
@@ -108,10 +110,12 @@ def run_reference(args, rank, world):
     """--impl reference: the oracle timed as the reference arm (bounded samples)."""
     if rank != 0:
         return
+    from synth import layer_inputs
+    d = layer_inputs(H, N_HEADS, FFN, 512, 1, seed=42)      # generated once, reused by every step
     cb = None
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(sample_s=512)
+        r = cpu_baseline(sample_s=512, d=d)
         if i >= args.warmup:
             vals.append(r["seconds"])
         cb = r
