@@ -208,6 +208,10 @@ pds_status pds_profile_read(pds_ctx* ctx, int32_t klass, double* ms, int64_t* la
                             double* flops, double* bytes);
 pds_status pds_profile_reset(pds_ctx* ctx);
 
+/* Development aid: copies `rows` x 8 clock64 stamps of one dQ-kernel CTA's timeline
+ * (host int64) from a library built with -DPDS_TRACE; PDS_ENOTIMPL otherwise. */
+pds_status pds_debug_trace(int64_t* host_out, int32_t rows);
+
 /* ------------------------------------------------------------------ kernel-level entry points
  * Per-stage parity (fp32-accumulate path, reading R-14).  Device pointers, stream-
  * ordered, no context needed. */

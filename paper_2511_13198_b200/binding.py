@@ -112,6 +112,7 @@ _SIGS = {
     "pds_layer_step_host": [C.c_void_p, C.c_uint8, C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(_Weights),
                             C.POINTER(_Grads), C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_host_drain": [C.c_void_p, C.c_void_p],
+    "pds_debug_trace": [C.c_void_p, C.c_int32],
     "pds_saved_release": [C.c_void_p, C.c_void_p],
     "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
     "pds_profile_enable": [C.c_void_p, C.c_int32],

@@ -99,3 +99,11 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
   cudaFreeAsync(dd, st);
   return r;
 }
+
+extern "C" pds_status pds_debug_trace(int64_t* host_out, int32_t rows) {
+  if (!host_out || rows <= 0 || rows > 4096) PDS_FAIL(PDS_EINVAL, "bad trace buffer");
+  const int rc = attn_debug_trace(reinterpret_cast<long long*>(host_out), rows);
+  if (rc < 0) PDS_FAIL(PDS_ENOTIMPL, "library built without PDS_TRACE");
+  if (rc) PDS_FAIL(PDS_ECUDA, "trace copy failed");
+  return PDS_OK;
+}

@@ -126,6 +126,26 @@ __device__ __forceinline__ f2 exp2_fma2(f2 x) {
 #endif
 __host__ __device__ constexpr bool emu_pair(int pair) { return (PDS_EMU_MASK >> (pair & 7)) & 1; }
 
+// Optional timeline trace of one CTA (build with -DPDS_TRACE=1 for the dQ kernel, =2 for
+// dK/dV; read with pds_debug_trace): clock64 stamps per block, see the kernels.
+#ifdef PDS_TRACE
+__device__ long long g_trace[4096][8];
+#define PDS_TR_(j, k) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (j) < 4096) g_trace[j][k] = clock64();
+#else
+#define PDS_TR_(j, k)
+#endif
+#if defined(PDS_TRACE) && PDS_TRACE == 1
+#define PDS_TR(j, k) PDS_TR_(j, k)
+#else
+#define PDS_TR(j, k)
+#endif
+#if defined(PDS_TRACE) && PDS_TRACE == 2
+#define PDS_TR2(j, k) PDS_TR_(j, k)
+#else
+#define PDS_TR2(j, k)
+#endif
+
 // 16-byte chunk store into a K-major SW128 tile: row r, 16-byte chunk c of atom a
 __device__ __forceinline__ void st_sw128(uint8_t* tile, uint32_t atom, int r, int a, int c, uint4 v) {
   *reinterpret_cast<uint4*>(tile + a * atom + r * 128 + ((c ^ (r & 7)) << 4)) = v;
@@ -587,7 +607,9 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     issue_s(0);
     issue_dp(0);
     for (int i = 0; i < nq; ++i) {
+      if (lane == 0) PDS_TR2(i, 7);
       mbar_wait(p_full, i & 1);
+      if (lane == 0) PDS_TR2(i, 0);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t so = otile(i);
@@ -598,6 +620,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       __syncwarp();
       if (i + 1 < nq) issue_s(i + 1);
       mbar_wait(ds_full, i & 1);
+      if (lane == 0) PDS_TR2(i, 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sq = qtile(i);
@@ -627,10 +650,12 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       {
         uint32_t sr[CW / 32][32];
         mbar_wait(s_full, i & 1);
+        if (warp == 4 && lane == 0) PDS_TR2(i, 2);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < CW / 32; ++h) tmem_ld32(c_s + 32 * h, sr[h]);
         tmem_ld_wait();
+        if (warp == 4 && lane == 0) PDS_TR2(i, 3);
         const f2 sl2{scale_log2, scale_log2}, nlog2e{-LOG2E, -LOG2E};
 #pragma unroll
         for (int e = 0; e < CW; e += 4) {
@@ -669,9 +694,11 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        if (warp == 4 && lane == 0) PDS_TR2(i, 4);
       }
       {
         mbar_wait(dp_full, i & 1);
+        if (warp == 4 && lane == 0) PDS_TR2(i, 5);
         tc_fence_after();
         uint32_t pk[CW / 2];
 #pragma unroll
@@ -696,6 +723,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ds_full);
+        if (warp == 4 && lane == 0) PDS_TR2(i, 6);
       }
     }
     mbar_wait(fin, 0);
@@ -844,12 +872,15 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     issue_s(0);
     issue_dp(0);
     for (int j = 0; j < nkv; ++j) {
+      if (lane == 0) PDS_TR(j, 7);
       if (j + 1 < nkv) {
         mbar_wait(s_free, j & 1);
+        if (lane == 0) PDS_TR(j, 0);
         tc_fence_after();
         issue_s(j + 1);
       }
       mbar_wait(ds_full, j & 1);
+      if (lane == 0) PDS_TR(j, 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sk = ktile(j);
@@ -887,6 +918,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       {
         uint32_t sr[CW / 32][32];
         mbar_wait(s_full, j & 1);
+        if (warp == 4 && lane == 0) PDS_TR(j, 2);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < CW / 32; ++h) tmem_ld32(c_s + 32 * h, sr[h]);
@@ -894,6 +926,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
+        if (warp == 4 && lane == 0) PDS_TR(j, 3);
         const f2 sl2{scale_log2, scale_log2}, nl{nl2, nl2};
 #pragma unroll
         for (int e = 0; e < CW; e += 2) {
@@ -915,7 +948,9 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
             if (CW * wg + e > t) p[e] = 0.f;
         }
       }
+      if (warp == 4 && lane == 0) PDS_TR(j, 4);
       mbar_wait(dp_full, j & 1);
+      if (warp == 4 && lane == 0) PDS_TR(j, 5);
       tc_fence_after();
       uint32_t pk[CW / 2];
 #pragma unroll
@@ -936,6 +971,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (warp == 4 && lane == 0) PDS_TR(j, 6);
     }
     mbar_wait(fin, 0);
     tc_fence_after();
@@ -962,6 +998,16 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
 }
 
 // ------------------------------------------------------------------ host
+int attn_debug_trace(long long* host_out, int rows) {
+#ifdef PDS_TRACE
+  return (int)cudaMemcpyFromSymbol(host_out, g_trace, (size_t)rows * 8 * sizeof(long long));
+#else
+  (void)host_out;
+  (void)rows;
+  return -1;
+#endif
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {

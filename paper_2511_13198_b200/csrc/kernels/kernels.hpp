@@ -4,6 +4,8 @@
 #include <stdint.h>
 
 namespace pds {
+// clock64 timeline of one dQ-kernel CTA (trace builds, -DPDS_TRACE); -1 otherwise
+int attn_debug_trace(long long* host_out, int rows);
 int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
              void* lse, cudaStream_t st);
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
