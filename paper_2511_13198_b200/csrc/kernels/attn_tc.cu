@@ -525,7 +525,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   uint64_t* p_full = bar + 2 * NST + 3;
   uint64_t* ds_full = bar + 2 * NST + 4;
   uint64_t* fin = bar + 2 * NST + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 6);
+  uint64_t* p_half = bar + 2 * NST + 6;   // first half of every warpgroup's P^T columns written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x, head = blockIdx.y;
   const int hq = heads * D;
@@ -546,6 +547,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
     mbar_init(p_full, 4 * NWG);
+    mbar_init(p_half, 4 * NWG);
     mbar_init(ds_full, 4 * NWG);
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -608,14 +610,34 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     issue_dp(0);
     for (int i = 0; i < nq; ++i) {
       if (lane == 0) PDS_TR2(i, 7);
+      // dV += P^T dO in two halves: the k-steps of every warpgroup's first half of
+      // columns as soon as those are written, overlapping the second half's exponentials
+      constexpr int KPW = 8 / NWG;            // k-steps (16 queries) per warpgroup
+      mbar_wait(p_half, i & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t so = otile(i);
+#pragma unroll
+        for (int w = 0; w < NWG; ++w)
+#pragma unroll
+          for (int jj = 0; jj < KPW / 2; ++jj) {
+            const int kk = w * KPW + jj;
+            umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
+          }
+      }
+      __syncwarp();
       mbar_wait(p_full, i & 1);
       if (lane == 0) PDS_TR2(i, 0);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t so = otile(i);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
+        for (int w = 0; w < NWG; ++w)
+#pragma unroll
+          for (int jj = KPW / 2; jj < KPW; ++jj) {
+            const int kk = w * KPW + jj;
+            umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, 1);
+          }
       }
       __syncwarp();
       if (i + 1 < nq) issue_s(i + 1);
@@ -657,42 +679,44 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tmem_ld_wait();
         if (warp == 4 && lane == 0) PDS_TR2(i, 3);
         const f2 sl2{scale_log2, scale_log2}, nlog2e{-LOG2E, -LOG2E};
+        // two halves of CW / 2 columns; the first releases its dV MMAs early (p_half)
 #pragma unroll
-        for (int e = 0; e < CW; e += 4) {
-          const float4 L = lds4(lsm + e * 4);
+        for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
-          for (int u = 0; u < 4; u += 2) {
-            const f2 sv{__uint_as_float(sr[(e + u) / 32][(e + u) % 32]),
-                        __uint_as_float(sr[(e + u + 1) / 32][(e + u + 1) % 32])};
-            const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
-            const f2 x = fma2(sv, sl2, nl);
-            f2 pp;
-            if (emu_pair((e + u) >> 1)) {
-              pp = exp2_fma2(x);                 // share of the pairs on the FMA pipe
-            } else {
-              pp.x = ex2(x.x);
-              pp.y = ex2(x.y);
+          for (int e = hf * CW / 2; e < (hf + 1) * CW / 2; e += 4) {
+            const float4 L = lds4(lsm + e * 4);
+#pragma unroll
+            for (int u = 0; u < 4; u += 2) {
+              const f2 sv{__uint_as_float(sr[(e + u) / 32][(e + u) % 32]),
+                          __uint_as_float(sr[(e + u + 1) / 32][(e + u + 1) % 32])};
+              const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
+              const f2 x = fma2(sv, sl2, nl);
+              f2 pp;
+              if (emu_pair((e + u) >> 1)) {
+                pp = exp2_fma2(x);               // share of the pairs on the FMA pipe
+              } else {
+                pp.x = ex2(x.x);
+                pp.y = ex2(x.y);
+              }
+              p[e + u] = pp.x;
+              p[e + u + 1] = pp.y;
             }
-            p[e + u] = pp.x;
-            p[e + u + 1] = pp.y;
           }
-        }
-        if (diag) {
+          if (diag) {
 #pragma unroll
-          for (int e = 0; e < CW; ++e)
-            if (t > CW * wg + e) p[e] = 0.f;
-        }
+            for (int e = hf * CW / 2; e < (hf + 1) * CW / 2; ++e)
+              if (t > CW * wg + e) p[e] = 0.f;
+          }
+          uint32_t pk[CW / 4];
 #pragma unroll
-        for (int h = 0; h < CW / 64 + (CW < 64); ++h) {   // 32 packed columns per store
-          uint32_t pk[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) pk[e] = (64 * h + 2 * e < CW) ? pack_bf16(p[64 * h + 2 * e], p[64 * h + 2 * e + 1]) : 0u;
-          if (CW >= 64) tmem_st32(c_s + 32 * h, pk);
-          else tmem_st16(c_s, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+          for (int e = 0; e < CW / 4; ++e) pk[e] = pack_bf16(p[hf * CW / 2 + 2 * e], p[hf * CW / 2 + 2 * e + 1]);
+          if (CW == 64) tmem_st16(c_s + hf * CW / 4, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+          else tmem_st8(c_s + hf * CW / 4, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && hf == 0) mbar_arrive(p_half);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
         if (warp == 4 && lane == 0) PDS_TR2(i, 4);
       }
