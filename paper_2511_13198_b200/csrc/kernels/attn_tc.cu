@@ -822,7 +822,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   uint64_t* ds_full = bar + 2 * NST + 3;
   uint64_t* q_ready = bar + 2 * NST + 4;
   uint64_t* fin = bar + 2 * NST + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 6);
+  uint64_t* ds_half = bar + 2 * NST + 6;  // first half of every warpgroup's dS columns written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / 128;
   const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
@@ -842,6 +843,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     mbar_init(s_free, 4 * NWG);
     mbar_init(dp_full, 1);
     mbar_init(ds_full, 4 * NWG);
+    mbar_init(ds_half, 4 * NWG);
     mbar_init(q_ready, 8);
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -903,14 +905,34 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tc_fence_after();
         issue_s(j + 1);
       }
+      // dQ += dS K in two halves: every warpgroup's first half of dS columns is released
+      // while it computes the second
+      constexpr int KPW = 8 / NWG;
+      mbar_wait(ds_half, j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = ktile(j);
+#pragma unroll
+        for (int w = 0; w < NWG; ++w)
+#pragma unroll
+          for (int jj = 0; jj < KPW / 2; ++jj) {
+            const int kk = w * KPW + jj;
+            umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol<NWG>(kk), mnmaj_desc(sk, kk), idesc_q, (j | kk) != 0);
+          }
+      }
+      __syncwarp();
       mbar_wait(ds_full, j & 1);
       if (lane == 0) PDS_TR(j, 1);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sk = ktile(j);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol<NWG>(kk), mnmaj_desc(sk, kk), idesc_q, (j | kk) != 0);
+        for (int w = 0; w < NWG; ++w)
+#pragma unroll
+          for (int jj = KPW / 2; jj < KPW; ++jj) {
+            const int kk = w * KPW + jj;
+            umma_f16_ts(tmem + DQ_COL, tmem + DP_COL + acol<NWG>(kk), mnmaj_desc(sk, kk), idesc_q, 1);
+          }
         umma_commit(&kv_empty[j % NST]);
       }
       __syncwarp();
@@ -976,25 +998,28 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       mbar_wait(dp_full, j & 1);
       if (warp == 4 && lane == 0) PDS_TR(j, 5);
       tc_fence_after();
-      uint32_t pk[CW / 2];
+      // two halves of CW / 2 columns; the first releases its dQ MMAs early (ds_half)
 #pragma unroll
-      for (int h = 0; h < CW / 32; ++h) {
-        uint32_t dv[32];
-        tmem_ld32(c_d + 32 * h, dv);
+      for (int hf = 0; hf < 2; ++hf) {
+        constexpr int HW = CW / 2;
+        uint32_t dv[HW];
+        if (HW == 32) tmem_ld32(c_d + hf * HW, *reinterpret_cast<uint32_t(*)[32]>(&dv[0]));
+        else tmem_ld16(c_d + hf * HW, *reinterpret_cast<uint32_t(*)[16]>(&dv[0]));
         tmem_ld_wait();
+        uint32_t pk[HW / 2];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const f2 d = mul2(f2{p[32 * h + e], p[32 * h + e + 1]},
+        for (int e = 0; e < HW; e += 2) {
+          const f2 d = mul2(f2{p[hf * HW + e], p[hf * HW + e + 1]},
                             sub2(f2{__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])}, f2{dd, dd}));
-          pk[16 * h + e / 2] = pack_bf16(d.x, d.y);
+          pk[e / 2] = pack_bf16(d.x, d.y);
         }
+        if (HW == 32) tmem_st16(c_d + hf * HW / 2, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        else tmem_st8(c_d + hf * HW / 2, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(hf == 0 ? ds_half : ds_full);
       }
-      if (CW == 64) tmem_st32(c_d, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      else tmem_st16(c_d, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
       if (warp == 4 && lane == 0) PDS_TR(j, 6);
     }
     mbar_wait(fin, 0);
