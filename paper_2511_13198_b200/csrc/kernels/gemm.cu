@@ -104,9 +104,20 @@ __device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int&
 // of a warp hold 32 consecutive rows, so each column is one 64-byte segment
 __device__ __forceinline__ void store_col32_bf16(__nv_bfloat16* dst, int64_t ld, int row, int col, const float* v,
                                                  int valid) {
+  __nv_bfloat16* p = dst + (int64_t)col * ld + row;
+  if (valid == 32) {                           // full chunk: no predicates, one pointer walk
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (i < valid) dst[(int64_t)(col + i) * ld + row] = __float2bfloat16_rn(v[i]);
+    for (int i = 0; i < 32; i += 2) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(v[i], v[i + 1]);
+      p[0] = b.x;
+      p[ld] = b.y;
+      p += 2 * ld;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < valid) p[(int64_t)i * ld] = __float2bfloat16_rn(v[i]);
+  }
 }
 
 // store 32 consecutive bf16 values of one row
