@@ -1,16 +1,23 @@
-// Persistent, warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+// Persistent, warp-specialised tcgen05 GEMMs for sm_100a with fused epilogues.
 //
 // The dense contractions of the layer (Eqs. 1, 3, 4 and their
 // gradients) all run here:  C[M,N] = A[M,K] * B[N,K]^T, bf16 operands staged by
-// TMA (SWIZZLE_128B) into a STAGES-deep shared-memory ring, one elected thread
-// issuing tcgen05.mma (M = 128, N = BN, K = 16) into a double-buffered TMEM
-// accumulator, and four epilogue warps draining TMEM with tcgen05.ld while the
-// next tile accumulates.
+// TMA (SWIZZLE_128B) into a shared-memory ring, one elected thread issuing
+// tcgen05.mma into a double-buffered TMEM accumulator, epilogue warps draining
+// TMEM with tcgen05.ld while the next tile accumulates.  Two kernels:
+//
+//   gemm_tc_kernel   1 CTA, M = 128, N = BN (128 / 256) per MMA, 4-6 stages;
+//                    warps 4..7 epilogue (TMEM lanes 32*(warp%4) .. +31, one
+//                    output row per thread)
+//   gemm2_tc_kernel  CTA pair (cluster of 2, cta_group::2): M = 256, N = 256 per
+//                    MMA, each CTA stages half of A and half of B (6 x 32 KB),
+//                    TMA completion on the leader's mbarrier, commits multicast to
+//                    both CTAs; warps 4..11 epilogue, two warpgroups splitting the
+//                    256 accumulator columns
 //
 //   warp 0      TMA producer (one elected lane)
-//   warp 1      MMA issuer   (one elected lane)
+//   warp 1      MMA issuer   (one elected lane; the leader CTA's in the pair kernel)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue (TMEM lanes 32*(warp%4) .. +31, one output row per thread)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
