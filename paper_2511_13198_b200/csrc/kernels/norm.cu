@@ -38,10 +38,11 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Block-per-row layout for the two norm kernels: NT = min(h / 8, 256) threads, each
-// owning VPT = h / (8 NT) 16-byte vectors of the row (8 bf16 columns per vector), so
-// a row is one fully coalesced pass and the only cross-thread step is the row sum
-// (warp shuffle + one shared-memory exchange).
+// Block-per-row layout for the norm kernels: NT threads (min(h/8, 256) for h <= 4096,
+// 512 above), each owning VPT = ceil(h / (8 NT)) 16-byte vectors of the row (8 bf16
+// columns per vector; the last one predicated when NT does not divide h/8), so a row
+// is one fully coalesced pass and the only cross-thread step is the row sum (warp
+// shuffle + one shared-memory exchange).  Any h that is a multiple of 256 up to 16384.
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int nw = blockDim.x >> 5;
@@ -52,22 +53,27 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-template <int VPT>
-__global__ void __launch_bounds__(256)
+template <int VPT, int NT, bool TAIL>
+__global__ void __launch_bounds__(NT)
     rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ res,
                        const __nv_bfloat16* __restrict__ g, int64_t rows, int h, float eps,
                        __nv_bfloat16* __restrict__ x1_out, __nv_bfloat16* __restrict__ u_out,
                        float* __restrict__ rstd_out) {
-  __shared__ float red[8];
+  __shared__ float red[16];
   const int64_t row = blockIdx.x;
+  const int nvec = h >> 3;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * h);
   const uint4* rr = reinterpret_cast<const uint4*>(res + row * h);
   uint4 w[VPT], rw[VPT];
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
-    w[k] = __ldcs(xr + c);
-    if (res) rw[k] = __ldcs(rr + c);
+    w[k] = make_uint4(0, 0, 0, 0);
+    rw[k] = make_uint4(0, 0, 0, 0);
+    if (!TAIL || c < nvec) {
+      w[k] = __ldcs(xr + c);
+      if (res) rw[k] = __ldcs(rr + c);
+    }
   }
   float ss = 0.f;
 #pragma unroll
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(256)
       for (int e = 0; e < 8; ++e) v[e] += r[e];
       w[k] = pack8(v);                         // x1 = bf16(x + res)
       unpack8(w[k], v);
-      reinterpret_cast<uint4*>(x1_out + row * h)[c] = w[k];
+      if (!TAIL || c < nvec) reinterpret_cast<uint4*>(x1_out + row * h)[c] = w[k];
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) ss += v[e] * v[e];
@@ -94,6 +100,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int c = threadIdx.x + k * blockDim.x;
+    if (TAIL && c >= nvec) continue;
     float v[8], gg[8], o[8];
     unpack8(w[k], v);
     unpack8(__ldg(gr + c), gg);
@@ -106,18 +113,20 @@ __global__ void __launch_bounds__(256)
 // dx = r (a - xhat mean(a xhat)) + dres, a = du g, xhat = x r;  dg_part[block][:] =
 // sum over the block's rows of du xhat (each thread keeps its columns' partials in
 // registers across the grid-stride row loop).
-template <int VPT>
-__global__ void __launch_bounds__(256, 3)
+template <int VPT, int NT, bool TAIL>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1)
     rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ du, const __nv_bfloat16* __restrict__ x,
                        const float* __restrict__ rstd, const __nv_bfloat16* __restrict__ g,
                        const __nv_bfloat16* __restrict__ dres, int64_t rows, int h,
                        __nv_bfloat16* __restrict__ dx, float* __restrict__ dg_part) {
-  __shared__ float red[2][8];
+  __shared__ float red[2][16];
+  const int nvec = h >> 3;
   uint4 gw[VPT];
   float dga[VPT][8];
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    gw[k] = __ldg(reinterpret_cast<const uint4*>(g) + threadIdx.x + k * blockDim.x);
+    const int c = threadIdx.x + k * blockDim.x;
+    gw[k] = (!TAIL || c < nvec) ? __ldg(reinterpret_cast<const uint4*>(g) + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int e = 0; e < 8; ++e) dga[k][e] = 0.f;
   }
@@ -128,9 +137,13 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = threadIdx.x + k * blockDim.x;
-      xw[k] = __ldcs(reinterpret_cast<const uint4*>(x + row * h) + c);
-      dw[k] = __ldcs(reinterpret_cast<const uint4*>(du + row * h) + c);
-      if (dres) rw[k] = __ldcs(reinterpret_cast<const uint4*>(dres + row * h) + c);
+      if (!TAIL || c < nvec) {
+        xw[k] = __ldcs(reinterpret_cast<const uint4*>(x + row * h) + c);
+        dw[k] = __ldcs(reinterpret_cast<const uint4*>(du + row * h) + c);
+        if (dres) rw[k] = __ldcs(reinterpret_cast<const uint4*>(dres + row * h) + c);
+      } else {
+        xw[k] = dw[k] = rw[k] = make_uint4(0, 0, 0, 0);
+      }
     }
     float dot = 0.f;
 #pragma unroll
@@ -150,6 +163,7 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = threadIdx.x + k * blockDim.x;
+      if (TAIL && c >= nvec) continue;
       float xh[8], d8[8], dr[8], o[8], gg[8];
       unpack8(xw[k], xh);
       unpack8(dw[k], d8);
@@ -162,7 +176,9 @@ __global__ void __launch_bounds__(256, 3)
   }
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    float4* o = reinterpret_cast<float4*>(dg_part + (int64_t)blockIdx.x * h + 8 * (threadIdx.x + k * blockDim.x));
+    const int c = threadIdx.x + k * blockDim.x;
+    if (TAIL && c >= nvec) continue;
+    float4* o = reinterpret_cast<float4*>(dg_part + (int64_t)blockIdx.x * h + 8 * c);
     o[0] = make_float4(dga[k][0], dga[k][1], dga[k][2], dga[k][3]);
     o[1] = make_float4(dga[k][4], dga[k][5], dga[k][6], dga[k][7]);
   }
@@ -188,19 +204,19 @@ __global__ void __launch_bounds__(256)
 }
 
 // u = x * rstd * g  (recompute of a normalised activation from saved x, rstd)
-template <int VPL>
-__global__ void __launch_bounds__(128)
+template <int VPT, int NT, bool TAIL>
+__global__ void __launch_bounds__(NT)
     apply_norm_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ rstd,
                       const __nv_bfloat16* __restrict__ g, int64_t rows, int h,
                       __nv_bfloat16* __restrict__ u) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const int64_t row = blockIdx.x;
+  const int nvec = h >> 3;
   const float r = rstd[row];
   const uint4* gr = reinterpret_cast<const uint4*>(g);
 #pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = lane + i * 32;
+  for (int k = 0; k < VPT; ++k) {
+    const int c = threadIdx.x + k * blockDim.x;
+    if (TAIL && c >= nvec) continue;
     float v[8], gg[8];
     unpack8(__ldcs(reinterpret_cast<const uint4*>(x + row * h) + c), v);
     unpack8(__ldg(gr + c), gg);
@@ -339,21 +355,28 @@ __global__ void rope_table_kernel(float2* __restrict__ t, int64_t n_pos, int d, 
 }
 
 // ------------------------------------------------------------------ launchers
-#define PDS_UNPACK(...) __VA_ARGS__
-#define PDS_VPL_DISPATCH(h, KERN, LAUNCH, ARGS)                 \
-  switch ((h) / 256) {                                         \
-    case 1: KERN<1><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
-    case 2: KERN<2><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
-    case 4: KERN<4><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
-    case 8: KERN<8><<<PDS_UNPACK LAUNCH>>> ARGS; break;        \
-    case 16: KERN<16><<<PDS_UNPACK LAUNCH>>> ARGS; break;      \
-    default: return (int)cudaErrorInvalidValue;                \
-  }
-
-static bool h_ok(int h) {
-  const int v = h / 256;
-  return h % 256 == 0 && (v == 1 || v == 2 || v == 4 || v == 8 || v == 16);
-}
+// NT x VPT dispatch of the block-per-row kernels (see the layout note above)
+static bool h_ok(int h) { return h % 256 == 0 && h >= 256 && h <= 16384; }
+static int row_threads(int h) { return h <= 4096 ? (h / 8 < 256 ? h / 8 : 256) : 512; }
+#define PDS_ROW_DISPATCH(h, KERN, GRID, SMEM, ST, ...)                                    \
+  do {                                                                                 \
+    const int nt_ = row_threads(h), vpt_ = (h / 8 + nt_ - 1) / nt_;                    \
+    const bool tail_ = vpt_ * nt_ != h / 8;                                            \
+    if (nt_ <= 256 && vpt_ == 1) {                                                     \
+      KERN<1, 256, false><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);                       \
+    } else if (nt_ <= 256) {                                                           \
+      if (tail_) KERN<2, 256, true><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);             \
+      else KERN<2, 256, false><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);                  \
+    } else if (vpt_ == 2) {                                                            \
+      if (tail_) KERN<2, 512, true><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);             \
+      else KERN<2, 512, false><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);                  \
+    } else if (vpt_ == 3) {                                                            \
+      if (tail_) KERN<3, 512, true><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);             \
+      else KERN<3, 512, false><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);                  \
+    } else {                                                                           \
+      KERN<4, 512, true><<<GRID, nt_, SMEM, ST>>>(__VA_ARGS__);                        \
+    }                                                                                  \
+  } while (0)
 
 int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps,
                 void* x1_out, void* u_out, void* rstd, cudaStream_t st) {
@@ -365,11 +388,7 @@ int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int
   auto X1 = reinterpret_cast<__nv_bfloat16*>(x1_out);
   auto U = reinterpret_cast<__nv_bfloat16*>(u_out);
   auto RS = reinterpret_cast<float*>(rstd);
-  const int nt = h / 8 < 256 ? h / 8 : 256;
-  if (h / 8 / nt == 2)
-    rmsnorm_fwd_kernel<2><<<(unsigned)rows, nt, 0, st>>>(X, R, G, rows, h, eps, X1, U, RS);
-  else
-    rmsnorm_fwd_kernel<1><<<(unsigned)rows, nt, 0, st>>>(X, R, G, rows, h, eps, X1, U, RS);
+  PDS_ROW_DISPATCH(h, rmsnorm_fwd_kernel, (unsigned)rows, 0, st, X, R, G, rows, h, eps, X1, U, RS);
   return (int)cudaGetLastError();
 }
 
@@ -390,11 +409,9 @@ int rmsnorm_bwd(const void* du, const void* x, const void* rstd, const void* g, 
   auto G = reinterpret_cast<const __nv_bfloat16*>(g);
   auto DR = reinterpret_cast<const __nv_bfloat16*>(dres);
   auto DX = reinterpret_cast<__nv_bfloat16*>(dx);
-  const int nt = h / 8 < 256 ? h / 8 : 256;
-  if (h / 8 / nt == 2)
-    rmsnorm_bwd_kernel<2><<<grid, nt, 0, st>>>(DU, X, RS, G, DR, rows, h, DX, dg_part);
-  else
-    rmsnorm_bwd_kernel<1><<<grid, nt, 0, st>>>(DU, X, RS, G, DR, rows, h, DX, dg_part);
+  PDS_ROW_DISPATCH(h, rmsnorm_bwd_kernel, grid, 0, st, DU, X, RS, G, DR, rows, h, DX, dg_part);
+  int rc = (int)cudaGetLastError();
+  if (rc) return rc;
   reduce_rows_add_kernel<<<(h + 31) / 32, 256, 0, st>>>(dg_part, grid, h, dg);
   return (int)cudaGetLastError();
 }
@@ -403,12 +420,11 @@ int apply_norm(const void* x, const void* rstd, const void* g, int64_t rows, int
                cudaStream_t st) {
   if (!h_ok(h)) return (int)cudaErrorInvalidValue;
   if (rows <= 0) return 0;
-  const unsigned grid = (unsigned)((rows + 3) / 4);
   auto X = reinterpret_cast<const __nv_bfloat16*>(x);
   auto RS = reinterpret_cast<const float*>(rstd);
   auto G = reinterpret_cast<const __nv_bfloat16*>(g);
   auto U = reinterpret_cast<__nv_bfloat16*>(u);
-  PDS_VPL_DISPATCH(h, apply_norm_kernel, (grid, 128, 0, st), (X, RS, G, rows, h, U));
+  PDS_ROW_DISPATCH(h, apply_norm_kernel, (unsigned)rows, 0, st, X, RS, G, rows, h, U);
   return (int)cudaGetLastError();
 }
 

@@ -119,8 +119,10 @@ def test_rope_table_and_gemm_rope(d):
     assert rel(host(c), exp) < 1e-2
 
 
-@pytest.mark.parametrize("h", [256, 4096])
+@pytest.mark.parametrize("h", [256, 768, 2304, 4096, 8192, 12288])
 def test_rmsnorm_fwd_bwd(h):
+    # every block-per-row shape: 1 / 2 vectors per thread at <= 4096 (2304: predicated
+    # tail), 512 threads with 2 / 3 vectors above (Table 4's LLaMA h = 8192, GPT 12288)
     rows = 300
     x = _mat(4, 1, (rows, h))
     r = _mat(4, 2, (rows, h))

@@ -95,15 +95,17 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
     return outs
 
 
-def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0):
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True):
     d = layer_inputs(h, n, F, s, 1, seed=seed)
-    y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
-    g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
+    y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
+                            causal=causal)
+    g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
+                         causal=causal)
     W = OS.shard_weights(d, n, P)
     xs = OS.shard_act(d["x"], P)
     dys = OS.shard_act(d["dy"], P)
     ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
-    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks)
+    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0)
     outs = run_ranks(model, P, [pi], [ranks], xs, dys)
     y = np.concatenate([o[0] for o in outs])[:, None, :]
     dx = np.concatenate([o[1] for o in outs])[:, None, :]
@@ -142,6 +144,12 @@ def test_layer_p2_c1(pi):
 def test_layer_p4_d128(pi):
     # d = 128 heads, P = 4, METP c = 2 waves of 128 rows per rank
     _check_layer(pi, 4, 1024, 8, 4096, 1024, chunks=2)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2])
+def test_layer_bert_shape_noncausal(pi):
+    # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
+    _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
 
 
 def test_switched_chain_p2():
