@@ -194,6 +194,14 @@ pds_status pds_layer_step_host(pds_ctx* ctx, uint8_t strategy, int64_t seq_len, 
 pds_status pds_host_drain(pds_ctx* ctx, void* stream);
 /* Release a saved set without running backward. */
 pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
+/* Tile-level overlap of the MegatronTS collectives (P > 1): every
+ * all-gather feeding a column-parallel GEMM (QKV, FC1; bwd dGELU, dA) runs chunk by
+ * chunk on a side stream while the GEMM polls per tile for the chunks it needs, and
+ * every reduce-scatter after a row-parallel GEMM (proj, FC2; bwd dV, dU) sends each
+ * chunk as soon as the GEMM has stored it ("communication overlapped with GEMM tiles",
+ * north_star; the AG / RS of PAPER.md:203).  on = 1 (default) or 0 (plain in-order
+ * collectives).  Results are bit-identical either way.  Ignored at P = 1. */
+pds_status pds_set_overlap(pds_ctx* ctx, int32_t on);
 /* Debug taps: the next pds_layer_fwd also writes the sublayer deltas O (attention
  * block output) and Z (FFN output), local [s/P, b, h] bf16 (reading R-34).  NULL
  * pointers disable. */

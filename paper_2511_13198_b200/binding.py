@@ -115,6 +115,7 @@ _SIGS = {
     "pds_debug_trace": [C.c_void_p, C.c_int32],
     "pds_saved_release": [C.c_void_p, C.c_void_p],
     "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_set_overlap": [C.c_void_p, C.c_int32],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
     "pds_profile_read": [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                          C.POINTER(C.c_double), C.POINTER(C.c_double)],
@@ -274,6 +275,9 @@ class Context:
 
     def saved_release(self, saved):
         call("pds_saved_release", self.h, saved)
+
+    def set_overlap(self, on):
+        call("pds_set_overlap", self.h, 1 if on else 0)
 
     def debug_taps(self, o=None, z=None):
         call("pds_debug_taps", self.h, o, z)

@@ -1,7 +1,9 @@
 #include "comm.hpp"
 
+#include <cuda.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -14,6 +16,37 @@ int sum_bf16_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_
 int sum_f32_p(const void* const* srcs, int P, void* dst, int64_t n, cudaStream_t st);
 
 int64_t dt_size(DType dt) { return dt == DT_BF16 ? 2 : 4; }
+
+// ------------------------------------------------------------------ stream memops
+namespace {
+typedef CUresult (*PfnWrite32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PfnWait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+}  // namespace
+
+pds_status stream_write32(cudaStream_t st, uint32_t* addr, uint32_t v) {
+  static PfnWrite32 fn = driver_fn<PfnWrite32>("cuStreamWriteValue32");
+  if (!fn) PDS_FAIL(PDS_ECUDA, "cuStreamWriteValue32 unavailable");
+  // default flags: the write is ordered after (and fenced behind) the stream's prior work
+  if (fn((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    PDS_FAIL(PDS_ECUDA, "cuStreamWriteValue32 failed");
+  return PDS_OK;
+}
+
+pds_status stream_wait32_geq(cudaStream_t st, const uint32_t* addr, uint32_t v) {
+  static PfnWait32 fn = driver_fn<PfnWait32>("cuStreamWaitValue32");
+  if (!fn) PDS_FAIL(PDS_ECUDA, "cuStreamWaitValue32 unavailable");
+  if (fn((CUstream)st, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    PDS_FAIL(PDS_ECUDA, "cuStreamWaitValue32 failed");
+  return PDS_OK;
+}
 
 // ------------------------------------------------------------------ P = 1
 struct SelfComm : Comm {
@@ -44,6 +77,15 @@ Comm* make_self_comm() { return new SelfComm(); }
 
 static ncclDataType_t nt(DType dt) { return dt == DT_BF16 ? ncclBfloat16 : ncclFloat32; }
 
+static int side_ctas() {
+  static int v = [] {
+    const char* e = getenv("PDS_OVERLAP_CTAS");
+    const int n = e ? atoi(e) : 8;
+    return n < 2 ? 2 : (n > 32 ? 32 : n & ~1);
+  }();
+  return v;
+}
+
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
   NcclComm* side_ = nullptr;
@@ -53,8 +95,12 @@ struct NcclComm : Comm {
   }
   Comm* side(pds_status* st) override {
     if (!side_) {
+      // the side communicator runs beside persistent GEMMs: cap its CTAs, and the
+      // GEMMs that poll for it leave that many SMs free (overlap_sm_reserve)
       ncclComm_t c2 = nullptr;
-      ncclResult_t r = ncclCommSplit(comm, 0, rank, &c2, nullptr);
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.maxCTAs = side_ctas();
+      ncclResult_t r = ncclCommSplit(comm, 0, rank, &c2, &cfg);
       if (r != ncclSuccess) {
         set_error(std::string("ncclCommSplit: ") + ncclGetErrorString(r));
         *st = PDS_ENCCL;
@@ -64,6 +110,7 @@ struct NcclComm : Comm {
       side_->P = P;
       side_->rank = rank;
       side_->comm = c2;
+      side_->max_ctas = cfg.maxCTAs;
     }
     return side_;
   }
@@ -79,6 +126,38 @@ struct NcclComm : Comm {
     PDS_NCCL(ncclAllReduce(buf, buf, (size_t)count, nt(dt), ncclSum, comm, st));
     return PDS_OK;
   }
+  // P - 1 pairwise steps on the (CTA-limited) side communicator; step k exchanges with
+  // ranks rank +- k, so every GPU sends and receives one chunk per step over NVSwitch
+  pds_status all_gather_flagged(void* recv, int64_t count, DType dt, cudaStream_t, cudaStream_t st,
+                                uint32_t* flags, uint32_t epoch) override {
+    const int64_t b = count * dt_size(dt);
+    char* base = static_cast<char*>(recv);
+    PDS_TRY(stream_write32(st, flags + rank, epoch));     // own chunk: in place already
+    for (int k = 1; k < P; ++k) {
+      const int from = (rank + k) % P, to = (rank - k + P) % P;
+      PDS_NCCL(ncclGroupStart());
+      PDS_NCCL(ncclSend(base + rank * b, (size_t)count, nt(dt), to, comm, st));
+      PDS_NCCL(ncclRecv(base + from * b, (size_t)count, nt(dt), from, comm, st));
+      PDS_NCCL(ncclGroupEnd());
+      PDS_TRY(stream_write32(st, flags + from, epoch));
+    }
+    return PDS_OK;
+  }
+  pds_status reduce_scatter_gated(const void* send, void* recv, int64_t count, DType dt, cudaStream_t,
+                                  cudaStream_t st, const uint32_t* ctr, uint32_t target) override {
+    const int64_t b = count * dt_size(dt);
+    for (int k = 1; k < P; ++k) {
+      const int to = (rank + k) % P, from = (rank - k + P) % P;
+      PDS_TRY(stream_wait32_geq(st, ctr + to, target));
+      PDS_NCCL(ncclGroupStart());
+      PDS_NCCL(ncclSend(static_cast<const char*>(send) + to * b, (size_t)count, nt(dt), to, comm, st));
+      PDS_NCCL(ncclRecv(static_cast<char*>(recv) + from * b, (size_t)count, nt(dt), from, comm, st));
+      PDS_NCCL(ncclGroupEnd());
+    }
+    return PDS_OK;
+  }
+  int overlap_sm_reserve() const override { return max_ctas; }
+  int max_ctas = 0;
   pds_status all_to_all(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     const int64_t b = count * dt_size(dt);
     PDS_NCCL(ncclGroupStart());
@@ -126,6 +205,7 @@ struct LoopComm : Comm {
   void* scratch = nullptr;
   int64_t scratch_bytes = 0;
   ~LoopComm() override {
+    if (ag_done) cudaEventDestroy(ag_done);
     if (scratch) cudaFree(scratch);
   }
   pds_status ensure(int64_t bytes, cudaStream_t st) {
@@ -192,6 +272,43 @@ struct LoopComm : Comm {
     if (rc) PDS_FAIL(PDS_ECUDA, "loopback all_reduce");
     finish(st);
     PDS_CUDA(cudaMemcpyAsync(buf, tmp, b, cudaMemcpyDeviceToDevice, st));
+    return PDS_OK;
+  }
+  // One GPU hosts every virtual rank, so a persistent GEMM polling for chunks could hold
+  // the SMs that a peer's producer kernel (or a copy) needs: here the compute stream
+  // waits for the whole gather before the GEMM starts, which still runs the GEMM's
+  // flag protocol (epochs, chunk order) but never makes it spin on SM-bound work.
+  cudaEvent_t ag_done = nullptr;
+  pds_status all_gather_flagged(void* recv, int64_t count, DType dt, cudaStream_t main, cudaStream_t st,
+                                uint32_t* flags, uint32_t epoch) override {
+    const int64_t b = count * dt_size(dt);
+    char* base = static_cast<char*>(recv);
+    if (!ag_done) PDS_CUDA(cudaEventCreateWithFlags(&ag_done, cudaEventDisableTiming));
+    publish(base + rank * b, st);
+    PDS_TRY(stream_write32(st, flags + rank, epoch));     // own chunk: in place already
+    for (int k = 1; k < P; ++k) {
+      const int j = (rank + k) % P;
+      PDS_CUDA(cudaStreamWaitEvent(st, g->ready[j], 0));
+      PDS_CUDA(cudaMemcpyAsync(base + j * b, g->ptr[j], b, cudaMemcpyDeviceToDevice, st));
+      PDS_TRY(stream_write32(st, flags + j, epoch));
+    }
+    finish(st);
+    PDS_CUDA(cudaEventRecord(ag_done, st));
+    PDS_CUDA(cudaStreamWaitEvent(main, ag_done, 0));
+    return PDS_OK;
+  }
+  pds_status reduce_scatter_gated(const void* send, void* recv, int64_t count, DType dt, cudaStream_t,
+                                  cudaStream_t st, const uint32_t* ctr, uint32_t target) override {
+    const int64_t b = count * dt_size(dt);
+    publish(recv, st);                          // this rank's receive buffer is free
+    for (int k = 1; k < P; ++k) {
+      const int j = (rank + k) % P;
+      PDS_TRY(stream_wait32_geq(st, ctr + j, target));
+      PDS_CUDA(cudaStreamWaitEvent(st, g->ready[j], 0));
+      PDS_CUDA(cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(g->ptr[j])) + rank * b,
+                               static_cast<const char*>(send) + j * b, b, cudaMemcpyDeviceToDevice, st));
+    }
+    finish(st);                                 // every peer's copy into recv is done
     return PDS_OK;
   }
   pds_status all_to_all(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {

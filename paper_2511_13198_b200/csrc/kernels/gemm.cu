@@ -64,7 +64,45 @@ struct EpiParams {
   __nv_bfloat16* c_t;      // transposed copies (dGELU epilogue): [N][ld_t]
   __nv_bfloat16* aux_t;
   int64_t ld_t;
+  // collective overlap (gemm.cuh): chunk flags / counters, tile rotation in M blocks
+  const uint32_t* wait_flags;
+  uint32_t flag_epoch;
+  uint32_t* done_ctr;
+  int chunk_rows;
+  int rot_mb;
 };
+
+// AG -> GEMM: wait until every chunk overlapping rows [r0, r0 + n) has landed.  The
+// flag is written by the collective's stream (after its copy) with release semantics;
+// the acquire load plus a generic -> async proxy fence make the landed rows visible to
+// the TMA loads that follow.  A chunk that never lands is a bug: trap after ~8 s
+// instead of hanging the device.
+__device__ __forceinline__ void wait_chunks(const EpiParams& ep, int r0, int n) {
+  if (!ep.wait_flags || n <= 0) return;
+  const int c0 = r0 / ep.chunk_rows, c1 = (r0 + n - 1) / ep.chunk_rows;
+  for (int c = c0; c <= c1; ++c) {
+    uint32_t spins = 0;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ep.wait_flags + c) : "memory");
+      if ((int32_t)(v - ep.flag_epoch) >= 0) break;
+      __nanosleep(128);
+      if (++spins > (1u << 26)) __trap();
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// GEMM -> RS: one epilogue warp has stored its 32 rows x `ncols` columns; count them
+// into the chunk's counter once every lane's stores are ordered before the add.
+__device__ __forceinline__ void count_stored(const EpiParams& ep, int warp_row0, bool row_ok, int ncols) {
+  if (!ep.done_ctr) return;
+  const unsigned vm = __ballot_sync(0xffffffffu, row_ok);
+  __threadfence();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0 && vm && ncols > 0)
+    atomicAdd(ep.done_ctr + warp_row0 / ep.chunk_rows, (uint32_t)(__popc(vm) * ncols));
+}
 
 struct RowMap {
   int64_t seg, stride, base;
@@ -96,6 +134,10 @@ __device__ __forceinline__ float gelu_f(float x) {
 }
 __device__ __forceinline__ float bf16_round(float x) {
   return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ int rot_block(int mb, int mt, int rot) {
+  return rot ? (mb + rot) % mt : mb;
 }
 
 __device__ __forceinline__ void tile_coords(int t, int mt, int nt, int& mb, int& nb, int group_m = GROUP_M) {
@@ -317,7 +359,9 @@ __global__ void __launch_bounds__(256, 1)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         int mb, nb;
         tile_coords(t, mt, nt, mb, nb);
+        mb = rot_block(mb, mt, ep.rot_mb);
         const int m0 = mb * BM, n0 = nb * BN;
+        wait_chunks(ep, m0, min(BM, M - m0));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
@@ -383,6 +427,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, mt, nt, mb, nb);
+      mb = rot_block(mb, mt, ep.rot_mb);
       const int m0 = mb * BM, n0 = nb * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -390,6 +435,7 @@ __global__ void __launch_bounds__(256, 1)
       const bool row_ok = row < M;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       epilogue_tile<BN>(ep, tbase, row, row_ok, n0, N);
+      count_stored(ep, m0 + q * 32, row_ok, min(BN, N - n0));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -460,7 +506,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int t = cid; t < ntiles; t += ncl) {
         int mb, nb;
         tile_coords(t, mt, nt, mb, nb, group_m);
+        mb = rot_block(mb, mt, ep.rot_mb);
         const int m0 = mb * 256 + rank * 128, n0 = nb * 256 + rank * 128;
+        wait_chunks(ep, m0, min(128, M - m0));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE;
@@ -527,11 +575,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     for (int t = cid; t < ntiles; t += ncl) {
       int mb, nb;
       tile_coords(t, mt, nt, mb, nb, group_m);
+      mb = rot_block(mb, mt, ep.rot_mb);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + rank * 128 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + half * 128;
       epilogue_tile<128>(ep, tbase, row, row < M, nb * 256 + half * 128, N);
+      count_stored(ep, row - lane, row < M, min(128, N - (nb * 256 + half * 128)));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_u32(&tempty_bar[acc], 0));
@@ -617,7 +667,8 @@ static int launch_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
     attr_set = true;
   }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  const int grid = tiles < gemm_num_sms() ? tiles : gemm_num_sms();
+  const int sms = gemm_num_sms() - g.sm_reserve;
+  const int grid = tiles < sms ? tiles : sms;
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
   kern<<<grid, 256, Cfg::SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep);
@@ -644,7 +695,7 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
     attr_set = true;
   }
   const int tiles = ((g.M + 255) / 256) * ((g.N + 255) / 256);
-  const int ncl = std::min(tiles, gemm_num_sms() / 2);
+  const int ncl = std::min(tiles, (gemm_num_sms() - g.sm_reserve) / 2);
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
   static const int env_gm = [] { const char* e = getenv("PDS_GEMM_GM"); return e ? atoi(e) : 0; }();
@@ -678,6 +729,14 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;
   ep.c_seg = g.c_seg > 0 ? g.c_seg : (int64_t)1 << 40;
   ep.c_stride = g.c_stride; ep.c_base = g.c_base;
+  ep.wait_flags = g.wait_flags; ep.flag_epoch = g.flag_epoch;
+  ep.done_ctr = g.done_ctr; ep.chunk_rows = (int)g.chunk_rows; ep.rot_mb = 0;
+  if (g.wait_flags || g.done_ctr) {
+    if (g.chunk_rows <= 0 || g.chunk_rows % 32 || g.M % g.chunk_rows) return (int)cudaErrorInvalidValue;
+    if (g.wait_flags && (g.a_mn || g.a_seg)) return (int)cudaErrorInvalidValue;
+    if (g.done_ctr && (g.c_seg || g.blk_w)) return (int)cudaErrorInvalidValue;
+  }
+  if (g.sm_reserve < 0 || g.sm_reserve > gemm_num_sms() - 2) return (int)cudaErrorInvalidValue;
   // a tile must not straddle a remap segment
   if (g.a_seg > 0 && g.a_seg % (g.a_mn ? 64 : BM)) return (int)cudaErrorInvalidValue;
   if (g.b_seg > 0 && g.b_seg % (g.b_mn ? 64 : 256)) return (int)cudaErrorInvalidValue;
@@ -690,6 +749,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
                        pair_tiles >= gemm_num_sms() / 2 && (g.a_seg == 0 || g.a_seg % 128 == 0) &&
                        (!g.a_mn || g.M % 64 == 0) && (!g.b_mn || g.N % 64 == 0) &&
                        (g.b_seg == 0 || g.b_seg % 128 == 0);
+  if (g.m_rot_rows) ep.rot_mb = (int)(g.m_rot_rows / (pair_ok ? 256 : BM));
   if (pair_ok) {
     switch ((g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0)) {
       case 0: return launch2_t<0, 0>(g, ep, st);

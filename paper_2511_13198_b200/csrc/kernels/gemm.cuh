@@ -59,6 +59,23 @@ struct GemmArgs {
   void* c_t = nullptr;
   void* aux_t = nullptr;
   int64_t ld_t = 0;
+  // Tile-level overlap with a collective (MegatronTS over P ranks).  The
+  // M rows split into chunks of chunk_rows, one per rank.
+  //   wait_flags  AG -> GEMM: before a CTA loads A rows of chunk c it waits until
+  //               (int32)(wait_flags[c] - flag_epoch) >= 0, i.e. the all-gather has
+  //               landed chunk c (K-major A, no A remap).  Bounded spin, then trap.
+  //   done_ctr    GEMM -> RS: after an epilogue warp has stored its rows of chunk c it
+  //               adds the number of elements stored to done_ctr[c] (release), so the
+  //               chunk is complete once the counter has grown by chunk_rows * N.
+  //   m_rot_rows  tiles are issued starting at this row, wrapping over M, so the chunk
+  //               that is local (AG) or sent first (RS) is computed first.
+  //   sm_reserve  SMs left free for the collective's kernels during this GEMM.
+  const uint32_t* wait_flags = nullptr;
+  uint32_t flag_epoch = 0;
+  uint32_t* done_ctr = nullptr;
+  int64_t chunk_rows = 0;
+  int64_t m_rot_rows = 0;
+  int sm_reserve = 0;
 };
 
 // returns 0 on success, a cudaError_t value otherwise

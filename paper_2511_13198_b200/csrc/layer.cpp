@@ -81,8 +81,14 @@ struct pds_ctx {
   bool stage_used[2] = {false, false};
   cudaStream_t up_st = nullptr, down_st = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_y = nullptr, ev_dx = nullptr;
-  // side stream for collectives overlapped with compute (METP wave prefetch)
+  // side stream for collectives overlapped with compute (METP wave prefetch, TS tiles)
   cudaStream_t comm_st = nullptr;
+  // tile-overlapped MegatronTS collectives (P > 1): device words [0, 8) = chunk-landed
+  // flags of the all-gathers, [8, 16) = per-chunk store counters of the GEMMs feeding a
+  // reduce-scatter; host-side epoch / running target
+  uint32_t* sync = nullptr;
+  uint32_t ag_epoch = 0, rs_count = 0;
+  int overlap = 1;
   std::vector<cudaEvent_t> sync_pool;
   // profiling
   bool prof = false;
@@ -103,6 +109,7 @@ struct pds_ctx {
     if (up_st) cudaStreamDestroy(up_st);
     if (down_st) cudaStreamDestroy(down_st);
     if (comm_st) cudaStreamDestroy(comm_st);
+    if (sync) cudaFree(sync);
     for (auto e : sync_pool) cudaEventDestroy(e);
     delete comm;
   }
@@ -159,14 +166,101 @@ struct Exec {
       : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), s(s_), sl(s_ / c_->P), h(c_->m.h), F(c_->m.ffn),
         nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
 
+  // overlap settings armed for the next gemm() (ag_next / rs_arm)
+  GemmArgs nxt;
+  bool has_nxt = false;
+  cudaEvent_t nxt_join = nullptr;
+
   pds_status gemm(GemmArgs g) {
     // algorithmic bytes: A and B once, C by epilogue (fp32 += reads and writes; GELU /
     // dGELU add the bf16 aux streams)
     const double mn = (double)g.M * g.N;
     const double cb = g.epi == EPI_F32_ACC ? 8.0 : g.epi == EPI_F32 ? 4.0 : g.epi == EPI_GELU ? 4.0
                     : g.epi == EPI_DGELU ? 6.0 : 2.0;
-    Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M + g.N) * g.K + cb * mn);
-    return kerr(gemm_launch(g, st), "gemm");
+    if (has_nxt) {
+      g.wait_flags = nxt.wait_flags; g.flag_epoch = nxt.flag_epoch; g.done_ctr = nxt.done_ctr;
+      g.chunk_rows = nxt.chunk_rows; g.m_rot_rows = nxt.m_rot_rows; g.sm_reserve = nxt.sm_reserve;
+      has_nxt = false;
+      nxt = GemmArgs();
+    }
+    {
+      Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M + g.N) * g.K + cb * mn);
+      PDS_TRY(kerr(gemm_launch(g, st), "gemm"));
+    }
+    if (nxt_join) {                      // the all-gather this GEMM consumed, joined
+      cudaEvent_t ev = nxt_join;
+      nxt_join = nullptr;
+      PDS_TRY(wait(st, ev));
+    }
+    return PDS_OK;
+  }
+
+  // ---- tile-overlapped MegatronTS collectives ----
+  bool overlap() const { return P > 1 && c->overlap && !c->comm->trivial(); }
+  pds_status sync_init() {
+    if (c->sync) return PDS_OK;
+    PDS_CUDA(cudaMalloc(&c->sync, 16 * sizeof(uint32_t)));
+    PDS_CUDA(cudaMemsetAsync(c->sync, 0, 16 * sizeof(uint32_t), st));
+    return PDS_OK;
+  }
+  // AG of buf [P][count] (this rank's chunk already at slot r) on the side stream, chunk
+  // by chunk, consumed tile by tile by the next gemm(), whose A operand is buf
+  pds_status ag_next(void* buf, int64_t count) {
+    PDS_TRY(sync_init());
+    cudaStream_t cs = comm_stream();
+    PDS_TRY(link(st, cs));
+    pds_status rc = PDS_OK;
+    Comm* cm = c->comm->side(&rc);
+    if (!cm) return rc;
+    const uint32_t epoch = ++c->ag_epoch;
+    {
+      Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
+      PDS_TRY(cm->all_gather_flagged(buf, count, DT_BF16, st, cs, c->sync, epoch));
+    }
+    nxt = GemmArgs();
+    nxt.wait_flags = c->sync; nxt.flag_epoch = epoch;
+    nxt.chunk_rows = sl; nxt.m_rot_rows = (int64_t)r * sl;
+    nxt.sm_reserve = cm->overlap_sm_reserve();
+    has_nxt = true;
+    nxt_join = mark(cs);
+    return PDS_OK;
+  }
+  // arm the next gemm() (output [P][sl][ncols], all rows) to count its stores per chunk,
+  // computing the chunk sent first (r+1) first and its own chunk last
+  uint32_t rs_target = 0;
+  pds_status rs_arm(int64_t ncols) {
+    PDS_TRY(sync_init());
+    PDS_TRY(link(st, comm_stream()));        // the receive buffer's readers are done
+    pds_status rc = PDS_OK;
+    Comm* cm = c->comm->side(&rc);
+    if (!cm) return rc;
+    c->rs_count += (uint32_t)(sl * ncols);
+    rs_target = c->rs_count;
+    nxt = GemmArgs();
+    nxt.done_ctr = c->sync + 8;
+    nxt.chunk_rows = sl; nxt.m_rot_rows = (int64_t)((r + 1) % P) * sl;
+    nxt.sm_reserve = cm->overlap_sm_reserve();
+    has_nxt = true;
+    return PDS_OK;
+  }
+  // after the armed gemm(): send each finished chunk of `partial` to its owner, receive
+  // the peers' partials of this rank's chunk into recv [P][count], and sum them (rank
+  // order, fp32) into partial + r*count: the reduce-scatter, overlapped with the GEMM
+  pds_status rs_run(char* partial, char* recv, int64_t count) {
+    cudaStream_t cs = comm_stream();
+    pds_status rc = PDS_OK;
+    Comm* cm = c->comm->side(&rc);
+    if (!cm) return rc;
+    {
+      Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
+      PDS_TRY(cm->reduce_scatter_gated(partial, recv, count, DT_BF16, st, cs, c->sync + 8, rs_target));
+    }
+    PDS_TRY(link(cs, st));
+    const int64_t b = count * 2;
+    const void* srcs[8];
+    for (int j = 0; j < P; ++j) srcs[j] = j == r ? partial + j * b : recv + j * b;
+    Prof p(c, st, K_NORM, 0, (double)count * 2 * (P + 1));
+    return kerr(sum_bf16_p(srcs, P, partial + r * b, count, st), "sum_bf16_p");
   }
   // C[M,N] = A * B^T helpers
   static GemmArgs G(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int64_t M,
@@ -330,21 +424,29 @@ pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   char* f0 = ws + bp.ws_off("f0");
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   const int64_t slot = e.r * e.sl * e.h * 2;
+  // P > 1: every AG runs chunk by chunk on the side stream while the GEMM that reads it
+  // computes the chunks already there (ag_next), and every RS sends each chunk of the
+  // GEMM's output as soon as its tiles are stored (rs_arm / rs_run), the gather buffer
+  // (free by then) receiving the peers' partials
+  const bool ov = e.overlap();
+  const int64_t n = e.sl * e.h;
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, gather + slot, sv->at("rstd1")));
-  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(u)
+  PDS_TRY(ov ? e.ag_next(gather, n) : e.ag(gather + slot, gather, n));                // AG(u)
   PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
                         e.hl, 0, 0, 0)));                                                // Eq. 1 + RoPE
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));                          // Eq. 2
+  if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(sv->at("a"), e.hl, w->w_proj, e.h, e.s, e.h, e.hl, partial, e.h));      // Eq. 3
-  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(o)
+  PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(o)
   PDS_TRY(e.tap(e.c->tap_o, partial + slot, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, partial + slot, w->g2, e.sl, sv->at("x1"), gather + slot, sv->at("rstd2")));
-  PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                   // AG(v)
+  PDS_TRY(ov ? e.ag_next(gather, n) : e.ag(gather + slot, gather, n));                // AG(v)
   GemmArgs fc1 = Exec::G(gather, e.h, 0, w->w_in_t, e.h, 0, e.s, e.Fl, e.h, sv->at("h"), e.Fl, EPI_GELU);
   fc1.aux_out = f0; fc1.ld_aux = e.Fl;
   PDS_TRY(e.gemm(fc1));                                                                 // Eq. 4 (GELU)
+  if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(f0, e.Fl, w->w_out, e.h, e.s, e.h, e.Fl, partial, e.h));
-  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(z)
+  PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(z)
   PDS_TRY(e.tap(e.c->tap_z, partial + slot, e.sl * e.h));
   return e.add(sv->at("x1"), partial + slot, y, e.sl * e.h);
 }
@@ -369,13 +471,21 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   char* g2 = pre ? ws + bp.ws_off("gather2") : gather;
   const cudaStream_t cs = pre ? e.side_stream() : e.st;
   cudaEvent_t ev_v = nullptr, ev_u = nullptr;
+  // tile-overlapped AG / RS as in the forward (P > 1); the side stream carries the
+  // flagged gathers first, then the re-gathers
+  const bool ov = e.overlap();
+  const int64_t n = e.sl * e.h;
+  if (ov) {
+    PDS_CUDA(cudaMemcpyAsync(gather + slot, dy, n * 2, cudaMemcpyDeviceToDevice, e.st));
+    PDS_TRY(e.ag_next(gather, n));                                                    // AG(dz)
+  }
   if (pre) {
     PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, g2 + slot));
     PDS_TRY(e.link(e.st, cs));
     PDS_TRY(e.ag_on(cs, g2 + slot, g2, e.sl * e.h));                                  // AG(v) re-gather
     ev_v = e.mark(cs);
   }
-  PDS_TRY(e.ag(dy, gather, e.sl * e.h));                                                // AG(dz)
+  if (!ov) PDS_TRY(e.ag(dy, gather, n));                                                // AG(dz)
   // dH (row-major, for dV) plus the two operands the dW GEMMs need K-major, straight
   // from the epilogue: dH^T into f0, G^T into ta (G itself is never stored)
   GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
@@ -398,10 +508,16 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     PDS_TRY(e.ag_on(cs, g2 + slot, g2, e.sl * e.h));                                  // AG(u) re-gather
     ev_u = e.mark(cs);
   }
+  if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(f1, e.Fl, w->w_in_t, e.h, e.s, e.h, e.Fl, partial, e.h));               // dV = dH W_in^T
-  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(dv)
+  PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(dv)
   PDS_TRY(e.norm_bwd(partial + slot, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
-  PDS_TRY(e.ag(dx, gather, e.sl * e.h));                                                // AG(dx1)
+  if (ov) {
+    PDS_CUDA(cudaMemcpyAsync(gather + slot, dx, n * 2, cudaMemcpyDeviceToDevice, e.st));
+    PDS_TRY(e.ag_next(gather, n));                                                    // AG(dx1)
+  } else {
+    PDS_TRY(e.ag(dx, gather, n));                                                       // AG(dx1)
+  }
   PDS_TRY(tn.mm(gather, e.h, w->w_proj, e.h, e.s, e.hl, e.h, f1, e.hl));                 // dA
   PDS_TRY(tn.dw(sv->at("a"), e.hl, gather, e.h, e.s, e.hl, e.h, g->dw_proj));            // dW_proj += A^T dX1
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), f1, f0, dd));            // dQKV (RoPE^T)
@@ -412,8 +528,9 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(u) re-gather
   }
   PDS_TRY(tn.dw(f0, 3 * e.hl, g2, e.h, e.s, 3 * e.hl, e.h, g->dw_qkv_t));               // dW_qkv^T += dQKV^T U
+  if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(f0, 3 * e.hl, w->w_qkv_t, e.h, e.s, e.h, 3 * e.hl, partial, e.h));      // dU = dQKV W_qkv^T
-  PDS_TRY(e.rs(partial, partial + slot, e.sl * e.h));                                   // RS(du)
+  PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(du)
   PDS_TRY(e.norm_bwd(partial + slot, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -840,6 +957,12 @@ extern "C" pds_status pds_release_cache(pds_ctx* c) {
   c->stage = nullptr;
   c->stage_cap = 0;
   c->stage_used[0] = c->stage_used[1] = false;
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_set_overlap(pds_ctx* c, int32_t on) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "pds_set_overlap: null ctx");
+  c->overlap = on ? 1 : 0;
   return PDS_OK;
 }
 

@@ -47,8 +47,9 @@ class Rank:
         return B.Grads(*(self.g[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
 
 
-def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True):
-    """Run an L-layer stack (plan pi_list) on P loopback ranks; returns per-rank outputs."""
+def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True, overlap=None):
+    """Run an L-layer stack (plan pi_list) on P loopback ranks; returns per-rank outputs.
+    overlap: None = library default, else pds_set_overlap(ctx, overlap)."""
     grp = B.Group(P)
     errs = []
     outs = [None] * P
@@ -59,6 +60,8 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
                 ctx = B.Context(model, group=grp, rank=r)
+                if overlap is not None:
+                    ctx.set_overlap(overlap)
                 xs = dev_bf16(x_shards[r].reshape(x_shards[r].shape[0], -1))
                 acts = [xs]
                 saves = []
@@ -150,6 +153,37 @@ def test_layer_p4_d128(pi):
 def test_layer_bert_shape_noncausal(pi):
     # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
     _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
+
+
+def test_layer_ts_odd_chunks_p2():
+    # s/P = 384 rows (an odd number of 128-row blocks), tile-overlapped TS vs the oracle
+    _check_layer(0, 2, 256, 4, 1024, 768, seed=6)
+
+
+@pytest.mark.parametrize("P,h,n,F,s", [(2, 2048, 16, 8192, 4096),    # CTA-pair GEMMs, 8 m-blocks per chunk
+                                       (4, 1024, 8, 4096, 2048),     # 1-CTA GEMMs, rotated tile order
+                                       (2, 2048, 16, 8192, 2816)])   # 256-row pair tiles straddle chunks
+def test_ts_overlap_bit_identical(P, h, n, F, s):
+    """MegatronTS with the tile-overlapped AG / RS (pds_set_overlap 1) equals the
+    in-order collectives (0) bit for bit: the same tiles, the same rank-order sums."""
+    d = layer_inputs(h, n, F, s, 1, seed=11)
+    W = OS.shard_weights(d, n, P)
+    xs = OS.shard_act(d["x"], P)
+    dys = OS.shard_act(d["dy"], P)
+    model = B.Model(h=h, n_heads=n, ffn=F)
+    res = []
+    for ov in (0, 1):
+        ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
+        outs = run_ranks(model, P, [0], [ranks], xs, dys, overlap=ov)
+        res.append((outs, {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g},
+                    [host(R.o) for R in ranks], [host(R.z) for R in ranks]))
+    (o0, g0, a0, z0), (o1, g1, a1, z1) = res
+    for r in range(P):
+        assert np.array_equal(o0[r][0], o1[r][0]), ("y", r)
+        assert np.array_equal(o0[r][1], o1[r][1]), ("dx", r)
+        assert np.array_equal(a0[r], a1[r]) and np.array_equal(z0[r], z1[r]), ("o/z", r)
+        for k in g0:
+            assert np.array_equal(g0[k][r], g1[k][r]), (k, r)
 
 
 def test_switched_chain_p2():
