@@ -231,6 +231,22 @@ pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const void* B, i
                       int32_t b_mn, int32_t M, int32_t N, int32_t K, void* C, int64_t ldc,
                       int32_t epi, const void* aux_in, void* aux_out, int64_t ld_aux,
                       void* stream);
+/* The collective-overlap protocol of the MegatronTS GEMMs (pds_set_overlap), bf16
+ * C = A B^T with both operands K-major.  M splits into chunks of chunk_rows (a
+ * multiple of 32 dividing M).  wait_flags (nullable, device uint32 [M/chunk_rows]):
+ * a CTA loads A rows of chunk c only once (int32)(wait_flags[c] - flag_epoch) >= 0
+ * (traps after ~8 s).  done_ctr (nullable, device uint32 [M/chunk_rows]): grows by
+ * the number of elements stored in chunk c, so it has grown by chunk_rows*N when the
+ * chunk is complete.  m_rot_rows: first row of the tile order (wraps).  sm_reserve:
+ * SMs left idle.  Bad chunking -> PDS_EINVAL. */
+pds_status pds_k_gemm_sync(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                           int32_t N, int32_t K, void* C, int64_t ldc, const uint32_t* wait_flags,
+                           uint32_t flag_epoch, uint32_t* done_ctr, int64_t chunk_rows,
+                           int64_t m_rot_rows, int32_t sm_reserve, void* stream);
+/* Stream memory operations (no SM): *addr := value after the stream's prior work;
+ * block the stream until (int32)(*addr - value) >= 0.  addr: device memory. */
+pds_status pds_k_stream_write32(void* stream, uint32_t* addr, uint32_t value);
+pds_status pds_k_stream_wait32(void* stream, const uint32_t* addr, uint32_t value);
 /* QKV GEMM with fused RoPE on the Q and K columns: C [M, N] where columns form
  * groups of 3*hq ([Q | K | V], hq = heads*d); row r has global position
  * (r / seg) * seg_stride + seg_base + r % seg.  rope: [positions][d/2] float2. */

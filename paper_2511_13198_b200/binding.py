@@ -115,6 +115,11 @@ _SIGS = {
     "pds_debug_trace": [C.c_void_p, C.c_int32],
     "pds_saved_release": [C.c_void_p, C.c_void_p],
     "pds_debug_taps": [C.c_void_p, C.c_void_p, C.c_void_p],
+    "pds_k_gemm_sync": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                        C.c_void_p, C.c_int64, C.c_void_p, C.c_uint32, C.c_void_p, C.c_int64, C.c_int64,
+                        C.c_int32, C.c_void_p],
+    "pds_k_stream_write32": [C.c_void_p, C.c_void_p, C.c_uint32],
+    "pds_k_stream_wait32": [C.c_void_p, C.c_void_p, C.c_uint32],
     "pds_set_overlap": [C.c_void_p, C.c_int32],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
     "pds_profile_read": [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
@@ -297,6 +302,20 @@ class Context:
 # ------------------------------------------------------------------ kernel-level entry points
 def k_gemm(A, lda, a_mn, B, ldb, b_mn, M, N, K, Cp, ldc, epi=0, aux_in=None, aux_out=None, ld_aux=0, stream=0):
     call("pds_k_gemm", A, lda, a_mn, B, ldb, b_mn, M, N, K, Cp, ldc, epi, aux_in, aux_out, ld_aux, stream)
+
+
+def k_gemm_sync(A, lda, B, ldb, M, N, K, Cp, ldc, wait_flags=None, epoch=0, done_ctr=None, chunk_rows=0,
+                m_rot_rows=0, sm_reserve=0, stream=0):
+    call("pds_k_gemm_sync", A, lda, B, ldb, M, N, K, Cp, ldc, wait_flags, epoch, done_ctr, chunk_rows, m_rot_rows,
+         sm_reserve, stream)
+
+
+def k_stream_write32(stream, addr, value):
+    call("pds_k_stream_write32", stream, addr, value)
+
+
+def k_stream_wait32(stream, addr, value):
+    call("pds_k_stream_wait32", stream, addr, value)
 
 
 def k_gemm_rope(A, lda, B, ldb, M, N, K, Cp, ldc, rope, d, hq, seg=0, seg_stride=0, seg_base=0, stream=0):

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <string>
 
+#include "comm.hpp"
 #include "internal.hpp"
 #include "kernels/gemm.cuh"
 #include "kernels/kernels.hpp"
@@ -39,6 +40,29 @@ extern "C" pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const
   g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc; g.epi = epi;
   g.aux_in = aux_in; g.aux_out = aux_out; g.ld_aux = ld_aux;
   return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm");
+}
+
+extern "C" pds_status pds_k_gemm_sync(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                                      int32_t N, int32_t K, void* C, int64_t ldc, const uint32_t* wait_flags,
+                                      uint32_t flag_epoch, uint32_t* done_ctr, int64_t chunk_rows,
+                                      int64_t m_rot_rows, int32_t sm_reserve, void* stream) {
+  if (!A || !B || !C) PDS_FAIL(PDS_EINVAL, "NULL operand");
+  if ((wait_flags || done_ctr) && chunk_rows <= 0) PDS_FAIL(PDS_EINVAL, "chunk_rows must be > 0");
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.wait_flags = wait_flags; g.flag_epoch = flag_epoch; g.done_ctr = done_ctr;
+  g.chunk_rows = chunk_rows; g.m_rot_rows = m_rot_rows; g.sm_reserve = sm_reserve;
+  return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm_sync");
+}
+
+extern "C" pds_status pds_k_stream_write32(void* stream, uint32_t* addr, uint32_t value) {
+  if (!addr) PDS_FAIL(PDS_EINVAL, "NULL address");
+  return stream_write32(static_cast<cudaStream_t>(stream), addr, value);
+}
+
+extern "C" pds_status pds_k_stream_wait32(void* stream, const uint32_t* addr, uint32_t value) {
+  if (!addr) PDS_FAIL(PDS_EINVAL, "NULL address");
+  return stream_wait32_geq(static_cast<cudaStream_t>(stream), addr, value);
 }
 
 extern "C" pds_status pds_k_gemm_rope(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,

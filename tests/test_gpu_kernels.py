@@ -255,3 +255,65 @@ def test_attention_sync_baseline_matches_tcgen05(tmp_path):
     a = outs["tc"].view(np.float32).astype(np.float64)
     b = outs["sync"].view(np.float32).astype(np.float64)
     assert rel(b, a) < 1e-2
+
+
+# ---------------------------------------------------------------- collective overlap protocol
+# The tile-overlapped MegatronTS collectives (pds_set_overlap) rest on two GEMM hooks:
+# per-chunk "landed" flags polled by the TMA producer before it loads A rows, and
+# per-chunk store counters the reduce-scatter waits on.  Here the chunks really arrive
+# (and leave) WHILE the GEMM runs: pinned-host copies on a second stream (copy engine,
+# no SM), behind a large dummy copy so the GEMM starts first and has to spin.
+
+@pytest.mark.parametrize("M,N,K,chunk,rot", [(4096, 2048, 2048, 1024, 1024),   # CTA-pair kernel
+                                             (1536, 384, 512, 384, 768)])      # 1-CTA kernel, 3 m-blocks/chunk
+def test_gemm_waits_for_chunk_flags(M, N, K, chunk, rot):
+    A = round_bf16(_mat(3, 1, (M, K), std=1 / math.sqrt(K)))
+    W = _mat(3, 2, (N, K))
+    tw = dev_bf16(W)
+    ta_ref = dev_bf16(A)
+    ref = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm(ta_ref.data_ptr(), K, 0, tw.data_ptr(), K, 0, M, N, K, ref.data_ptr(), N, 0, stream=stream())
+    torch.cuda.synchronize()
+
+    a_host = ta_ref.cpu().pin_memory()
+    dummy_h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    dummy_d = torch.empty_like(dummy_h, device="cuda")
+    ta = torch.full((M, K), float("nan"), dtype=torch.bfloat16, device="cuda")
+    flags = torch.zeros(M // chunk, dtype=torch.int32, device="cuda")
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    epoch = 7
+    B.k_gemm_sync(ta.data_ptr(), K, tw.data_ptr(), K, M, N, K, out.data_ptr(), N, wait_flags=flags.data_ptr(),
+                  epoch=epoch, chunk_rows=chunk, m_rot_rows=rot, stream=sa.cuda_stream)
+    with torch.cuda.stream(sb):
+        dummy_d.copy_(dummy_h, non_blocking=True)         # ~5-10 ms: the GEMM is already spinning
+        for c in [(rot // chunk + i) % (M // chunk) for i in range(M // chunk)]:
+            ta[c * chunk:(c + 1) * chunk].copy_(a_host[c * chunk:(c + 1) * chunk], non_blocking=True)
+            B.k_stream_write32(sb.cuda_stream, flags.data_ptr() + 4 * c, epoch)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("M,N,K,chunk,rot", [(4096, 2048, 2048, 1024, 2048), (1536, 384, 512, 384, 0)])
+def test_gemm_store_counters_gate_chunk_reads(M, N, K, chunk, rot):
+    A = _mat(4, 1, (M, K), std=1 / math.sqrt(K))
+    W = _mat(4, 2, (N, K))
+    ta, tw = dev_bf16(A), dev_bf16(W)
+    nch = M // chunk
+    ctr = torch.zeros(nch, dtype=torch.int32, device="cuda")
+    out = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    got = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    # the reader is enqueued FIRST: each chunk is copied out as soon as its counter says so
+    for c in range(nch):
+        B.k_stream_wait32(sb.cuda_stream, ctr.data_ptr() + 4 * c, chunk * N)
+        with torch.cuda.stream(sb):
+            got[c * chunk:(c + 1) * chunk].copy_(out[c * chunk:(c + 1) * chunk], non_blocking=True)
+    B.k_gemm_sync(ta.data_ptr(), K, tw.data_ptr(), K, M, N, K, out.data_ptr(), N, done_ctr=ctr.data_ptr(),
+                  chunk_rows=chunk, m_rot_rows=rot, stream=sa.cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), out.cpu().view(torch.int16))
+    assert ctr.cpu().tolist() == [chunk * N] * nch
+    assert rel(host(out), A.astype(np.float64) @ W.T) < 1e-2
