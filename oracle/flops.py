@@ -31,8 +31,9 @@ def layer_flops(h, s, ffn=None, causal=True, b=1):
     return layer_flops_per_token(h, s, ffn, causal) * s * b
 
 
-def comm_bytes(pi, h, s, P, ffn=None, b=1):
-    """Bytes each rank sends per layer (fwd + bwd), payload convention SPEC.md:109."""
+def comm_bytes(pi, h, s, P, ffn=None, b=1, metp_recompute="ffn"):
+    """Bytes each rank sends per layer (fwd + bwd), payload convention SPEC.md:109.
+    METP with metp_recompute='full' re-gathers u once more (SURVEY O-5 table)."""
     f = 4 * h if ffn is None else ffn
     if P == 1:
         return 0
@@ -40,7 +41,8 @@ def comm_bytes(pi, h, s, P, ffn=None, b=1):
     act = s * b * h * 2
     ar = 2 * fr * 2 * h * 4
     if pi == 0 or pi == 2:   # TS / METP (same bytes, c x more messages)
-        return int(round(10 * fr * act + ar))
+        extra = 1 if (pi == 2 and metp_recompute == "full") else 0
+        return int(round((10 + extra) * fr * act + ar))
     if pi == 1:
         a2a = 2 * fr * (s // P) * b * (3 * h + h) * 2
         wb = 4 * h * h + 2 * h * f

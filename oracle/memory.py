@@ -52,7 +52,7 @@ def _norm_bwd_grid(rows):
     return min((rows + 3) // 4, 444)   # 148 SMs x 3 resident 256-thread blocks
 
 
-def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
+def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None, metp_recompute="ffn"):
     """Workspace bytes per rank of the CUDA path's buffer plan,
     each buffer rounded up to 256 B.  Written out from the plan table, not shared
     with the library (tests compare it with pds_mem_bytes)."""
@@ -78,6 +78,8 @@ def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
         bufs = [u, u, P * uw, P * uw, P * uw, P * w * Fl * 2, P * w * Fl * 2, P * w * Fl * 2,
                 s * hl * 2, s * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4,
                 max(Fl, 3 * hl) * P * w * 2, h * P * w * 2, h * max(Fl, 3 * hl) * 2]
+        if metp_recompute == "full":
+            bufs.append(s * 3 * hl * 2)     # QKV (fwd, then recomputed in bwd), not saved
     else:
         raise KeyError(pi)
     return sum(_al(x) for x in bufs) + small

@@ -37,10 +37,14 @@ NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
 
 
 class Cfg:
-    def __init__(self, h, n, ffn, causal=True, eps=EPS, theta=ROPE_THETA, metp_chunks=None):
+    def __init__(self, h, n, ffn, causal=True, eps=EPS, theta=ROPE_THETA, metp_chunks=None,
+                 metp_recompute="ffn"):
         self.h, self.n, self.ffn = h, n, ffn
         self.causal, self.eps, self.theta = causal, eps, theta
         self.metp_chunks = metp_chunks
+        if metp_recompute not in ("ffn", "full"):
+            raise ValueError(f"metp_recompute must be 'ffn' or 'full', not {metp_recompute!r}")
+        self.metp_recompute = metp_recompute      # R-11 / SURVEY O-6: 'full' also recomputes QKV
 
 
 def _save(grid, r, saved, name, arr, bpe):
@@ -331,7 +335,8 @@ def metp_fwd(grid, xs, W, cfg):
         sv = saved[r]
         _save(grid, r, sv, "x", xs[r], 2)
         _save(grid, r, sv, "r1", r1[r], 4)
-        _save(grid, r, sv, "qkv", qkv[r], 2)
+        if cfg.metp_recompute == "ffn":           # 'full': QKV recomputed in backward
+            _save(grid, r, sv, "qkv", qkv[r], 2)
         _save(grid, r, sv, "a", att[r][0], 2)
         _save(grid, r, sv, "lse", att[r][1], 4)
         _save(grid, r, sv, "x1", x1[r], 2)
@@ -377,7 +382,18 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
         for r in range(P):
             da[r][posw] = dX1w[r] @ W["w_proj"][r].T
             grads["dw_proj"][r] += np.tensordot(sv[r]["a"][posw], dX1w[r], axes=([0, 1], [0, 1]))
-    dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
+    if cfg.metp_recompute == "full":   # QKV recompute: per wave AG(u) and the QKV GEMM again
+        qkv = [np.zeros((s, b, 3 * hl)) for _ in range(P)]
+        for k in range(c):
+            rows = _wave_rows(sl, c, k)
+            posw = _wave_positions(P, sl, c, k)
+            uloc = [_apply_norm(sv[r]["x"][rows], sv[r]["r1"][rows], W["g1"][r]) for r in range(P)]
+            Uw = grid.all_gather(uloc)                             # AG(u) wave k (recompute)
+            for r in range(P):
+                qkv[r][posw] = Uw[r] @ W["w_qkv_t"][r].T
+    else:
+        qkv = [sv[r]["qkv"] for r in range(P)]
+    dqkv = [mha_core_bwd(da[r], qkv[r], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
                          cfg.causal, cfg.theta) for r in range(P)]
     dx = [np.zeros_like(d) for d in dys]
     dg1 = [np.zeros(cfg.h) for _ in range(P)]

@@ -177,3 +177,48 @@ def test_memory_ordering():
         for P in (2, 4, 8):
             m = [memory.saved(pi, 4096, 32, 16384, s, P) for pi in (S.TS, S.UZ, S.METP)]
             assert m[2] < m[0] and m[2] < m[1]
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_metp_full_recompute_equals_unsharded(P):
+    # metp_recompute = 'full' (SURVEY O-5 / O-6): QKV is not saved but recomputed in the
+    # backward from per-wave re-gathers of u; the layer is still the unsharded layer
+    s = 32
+    d = layer_inputs(H, N, F, s, 1, seed=23)
+    y_ref, c = layer.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"],
+                               d["g2"], n=N)
+    g_ref = layer.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"],
+                            d["g2"], n=N)
+    g = Grid(P)
+    cfg = S.Cfg(H, N, F, metp_chunks=2, metp_recompute="full")
+    W = shard.shard_weights(d, N, P)
+    ys, saved, taps = S.layer_fwd(S.METP, g, shard.shard_act(d["x"], P), W, cfg)
+    for r in range(P):
+        assert "qkv" not in saved[r]
+        assert g.live_bytes(r, "saved") == memory.saved(S.METP, H, N, F, s, P, metp_recompute="full")
+    n_fwd = len(g.comm_log)
+    grads = S.new_grads(W)
+    dxs = S.layer_bwd(S.METP, g, shard.shard_act(d["dy"], P), saved, W, cfg, grads)
+    assert _rel(shard.unshard_act(ys), y_ref) < 1e-12
+    assert _rel(shard.unshard_act(dxs), g_ref["dx"]) < 1e-12
+    dense = shard.unshard_grads(grads, N)
+    for k in ("dw_qkv", "dw_proj", "dw_in", "dw_out", "dg1", "dg2"):
+        assert _rel(dense[k], g_ref[k]) < 1e-12, k
+    if P > 1:
+        # signature: the 'ffn' backward plus c = 2 extra wave gathers of u
+        bwd = _signature(g.comm_log[n_fwd:])
+        assert bwd == Counter({"AllGather": 8 + 2, "ReduceScatter": 4, "AllReduce": 1})
+        assert sum(e["bytes"] for e in g.comm_log) == flops.comm_bytes(S.METP, H, s, P, F,
+                                                                         metp_recompute="full")
+    assert all(g.live_bytes(r) == 0 for r in range(P))
+
+
+def test_metp_full_recompute_halves_saved_bytes():
+    # SURVEY O-6: METP saves 6u + 2l + lam ('ffn') or 3u + 2l + lam ('full')
+    for s, P in ((4096, 1), (65536, 2), (638976, 8)):
+        u, l, lam = memory.units(4096, 32, s, P)
+        ffn = memory.saved(S.METP, 4096, 32, 16384, s, P)
+        full = memory.saved(S.METP, 4096, 32, 16384, s, P, metp_recompute="full")
+        assert ffn - full == 3 * u
+    with pytest.raises(ValueError):
+        S.Cfg(H, N, F, metp_recompute="qkv")
