@@ -77,7 +77,9 @@ typedef struct {
   double rope_theta;      /* RoPE base (10000, R-3)                          */
   int32_t causal;         /* 1 = causal mask (north_star), 0 = none          */
   int32_t metp_chunks;    /* METP wave count c (0 -> P)                      */
-  int32_t metp_recompute; /* 0 = recompute FFN intermediates in bwd (R-11)   */
+  int32_t metp_recompute; /* 0 = recompute FFN intermediates in bwd (R-11);
+                              1 = also recompute Q/K/V (saved 3u + 2l + lam
+                              instead of 6u + ..., SURVEY O-6); else EINVAL  */
 } pds_model;
 
 typedef struct pds_ctx pds_ctx;     /* opaque: rank, P, comm, streams, arenas, costs, plan cache */

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256)
   __shared__ uint32_t tile[128][33];
   const int64_t r0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
   const int t = threadIdx.x;
-  const bool remap = seg < rows;
+  const bool remap = seg < rows || base != 0;     // one segment with an offset is a remap too
   uint4 x[4];
 #pragma unroll
   for (int h4 = 0; h4 < 4; ++h4) {

@@ -677,6 +677,8 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   const int64_t row = e.h * 2;
   const int64_t slot = e.r * wr * e.h * 2;
   const char* xb = static_cast<const char*>(x);
+  // metp_recompute = full: Q/K/V live in the workspace (recomputed in bwd), not saved
+  char* qkv = e.m.metp_recompute ? ws + bp.ws_off("qkv") : sv->at("qkv");
   // Wave gathers run on a side stream one wave ahead of the GEMMs ("asynchronous
   // ring-based execution"): AG(k+1) into one of two buffers while the
   // GEMM of wave k reads the other.  At P = 1 the gathers are identities.
@@ -695,12 +697,12 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   };
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, ul, sv->at("rstd1")));
   PDS_TRY(waves(ul, [&](int64_t k, char* buf) -> pds_status {   // QKV waves: rows land at global positions
-    GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
+    GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, qkv, 3 * e.hl),
                         e.hl, wr, e.sl, k * wr);
     q.c_seg = wr; q.c_stride = e.sl; q.c_base = k * wr;
     return e.gemm(q);
   }));
-  PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));  // query-chunk x KV-chunk loop
+  PDS_TRY(e.attn_f(qkv, sv->at("a"), sv->at("lse")));             // query-chunk x KV-chunk loop
   PDS_TRY(tn.tr(w->w_proj, e.h, e.hl, e.h, wt));                 // W_proj^T, reused by every wave
   for (int64_t k = 0; k < c; ++k) {   // projection waves (A rows read through the TMA row remap)
     GemmArgs pj = Exec::G(sv->at("a"), e.hl, 0, wt, e.hl, 0, W, e.h, e.hl, pw, e.h);
@@ -776,7 +778,19 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     PDS_TRY(e.gemm(dA));
     PDS_TRY(tn.dw(sv->at("a"), e.hl, wg, e.h, W, e.hl, e.h, g->dw_proj, EPI_F32_ACC, wr, e.sl, o));
   }
-  PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), da, dqkv, dd));
+  char* qkv = sv->plan.has_ws("qkv") ? ws + bp.ws_off("qkv") : sv->at("qkv");
+  if (e.m.metp_recompute) {           // full: Q/K/V recomputed from per-wave re-gathers of u
+    for (int64_t k = 0; k < c; ++k) {
+      const int64_t o = k * wr;
+      PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
+      PDS_TRY(e.ag(ul, wg, wr * e.h));                                                   // AG(u) recompute
+      GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, qkv, 3 * e.hl),
+                          e.hl, wr, e.sl, o);
+      q.c_seg = wr; q.c_stride = e.sl; q.c_base = o;
+      PDS_TRY(e.gemm(q));
+    }
+  }
+  PDS_TRY(e.attn_b(qkv, sv->at("a"), sv->at("lse"), da, dqkv, dd));
   PDS_TRY(tn.tr(w->w_qkv_t, e.h, 3 * e.hl, e.h, wt));            // W_qkv for dU, every wave
   for (int64_t k = 0; k < c; ++k) {   // QKV backward waves
     const int64_t o = k * wr;

@@ -289,10 +289,12 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       if (sl % c) PDS_FAIL(PDS_EDIVISIBILITY, "s/P not divisible by metp_chunks");
       const int64_t w = sl / c;
       if (w % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/(P*metp_chunks)=" + std::to_string(w) + " must be a multiple of 128");
-      if (m.metp_recompute != 0) PDS_FAIL(PDS_ENOTIMPL, "metp_recompute=full is not implemented");
+      if (m.metp_recompute != 0 && m.metp_recompute != 1)
+        PDS_FAIL(PDS_EINVAL, "metp_recompute must be 0 (ffn) or 1 (full)");
+      const bool full = m.metp_recompute == 1;     // QKV recomputed in bwd, not saved
       const int64_t uw = w * h * 2;
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", s * 3 * hl * 2);
+      if (!full) push(p.saved, ts, "qkv", s * 3 * hl * 2);
       push(p.saved, ts, "a", s * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
@@ -313,6 +315,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * w * 2);
       push(p.ws, tw, "tb", h * P * w * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      if (full) push(p.ws, tw, "qkv", s * 3 * hl * 2);
       break;
     }
     default:

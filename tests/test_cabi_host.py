@@ -91,6 +91,21 @@ def test_mem_bytes_vs_oracle(B, cfg):
         assert tr == OM.transient(pi, h, n, F, s, P), (pi, cfg)
 
 
+@pytest.mark.parametrize("cfg", [(256, 4, 1024, 512, 2), (4096, 32, 16384, 638976, 8), (4096, 32, 16384, 65536, 1)])
+def test_mem_bytes_metp_full_vs_oracle(B, cfg):
+    # metp_recompute = 1 ('full'): saved 3u + 2l + lam, Q/K/V in the workspace instead
+    h, n, F, s, P = cfg
+    m = B.Model(h=h, n_heads=n, ffn=F, metp_recompute=1)
+    saved, tr, pers = B.mem_bytes(m, P, 2, s)
+    assert saved == OM.saved(2, h, n, F, s, P, metp_recompute="full")
+    assert tr == OM.transient(2, h, n, F, s, P, metp_recompute="full")
+    saved0, _, _ = B.mem_bytes(B.Model(h=h, n_heads=n, ffn=F), P, 2, s)
+    assert saved0 - saved == 3 * (s // P) * h * 2
+    with pytest.raises(B.PdsError) as e:
+        B.mem_bytes(B.Model(h=h, n_heads=n, ffn=F, metp_recompute=2), P, 2, s)
+    assert e.value.code == -1
+
+
 def test_mem_bytes_errors(B):
     m = B.Model(h=256, n_heads=4, ffn=1024)
     with pytest.raises(B.PdsError) as e:

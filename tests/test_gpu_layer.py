@@ -98,7 +98,7 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
     return outs
 
 
-def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True):
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0):
     d = layer_inputs(h, n, F, s, 1, seed=seed)
     y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
                             causal=causal)
@@ -108,7 +108,8 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True):
     xs = OS.shard_act(d["x"], P)
     dys = OS.shard_act(d["dy"], P)
     ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
-    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0)
+    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0,
+                    metp_recompute=recompute)
     outs = run_ranks(model, P, [pi], [ranks], xs, dys)
     y = np.concatenate([o[0] for o in outs])[:, None, :]
     dx = np.concatenate([o[1] for o in outs])[:, None, :]
@@ -153,6 +154,34 @@ def test_layer_p4_d128(pi):
 def test_layer_bert_shape_noncausal(pi):
     # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
     _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
+
+
+@pytest.mark.parametrize("recompute", [0, 1])
+@pytest.mark.parametrize("P,h,n,F,s,chunks", [(1, 256, 4, 1024, 512, 2), (2, 256, 4, 1024, 512, 0),
+                                              (4, 1024, 8, 4096, 1024, 2)])
+def test_layer_metp_recompute_modes(P, h, n, F, s, chunks, recompute):
+    # metp_recompute = full: Q/K/V recomputed in backward from re-gathered u (SURVEY O-6).
+    # P = 1 with c = 2 waves: a single-segment row remap with an offset (wave 1 of rank 0)
+    _check_layer(2, P, h, n, F, s, chunks=chunks, recompute=recompute)
+
+
+def test_metp_full_equals_ffn_bitwise():
+    # the recomputed Q/K/V are the forward's bit for bit, so every output and gradient is
+    P, h, n, F, s = 2, 1024, 8, 4096, 1024
+    d = layer_inputs(h, n, F, s, 1, seed=12)
+    W = OS.shard_weights(d, n, P)
+    xs = OS.shard_act(d["x"], P)
+    dys = OS.shard_act(d["dy"], P)
+    res = []
+    for rc in (0, 1):
+        ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
+        outs = run_ranks(B.Model(h=h, n_heads=n, ffn=F, metp_recompute=rc), P, [2], [ranks], xs, dys)
+        res.append((outs, {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g}))
+    for r in range(P):
+        assert np.array_equal(res[0][0][r][0], res[1][0][r][0])
+        assert np.array_equal(res[0][0][r][1], res[1][0][r][1])
+        for k in res[0][1]:
+            assert np.array_equal(res[0][1][k][r], res[1][1][k][r]), k
 
 
 def test_layer_ts_odd_chunks_p2():
