@@ -80,10 +80,12 @@ def main():
     ap.add_argument("--reserve-gb", type=float, default=4.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-run", action="store_true")
+    ap.add_argument("--metp-recompute", type=int, default=0, help="0 = ffn, 1 = full (Q/K/V recomputed too)")
+    ap.add_argument("--plans", default="MegatronTS,UlyssesZ,METP,adaptive")
     a = ap.parse_args()
     H, N, F = 4096, 32, 16384
     P = 1
-    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)
+    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L, metp_recompute=a.metp_recompute)
     ctx = B.Context(model)
     bundle = os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt")
     ctx.load_costs(bundle)
@@ -102,10 +104,13 @@ def main():
     pers = sum(B.mem_bytes(model, P, 0, 1024)[2] for _ in range(a.L))
     ctx.set_capacity(cap + pers, 0.0)   # the planner's M includes persistent bytes
     res = {"device_total_bytes": total, "free_after_weights": free, "capacity_for_plan": cap + pers,
-           "L": a.L, "P": P, "model": {"h": H, "n": N, "ffn": F}, "step": a.step, "plans": {}}
+           "L": a.L, "P": P, "model": {"h": H, "n": N, "ffn": F, "metp_recompute": a.metp_recompute},
+           "step": a.step, "plans": {}}
     lay = [(W, G) for W, G, _, _ in layers]
     candidates = {"MegatronTS": [0] * a.L, "UlyssesZ": [1] * a.L, "METP": [2] * a.L, "adaptive": None}
     for name, fixed in candidates.items():
+        if name not in a.plans.split(","):
+            continue
         best = None
         s = a.step
         while s <= a.smax:
