@@ -237,7 +237,7 @@ pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const void* B, i
  * C = A B^T with both operands K-major.  M splits into chunks of chunk_rows (a
  * multiple of 32 dividing M).  wait_flags (nullable, device uint32 [M/chunk_rows]):
  * a CTA loads A rows of chunk c only once (int32)(wait_flags[c] - flag_epoch) >= 0
- * (traps after ~8 s).  done_ctr (nullable, device uint32 [M/chunk_rows]): grows by
+ * (traps after > 30 s).  done_ctr (nullable, device uint32 [M/chunk_rows]): grows by
  * the number of elements stored in chunk c, so it has grown by chunk_rows*N when the
  * chunk is complete.  m_rot_rows: first row of the tile order (wraps).  sm_reserve:
  * SMs left idle.  Bad chunking -> PDS_EINVAL. */

@@ -111,6 +111,12 @@ struct NcclComm : Comm {
       side_->rank = rank;
       side_->comm = c2;
       side_->max_ctas = cfg.maxCTAs;
+      // NCCL connects point-to-point peers lazily, which can take a while; connect them
+      // now so no tile-polling GEMM ever waits on connection setup
+      if (side_->warm_p2p() != PDS_OK) {
+        *st = PDS_ENCCL;
+        return nullptr;
+      }
     }
     return side_;
   }
@@ -157,6 +163,27 @@ struct NcclComm : Comm {
     return PDS_OK;
   }
   int overlap_sm_reserve() const override { return max_ctas; }
+  pds_status warm_p2p() {
+    void* buf = nullptr;
+    cudaStream_t s = nullptr;
+    PDS_CUDA(cudaMalloc(&buf, 2 * 256));
+    PDS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    pds_status rc = PDS_OK;
+    for (int k = 1; k < P && rc == PDS_OK; ++k) {
+      const int to = (rank + k) % P, from = (rank - k + P) % P;
+      if (ncclGroupStart() != ncclSuccess ||
+          ncclSend(buf, 64, ncclFloat32, to, comm, s) != ncclSuccess ||
+          ncclRecv(static_cast<char*>(buf) + 256, 64, ncclFloat32, from, comm, s) != ncclSuccess ||
+          ncclGroupEnd() != ncclSuccess) {
+        set_error("NCCL point-to-point warm-up failed");
+        rc = PDS_ENCCL;
+      }
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaFree(buf);
+    return rc;
+  }
   int max_ctas = 0;
   pds_status all_to_all(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     const int64_t b = count * dt_size(dt);

@@ -75,7 +75,7 @@ struct EpiParams {
 // AG -> GEMM: wait until every chunk overlapping rows [r0, r0 + n) has landed.  The
 // flag is written by the collective's stream (after its copy) with release semantics;
 // the acquire load plus a generic -> async proxy fence make the landed rows visible to
-// the TMA loads that follow.  A chunk that never lands is a bug: trap after ~8 s
+// the TMA loads that follow.  A chunk that never lands is a bug: trap after > 30 s
 // instead of hanging the device.
 __device__ __forceinline__ void wait_chunks(const EpiParams& ep, int r0, int n) {
   if (!ep.wait_flags || n <= 0) return;
@@ -87,7 +87,7 @@ __device__ __forceinline__ void wait_chunks(const EpiParams& ep, int r0, int n) 
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ep.wait_flags + c) : "memory");
       if ((int32_t)(v - ep.flag_epoch) >= 0) break;
       __nanosleep(128);
-      if (++spins > (1u << 26)) __trap();
+      if (++spins > (1u << 28)) __trap();
     }
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
