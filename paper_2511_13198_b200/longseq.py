@@ -31,18 +31,26 @@ def main():
     ap.add_argument("--seqs", type=int, nargs="+", default=[65536, 131072])
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--strategies", default="0,1,2", help="subset of 0 (TS), 1 (UZ), 2 (METP)")
+    ap.add_argument("--metp-recompute", type=int, default=0)
+    ap.add_argument("--metp-chunks", type=int, default=0)
     a = ap.parse_args()
     H, N, F, P = 4096, 32, 16384, 1
-    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=1)
+    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=1, metp_recompute=a.metp_recompute,
+                    metp_chunks=a.metp_chunks)
+    want = {int(x) for x in a.strategies.split(",")}
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
-    res = {"model": {"h": H, "n": N, "ffn": F}, "P": P, "runs": []}
+    res = {"model": {"h": H, "n": N, "ffn": F, "metp_recompute": a.metp_recompute, "metp_chunks": a.metp_chunks},
+           "P": P, "runs": []}
     for s in a.seqs:
         w, gr, x, dy = make_layer_buffers(torch, model, P, s, seed=7)
         W = B.Weights(*(w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
         G = B.Grads(*(gr[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
         y, dx = torch.empty_like(x), torch.empty_like(x)
         for pi, name in ((0, "MegatronTS"), (1, "UlyssesZ"), (2, "METP")):
+            if pi not in want:
+                continue
             ctx = B.Context(model)
             saved_b, trans_b, _ = B.mem_bytes(model, P, pi, s)
             torch.cuda.synchronize()
@@ -64,6 +72,8 @@ def main():
                     times.append(e0.elapsed_time(e1) / 1e3)
             t = min(times)
             rec = {"s": s, "strategy": name, "seconds": t, "tokens_per_s": s / t,
+                   # model FLOPs of one causal layer fwd + bwd: s (72 h^2 + 6 s h) (SURVEY O-7)
+                   "model_tflops": s * (72.0 * H * H + 6.0 * s * H) / t / 1e12,
                    "predicted_saved_bytes": saved_b, "predicted_transient_bytes": trans_b,
                    "predicted_total_bytes": saved_b + trans_b, "measured_library_bytes": measured,
                    "rope_table_bytes": s * (H // N // 2) * 8,
