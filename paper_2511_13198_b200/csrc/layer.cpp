@@ -205,7 +205,8 @@ struct Exec {
   }
   // AG of buf [P][count] (this rank's chunk already at slot r) on the side stream, chunk
   // by chunk, consumed tile by tile by the next gemm(), whose A operand is buf
-  pds_status ag_next(void* buf, int64_t count) {
+  pds_status ag_next(void* buf, int64_t count, int64_t rows = 0) {
+    if (!rows) rows = sl;                    // rows per rank chunk (METP: one wave's)
     PDS_TRY(sync_init());
     cudaStream_t cs = comm_stream();
     PDS_TRY(link(st, cs));
@@ -219,7 +220,7 @@ struct Exec {
     }
     nxt = GemmArgs();
     nxt.wait_flags = c->sync; nxt.flag_epoch = epoch;
-    nxt.chunk_rows = sl; nxt.m_rot_rows = (int64_t)r * sl;
+    nxt.chunk_rows = rows; nxt.m_rot_rows = (int64_t)r * rows;
     nxt.sm_reserve = cm->overlap_sm_reserve();
     has_nxt = true;
     nxt_join = mark(cs);
@@ -228,17 +229,18 @@ struct Exec {
   // arm the next gemm() (output [P][sl][ncols], all rows) to count its stores per chunk,
   // computing the chunk sent first (r+1) first and its own chunk last
   uint32_t rs_target = 0;
-  pds_status rs_arm(int64_t ncols) {
+  pds_status rs_arm(int64_t ncols, int64_t rows = 0) {
+    if (!rows) rows = sl;
     PDS_TRY(sync_init());
     PDS_TRY(link(st, comm_stream()));        // the receive buffer's readers are done
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
-    c->rs_count += (uint32_t)(sl * ncols);
+    c->rs_count += (uint32_t)(rows * ncols);
     rs_target = c->rs_count;
     nxt = GemmArgs();
     nxt.done_ctr = c->sync + 8;
-    nxt.chunk_rows = sl; nxt.m_rot_rows = (int64_t)((r + 1) % P) * sl;
+    nxt.chunk_rows = rows; nxt.m_rot_rows = (int64_t)((r + 1) % P) * rows;
     nxt.sm_reserve = cm->overlap_sm_reserve();
     has_nxt = true;
     return PDS_OK;
@@ -704,11 +706,15 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   }));
   PDS_TRY(e.attn_f(qkv, sv->at("a"), sv->at("lse")));             // query-chunk x KV-chunk loop
   PDS_TRY(tn.tr(w->w_proj, e.h, e.hl, e.h, wt));                 // W_proj^T, reused by every wave
+  // P > 1: each wave's RS leaves tile by tile while its GEMM runs (as in TS, §7); the
+  // wave-gather buffers, free during the projection waves, receive the peers' partials
+  const bool ov = e.overlap();
   for (int64_t k = 0; k < c; ++k) {   // projection waves (A rows read through the TMA row remap)
     GemmArgs pj = Exec::G(sv->at("a"), e.hl, 0, wt, e.hl, 0, W, e.h, e.hl, pw, e.h);
     pj.a_seg = wr; pj.a_stride = e.sl; pj.a_base = k * wr; pj.a_rows = e.s;
+    if (ov) PDS_TRY(e.rs_arm(e.h, wr));
     PDS_TRY(e.gemm(pj));
-    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
+    PDS_TRY(ov ? e.rs_run(pw, gb[k & 1], wr * e.h) : e.rs(pw, pw + slot, wr * e.h));
     if (e.c->tap_o) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_o) + k * wr * row, pw + slot, wr * e.h));
     PDS_TRY(e.norm_fwd(xb + k * wr * row, pw + slot, w->g2, wr, sv->at("x1") + k * wr * row, vl + k * wr * row,
                        sv->at("rstd2") + k * wr * 4));
@@ -718,8 +724,9 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
     GemmArgs fc1 = Exec::G(buf, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
     fc1.aux_out = gw; fc1.ld_aux = e.Fl;
     PDS_TRY(e.gemm(fc1));
+    if (ov) PDS_TRY(e.rs_arm(e.h, wr));
     PDS_TRY(tn.mm(gw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
-    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));
+    PDS_TRY(ov ? e.rs_run(pw, buf, wr * e.h) : e.rs(pw, pw + slot, wr * e.h));   // buf: consumed by FC1
     if (e.c->tap_z) PDS_TRY(e.tap(static_cast<char*>(e.c->tap_z) + k * wr * row, pw + slot, wr * e.h));
     return e.add(sv->at("x1") + k * wr * row, pw + slot, static_cast<char*>(y) + k * wr * row, wr * e.h);
   });
@@ -750,13 +757,22 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
   const char* xb = static_cast<const char*>(sv->x);
   char* dxb = static_cast<char*>(dx);
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  const bool ov = e.overlap();       // P > 1: wave AG / RS overlapped with the wave GEMMs' tiles
   PDS_TRY(tn.tr(w->w_in_t, e.h, e.Fl, e.h, wt));                 // W_in (= (W_in^T)^T) for dV, every wave
   for (int64_t k = 0; k < c; ++k) {   // FFN backward waves, recomputing v, H, G
     const int64_t o = k * wr;
-    PDS_TRY(e.ag(dyb + o * row, wg, wr * e.h));                                         // AG(dz)
     PDS_TRY(e.apply(sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, wr, vl));
-    PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                    // AG(v)
-    PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                   // H recompute
+    if (ov) {                          // tile-overlapped wave gathers (§7)
+      PDS_CUDA(cudaMemcpyAsync(wg2 + slot, vl, wr * row, cudaMemcpyDeviceToDevice, e.st));
+      PDS_TRY(e.ag_next(wg2, wr * e.h, wr));                                             // AG(v)
+      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                 // H recompute
+      PDS_CUDA(cudaMemcpyAsync(wg + slot, dyb + o * row, wr * row, cudaMemcpyDeviceToDevice, e.st));
+      PDS_TRY(e.ag_next(wg, wr * e.h, wr));                                              // AG(dz)
+    } else {
+      PDS_TRY(e.ag(dyb + o * row, wg, wr * e.h));                                       // AG(dz)
+      PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                  // AG(v)
+      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                 // H recompute
+    }
     GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.Fl, EPI_DGELU);
     dgel.aux_in = hw; dgel.ld_aux = e.Fl;
     dgel.aux_t = tn.ta; dgel.c_t = gw; dgel.ld_t = W;                                  // G^T, dH^T
@@ -765,14 +781,20 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     PDS_TRY(tn.mm(tn.ta, W, tn.tb, W, e.Fl, e.h, W, g->dw_out, e.h, EPI_F32_ACC));      // dW_out += G^T dZ
     PDS_TRY(tn.tr(wg2, e.h, W, e.h, tn.tb));
     PDS_TRY(tn.mm(gw, W, tn.tb, W, e.Fl, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC));        // dW_in^T += dH^T V
+    if (ov) PDS_TRY(e.rs_arm(e.h, wr));
     PDS_TRY(tn.mm(dhw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
-    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(dv)
+    PDS_TRY(ov ? e.rs_run(pw, wg, wr * e.h) : e.rs(pw, pw + slot, wr * e.h));            // RS(dv)
     PDS_TRY(e.norm_bwd(pw + slot, sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, dyb + o * row, wr,
                        dxb + o * row, dgp, dgl + e.h));
   }
   for (int64_t k = 0; k < c; ++k) {   // projection backward waves
     const int64_t o = k * wr;
-    PDS_TRY(e.ag(dxb + o * row, wg, wr * e.h));                                          // AG(dx1)
+    if (ov) {
+      PDS_CUDA(cudaMemcpyAsync(wg + slot, dxb + o * row, wr * row, cudaMemcpyDeviceToDevice, e.st));
+      PDS_TRY(e.ag_next(wg, wr * e.h, wr));                                              // AG(dx1)
+    } else {
+      PDS_TRY(e.ag(dxb + o * row, wg, wr * e.h));                                        // AG(dx1)
+    }
     GemmArgs dA = Exec::G(wg, e.h, 0, w->w_proj, e.h, 0, W, e.hl, e.h, da, e.hl);
     dA.c_seg = wr; dA.c_stride = e.sl; dA.c_base = o;
     PDS_TRY(e.gemm(dA));
@@ -799,8 +821,9 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     PDS_TRY(tn.dw(dqkv, 3 * e.hl, wg, e.h, W, 3 * e.hl, e.h, g->dw_qkv_t, EPI_F32_ACC, wr, e.sl, o));
     GemmArgs du = Exec::G(dqkv, 3 * e.hl, 0, wt, 3 * e.hl, 0, W, e.h, 3 * e.hl, pw, e.h);
     du.a_seg = wr; du.a_stride = e.sl; du.a_base = o; du.a_rows = e.s;
+    if (ov) PDS_TRY(e.rs_arm(e.h, wr));
     PDS_TRY(e.gemm(du));
-    PDS_TRY(e.rs(pw, pw + slot, wr * e.h));                                              // RS(du)
+    PDS_TRY(ov ? e.rs_run(pw, wg2, wr * e.h) : e.rs(pw, pw + slot, wr * e.h));           // RS(du)
     PDS_TRY(e.norm_bwd(pw + slot, xb + o * row, sv->at("rstd1") + o * 4, w->g1, dxb + o * row, wr, dxb + o * row,
                        dgp, dgl));
   }

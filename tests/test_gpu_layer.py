@@ -189,21 +189,24 @@ def test_layer_ts_odd_chunks_p2():
     _check_layer(0, 2, 256, 4, 1024, 768, seed=6)
 
 
-@pytest.mark.parametrize("P,h,n,F,s", [(2, 2048, 16, 8192, 4096),    # CTA-pair GEMMs, 8 m-blocks per chunk
-                                       (4, 1024, 8, 4096, 2048),     # 1-CTA GEMMs, rotated tile order
-                                       (2, 2048, 16, 8192, 2816)])   # 256-row pair tiles straddle chunks
-def test_ts_overlap_bit_identical(P, h, n, F, s):
-    """MegatronTS with the tile-overlapped AG / RS (pds_set_overlap 1) equals the
+@pytest.mark.parametrize("pi,P,h,n,F,s,chunks", [
+    (0, 2, 2048, 16, 8192, 4096, 0),    # TS, CTA-pair GEMMs, 8 m-blocks per chunk
+    (0, 4, 1024, 8, 4096, 2048, 0),     # TS, 1-CTA GEMMs, rotated tile order
+    (0, 2, 2048, 16, 8192, 2816, 0),    # TS, 256-row pair tiles straddle chunks
+    (2, 2, 2048, 16, 8192, 4096, 2),    # METP, 2 waves of 1024 rows per rank
+    (2, 4, 1024, 8, 4096, 2048, 2)])    # METP, 4 ranks x 2 waves of 256 rows
+def test_overlap_bit_identical(pi, P, h, n, F, s, chunks):
+    """MegatronTS / METP with the tile-overlapped AG / RS (pds_set_overlap 1) equal the
     in-order collectives (0) bit for bit: the same tiles, the same rank-order sums."""
     d = layer_inputs(h, n, F, s, 1, seed=11)
     W = OS.shard_weights(d, n, P)
     xs = OS.shard_act(d["x"], P)
     dys = OS.shard_act(d["dy"], P)
-    model = B.Model(h=h, n_heads=n, ffn=F)
+    model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks)
     res = []
     for ov in (0, 1):
         ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
-        outs = run_ranks(model, P, [0], [ranks], xs, dys, overlap=ov)
+        outs = run_ranks(model, P, [pi], [ranks], xs, dys, overlap=ov)
         res.append((outs, {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g},
                     [host(R.o) for R in ranks], [host(R.z) for R in ranks]))
     (o0, g0, a0, z0), (o1, g1, a1, z1) = res
