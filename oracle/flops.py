@@ -47,4 +47,7 @@ def comm_bytes(pi, h, s, P, ffn=None, b=1, metp_recompute="ffn"):
         a2a = 2 * fr * (s // P) * b * (3 * h + h) * 2
         wb = 4 * h * h + 2 * h * f
         return int(round(a2a + fr * wb * (2 + 2 + 4) + ar))
+    if pi == 3:              # CZ: AG(QKV) fwd + re-gather bwd + RS(dQKV), ZeRO3 weights as UZ
+        wb = 4 * h * h + 2 * h * f
+        return int(round(3 * fr * s * b * 3 * h * 2 + fr * wb * (2 + 2 + 4) + ar))
     raise KeyError(pi)

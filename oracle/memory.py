@@ -20,7 +20,7 @@ workspace plan of the CUDA path (DESIGN.md §Memory) written out independently;
 """
 from __future__ import annotations
 
-TS, UZ, METP = 0, 1, 2
+TS, UZ, METP, CZ = 0, 1, 2, 3
 
 
 def units(h, n, s, P, b=1):
@@ -35,7 +35,7 @@ def persistent(h, ffn, P):
 def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
     u, l, lam = units(h, n, s, P, b)
     f = ffn // h
-    if pi == TS:
+    if pi == TS or pi == CZ:           # CZ saves its local rows of the same tensors
         return (6 + f) * u + 2 * l + lam
     if pi == UZ:
         return (7 + f) * u + 2 * l + lam
@@ -70,6 +70,12 @@ def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None, metp_recompute="ffn"):
     elif pi == UZ:
         bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
                 u, 3 * u, 3 * u, sl * ffn * 2, sl * ffn * 2, 3 * u, 3 * u, u, lam,
+                _norm_bwd_grid(sl) * h * 4, max(ffn, 3 * h) * sl * 2, h * sl * 2, h * max(ffn, 3 * h) * 2]
+    elif pi == CZ:
+        # full weights + fp32 dW (ZeRO3), gathered Q/K/V of the whole context and the
+        # all-rows dQ/dK/dV partials (RS in place), local FFN / attention scratch
+        bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
+                u, s * 3 * h * 2, s * 3 * h * 2, sl * ffn * 2, sl * ffn * 2, u, u, lam,
                 _norm_bwd_grid(sl) * h * 4, max(ffn, 3 * h) * sl * 2, h * sl * 2, h * max(ffn, 3 * h) * 2]
     elif pi == METP:
         c = metp_chunks or P

@@ -32,8 +32,8 @@ import numpy as np
 from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
                     rmsnorm, rmsnorm_bwd)
 
-TS, UZ, METP = 0, 1, 2
-NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
+TS, UZ, METP, CZ = 0, 1, 2, 3
+NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ"}
 
 
 class Cfg:
@@ -418,7 +418,132 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
     return dx
 
 
-REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd)}
+# ------------------------------------------------------------------ MegatronCZ
+# Megatron-LM CP + ZeRO3 (reading R-CZ): weights gathered
+# ZeRO3-style as in UlyssesZ, every GEMM local on the rank's s/P rows; the context-
+# parallel attention all-gathers the sequence's Q/K/V and computes the rank's own
+# query rows against every key (causal: keys <= the query position).  In backward the
+# key / value gradients of every rank's queries are reduce-scattered back to the rows'
+# owners.  The W_qkv spec shard [Q_r; K_r; V_r] is gathered part by part so the full
+# weight is [Q all; K all; V all] (one attention call over all heads), and its
+# gradient is reduce-scattered part by part back into the spec layout.
+
+def _gather_qkv_parts(grid, W, h):
+    P = grid.p
+    hl = h // P
+    parts = [grid.all_gather([W["w_qkv_t"][r][i * hl:(i + 1) * hl] for r in range(P)])[0]
+             for i in range(3)]                                    # 3 x AG: Q, K, V rows
+    return np.concatenate(parts, axis=0)                           # [3h, h], [Q all; K all; V all]
+
+
+def cz_fwd(grid, xs, W, cfg):
+    P = grid.p
+    sl = xs[0].shape[0]
+    s = sl * P
+    wq = _gather_qkv_parts(grid, W, cfg.h)
+    wp = grid.all_gather(W["w_proj"])[0]
+    wi = grid.all_gather(W["w_in_t"])[0]
+    wo = grid.all_gather(W["w_out"])[0]
+    saved = [dict() for _ in range(P)]
+    u, r1, qkv_loc = [], [], []
+    for r in range(P):
+        ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
+        u.append(ur)
+        r1.append(rr)
+        qkv_loc.append(ur @ wq.T)                                  # [s/P, b, 3h], [Q | K | V] all heads
+    qkv = grid.all_gather(qkv_loc)                                 # AG(QKV): the whole context
+    a_all, lse_all = mha_core_fwd(qkv[0], cfg.n, np.arange(s), cfg.causal, cfg.theta)
+    y, o, z = [], [], []
+    for r in range(P):
+        rows = slice(r * sl, (r + 1) * sl)
+        a_r = a_all[rows]                                          # this rank's query rows
+        lse_r = lse_all[..., rows]
+        o_r = a_r @ wp
+        x1 = xs[r] + o_r
+        vr, _, rr2 = rmsnorm(x1, W["g2"][r], cfg.eps)
+        hp = vr @ wi.T
+        z_r = gelu(hp) @ wo
+        o.append(o_r)
+        z.append(z_r)
+        y.append(x1 + z_r)
+        sv = saved[r]
+        _save(grid, r, sv, "x", xs[r], 2)
+        _save(grid, r, sv, "r1", r1[r], 4)
+        _save(grid, r, sv, "qkv", qkv_loc[r], 2)
+        _save(grid, r, sv, "a", a_r, 2)
+        _save(grid, r, sv, "lse", lse_r, 4)
+        _save(grid, r, sv, "x1", x1, 2)
+        _save(grid, r, sv, "r2", rr2, 4)
+        _save(grid, r, sv, "h", hp, 2)
+    return y, saved, dict(o=o, z=z)
+
+
+def cz_bwd(grid, dys, saved, W, cfg, grads):
+    P = grid.p
+    sl = dys[0].shape[0]
+    s = sl * P
+    h = cfg.h
+    hl = h // P
+    sv = saved
+    wq = _gather_qkv_parts(grid, W, h)
+    wp = grid.all_gather(W["w_proj"])[0]
+    wi = grid.all_gather(W["w_in_t"])[0]
+    wo = grid.all_gather(W["w_out"])[0]
+    dwo, dwi, dwp, dwq = [], [], [], []
+    dx1, dg2, da = [], [], []
+    for r in range(P):
+        hp = sv[r]["h"]
+        v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
+        dg = dys[r] @ wo.T
+        dh = dg * gelu_grad(hp)
+        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
+        xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
+        d, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
+        dx1.append(dys[r] + d)
+        dg2.append(dgr)
+        da.append(dx1[r] @ wp.T)                                   # dA, local rows
+        dwp.append(np.tensordot(sv[r]["a"], dx1[r], axes=([0, 1], [0, 1])))
+    qkv = grid.all_gather([sv[r]["qkv"] for r in range(P)])        # AG(QKV) re-gather
+    # every rank: the gradients its own query rows induce on all of Q / K / V (the
+    # other rows' cotangents are zero), then RS sums the key / value parts over ranks
+    parts = []
+    for r in range(P):
+        rows = slice(r * sl, (r + 1) * sl)
+        da_full = np.zeros(qkv[r].shape[:-1] + (h,))
+        da_full[rows] = da[r]
+        a_full = np.zeros_like(da_full)
+        a_full[rows] = sv[r]["a"]
+        lse_full = np.zeros(sv[r]["lse"].shape[:-1] + (s,))
+        lse_full[..., rows] = sv[r]["lse"]
+        parts.append(mha_core_bwd(da_full, qkv[r], a_full, lse_full, cfg.n, np.arange(s), cfg.causal,
+                                  cfg.theta))
+    dqkv = grid.reduce_scatter(parts)                              # RS(dQKV)
+    dx, dg1 = [], []
+    for r in range(P):
+        u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
+        dwq.append(np.tensordot(dqkv[r], u, axes=([0, 1], [0, 1])))   # [3h, h], [Q; K; V] all
+        du = dqkv[r] @ wq
+        xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
+        d, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
+        dx.append(dx1[r] + d)
+        dg1.append(dgr)
+    # ZeRO3 reduce-scatters (fp32): W_qkv^T part by part back into [Q_r; K_r; V_r]
+    qparts = [grid.reduce_scatter([dwq[r][i * h:(i + 1) * h] for r in range(P)], axis=0, bpe=4)
+              for i in range(3)]
+    for r in range(P):
+        grads["dw_qkv_t"][r] += np.concatenate([qparts[i][r] for i in range(3)], axis=0)
+    for key, full in (("dw_proj", dwp), ("dw_in_t", dwi), ("dw_out", dwo)):
+        part = grid.reduce_scatter(full, axis=0, bpe=4)
+        for r in range(P):
+            grads[key][r] += part[r]
+    _finish_dgamma(grid, grads, dg1, dg2)
+    for r in range(P):
+        _release(grid, sv[r])
+    return dx
+
+
+REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd), CZ: (cz_fwd, cz_bwd)}
 
 
 def layer_fwd(pi, grid, xs, W, cfg):

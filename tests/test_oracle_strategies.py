@@ -31,7 +31,7 @@ def _run(pi, P, d, s, causal=True, chunks=None):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
-@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP])
+@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ])
 def test_strategy_equals_unsharded(pi, P):
     s = 32
     d = layer_inputs(H, N, F, s, 1, seed=21)
@@ -64,7 +64,7 @@ def test_noncausal_and_batch(P):
     d = layer_inputs(H, N, F, s, 2, seed=5)
     y_ref, c = layer.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"],
                                d["g2"], n=N, causal=False)
-    for pi in (S.TS, S.UZ, S.METP):
+    for pi in (S.TS, S.UZ, S.METP, S.CZ):
         _, ys, _, _, _, _ = _run(pi, P, d, s, causal=False)
         assert _rel(shard.unshard_act(ys), y_ref) < 1e-12
 
@@ -85,6 +85,10 @@ def test_comm_signatures_and_bytes_c1():
          {"AllGather": 8, "AllToAll": 4, "ReduceScatter": 4, "AllReduce": 1}),
         (S.METP, {"AllGather": 4, "ReduceScatter": 4},     # c = P = 2 waves
          {"AllGather": 12, "ReduceScatter": 8, "AllReduce": 1}),
+        # CZ: 6 weight AGs (W_qkv^T in its Q, K, V parts) + AG(QKV) per pass; bwd adds
+        # RS(dQKV) and the 6 fp32 dW reduce-scatters
+        (S.CZ, {"AllGather": 7},
+         {"AllGather": 14, "ReduceScatter": 7, "AllReduce": 1}),
     ]:
         g, _, _, _, _, flog = _run(pi, P, d, s)
         assert _signature(flog) == Counter(fwd_sig), pi
@@ -105,7 +109,7 @@ def test_switched_chain_equals_stack(P):
     x = layers[0]["x"]
     dy = layers[0]["dy"]
     for trial in range(3):
-        plan = list(rng.integers(0, 3, size=Ln))
+        plan = list(rng.integers(0, 4, size=Ln))
         # dense stack
         yd = x
         caches = []
@@ -147,7 +151,7 @@ def test_switched_chain_equals_stack(P):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4])
-@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP])
+@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ])
 def test_ledger_equals_memory_model(pi, P):
     # the ledger recount of saved tensors equals the analytic formula
     s = 32
