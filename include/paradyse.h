@@ -56,9 +56,11 @@ typedef enum {
 typedef enum {
   PDS_MEGATRON_TS = 0,     /* Megatron-LM TP+SP                    */
   PDS_ULYSSES_Z = 1,       /* DeepSpeed Ulysses + ZeRO3 weight gathering*/
-  PDS_METP = 2             /* METP-style chunked, memory-bounded (R-11)  */
+  PDS_METP = 2,            /* METP-style chunked, memory-bounded (R-11)  */
+  PDS_MEGATRON_CZ = 3      /* Megatron-LM CP + ZeRO3: context-parallel attention over
+                              the all-gathered Q/K/V (reading R-CZ)     */
 } pds_strategy;
-#define PDS_N_STRATEGIES 3
+#define PDS_N_STRATEGIES 4
 
 /* pds_plan flags */
 #define PDS_PLAN_INFEASIBLE 1u  /* no plan satisfies Eq. 6; least-memory fallback returned */
@@ -278,6 +280,19 @@ pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads,
 pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
                           const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                           int32_t causal, void* dqkv, void* stream);
+/* Context-parallel attention (MegatronCZ): the query rows [qlo, qlo + qn) of the s
+ * positions of qkv [s][ld] against every key (causal: keys <= the query position).
+ * out [qn][ld_out] and lse fp32 [heads][qn] hold the local rows.  Backward: from the
+ * local out / lse / dout, dQ of rows [qlo, qlo + qn) and the dK / dV contributions of
+ * those queries to every key row, into dqkv [s][ld]; under the causal mask key rows
+ * >= qlo + qn are not written (the caller zeroes dqkv first).  qlo, qn multiples of
+ * 128, qlo + qn <= s, else PDS_EINVAL. */
+pds_status pds_k_attn_fwd_rows(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
+                               int32_t causal, int32_t qlo, int32_t qn, void* out, int64_t ld_out,
+                               void* lse, void* stream);
+pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                               const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
+                               int32_t causal, int32_t qlo, int32_t qn, void* dqkv, void* stream);
 
 const char* pds_last_error(void);
 const char* pds_version(void);

@@ -13,8 +13,9 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDS_LIB") or os.path.join(HERE, "libparadyse.so")   # PDS_LIB: A/B builds
 
-TS, UZ, METP = 0, 1, 2
-STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP"}
+TS, UZ, METP, CZ = 0, 1, 2, 3
+STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ"}
+N_STRATEGIES = 4
 
 STATUS = {0: "PDS_OK", -1: "PDS_EINVAL", -2: "PDS_EDIVISIBILITY", -3: "PDS_ESTRATEGY", -4: "PDS_ENOMEM",
           -5: "PDS_ECUDA", -6: "PDS_ENCCL", -7: "PDS_ESTATE", -8: "PDS_ENOCOSTS", -9: "PDS_ENOTIMPL"}
@@ -139,6 +140,10 @@ _SIGS = {
                        C.c_int64, C.c_void_p, C.c_void_p],
     "pds_k_attn_bwd": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
                        C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
+    "pds_k_attn_fwd_rows": [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                            C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
+    "pds_k_attn_bwd_rows": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
+                            C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
     "pds_last_error": [],
     "pds_version": [],
 }
@@ -253,9 +258,9 @@ class Context:
         return list(out), fl.value
 
     def cost_eval(self, s):
-        t = (C.c_double * 3)()
-        m = (C.c_double * 3)()
-        b = (C.c_int32 * 3)()
+        t = (C.c_double * N_STRATEGIES)()
+        m = (C.c_double * N_STRATEGIES)()
+        b = (C.c_int32 * N_STRATEGIES)()
         call("pds_cost_eval", self.h, s, t, m, b)
         return list(t), list(m), list(b)
 
@@ -340,3 +345,11 @@ def k_attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, stream=0):
 
 def k_attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream=0):
     call("pds_k_attn_bwd", qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream)
+
+
+def k_attn_fwd_rows(qkv, ld, s, heads, d, causal, qlo, qn, out, ld_out, lse, stream=0):
+    call("pds_k_attn_fwd_rows", qkv, ld, s, heads, d, causal, qlo, qn, out, ld_out, lse, stream)
+
+
+def k_attn_bwd_rows(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, qlo, qn, dqkv, stream=0):
+    call("pds_k_attn_bwd_rows", qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, qlo, qn, dqkv, stream)

@@ -124,6 +124,28 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
   return r;
 }
 
+extern "C" pds_status pds_k_attn_fwd_rows(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
+                                          int32_t causal, int32_t qlo, int32_t qn, void* out, int64_t ld_out,
+                                          void* lse, void* stream) {
+  if (!qkv || !out || !lse) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_fwd_rows(qkv, ld, s, heads, d, causal, qlo, qn, out, ld_out, lse,
+                            static_cast<cudaStream_t>(stream)), "pds_k_attn_fwd_rows");
+}
+
+extern "C" pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                                          const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
+                                          int32_t causal, int32_t qlo, int32_t qn, void* dqkv, void* stream) {
+  if (!qkv || !out || !lse || !dout || !dqkv) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  if (qn <= 0 || qn % 128) PDS_FAIL(PDS_EINVAL, "qn must be a positive multiple of 128");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* dd = nullptr;
+  PDS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dd), (size_t)heads * qn * 4, st));
+  pds_status r = rc2s(attn_bwd_rows(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, qlo, qn, dqkv, nullptr,
+                                    dd, st), "pds_k_attn_bwd_rows");
+  cudaFreeAsync(dd, st);
+  return r;
+}
+
 extern "C" pds_status pds_debug_trace(int64_t* host_out, int32_t rows) {
   if (!host_out || rows <= 0 || rows > 4096) PDS_FAIL(PDS_EINVAL, "bad trace buffer");
   const int rc = attn_debug_trace(reinterpret_cast<long long*>(host_out), rows);

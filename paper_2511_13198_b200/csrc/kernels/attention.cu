@@ -549,7 +549,7 @@ static int fwd_t(const void* qkv, int64_t ld, int s, int heads, int causal, void
 }
 
 int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-                void* lse, cudaStream_t st);
+                void* lse, cudaStream_t st, int qlo = 0, int qn = -1);
 
 // warp-level mma.sync FA2 forward (round-1 baseline, kept for A/B: PDS_ATTN_FWD=sync)
 int attn_fwd_sync(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out,
@@ -602,7 +602,8 @@ int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, v
 }
 
 int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
-                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st);
+                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo = 0,
+                int qn = -1);
 
 // Dd: fp32 scratch [heads][s]
 int attn_bwd_sync(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
@@ -627,6 +628,25 @@ int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const
                                                           reinterpret_cast<const __nv_bfloat16*>(dout), s, heads,
                                                           d, Dd);
   return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st);
+}
+
+// Context parallelism (MegatronCZ): queries [qlo, qlo + qn) of the s positions against
+// all keys of qkv [s][ld]; out [qn][ld_out], lse / Dd [heads][qn] local.  Backward:
+// dQ rows [qlo, qlo + qn) and the dK / dV contributions of those queries to every key
+// row into dqkv [s][ld] (key blocks past the last query, causal, are not written).
+int attn_fwd_rows(const void* qkv, int64_t ld, int s, int heads, int d, int causal, int qlo, int qn, void* out,
+                  int64_t ld_out, void* lse, cudaStream_t st) {
+  return attn_fwd_tc(qkv, ld, s, heads, d, causal, out, ld_out, lse, st, qlo, qn);
+}
+
+int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
+                  const void* dout, int s, int heads, int d, int causal, int qlo, int qn, void* dqkv,
+                  const void* rope, float* Dd, cudaStream_t st) {
+  if (qn % 128 || qn <= 0) return (int)cudaErrorInvalidValue;
+  attn_bwd_dot_kernel<<<(qn * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
+                                                           reinterpret_cast<const __nv_bfloat16*>(dout), qn, heads,
+                                                           d, Dd);
+  return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, qlo, qn);
 }
 
 }  // namespace pds

@@ -173,7 +173,7 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int heads, int causal,
                        __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
-                       float scale_log2) {
+                       float scale_log2, int qlo, int qn) {
   using C = Fwd2Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -188,11 +188,13 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = (s + 255) / 256;
+  // query rows [qlo, qlo + qn) of the s positions (context parallelism; default all):
+  // out / lse are indexed by the local row (row - qlo)
+  const int nqb = (qn + 255) / 256;
   const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int head = blockIdx.y;
   const int hq = heads * D;
-  const int q0 = qb * 256;
+  const int q0 = qlo + qb * 256;
   const int nkv = causal ? min(s, q0 + 256) / BN : s / BN;
 
   if (warp == 0 && lane == 0) {
@@ -395,8 +397,8 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(&o_done[tile], 0);
     tc_fence_after();
     const float inv = 1.0f / l;
-    const bool ok = row < s;
-    __nv_bfloat16* o = out + (int64_t)row * ld_out + head * D;
+    const bool ok = row < qlo + qn;
+    __nv_bfloat16* o = out + (int64_t)(row - qlo) * ld_out + head * D;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t r[32];
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(384, 1)
                              pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
       }
     }
-    if (ok) lse[(int64_t)head * s + row] = (m_used + log2f(l)) * LN2;
+    if (ok) lse[(int64_t)head * qn + (row - qlo)] = (m_used + log2f(l)) * LN2;
   }
   tc_fence_before();
   __syncthreads();
@@ -511,7 +513,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     attn_bwd_dkdv4_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq,
                           const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
-                          int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2) {
+                          int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2, int qlo,
+                          int qn) {
   using C = BwdKV4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -531,8 +534,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   const int kb = blockIdx.x, head = blockIdx.y;
   const int hq = heads * D;
   const int k0 = kb * 128;
-  const int qstart = causal ? kb : 0;
-  const int nq = s / 128 - qstart;
+  // only the query blocks of [qlo, qlo + qn) contribute (dO, LSE, D are local to them);
+  // the launch covers only key blocks that have at least one
+  const int qstart = max(causal ? kb : 0, qlo / 128);
+  const int nq = (qlo + qn) / 128 - qstart;
   constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
 
   if (warp == 0 && lane == 0) {
@@ -571,10 +576,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         mbar_arrive_expect_tx(&q_full[b], 2 * C::T + 1024);
         for (int a = 0; a < D / 64; ++a) {
           tma_load_2d(sm + C::Q_OFF + b * C::T + a * 16384, &tq, &q_full[b], head * D + a * 64, q0);
-          tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &q_full[b], head * D + a * 64, q0);
+          tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &q_full[b], head * D + a * 64, q0 - qlo);
         }
-        bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)head * s + q0, 512, &q_full[b]);
-        bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)head * s + q0, 512, &q_full[b]);
+        bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)head * qn + (q0 - qlo), 512, &q_full[b]);
+        bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)head * qn + (q0 - qlo), 512, &q_full[b]);
       }
     }
   } else if (warp == 1) {
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       const int b = i % NST;
       const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * CW * 4;
       const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * CW * 4;
-      const bool diag = causal && i == 0;
+      const bool diag = causal && qstart + i == kb;     // the query block on the key block's diagonal
       float p[CW];
       {
         uint32_t sr[CW / 32][32];
@@ -808,7 +813,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     attn_bwd_dq4_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
                         int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
                         const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
-                        const float2* __restrict__ rope, float scale, float scale_log2) {
+                        const float2* __restrict__ rope, float scale, float scale_log2, int qlo, int qn) {
   using C = BwdQ4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -825,12 +830,12 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   uint64_t* ds_half = bar + 2 * NST + 6;  // first half of every warpgroup's dS columns written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = s / 128;
-  const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  const int nqb = qn / 128;                 // local query blocks of [qlo, qlo + qn)
+  const int qb = qlo / 128 + (causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x);
   const int head = blockIdx.y;
   const int hq = heads * D;
   const int q0 = qb * 128;
-  const int nkv = causal ? qb + 1 : nqb;
+  const int nkv = causal ? qb + 1 : s / 128;
   constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
 
   if (warp == 0 && lane == 0) {
@@ -948,15 +953,15 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     const int row = q0 + t;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     if (wg == 0) row_to_tmem<D>(lb, Q_COL, qkv + (int64_t)row * ld + head * D, true);
-    else if (wg == 1) row_to_tmem<D>(lb, O_COL, dout + (int64_t)row * ld_out + head * D, true);
+    else if (wg == 1) row_to_tmem<D>(lb, O_COL, dout + (int64_t)(row - qlo) * ld_out + head * D, true);
     if (wg < 2) {
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(q_ready);
     }
-    const float nl2 = -lse[(int64_t)head * s + row] * LOG2E;
-    const float dd = Dd[(int64_t)head * s + row];
+    const float nl2 = -lse[(int64_t)head * qn + (row - qlo)] * LOG2E;
+    const float dd = Dd[(int64_t)head * qn + (row - qlo)];
     const uint32_t c_s = lb + S_COL + CW * wg, c_d = lb + DP_COL + CW * wg;
     for (int j = 0; j < nkv; ++j) {
       const bool diag = causal && j == nkv - 1;
@@ -1084,7 +1089,7 @@ int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
 
 template <int D>
 static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, void* out, int64_t ld_out,
-                    void* lse, cudaStream_t st) {
+                    void* lse, int qlo, int qn, cudaStream_t st) {
   CUtensorMap tm;
   int rc = make_map_rows(&tm, qkv, (uint64_t)3 * heads * D, (uint64_t)s, (uint64_t)ld);
   if (rc) return rc;
@@ -1094,17 +1099,18 @@ static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, v
     once = true;
   }
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
-  attn_fwd_tc_kernel<D><<<dim3((s + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
+  attn_fwd_tc_kernel<D><<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
       tm, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
-      scale_log2);
+      scale_log2, qlo, qn);
   return (int)cudaGetLastError();
 }
 
 int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-                void* lse, cudaStream_t st) {
-  if (s % 128 || (ld % 8)) return (int)cudaErrorInvalidValue;
-  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
-  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, heads, causal, out, ld_out, lse, st);
+                void* lse, cudaStream_t st, int qlo, int qn) {
+  if (qn < 0) qn = s;
+  if (s % 128 || (ld % 8) || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s) return (int)cudaErrorInvalidValue;
+  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, heads, causal, out, ld_out, lse, qlo, qn, st);
+  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, heads, causal, out, ld_out, lse, qlo, qn, st);
   return (int)cudaErrorInvalidValue;
 }
 
@@ -1113,11 +1119,11 @@ int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal
 namespace pds {
 template <int D>
 static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
-                    int s, int heads, int causal, void* dqkv, const void* rope, cudaStream_t st) {
+                    int s, int heads, int causal, void* dqkv, const void* rope, int qlo, int qn, cudaStream_t st) {
   const uint64_t cols = (uint64_t)3 * heads * D;
   CUtensorMap kv128, do128;
   int rc = make_map_rows(&kv128, qkv, cols, s, ld, 128);
-  rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, s, ld_out, 128);
+  rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, qn, ld_out, 128);
   if (rc) return (int)cudaErrorInvalidValue;
   // Elementwise warpgroups per CTA, measured under fixed clocks (ncu --clock-control
   // base, s = 16384): dK/dV 4 (4766 us vs 4792 with 2), dQ 2 (3408 us vs 3484 with 4).
@@ -1139,16 +1145,19 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   auto dkdv = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
     // the Q map is the K/V map (same buffer, same box): only the column offset differs
-    attn_bwd_dkdv4_kernel<D, NW><<<dim3(s / 128, heads), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
+    // causal: key blocks past the last local query get nothing (the caller zeroes them)
+    const int nkb = causal ? (qlo + qn) / 128 : s / 128;
+    attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
         kv128, kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
-        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2);
+        reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2,
+        qlo, qn);
   };
   auto dq = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
-    attn_bwd_dq4_kernel<D, NW><<<dim3(s / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
+    attn_bwd_dq4_kernel<D, NW><<<dim3(qn / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
         reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2);
+        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn);
   };
   if (force == 2) dkdv(std::integral_constant<int, 2>{});
   else dkdv(std::integral_constant<int, 4>{});
@@ -1159,10 +1168,12 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
 
 // dQ, dK, dV into dqkv (same [s][ld] layout as qkv); Dd = rowsum(dO o O) precomputed
 int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
-                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st) {
-  if (s % 128 || ld % 8 || ld_out % 8) return (int)cudaErrorInvalidValue;
-  if (d == 128) return bwd_tc_t<128>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, st);
-  if (d == 64) return bwd_tc_t<64>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, st);
+                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo, int qn) {
+  if (qn < 0) qn = s;
+  if (s % 128 || ld % 8 || ld_out % 8 || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s)
+    return (int)cudaErrorInvalidValue;
+  if (d == 128) return bwd_tc_t<128>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, qlo, qn, st);
+  if (d == 64) return bwd_tc_t<64>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, qlo, qn, st);
   return (int)cudaErrorInvalidValue;
 }
 }  // namespace pds

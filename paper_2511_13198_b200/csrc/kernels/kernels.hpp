@@ -10,6 +10,12 @@ int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, v
              void* lse, cudaStream_t st);
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
              int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st);
+// context parallelism: queries [qlo, qlo + qn) against all s keys (attention.cu)
+int attn_fwd_rows(const void* qkv, int64_t ld, int s, int heads, int d, int causal, int qlo, int qn, void* out,
+                  int64_t ld_out, void* lse, cudaStream_t st);
+int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
+                  const void* dout, int s, int heads, int d, int causal, int qlo, int qn, void* dqkv,
+                  const void* rope, float* Dd, cudaStream_t st);
 int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps, void* x1_out,
                 void* u_out, void* rstd, cudaStream_t st);
 int rmsnorm_bwd_grid(int64_t rows);

@@ -67,7 +67,7 @@ struct pds_ctx {
   // planner
   Bundle bundle;
   double capacity = 0, gamma = 0;
-  uint32_t enabled = 0x7;
+  uint32_t enabled = (1u << PDS_N_STRATEGIES) - 1;
   std::map<std::pair<int, int64_t>, std::pair<std::vector<uint8_t>, bool>> cache;
   std::vector<uint8_t> prev;
   // debug taps
@@ -301,6 +301,23 @@ struct Exec {
     const double fl = 4.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
     Prof p(c, st, K_ATTN_F, fl, 0);
     return kerr(attn_fwd(qkv, 3 * hl, (int)s, (int)nl, (int)d, m.causal, out, hl, lse, st), "attn_fwd");
+  }
+  // context parallelism (CZ): this rank's query rows [r s/P, (r+1) s/P) of all n heads
+  // against every key of the all-gathered qkv [s][3h]
+  double cz_fl(double mult) const {
+    const double q0 = (double)r * sl;
+    return mult * m.h * (m.causal ? sl * (q0 + 0.5 * sl) : (double)sl * s);
+  }
+  pds_status attn_rows_f(const void* qkvg, void* out, void* lse) {
+    Prof p(c, st, K_ATTN_F, cz_fl(4.0), 0);
+    return kerr(attn_fwd_rows(qkvg, 3 * h, (int)s, (int)m.n_heads, (int)d, m.causal, (int)(r * sl), (int)sl, out, h,
+                              lse, st), "attn_fwd_rows");
+  }
+  pds_status attn_rows_b(const void* qkvg, const void* out, const void* lse, const void* dout, void* dqkvf,
+                         float* dd) {
+    Prof p(c, st, K_ATTN_B, cz_fl(10.0), 0);
+    return kerr(attn_bwd_rows(qkvg, 3 * h, out, h, lse, dout, (int)s, (int)m.n_heads, (int)d, m.causal,
+                              (int)(r * sl), (int)sl, dqkvf, c->rope, dd, st), "attn_bwd_rows");
   }
   pds_status attn_b(const void* qkv, const void* out, const void* lse, const void* dout, void* dqkv, float* dd) {
     const double fl = 10.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
@@ -658,6 +675,130 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(uz_dw(e, dw, 3 * e.h, g->dw_qkv_t));
   PDS_TRY(e.wait(e.st, ev_qkv));
   PDS_TRY(tn.xw(x4, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));
+  PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
+  return e.dgamma(dgl, g);
+}
+
+// ================================================================== MegatronCZ
+// Megatron-LM CP + ZeRO3 (reading R-CZ): ZeRO3 weight gathers
+// as in UlyssesZ, every GEMM local on the rank's s/P rows, the context-parallel
+// attention over the all-gathered Q/K/V for the rank's own query rows, and in backward
+// a reduce-scatter of the dQ/dK/dV partials.  W_qkv^T is gathered part by part (the
+// Q, K, V rows of every spec shard) into [Q all; K all; V all], so one attention
+// launch covers all heads; its gradient is reduce-scattered part by part back into
+// the spec layout.
+pds_status cz_wqkv(Exec& e, const pds_weights* w, char* wqkv, cudaStream_t on) {
+  for (int i = 0; i < 3; ++i)
+    PDS_TRY(on == e.st ? e.ag(static_cast<const char*>(w->w_qkv_t) + i * e.hl * e.h * 2, wqkv + i * e.h * e.h * 2, e.hl * e.h)
+                       : e.ag_on(on, static_cast<const char*>(w->w_qkv_t) + i * e.hl * e.h * 2, wqkv + i * e.h * e.h * 2,
+                                 e.hl * e.h));
+  return PDS_OK;
+}
+
+pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
+  const BufPlan& bp = sv->plan;
+  const cudaStream_t cs = e.side_stream();
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* u1 = ws + bp.ws_off("u1");
+  char* qkvg = ws + bp.ws_off("qkvg");
+  char* v2 = ws + bp.ws_off("v2");
+  char* f0 = ws + bp.ws_off("f0");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
+  PDS_TRY(e.link(e.st, cs));                 // gather buffers free (previous layer done with them)
+  PDS_TRY(cz_wqkv(e, w, wqkv, e.st));
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * e.h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * e.h));
+  cudaEvent_t ev_ffn = e.mark(cs);
+  PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
+  // local Q/K/V of all heads ([Q | K | V] column blocks of h), RoPE at global positions
+  PDS_TRY(e.gemm(e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, 3 * e.h, e.h, sv->at("qkv"), 3 * e.h), e.h, 0, 0,
+                        e.r * e.sl)));
+  PDS_TRY(e.ag(sv->at("qkv"), qkvg, e.sl * 3 * e.h));                                   // AG(QKV)
+  PDS_TRY(e.attn_rows_f(qkvg, sv->at("a"), sv->at("lse")));                              // own queries
+  PDS_TRY(e.wait(e.st, ev_proj));
+  PDS_TRY(tn.xw(sv->at("a"), e.h, wproj, e.h, e.sl, e.h, e.h, u1, e.h));                // O
+  PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
+  PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), v2, sv->at("rstd2")));
+  PDS_TRY(e.wait(e.st, ev_ffn));
+  GemmArgs fc1 = Exec::G(v2, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
+  fc1.aux_out = f0; fc1.ld_aux = e.F;
+  PDS_TRY(e.gemm(fc1));
+  PDS_TRY(tn.xw(f0, e.F, wout, e.h, e.sl, e.h, e.F, u1, e.h));                          // Z
+  PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * e.h));
+  return e.add(sv->at("x1"), u1, y, e.sl * e.h);
+}
+
+pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
+                  char* ws) {
+  const BufPlan& bp = sv->plan;
+  const cudaStream_t cs = e.side_stream();
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* dw = ws + bp.ws_off("dw");
+  char* u1 = ws + bp.ws_off("u1");
+  char* qkvg = ws + bp.ws_off("qkvg");
+  char* dqkvf = ws + bp.ws_off("dqkvf");
+  char* f0 = ws + bp.ws_off("f0");
+  char* f1 = ws + bp.ws_off("f1");
+  char* v2 = ws + bp.ws_off("v2");
+  char* da = ws + bp.ws_off("da");
+  float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
+  float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
+  float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
+  PDS_TRY(e.link(e.st, cs));
+  PDS_TRY(e.ag(w->w_out, wout, e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * e.h));
+  cudaEvent_t ev_in = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * e.h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(cz_wqkv(e, w, wqkv, cs));
+  cudaEvent_t ev_qkv = e.mark(cs);
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  // FFN: local with full weights (as UlyssesZ)
+  GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;                                 // G^T, dH^T
+  PDS_TRY(e.gemm(dgel));
+  PDS_TRY(tn.tr(dy, e.h, e.sl, e.h, tn.tb));
+  PDS_TRY(tn.mm(tn.ta, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));           // dW_out (full, local)
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
+  PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
+  PDS_TRY(tn.tr(u1, e.h, e.sl, e.h, tn.tb));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));              // dW_in^T (full, local)
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(e.wait(e.st, ev_in));
+  PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
+  PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
+  PDS_TRY(e.wait(e.st, ev_proj));
+  PDS_TRY(e.gemm(Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, da, e.h)));        // dA = dX1 W_proj^T
+  PDS_TRY(tn.dw(sv->at("a"), e.h, dx, e.h, e.sl, e.h, e.h, dw, EPI_F32));
+  PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
+  // attention: re-gather the context's Q/K/V; this rank's queries give dQ of its rows
+  // and dK / dV contributions to every key row; RS sums those over ranks
+  PDS_TRY(e.ag(sv->at("qkv"), qkvg, e.sl * 3 * e.h));                                   // AG(QKV)
+  PDS_CUDA(cudaMemsetAsync(dqkvf, 0, e.s * 3 * e.h * 2, e.st));
+  PDS_TRY(e.attn_rows_b(qkvg, sv->at("a"), sv->at("lse"), da, dqkvf, dd));
+  char* dqkv = dqkvf + e.r * e.sl * 3 * e.h * 2;
+  PDS_TRY(e.rs(dqkvf, dqkv, e.sl * 3 * e.h));                                           // RS(dQKV)
+  PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
+  PDS_TRY(tn.dw(dqkv, 3 * e.h, u1, e.h, e.sl, 3 * e.h, e.h, dw, EPI_F32));              // [Q; K; V] all rows
+  for (int i = 0; i < 3; ++i) {       // ZeRO3 RS part by part into the spec shard [Q_r; K_r; V_r]
+    char* part = dw + i * e.h * e.h * 4;
+    const int64_t cnt = e.hl * e.h;
+    char* mine = part + e.r * cnt * 4;
+    PDS_TRY(e.rs(part, mine, cnt, DT_F32));
+    PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + i * cnt * 4, cnt, e.st), "add_f32"));
+  }
+  PDS_TRY(e.wait(e.st, ev_qkv));
+  PDS_TRY(tn.xw(dqkv, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));                // dU
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -1034,6 +1175,7 @@ extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_le
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_fwd(e, x, w, y, sv.get(), c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_fwd(e, x, w, y, sv.get(), c->ws); break;
+    case PDS_MEGATRON_CZ: rc = cz_fwd(e, x, w, y, sv.get(), c->ws); break;
     default: rc = metp_fwd(e, x, w, y, sv.get(), c->ws); break;
   }
   c->tap_o = c->tap_z = nullptr;
@@ -1063,6 +1205,7 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_bwd(e, dy, saved, w, g, dx, c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_bwd(e, dy, saved, w, g, dx, c->ws); break;
+    case PDS_MEGATRON_CZ: rc = cz_bwd(e, dy, saved, w, g, dx, c->ws); break;
     default: rc = metp_bwd(e, dy, saved, w, g, dx, c->ws); break;
   }
   c->saved_live -= saved->bytes;
@@ -1201,7 +1344,7 @@ static pds_status costs(pds_ctx* c, int64_t s, double* t, double* mm, int* branc
 extern "C" pds_status pds_cost_eval(pds_ctx* c, int64_t s, double* t_layer, double* m_layer, int32_t* branch) {
   if (!c || !t_layer || !m_layer) PDS_FAIL(PDS_EINVAL, "NULL argument");
   double t[PDS_N_STRATEGIES], mm[PDS_N_STRATEGIES];
-  int br[PDS_N_STRATEGIES] = {0, 0, 0};
+  int br[PDS_N_STRATEGIES] = {};
   PDS_TRY(costs(c, s, t, mm, br, nullptr));
   for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
     t_layer[i] = t[i];

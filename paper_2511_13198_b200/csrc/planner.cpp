@@ -318,6 +318,35 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       if (full) push(p.ws, tw, "qkv", s * 3 * hl * 2);
       break;
     }
+    case PDS_MEGATRON_CZ: {
+      // saved: the local rows of TS's tensors (Q/K/V of all heads, A, LSE, H)
+      push(p.saved, ts, "rstd1", ell);
+      push(p.saved, ts, "qkv", sl * 3 * h * 2);
+      push(p.saved, ts, "a", u);
+      push(p.saved, ts, "lse", lam);
+      push(p.saved, ts, "x1", u);
+      push(p.saved, ts, "rstd2", ell);
+      push(p.saved, ts, "h", sl * F * 2);
+      push(p.ws, tw, "wqkv", 3 * h * h * 2);      // [Q all; K all; V all] rows
+      push(p.ws, tw, "wproj", h * h * 2);
+      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "wout", F * h * 2);
+      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "u1", u);
+      push(p.ws, tw, "qkvg", s * 3 * h * 2);      // all-gathered Q/K/V of the context
+      push(p.ws, tw, "dqkvf", s * 3 * h * 2);     // dQ/dK/dV partials of all rows (RS in place)
+      push(p.ws, tw, "f0", sl * F * 2);
+      push(p.ws, tw, "f1", sl * F * 2);
+      push(p.ws, tw, "v2", u);
+      push(p.ws, tw, "da", u);
+      push(p.ws, tw, "dd", lam);
+      push(p.ws, tw, "dgp", dgp);
+      push(p.ws, tw, "dgl", 2 * h * 4);
+      push(p.ws, tw, "ta", std::max(3 * h, F) * sl * 2);
+      push(p.ws, tw, "tb", h * sl * 2);
+      push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
+      break;
+    }
     default:
       PDS_FAIL(PDS_ESTRATEGY, "unknown strategy id " + std::to_string(strategy));
   }

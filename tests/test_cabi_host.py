@@ -81,7 +81,7 @@ def test_plan_ex_worked_examples(B):
 def test_mem_bytes_vs_oracle(B, cfg):
     h, n, F, s, P = cfg
     m = B.Model(h=h, n_heads=n, ffn=F)
-    for pi in (0, 1, 2):
+    for pi in (0, 1, 2, 3):
         c = P
         if pi == 2 and (s // P) % c == 0 and (s // P // c) % 128:
             continue

@@ -39,7 +39,7 @@ def _inputs(s, seed):
 
 
 @pytest.mark.parametrize("s", [4096])
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_fullsize_sampled(s, pi):
     d = _inputs(s, 11 + pi)
     R = np.array([5, 700, 1500, s // 2 + 3, s - 700, s - 2, s - 1]) if pi == 0 else np.array([3, 1024, s // 2 + 11, s - 129])

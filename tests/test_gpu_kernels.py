@@ -317,3 +317,51 @@ def test_gemm_store_counters_gate_chunk_reads(M, N, K, chunk, rot):
     assert torch.equal(got.view(torch.int16), out.cpu().view(torch.int16))
     assert ctr.cpu().tolist() == [chunk * N] * nch
     assert rel(host(out), A.astype(np.float64) @ W.T) < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [1, 0])
+@pytest.mark.parametrize("s,qn", [(1024, 256), (768, 384)])   # 384: the 256-row forward tiles straddle ranks
+def test_attention_query_rows(d, causal, s, qn):
+    """Context-parallel attention (MegatronCZ): every rank's query rows against all keys;
+    the forward rows are the full attention's, and the per-rank dQ / dK / dV
+    contributions sum to the full backward."""
+    heads = 2
+    hq = heads * d
+    qkv = _mat(7 + d, 1, (s, 3 * hq))
+    dout = _mat(7 + d, 2, (s, hq))
+    tq, tdo = dev_bf16(qkv), dev_bf16(dout)
+    ref_o = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+    ref_l = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+    B.k_attn_fwd(tq.data_ptr(), 3 * hq, s, heads, d, causal, ref_o.data_ptr(), hq, ref_l.data_ptr(), stream())
+    acc = torch.zeros(s, 3 * hq, dtype=torch.float32, device="cuda")
+    o_rows = []
+    for qlo in range(0, s, qn):
+        out = torch.empty(qn, hq, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(heads, qn, dtype=torch.float32, device="cuda")
+        B.k_attn_fwd_rows(tq.data_ptr(), 3 * hq, s, heads, d, causal, qlo, qn, out.data_ptr(), hq, lse.data_ptr(),
+                          stream())
+        torch.cuda.synchronize()
+        if qlo % 256 == 0:      # same 256-row tiles as the full launch: the same arithmetic
+            assert torch.equal(out.view(torch.int16), ref_o[qlo:qlo + qn].view(torch.int16)), qlo
+        else:
+            assert rel(host(out), host(ref_o[qlo:qlo + qn])) < 2e-3, qlo
+        assert torch.allclose(lse, ref_l[:, qlo:qlo + qn], rtol=0, atol=1e-4), qlo
+        o_rows.append(out)
+        dq = torch.zeros(s, 3 * hq, dtype=torch.bfloat16, device="cuda")
+        B.k_attn_bwd_rows(tq.data_ptr(), 3 * hq, out.data_ptr(), hq, lse.data_ptr(), tdo[qlo:qlo + qn].data_ptr(),
+                          s, heads, d, causal, qlo, qn, dq.data_ptr(), stream())
+        torch.cuda.synchronize()
+        acc += dq.float()
+    g = host(acc)
+    o_gpu = host(torch.cat(o_rows))
+    for hh in range(heads):
+        q = qkv[:, hh * d:(hh + 1) * d]
+        k = qkv[:, hq + hh * d:hq + (hh + 1) * d]
+        v = qkv[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d]
+        _, l = OL.attention_fwd(q, k, v, causal=bool(causal))
+        dqr, dkr, dvr = OL.attention_bwd(q, k, v, o_gpu[:, hh * d:(hh + 1) * d], l, dout[:, hh * d:(hh + 1) * d],
+                                         causal=bool(causal))
+        assert rel(g[:, hh * d:(hh + 1) * d], dqr) < 1e-2
+        assert rel(g[:, hq + hh * d:hq + (hh + 1) * d], dkr) < 1e-2
+        assert rel(g[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d], dvr) < 1e-2

@@ -132,25 +132,25 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0):
     return res
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_p1_c1(pi):
     # C1 shapes (h=256, n=4, d=64, F=1024, s=512), P = 1: every strategy degenerates
     _check_layer(pi, 1, 256, 4, 1024, 512)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_p2_c1(pi):
     # C1 at P = 2 (the configs[0] case), METP with c = 2 waves
     _check_layer(pi, 2, 256, 4, 1024, 512)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_p4_d128(pi):
     # d = 128 heads, P = 4, METP c = 2 waves of 128 rows per rank
     _check_layer(pi, 4, 1024, 8, 4096, 1024, chunks=2)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_bert_shape_noncausal(pi):
     # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
     _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
@@ -221,7 +221,7 @@ def test_overlap_bit_identical(pi, P, h, n, F, s, chunks):
 def test_switched_chain_p2():
     # a 4-layer stack with a switched plan; boundary tensors pass unchanged (R-31)
     P, h, n, F, s = 2, 256, 4, 1024, 512
-    plan = [2, 0, 1, 2]
+    plan = [2, 0, 3, 1]
     layers = [layer_inputs(h, n, F, s, 1, seed=5, layer=i) for i in range(4)]
     yd = layers[0]["x"]
     caches = []
