@@ -138,21 +138,33 @@ def comm_bytes_per_rank(pi, h, F, s, P):
     act = s * h * 2
     if pi in (0, 2):
         return 10 * fr * act + 2 * fr * 8 * h
-    a2a = 2 * fr * (s // P) * 4 * h * 2
     wb = 4 * h * h + 2 * h * F
+    if pi == 3:              # CZ: AG(QKV) fwd + re-gather bwd + RS(dQKV), ZeRO3 weights
+        return 3 * fr * 3 * act + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+    a2a = 2 * fr * (s // P) * 4 * h * 2
     return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+
+
+def attention_seconds(torch, B, ctx, pi, s, w, gr, x, dy):
+    """Device time of the attention kernels in one layer fwd + bwd (library profiler)."""
+    ctx.profile(True)
+    ctx.profile_reset()
+    time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0)
+    ms = ctx.profile_read(1)["ms"] + ctx.profile_read(2)["ms"]
+    ctx.profile(False)
+    return ms / 1e3
 
 
 def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.0):
     import torch
     from . import binding as B
     model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L)
-    records = {0: [], 1: [], 2: []}
+    records = {0: [], 1: [], 2: [], 3: []}
     if P_target == 1:
         ctx = B.Context(model)
         for s in grid:
             w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
-            for pi in (0, 1, 2):
+            for pi in (0, 1, 2, 3):
                 t = time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=reps)
                 records[pi].append((int(s), t))
                 print(f"P=1 s={s} pi={pi} t={t * 1e3:.3f} ms", flush=True)
@@ -169,16 +181,25 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx_m = B.Context(B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, metp_chunks=P_target))
         for s in grid:
             t_unit = {}
-            for pi in (0, 1, 2):
+            t_att = 0.0
+            for pi in (0, 1, 2, 3):
                 w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
                 t1 = time_layer(torch, B, ctx_m if pi == 2 else ctx, pi, s, w, gr, x, dy, reps=reps)
                 t_unit[pi] = t1
+                if pi == 3:
+                    t_att = attention_seconds(torch, B, ctx, pi, s, w, gr, x, dy)
                 del w, gr, x, dy
             torch.cuda.empty_cache()
-            for pi in (0, 1, 2):
+            for pi in (0, 1, 2, 3):
                 comp = t_unit[pi] / P
+                if pi == 3 and model.causal:
+                    # contiguous context chunks: the last rank's queries see every key, so
+                    # its causal attention share is (2P - 1) / P^2 instead of 1 / P
+                    comp += t_att * ((2 * P - 1) / (P * P) - 1.0 / P)
                 comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
                 extra = (2 * P - 1) * 8e-6 * (P if pi == 2 else 1)   # collective launch latency
+                if pi == 3:
+                    extra += 6 * 8e-6 * (P - 1)                           # part-wise weight AG / RS
                 records[pi].append((int(s), comp + comm + extra))
         ctx.close()
         ctx_m.close()

@@ -4,10 +4,11 @@ The library's strategies assume NCCL's collective conventions: AllGather
 concatenates in rank order (in place: rank r's send buffer is slot r of the
 receive buffer), ReduceScatter hands chunk r of the sum to rank r (in place:
 the output is slot r of the input), All-to-All sends block j to rank j and
-receives rank j's block in slot j.  These tests run the MegatronTS and UlyssesZ
-forward dataflow of csrc/layer.cpp in two real processes with torch.distributed
+receives rank j's block in slot j.  These tests run the MegatronTS, UlyssesZ and
+MegatronCZ forward dataflow of csrc/layer.cpp in two / four real processes with torch.distributed
 (gloo, fp64) using exactly those conventions, and compare with the oracle's
-unsharded layer.  They also cover the bench's host logic: NCCL-uid broadcast via
+unsharded layer, and the pairwise-step schedule of the tile-overlapped AG / RS
+(comm.cpp) against the plain collectives.  They also cover the bench's host logic: NCCL-uid broadcast via
 broadcast_object_list, max-over-ranks timing, and that every rank's planner
 returns the same plan (Algorithm 1 is deterministic).
 """
@@ -119,6 +120,42 @@ def _worker(rank, P, port, q):
         afull = torch.cat(back, 1)                              # unpack: slot j = group j columns
         x1u = x + afull @ wpf
         y_uz = x1u + gelu(_rmsnorm(x1u, g2) @ wif.T) @ wof
+        # ---- MegatronCZ forward (csrc/layer.cpp cz_fwd): W_qkv^T gathered part by part
+        # into [Q all; K all; V all], local QKV, AG(QKV), own query rows vs every key
+        wq_all = torch.cat([_ag(wq[i * hl:(i + 1) * hl].contiguous(), P) for i in range(3)], 0)
+        qkv_c = _ag(_rmsnorm(x, g1) @ wq_all.T, P)                # [s, 3h] of the whole context
+        a_c = _attn(qkv_c, N, d_, torch.arange(S))[rank * sl:(rank + 1) * sl]
+        x1c = x + a_c @ wpf
+        y_cz = x1c + gelu(_rmsnorm(x1c, g2) @ wif.T) @ wof
+        # ---- tile-overlapped TS collectives (comm.cpp all_gather_flagged /
+        # reduce_scatter_gated): P - 1 pairwise steps; AG step k sends the own chunk to
+        # rank - k and receives chunk rank + k; RS step k sends chunk rank + k to its
+        # owner and receives this rank's chunk from rank - k; then the rank-order sum
+        u_loc = _rmsnorm(x, g1)
+        ag = [None] * P
+        ag[rank] = u_loc
+        for k in range(1, P):
+            frm, to = (rank + k) % P, (rank - k) % P
+            buf = torch.empty_like(u_loc)
+            reqs = [dist.isend(u_loc.contiguous(), to), dist.irecv(buf, frm)]
+            for rq in reqs:
+                rq.wait()
+            ag[frm] = buf
+        ag_ok = torch.equal(torch.cat(ag, 0), U)
+        part = (a @ wp).contiguous()                            # [P][sl][h] partials
+        recv = [None] * P
+        for k in range(1, P):
+            to, frm = (rank + k) % P, (rank - k) % P
+            buf = torch.empty(sl, H, dtype=part.dtype)
+            reqs = [dist.isend(part[to * sl:(to + 1) * sl].contiguous(), to), dist.irecv(buf, frm)]
+            for rq in reqs:
+                rq.wait()
+            recv[frm] = buf
+        recv[rank] = part[rank * sl:(rank + 1) * sl]
+        rs_sum = recv[0].clone()
+        for j in range(1, P):
+            rs_sum += recv[j]
+        rs_ok = torch.allclose(rs_sum, o, rtol=0, atol=1e-12)
         # ---- bench host logic: uid broadcast, max over ranks, plan agreement
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -128,12 +165,12 @@ def _worker(rank, P, port, q):
         plan, _ = B.plan_ex(32, [1.0, 1.5, 3.0], [5.0, 4.0, 1.0], [1, 1, 1], 100.0)
         plans = [None] * P
         dist.all_gather_object(plans, plan)
-        q.put((rank, y_ts.numpy(), y_uz.numpy(), obj[0], float(t), plans))
+        q.put((rank, y_ts.numpy(), y_uz.numpy(), obj[0], float(t), plans, y_cz.numpy(), ag_ok, rs_ok))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P", [2])
+@pytest.mark.parametrize("P", [2, 4])
 def test_two_process_strategies_and_host_logic(P):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -151,7 +188,10 @@ def test_two_process_strategies_and_host_logic(P):
     y_uz = np.concatenate([r[2] for r in res])
     assert np.max(np.abs(y_ts - y_ref[:, 0])) < 1e-10
     assert np.max(np.abs(y_uz - y_ref[:, 0])) < 1e-10
+    y_cz = np.concatenate([r[6] for r in res])
+    assert np.max(np.abs(y_cz - y_ref[:, 0])) < 1e-10
     for r in res:
+        assert r[7] and r[8]                      # pairwise-step AG / RS = the collectives
         assert r[3] == bytes(range(128))          # NCCL uid broadcast
         assert r[4] == float(P)                   # max over ranks
         assert r[5][0] == r[5][1]                 # identical plans on every rank
