@@ -12,7 +12,7 @@ feasible plan (proactive OOM prediction).
 
 --ablation runs ParaDySe (full) = all strategies, RF + PR cost model, smoothing
 gamma = 0.05, and the variants w/o MegatronTS, w/o UlyssesZ, w/o
-METP (strategy set), w/o RF (PR everywhere: the bundle's s_profile_max set to 0,
+METP, w/o MegatronCZ (strategy set), w/o RF (PR everywhere: the bundle's s_profile_max set to 0,
 Eq. 9), w/o Smoothing (gamma = 0), and reports Table 5's columns:
   Seq_len   = largest length trained before OOM,
   Time      = cumulative device time of the variant,
@@ -170,7 +170,9 @@ def main():
     lens = sorted(min(int(pad_to(int(x), 128 * P)), a.cap_s) for x in lens)   # curriculum
     out = {"dataset": a.dataset, "n": a.n, "L": a.L, "P": P, "lengths": lens, "capacity_for_plan": cap, "runs": {}}
 
-    def context(mask=0x7, gamma=0.0, pr_only=False):
+    ALL = (1 << B.N_STRATEGIES) - 1
+
+    def context(mask=ALL, gamma=0.0, pr_only=False):
         ctx = B.Context(model)
         ctx.load_costs(pr_only_bundle(bundle) if pr_only else bundle)
         ctx.set_enabled(mask)
@@ -179,8 +181,9 @@ def main():
 
     out["timing"] = "per (s, plan): one untimed warm-up pass, then one timed fwd + bwd of the stack (memoised)"
     if a.ablation:
-        variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=0x6, gamma=0.05)),
-                    ("w/o UlyssesZ", dict(mask=0x5, gamma=0.05)), ("w/o METP", dict(mask=0x3, gamma=0.05)),
+        variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=ALL & ~1, gamma=0.05)),
+                    ("w/o MegatronCZ", dict(mask=ALL & ~8, gamma=0.05)),
+                    ("w/o UlyssesZ", dict(mask=ALL & ~2, gamma=0.05)), ("w/o METP", dict(mask=ALL & ~4, gamma=0.05)),
                     ("w/o RF", dict(gamma=0.05, pr_only=True)), ("w/o Smoothing", dict(gamma=0.0))]
         out["gamma_full"] = 0.05
         memo = {}
@@ -204,8 +207,8 @@ def main():
             print(row, flush=True)
     else:
         memo = {}
-        for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1)):
-            ctx = context(mask=0x7 if fixed is None else 1 << fixed, gamma=a.gamma)
+        for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1), ("MegatronCZ", 3)):
+            ctx = context(mask=ALL if fixed is None else 1 << fixed, gamma=a.gamma)
             out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, fixed, memo=memo)
             ctx.close()
             r = out["runs"][name]
