@@ -99,6 +99,7 @@ struct NcclComm : Comm {
       // GEMMs that poll for it leave that many SMs free (overlap_sm_reserve)
       ncclComm_t c2 = nullptr;
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.minCTAs = 1;
       cfg.maxCTAs = side_ctas();
       ncclResult_t r = ncclCommSplit(comm, 0, rank, &c2, &cfg);
       if (r != ncclSuccess) {

@@ -151,6 +151,13 @@ def test_layer_p4_d128(pi):
 
 
 @pytest.mark.parametrize("pi", [0, 1, 2, 3])
+def test_layer_p8(pi):
+    # eight ranks (the paper's node) on the loopback group: s/P = 128 rows,
+    # one head per rank; METP with c = 1 wave
+    _check_layer(pi, 8, 1024, 8, 4096, 1024, seed=8, chunks=1)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_bert_shape_noncausal(pi):
     # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
     _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
@@ -298,7 +305,7 @@ def test_step_host(pi):
     ctx.close()
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_nccl_one_rank_equals_self(pi):
     """The NCCL backend (a one-rank communicator: pds_create with P = 1 and a unique
     id) runs every collective of the strategy, METP's side-stream wave gathers on a
