@@ -169,7 +169,7 @@ def main():
     have_bundle = os.path.exists(bundle)
     if have_bundle:
         ctx.load_costs(bundle)
-    ctx.reserve(max(args.seqs), 0x7 if args.strategy < 0 else (1 << args.strategy))
+    ctx.reserve(max(args.seqs), (1 << B.N_STRATEGIES) - 1 if args.strategy < 0 else (1 << args.strategy))
 
     st = torch.cuda.current_stream()
     bufs = {}

@@ -236,7 +236,7 @@ class Context:
             lib().pds_destroy(self.h)
             self.h = None
 
-    def reserve(self, max_seq_len, mask=0x7):
+    def reserve(self, max_seq_len, mask=(1 << N_STRATEGIES) - 1):
         call("pds_reserve", self.h, max_seq_len, mask)
 
     def release_cache(self):
