@@ -97,7 +97,7 @@ def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None, memo=None):
             recs.append({"s": s, "oom": True})
             break
         cum += t
-        recs.append({"s": s, "plan": "".join("TUM"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
+        recs.append({"s": s, "plan": "".join("TUMC"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
     per_bucket = {}
     for r in recs:
         if r.get("oom"):
@@ -130,9 +130,9 @@ def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
         per_layer[pi] = t / n_short
     t_mixed = measure(torch, B, ctx, model, plan, s, layers, memo)
     pred = sum(per_layer[p] for p in plan)
-    return {"s": s, "plan": "".join("TUM"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
+    return {"s": s, "plan": "".join("TUMC"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
             "overhead": t_mixed / pred - 1.0,
-            "per_layer_s": {"TUM"[k]: v for k, v in per_layer.items()}}
+            "per_layer_s": {"TUMC"[k]: v for k, v in per_layer.items()}}
 
 
 def main():
