@@ -38,8 +38,8 @@ def _inputs(s, seed):
                 g1=g(H, std=0.1, mean=1.0), g2=g(H, std=0.1, mean=1.0), dyR=None)
 
 
-@pytest.mark.parametrize("s", [4096])
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("s,pi", [(4096, 0), (4096, 1), (4096, 2), (4096, 3),
+                                  (32768, 0)])      # the bench's longest length, its planned strategy
 def test_fullsize_sampled(s, pi):
     d = _inputs(s, 11 + pi)
     R = np.array([5, 700, 1500, s // 2 + 3, s - 700, s - 2, s - 1]) if pi == 0 else np.array([3, 1024, s // 2 + 11, s - 129])
