@@ -18,8 +18,9 @@
  *     the host unless stated.
  *   - Dtypes: activations / weights bf16; weight gradients fp32, ACCUMULATED (+=).
  *   - Boundary activation layout: [s/P, b, h] row-major bf16, rank r holding
- *     global positions [r*s/P, (r+1)*s/P) (reading R-10).  This build supports
- *     b = 1 (other b -> PDS_ENOTIMPL).
+ *     global positions [r*s/P, (r+1)*s/P) (reading R-10); token row t*b + j is
+ *     position t of sequence j.  b >= 1 independent equal-length sequences (no
+ *     attention across them, reading Q-35); b < 1 -> PDS_EINVAL.
  *   - Weight shards (spec layout, reading R-9), rank r of P, n heads, d = h/n, F = ffn:
  *       w_qkv_t [3h/P, h]  rows: Q rows of head group r (heads [r n/P, (r+1) n/P)),
  *                          then its K rows, then its V rows  ((3h/p x h)^T of Table 2)

@@ -55,37 +55,39 @@ def _norm_bwd_grid(rows):
 def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None, metp_recompute="ffn"):
     """Workspace bytes per rank of the CUDA path's buffer plan,
     each buffer rounded up to 256 B.  Written out from the plan table, not shared
-    with the library (tests compare it with pds_mem_bytes)."""
+    with the library (tests compare it with pds_mem_bytes).  Token buffers hold
+    rows = positions x b (layout [s, b, h])."""
     sl = s // P
     u = sl * b * h * 2
     lam = (n // P) * s * b * 4
     hl, Fl = h // P, ffn // P
     small = _al(2 * h * 4)
+    S, SL = s * b, sl * b                  # token rows (all / this rank)
     if pi == TS:
-        bufs = [s * h * 2, s * h * 2, s * Fl * 2, s * Fl * 2, lam, _norm_bwd_grid(sl) * h * 4,
-                max(Fl, 3 * hl) * s * 2, h * s * 2, h * max(Fl, 3 * hl) * 2]
+        bufs = [S * h * 2, S * h * 2, S * Fl * 2, S * Fl * 2, lam, _norm_bwd_grid(SL) * h * 4,
+                max(Fl, 3 * hl) * S * 2, h * S * 2, h * max(Fl, 3 * hl) * 2]
         if P > 1:
-            bufs.append(s * h * 2)      # second gather buffer: bwd re-gathers prefetched
+            bufs.append(S * h * 2)      # second gather buffer: bwd re-gathers prefetched
 
     elif pi == UZ:
         bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
-                u, 3 * u, 3 * u, sl * ffn * 2, sl * ffn * 2, 3 * u, 3 * u, u, lam,
-                _norm_bwd_grid(sl) * h * 4, max(ffn, 3 * h) * sl * 2, h * sl * 2, h * max(ffn, 3 * h) * 2]
+                u, 3 * u, 3 * u, SL * ffn * 2, SL * ffn * 2, 3 * u, 3 * u, u, lam,
+                _norm_bwd_grid(SL) * h * 4, max(ffn, 3 * h) * SL * 2, h * SL * 2, h * max(ffn, 3 * h) * 2]
     elif pi == CZ:
         # full weights + fp32 dW (ZeRO3), gathered Q/K/V of the whole context and the
         # all-rows dQ/dK/dV partials (RS in place), local FFN / attention scratch
         bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
-                u, s * 3 * h * 2, s * 3 * h * 2, sl * ffn * 2, sl * ffn * 2, u, u, lam,
-                _norm_bwd_grid(sl) * h * 4, max(ffn, 3 * h) * sl * 2, h * sl * 2, h * max(ffn, 3 * h) * 2]
+                u, S * 3 * h * 2, S * 3 * h * 2, SL * ffn * 2, SL * ffn * 2, u, u, lam,
+                _norm_bwd_grid(SL) * h * 4, max(ffn, 3 * h) * SL * 2, h * SL * 2, h * max(ffn, 3 * h) * 2]
     elif pi == METP:
         c = metp_chunks or P
-        w = sl // c
+        w = sl // c * b                    # rows of one wave per rank
         uw = w * h * 2
         bufs = [u, u, P * uw, P * uw, P * uw, P * w * Fl * 2, P * w * Fl * 2, P * w * Fl * 2,
-                s * hl * 2, s * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4,
+                S * hl * 2, S * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4,
                 max(Fl, 3 * hl) * P * w * 2, h * P * w * 2, h * max(Fl, 3 * hl) * 2]
         if metp_recompute == "full":
-            bufs.append(s * 3 * hl * 2)     # QKV (fwd, then recomputed in bwd), not saved
+            bufs.append(S * 3 * hl * 2)     # QKV (fwd, then recomputed in bwd), not saved
     else:
         raise KeyError(pi)
     return sum(_al(x) for x in bufs) + small

@@ -58,7 +58,7 @@ struct EpiParams {
   __nv_bfloat16* aux_out;
   int64_t ld_aux;
   const float2* rope;
-  int rope_d, rope_hq;
+  int rope_d, rope_hq, rope_b;
   int64_t seg, seg_stride, seg_base;
   int64_t c_seg, c_stride, c_base;
   __nv_bfloat16* c_t;      // transposed copies (dGELU epilogue): [N][ld_t]
@@ -220,7 +220,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
     int64_t pos = 0;
     if (row_ok) {
       const int64_t r = row;
-      pos = (r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg);
+      pos = ((r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg)) / ep.rope_b;
     }
     for (int hs = 0; hs < BN; hs += d) {
       for (int j0 = 0; j0 < d2; j0 += 32) {
@@ -724,7 +724,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.c_t = reinterpret_cast<__nv_bfloat16*>(g.c_t);
   ep.aux_t = reinterpret_cast<__nv_bfloat16*>(g.aux_t);
   ep.ld_t = g.ld_t;
-  ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq;
+  ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq; ep.rope_b = g.rope_b > 0 ? g.rope_b : 1;
   ep.seg = g.seg > 0 ? g.seg : (int64_t)1 << 40;
   ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;
   ep.c_seg = g.c_seg > 0 ? g.c_seg : (int64_t)1 << 40;

@@ -39,10 +39,11 @@ struct GemmArgs {
   void* aux_out = nullptr;
   int64_t ld_aux = 0;
   // RoPE: columns laid out in groups of 3*hq = [Q | K | V] (hq = heads * d);
-  // position of row r: (r / seg) * seg_stride + seg_base + (r % seg)
+  // position of row r: ((r / seg) * seg_stride + seg_base + (r % seg)) / rope_b
   const float2* rope = nullptr;   // [positions][d/2] (cos, sin)
   int rope_d = 0;
   int rope_hq = 0;
+  int rope_b = 1;                 // rows per position (batch b, layout [s, b, h]): pos = mapped row / b
   int64_t seg = 0, seg_stride = 0, seg_base = 0;
   // Row remaps of the STORED matrices (seg = 0: identity): logical row r lives at
   // storage row (r / seg) * stride + base + r % seg.  For A/B this is the TMA outer

@@ -161,9 +161,12 @@ struct Exec {
   cudaStream_t st;
   const pds_model& m;
   int P, r;
-  int64_t s, sl, h, F, nl, d, hl, Fl;
+  // s, sl: TOKEN ROWS (all / this rank) of the [s, b, h] layout = positions x b; every
+  // GEMM, norm and collective counts rows.  sq, sp: positions (attention, RoPE).
+  int64_t b, sq, sp, s, sl, h, F, nl, d, hl, Fl;
   Exec(pds_ctx* c_, cudaStream_t st_, int64_t s_)
-      : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), s(s_), sl(s_ / c_->P), h(c_->m.h), F(c_->m.ffn),
+      : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), b(c_->m.batch), sq(s_), sp(s_ / c_->P),
+        s(s_ * c_->m.batch), sl(s_ / c_->P * c_->m.batch), h(c_->m.h), F(c_->m.ffn),
         nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
 
   // overlap settings armed for the next gemm() (ag_next / rs_arm)
@@ -278,6 +281,7 @@ struct Exec {
     g.rope_d = (int)d;
     g.rope_hq = (int)hq;
     g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
+    g.rope_b = (int)b;                 // row -> position: the mapped row / b
     return g;
   }
   pds_status norm_fwd(const void* x, const void* res, const void* g, int64_t rows, void* x1, void* u, void* rstd) {
@@ -297,33 +301,55 @@ struct Exec {
     Prof p(c, st, K_NORM, 0, (double)n * 6);
     return kerr(add_bf16(a, b, out, n, st), "add_bf16");
   }
+  // attention over the sq positions of each of the b sequences: sequence bi is every
+  // b-th row of the [s, b, .] buffers (row stride b x ld), LSE / D [b][heads][sq]
   pds_status attn_f(const void* qkv, void* out, void* lse) {
-    const double fl = 4.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
+    const double fl = b * 4.0 * nl * d * (m.causal ? 0.5 * sq * sq : (double)sq * sq);
     Prof p(c, st, K_ATTN_F, fl, 0);
-    return kerr(attn_fwd(qkv, 3 * hl, (int)s, (int)nl, (int)d, m.causal, out, hl, lse, st), "attn_fwd");
+    for (int64_t bi = 0; bi < b; ++bi)
+      PDS_TRY(kerr(attn_fwd(static_cast<const char*>(qkv) + bi * 3 * hl * 2, 3 * hl * b, (int)sq, (int)nl, (int)d,
+                            m.causal, static_cast<char*>(out) + bi * hl * 2, hl * b,
+                            static_cast<float*>(lse) + bi * nl * sq, st), "attn_fwd"));
+    return PDS_OK;
   }
   // context parallelism (CZ): this rank's query rows [r s/P, (r+1) s/P) of all n heads
   // against every key of the all-gathered qkv [s][3h]
   double cz_fl(double mult) const {
-    const double q0 = (double)r * sl;
-    return mult * m.h * (m.causal ? sl * (q0 + 0.5 * sl) : (double)sl * s);
+    const double q0 = (double)r * sp;
+    return b * mult * m.h * (m.causal ? sp * (q0 + 0.5 * sp) : (double)sp * sq);
   }
   pds_status attn_rows_f(const void* qkvg, void* out, void* lse) {
     Prof p(c, st, K_ATTN_F, cz_fl(4.0), 0);
-    return kerr(attn_fwd_rows(qkvg, 3 * h, (int)s, (int)m.n_heads, (int)d, m.causal, (int)(r * sl), (int)sl, out, h,
-                              lse, st), "attn_fwd_rows");
+    const int64_t n = m.n_heads;
+    for (int64_t bi = 0; bi < b; ++bi)
+      PDS_TRY(kerr(attn_fwd_rows(static_cast<const char*>(qkvg) + bi * 3 * h * 2, 3 * h * b, (int)sq, (int)n, (int)d,
+                                 m.causal, (int)(r * sp), (int)sp, static_cast<char*>(out) + bi * h * 2, h * b,
+                                 static_cast<float*>(lse) + bi * n * sp, st), "attn_fwd_rows"));
+    return PDS_OK;
   }
   pds_status attn_rows_b(const void* qkvg, const void* out, const void* lse, const void* dout, void* dqkvf,
                          float* dd) {
     Prof p(c, st, K_ATTN_B, cz_fl(10.0), 0);
-    return kerr(attn_bwd_rows(qkvg, 3 * h, out, h, lse, dout, (int)s, (int)m.n_heads, (int)d, m.causal,
-                              (int)(r * sl), (int)sl, dqkvf, c->rope, dd, st), "attn_bwd_rows");
+    const int64_t n = m.n_heads;
+    for (int64_t bi = 0; bi < b; ++bi)
+      PDS_TRY(kerr(attn_bwd_rows(static_cast<const char*>(qkvg) + bi * 3 * h * 2, 3 * h * b,
+                                 static_cast<const char*>(out) + bi * h * 2, h * b,
+                                 static_cast<const float*>(lse) + bi * n * sp,
+                                 static_cast<const char*>(dout) + bi * h * 2, (int)sq, (int)n, (int)d, m.causal,
+                                 (int)(r * sp), (int)sp, static_cast<char*>(dqkvf) + bi * 3 * h * 2, c->rope,
+                                 dd + bi * n * sp, st), "attn_bwd_rows"));
+    return PDS_OK;
   }
   pds_status attn_b(const void* qkv, const void* out, const void* lse, const void* dout, void* dqkv, float* dd) {
-    const double fl = 10.0 * nl * d * (m.causal ? 0.5 * s * s : (double)s * s);
+    const double fl = b * 10.0 * nl * d * (m.causal ? 0.5 * sq * sq : (double)sq * sq);
     Prof p(c, st, K_ATTN_B, fl, 0);
-    return kerr(attn_bwd(qkv, 3 * hl, out, hl, lse, dout, (int)s, (int)nl, (int)d, m.causal, dqkv, c->rope, dd, st),
-                "attn_bwd");
+    for (int64_t bi = 0; bi < b; ++bi)
+      PDS_TRY(kerr(attn_bwd(static_cast<const char*>(qkv) + bi * 3 * hl * 2, 3 * hl * b,
+                            static_cast<const char*>(out) + bi * hl * 2, hl * b,
+                            static_cast<const float*>(lse) + bi * nl * sq, static_cast<const char*>(dout) + bi * hl * 2,
+                            (int)sq, (int)nl, (int)d, m.causal, static_cast<char*>(dqkv) + bi * 3 * hl * 2, c->rope,
+                            dd + bi * nl * sq, st), "attn_bwd"));
+    return PDS_OK;
   }
   // collectives
   pds_status ag(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {

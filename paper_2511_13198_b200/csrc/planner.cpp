@@ -218,7 +218,7 @@ int64_t persistent_bytes(const pds_model& m, int P) {
 pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan* out) {
   if (P < 1) PDS_FAIL(PDS_EINVAL, "P must be >= 1");
   if (m.h <= 0 || m.n_heads <= 0 || m.ffn <= 0) PDS_FAIL(PDS_EINVAL, "model dims must be positive");
-  if (m.batch != 1) PDS_FAIL(PDS_ENOTIMPL, "batch != 1 is not supported in this build");
+  if (m.batch < 1) PDS_FAIL(PDS_EINVAL, "batch must be >= 1");
   if (m.h % m.n_heads) PDS_FAIL(PDS_EDIVISIBILITY, "h not divisible by n_heads");
   const int64_t d = m.h / m.n_heads;
   if (d != 64 && d != 128) PDS_FAIL(PDS_ENOTIMPL, "head dim must be 64 or 128");
@@ -229,40 +229,43 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   const int64_t sl = s / P;
   if (sl % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/P=" + std::to_string(sl) + " must be a multiple of 128 (caller pads, R-15)");
   const int64_t h = m.h, F = m.ffn, nl = m.n_heads / P, hl = h / P, Fl = F / P;
-  const int64_t u = sl * h * 2, lam = nl * s * 4, ell = sl * 4;
+  // token buffers hold rows = positions x b (layout [s, b, h], reading Q-35); the
+  // divisibility checks above are on positions
+  const int64_t S = s * m.batch, SL = sl * m.batch;
+  const int64_t u = SL * h * 2, lam = nl * S * 4, ell = SL * 4;
   BufPlan p;
   int64_t ts = 0, tw = 0;
-  const int64_t dgp = (int64_t)rmsnorm_bwd_grid(sl) * h * 4;
+  const int64_t dgp = (int64_t)rmsnorm_bwd_grid(SL) * h * 4;
   switch (strategy) {
     case PDS_MEGATRON_TS:
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", s * 3 * hl * 2);
-      push(p.saved, ts, "a", s * hl * 2);
+      push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", s * Fl * 2);
-      push(p.ws, tw, "gather", s * h * 2);
-      push(p.ws, tw, "partial", s * h * 2);
-      push(p.ws, tw, "f0", s * Fl * 2);
-      push(p.ws, tw, "f1", s * Fl * 2);
+      push(p.saved, ts, "h", S * Fl * 2);
+      push(p.ws, tw, "gather", S * h * 2);
+      push(p.ws, tw, "partial", S * h * 2);
+      push(p.ws, tw, "f0", S * Fl * 2);
+      push(p.ws, tw, "f1", S * Fl * 2);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * s * 2);   // transposed operands (all GEMMs TN)
-      push(p.ws, tw, "tb", h * s * 2);
+      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * S * 2);   // transposed operands (all GEMMs TN)
+      push(p.ws, tw, "tb", h * S * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
-      if (P > 1) push(p.ws, tw, "gather2", s * h * 2);      // bwd re-gathers prefetched on the side stream
+      if (P > 1) push(p.ws, tw, "gather2", S * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", s * 3 * hl * 2);
-      push(p.saved, ts, "a", s * hl * 2);
+      push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "afull", u);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", sl * F * 2);
+      push(p.saved, ts, "h", SL * F * 2);
       push(p.ws, tw, "wqkv", 3 * h * h * 2);
       push(p.ws, tw, "wproj", h * h * 2);
       push(p.ws, tw, "win", F * h * 2);
@@ -271,16 +274,16 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "u1", u);
       push(p.ws, tw, "s1", 3 * u);
       push(p.ws, tw, "r1", 3 * u);
-      push(p.ws, tw, "f0", sl * F * 2);
-      push(p.ws, tw, "f1", sl * F * 2);
+      push(p.ws, tw, "f0", SL * F * 2);
+      push(p.ws, tw, "f1", SL * F * 2);
       push(p.ws, tw, "x3", 3 * u);
       push(p.ws, tw, "x4", 3 * u);
       push(p.ws, tw, "v2", u);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(F, 3 * h) * sl * 2);
-      push(p.ws, tw, "tb", h * sl * 2);
+      push(p.ws, tw, "ta", std::max(F, 3 * h) * SL * 2);
+      push(p.ws, tw, "tb", h * SL * 2);
       push(p.ws, tw, "wt", h * std::max(F, 3 * h) * 2);
       break;
     }
@@ -292,10 +295,11 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       if (m.metp_recompute != 0 && m.metp_recompute != 1)
         PDS_FAIL(PDS_EINVAL, "metp_recompute must be 0 (ffn) or 1 (full)");
       const bool full = m.metp_recompute == 1;     // QKV recomputed in bwd, not saved
-      const int64_t uw = w * h * 2;
+      const int64_t W = w * m.batch;               // rows of one wave per rank
+      const int64_t uw = W * h * 2;
       push(p.saved, ts, "rstd1", ell);
-      if (!full) push(p.saved, ts, "qkv", s * 3 * hl * 2);
-      push(p.saved, ts, "a", s * hl * 2);
+      if (!full) push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
@@ -304,46 +308,46 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "wg", P * uw);
       push(p.ws, tw, "wg2", P * uw);
       push(p.ws, tw, "pw", P * uw);
-      push(p.ws, tw, "hw", P * w * Fl * 2);
-      push(p.ws, tw, "gw", P * w * Fl * 2);
-      push(p.ws, tw, "dhw", P * w * Fl * 2);
-      push(p.ws, tw, "da", s * hl * 2);
-      push(p.ws, tw, "dqkv", s * 3 * hl * 2);
+      push(p.ws, tw, "hw", P * W * Fl * 2);
+      push(p.ws, tw, "gw", P * W * Fl * 2);
+      push(p.ws, tw, "dhw", P * W * Fl * 2);
+      push(p.ws, tw, "da", S * hl * 2);
+      push(p.ws, tw, "dqkv", S * 3 * hl * 2);
       push(p.ws, tw, "dd", lam);
-      push(p.ws, tw, "dgp", (int64_t)rmsnorm_bwd_grid(w) * h * 4);
+      push(p.ws, tw, "dgp", (int64_t)rmsnorm_bwd_grid(W) * h * 4);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * w * 2);
-      push(p.ws, tw, "tb", h * P * w * 2);
+      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * W * 2);
+      push(p.ws, tw, "tb", h * P * W * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
-      if (full) push(p.ws, tw, "qkv", s * 3 * hl * 2);
+      if (full) push(p.ws, tw, "qkv", S * 3 * hl * 2);
       break;
     }
     case PDS_MEGATRON_CZ: {
       // saved: the local rows of TS's tensors (Q/K/V of all heads, A, LSE, H)
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", sl * 3 * h * 2);
+      push(p.saved, ts, "qkv", SL * 3 * h * 2);
       push(p.saved, ts, "a", u);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", sl * F * 2);
+      push(p.saved, ts, "h", SL * F * 2);
       push(p.ws, tw, "wqkv", 3 * h * h * 2);      // [Q all; K all; V all] rows
       push(p.ws, tw, "wproj", h * h * 2);
       push(p.ws, tw, "win", F * h * 2);
       push(p.ws, tw, "wout", F * h * 2);
       push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
       push(p.ws, tw, "u1", u);
-      push(p.ws, tw, "qkvg", s * 3 * h * 2);      // all-gathered Q/K/V of the context
-      push(p.ws, tw, "dqkvf", s * 3 * h * 2);     // dQ/dK/dV partials of all rows (RS in place)
-      push(p.ws, tw, "f0", sl * F * 2);
-      push(p.ws, tw, "f1", sl * F * 2);
+      push(p.ws, tw, "qkvg", S * 3 * h * 2);      // all-gathered Q/K/V of the context
+      push(p.ws, tw, "dqkvf", S * 3 * h * 2);     // dQ/dK/dV partials of all rows (RS in place)
+      push(p.ws, tw, "f0", SL * F * 2);
+      push(p.ws, tw, "f1", SL * F * 2);
       push(p.ws, tw, "v2", u);
       push(p.ws, tw, "da", u);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(3 * h, F) * sl * 2);
-      push(p.ws, tw, "tb", h * sl * 2);
+      push(p.ws, tw, "ta", std::max(3 * h, F) * SL * 2);
+      push(p.ws, tw, "tb", h * SL * 2);
       push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
       break;
     }

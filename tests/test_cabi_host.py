@@ -115,5 +115,15 @@ def test_mem_bytes_errors(B):
         B.mem_bytes(m, 2, 9, 512)
     assert e.value.code == -3
     with pytest.raises(B.PdsError) as e:
-        B.mem_bytes(B.Model(h=256, n_heads=4, ffn=1024, batch=2), 2, 0, 512)
-    assert e.value.code == -9
+        B.mem_bytes(B.Model(h=256, n_heads=4, ffn=1024, batch=0), 2, 0, 512)
+    assert e.value.code == -1
+
+
+@pytest.mark.parametrize("b", [2, 3])
+def test_mem_bytes_batch_vs_oracle(B, b):
+    # b sequences in the [s/P, b, h] layout: every token buffer holds positions x b rows
+    for (h, n, F, s, P) in [(256, 4, 1024, 512, 2), (4096, 32, 16384, 8192, 4)]:
+        for pi in (0, 1, 2, 3):
+            saved, tr, pers = B.mem_bytes(B.Model(h=h, n_heads=n, ffn=F, batch=b), P, pi, s)
+            assert saved == OM.saved(pi, h, n, F, s, P, b=b), (pi, b)
+            assert tr == OM.transient(pi, h, n, F, s, P, b=b), (pi, b)

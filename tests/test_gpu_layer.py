@@ -98,8 +98,8 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
     return outs
 
 
-def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0):
-    d = layer_inputs(h, n, F, s, 1, seed=seed)
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, b=1):
+    d = layer_inputs(h, n, F, s, b, seed=seed)
     y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
                             causal=causal)
     g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
@@ -109,12 +109,12 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0):
     dys = OS.shard_act(d["dy"], P)
     ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
     model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0,
-                    metp_recompute=recompute)
+                    metp_recompute=recompute, batch=b)
     outs = run_ranks(model, P, [pi], [ranks], xs, dys)
-    y = np.concatenate([o[0] for o in outs])[:, None, :]
-    dx = np.concatenate([o[1] for o in outs])[:, None, :]
-    o = np.concatenate([host(R.o) for R in ranks])[:, None, :]
-    z = np.concatenate([host(R.z) for R in ranks])[:, None, :]
+    y = np.concatenate([o[0] for o in outs]).reshape(s, b, h)
+    dx = np.concatenate([o[1] for o in outs]).reshape(s, b, h)
+    o = np.concatenate([host(R.o) for R in ranks]).reshape(s, b, h)
+    z = np.concatenate([host(R.z) for R in ranks]).reshape(s, b, h)
     res = dict(y=rel(y, y_ref), o=rel(o, c["o"]), z=rel(z, c["z"]), dx=rel(dx, g_ref["dx"]),
                dxmdy=rel(dx - d["dy"], g_ref["dx"] - d["dy"]))
     gsh = {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g}
@@ -126,7 +126,7 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0):
                                    w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P)
     for r in range(P):
         res[f"qkv_shard{r}"] = rel(gsh["dw_qkv_t"][r], ref_sh["w_qkv_t"][r])
-        res[f"y_shard{r}"] = rel(outs[r][0], y_ref[r * (s // P):(r + 1) * (s // P), 0])
+        res[f"y_shard{r}"] = rel(outs[r][0].reshape(s // P, b, h), y_ref[r * (s // P):(r + 1) * (s // P)])
     bad = {k: v for k, v in res.items() if not v < TOL}
     assert not bad, (pi, P, bad, res)
     return res
@@ -148,6 +148,14 @@ def test_layer_p2_c1(pi):
 def test_layer_p4_d128(pi):
     # d = 128 heads, P = 4, METP c = 2 waves of 128 rows per rank
     _check_layer(pi, 4, 1024, 8, 4096, 1024, chunks=2)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("P", [1, 2])
+def test_layer_batch2(pi, P):
+    # b = 2 independent sequences in the [s/P, b, h] boundary layout (Table 1's b,
+    # reading Q-35): token rows t*b + bi, attention per sequence, RoPE at position t
+    _check_layer(pi, P, 256, 4, 1024, 512, seed=13, b=2, chunks=2 if P == 1 else 0)
 
 
 @pytest.mark.parametrize("pi", [0, 1, 2, 3])
