@@ -164,8 +164,16 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx = B.Context(model)
         for s in grid:
             w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
+            # strategies interleaved rep by rep (one warm-up pass each first), so slow drift
+            # of the power-capped clock does not favour whichever strategy runs last
             for pi in (0, 1, 2, 3):
-                t = time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=reps)
+                time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=1)
+            ts = {pi: [] for pi in (0, 1, 2, 3)}
+            for _ in range(reps):
+                for pi in (0, 1, 2, 3):
+                    ts[pi].append(time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0))
+            for pi in (0, 1, 2, 3):
+                t = float(np.median(ts[pi]))
                 records[pi].append((int(s), t))
                 print(f"P=1 s={s} pi={pi} t={t * 1e3:.3f} ms", flush=True)
             del w, gr, x, dy
