@@ -14,7 +14,8 @@ For P > 1 on a single-GPU box the profile is MODELLED: the per-rank compute of
 each strategy is measured on one GPU at the per-rank shapes through the
 loopback group, and the collective time is its byte count (oracle-independent
 formula of DESIGN.md §Comm) over the measured NVLink peer bandwidth (770 GB/s,
-B200_PROFILING.md).  The bundle header records which.
+B200_PROFILING.md), minus what the tile-overlapped MegatronTS / METP collectives
+hide under their GEMMs.  The bundle header records which.
 """
 from __future__ import annotations
 
@@ -145,12 +146,13 @@ def comm_bytes_per_rank(pi, h, F, s, P):
     return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
 
 
-def attention_seconds(torch, B, ctx, pi, s, w, gr, x, dy):
-    """Device time of the attention kernels in one layer fwd + bwd (library profiler)."""
+def class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, classes):
+    """Device time of the kernels of the given profiler classes (0 GEMM, 1 attention
+    fwd, 2 attention bwd, 3 norm / elementwise) in one layer fwd + bwd."""
     ctx.profile(True)
     ctx.profile_reset()
     time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0)
-    ms = ctx.profile_read(1)["ms"] + ctx.profile_read(2)["ms"]
+    ms = sum(ctx.profile_read(k)["ms"] for k in classes)
     ctx.profile(False)
     return ms / 1e3
 
@@ -188,14 +190,16 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx = B.Context(model)
         ctx_m = B.Context(B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, metp_chunks=P_target))
         for s in grid:
-            t_unit = {}
+            t_unit, t_gemm = {}, {}
             t_att = 0.0
             for pi in (0, 1, 2, 3):
                 w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
-                t1 = time_layer(torch, B, ctx_m if pi == 2 else ctx, pi, s, w, gr, x, dy, reps=reps)
+                cx = ctx_m if pi == 2 else ctx
+                t1 = time_layer(torch, B, cx, pi, s, w, gr, x, dy, reps=reps)
                 t_unit[pi] = t1
+                t_gemm[pi] = class_seconds(torch, B, cx, pi, s, w, gr, x, dy, (0,))
                 if pi == 3:
-                    t_att = attention_seconds(torch, B, ctx, pi, s, w, gr, x, dy)
+                    t_att = class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, (1, 2))
                 del w, gr, x, dy
             torch.cuda.empty_cache()
             for pi in (0, 1, 2, 3):
@@ -205,6 +209,11 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                     # its causal attention share is (2P - 1) / P^2 instead of 1 / P
                     comp += t_att * ((2 * P - 1) / (P * P) - 1.0 / P)
                 comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
+                if pi in (0, 2):
+                    # tile-overlapped AG / RS: each runs under the GEMM that
+                    # consumes / produces it (those GEMMs carry 48h^2 of the 72h^2 GEMM
+                    # flops per token); at least one chunk per collective stays exposed
+                    comm = max(comm / P, comm - (2.0 / 3.0) * t_gemm[pi] / P)
                 extra = (2 * P - 1) * 8e-6 * (P if pi == 2 else 1)   # collective launch latency
                 if pi == 3:
                     extra += 6 * 8e-6 * (P - 1)                           # part-wise weight AG / RS
@@ -212,7 +221,9 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx.close()
         ctx_m.close()
         note = (f"modelled for P={P_target}: P=1 device time / P + comm bytes / {link_gbs} GB/s "
-                "(+ per-collective latency); replace with a measured profile on an 8xB200 box")
+                "(+ per-collective latency; TS / METP: minus the share hidden under the tile-overlapped "
+                "GEMMs, at least one chunk per collective exposed; CZ: + the causal imbalance of contiguous "
+                "chunks); replace with a measured profile on an 8xB200 box")
     os.makedirs(out_dir, exist_ok=True)
     path = os.path.join(out_dir, f"h{h}_n{n}_f{ffn}_P{P_target}.txt")
     cap = float(torch.cuda.get_device_properties(0).total_memory)
