@@ -204,7 +204,9 @@ pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
  * chunk on a side stream while the GEMM polls per tile for the chunks it needs, and
  * every reduce-scatter after a row-parallel GEMM (proj, FC2; bwd dV, dU) sends each
  * chunk as soon as the GEMM has stored it ("communication overlapped with GEMM tiles",
- * north_star; the AG / RS of PAPER.md:203).  on = 1 (default) or 0 (plain in-order
+ * north_star; the AG / RS of PAPER.md:203); METP does the same per wave, and
+ * UlyssesZ sends each head-group block of its sequence -> head All-to-Alls as soon
+ * as the packing GEMM has stored it.  on = 1 (default) or 0 (plain in-order
  * collectives).  Results are bit-identical either way.  Ignored at P = 1. */
 pds_status pds_set_overlap(pds_ctx* ctx, int32_t on);
 /* Debug taps: the next pds_layer_fwd also writes the sublayer deltas O (attention

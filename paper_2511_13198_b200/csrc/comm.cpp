@@ -163,6 +163,23 @@ struct NcclComm : Comm {
     }
     return PDS_OK;
   }
+  pds_status all_to_all_gated(const void* send, void* recv, int64_t count, DType dt, cudaStream_t,
+                              cudaStream_t st, const uint32_t* ctr, uint32_t target) override {
+    const int64_t b = count * dt_size(dt);
+    const char* sb = static_cast<const char*>(send);
+    char* rb = static_cast<char*>(recv);
+    PDS_TRY(stream_wait32_geq(st, ctr + rank, target));
+    PDS_CUDA(cudaMemcpyAsync(rb + rank * b, sb + rank * b, b, cudaMemcpyDeviceToDevice, st));
+    for (int k = 1; k < P; ++k) {
+      const int to = (rank + k) % P, from = (rank - k + P) % P;
+      PDS_TRY(stream_wait32_geq(st, ctr + to, target));
+      PDS_NCCL(ncclGroupStart());
+      PDS_NCCL(ncclSend(sb + to * b, (size_t)count, nt(dt), to, comm, st));
+      PDS_NCCL(ncclRecv(rb + from * b, (size_t)count, nt(dt), from, comm, st));
+      PDS_NCCL(ncclGroupEnd());
+    }
+    return PDS_OK;
+  }
   int overlap_sm_reserve() const override { return max_ctas; }
   pds_status warm_p2p() {
     void* buf = nullptr;
@@ -337,6 +354,23 @@ struct LoopComm : Comm {
                                static_cast<const char*>(send) + j * b, b, cudaMemcpyDeviceToDevice, st));
     }
     finish(st);                                 // every peer's copy into recv is done
+    return PDS_OK;
+  }
+  pds_status all_to_all_gated(const void* send, void* recv, int64_t count, DType dt, cudaStream_t,
+                              cudaStream_t st, const uint32_t* ctr, uint32_t target) override {
+    const int64_t b = count * dt_size(dt);
+    const char* sb = static_cast<const char*>(send);
+    publish(recv, st);                          // this rank's receive buffer is free
+    PDS_TRY(stream_wait32_geq(st, ctr + rank, target));
+    PDS_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + rank * b, sb + rank * b, b, cudaMemcpyDeviceToDevice, st));
+    for (int k = 1; k < P; ++k) {
+      const int j = (rank + k) % P;
+      PDS_TRY(stream_wait32_geq(st, ctr + j, target));
+      PDS_CUDA(cudaStreamWaitEvent(st, g->ready[j], 0));
+      PDS_CUDA(cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(g->ptr[j])) + rank * b, sb + j * b, b,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    finish(st);                                 // every peer's block has landed in recv
     return PDS_OK;
   }
   pds_status all_to_all(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {

@@ -49,6 +49,14 @@ struct Comm {
                                           cudaStream_t st, const uint32_t* ctr, uint32_t target) {
     return PDS_ENOTIMPL;
   }
+  // all_to_all_gated: send [P][count] blocks from the producing GEMM (column-blocked
+  // epilogue); block j is sent to rank j once ctr[j] has reached `target` (own block:
+  // copied into recv + rank*count), and rank i's block for this rank lands in
+  // recv + i*count.
+  virtual pds_status all_to_all_gated(const void* send, void* recv, int64_t count, DType dt, cudaStream_t main,
+                                      cudaStream_t st, const uint32_t* ctr, uint32_t target) {
+    return PDS_ENOTIMPL;
+  }
   // SMs a GEMM must leave free while one of the above is in flight (the collective's
   // own kernels must be able to run beside a persistent GEMM that polls for them)
   virtual int overlap_sm_reserve() const { return 0; }

@@ -70,6 +70,8 @@ struct EpiParams {
   uint32_t* done_ctr;
   int chunk_rows;
   int rot_mb;
+  int chunk_cols;      // > 0: done_ctr counts per column block instead of per row chunk
+  int rot_nb;
 };
 
 // AG -> GEMM: wait until every chunk overlapping rows [r0, r0 + n) has landed.  The
@@ -95,13 +97,24 @@ __device__ __forceinline__ void wait_chunks(const EpiParams& ep, int r0, int n) 
 
 // GEMM -> RS: one epilogue warp has stored its 32 rows x `ncols` columns; count them
 // into the chunk's counter once every lane's stores are ordered before the add.
-__device__ __forceinline__ void count_stored(const EpiParams& ep, int warp_row0, bool row_ok, int ncols) {
+__device__ __forceinline__ void count_stored(const EpiParams& ep, int warp_row0, bool row_ok, int n0, int ncols) {
   if (!ep.done_ctr) return;
   const unsigned vm = __ballot_sync(0xffffffffu, row_ok);
   __threadfence();
   __syncwarp();
-  if ((threadIdx.x & 31) == 0 && vm && ncols > 0)
-    atomicAdd(ep.done_ctr + warp_row0 / ep.chunk_rows, (uint32_t)(__popc(vm) * ncols));
+  if ((threadIdx.x & 31) == 0 && vm && ncols > 0) {
+    const uint32_t nrows = __popc(vm);
+    if (ep.chunk_cols > 0) {            // column blocks (All-to-All): split the range over blocks
+      for (int c = n0; c < n0 + ncols;) {
+        const int blk = c / ep.chunk_cols;
+        const int end = min(n0 + ncols, (blk + 1) * ep.chunk_cols);
+        atomicAdd(ep.done_ctr + blk, nrows * (uint32_t)(end - c));
+        c = end;
+      }
+    } else {
+      atomicAdd(ep.done_ctr + warp_row0 / ep.chunk_rows, nrows * (uint32_t)ncols);
+    }
+  }
 }
 
 struct RowMap {
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(256, 1)
         int mb, nb;
         tile_coords(t, mt, nt, mb, nb);
         mb = rot_block(mb, mt, ep.rot_mb);
+        nb = rot_block(nb, nt, ep.rot_nb);
         const int m0 = mb * BM, n0 = nb * BN;
         wait_chunks(ep, m0, min(BM, M - m0));
         for (int kb = 0; kb < nkb; ++kb) {
@@ -428,6 +442,7 @@ __global__ void __launch_bounds__(256, 1)
       int mb, nb;
       tile_coords(t, mt, nt, mb, nb);
       mb = rot_block(mb, mt, ep.rot_mb);
+      nb = rot_block(nb, nt, ep.rot_nb);
       const int m0 = mb * BM, n0 = nb * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -435,7 +450,7 @@ __global__ void __launch_bounds__(256, 1)
       const bool row_ok = row < M;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       epilogue_tile<BN>(ep, tbase, row, row_ok, n0, N);
-      count_stored(ep, m0 + q * 32, row_ok, min(BN, N - n0));
+      count_stored(ep, m0 + q * 32, row_ok, n0, min(BN, N - n0));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -507,6 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         int mb, nb;
         tile_coords(t, mt, nt, mb, nb, group_m);
         mb = rot_block(mb, mt, ep.rot_mb);
+        nb = rot_block(nb, nt, ep.rot_nb);
         const int m0 = mb * 256 + rank * 128, n0 = nb * 256 + rank * 128;
         wait_chunks(ep, m0, min(128, M - m0));
         for (int kb = 0; kb < nkb; ++kb) {
@@ -576,12 +592,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       int mb, nb;
       tile_coords(t, mt, nt, mb, nb, group_m);
       mb = rot_block(mb, mt, ep.rot_mb);
+      nb = rot_block(nb, nt, ep.rot_nb);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + rank * 128 + q * 32 + lane;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + half * 128;
       epilogue_tile<128>(ep, tbase, row, row < M, nb * 256 + half * 128, N);
-      count_stored(ep, row - lane, row < M, min(128, N - (nb * 256 + half * 128)));
+      count_stored(ep, row - lane, row < M, nb * 256 + half * 128, min(128, N - (nb * 256 + half * 128)));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa_u32(&tempty_bar[acc], 0));
@@ -731,11 +748,13 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.c_stride = g.c_stride; ep.c_base = g.c_base;
   ep.wait_flags = g.wait_flags; ep.flag_epoch = g.flag_epoch;
   ep.done_ctr = g.done_ctr; ep.chunk_rows = (int)g.chunk_rows; ep.rot_mb = 0;
-  if (g.wait_flags || g.done_ctr) {
+  ep.chunk_cols = (int)g.chunk_cols; ep.rot_nb = 0;
+  if (g.wait_flags || (g.done_ctr && g.chunk_cols <= 0)) {
     if (g.chunk_rows <= 0 || g.chunk_rows % 32 || g.M % g.chunk_rows) return (int)cudaErrorInvalidValue;
     if (g.wait_flags && (g.a_mn || g.a_seg)) return (int)cudaErrorInvalidValue;
     if (g.done_ctr && (g.c_seg || g.blk_w)) return (int)cudaErrorInvalidValue;
   }
+  if (g.chunk_cols < 0 || (g.chunk_cols > 0 && (!g.done_ctr || g.N % g.chunk_cols))) return (int)cudaErrorInvalidValue;
   if (g.sm_reserve < 0 || g.sm_reserve > gemm_num_sms() - 2) return (int)cudaErrorInvalidValue;
   // a tile must not straddle a remap segment
   if (g.a_seg > 0 && g.a_seg % (g.a_mn ? 64 : BM)) return (int)cudaErrorInvalidValue;
@@ -750,6 +769,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
                        (!g.a_mn || g.M % 64 == 0) && (!g.b_mn || g.N % 64 == 0) &&
                        (g.b_seg == 0 || g.b_seg % 128 == 0);
   if (g.m_rot_rows) ep.rot_mb = (int)(g.m_rot_rows / (pair_ok ? 256 : BM));
+  if (g.n_rot_cols) ep.rot_nb = (int)(g.n_rot_cols / (pair_ok || use256 ? 256 : 128));
   if (pair_ok) {
     switch ((g.a_mn ? 2 : 0) | (g.b_mn ? 1 : 0)) {
       case 0: return launch2_t<0, 0>(g, ep, st);

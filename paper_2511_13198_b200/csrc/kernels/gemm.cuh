@@ -77,6 +77,12 @@ struct GemmArgs {
   int64_t chunk_rows = 0;
   int64_t m_rot_rows = 0;
   int sm_reserve = 0;
+  // GEMM -> All-to-All (UlyssesZ, column-blocked output): chunk_cols > 0 makes done_ctr
+  // count per block of chunk_cols LOGICAL output columns (block j goes to rank j), so
+  // block j is complete once done_ctr[j] has grown by M * chunk_cols; n_rot_cols: first
+  // column of the tile order (wraps).
+  int64_t chunk_cols = 0;
+  int64_t n_rot_cols = 0;
 };
 
 // returns 0 on success, a cudaError_t value otherwise

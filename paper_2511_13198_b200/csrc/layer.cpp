@@ -83,11 +83,12 @@ struct pds_ctx {
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_y = nullptr, ev_dx = nullptr;
   // side stream for collectives overlapped with compute (METP wave prefetch, TS tiles)
   cudaStream_t comm_st = nullptr;
-  // tile-overlapped MegatronTS collectives (P > 1): device words [0, 8) = chunk-landed
-  // flags of the all-gathers, [8, 16) = per-chunk store counters of the GEMMs feeding a
-  // reduce-scatter; host-side epoch / running target
+  // tile-overlapped collectives (P > 1): device words [0, 8) = chunk-landed flags of the
+  // all-gathers, [8, 16) = per-chunk store counters of the GEMMs feeding a
+  // reduce-scatter, [16, 24) = per-block counters of the GEMMs feeding an all-to-all;
+  // host-side epoch / running targets
   uint32_t* sync = nullptr;
-  uint32_t ag_epoch = 0, rs_count = 0;
+  uint32_t ag_epoch = 0, rs_count = 0, a2a_count = 0;
   int overlap = 1;
   std::vector<cudaEvent_t> sync_pool;
   // profiling
@@ -183,6 +184,7 @@ struct Exec {
     if (has_nxt) {
       g.wait_flags = nxt.wait_flags; g.flag_epoch = nxt.flag_epoch; g.done_ctr = nxt.done_ctr;
       g.chunk_rows = nxt.chunk_rows; g.m_rot_rows = nxt.m_rot_rows; g.sm_reserve = nxt.sm_reserve;
+      g.chunk_cols = nxt.chunk_cols; g.n_rot_cols = nxt.n_rot_cols;
       has_nxt = false;
       nxt = GemmArgs();
     }
@@ -202,8 +204,8 @@ struct Exec {
   bool overlap() const { return P > 1 && c->overlap && !c->comm->trivial(); }
   pds_status sync_init() {
     if (c->sync) return PDS_OK;
-    PDS_CUDA(cudaMalloc(&c->sync, 16 * sizeof(uint32_t)));
-    PDS_CUDA(cudaMemsetAsync(c->sync, 0, 16 * sizeof(uint32_t), st));
+    PDS_CUDA(cudaMalloc(&c->sync, 32 * sizeof(uint32_t)));
+    PDS_CUDA(cudaMemsetAsync(c->sync, 0, 32 * sizeof(uint32_t), st));
     return PDS_OK;
   }
   // AG of buf [P][count] (this rank's chunk already at slot r) on the side stream, chunk
@@ -247,6 +249,36 @@ struct Exec {
     nxt.sm_reserve = cm->overlap_sm_reserve();
     has_nxt = true;
     return PDS_OK;
+  }
+  // arm the next gemm() (column-blocked output [P][sl][blk], block j for rank j) to
+  // count its stores per block, computing the block sent first (r+1) first
+  uint32_t a2a_target = 0;
+  pds_status a2a_arm(int64_t blk) {
+    PDS_TRY(sync_init());
+    PDS_TRY(link(st, comm_stream()));        // the receive buffer's readers are done
+    pds_status rc = PDS_OK;
+    Comm* cm = c->comm->side(&rc);
+    if (!cm) return rc;
+    c->a2a_count += (uint32_t)(sl * blk);
+    a2a_target = c->a2a_count;
+    nxt = GemmArgs();
+    nxt.done_ctr = c->sync + 16;
+    nxt.chunk_cols = blk; nxt.n_rot_cols = (int64_t)((r + 1) % P) * blk;
+    nxt.sm_reserve = cm->overlap_sm_reserve();
+    has_nxt = true;
+    return PDS_OK;
+  }
+  // after the armed gemm(): the All-to-All, each block leaving as soon as it is stored
+  pds_status a2a_run(const char* send, char* recv, int64_t count) {
+    cudaStream_t cs = comm_stream();
+    pds_status rc = PDS_OK;
+    Comm* cm = c->comm->side(&rc);
+    if (!cm) return rc;
+    {
+      Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
+      PDS_TRY(cm->all_to_all_gated(send, recv, count, DT_BF16, st, cs, c->sync + 16, a2a_target));
+    }
+    return link(cs, st);
   }
   // after the armed gemm(): send each finished chunk of `partial` to its owner, receive
   // the peers' partials of this rank's chunk into recv [P][count], and sum them (rank
@@ -609,8 +641,12 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, 3 * e.h, e.h, s1, 3 * e.hl), e.hl, 0, 0, e.r * e.sl);
   q.blk_w = (int)(3 * e.hl);
   q.blk_stride = e.sl * 3 * e.hl;
+  // P > 1: block j of the packed output leaves for rank j as soon as its tiles are stored
+  const bool ov = e.overlap();
+  if (ov) PDS_TRY(e.a2a_arm(3 * e.hl));
   PDS_TRY(e.gemm(q));
-  PDS_TRY(e.a2a(s1, sv->at("qkv"), e.sl * 3 * e.hl));                                  // A2A seq -> heads
+  PDS_TRY(ov ? e.a2a_run(s1, sv->at("qkv"), e.sl * 3 * e.hl)
+             : e.a2a(s1, sv->at("qkv"), e.sl * 3 * e.hl));                               // A2A seq -> heads
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));
   PDS_TRY(e.a2a(sv->at("a"), r1, e.sl * e.hl));                                        // A2A heads -> seq
   {
@@ -686,10 +722,13 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   GemmArgs dafull = Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, s1, e.hl);
   dafull.blk_w = (int)e.hl;
   dafull.blk_stride = e.sl * e.hl;
+  const bool ov = e.overlap();       // P > 1: A2A(dO) block by block, under the dW_proj work too
+  if (ov) PDS_TRY(e.a2a_arm(e.hl));
   PDS_TRY(e.gemm(dafull));                                                              // packed for A2A
+  if (ov) PDS_TRY(e.a2a_run(s1, r1, e.sl * e.hl));                                     // A2A(dO)
   PDS_TRY(tn.dw(sv->at("afull"), e.h, dx, e.h, e.sl, e.h, e.h, dw, EPI_F32));
   PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
-  PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                                 // A2A(dO)
+  if (!ov) PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                         // A2A(dO)
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), r1, x3, dd));
   PDS_TRY(e.a2a(x3, r1, e.sl * 3 * e.hl));                                             // A2A(dQKV)
   {

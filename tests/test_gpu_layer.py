@@ -209,10 +209,13 @@ def test_layer_ts_odd_chunks_p2():
     (0, 4, 1024, 8, 4096, 2048, 0),     # TS, 1-CTA GEMMs, rotated tile order
     (0, 2, 2048, 16, 8192, 2816, 0),    # TS, 256-row pair tiles straddle chunks
     (2, 2, 2048, 16, 8192, 4096, 2),    # METP, 2 waves of 1024 rows per rank
-    (2, 4, 1024, 8, 4096, 2048, 2)])    # METP, 4 ranks x 2 waves of 256 rows
+    (2, 4, 1024, 8, 4096, 2048, 2),     # METP, 4 ranks x 2 waves of 256 rows
+    (1, 2, 2048, 16, 8192, 4096, 0),    # UlyssesZ, A2A blocks of 3h/P columns, pair GEMMs
+    (1, 4, 1024, 8, 4096, 2048, 0)])    # UlyssesZ, 4 ranks
 def test_overlap_bit_identical(pi, P, h, n, F, s, chunks):
-    """MegatronTS / METP with the tile-overlapped AG / RS (pds_set_overlap 1) equal the
-    in-order collectives (0) bit for bit: the same tiles, the same rank-order sums."""
+    """MegatronTS / METP with the tile-overlapped AG / RS and UlyssesZ with the
+    block-gated All-to-Alls (pds_set_overlap 1) equal the in-order collectives (0) bit
+    for bit: the same tiles, the same rank-order sums."""
     d = layer_inputs(h, n, F, s, 1, seed=11)
     W = OS.shard_weights(d, n, P)
     xs = OS.shard_act(d["x"], P)
