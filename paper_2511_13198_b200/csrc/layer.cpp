@@ -1380,8 +1380,9 @@ extern "C" pds_status pds_set_capacity(pds_ctx* c, double capacity, double gamma
 }
 
 extern "C" pds_status pds_set_enabled(pds_ctx* c, uint32_t mask) {
-  if (!c || !(mask & 0x7)) PDS_FAIL(PDS_EINVAL, "empty strategy mask");
-  c->enabled = mask & 0x7;
+  const uint32_t all = (1u << PDS_N_STRATEGIES) - 1;
+  if (!c || !(mask & all)) PDS_FAIL(PDS_EINVAL, "empty strategy mask");
+  c->enabled = mask & all;
   c->cache.clear();
   c->prev.clear();
   return PDS_OK;
