@@ -279,6 +279,23 @@ def test_layer_errors():
     ctx.close()
 
 
+def test_plan_strategy_masks():
+    # pds_set_enabled covers all four strategies: each alone yields its uniform plan
+    import os
+    m = B.Model(h=4096, n_heads=32, ffn=16384, n_layers=8)
+    ctx = B.Context(m)
+    ctx.load_costs(os.path.join(os.path.dirname(B.__file__), "bundles", "h4096_n32_f16384_P1.txt"))
+    ctx.set_capacity(1e15, 0.0)
+    for pi in range(B.N_STRATEGIES):
+        ctx.set_enabled(1 << pi)
+        plan, _ = ctx.plan(8192, 8)
+        assert plan == [pi] * 8, (pi, plan)
+    with pytest.raises(B.PdsError) as e:
+        ctx.set_enabled(1 << B.N_STRATEGIES)
+    assert e.value.code == -1
+    ctx.close()
+
+
 @pytest.mark.parametrize("pi", [0, 2])
 def test_step_host(pi):
     """pds_layer_step_host (host x, dy in; host y, dx out; copies overlapped on a copy
