@@ -170,10 +170,14 @@ struct Exec {
         s(s_ * c_->m.batch), sl(s_ / c_->P * c_->m.batch), h(c_->m.h), F(c_->m.ffn),
         nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
 
-  // overlap settings armed for the next gemm() (ag_next / rs_arm)
+  // overlap settings armed for the next gemm() (ag_next / rs_arm / a2a_arm); a store
+  // counter's running host target advances only once that GEMM has been launched, so
+  // a failed launch never leaves a later stream wait behind an unreachable value
   GemmArgs nxt;
   bool has_nxt = false;
   cudaEvent_t nxt_join = nullptr;
+  uint32_t* nxt_count = nullptr;
+  uint32_t nxt_count_value = 0;
 
   pds_status gemm(GemmArgs g) {
     // algorithmic bytes: A and B once, C by epilogue (fp32 += reads and writes; GELU /
@@ -191,6 +195,10 @@ struct Exec {
     {
       Prof p(c, st, K_GEMM, 2.0 * g.M * g.N * g.K, 2.0 * ((double)g.M + g.N) * g.K + cb * mn);
       PDS_TRY(kerr(gemm_launch(g, st), "gemm"));
+    }
+    if (nxt_count) {
+      *nxt_count = nxt_count_value;
+      nxt_count = nullptr;
     }
     if (nxt_join) {                      // the all-gather this GEMM consumed, joined
       cudaEvent_t ev = nxt_join;
@@ -241,8 +249,9 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
-    c->rs_count += (uint32_t)(rows * ncols);
-    rs_target = c->rs_count;
+    rs_target = c->rs_count + (uint32_t)(rows * ncols);
+    nxt_count = &c->rs_count;
+    nxt_count_value = rs_target;
     nxt = GemmArgs();
     nxt.done_ctr = c->sync + 8;
     nxt.chunk_rows = rows; nxt.m_rot_rows = (int64_t)((r + 1) % P) * rows;
@@ -259,8 +268,9 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
-    c->a2a_count += (uint32_t)(sl * blk);
-    a2a_target = c->a2a_count;
+    a2a_target = c->a2a_count + (uint32_t)(sl * blk);
+    nxt_count = &c->a2a_count;
+    nxt_count_value = a2a_target;
     nxt = GemmArgs();
     nxt.done_ctr = c->sync + 16;
     nxt.chunk_cols = blk; nxt.n_rot_cols = (int64_t)((r + 1) % P) * blk;
