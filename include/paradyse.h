@@ -243,8 +243,8 @@ pds_status pds_k_gemm(const void* A, int64_t lda, int32_t a_mn, const void* B, i
  * multiple of 32 dividing M).  wait_flags (nullable, device uint32 [M/chunk_rows]):
  * a CTA loads A rows of chunk c only once (int32)(wait_flags[c] - flag_epoch) >= 0
  * (traps after > 30 s).  done_ctr (nullable, device uint32 [M/chunk_rows]): grows by
- * the number of elements stored in chunk c, so it has grown by chunk_rows*N when the
- * chunk is complete.  m_rot_rows: first row of the tile order (wraps).  sm_reserve:
+ * the number of elements stored in chunk c divided by 8, so it has grown by
+ * chunk_rows*N/8 when the chunk is complete.  m_rot_rows: first row of the tile order (wraps).  sm_reserve:
  * SMs left idle.  Bad chunking -> PDS_EINVAL. */
 pds_status pds_k_gemm_sync(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
                            int32_t N, int32_t K, void* C, int64_t ldc, const uint32_t* wait_flags,

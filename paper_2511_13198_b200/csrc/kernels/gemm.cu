@@ -95,8 +95,10 @@ __device__ __forceinline__ void wait_chunks(const EpiParams& ep, int r0, int n) 
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// GEMM -> RS: one epilogue warp has stored its 32 rows x `ncols` columns; count them
-// into the chunk's counter once every lane's stores are ordered before the add.
+// GEMM -> RS / A2A: one epilogue warp has stored its 32 rows x `ncols` columns; count
+// them, in units of 8 elements (N and the column blocks are multiples of 8, and the
+// unit keeps a chunk's per-call growth far below 2^31), into the chunk's counter once
+// every lane's stores are ordered before the add.
 __device__ __forceinline__ void count_stored(const EpiParams& ep, int warp_row0, bool row_ok, int n0, int ncols) {
   if (!ep.done_ctr) return;
   const unsigned vm = __ballot_sync(0xffffffffu, row_ok);
@@ -108,11 +110,11 @@ __device__ __forceinline__ void count_stored(const EpiParams& ep, int warp_row0,
       for (int c = n0; c < n0 + ncols;) {
         const int blk = c / ep.chunk_cols;
         const int end = min(n0 + ncols, (blk + 1) * ep.chunk_cols);
-        atomicAdd(ep.done_ctr + blk, nrows * (uint32_t)(end - c));
+        atomicAdd(ep.done_ctr + blk, nrows * (uint32_t)((end - c) >> 3));
         c = end;
       }
     } else {
-      atomicAdd(ep.done_ctr + warp_row0 / ep.chunk_rows, nrows * (uint32_t)ncols);
+      atomicAdd(ep.done_ctr + warp_row0 / ep.chunk_rows, nrows * (uint32_t)(ncols >> 3));
     }
   }
 }
@@ -754,7 +756,8 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
     if (g.wait_flags && (g.a_mn || g.a_seg)) return (int)cudaErrorInvalidValue;
     if (g.done_ctr && (g.c_seg || g.blk_w)) return (int)cudaErrorInvalidValue;
   }
-  if (g.chunk_cols < 0 || (g.chunk_cols > 0 && (!g.done_ctr || g.N % g.chunk_cols))) return (int)cudaErrorInvalidValue;
+  if (g.chunk_cols < 0 || (g.chunk_cols > 0 && (!g.done_ctr || g.N % g.chunk_cols || g.chunk_cols % 8)))
+    return (int)cudaErrorInvalidValue;
   if (g.sm_reserve < 0 || g.sm_reserve > gemm_num_sms() - 2) return (int)cudaErrorInvalidValue;
   // a tile must not straddle a remap segment
   if (g.a_seg > 0 && g.a_seg % (g.a_mn ? 64 : BM)) return (int)cudaErrorInvalidValue;

@@ -66,8 +66,8 @@ struct GemmArgs {
   //               (int32)(wait_flags[c] - flag_epoch) >= 0, i.e. the all-gather has
   //               landed chunk c (K-major A, no A remap).  Bounded spin, then trap.
   //   done_ctr    GEMM -> RS: after an epilogue warp has stored its rows of chunk c it
-  //               adds the number of elements stored to done_ctr[c] (release), so the
-  //               chunk is complete once the counter has grown by chunk_rows * N.
+  //               adds the number of elements stored / 8 to done_ctr[c] (release), so
+  //               the chunk is complete once the counter has grown by chunk_rows * N / 8.
   //   m_rot_rows  tiles are issued starting at this row, wrapping over M, so the chunk
   //               that is local (AG) or sent first (RS) is computed first.
   //   sm_reserve  SMs left free for the collective's kernels during this GEMM.
@@ -79,7 +79,7 @@ struct GemmArgs {
   int sm_reserve = 0;
   // GEMM -> All-to-All (UlyssesZ, column-blocked output): chunk_cols > 0 makes done_ctr
   // count per block of chunk_cols LOGICAL output columns (block j goes to rank j), so
-  // block j is complete once done_ctr[j] has grown by M * chunk_cols; n_rot_cols: first
+  // block j is complete once done_ctr[j] has grown by M * chunk_cols / 8; n_rot_cols: first
   // column of the tile order (wraps).
   int64_t chunk_cols = 0;
   int64_t n_rot_cols = 0;

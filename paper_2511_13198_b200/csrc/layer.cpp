@@ -249,7 +249,7 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
-    rs_target = c->rs_count + (uint32_t)(rows * ncols);
+    rs_target = c->rs_count + (uint32_t)(rows * ncols / 8);     // counted in units of 8 elements
     nxt_count = &c->rs_count;
     nxt_count_value = rs_target;
     nxt = GemmArgs();
@@ -268,7 +268,7 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
-    a2a_target = c->a2a_count + (uint32_t)(sl * blk);
+    a2a_target = c->a2a_count + (uint32_t)(sl * blk / 8);
     nxt_count = &c->a2a_count;
     nxt_count_value = a2a_target;
     nxt = GemmArgs();

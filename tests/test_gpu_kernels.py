@@ -308,14 +308,14 @@ def test_gemm_store_counters_gate_chunk_reads(M, N, K, chunk, rot):
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
     # the reader is enqueued FIRST: each chunk is copied out as soon as its counter says so
     for c in range(nch):
-        B.k_stream_wait32(sb.cuda_stream, ctr.data_ptr() + 4 * c, chunk * N)
+        B.k_stream_wait32(sb.cuda_stream, ctr.data_ptr() + 4 * c, chunk * N // 8)
         with torch.cuda.stream(sb):
             got[c * chunk:(c + 1) * chunk].copy_(out[c * chunk:(c + 1) * chunk], non_blocking=True)
     B.k_gemm_sync(ta.data_ptr(), K, tw.data_ptr(), K, M, N, K, out.data_ptr(), N, done_ctr=ctr.data_ptr(),
                   chunk_rows=chunk, m_rot_rows=rot, stream=sa.cuda_stream)
     torch.cuda.synchronize()
     assert torch.equal(got.view(torch.int16), out.cpu().view(torch.int16))
-    assert ctr.cpu().tolist() == [chunk * N] * nch
+    assert ctr.cpu().tolist() == [chunk * N // 8] * nch
     assert rel(host(out), A.astype(np.float64) @ W.T) < 1e-2
 
 
