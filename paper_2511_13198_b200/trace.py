@@ -111,6 +111,25 @@ def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None, memo=None):
             "switching": switches(recs)}
 
 
+def common_bucket_table(runs, L):
+    """Per Table 3 bucket, tokens/s per layer of every run over the sequences EVERY run
+    completed (a static strategy that OOMs drops its longest sequences; comparing
+    bucket rates over different sequence sets would favour it), and the adaptive
+    plan's ratio to the best static strategy."""
+    done = {n: {(i, r["s"]): r["seconds"] for i, r in enumerate(v["records"]) if not r.get("oom")}
+            for n, v in runs.items()}
+    common = set.intersection(*[set(d) for d in done.values()])
+    out = {}
+    for b in sorted({bucket_of(k[1]) for k in common}):
+        keys = [k for k in common if bucket_of(k[1]) == b]
+        tps = {n: sum(k[1] for k in keys) * L / sum(done[n][k] for k in keys) for n in runs}
+        statics = {n: v for n, v in tps.items() if n != "adaptive"}
+        best = max(statics, key=statics.get)
+        out[str(b)] = {"sequences": len(keys), "tokens_per_s_per_layer": tps, "best_static": best,
+                       "adaptive_over_best_static": tps["adaptive"] / statics[best] if "adaptive" in tps else None}
+    return out
+
+
 def time_full_at(full, s_max):
     t = 0.0
     for r in full["records"]:
@@ -214,6 +233,11 @@ def main():
             r = out["runs"][name]
             print(name, "cum %.1fs" % r["cumulative_s"], "oom_at", r["oom_at"], "max_s", r["max_s_trained"],
                   flush=True)
+    if not a.ablation:
+        out["bucket_common"] = common_bucket_table(out["runs"], a.L)
+        for b, row in out["bucket_common"].items():
+            print("bucket", b, row["sequences"], "adaptive / best static (%s) = %.4f"
+                  % (row["best_static"], row["adaptive_over_best_static"]), flush=True)
     if a.switch_cost:
         ctx = context()
         mixed = None
