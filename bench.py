@@ -288,6 +288,30 @@ def main():
             traffic = None
     attn = {k: (prof[k]["flops"] / (prof[k]["ms"] / 1e3) / 1e12 if prof[k]["ms"] > 0 else 0.0) for k in (1, 2)}
     model_flops = sum((72 * H * H + 6 * s * H) * s for s in args.seqs) * args.steps / P
+
+    # the metric's second half, "max seq len before OOM": the longest s (a multiple of
+    # 1024 P, reading R-15) whose adaptive plan for the L = 32 stack satisfies Eq. 6 on
+    # this device (exact memory model; confirmed by running it in profiles/*oom_frontier*)
+    frontier = None
+    if have_bundle and args.strategy < 0:
+        step_s = 1024 * P
+
+        def feasible(sv):
+            plan, flags = ctx.plan(sv, L_STACK)
+            return not (flags & B.PLAN_INFEASIBLE), plan
+        lo, hi = 0, step_s
+        while feasible(hi)[0] and hi < (1 << 24):
+            lo, hi = hi, hi * 2
+        while hi - lo > step_s:
+            mid = (lo + hi) // 2 // step_s * step_s
+            if feasible(mid)[0]:
+                lo = mid
+            else:
+                hi = mid
+        if lo:
+            frontier = {"s": lo, "layers": L_STACK, "plan": "".join("TUMC"[q] for q in feasible(lo)[1]),
+                        "source": "pds_plan (Algorithm 1, Eq. 6 on the exact memory plan, device capacity "
+                                  "minus the bundle's reserve); measured frontiers in profiles/"}
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -299,7 +323,8 @@ def main():
                    "plan_source": "calibrated bundle" if have_bundle else "no bundle: MegatronTS",
                    "l2": "flushed (256 MB write) between timed iterations; weights 403 MB > L2",
                    "per_seq_tokens_per_s": {str(s): s * args.steps / (per_s[s] / 1e3) for s in args.seqs},
-                   "model_tflops_per_gpu": model_flops / (total_ms / 1e3) / 1e12},
+                   "model_tflops_per_gpu": model_flops / (total_ms / 1e3) / 1e12,
+                   "max_seq_len_before_oom": frontier},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),

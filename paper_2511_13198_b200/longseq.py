@@ -31,7 +31,7 @@ def main():
     ap.add_argument("--seqs", type=int, nargs="+", default=[65536, 131072])
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--strategies", default="0,1,2", help="subset of 0 (TS), 1 (UZ), 2 (METP)")
+    ap.add_argument("--strategies", default="0,1,2,3", help="subset of 0 (TS), 1 (UZ), 2 (METP), 3 (CZ)")
     ap.add_argument("--metp-recompute", type=int, default=0)
     ap.add_argument("--metp-chunks", type=int, default=0)
     a = ap.parse_args()
@@ -48,7 +48,7 @@ def main():
         W = B.Weights(*(w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
         G = B.Grads(*(gr[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
         y, dx = torch.empty_like(x), torch.empty_like(x)
-        for pi, name in ((0, "MegatronTS"), (1, "UlyssesZ"), (2, "METP")):
+        for pi, name in ((0, "MegatronTS"), (1, "UlyssesZ"), (2, "METP"), (3, "MegatronCZ")):
             if pi not in want:
                 continue
             ctx = B.Context(model)
