@@ -718,7 +718,10 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
   static const int env_gm = [] { const char* e = getenv("PDS_GEMM_GM"); return e ? atoi(e) : 0; }();
-  const int group_m = env_gm > 0 ? env_gm : GROUP_M;
+  // CTA-pair raster band: 8 m-blocks (2048 rows).  At fixed clocks 16 was best, but
+  // under the 1000 W power cap 8 reads less DRAM and won 5 of 6 interleaved whole-bench
+  // rounds (+0.7 %, profiles/round1_ab_gemm_group_m*.txt); PDS_GEMM_GM overrides.
+  const int group_m = env_gm > 0 ? env_gm : 8;
   kern<<<2 * ncl, 384, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep, group_m);
   return (int)cudaGetLastError();
 }
