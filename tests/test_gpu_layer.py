@@ -159,6 +159,13 @@ def test_layer_batch2(pi, P):
 
 
 @pytest.mark.parametrize("pi", [0, 1, 2, 3])
+def test_layer_p4_batch2_d128(pi):
+    # b = 2 with d = 128 heads at P = 4 (METP: 2 waves of 128 positions x 2 sequences),
+    # tile-overlapped collectives on
+    _check_layer(pi, 4, 1024, 8, 4096, 1024, seed=14, b=2, chunks=2)
+
+
+@pytest.mark.parametrize("pi", [0, 1, 2, 3])
 def test_layer_p8(pi):
     # eight ranks (the paper's node) on the loopback group: s/P = 128 rows,
     # one head per rank; METP with c = 1 wave
