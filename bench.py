@@ -95,15 +95,27 @@ def cpu_baseline(sample_s=1024, d=None):
     y, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=N_HEADS)
     OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=N_HEADS)
     dt = time.perf_counter() - t0
-    cores = os.cpu_count()
+    cores, blas = os.cpu_count(), "unknown"
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 0) for i in threadpool_info()] + [1])
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"] or threadpool_info()
+        cores = max([i.get("num_threads", 0) for i in info] + [1])
+        blas = ", ".join(f"{i.get('internal_api')} {i.get('version')} ({i.get('architecture')})" for i in info)
     except Exception:
         pass
+    cpu = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     return {"value": sample_s / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"numpy fp64 oracle, one 7B layer (h={H}, n={N_HEADS}, F={FFN}) fwd+bwd at s={sample_s}, "
-                      f"{dt:.2f} s", "seconds": dt}
+                      f"{dt:.2f} s", "seconds": dt,
+            "cpu_model": cpu, "affinity_cores": aff, "os_cpu_count": os.cpu_count(), "blas": blas}
 
 
 def run_reference(args, rank, world):
@@ -128,9 +140,22 @@ def run_reference(args, rank, world):
            "impl": "reference",
            "config": {"workload": "configs[1]: Llama-style 7B layer, seq 4K-32K (oracle sample s=512)",
                       "h": H, "n_heads": N_HEADS, "ffn": FFN, "seq_lens": [512]},
-           "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                               "affinity_cores", "os_cpu_count", "blas")},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def self_launch(n):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 with this same command line, and exit with its code."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 def main():
@@ -143,9 +168,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strategy", type=int, default=-1, help="force a static strategy (default: pds_plan)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -309,7 +338,7 @@ def main():
             else:
                 hi = mid
         if lo:
-            frontier = {"s": lo, "layers": L_STACK, "plan": "".join("TUMC"[q] for q in feasible(lo)[1]),
+            frontier = {"s": lo, "layers": L_STACK, "plan": "".join("TUMCF"[q] for q in feasible(lo)[1]),
                         "source": "pds_plan (Algorithm 1, Eq. 6 on the exact memory plan, device capacity "
                                   "minus the bundle's reserve); measured frontiers in profiles/"}
     out = {
@@ -340,9 +369,17 @@ def main():
                      "norm_ms": prof[3]["ms"], "norm_gbs": (prof[3]["bytes"] / (prof[3]["ms"] / 1e3) / 1e9
                                                              if prof[3]["ms"] > 0 else None)},
     }
+    if world > 1:
+        # collective bus bandwidth at this run's message sizes (torch.distributed's NCCL,
+        # nccl-tests convention), the NVLink side of the roofline
+        from paper_2511_13198_b200.nccl_bw import measure
+        bw = measure(torch, dist, world, h=H, seqs=(max(args.seqs),), reps=5, warm=2)
+        out["nccl_busbw"] = {"unit": "GB/s", "peak_per_direction": 900.0,
+                             "results": [{k: r[k] for k in ("op", "what", "bytes", "busbw_gbs")} for r in bw]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline()
-        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                  "affinity_cores", "os_cpu_count", "blas")}
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()

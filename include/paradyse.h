@@ -50,7 +50,7 @@ typedef enum {
   PDS_ENCCL = -6,          /* NCCL error                                               */
   PDS_ESTATE = -7,         /* call order / state error (e.g. bwd strategy != fwd)      */
   PDS_ENOCOSTS = -8,       /* pds_plan without a loaded cost bundle                    */
-  PDS_ENOTIMPL = -9        /* feature outside this build (e.g. b > 1)                  */
+  PDS_ENOTIMPL = -9        /* feature outside this build (e.g. head dim not 64 / 128)  */
 } pds_status;
 
 /* Strategy ids, stored as uint8_t in plans. */
@@ -58,10 +58,13 @@ typedef enum {
   PDS_MEGATRON_TS = 0,     /* Megatron-LM TP+SP                    */
   PDS_ULYSSES_Z = 1,       /* DeepSpeed Ulysses + ZeRO3 weight gathering*/
   PDS_METP = 2,            /* METP-style chunked, memory-bounded (R-11)  */
-  PDS_MEGATRON_CZ = 3      /* Megatron-LM CP + ZeRO3: context-parallel attention over
+  PDS_MEGATRON_CZ = 3,     /* Megatron-LM CP + ZeRO3: context-parallel attention over
                               the all-gathered Q/K/V (reading R-CZ)     */
+  PDS_METP_FULL = 4        /* METP with Q/K/V also recomputed in bwd (saved 3u + 2l +
+                              lam instead of 6u + ..., SURVEY O-6): the planner's
+                              deepest memory saver, chosen per layer   */
 } pds_strategy;
-#define PDS_N_STRATEGIES 4
+#define PDS_N_STRATEGIES 5
 
 /* pds_plan flags */
 #define PDS_PLAN_INFEASIBLE 1u  /* no plan satisfies Eq. 6; least-memory fallback returned */
@@ -75,14 +78,15 @@ typedef struct {
   int32_t n_heads;        /* attention heads n (d = h / n, d in {64, 128})   */
   int32_t ffn;            /* FFN width F (4h in the paper, Eq. 4)            */
   int32_t n_layers;       /* L                                               */
-  int32_t batch;          /* b (must be 1 in this build)                     */
+  int32_t batch;          /* b >= 1 equal-length sequences (reading Q-35)    */
   float norm_eps;         /* RMSNorm epsilon (1e-5, R-2)                     */
   double rope_theta;      /* RoPE base (10000, R-3)                          */
   int32_t causal;         /* 1 = causal mask (north_star), 0 = none          */
   int32_t metp_chunks;    /* METP wave count c (0 -> P)                      */
-  int32_t metp_recompute; /* 0 = recompute FFN intermediates in bwd (R-11);
-                              1 = also recompute Q/K/V (saved 3u + 2l + lam
-                              instead of 6u + ..., SURVEY O-6); else EINVAL  */
+  int32_t metp_recompute; /* what PDS_METP recomputes in bwd: 0 = the FFN
+                              intermediates (R-11); 1 = also Q/K/V (then
+                              PDS_METP behaves as PDS_METP_FULL); else EINVAL.
+                              PDS_METP_FULL always recomputes Q/K/V.          */
 } pds_model;
 
 typedef struct pds_ctx pds_ctx;     /* opaque: rank, P, comm, streams, arenas, costs, plan cache */
@@ -103,7 +107,13 @@ pds_status pds_nccl_unique_id(void* out128);
  * communicator (collectives are identities).  Otherwise nccl_unique_id (host, 128 B)
  * must be the same on all ranks and the NCCL communicator is created collectively
  * (blocks until all ranks join); P = 1 with an id gives a one-rank NCCL
- * communicator, which runs the NCCL code path on a single GPU. */
+ * communicator, which runs the NCCL code path on a single GPU.
+ * device < 0 (any P in [1, 8], nccl_unique_id = NULL): a HOST-ONLY planner context —
+ * no CUDA or NCCL call is made; pds_load_costs / pds_set_capacity / pds_set_enabled /
+ * pds_plan / pds_cost_eval work as on a device context (capacity from the bundle or
+ * pds_set_capacity), every layer / reserve call returns PDS_ESTATE.
+ * With NCCL and P > 1 the tile-overlapped collectives (pds_set_overlap) start OFF
+ * unless the environment sets PDS_OVERLAP=1 (not yet validated with real peers). */
 pds_status pds_create(const pds_model* model, int32_t P, int32_t rank, int32_t device,
                       const void* nccl_unique_id, pds_ctx** out);
 
@@ -129,8 +139,10 @@ pds_status pds_release_cache(pds_ctx* ctx);
  * selected polynomial (PR, extrapolation) for T_pi(s), plus s_profile_max (Eq. 9). */
 pds_status pds_load_costs(pds_ctx* ctx, const char* bundle_path);
 /* Device capacity (bytes) the plan must stay strictly below (Eq. 6) and the
- * smoothing ratio gamma.  Defaults: cudaMemGetInfo total minus
- * the reserve in the bundle; gamma = 0. */
+ * smoothing ratio gamma.  Defaults: after pds_load_costs, the
+ * bundle's recorded `capacity` minus its `reserve` (the device the bundle was
+ * calibrated on); before any bundle, cudaMemGetInfo's total (0 on a host-only
+ * context); gamma = 0.  Either call clears the (b, s) dictionary. */
 pds_status pds_set_capacity(pds_ctx* ctx, double capacity_bytes, double gamma);
 /* Enable / disable strategies (bit mask; default: all). */
 pds_status pds_set_enabled(pds_ctx* ctx, uint32_t strategy_mask);
@@ -156,8 +168,11 @@ pds_status pds_plan_ex(int32_t L, int32_t n_strat, const double* t_layer, const 
                        const uint8_t* prev_plan, uint8_t* strategy_out, uint32_t* flags_out,
                        int64_t* counters_out);
 
-/* T_pi(s) and M_pi(s) for every strategy (host arrays of PDS_N_STRATEGIES);
- * branch_out (nullable, host int32[3]): 0 = RF, 1 = PR. */
+/* T_pi(s) and M_pi(s) for every strategy (host arrays of PDS_N_STRATEGIES entries):
+ * t_layer[i] = Eq. 9 (RF iff s <= s_profile_max of strategy i, else PR; 1e300 for a
+ * strategy absent from the bundle), m_layer[i] = persistent + saved bytes of one layer
+ * (1e300 where the strategy is invalid at this s, e.g. divisibility);
+ * branch_out (nullable, host int32[PDS_N_STRATEGIES]): 0 = RF, 1 = PR. */
 pds_status pds_cost_eval(pds_ctx* ctx, int64_t seq_len, double* t_layer, double* m_layer,
                          int32_t* branch_out);
 
@@ -206,8 +221,10 @@ pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
  * chunk as soon as the GEMM has stored it ("communication overlapped with GEMM tiles",
  * north_star; the AG / RS of PAPER.md:203); METP does the same per wave, and
  * UlyssesZ sends each head-group block of its sequence -> head All-to-Alls as soon
- * as the packing GEMM has stored it.  on = 1 (default) or 0 (plain in-order
- * collectives).  Results are bit-identical either way.  Ignored at P = 1. */
+ * as the packing GEMM has stored it.  on = 1 or 0 (plain in-order collectives);
+ * default 1 for the loopback group, 0 for an NCCL communicator with P > 1 unless
+ * PDS_OVERLAP=1 (see pds_create).  Results are bit-identical either way.  Ignored at
+ * P = 1. */
 pds_status pds_set_overlap(pds_ctx* ctx, int32_t on);
 /* Debug taps: the next pds_layer_fwd also writes the sublayer deltas O (attention
  * block output) and Z (FFN output), local [s/P, b, h] bf16 (reading R-34).  NULL

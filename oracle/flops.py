@@ -40,8 +40,8 @@ def comm_bytes(pi, h, s, P, ffn=None, b=1, metp_recompute="ffn"):
     fr = (P - 1) / P
     act = s * b * h * 2
     ar = 2 * fr * 2 * h * 4
-    if pi == 0 or pi == 2:   # TS / METP (same bytes, c x more messages)
-        extra = 1 if (pi == 2 and metp_recompute == "full") else 0
+    if pi in (0, 2, 4):      # TS / METP / METP-full (same bytes, c x more messages)
+        extra = 1 if (pi == 4 or (pi == 2 and metp_recompute == "full")) else 0
         return int(round((10 + extra) * fr * act + ar))
     if pi == 1:
         a2a = 2 * fr * (s // P) * b * (3 * h + h) * 2

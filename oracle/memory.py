@@ -9,18 +9,20 @@ this build reads M analytically (R-22, SURVEY O-6):
   saved   TS   = 6u + (F/h)u + 2l + lam   x, r1, QKV(3u), A(1u), LSE, x1, r2, H(F/h u)
           UZ   = 7u + (F/h)u + 2l + lam   as TS + post-A2A attention output (1u)
           METP = 6u + 2l + lam            (metp_recompute = ffn: H recomputed)
-          METP = 3u + 2l + lam            (metp_recompute = full: QKV recomputed too)
-  plan    sum_l (W + saved_{pi_l}) + max_{pi enabled} transient_pi + reserve < capacity
+          METP = 3u + 2l + lam            (metp_recompute = full, and METP-full: QKV recomputed too)
+  plan    sum_l (W + saved_{pi_l}) + max_{pi in plan} workspace_pi + reserve < capacity (R-22)
 
-Pin: the saved formula equals the simulated grid's ledger recount of the
-tensors the sharded simulations keep for backward (tests/test_oracle_memory.py,
-SPEC.md:99); the C1 worked example of SURVEY O-6.  The transient term is the
-workspace plan of the CUDA path (DESIGN.md §Memory) written out independently;
-"parity unpinned" against a measured device peak until the T5 measurement.
+Pins: the saved formula equals the simulated grid's ledger recount of the
+tensors the sharded simulations keep for backward (tests/test_oracle_strategies.py,
+SPEC.md:99); the C1 worked example of SURVEY O-6.  The transient (workspace) term
+of the plan is NOT modelled here exactly — it is a property of an implementation's
+buffer plan.  `transient_floor` is the dataflow lower bound (O-5 / O-6); the
+library's exact workspace is pinned by measuring its device allocation
+(tests/test_gpu_memory.py).  "parity unpinned" for an exact oracle transient.
 """
 from __future__ import annotations
 
-TS, UZ, METP, CZ = 0, 1, 2, 3
+TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
 
 
 def units(h, n, s, P, b=1):
@@ -41,56 +43,61 @@ def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
         return (7 + f) * u + 2 * l + lam
     if pi == METP:
         return (6 if metp_recompute == "ffn" else 3) * u + 2 * l + lam
+    if pi == METP_FULL:
+        return 3 * u + 2 * l + lam
     raise KeyError(pi)
 
 
-def _al(x):
-    return (x + 255) // 256 * 256
-
-
-def _norm_bwd_grid(rows):
-    return min((rows + 3) // 4, 444)   # 148 SMs x 3 resident 256-thread blocks
-
-
-def transient(pi, h, n, ffn, s, P, b=1, metp_chunks=None, metp_recompute="ffn"):
-    """Workspace bytes per rank of the CUDA path's buffer plan,
-    each buffer rounded up to 256 B.  Written out from the plan table, not shared
-    with the library (tests compare it with pds_mem_bytes).  Token buffers hold
-    rows = positions x b (layout [s, b, h])."""
-    sl = s // P
-    u = sl * b * h * 2
-    lam = (n // P) * s * b * 4
-    hl, Fl = h // P, ffn // P
-    small = _al(2 * h * 4)
-    S, SL = s * b, sl * b                  # token rows (all / this rank)
-    if pi == TS:
-        bufs = [S * h * 2, S * h * 2, S * Fl * 2, S * Fl * 2, lam, _norm_bwd_grid(SL) * h * 4,
-                max(Fl, 3 * hl) * S * 2, h * S * 2, h * max(Fl, 3 * hl) * 2]
-        if P > 1:
-            bufs.append(S * h * 2)      # second gather buffer: bwd re-gathers prefetched
-
-    elif pi == UZ:
-        bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
-                u, 3 * u, 3 * u, SL * ffn * 2, SL * ffn * 2, 3 * u, 3 * u, u, lam,
-                _norm_bwd_grid(SL) * h * 4, max(ffn, 3 * h) * SL * 2, h * SL * 2, h * max(ffn, 3 * h) * 2]
-    elif pi == CZ:
-        # full weights + fp32 dW (ZeRO3), gathered Q/K/V of the whole context and the
-        # all-rows dQ/dK/dV partials (RS in place), local FFN / attention scratch
-        bufs = [3 * h * h * 2, h * h * 2, ffn * h * 2, ffn * h * 2, max(3 * h, ffn) * h * 4,
-                u, S * 3 * h * 2, S * 3 * h * 2, SL * ffn * 2, SL * ffn * 2, u, u, lam,
-                _norm_bwd_grid(SL) * h * 4, max(ffn, 3 * h) * SL * 2, h * SL * 2, h * max(ffn, 3 * h) * 2]
-    elif pi == METP:
+def valid(pi, h, n, ffn, s, P, metp_chunks=None):
+    """Reading R-15: the library runs a strategy at (s, P) only when
+    P | s, P | n, 128 | s/P (tile rows), 64 | F/P, and for METP / METP-full also
+    c | s/P and 128 | s/(P c) (c = metp_chunks, default P).  Never padded."""
+    if s <= 0 or s % P or n % P or (s // P) % 128 or ffn % P or (ffn // P) % 64:
+        return False
+    if pi in (METP, METP_FULL):
         c = metp_chunks or P
-        w = sl // c * b                    # rows of one wave per rank
-        uw = w * h * 2
-        bufs = [u, u, P * uw, P * uw, P * uw, P * w * Fl * 2, P * w * Fl * 2, P * w * Fl * 2,
-                S * hl * 2, S * 3 * hl * 2, lam, _norm_bwd_grid(w) * h * 4,
-                max(Fl, 3 * hl) * P * w * 2, h * P * w * 2, h * max(Fl, 3 * hl) * 2]
-        if metp_recompute == "full":
-            bufs.append(S * 3 * hl * 2)     # QKV (fwd, then recomputed in bwd), not saved
-    else:
-        raise KeyError(pi)
-    return sum(_al(x) for x in bufs) + small
+        sl = s // P
+        if sl % c or (sl // c) % 128:
+            return False
+    return True
+
+
+def transient_floor(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
+    """A LOWER BOUND on any implementation's per-rank workspace (bytes) for one layer,
+    from the dataflow of SURVEY O-5 / O-6 (not from this build's buffer table): the
+    non-saved tensors that must be live together at one step of the strategy.
+
+      TS    the row-parallel FC2 step: its input G = GELU(H) [s, F/P] (not saved,
+            (F/h) u) and its output partial [s, h] before the RS (P u)   -> (P + F/h) u
+      UZ    FC2 with the gathered W_out [F, h] (bf16), local G [s/P, F] and output
+            [s/P, h]; backward: the full local fp32 dW_out [F, h] beside G   -> max of both
+      CZ    the context-parallel attention over the all-gathered Q/K/V [s, 3h] (3P u),
+            plus UZ's FC2 step in its own phase                           -> max of both
+      METP  one wave of TS's FC2 step: G [P w, F/P] and partial [P w, h], w = s/(P c)
+            rows of each rank, plus the gathered wave input [P w, h]      -> (2P/c + F/(h c)) u
+      METP-full  as METP plus the recomputed Q/K/V of the own heads [s, 3h/P] (3u)
+
+    O-6's TS ~ 2P u fwd / (2P + 8) u bwd and METP ~ (2P/c + 8/c + 2) u are estimates of
+    an implementation; this floor keeps only what the dataflow cannot avoid.  Pin: the
+    library's workspace is never below it (tests/test_planner_host.py), and the
+    library's reported workspace equals its measured device allocation
+    (tests/test_gpu_memory.py) — "parity unpinned" for any exact transient value."""
+    u, _, _ = units(h, n, s, P, b)
+    f = ffn // h
+    if pi == TS:
+        return (P + f) * u
+    uz = max((f + 1) * u + ffn * h * 2, ffn * h * 4 + f * u)
+    if pi == UZ:
+        return uz
+    if pi == CZ:
+        return max(3 * P * u, uz)
+    c = metp_chunks or P
+    base = (2 * P * u + f * u) // c
+    if pi == METP:
+        return base
+    if pi == METP_FULL:
+        return base + 3 * u
+    raise KeyError(pi)
 
 
 def layer_bytes(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):

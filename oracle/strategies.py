@@ -27,13 +27,15 @@ documented signature.  METP's true external schedule is
 """
 from __future__ import annotations
 
+import copy
+
 import numpy as np
 
 from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
                     rmsnorm, rmsnorm_bwd)
 
-TS, UZ, METP, CZ = 0, 1, 2, 3
-NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ"}
+TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
+NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full"}
 
 
 class Cfg:
@@ -543,7 +545,24 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
     return dx
 
 
-REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd), CZ: (cz_fwd, cz_bwd)}
+def _full(cfg):
+    """METP-full (strategy 4) = R-METP with metp_recompute = 'full' (SURVEY O-5 / O-6),
+    a strategy of its own so the planner can choose it per layer."""
+    c = copy.copy(cfg)
+    c.metp_recompute = "full"
+    return c
+
+
+def metp_full_fwd(grid, xs, W, cfg):
+    return metp_fwd(grid, xs, W, _full(cfg))
+
+
+def metp_full_bwd(grid, dys, saved, W, cfg, grads):
+    return metp_bwd(grid, dys, saved, W, _full(cfg), grads)
+
+
+REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd), CZ: (cz_fwd, cz_bwd),
+            METP_FULL: (metp_full_fwd, metp_full_bwd)}
 
 
 def layer_fwd(pi, grid, xs, W, cfg):

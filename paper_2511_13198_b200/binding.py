@@ -13,9 +13,9 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDS_LIB") or os.path.join(HERE, "libparadyse.so")   # PDS_LIB: A/B builds
 
-TS, UZ, METP, CZ = 0, 1, 2, 3
-STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ"}
-N_STRATEGIES = 4
+TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
+STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full"}
+N_STRATEGIES = 5
 
 STATUS = {0: "PDS_OK", -1: "PDS_EINVAL", -2: "PDS_EDIVISIBILITY", -3: "PDS_ESTRATEGY", -4: "PDS_ENOMEM",
           -5: "PDS_ECUDA", -6: "PDS_ENCCL", -7: "PDS_ESTATE", -8: "PDS_ENOCOSTS", -9: "PDS_ENOTIMPL"}

@@ -29,6 +29,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUNDLES = os.path.join(HERE, "bundles")
+ALL = (0, 1, 2, 3, 4)       # TS, UZ, METP, CZ, METP-full (include/paradyse.h)
 
 
 def aic_poly(s, y):
@@ -139,6 +140,8 @@ def comm_bytes_per_rank(pi, h, F, s, P):
     act = s * h * 2
     if pi in (0, 2):
         return 10 * fr * act + 2 * fr * 8 * h
+    if pi == 4:              # METP-full: TS bytes + one more AG(u) for the Q/K/V recompute
+        return 11 * fr * act + 2 * fr * 8 * h
     wb = 4 * h * h + 2 * h * F
     if pi == 3:              # CZ: AG(QKV) fwd + re-gather bwd + RS(dQKV), ZeRO3 weights
         return 3 * fr * 3 * act + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
@@ -161,20 +164,20 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
     import torch
     from . import binding as B
     model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L)
-    records = {0: [], 1: [], 2: [], 3: []}
+    records = {pi: [] for pi in ALL}
     if P_target == 1:
         ctx = B.Context(model)
         for s in grid:
             w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
             # strategies interleaved rep by rep (one warm-up pass each first), so slow drift
             # of the power-capped clock does not favour whichever strategy runs last
-            for pi in (0, 1, 2, 3):
+            for pi in ALL:
                 time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=1)
-            ts = {pi: [] for pi in (0, 1, 2, 3)}
+            ts = {pi: [] for pi in ALL}
             for _ in range(reps):
-                for pi in (0, 1, 2, 3):
+                for pi in ALL:
                     ts[pi].append(time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0))
-            for pi in (0, 1, 2, 3):
+            for pi in ALL:
                 t = float(np.median(ts[pi]))
                 records[pi].append((int(s), t))
                 print(f"P=1 s={s} pi={pi} t={t * 1e3:.3f} ms", flush=True)
@@ -192,9 +195,9 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         for s in grid:
             t_unit, t_gemm = {}, {}
             t_att = 0.0
-            for pi in (0, 1, 2, 3):
+            for pi in ALL:
                 w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
-                cx = ctx_m if pi == 2 else ctx
+                cx = ctx_m if pi in (2, 4) else ctx
                 t1 = time_layer(torch, B, cx, pi, s, w, gr, x, dy, reps=reps)
                 t_unit[pi] = t1
                 t_gemm[pi] = class_seconds(torch, B, cx, pi, s, w, gr, x, dy, (0,))
@@ -202,19 +205,19 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                     t_att = class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, (1, 2))
                 del w, gr, x, dy
             torch.cuda.empty_cache()
-            for pi in (0, 1, 2, 3):
+            for pi in ALL:
                 comp = t_unit[pi] / P
                 if pi == 3 and model.causal:
                     # contiguous context chunks: the last rank's queries see every key, so
                     # its causal attention share is (2P - 1) / P^2 instead of 1 / P
                     comp += t_att * ((2 * P - 1) / (P * P) - 1.0 / P)
                 comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
-                if pi in (0, 2):
+                if pi in (0, 2, 4):
                     # tile-overlapped AG / RS: each runs under the GEMM that
                     # consumes / produces it (those GEMMs carry 48h^2 of the 72h^2 GEMM
                     # flops per token); at least one chunk per collective stays exposed
                     comm = max(comm / P, comm - (2.0 / 3.0) * t_gemm[pi] / P)
-                extra = (2 * P - 1) * 8e-6 * (P if pi == 2 else 1)   # collective launch latency
+                extra = (2 * P - 1) * 8e-6 * (P if pi in (2, 4) else 1)   # collective launch latency
                 if pi == 3:
                     extra += 6 * 8e-6 * (P - 1)                           # part-wise weight AG / RS
                 records[pi].append((int(s), comp + comm + extra))
@@ -231,6 +234,57 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
     return path
 
 
+def profile_measured(h, n, ffn, L, grid, out_dir=BUNDLES, reps=3):
+    """P > 1 MEASURED: run under torchrun with one rank per GPU (WORLD_SIZE = P), e.g.
+      python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 \
+          -m paper_2511_13198_b200.calibrate --measured
+    Every rank runs the strategy's layer fwd + bwd on its [s/P, h] shard over NCCL;
+    the layer time is the max over ranks of the device-timed median (CUDA events on
+    the launching stream).  Rank 0 fits and exports the bundle."""
+    import torch
+    import torch.distributed as dist
+    from . import binding as B
+    rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [B.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L)
+    ctx = B.Context(model, P=P, rank=rank, device=local, uid=obj[0])
+    records = {pi: [] for pi in ALL}
+    for s in grid:
+        if s % (P * 128) or (s // P) % (P * 128):
+            continue                                  # METP waves need s/(P c) % 128 == 0, c = P
+        w, gr, x, dy = make_layer_buffers(torch, model, P, s, seed=1 + rank)
+        for pi in ALL:
+            time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=1)
+        ts = {pi: [] for pi in ALL}
+        for _ in range(reps):
+            for pi in ALL:
+                ts[pi].append(time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0))
+        med = torch.tensor([float(np.median(ts[pi])) for pi in ALL], dtype=torch.float64, device="cuda")
+        dist.all_reduce(med, op=dist.ReduceOp.MAX)
+        for i, pi in enumerate(ALL):
+            records[pi].append((int(s), float(med[i])))
+        if rank == 0:
+            print(f"P={P} s={s} " + " ".join(f"pi{pi}={float(med[i]) * 1e3:.3f}ms" for i, pi in enumerate(ALL)),
+                  flush=True)
+        del w, gr, x, dy
+        torch.cuda.empty_cache()
+    ctx.close()
+    path = None
+    if rank == 0:
+        os.makedirs(out_dir, exist_ok=True)
+        path = os.path.join(out_dir, f"h{h}_n{n}_f{ffn}_P{P}.txt")
+        cap = float(torch.cuda.get_device_properties(local).total_memory)
+        fit_and_export(path, P, h, n, ffn, L, records, capacity=cap, reserve=8.0 * 2 ** 30,
+                       note=f"measured: device-timed one-layer fwd+bwd on {P} B200 over NCCL, max over ranks")
+    dist.barrier()
+    dist.destroy_process_group()
+    return path
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--P", type=int, nargs="+", default=[1])
@@ -241,7 +295,12 @@ if __name__ == "__main__":
     ap.add_argument("--grid", type=int, nargs="+",
                     default=[1024, 2048, 4096, 8192, 16384, 32768, 65536])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--measured", action="store_true", help="P = WORLD_SIZE ranks under torchrun, over NCCL")
     a = ap.parse_args()
+    if a.measured:
+        grid = a.grid if a.grid != ap.get_default("grid") else [8192, 16384, 32768, 65536, 131072]
+        print(profile_measured(a.h, a.n, a.ffn, a.L, grid, reps=a.reps))
+        raise SystemExit(0)
     for P in a.P:
         t0 = time.time()
         print(profile(P, a.h, a.n, a.ffn, a.L, a.grid, reps=a.reps), f"{time.time() - t0:.1f}s")

@@ -22,6 +22,7 @@ void set_error(const std::string& msg);
   do {                                                                              \
     cudaError_t e__ = (cudaError_t)(expr);                                          \
     if (e__ != cudaSuccess) {                                                       \
+      cudaGetLastError(); /* a failed call must not resurface in a later check */  \
       ::pds::set_error(std::string(#expr) + ": " + cudaGetErrorString(e__));        \
       return e__ == cudaErrorMemoryAllocation ? PDS_ENOMEM : PDS_ECUDA;             \
     }                                                                               \

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -896,7 +897,7 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   const int64_t slot = e.r * wr * e.h * 2;
   const char* xb = static_cast<const char*>(x);
   // metp_recompute = full: Q/K/V live in the workspace (recomputed in bwd), not saved
-  char* qkv = e.m.metp_recompute ? ws + bp.ws_off("qkv") : sv->at("qkv");
+  char* qkv = bp.has_ws("qkv") ? ws + bp.ws_off("qkv") : sv->at("qkv");
   // Wave gathers run on a side stream one wave ahead of the GEMMs ("asynchronous
   // ring-based execution"): AG(k+1) into one of two buffers while the
   // GEMM of wave k reads the other.  At P = 1 the gathers are identities.
@@ -1017,7 +1018,7 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
     PDS_TRY(tn.dw(sv->at("a"), e.hl, wg, e.h, W, e.hl, e.h, g->dw_proj, EPI_F32_ACC, wr, e.sl, o));
   }
   char* qkv = sv->plan.has_ws("qkv") ? ws + bp.ws_off("qkv") : sv->at("qkv");
-  if (e.m.metp_recompute) {           // full: Q/K/V recomputed from per-wave re-gathers of u
+  if (bp.has_ws("qkv")) {             // full: Q/K/V recomputed from per-wave re-gathers of u
     for (int64_t k = 0; k < c; ++k) {
       const int64_t o = k * wr;
       PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
@@ -1095,6 +1096,7 @@ pds_status alloc_saved(pds_ctx* c, int64_t bytes, char** out) {
 
 pds_status check_layer(pds_ctx* c, uint8_t strategy, int64_t s) {
   if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (c->device < 0) PDS_FAIL(PDS_ESTATE, "host-only planner context (device < 0) runs no layer");
   if (strategy >= PDS_N_STRATEGIES) PDS_FAIL(PDS_ESTRATEGY, "unknown strategy id " + std::to_string(strategy));
   return PDS_OK;
 }
@@ -1116,6 +1118,10 @@ static pds_status ctx_common(pds_ctx* c, const pds_model* m, int P, int rank, in
   c->device = device;
   BufPlan probe;
   PDS_TRY(make_plan(c->m, P, PDS_MEGATRON_TS, (int64_t)128 * P, &probe));   // validates dims
+  if (device < 0) {            // host-only planner context: no CUDA call, capacity from the bundle
+    c->capacity = 0;
+    return PDS_OK;
+  }
   PDS_CUDA(cudaSetDevice(device));
   size_t fr = 0, tot = 0;
   PDS_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -1128,6 +1134,11 @@ extern "C" pds_status pds_create(const pds_model* model, int32_t P, int32_t rank
   if (!out) PDS_FAIL(PDS_EINVAL, "NULL out");
   std::unique_ptr<pds_ctx> c(new pds_ctx());
   PDS_TRY(ctx_common(c.get(), model, P, rank, device));
+  if (device < 0) {            // planner only (pds_plan / pds_cost_eval): no communicator
+    if (nccl_unique_id) PDS_FAIL(PDS_EINVAL, "a host-only context (device < 0) takes no NCCL id");
+    *out = c.release();
+    return PDS_OK;
+  }
   if (P == 1 && !nccl_unique_id) {
     c->comm = make_self_comm();
   } else {       // P = 1 with an id: a one-rank NCCL communicator (exercises the NCCL path)
@@ -1135,6 +1146,12 @@ extern "C" pds_status pds_create(const pds_model* model, int32_t P, int32_t rank
     pds_status st = PDS_OK;
     c->comm = make_nccl_comm(P, rank, nccl_unique_id, &st);
     if (st != PDS_OK) return st;
+    // The tile-overlapped collectives (persistent GEMMs polling flags that a CTA-capped
+    // NCCL side communicator sets) have run on one GPU only (loopback, one-rank NCCL);
+    // with real peers they are opt-in until tests/test_multigpu_nccl.py has passed on
+    // the hardware: PDS_OVERLAP=1 or pds_set_overlap(ctx, 1).
+    const char* ov = getenv("PDS_OVERLAP");
+    if (P > 1) c->overlap = ov && atoi(ov) != 0;
   }
   *out = c.release();
   return PDS_OK;
@@ -1177,14 +1194,17 @@ extern "C" pds_status pds_create_loopback(const pds_model* model, pds_group* g, 
 
 extern "C" pds_status pds_destroy(pds_ctx* c) {
   if (!c) return PDS_OK;
-  cudaSetDevice(c->device);
-  cudaDeviceSynchronize();
+  if (c->device >= 0) {
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+  }
   delete c;
   return PDS_OK;
 }
 
 extern "C" pds_status pds_reserve(pds_ctx* c, int64_t max_seq_len, uint32_t mask) {
   if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (c->device < 0) PDS_FAIL(PDS_ESTATE, "host-only planner context (device < 0)");
   int64_t need = 0;
   for (int i = 0; i < PDS_N_STRATEGIES; ++i) {
     if (!(mask >> i & 1)) continue;
@@ -1199,6 +1219,7 @@ extern "C" pds_status pds_reserve(pds_ctx* c, int64_t max_seq_len, uint32_t mask
 
 extern "C" pds_status pds_release_cache(pds_ctx* c) {
   if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (c->device < 0) return PDS_OK;
   PDS_CUDA(cudaSetDevice(c->device));
   PDS_CUDA(cudaDeviceSynchronize());
   for (auto& kv : c->free_blocks) cudaFree(kv.second);
@@ -1302,7 +1323,7 @@ extern "C" pds_status pds_layer_step_host(pds_ctx* c, uint8_t strategy, int64_t 
   if (seq_len <= 0 || seq_len % c->P) PDS_FAIL(PDS_EDIVISIBILITY, "seq_len not divisible by P");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   PDS_CUDA(cudaSetDevice(c->device));
-  const int64_t nb = seq_len / c->P * c->m.h * 2;       // one local [s/P, b, h] bf16 activation
+  const int64_t nb = seq_len / c->P * c->m.batch * c->m.h * 2;   // one local [s/P, b, h] bf16 activation
   const int64_t slot = (nb + 255) / 256 * 256;
   if (!c->up_st) {
     PDS_CUDA(cudaStreamCreateWithFlags(&c->up_st, cudaStreamNonBlocking));
@@ -1456,7 +1477,9 @@ extern "C" pds_status pds_plan(pds_ctx* c, int64_t s, uint8_t* out, int32_t L, u
     flags |= (inf ? PDS_PLAN_INFEASIBLE : 0u) | (early ? PDS_PLAN_EARLY : 0u);
     c->cache[key] = std::make_pair(plan, inf);
   }
-  if (c->gamma > 0 && (int)c->prev.size() == L && c->prev != plan) {
+  // smoothing (R-19) exactly as pds_plan_ex: keep the previous plan if it is valid,
+  // feasible and within (1 + gamma) of the new one (gamma = 0: only exact time ties)
+  if ((int)c->prev.size() == L && c->prev != plan) {
     if (need_costs) PDS_TRY(costs(c, s, t, mm, nullptr, ws));
     bool valid = true;
     for (uint8_t p : c->prev) valid &= (c->enabled >> p & 1) && mm[p] < 1e299;

@@ -287,14 +287,16 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "wt", h * std::max(F, 3 * h) * 2);
       break;
     }
-    case PDS_METP: {
+    case PDS_METP:
+    case PDS_METP_FULL: {
       const int64_t c = m.metp_chunks > 0 ? m.metp_chunks : P;
       if (sl % c) PDS_FAIL(PDS_EDIVISIBILITY, "s/P not divisible by metp_chunks");
       const int64_t w = sl / c;
       if (w % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/(P*metp_chunks)=" + std::to_string(w) + " must be a multiple of 128");
       if (m.metp_recompute != 0 && m.metp_recompute != 1)
         PDS_FAIL(PDS_EINVAL, "metp_recompute must be 0 (ffn) or 1 (full)");
-      const bool full = m.metp_recompute == 1;     // QKV recomputed in bwd, not saved
+      // QKV recomputed in bwd, not saved
+      const bool full = strategy == PDS_METP_FULL || m.metp_recompute == 1;
       const int64_t W = w * m.batch;               // rows of one wave per rank
       const int64_t uw = W * h * 2;
       push(p.saved, ts, "rstd1", ell);

@@ -132,25 +132,25 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, 
     return res
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p1_c1(pi):
     # C1 shapes (h=256, n=4, d=64, F=1024, s=512), P = 1: every strategy degenerates
     _check_layer(pi, 1, 256, 4, 1024, 512)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p2_c1(pi):
     # C1 at P = 2 (the configs[0] case), METP with c = 2 waves
     _check_layer(pi, 2, 256, 4, 1024, 512)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p4_d128(pi):
     # d = 128 heads, P = 4, METP c = 2 waves of 128 rows per rank
     _check_layer(pi, 4, 1024, 8, 4096, 1024, chunks=2)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("P", [1, 2])
 def test_layer_batch2(pi, P):
     # b = 2 independent sequences in the [s/P, b, h] boundary layout (Table 1's b,
@@ -158,21 +158,21 @@ def test_layer_batch2(pi, P):
     _check_layer(pi, P, 256, 4, 1024, 512, seed=13, b=2, chunks=2 if P == 1 else 0)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p4_batch2_d128(pi):
     # b = 2 with d = 128 heads at P = 4 (METP: 2 waves of 128 positions x 2 sequences),
     # tile-overlapped collectives on
     _check_layer(pi, 4, 1024, 8, 4096, 1024, seed=14, b=2, chunks=2)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p8(pi):
     # eight ranks (the paper's node) on the loopback group: s/P = 128 rows,
     # one head per rank; METP with c = 1 wave
     _check_layer(pi, 8, 1024, 8, 4096, 1024, seed=8, chunks=1)
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_bert_shape_noncausal(pi):
     # Table 4's BERT layer (h = 1024, 16 heads of d = 64, F = 4h, bidirectional) at P = 2
     _check_layer(pi, 2, 1024, 16, 4096, 512, seed=4, causal=False)
@@ -246,22 +246,22 @@ def test_overlap_bit_identical(pi, P, h, n, F, s, chunks):
 def test_switched_chain_p2():
     # a 4-layer stack with a switched plan; boundary tensors pass unchanged (R-31)
     P, h, n, F, s = 2, 256, 4, 1024, 512
-    plan = [2, 0, 3, 1]
-    layers = [layer_inputs(h, n, F, s, 1, seed=5, layer=i) for i in range(4)]
+    plan = [2, 0, 3, 1, 4]                     # every strategy once, METP-full last
+    layers = [layer_inputs(h, n, F, s, 1, seed=5, layer=i) for i in range(len(plan))]
     yd = layers[0]["x"]
     caches = []
     for L in layers:
         yd, cc = OL.layer_fwd(yd, L["w_qkv"], L["w_proj"], L["w_in"], L["w_out"], L["g1"], L["g2"], n=n)
         caches.append(cc)
     dd = layers[0]["dy"]
-    for i in reversed(range(4)):
+    for i in reversed(range(len(plan))):
         L = layers[i]
         dd = OL.layer_bwd(dd, caches[i], L["w_qkv"], L["w_proj"], L["w_in"], L["w_out"], L["g1"], L["g2"],
                           n=n)["dx"]
     xs = OS.shard_act(layers[0]["x"], P)
     dys = OS.shard_act(layers[0]["dy"], P)
     rpl = []
-    for i in range(4):
+    for i in range(len(plan)):
         W = OS.shard_weights(layers[i], n, P)
         rpl.append([Rank(W, r, xs[r], dys[r]) for r in range(P)])
     outs = run_ranks(B.Model(h=h, n_heads=n, ffn=F), P, plan, rpl, xs, dys, taps=False)
@@ -287,13 +287,15 @@ def test_layer_errors():
 
 
 def test_plan_strategy_masks():
-    # pds_set_enabled covers all four strategies: each alone yields its uniform plan
+    # pds_set_enabled covers every strategy of the bundle: each alone yields its uniform plan
     import os
+    from oracle import costmodel as CM
+    path = os.path.join(os.path.dirname(B.__file__), "bundles", "h4096_n32_f16384_P1.txt")
     m = B.Model(h=4096, n_heads=32, ffn=16384, n_layers=8)
     ctx = B.Context(m)
-    ctx.load_costs(os.path.join(os.path.dirname(B.__file__), "bundles", "h4096_n32_f16384_P1.txt"))
+    ctx.load_costs(path)
     ctx.set_capacity(1e15, 0.0)
-    for pi in range(B.N_STRATEGIES):
+    for pi in sorted(CM.read_bundle(path)["strat"]):
         ctx.set_enabled(1 << pi)
         plan, _ = ctx.plan(8192, 8)
         assert plan == [pi] * 8, (pi, plan)
@@ -303,18 +305,19 @@ def test_plan_strategy_masks():
     ctx.close()
 
 
-@pytest.mark.parametrize("pi", [0, 2])
-def test_step_host(pi):
+@pytest.mark.parametrize("pi,b", [(0, 1), (2, 1), (0, 2), (4, 2)])
+def test_step_host(pi, b):
     """pds_layer_step_host (host x, dy in; host y, dx out; copies overlapped on a copy
-    stream) equals the device-pointer fwd + bwd bit for bit and the oracle within TOL."""
+    stream) equals the device-pointer fwd + bwd bit for bit and the oracle within TOL,
+    b = 1 and b = 2 sequences (staging holds s/P x b x h)."""
     h, n, F, s = 256, 4, 1024, 512
-    d = layer_inputs(h, n, F, s, 1, seed=3)
+    d = layer_inputs(h, n, F, s, b, seed=3)
     y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
     g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
     W = OS.shard_weights(d, n, 1)
     R1 = Rank(W, 0, d["x"], d["dy"])
     R2 = Rank(W, 0, d["x"], d["dy"])
-    ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F))
+    ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F, batch=b))
     st = torch.cuda.current_stream()
     sv = ctx.layer_fwd(pi, s, R1.x.data_ptr(), R1.weights(), R1.y.data_ptr(), st.cuda_stream)
     ctx.layer_bwd(pi, R1.dy.data_ptr(), sv, R1.weights(), R1.grads(), R1.dx.data_ptr(), st.cuda_stream)
@@ -335,12 +338,12 @@ def test_step_host(pi):
     assert torch.equal(yh, R1.y.cpu()) and torch.equal(dxh, R1.dx.cpu())
     for k in R1.g:
         assert torch.equal(R1.g[k], R2.g[k]), k
-    assert rel(host(yh)[:, None, :], y_ref) < TOL
-    assert rel(host(dxh)[:, None, :], g_ref["dx"]) < TOL
+    assert rel(host(yh).reshape(s, b, h), y_ref) < TOL
+    assert rel(host(dxh).reshape(s, b, h), g_ref["dx"]) < TOL
     ctx.close()
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_nccl_one_rank_equals_self(pi):
     """The NCCL backend (a one-rank communicator: pds_create with P = 1 and a unique
     id) runs every collective of the strategy, METP's side-stream wave gathers on a

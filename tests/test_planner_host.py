@@ -1,0 +1,215 @@
+"""H1-H3 end to end on the host: the library's cost evaluation (Eq. 9)
+and its stateful planner pds_plan (Algorithm 1 + dictionary D + gamma smoothing,
+PAPER.md:147-187, 263-277) against the oracle, on the committed calibrated bundles,
+through a host-only planner context (pds_create with device < 0: no GPU needed).
+
+Oracle side: T from oracle.costmodel (its own bundle reader, forest walk, Horner
+polynomial, feature map), M from oracle.memory (saved + persistent, pinned by the
+ledger recount), strategy validity from oracle.memory.valid (R-15), Algorithm 1,
+D and smoothing from oracle.selector.  The one library-supplied input is the
+per-strategy workspace w of reading R-22 (an implementation property, pinned by the
+device measurement of tests/test_gpu_memory.py, and bounded below here by the
+dataflow floor)."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle import costmodel as CM
+from oracle import memory as OM
+from oracle import selector as OA
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUNDLES = sorted(glob.glob(os.path.join(ROOT, "paper_2511_13198_b200", "bundles", "*.txt")))
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2511_13198_b200 import binding
+    binding.lib()
+    return binding
+
+
+# ---------------------------------------------------------------- pins of the oracle's Eq. 9 pieces
+def test_poly_eval_pin():
+    # hand value: 2 x^2 - 3 x + 1 at x = s / scale = 4 / 2 = 2 -> 3
+    assert CM.poly_eval([2.0, -3.0, 1.0], 2.0, 4.0) == 3.0
+    # an independent library routine: numpy.polyval (highest degree first)
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        deg = int(rng.integers(0, 4))
+        coef = list(rng.standard_normal(deg + 1))
+        scale = float(rng.uniform(1e3, 1e6))
+        s = float(rng.uniform(1, 2e6))
+        assert CM.poly_eval(coef, scale, s) == pytest.approx(float(np.polyval(coef, s / scale)), rel=1e-12, abs=1e-12)
+    # a reversed coefficient order (a plausible bug) is caught
+    assert CM.poly_eval([1.0, 0.0, 0.0], 1.0, 3.0) == 9.0
+
+
+def test_features_pin():
+    norm = [(4096.0, 4096.0), (32.0, 32.0), (32.0, 32.0), (1024.0, 65536.0)]
+    # hand-computed: one-hot over the enabled (present) strategies in id order, then the
+    # normalised (h, n, L, s); a degenerate range normalises to 0 (R-25)
+    v = CM.features(2, [0, 1, 2, 3], 4096, 32, 32, 33280, norm)
+    assert list(v) == [0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.5]
+    v = CM.features(3, [0, 3, 1], 4096, 32, 32, 1024, norm)          # sorted: [0, 1, 3]
+    assert list(v) == [0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 0.0]
+    v = CM.features(0, [0, 1, 2, 3, 4], 8192, 64, 8, 65536,
+                    [(4096.0, 12288.0), (32.0, 96.0), (8.0, 32.0), (1024.0, 65536.0)])
+    assert list(v) == [1.0, 0.0, 0.0, 0.0, 0.0, 0.5, 0.5, 0.0, 1.0]
+
+
+def test_predict_time_branches():
+    # Eq. 9 dispatch on a two-node forest and a degree-1 polynomial
+    tree = dict(feature=[4, -2, -2], threshold=[0.5, -2.0, -2.0], left=[1, -1, -1], right=[2, -1, -1],
+                value=[0.0, 10.0, 20.0])
+    e = dict(s_profile_max=1000.0, trees=[tree, tree], poly_coef=[2.0, 1.0], poly_scale=1000.0)
+    xlo = np.array([1.0, 0.0, 0.0, 0.0, 0.25])
+    xhi = np.array([1.0, 0.0, 0.0, 0.0, 0.75])
+    assert CM.predict_time(e, xlo, 1000) == (10.0, "rf")            # s = s_profile_max: RF
+    assert CM.predict_time(e, xhi, 500) == (20.0, "rf")
+    assert CM.predict_time(e, xhi, 1001) == (2.0 * 1.001 + 1.0, "pr")   # s_profile_max + 1: PR
+
+
+# ---------------------------------------------------------------- library vs oracle on the bundles
+def _bundle_ctx(B, path):
+    bd = CM.read_bundle(path)
+    hd = bd["hdr"]
+    ctx = B.Context(B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=hd["L"]), P=hd["P"], device=-1)
+    ctx.load_costs(path)
+    return ctx, bd
+
+
+def _oracle_costs(bd, s, present):
+    hd = bd["hdr"]
+    t, br = {}, {}
+    for pi in present:
+        x = CM.features(pi, present, hd["h"], hd["n"], hd["L"], s, bd["norm"])
+        t[pi], br[pi] = CM.predict_time(bd["strat"][pi], x, s)
+    return t, br
+
+
+def _lengths(bd, n=220, seed=0):
+    P = bd["hdr"]["P"]
+    smax = max(e["s_profile_max"] for e in bd["strat"].values())
+    rng = np.random.default_rng(seed)
+    ls = set(int(v) for v in np.exp(rng.uniform(np.log(128), np.log(3 * smax), n)))
+    for e in bd["strat"].values():       # the Eq. 9 boundary and one past it
+        ls |= {int(e["s_profile_max"]), int(e["s_profile_max"]) + 1, int(e["s_profile_max"]) + P * 128}
+    return sorted(ls)
+
+
+@pytest.mark.parametrize("path", BUNDLES, ids=[os.path.basename(p) for p in BUNDLES])
+def test_cost_eval_vs_oracle(B, path):
+    assert BUNDLES, "no committed bundles"
+    ctx, bd = _bundle_ctx(B, path)
+    hd = bd["hdr"]
+    h, n, F, P = hd["h"], hd["n"], hd["ffn"], hd["P"]
+    present = sorted(bd["strat"])
+    n_rf = n_pr = 0
+    ls = _lengths(bd)
+    assert len(ls) >= 200
+    for s in ls:
+        t, m, br = ctx.cost_eval(s)
+        to, bro = _oracle_costs(bd, s, present)
+        for pi in range(B.N_STRATEGIES):
+            if pi not in present:
+                assert t[pi] == 1e300
+                continue
+            assert t[pi] == pytest.approx(to[pi], rel=1e-12, abs=0), (s, pi)
+            assert br[pi] == (0 if bro[pi] == "rf" else 1), (s, pi)
+            n_rf += bro[pi] == "rf"
+            n_pr += bro[pi] == "pr"
+            if OM.valid(pi, h, n, F, s, P):
+                assert m[pi] == OM.layer_bytes(pi, h, n, F, s, P), (s, pi)
+            else:
+                assert m[pi] == 1e300, (s, pi)
+    assert n_rf > 100 and n_pr > 100
+    ctx.close()
+
+
+def _plan_oracle(bd, B, s, L, mask, cap, gamma, cache, prev, wlib):
+    hd = bd["hdr"]
+    h, n, F, P = hd["h"], hd["n"], hd["ffn"], hd["P"]
+    present = sorted(bd["strat"])
+    t, _ = _oracle_costs(bd, s, present)
+    en = [pi for pi in present if (mask >> pi) & 1 and OM.valid(pi, h, n, F, s, P)]
+    m = {pi: float(OM.layer_bytes(pi, h, n, F, s, P)) for pi in en}
+    w = {pi: float(wlib(pi, s)) for pi in en}
+    assert all(w[pi] >= OM.transient_floor(pi, h, n, F, s, P) for pi in en)
+    cached = (1, s) in cache
+    plan, inf = OA.alg1(L, t, m, en, cap, cache=cache, key=(1, s), w=w)
+    plan2, kept = OA.smooth(plan, prev, t, m, cap, gamma, en, w=w)
+    flags = (B.PLAN_CACHED if cached else 0) | (B.PLAN_SMOOTHED if kept else 0) | \
+            (B.PLAN_INFEASIBLE if inf and not kept else 0)
+    return plan2, flags
+
+
+@pytest.mark.parametrize("path", BUNDLES, ids=[os.path.basename(p) for p in BUNDLES])
+@pytest.mark.parametrize("gamma", [0.0, 0.05])
+def test_plan_sequence_vs_oracle(B, path, gamma):
+    """A sequence of pds_plan calls (curriculum-ish order with repeats -> dictionary
+    hits, a strategy-mask change mid-way, a capacity change) equals the oracle's
+    Algorithm 1 + D + smoothing bit for bit, flags included."""
+    ctx, bd = _bundle_ctx(B, path)
+    hd = bd["hdr"]
+    P, L = hd["P"], hd["L"]
+    wl = {}
+
+    def wlib(pi, s):
+        if (pi, s) not in wl:
+            m = B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=L)
+            wl[(pi, s)] = B.mem_bytes(m, P, pi, s)[1]
+        return wl[(pi, s)]
+
+    cap = hd["capacity"] - hd["reserve"]
+    rng = np.random.default_rng(7 + P)
+    q = P * 128
+    base = [int(v) // q * q + q for v in np.exp(rng.uniform(np.log(q), np.log(1.2e6 if P > 1 else 2.4e5), 120))]
+    # ascending (curriculum), then repeats, then a fine sweep down and up again (plans
+    # flip back and forth between neighbouring lengths: smoothing's case)
+    fine = sorted({int(v) // q * q + q for v in np.geomspace(q, 1.2e6 if P > 1 else 2.4e5, 90)})
+    seq = sorted(base) + list(rng.choice(base, 60)) + fine[::-1] + fine
+    all_mask = (1 << B.N_STRATEGIES) - 1
+    masks = {0: all_mask, 90: all_mask & ~(1 << B.TS), 130: all_mask & ~(1 << B.METP), 180: all_mask}
+    cache, prev, mask = {}, None, all_mask
+    ctx.set_capacity(cap, gamma)
+    seen = {"cached": 0, "smoothed": 0, "inf": 0, "mixed": 0}
+    for i, s in enumerate(seq):
+        if i in masks and masks[i] != mask:
+            mask = masks[i]
+            ctx.set_enabled(mask)                # clears D and the previous plan
+            cache, prev = {}, None
+        if i == 150:
+            cap *= 0.8
+            ctx.set_capacity(cap, gamma)         # clears D, keeps the previous plan
+            cache = {}
+        got, fl = ctx.plan(s, L)
+        ref, rfl = _plan_oracle(bd, B, s, L, mask, cap, gamma, cache, prev, wlib)
+        assert got == ref, (i, s, got, ref)
+        keep = B.PLAN_CACHED | B.PLAN_SMOOTHED | B.PLAN_INFEASIBLE
+        assert fl & keep == rfl, (i, s, fl, rfl)
+        prev = got
+        seen["cached"] += bool(fl & B.PLAN_CACHED)
+        seen["smoothed"] += bool(fl & B.PLAN_SMOOTHED)
+        seen["inf"] += bool(fl & B.PLAN_INFEASIBLE)
+        seen["mixed"] += len(set(got)) > 1
+    assert seen["cached"] > 20 and seen["inf"] > 0 and seen["mixed"] > 0, seen
+    if gamma > 0:
+        assert seen["smoothed"] > 0, seen
+    ctx.close()
+
+
+def test_host_only_context_rejects_layer_calls(B):
+    ctx = B.Context(B.Model(h=256, n_heads=4, ffn=1024), P=2, device=-1)
+    with pytest.raises(B.PdsError) as e:
+        ctx.layer_fwd(0, 512, 1, B.Weights(1, 1, 1, 1, 1, 1), 1)
+    assert e.value.code == -7
+    with pytest.raises(B.PdsError) as e:
+        ctx.plan(512, 4)                         # no bundle loaded
+    assert e.value.code == -8
+    with pytest.raises(B.PdsError) as e:
+        ctx.reserve(512)
+    assert e.value.code == -7
+    ctx.close()
