@@ -139,3 +139,18 @@ def test_mem_bytes_batch_vs_oracle(B, b):
             # token buffers scale with b: every term of the workspace but the weights does
             _, tr1, _ = B.mem_bytes(B.Model(h=h, n_heads=n, ffn=F, batch=1), P, pi, s)
             assert tr > tr1
+
+
+def test_product_library_is_tcgen05_only(B):
+    """Every tensor-core instruction in libparadyse.so is tcgen05 (UTCHMMA / UTCQMMA):
+    no warp-level mma.sync (HMMA) kernel ships in the product (the round-1 FA2
+    baseline lives in tools/fa2_sync_baseline.cu)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([exe, "-sass", B.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    ops = re.findall(r"^\s+/\*[0-9a-f]+\*/\s+([A-Z0-9_]+)", sass, re.M)
+    assert "UTCHMMA" in ops and "UTMALDG" in ops
+    assert not [o for o in ops if o.startswith("HMMA")], "legacy mma.sync in the product library"

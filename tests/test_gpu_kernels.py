@@ -236,27 +236,6 @@ def test_attention_bwd_warpgroup_variants_bitwise(tmp_path):
     assert rel(f32["4"][:, :hq], f32[""][:, :hq]) < 1e-3
 
 
-def test_attention_sync_baseline_matches_tcgen05(tmp_path):
-    """The warp-level mma.sync FA2 kernels kept as the A/B baseline (PDS_ATTN_FWD /
-    PDS_ATTN_BWD = sync) agree with the tcgen05 path within the bf16 tolerance."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = {}
-    for v in ("tc", "sync"):
-        f = tmp_path / f"dqkv_{v}.npy"
-        env = dict(os.environ)
-        if v == "sync":
-            env["PDS_ATTN_FWD"] = "sync"
-            env["PDS_ATTN_BWD"] = "sync"
-        subprocess.run([sys.executable, "-c", _NWG_SCRIPT, root, str(f)], check=True, env=env, timeout=300)
-        outs[v] = np.load(f).view(np.uint16).astype(np.uint32) << 16
-    a = outs["tc"].view(np.float32).astype(np.float64)
-    b = outs["sync"].view(np.float32).astype(np.float64)
-    assert rel(b, a) < 1e-2
-
-
 # ---------------------------------------------------------------- collective overlap protocol
 # The tile-overlapped MegatronTS collectives (pds_set_overlap) rest on two GEMM hooks:
 # per-chunk "landed" flags polled by the TMA producer before it loads A rows, and
