@@ -546,7 +546,9 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     tma_prefetch(&tdo);
     for (int i = 0; i < NST; ++i) {
       mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
+      // the dK MMA's commit plus every elementwise warp (done reading the stage's LSE / D
+      // rows: an explicit edge for the bulk copy that overwrites them)
+      mbar_init(&q_empty[i], 1 + 4 * NWG);
     }
     mbar_init(kv_full, 1);
     mbar_init(s_full, 1);
@@ -751,7 +753,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(ds_full);
+        if (lane == 0) {
+          mbar_arrive(ds_full);
+          mbar_arrive(&q_empty[b]);
+        }
         if (warp == 4 && lane == 0) PDS_TR2(i, 6);
       }
     }

@@ -81,7 +81,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-run", action="store_true")
     ap.add_argument("--metp-recompute", type=int, default=0, help="0 = ffn, 1 = full (Q/K/V recomputed too)")
-    ap.add_argument("--plans", default="MegatronTS,UlyssesZ,METP,MegatronCZ,adaptive")
+    ap.add_argument("--plans", default="MegatronTS,UlyssesZ,METP,MegatronCZ,METP-full,adaptive")
     a = ap.parse_args()
     H, N, F = 4096, 32, 16384
     P = 1
@@ -108,7 +108,7 @@ def main():
            "step": a.step, "plans": {}}
     lay = [(W, G) for W, G, _, _ in layers]
     candidates = {"MegatronTS": [0] * a.L, "UlyssesZ": [1] * a.L, "METP": [2] * a.L, "MegatronCZ": [3] * a.L,
-                  "adaptive": None}
+                  "METP-full": [4] * a.L, "adaptive": None}
     for name, fixed in candidates.items():
         if name not in a.plans.split(","):
             continue
@@ -127,7 +127,7 @@ def main():
             best = (s, list(plan))
             s += a.step
         entry = {"predicted_max_s": best[0] if best else 0,
-                 "plan_at_max": "".join("TUMC"[p] for p in best[1]) if best else None}
+                 "plan_at_max": "".join("TUMCF"[p] for p in best[1]) if best else None}
         if best and not a.no_run:
             s_ok, plan = best
             try:

@@ -18,7 +18,8 @@ Eq. 9), w/o Smoothing (gamma = 0), and reports Table 5's columns:
   Time      = cumulative device time of the variant,
   Time_full = cumulative time of ParaDySe (full) up to that Seq_len,
   Saving    = (Time - Time_full) / Time.
-MegatronCZ is not in this build's strategy set.  Switching
+"w/o METP" removes both METP variants (ffn and full recompute: one strategy of the
+paper, two memory modes here).  Switching
 statistics per run: plan changes between consecutive sequences and strategy
 boundaries inside the plans.  --switch-cost measures a mixed plan's stack time
 against the per-layer times of short uniform stacks at the same length.
@@ -97,7 +98,7 @@ def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None, memo=None):
             recs.append({"s": s, "oom": True})
             break
         cum += t
-        recs.append({"s": s, "plan": "".join("TUMC"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
+        recs.append({"s": s, "plan": "".join("TUMCF"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
     per_bucket = {}
     for r in recs:
         if r.get("oom"):
@@ -149,9 +150,9 @@ def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
         per_layer[pi] = t / n_short
     t_mixed = measure(torch, B, ctx, model, plan, s, layers, memo)
     pred = sum(per_layer[p] for p in plan)
-    return {"s": s, "plan": "".join("TUMC"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
+    return {"s": s, "plan": "".join("TUMCF"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
             "overhead": t_mixed / pred - 1.0,
-            "per_layer_s": {"TUMC"[k]: v for k, v in per_layer.items()}}
+            "per_layer_s": {"TUMCF"[k]: v for k, v in per_layer.items()}}
 
 
 def main():
@@ -165,7 +166,7 @@ def main():
     ap.add_argument("--dataset", default="grch38")
     ap.add_argument("--n", type=int, default=48)
     ap.add_argument("--L", type=int, default=32)
-    ap.add_argument("--cap-s", type=int, default=131072, help="truncate sampled lengths (1 GPU)")
+    ap.add_argument("--cap-s", type=int, default=163840, help="truncate sampled lengths (1 GPU)")
     ap.add_argument("--reserve-gb", type=float, default=4.0)
     ap.add_argument("--gamma", type=float, default=0.0)
     ap.add_argument("--ablation", action="store_true")
@@ -202,7 +203,8 @@ def main():
     if a.ablation:
         variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=ALL & ~1, gamma=0.05)),
                     ("w/o MegatronCZ", dict(mask=ALL & ~8, gamma=0.05)),
-                    ("w/o UlyssesZ", dict(mask=ALL & ~2, gamma=0.05)), ("w/o METP", dict(mask=ALL & ~4, gamma=0.05)),
+                    ("w/o UlyssesZ", dict(mask=ALL & ~2, gamma=0.05)),
+                    ("w/o METP", dict(mask=ALL & ~4 & ~16, gamma=0.05)),
                     ("w/o RF", dict(gamma=0.05, pr_only=True)), ("w/o Smoothing", dict(gamma=0.0))]
         out["gamma_full"] = 0.05
         memo = {}
@@ -226,7 +228,8 @@ def main():
             print(row, flush=True)
     else:
         memo = {}
-        for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1), ("MegatronCZ", 3)):
+        for name, fixed in (("adaptive", None), ("MegatronTS", 0), ("METP", 2), ("UlyssesZ", 1), ("MegatronCZ", 3),
+                            ("METP-full", 4)):
             ctx = context(mask=ALL if fixed is None else 1 << fixed, gamma=a.gamma)
             out["runs"][name] = run_trace(torch, B, ctx, model, lens, layers, a.L, fixed, memo=memo)
             ctx.close()

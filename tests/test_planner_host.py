@@ -196,8 +196,46 @@ def test_plan_sequence_vs_oracle(B, path, gamma):
         seen["inf"] += bool(fl & B.PLAN_INFEASIBLE)
         seen["mixed"] += len(set(got)) > 1
     assert seen["cached"] > 20 and seen["inf"] > 0 and seen["mixed"] > 0, seen
-    if gamma > 0:
-        assert seen["smoothed"] > 0, seen
+    ctx.close()
+
+
+def test_plan_smoothing_on_near_ties(B, tmp_path):
+    """A bundle whose MegatronTS and MegatronCZ times alternate within +-3 % (so
+    consecutive lengths flip the least-time plan) plus a 10 % slower METP: with
+    gamma = 0.05 smoothing must keep the previous plan on most flips (R-19), and
+    the library must still equal the oracle bit for bit, flags included."""
+    from paper_2511_13198_b200.calibrate import fit_and_export
+    grid = [1024 * k for k in range(1, 65)]
+    rec = {0: [(s, 1e-6 * s) for s in grid],
+           3: [(s, 1e-6 * s * (1.0 + 0.03 * np.sin(s / 2500.0))) for s in grid],
+           2: [(s, 1.1e-6 * s) for s in grid]}
+    path = str(tmp_path / "h4096_n32_f16384_P1.txt")
+    fit_and_export(path, 1, 4096, 32, 16384, 32, rec, capacity=1.0e15, reserve=0.0)
+    ctx, bd = _bundle_ctx(B, path)
+    hd = bd["hdr"]
+    wl = {}
+
+    def wlib(pi, s):
+        if (pi, s) not in wl:
+            wl[(pi, s)] = B.mem_bytes(B.Model(h=4096, n_heads=32, ffn=16384, n_layers=32), 1, pi, s)[1]
+        return wl[(pi, s)]
+
+    all_mask = (1 << B.N_STRATEGIES) - 1
+    for gamma in (0.0, 0.05):
+        ctx.set_enabled(all_mask)                  # clears D and the previous plan
+        ctx.set_capacity(1.0e15, gamma)
+        cache, prev, smoothed, flips = {}, None, 0, 0
+        for s in [1024 * k for k in range(1, 65)] + [1024 * k for k in range(64, 0, -1)]:
+            got, fl = ctx.plan(s, hd["L"])
+            ref, rfl = _plan_oracle(bd, B, s, hd["L"], all_mask, 1.0e15, gamma, cache, prev, wlib)
+            assert got == ref and fl & (B.PLAN_CACHED | B.PLAN_SMOOTHED | B.PLAN_INFEASIBLE) == rfl, (s, gamma)
+            smoothed += bool(fl & B.PLAN_SMOOTHED)
+            flips += prev is not None and cache[(1, s)][0] != prev
+            prev = got
+        if gamma > 0:
+            assert flips > 4 and smoothed > 4, (flips, smoothed)
+        else:
+            assert smoothed == 0
     ctx.close()
 
 
