@@ -296,7 +296,11 @@ pds_status pds_k_rmsnorm_bwd(const void* du, const void* x, const void* rstd, co
 pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
                           int32_t causal, void* out, int64_t ld_out, void* lse, void* stream);
 /* Attention backward: dqkv [s][ld] (pre-RoPE positions handled by caller), from
- * qkv (post-RoPE Q, K), out, lse, dout. */
+ * qkv (post-RoPE Q, K), out, lse, dout.  Two implementations (pds_set_attn_bwd):
+ * the split dK/dV + dQ kernels (default; d in {64, 128}, causal or not) and the fused
+ * kernel (d = 128, causal: one kernel for dQ, dK, dV, 5 matmuls per block pair, dQ
+ * summed over key blocks through an fp32 accumulator in a fixed order, so the result is
+ * deterministic; scratch heads * s * 128 fp32 cached by this entry point). */
 pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
                           const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                           int32_t causal, void* dqkv, void* stream);
@@ -313,6 +317,12 @@ pds_status pds_k_attn_fwd_rows(const void* qkv, int64_t ld, int32_t s, int32_t h
 pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
                                const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                                int32_t causal, int32_t qlo, int32_t qn, void* dqkv, void* stream);
+
+/* Attention backward implementation, process wide: 0 = the split dK/dV + dQ kernels
+ * (default), 1 = the fused kernel where it applies (d = 128, causal, all query rows;
+ * slower on B200: its dQ reduction through L2 is the bottleneck).
+ * Affects pds_layer_bwd and pds_k_attn_bwd; any other mode is PDS_EINVAL. */
+pds_status pds_set_attn_bwd(int32_t mode);
 
 const char* pds_last_error(void);
 const char* pds_version(void);

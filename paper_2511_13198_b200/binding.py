@@ -144,6 +144,7 @@ _SIGS = {
                             C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
     "pds_k_attn_bwd_rows": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
+    "pds_set_attn_bwd": [C.c_int32],
     "pds_last_error": [],
     "pds_version": [],
 }
@@ -345,6 +346,11 @@ def k_attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, stream=0):
 
 def k_attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream=0):
     call("pds_k_attn_bwd", qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream)
+
+
+def set_attn_bwd(mode):
+    """0 = split attention backward kernels (default), 1 = fused kernel where it applies (d = 128, causal)."""
+    call("pds_set_attn_bwd", mode)
 
 
 def k_attn_fwd_rows(qkv, ld, s, heads, d, causal, qlo, qn, out, ld_out, lse, stream=0):

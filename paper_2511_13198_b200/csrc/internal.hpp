@@ -58,6 +58,11 @@ struct BufPlan {
       if (std::strcmp(r.name, n) == 0) return true;
     return false;
   }
+  int64_t ws_size(const char* n) const {
+    for (const Region& r : ws)
+      if (std::strcmp(r.name, n) == 0) return r.bytes;
+    return 0;
+  }
 };
 
 int rmsnorm_bwd_grid(int64_t rows);

@@ -1,5 +1,6 @@
 // Kernel-level C-ABI entry points (per-stage parity) and the
 // NCCL unique-id helper.  Thin argument checks + launch; no context.
+#include <mutex>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -118,7 +119,29 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* dd = nullptr;
   PDS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dd), (size_t)heads * s * 4, st));
-  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st),
+  // the fused backward's scratch (fp32 dQ accumulator + counters) is cached across calls
+  // (grow-only, one per process): a stream-ordered allocation of hundreds of MB per call
+  // would be re-mapped at every synchronisation and dominate the kernel's time
+  static std::mutex mu;
+  static void* scratch = nullptr;
+  static size_t scratch_bytes = 0;
+  float* acc = nullptr;
+  int* ctr = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (attn_bwd_fused_applies(d, causal) && s > 0) {
+    const size_t acc_b = (size_t)heads * s * d * 4, need = acc_b + ((size_t)heads * (s / 128) + 1) * 4;
+    if (need > scratch_bytes) {
+      PDS_CUDA(cudaStreamSynchronize(st));
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      scratch_bytes = 0;
+      PDS_CUDA(cudaMalloc(&scratch, need));
+      scratch_bytes = need;
+    }
+    acc = static_cast<float*>(scratch);
+    ctr = reinterpret_cast<int*>(static_cast<char*>(scratch) + acc_b);
+  }
+  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st, acc, ctr),
                       "pds_k_attn_bwd");
   cudaFreeAsync(dd, st);
   return r;
@@ -144,6 +167,12 @@ extern "C" pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const voi
                                     dd, st), "pds_k_attn_bwd_rows");
   cudaFreeAsync(dd, st);
   return r;
+}
+
+extern "C" pds_status pds_set_attn_bwd(int32_t mode) {
+  if (mode != 0 && mode != 1) PDS_FAIL(PDS_EINVAL, "attention backward mode must be 0 (split) or 1 (fused)");
+  set_attn_bwd_mode(mode);
+  return PDS_OK;
 }
 
 extern "C" pds_status pds_debug_trace(int64_t* host_out, int32_t rows) {

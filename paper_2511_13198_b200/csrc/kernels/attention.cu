@@ -13,10 +13,13 @@
 namespace pds {
 
 // ------------------------------------------------------------------ backward: D = rowsum(dO o O)
+// (also zeroes the fused backward's nctr turn / ticket counters, one per thread)
 __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out, int64_t ld_out,
                                     const __nv_bfloat16* __restrict__ dout, int s, int heads, int d,
-                                    float* __restrict__ Dd) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                                    float* __restrict__ Dd, int* __restrict__ ctr, int nctr) {
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi < nctr) ctr[gi] = 0;
+  const int warp = gi >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= s * heads) return;
   const int row = warp / heads, head = warp % heads;
@@ -45,13 +48,29 @@ int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, c
                 int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo = 0,
                 int qn = -1);
 
+int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                      int s, int heads, void* dqkv, const void* rope, float* dqacc, int* ctr, cudaStream_t st);
+
+// 0: split dK/dV + dQ kernels (default), 1: fused kernel where it applies (pds_set_attn_bwd).
+// The fused kernel executes 5 matmuls instead of 7 but adds 64 KB of fp32 dQ reduction per
+// (key block, query block) pair through L2, which B200's L2 reduction throughput cannot
+// sustain at this tile shape: measured slower.
+static int g_bwd_mode = 0;
+void set_attn_bwd_mode(int mode) { g_bwd_mode = mode; }
+bool attn_bwd_fused_applies(int d, int causal) { return g_bwd_mode == 1 && d == 128 && causal; }
+
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
              const void* dout, int s, int heads, int d, int causal, void* dqkv, const void* rope,
-             float* Dd, cudaStream_t st) {
+             float* Dd, cudaStream_t st, float* dqacc, int* ctr) {
   if (s % 128) return (int)cudaErrorInvalidValue;
-  attn_bwd_dot_kernel<<<(s * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
-                                                          reinterpret_cast<const __nv_bfloat16*>(dout), s, heads,
-                                                          d, Dd);
+  const bool fused = dqacc && ctr && attn_bwd_fused_applies(d, causal);
+  const int nctr = fused ? heads * (s / 128) + 1 : 0;
+  const int nblk = (s * heads + 7) / 8;
+  if (nctr > nblk * 256) return (int)cudaErrorInvalidValue;
+  attn_bwd_dot_kernel<<<nblk, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
+                                            reinterpret_cast<const __nv_bfloat16*>(dout), s, heads, d, Dd, ctr,
+                                            nctr);
+  if (fused) return attn_bwd_fused_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, dqkv, rope, dqacc, ctr, st);
   return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st);
 }
 
@@ -70,7 +89,7 @@ int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, 
   if (qn % 128 || qn <= 0) return (int)cudaErrorInvalidValue;
   attn_bwd_dot_kernel<<<(qn * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
                                                            reinterpret_cast<const __nv_bfloat16*>(dout), qn, heads,
-                                                           d, Dd);
+                                                           d, Dd, nullptr, 0);
   return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, qlo, qn);
 }
 

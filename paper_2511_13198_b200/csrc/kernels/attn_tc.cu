@@ -1056,6 +1056,493 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   }
 }
 
+// ============================================================ fused backward (d = 128, causal)
+// One kernel for dQ, dK and dV: 5 matmuls per (key block, query block) pair instead of
+// the split kernels' 7 (the dQ kernel above recomputes S and dP).  CTA = (128-key block
+// kb, head), loop over the query blocks qb = kb, kb+1, ... (causal, all s positions):
+//   S^T = K Q^T (TMEM cols 0..127) -> P^T (packed bf16, same cols), dV += P^T dO
+//   dP^T = V dO^T (cols 128..255) -> dS^T (packed bf16, same cols), dK += dS^T Q
+//   dS (bf16) also stored to shared memory (into the dO slot, free once dV and dP^T
+//   have read it) and dQ_partial = dS K into cols 128..255 (after dK has read dS^T).
+// TMEM is full (S^T | dP^T | dV | dK), so dQ_partial reuses the dP^T region and is read
+// out by a dedicated warpgroup before the next dP^T is issued:
+//   MMA cycle:  dK_i  dQ_i | dV_{i+1}  dP^T_{i+1}  S^T_{i+2}
+// so the readout (and the exponentials of block i+1) overlap dK_i / dQ_i / dV_{i+1}.
+//
+// dQ across key blocks, deterministically: the partial of key block kb for query block qb
+// is added into an fp32 accumulator [heads][qb][32 col-chunks][128 rows][4] in a FIXED
+// order kb = qb, qb-1, ..., 0 (a per-(head, qb) counter, acquire / release at gpu scope):
+// the diagonal block stores, later ones red.add, and key block 0 (the last) adds its own
+// partial, applies RoPE^T and the scale, and writes bf16 dQ.  Key block kb+1 reaches
+// query block qb one iteration before key block kb does, so with CTAs of a head claimed
+// in the order kb = nkb-1 .. 0 (a ticket counter, not blockIdx, so a CTA only ever waits
+// for a CTA that is already running) the order costs no waiting in steady state.
+// Head-major claiming keeps one head's accumulator (16 MB at s = 32K) hot in L2.
+// ctr: [heads * nkb] turn counters + [1] ticket, zeroed before the launch.
+template <int NWG>
+struct BwdFCfg {
+  static constexpr int D = 128;
+  static constexpr int T = 128 * D * 2;      // one [128][128] bf16 tile
+  static constexpr int NST = 2;
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = T;
+  static constexpr int Q_OFF = 2 * T;        // [NST]
+  static constexpr int O_OFF = Q_OFF + NST * T;    // [NST] dO, then dS of the same query block
+  static constexpr int L_OFF = O_OFF + NST * T;    // lse [NST][128], then D [NST][128]
+  static constexpr int BAR_OFF = L_OFF + 2 * NST * 512;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int THREADS = 128 + 128 * NWG + 128;
+};
+static_assert(BwdFCfg<2>::SMEM <= 232448, "fused backward exceeds 227 KB of shared memory");
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_cg4(const float* p) {
+  float4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cg4(float* p, float4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+template <int R>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+template <int R>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
+}
+
+template <int NWG>
+__global__ void __launch_bounds__(BwdFCfg<NWG>::THREADS, 1)
+    attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tdo,
+                          const float* __restrict__ lse, const float* __restrict__ Dd, int s, int heads,
+                          __nv_bfloat16* __restrict__ dqkv, int64_t ld, const float2* __restrict__ rope, float scale,
+                          float scale_log2, float* __restrict__ dqacc, int* __restrict__ ctr) {
+  using C = BwdFCfg<NWG>;
+  constexpr int D = 128, NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;             // [NST] Q + LSE
+  uint64_t* q_empty = bar + NST;          // [NST]
+  uint64_t* o_full = bar + 2 * NST;       // [NST] dO + D
+  uint64_t* o_empty = bar + 3 * NST;      // [NST]
+  uint64_t* kv_full = bar + 4 * NST;
+  uint64_t* s_full = bar + 4 * NST + 1;
+  uint64_t* dp_full = bar + 4 * NST + 2;
+  uint64_t* p_full = bar + 4 * NST + 3;
+  uint64_t* ds_full = bar + 4 * NST + 4;
+  uint64_t* fin = bar + 4 * NST + 5;
+  uint64_t* p_half = bar + 4 * NST + 6;
+  uint64_t* dq_full = bar + 4 * NST + 7;
+  uint64_t* dq_free = bar + 4 * NST + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4 * NST + 9);
+  int* tick = reinterpret_cast<int*>(bar + 4 * NST + 10);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = s / 128;
+  const int hq = heads * D;
+  constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
+  constexpr int DQ_WARP0 = 4 + 4 * NWG;
+
+  if (threadIdx.x == 0) {
+    *tick = atomicAdd(ctr + heads * nkb, 1);
+    tma_prefetch(&tkv);
+    tma_prefetch(&tdo);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1 + 4 * NWG);     // dK commit + elementwise warps done with LSE
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 1 + 4 * NWG);     // dQ commit + elementwise warps done with D
+    }
+    mbar_init(kv_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, 4 * NWG);
+    mbar_init(p_half, 4 * NWG);
+    mbar_init(ds_full, 4 * NWG);
+    mbar_init(fin, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int tk = *tick;
+  const int head = tk / nkb;
+  const int kb = nkb - 1 - tk % nkb;          // short key blocks first within a head
+  const int k0 = kb * 128;
+  const int nq = nkb - kb;                    // query blocks kb .. nkb-1
+
+  if (warp < 4) {
+    reg_dealloc<72>();
+    if (warp == 0) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(kv_full, 2 * C::T);
+        for (int a = 0; a < D / 64; ++a) {
+          tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, hq + head * D + a * 64, k0);
+          tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, 2 * hq + head * D + a * 64, k0);
+        }
+        for (int i = 0; i < nq; ++i) {
+          const int b = i % NST, q0 = (kb + i) * 128;
+          if (i >= NST) mbar_wait(&q_empty[b], ((i / NST) - 1) & 1);
+          mbar_arrive_expect_tx(&q_full[b], C::T + 512);
+          for (int a = 0; a < D / 64; ++a)
+            tma_load_2d(sm + C::Q_OFF + b * C::T + a * 16384, &tkv, &q_full[b], head * D + a * 64, q0);
+          bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)head * s + q0, 512, &q_full[b]);
+          if (i >= NST) mbar_wait(&o_empty[b], ((i / NST) - 1) & 1);
+          mbar_arrive_expect_tx(&o_full[b], C::T + 512);
+          for (int a = 0; a < D / 64; ++a)
+            tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &o_full[b], head * D + a * 64, q0);
+          bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)head * s + q0, 512, &o_full[b]);
+        }
+      }
+    } else if (warp == 1) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_acc = umma_idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t idesc_dq = umma_idesc_bf16(128, D, 1, 1);
+      const uint32_t sk = smem_u32(sm + C::K_OFF), sv = smem_u32(sm + C::V_OFF);
+      auto qtile = [&](int i) { return smem_u32(sm + C::Q_OFF + (i % NST) * C::T); };
+      auto otile = [&](int i) { return smem_u32(sm + C::O_OFF + (i % NST) * C::T); };
+      auto issue_s = [&](int i) {
+        mbar_wait(&q_full[i % NST], (i / NST) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sq = qtile(i);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            umma_f16(tmem + ST_COL, kmaj_desc(sk, kk), kmaj_desc(sq, kk), idesc_s, kk > 0);
+          umma_commit(s_full);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int i) {
+        if (elect_one()) {
+          const uint32_t so = otile(i);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            umma_f16(tmem + DP_COL, kmaj_desc(sv, kk), kmaj_desc(so, kk), idesc_s, kk > 0);
+          umma_commit(dp_full);
+        }
+        __syncwarp();
+      };
+      // dV += P^T dO in two halves (every warpgroup's first half of P^T columns first)
+      auto issue_dv = [&](int i) {
+        constexpr int KPW = 8 / NWG;
+        mbar_wait(&o_full[i % NST], (i / NST) & 1);
+        mbar_wait(p_half, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t so = otile(i);
+#pragma unroll
+          for (int w = 0; w < NWG; ++w)
+#pragma unroll
+            for (int jj = 0; jj < KPW / 2; ++jj) {
+              const int kk = w * KPW + jj;
+              umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, (i | kk) != 0);
+            }
+        }
+        __syncwarp();
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t so = otile(i);
+#pragma unroll
+          for (int w = 0; w < NWG; ++w)
+#pragma unroll
+            for (int jj = KPW / 2; jj < KPW; ++jj) {
+              const int kk = w * KPW + jj;
+              umma_f16_ts(tmem + DV_COL, tmem + ST_COL + acol<NWG>(kk), mnmaj_desc(so, kk), idesc_acc, 1);
+            }
+        }
+        __syncwarp();
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      issue_dv(0);
+      issue_dp(0);
+      if (nq > 1) issue_s(1);
+      for (int i = 0; i < nq; ++i) {
+        mbar_wait(ds_full, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sq = qtile(i), sd = otile(i);
+          // dQ_partial = dS K: A = dS [queries x keys] (the smem tile read MN-major), B = K
+          // (MN-major), into the dP^T region (the elementwise warps have read dP^T)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16(tmem + DP_COL, mnmaj_desc(sd, kk), mnmaj_desc(sk, kk), idesc_dq, kk > 0);
+          umma_commit(dq_full);
+          // dK += dS^T Q: A = dS^T [keys x queries] (the same tile read K-major)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16(tmem + DK_COL, kmaj_desc(sd, kk), mnmaj_desc(sq, kk), idesc_acc, (i | kk) != 0);
+          umma_commit(&q_empty[i % NST]);
+          umma_commit(&o_empty[i % NST]);
+        }
+        __syncwarp();
+        if (i + 1 < nq) {
+          issue_dv(i + 1);
+          mbar_wait(dq_free, i & 1);          // dQ_i read out of the dP^T region
+          tc_fence_after();
+          issue_dp(i + 1);
+          if (i + 2 < nq) issue_s(i + 2);
+        }
+      }
+      if (elect_one()) umma_commit(fin);
+      __syncwarp();
+    }
+  } else if (warp < DQ_WARP0) {
+    reg_alloc<168>();
+    constexpr int CW = 128 / NWG;             // query columns per warpgroup
+    const int wg = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int t = q * 32 + lane;             // key row (TMEM lane)
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t c_s = lb + ST_COL + CW * wg, c_d = lb + DP_COL + CW * wg;
+    for (int i = 0; i < nq; ++i) {
+      const int b = i % NST;
+      const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * CW * 4;
+      const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * CW * 4;
+      const bool diag = i == 0;
+      float p[CW];
+      {
+        uint32_t sr[CW / 32][32];
+        mbar_wait(s_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h) tmem_ld32(c_s + 32 * h, sr[h]);
+        tmem_ld_wait();
+        const f2 sl2{scale_log2, scale_log2}, nlog2e{-LOG2E, -LOG2E};
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+          for (int e = hf * CW / 2; e < (hf + 1) * CW / 2; e += 4) {
+            const float4 L = lds4(lsm + e * 4);
+#pragma unroll
+            for (int u = 0; u < 4; u += 2) {
+              const f2 sv{__uint_as_float(sr[(e + u) / 32][(e + u) % 32]),
+                          __uint_as_float(sr[(e + u + 1) / 32][(e + u + 1) % 32])};
+              const f2 nl = mul2(u ? f2{L.z, L.w} : f2{L.x, L.y}, nlog2e);
+              const f2 x = fma2(sv, sl2, nl);
+              f2 pp;
+              if (emu_pair((e + u) >> 1)) {
+                pp = exp2_fma2(x);
+              } else {
+                pp.x = ex2(x.x);
+                pp.y = ex2(x.y);
+              }
+              p[e + u] = pp.x;
+              p[e + u + 1] = pp.y;
+            }
+          }
+          if (diag) {
+#pragma unroll
+            for (int e = hf * CW / 2; e < (hf + 1) * CW / 2; ++e)
+              if (t > CW * wg + e) p[e] = 0.f;
+          }
+          uint32_t pk[CW / 4];
+#pragma unroll
+          for (int e = 0; e < CW / 4; ++e) pk[e] = pack_bf16(p[hf * CW / 2 + 2 * e], p[hf * CW / 2 + 2 * e + 1]);
+          if (CW == 64) tmem_st16(c_s + hf * CW / 4, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+          else tmem_st8(c_s + hf * CW / 4, *reinterpret_cast<uint32_t(*)[8]>(&pk[0]));
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && hf == 0) mbar_arrive(p_half);
+        }
+        if (lane == 0) {
+          mbar_arrive(p_full);
+          mbar_arrive(&q_empty[b]);
+        }
+      }
+      {
+        mbar_wait(dp_full, i & 1);
+        tc_fence_after();
+        uint32_t pk[CW / 2];
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h) {
+          uint32_t dv[32];
+          tmem_ld32(c_d + 32 * h, dv);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 Dq = lds4(dsm + (32 * h + e) * 4);
+            const f2 d0 = mul2(f2{p[32 * h + e], p[32 * h + e + 1]},
+                               sub2(f2{__uint_as_float(dv[e]), __uint_as_float(dv[e + 1])}, f2{Dq.x, Dq.y}));
+            const f2 d1 = mul2(f2{p[32 * h + e + 2], p[32 * h + e + 3]},
+                               sub2(f2{__uint_as_float(dv[e + 2]), __uint_as_float(dv[e + 3])}, f2{Dq.z, Dq.w}));
+            pk[16 * h + e / 2] = pack_bf16(d0.x, d0.y);
+            pk[16 * h + e / 2 + 1] = pack_bf16(d1.x, d1.y);
+          }
+        }
+        // dS row (key t, this warpgroup's CW queries) into the dO slot: the MN-major A
+        // operand of dQ and the K-major A operand of dK; 64-query atom (CW wg) / 64,
+        // 16-byte chunks from (CW wg % 64) / 8
+        {
+          uint8_t* dst = sm + C::O_OFF + b * C::T;
+          const int atom = (CW * wg) / 64, c0 = ((CW * wg) % 64) / 8;
+#pragma unroll
+          for (int c = 0; c < CW / 8; ++c)
+            st_sw128(dst, 16384, t, atom, c0 + c, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(ds_full);
+          mbar_arrive(&o_empty[b]);
+        }
+      }
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const int key = k0 + t;
+    __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
+    for (int task = wg; task < D / 64 + D / 32; task += NWG) {
+      if (task < D / 64) {
+        const int c = task;
+        uint32_t ra[32], rb[32];
+        tmem_ld32(lb + DK_COL + c * 32, ra);
+        tmem_ld32(lb + DK_COL + c * 32 + D / 2, rb);
+        tmem_ld_wait();
+        float a[32], bb[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
+        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+        store32_bf16(rowp + hq + c * 32, a);
+        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+      } else {
+        const int c = task - D / 64;
+        uint32_t r[32];
+        tmem_ld32(lb + DV_COL + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        store32_bf16(rowp + 2 * hq + c * 32, v);
+      }
+    }
+  } else {
+    // dQ warpgroup: dQ_partial out of TMEM (query row t = TMEM lane) in 16-column chunks,
+    // added to the fp32 accumulator [head][s][128] with red.global.add.v4.f32 straight
+    // from registers, every thread along its own 512-byte row (no shared-memory staging:
+    // the staging stores plus bulk reductions cost more shared-memory bandwidth than the
+    // kernel has to spare; per-thread rows are the fastest register red pattern,
+    // tools/l2_reduce_probe.cu), in key-block order (the turn counter).
+    reg_dealloc<104>();
+    const int q = warp & 3;
+    const int t = q * 32 + lane;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    for (int i = 0; i < nq; ++i) {
+      const int qb = kb + i;
+      int* turn = ctr + head * nkb + qb;
+      float* acc = dqacc + ((int64_t)head * s + qb * 128 + t) * 128;
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      if (i > 0) {                           // not the diagonal block: key block kb+1 first
+        if (t == 0) {
+          int ns = 32;
+          while (ld_acquire_gpu(turn) < i) {
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+        }
+        named_bar(1, 128);
+      }
+      uint32_t r[2][16];
+      tmem_ld16(lb + DP_COL, r[0]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        tmem_ld_wait();
+        if (c + 1 < 8) {
+          tmem_ld16(lb + DP_COL + 16 * (c + 1), r[(c + 1) & 1]);
+        } else {                             // the dP^T region may be overwritten
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dq_free);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t* v = &r[c & 1][4 * j];
+          float* pp = acc + 16 * c + 4 * j;
+          if (i == 0) st_cg4(pp, make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                                             __uint_as_float(v[3])));
+          else red_add_v4(pp, __uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]),
+                          __uint_as_float(v[3]));
+        }
+      }
+      if (kb > 0) {                          // hand the turn to key block kb-1
+        __threadfence();
+        named_bar(1, 128);
+        if (t == 0) st_release_gpu(turn, i + 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// dQ = RoPE^T(scale * accumulator) in bf16 (the fused kernel's fp32 dQ, [heads][s][128]).
+// Thread = (row, 8-column group g): columns 8g..8g+7 and their RoPE partners 64+8g.. .
+__global__ void __launch_bounds__(256) attn_dq_finish_kernel(const float* __restrict__ dqacc, int s, int heads,
+                                                           __nv_bfloat16* __restrict__ dqkv, int64_t ld,
+                                                           const float2* __restrict__ rope, float scale) {
+  const int rl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t rb = blockIdx.x;                 // 32-row band of one head
+  const int head = (int)(rb / (s / 32));
+  const int row = (int)(rb % (s / 32)) * 32 + rl;
+  const float* acc = dqacc + ((int64_t)head * s + row) * 128;
+  const float4 a0 = __ldcs(reinterpret_cast<const float4*>(acc + 8 * g));
+  const float4 a1 = __ldcs(reinterpret_cast<const float4*>(acc + 8 * g + 4));
+  const float4 b0 = __ldcs(reinterpret_cast<const float4*>(acc + 64 + 8 * g));
+  const float4 b1 = __ldcs(reinterpret_cast<const float4*>(acc + 68 + 8 * g));
+  float a[8], b[8];
+  a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+  b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+  uint32_t pa[4], pb[4];
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) {
+    float x0 = a[i] * scale, y0 = b[i] * scale, x1 = a[i + 1] * scale, y1 = b[i + 1] * scale;
+    if (rope) {
+      const float4 cs = *reinterpret_cast<const float4*>(rope + (int64_t)row * 64 + 8 * g + i);
+      const float n0 = x0 * cs.x + y0 * cs.y, n1 = x1 * cs.z + y1 * cs.w;
+      y0 = -x0 * cs.y + y0 * cs.x;
+      y1 = -x1 * cs.w + y1 * cs.z;
+      x0 = n0;
+      x1 = n1;
+    }
+    pa[i / 2] = pack_bf16(x0, x1);
+    pb[i / 2] = pack_bf16(y0, y1);
+  }
+  __nv_bfloat16* o = dqkv + (int64_t)row * ld + head * 128 + 8 * g;
+  *reinterpret_cast<uint4*>(o) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+  *reinterpret_cast<uint4*>(o + 64) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+}
+
 // ------------------------------------------------------------------ host
 int attn_debug_trace(long long* host_out, int rows) {
 #ifdef PDS_TRACE
@@ -1168,6 +1655,31 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
   else dkdv(std::integral_constant<int, 4>{});
   if (force == 4) dq(std::integral_constant<int, 4>{});
   else dq(std::integral_constant<int, 2>{});
+  return (int)cudaGetLastError();
+}
+
+// Fused backward (d = 128, causal, all s query positions): dqacc holds heads * s * 128
+// fp32, ctr heads * (s / 128) + 1 ints that must be zero at launch.
+int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                      int s, int heads, void* dqkv, const void* rope, float* dqacc, int* ctr, cudaStream_t st) {
+  if (s % 128 || ld % 8 || ld_out % 8 || !dqacc || !ctr) return (int)cudaErrorInvalidValue;
+  constexpr int NWG = 2;
+  using C = BwdFCfg<NWG>;
+  CUtensorMap kv128, do128;
+  int rc = make_map_rows(&kv128, qkv, (uint64_t)3 * heads * 128, s, ld, 128);
+  rc |= make_map_rows(&do128, dout, (uint64_t)heads * 128, s, ld_out, 128);
+  if (rc) return (int)cudaErrorInvalidValue;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(attn_bwd_fused_kernel<NWG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    once = true;
+  }
+  const float scale = 1.0f / sqrtf(128.0f);
+  attn_bwd_fused_kernel<NWG><<<(s / 128) * heads, C::THREADS, C::SMEM, st>>>(
+      kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, reinterpret_cast<__nv_bfloat16*>(dqkv), ld,
+      reinterpret_cast<const float2*>(rope), scale, scale * LOG2E, dqacc, ctr);
+  attn_dq_finish_kernel<<<(s / 32) * heads, 256, 0, st>>>(dqacc, s, heads, reinterpret_cast<__nv_bfloat16*>(dqkv),
+                                                          ld, reinterpret_cast<const float2*>(rope), scale);
   return (int)cudaGetLastError();
 }
 

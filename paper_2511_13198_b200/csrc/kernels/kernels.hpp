@@ -8,8 +8,13 @@ namespace pds {
 int attn_debug_trace(long long* host_out, int rows);
 int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
              void* lse, cudaStream_t st);
+// dqacc (heads * s * d fp32) and ctr (heads * s / 128 + 1 ints) select the fused
+// one-kernel backward (d = 128, causal); NULL keeps the split dK/dV + dQ kernels
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
-             int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st);
+             int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st,
+             float* dqacc = nullptr, int* ctr = nullptr);
+bool attn_bwd_fused_applies(int d, int causal);
+void set_attn_bwd_mode(int mode);
 // context parallelism: queries [qlo, qlo + qn) against all s keys (attention.cu)
 int attn_fwd_rows(const void* qkv, int64_t ld, int s, int heads, int d, int causal, int qlo, int qn, void* out,
                   int64_t ld_out, void* lse, cudaStream_t st);

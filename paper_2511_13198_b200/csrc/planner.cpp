@@ -236,6 +236,10 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   BufPlan p;
   int64_t ts = 0, tw = 0;
   const int64_t dgp = (int64_t)rmsnorm_bwd_grid(SL) * h * 4;
+  // fused attention backward: turn counters per (local head, 128-query block) + ticket
+  // (its fp32 dQ accumulator borrows a region that is free during the attention
+  // backward: ta for TS / UZ, ul + vl for METP)
+  const int64_t actr = (nl * (s / 128) + 1) * 4;
   switch (strategy) {
     case PDS_MEGATRON_TS:
       push(p.saved, ts, "rstd1", ell);
@@ -255,6 +259,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * S * 2);   // transposed operands (all GEMMs TN)
       push(p.ws, tw, "tb", h * S * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      push(p.ws, tw, "actr", actr);
       if (P > 1) push(p.ws, tw, "gather2", S * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
@@ -285,6 +290,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "ta", std::max(F, 3 * h) * SL * 2);
       push(p.ws, tw, "tb", h * SL * 2);
       push(p.ws, tw, "wt", h * std::max(F, 3 * h) * 2);
+      push(p.ws, tw, "actr", actr);
       break;
     }
     case PDS_METP:
@@ -321,6 +327,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * W * 2);
       push(p.ws, tw, "tb", h * P * W * 2);
       push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      push(p.ws, tw, "actr", actr);
       if (full) push(p.ws, tw, "qkv", S * 3 * hl * 2);
       break;
     }

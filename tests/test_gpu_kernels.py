@@ -154,7 +154,20 @@ def test_rmsnorm_fwd_bwd(h):
 @pytest.mark.parametrize("causal", [1, 0])
 @pytest.mark.parametrize("s", [256, 640])
 def test_attention_fwd_bwd(d, causal, s):
-    heads = 2
+    _attention_fwd_bwd(d, causal, s)
+
+
+@pytest.mark.parametrize("s", [256, 640, 1152])
+def test_attention_bwd_fused_vs_oracle(s):
+    """The fused backward (pds_set_attn_bwd(1); d = 128, causal) against the oracle."""
+    B.set_attn_bwd(1)
+    try:
+        _attention_fwd_bwd(128, 1, s, heads=3)
+    finally:
+        B.set_attn_bwd(0)
+
+
+def _attention_fwd_bwd(d, causal, s, heads=2):
     hq = heads * d
     qkv = _mat(5 + d, 1, (s, 3 * hq))
     dout = _mat(5 + d, 2, (s, hq))
@@ -192,7 +205,8 @@ _NWG_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2511_13198_b200 import binding as B
-s, heads, d = 640, 2, 128
+s, heads, d = int(sys.argv[3]), int(sys.argv[4]), 128
+B.set_attn_bwd(int(sys.argv[5]))
 hq = heads * d
 g = torch.Generator().manual_seed(3)
 qkv = (torch.randn(s, 3 * hq, generator=g) * 0.5).to(torch.bfloat16).cuda()
@@ -209,7 +223,7 @@ np.save(sys.argv[2], dqkv.view(torch.int16).cpu().numpy())
 
 
 def test_attention_bwd_warpgroup_variants_bitwise(tmp_path):
-    """dK/dV and dQ kernels with 2 or 4 elementwise warpgroups (PDS_BWD_NWG) do the same
+    """(split kernels, the default) dK/dV and dQ kernels with 2 or 4 elementwise warpgroups (PDS_BWD_NWG) do the same
     per-element arithmetic; the MMA k-steps are issued in warpgroup-half order, which
     depends on the count.  So each kernel is bit-identical to the default where the
     count matches (dK/dV: 4 groups, dQ: 2 groups) and equal within fp32 summation
@@ -225,7 +239,8 @@ def test_attention_bwd_warpgroup_variants_bitwise(tmp_path):
         env.pop("PDS_BWD_NWG", None)
         if v:
             env["PDS_BWD_NWG"] = v
-        subprocess.run([sys.executable, "-c", _NWG_SCRIPT, root, str(f)], check=True, env=env, timeout=300)
+        subprocess.run([sys.executable, "-c", _NWG_SCRIPT, root, str(f), "640", "2", "0"], check=True, env=env,
+                       timeout=300)
         outs[v] = np.load(f)
     hq = outs[""].shape[1] // 3
     assert np.array_equal(outs[""][:, hq:], outs["4"][:, hq:])       # default dK/dV = 4 groups
@@ -234,6 +249,36 @@ def test_attention_bwd_warpgroup_variants_bitwise(tmp_path):
            for k, v in outs.items()}
     assert rel(f32["2"][:, hq:], f32[""][:, hq:]) < 1e-3
     assert rel(f32["4"][:, :hq], f32[""][:, :hq]) < 1e-3
+
+
+@pytest.mark.parametrize("s,heads", [(640, 2), (2048, 3), (4096, 5)])
+def test_attention_bwd_fused_vs_split(tmp_path, s, heads):
+    """The fused backward (one kernel, dQ partials summed over key blocks in a fixed
+    order) against the split kernels at the same elementwise warpgroup count (2):
+    dK / dV come from the same MMA and elementwise sequence, so they are bit-identical;
+    dQ differs only in fp32 summation order (per-key-block partials vs one TMEM
+    accumulator).  The fused result is reproducible bit for bit (run twice), and the
+    oracle check of the fused path is test_attention_bwd_fused_vs_oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, mode, nwg in (("fused", "1", None), ("fused2", "1", None), ("split2", "0", "2")):
+        f = tmp_path / f"{name}.npy"
+        env = dict(os.environ)
+        env.pop("PDS_BWD_NWG", None)
+        if nwg:
+            env["PDS_BWD_NWG"] = nwg
+        subprocess.run([sys.executable, "-c", _NWG_SCRIPT, root, str(f), str(s), str(heads), mode], check=True,
+                       env=env, timeout=300)
+        outs[name] = np.load(f)
+    hq = outs["fused"].shape[1] // 3
+    assert np.array_equal(outs["fused"], outs["fused2"])
+    assert np.array_equal(outs["fused"][:, hq:], outs["split2"][:, hq:])
+    f32 = {k: (v.view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+           for k, v in outs.items()}
+    assert rel(f32["fused"][:, :hq], f32["split2"][:, :hq]) < 2e-3
 
 
 # ---------------------------------------------------------------- collective overlap protocol

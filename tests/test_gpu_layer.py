@@ -165,6 +165,18 @@ def test_layer_p4_batch2_d128(pi):
     _check_layer(pi, 4, 1024, 8, 4096, 1024, seed=14, b=2, chunks=2)
 
 
+@pytest.mark.parametrize("pi", [0, 1, 2, 4])
+def test_layer_fused_attn_bwd(pi):
+    # the opt-in fused attention backward (pds_set_attn_bwd(1)) inside the layer: its fp32
+    # dQ accumulator borrows the TS / UZ transposition buffer or METP's ul + vl; b = 2
+    # (the accumulator is reused sequence after sequence)
+    B.set_attn_bwd(1)
+    try:
+        _check_layer(pi, 2, 1024, 8, 4096, 1024, seed=21, b=2, chunks=2)
+    finally:
+        B.set_attn_bwd(0)
+
+
 @pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
 def test_layer_p8(pi):
     # eight ranks (the paper's node) on the loopback group: s/P = 128 rows,

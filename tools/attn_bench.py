@@ -21,7 +21,9 @@ def main():
     ap.add_argument("--heads", type=int, default=32)
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--fused", action="store_true", help="fused backward kernel instead of the split dK/dV + dQ")
     a = ap.parse_args()
+    B.set_attn_bwd(1 if a.fused else 0)
     s, H, d = a.s, a.heads, a.d
     hq = H * d
     qkv = (torch.randn(s, 3 * hq, device="cuda") * 0.5).to(torch.bfloat16)
@@ -45,7 +47,7 @@ def main():
             if r:
                 ts.append(e0.elapsed_time(e1))
         ms = min(ts)
-        print(f"{name} s={s} {ms:.3f} ms {mult * fl / 2 / ms / 1e9:.1f} TF/s", flush=True)
+        print(f"{name}{' fused' if a.fused and name == 'bwd' else ''} s={s} {ms:.3f} ms {mult * fl / 2 / ms / 1e9:.1f} TF/s", flush=True)
 
 
 if __name__ == "__main__":
