@@ -65,7 +65,17 @@ def aic(y, yhat, k):
     return n * np.log(max(rss / n, floor)) + 2 * k
 
 
-def fit_poly(s, y, scale=None, degrees=(1, 2, 3)):
+def nondecreasing(coef, x0, x1, grid=4097):
+    """Reading R-26b's admissibility, checked the plain way: the derivative is >= 0 at
+    every point of a fine grid on [x0, x1] (plus both ends)."""
+    d = np.polyder(np.asarray(coef, dtype=np.float64))
+    xs = np.linspace(x0, x1, grid)
+    return bool(np.all(np.polyval(d, xs) >= -1e-15 * max(1.0, float(np.max(np.abs(d))))))
+
+
+def fit_poly(s, y, scale=None, degrees=(1, 2, 3), s_extrap_max=None):
+    """Degree 1..3 by AIC.  s_extrap_max (reading R-26b): only
+    degrees whose fit is non-decreasing on [min s, s_extrap_max] are candidates."""
     s = np.asarray(s, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     scale = float(s.max()) if scale is None else scale
@@ -75,6 +85,8 @@ def fit_poly(s, y, scale=None, degrees=(1, 2, 3)):
         if len(np.unique(x)) < d + 1:
             continue
         coef = np.polyfit(x, y, d)
+        if s_extrap_max is not None and not nondecreasing(coef, float(x.min()), s_extrap_max / scale):
+            continue
         a = aic(y, np.polyval(coef, x), d + 1)
         if best is None or a < best[0] - 1e-12:
             best = (a, d, coef)

@@ -32,23 +32,49 @@ BUNDLES = os.path.join(HERE, "bundles")
 ALL = (0, 1, 2, 3, 4)       # TS, UZ, METP, CZ, METP-full (include/paradyse.h)
 
 
-def aic_poly(s, y):
-    """Degree 1..3 least squares in x = s / s_max; AIC = n ln(max(RSS/n, 1e-12 var y)) + 2k."""
+S_EXTRAP_MAX = float(1 << 20)    # longest length the bundles extrapolate to (> 624K, Q-16)
+
+
+def monotone(c, x0, x1):
+    """The polynomial (numpy order) is non-decreasing on [x0, x1]: derivative >= 0 at
+    both ends and at every real critical point of the derivative inside."""
+    d = np.polyder(c)
+    pts = [x0, x1] + [float(r.real) for r in np.roots(np.polyder(d)) if abs(r.imag) < 1e-12 and x0 < r.real < x1] \
+        if len(d) > 1 else [x0, x1]
+    return all(np.polyval(d, t) >= 0 for t in pts)
+
+
+PR_DEGREES = (1, 2)
+
+
+def aic_poly(s, y, degrees=PR_DEGREES):
+    """Least squares in x = s / s_max, degree by AIC = n ln(max(RSS/n, 1e-12 var y)) + 2k.
+    Reading R-26b: of the paper's optional orders 1..3 only those up to
+    the layer's complexity order are candidates (time is O(s^2); O-7:
+    72h^2 s + 6hs^2 flops), and a fit that is not non-decreasing on [min s,
+    S_EXTRAP_MAX] is not admissible (a layer cannot get faster as s grows; PR only
+    extrapolates).  If no degree is admissible, the line with its slope clamped at 0."""
     s = np.asarray(s, dtype=np.float64)
     y = np.asarray(y, dtype=np.float64)
     scale = float(s.max())
     x = s / scale
     best = None
-    for deg in (1, 2, 3):
+    for deg in degrees:
         if len(np.unique(x)) < deg + 1:
             continue
         c = np.polyfit(x, y, deg)
+        if not monotone(c, float(x.min()), S_EXTRAP_MAX / scale):
+            continue
         rss = float(np.sum((np.polyval(c, x) - y) ** 2))
         n = len(y)
         floor = 1e-12 * float(np.var(y)) if np.var(y) > 0 else 1e-300
         a = n * math.log(max(rss / n, floor)) + 2 * (deg + 1)
         if best is None or a < best[0] - 1e-12:
             best = (a, deg, c)
+    if best is None:
+        c = np.polyfit(x, y, 1)
+        c[0] = max(c[0], 0.0)
+        best = (None, 1, c)
     return best[1], best[2], scale
 
 
@@ -91,6 +117,19 @@ def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
         json.dump({"P": P, "h": h, "n": n, "ffn": ffn, "L": L, "note": note,
                    "records": {str(k): v for k, v in records.items()}}, f, indent=1)
     return path
+
+
+def refit(path):
+    """Re-export a bundle from the profile records stored beside it (no GPU): the RF
+    (seed 42) and the PR fit are deterministic functions of the records."""
+    import re
+    meta = json.load(open(path + ".json"))
+    hdr = open(path).readline() and open(path).read().splitlines()[1]
+    cap = float(re.search(r"capacity ([0-9.eE+-]+)", hdr).group(1))
+    res = float(re.search(r"reserve ([0-9.eE+-]+)", hdr).group(1))
+    records = {int(k): [tuple(r) for r in v] for k, v in meta["records"].items()}
+    return fit_and_export(path, meta["P"], meta["h"], meta["n"], meta["ffn"], meta["L"], records, cap, res,
+                          note=meta.get("note", ""))
 
 
 # ------------------------------------------------------------------ profiling (GPU)
@@ -296,7 +335,12 @@ if __name__ == "__main__":
                     default=[1024, 2048, 4096, 8192, 16384, 32768, 65536])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--measured", action="store_true", help="P = WORLD_SIZE ranks under torchrun, over NCCL")
+    ap.add_argument("--refit", action="store_true", help="re-fit the committed bundles from their stored records (CPU)")
     a = ap.parse_args()
+    if a.refit:
+        for P in a.P:
+            print(refit(os.path.join(BUNDLES, f"h{a.h}_n{a.n}_f{a.ffn}_P{P}.txt")))
+        raise SystemExit(0)
     if a.measured:
         grid = a.grid if a.grid != ap.get_default("grid") else [8192, 16384, 32768, 65536, 131072]
         print(profile_measured(a.h, a.n, a.ffn, a.L, grid, reps=a.reps))

@@ -24,8 +24,16 @@ statistics per run: plan changes between consecutive sequences and strategy
 boundaries inside the plans.  --switch-cost measures a mixed plan's stack time
 against the per-layer times of short uniform stacks at the same length.
 
+--predict runs the same protocol WITHOUT a GPU on host-only planner contexts: every
+sequence's per-layer times are the cost model's T_pi(s) (Eq. 9 on the committed bundle
+of that P: measured at P = 1, modelled at P = 2, 4, 8 until an 8xB200 profile exists),
+OOM is Eq. 6 on the library's exact memory plan against the bundle's per-GPU capacity,
+and the output is labelled "predicted".  This is how the P > 1 rows of the north_star
+(per-bucket tokens/s at 1/2/4/8 GPUs, the 624K adaptive frontier) are reported here.
+
   python -m paper_2511_13198_b200.trace --dataset grch38 --n 48 --L 32 --out profiles/t.json
   python -m paper_2511_13198_b200.trace --ablation --out profiles/ablation.json
+  python -m paper_2511_13198_b200.trace --predict --P 8 --n 256 --gamma 0.05 --out profiles/p.json
 """
 from __future__ import annotations
 
@@ -117,7 +125,7 @@ def common_bucket_table(runs, L):
     completed (a static strategy that OOMs drops its longest sequences; comparing
     bucket rates over different sequence sets would favour it), and the adaptive
     plan's ratio to the best static strategy."""
-    done = {n: {(i, r["s"]): r["seconds"] for i, r in enumerate(v["records"]) if not r.get("oom")}
+    done = {n: {(i, r.get("real", r["s"])): r["seconds"] for i, r in enumerate(v["records"]) if "seconds" in r}
             for n, v in runs.items()}
     common = set.intersection(*[set(d) for d in done.values()])
     out = {}
@@ -155,8 +163,142 @@ def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
             "per_layer_s": {"TUMCF"[k]: v for k, v in per_layer.items()}}
 
 
+STATIC = (("MegatronTS", 0), ("UlyssesZ", 1), ("METP", 2), ("MegatronCZ", 3), ("METP-full", 4))
+
+
+def predict_trace(B, model, bundle, lens, L, gamma, fixed=None, real=None):
+    """The trace protocol on a host-only context: plan (adaptive) or the uniform plan
+    (static), time = sum over layers of the bundle's T_pi(s), OOM = Eq. 6 infeasible.
+    real[i]: the unpadded length of lens[i] (tokens/s counts real tokens, Q-15)."""
+    real = lens if real is None else real
+    ctx = B.Context(model, P=bundle_P(bundle), device=-1)
+    ctx.load_costs(bundle)
+    if fixed is not None:
+        ctx.set_enabled(1 << fixed)
+    ctx.set_capacity(bundle_capacity(bundle), gamma if gamma > 0 else 1e-9)
+    recs, cum, oom_at = [], 0.0, None
+    for s, rs in zip(lens, real):
+        try:
+            plan, flags = ctx.plan(s, L)
+        except B.PdsError as e:           # R-15: the strategy's divisibility does not hold at s
+            recs.append({"s": s, "invalid": str(e)})
+            continue
+        if flags & B.PLAN_INFEASIBLE:
+            oom_at = s
+            recs.append({"s": s, "oom": True, "predicted": True})
+            break
+        t = ctx.cost_eval(s)[0]
+        sec = sum(t[p] for p in plan)
+        cum += sec
+        recs.append({"s": s, "real": int(rs), "plan": "".join("TUMCF"[p] for p in plan), "seconds": sec, "cum": cum,
+                     "flags": flags})
+    ctx.close()
+    per_bucket = {}
+    for r in recs:
+        if "seconds" not in r:
+            continue
+        b = bucket_of(r["real"])
+        tok, sec = per_bucket.get(b, (0, 0.0))
+        per_bucket[b] = (tok + r["real"] * L, sec + r["seconds"])
+    return {"records": recs, "cumulative_s": cum, "oom_at": oom_at,
+            "max_s_trained": max([r["s"] for r in recs if "seconds" in r] + [0]),
+            "tokens_per_s_per_layer_by_bucket": {str(k): v[0] / v[1] for k, v in per_bucket.items()},
+            "switching": switches(recs)}
+
+
+def predict_frontier(B, model, bundle, L, unit, fixed=None, s_max=1 << 20):
+    """Largest multiple of `unit` up to s_max for which Eq. 6 has a feasible plan (the
+    adaptive plan, or the uniform plan of strategy `fixed`): bisection, feasibility
+    being monotone in s."""
+    ctx = B.Context(model, P=bundle_P(bundle), device=-1)
+    ctx.load_costs(bundle)
+    if fixed is not None:
+        ctx.set_enabled(1 << fixed)
+
+    def ok(k):
+        try:
+            return not ctx.plan(k * unit, L)[1] & B.PLAN_INFEASIBLE
+        except B.PdsError:
+            return False
+    lo, hi = 0, s_max // unit
+    if ok(hi):
+        lo = hi
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if ok(mid):
+            lo = mid
+        else:
+            hi = mid
+    plan = "".join("TUMCF"[p] for p in ctx.plan(lo * unit, L)[0]) if lo else None
+    ctx.close()
+    return {"s": lo * unit, "plan": plan}
+
+
+def bundle_P(path):
+    return int(re.search(r"_P(\d+)\.txt$", path).group(1))
+
+
+def bundle_capacity(path):
+    """The per-GPU capacity the bundle was calibrated with, minus its reserve (Eq. 6)."""
+    txt = open(path).read()
+    cap = float(re.search(r"\bcapacity ([0-9.eE+-]+)", txt).group(1))
+    m = re.search(r"\breserve ([0-9.eE+-]+)", txt)
+    return cap - (float(m.group(1)) if m else 0.0)
+
+
+def predict_main(a):
+    import sys
+    sys.path.insert(0, ROOT)
+    from synth import pad_to, sample_lengths
+    from . import binding as B
+    H, N, F = 4096, 32, 16384
+    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)
+    out = {"mode": "predicted (cost model + exact memory plan on host-only contexts; no device run)",
+           "dataset": a.dataset, "n": a.n, "L": a.L, "gamma": a.gamma, "by_P": {}}
+    raw = sample_lengths(a.dataset, a.n, seed=42)
+    for P in a.P:
+        bundle = os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt")
+        # pad to a multiple every strategy accepts (R-15; METP's c = P waves of 128 rows:
+        # 128 P^2), curriculum order (PAPER.md:336)
+        unit = 128 * P * P
+        real = sorted(int(x) for x in raw)
+        lens = [int(pad_to(x, unit)) for x in real]
+        meta = json.load(open(bundle + ".json"))
+        runs = {"adaptive": predict_trace(B, model, bundle, lens, a.L, a.gamma, real=real)}
+        for name, pi in STATIC:
+            runs[name] = predict_trace(B, model, bundle, lens, a.L, 0.0, fixed=pi, real=real)
+        frontier = {"adaptive": predict_frontier(B, model, bundle, a.L, unit)}
+        for name, pi in STATIC:
+            frontier[name] = predict_frontier(B, model, bundle, a.L, unit, fixed=pi)
+        entry = {"bundle": os.path.basename(bundle), "bundle_note": meta.get("note", "measured"),
+                 "capacity_bytes": bundle_capacity(bundle), "pad_unit": unit, "lengths": lens, "runs": runs,
+                 "bucket_common": common_bucket_table(runs, a.L),
+                 "max_s_trained": {n: r["max_s_trained"] for n, r in runs.items()},
+                 "frontier_L_stack": frontier}
+        out["by_P"][str(P)] = entry
+        print(f"P={P}", "max_s", entry["max_s_trained"], flush=True)
+        print("  frontier", {n: v["s"] for n, v in frontier.items()}, flush=True)
+        for b, row in entry["bucket_common"].items():
+            print("  bucket", b, row["sequences"], "adaptive / best static (%s) = %.4f"
+                  % (row["best_static"], row["adaptive_over_best_static"]), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(out, f, indent=1)
+    return out
+
+
 def main():
     import sys
+    if "--predict" in sys.argv:
+        ap = argparse.ArgumentParser()
+        ap.add_argument("--predict", action="store_true")
+        ap.add_argument("--dataset", default="grch38")
+        ap.add_argument("--n", type=int, default=256)
+        ap.add_argument("--L", type=int, default=32)
+        ap.add_argument("--P", type=int, nargs="+", default=[1, 2, 4, 8])
+        ap.add_argument("--gamma", type=float, default=0.0)
+        ap.add_argument("--out", default=None)
+        return predict_main(ap.parse_args())
     sys.path.insert(0, ROOT)
     import torch
     from synth import pad_to, sample_lengths

@@ -156,3 +156,28 @@ def test_table5_saving_and_case_study():
     assert math.isclose(329728 / 117248 - 1, 1.8122, rel_tol=1e-4)
     total = 2.5 + 5 + 22 + 1
     assert 30.5 <= total <= 31.5 and abs(22 / 31.3 - 0.702) < 1e-3
+
+
+def test_nondecreasing_pins():
+    # reading R-26b's admissibility on closed forms (numpy coefficient order)
+    assert CM.nondecreasing([1.0, 0.0], 0.0, 10.0)              # x
+    assert not CM.nondecreasing([-1.0, 0.0], 0.0, 10.0)         # -x
+    assert not CM.nondecreasing([1.0, -1.0, 0.0], 0.0, 1.0)     # x^2 - x falls on [0, 1/2)
+    assert CM.nondecreasing([1.0, -1.0, 0.0], 0.5, 3.0)         # ... and rises after
+    assert CM.nondecreasing([1.0, 0.0, 0.0, 0.0], -1.0, 1.0)    # x^3: derivative 3x^2 >= 0
+    assert not CM.nondecreasing([-1.0, 3.0, 0.0, 0.0], 0.0, 4.0)  # -x^3 + 3x^2: falls past x = 2
+    assert CM.nondecreasing([-1.0, 3.0, 0.0, 0.0], 0.0, 2.0)
+
+
+def test_fit_poly_monotone_reading():
+    # a noisy-looking cubic whose leading coefficient is negative extrapolates to a
+    # falling (eventually negative) time: not admissible under R-26b, degree 2 is chosen
+    s = np.array([1024, 2048, 4096, 8192, 16384, 32768, 65536], dtype=float)
+    x = s / s.max()
+    y = 0.001 + 0.05 * x + 0.12 * x * x - 0.03 * x ** 3
+    d, coef, sc = CM.fit_poly(s, y)
+    assert d == 3 and coef[0] < 0                          # plain AIC (exact cubic)
+    d, coef, sc = CM.fit_poly(s, y, s_extrap_max=float(1 << 20))
+    assert d in (1, 2) and CM.nondecreasing(coef, x.min(), (1 << 20) / sc)
+    d2, _, _ = CM.fit_poly(s, y, degrees=(1, 2), s_extrap_max=float(1 << 20))
+    assert d2 == d

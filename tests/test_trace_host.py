@@ -43,3 +43,47 @@ def test_time_full_at_and_saving():
 
 def test_bucket_edges():
     assert T.bucket_of(4095) == 0 and T.bucket_of(4096) == 1 and T.bucket_of(131072) == 6
+
+
+def test_committed_bundles_extrapolate_monotonically():
+    """Reading R-26b on the shipped bundles: every strategy's PR branch is positive and
+    non-decreasing from s_profile_max to 2^20 (beyond 624K), and the product's fit
+    (calibrate.aic_poly) equals the oracle's (degrees 1..2, non-decreasing filter) on the
+    stored profile records."""
+    import json
+    import numpy as np
+    from paper_2511_13198_b200 import calibrate as CAL
+    for P in (1, 2, 4, 8):
+        path = os.path.join(os.path.dirname(T.__file__), "bundles", f"h4096_n32_f16384_P{P}.txt")
+        b = OC.read_bundle(path)
+        recs = json.load(open(path + ".json"))["records"]
+        for sid, e in b["strat"].items():
+            ss = np.linspace(e["s_profile_max"], float(1 << 20), 257)
+            t = [OC.poly_eval(e["poly_coef"], e["poly_scale"], s) for s in ss]
+            assert min(t) > 0 and all(b2 >= a2 for a2, b2 in zip(t, t[1:])), (P, sid)
+            s_rec = [r[0] for r in recs[str(sid)]]
+            y_rec = [r[1] for r in recs[str(sid)]]
+            d, coef, sc = OC.fit_poly(s_rec, y_rec, degrees=(1, 2), s_extrap_max=float(1 << 20))
+            d2, coef2, sc2 = CAL.aic_poly(s_rec, y_rec)
+            assert d == d2 and sc == sc2 and np.allclose(coef, coef2, rtol=1e-12, atol=0), (P, sid)
+            assert np.allclose(coef, e["poly_coef"], rtol=1e-12, atol=0), (P, sid)
+
+
+def test_predicted_trace_adaptive_never_slower_than_a_static_strategy():
+    """--predict (host-only contexts, no GPU): with gamma = 0 the adaptive plan is the
+    least-time feasible plan of Algorithm 1's candidate space, which contains every
+    feasible uniform plan, so per sequence its predicted time is <= every static
+    strategy that can run that sequence, and it trains at least as long."""
+    from paper_2511_13198_b200 import binding as B
+    model = B.Model(h=4096, n_heads=32, ffn=16384, n_layers=32)
+    for P in (1, 8):
+        path = os.path.join(os.path.dirname(T.__file__), "bundles", f"h4096_n32_f16384_P{P}.txt")
+        lens = [8192 * k for k in (1, 2, 3, 5, 8, 13, 21, 34, 55, 78)]
+        ad = T.predict_trace(B, model, path, lens, 32, 0.0)
+        t_ad = {r["s"]: r["seconds"] for r in ad["records"] if "seconds" in r}
+        for name, pi in T.STATIC:
+            st = T.predict_trace(B, model, path, lens, 32, 0.0, fixed=pi)
+            assert ad["max_s_trained"] >= st["max_s_trained"], (P, name)
+            for r in st["records"]:
+                if "seconds" in r:
+                    assert t_ad[r["s"]] <= r["seconds"] * (1 + 1e-12), (P, name, r["s"])
