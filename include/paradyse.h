@@ -318,6 +318,32 @@ pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int
                                const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                                int32_t causal, int32_t qlo, int32_t qn, void* dqkv, void* stream);
 
+/* Ring attention (MegatronCZ, reading R-CZ): one (query block, key block) pair with
+ * queries q [sq][ld_q] (head i at column i*d) and keys / values at columns kcol / vcol
+ * (+ i*d) of kv [sk][ld_kv].  causal = the diagonal pair (sq == sk, aligned positions);
+ * otherwise every key is visible.  out [sq][ld_out] bf16 and lse fp32 [heads][sq] are the
+ * pair's own softmax result.  sq, sk multiples of 128, else PDS_EINVAL. */
+pds_status pds_k_attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int32_t kcol,
+                               int32_t vcol, int32_t sq, int32_t sk, int32_t heads, int32_t d, int32_t causal,
+                               void* out, int64_t ld_out, void* lse, void* stream);
+/* Its backward given the MERGED row statistics lse, Dd (fp32 [heads][sq]; Dd =
+ * rowsum(dO o O), pds_k_attn_dot): dQ * (1/sqrt d) is ADDED to dq_acc [sq][ld_dqa] fp32
+ * and dK * (1/sqrt d) / dV to dkv_acc [sk][ld_dkva] fp32 (dK at column i*d, dV at
+ * heads*d + i*d); no RoPE^T (the caller's, at the rows' positions). */
+pds_status pds_k_attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int32_t kcol,
+                               int32_t vcol, const void* dout, int64_t ld_out, const void* lse, const void* Dd,
+                               int32_t sq, int32_t sk, int32_t heads, int32_t d, int32_t causal, void* dq_acc,
+                               int64_t ld_dqa, void* dkv_acc, int64_t ld_dkva, void* stream);
+/* Log-sum-exp merge of a pair result (o_p bf16 [rows][ld_op], l_p fp32 [heads][lstride_p])
+ * into the running one (o_acc fp32 [rows][ld_oacc], l_acc fp32 [heads][lstride_acc]);
+ * first = 1: the running result is empty.  out (nullable): also the bf16 O. */
+pds_status pds_k_attn_merge(void* o_acc, int64_t ld_oacc, void* l_acc, int64_t lstride_acc, const void* o_p,
+                            int64_t ld_op, const void* l_p, int64_t lstride_p, int32_t rows, int32_t heads,
+                            int32_t d, int32_t first, void* out, int64_t ld_out, void* stream);
+/* D = rowsum(dO o O) per (head, row): Dd fp32 [heads][s]. */
+pds_status pds_k_attn_dot(const void* out, int64_t ld_out, const void* dout, int32_t s, int32_t heads, int32_t d,
+                          void* Dd, void* stream);
+
 /* Attention backward implementation, process wide: 0 = the split dK/dV + dQ kernels
  * (default), 1 = the fused kernel where it applies (d = 128, causal, all query rows;
  * slower on B200: its dQ reduction through L2 is the bottleneck).

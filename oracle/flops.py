@@ -47,7 +47,14 @@ def comm_bytes(pi, h, s, P, ffn=None, b=1, metp_recompute="ffn"):
         a2a = 2 * fr * (s // P) * b * (3 * h + h) * 2
         wb = 4 * h * h + 2 * h * f
         return int(round(a2a + fr * wb * (2 + 2 + 4) + ar))
-    if pi == 3:              # CZ: AG(QKV) fwd + re-gather bwd + RS(dQKV), ZeRO3 weights as UZ
+    if pi == 3:              # CZ (ring, zigzag), ZeRO3 weights as UZ
         wb = 4 * h * h + 2 * h * f
-        return int(round(3 * fr * s * b * 3 * h * 2 + fr * wb * (2 + 2 + 4) + ar))
+        c = s // (2 * P)                                       # half-chunk (positions)
+        # half-chunks whose zigzag owner (j < P ? j : 2P-1-j) is not their boundary
+        # owner j // 2 move in each boundary <-> zigzag exchange; per-rank mean
+        moved = sum(1 for j in range(2 * P) if (j if j < P else 2 * P - 1 - j) != j // 2)
+        zig = moved * c * b * (3 * h + h + h + h + 3 * h) * 2 / P   # QKV, O | O, dO, dQKV
+        kv = (s // P) * b * 2 * h                              # one rank's K/V block (elements)
+        ring = 2 * (P - 1) * kv * 2 + P * kv * 4               # K/V fwd + bwd (bf16), dK/dV (fp32)
+        return int(round(zig + ring + fr * wb * (2 + 2 + 4) + ar))
     raise KeyError(pi)

@@ -83,6 +83,22 @@ class Grid:
         self._log("RingPass", tensors[0].size * bpe, 1.0 if self.p > 1 else 0.0)
         return out
 
+    def permute(self, blocks, dest, bpe=2):
+        """Point-to-point exchange (SendRecv): blocks[r] is the list of blocks device r
+        holds, dest[r][i] the device block i goes to.  Returns, per device, the blocks it
+        receives ordered by (source device, block index).  The log records the mean
+        bytes a device sends off-device (blocks staying on their device are free)."""
+        out = [[] for _ in range(self.p)]
+        moved = 0
+        for r in range(self.p):
+            for i, blk in enumerate(blocks[r]):
+                out[dest[r][i]].append(blk.copy())
+                if dest[r][i] != r:
+                    moved += blk.size * bpe
+        self.comm_log.append({"primitive": "SendRecv", "bytes": int(round(moved / self.p)),
+                              "participants": list(range(self.p))})
+        return out
+
     # ---------------- memory ledger ----------------
     def track(self, dev: int, nbytes: int, tag: str = "") -> int:
         if self.alloc[dev] + nbytes < 0:

@@ -50,8 +50,9 @@ def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
 
 def valid(pi, h, n, ffn, s, P, metp_chunks=None):
     """Reading R-15: the library runs a strategy at (s, P) only when
-    P | s, P | n, 128 | s/P (tile rows), 64 | F/P, and for METP / METP-full also
-    c | s/P and 128 | s/(P c) (c = metp_chunks, default P).  Never padded."""
+    P | s, P | n, 128 | s/P (tile rows), 64 | F/P, for METP / METP-full also
+    c | s/P and 128 | s/(P c) (c = metp_chunks, default P), and for MegatronCZ
+    128 | s/(2P) (its zigzag half-chunks, R-CZ).  Never padded."""
     if s <= 0 or s % P or n % P or (s // P) % 128 or ffn % P or (ffn // P) % 64:
         return False
     if pi in (METP, METP_FULL):
@@ -59,6 +60,8 @@ def valid(pi, h, n, ffn, s, P, metp_chunks=None):
         sl = s // P
         if sl % c or (sl // c) % 128:
             return False
+    if pi == CZ and (s // P) % 256:      # R-CZ: zigzag half-chunks of s/(2P) positions, 128 | s/(2P)
+        return False
     return True
 
 
@@ -71,8 +74,10 @@ def transient_floor(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
             (F/h) u) and its output partial [s, h] before the RS (P u)   -> (P + F/h) u
       UZ    FC2 with the gathered W_out [F, h] (bf16), local G [s/P, F] and output
             [s/P, h]; backward: the full local fp32 dW_out [F, h] beside G   -> max of both
-      CZ    the context-parallel attention over the all-gathered Q/K/V [s, 3h] (3P u),
-            plus UZ's FC2 step in its own phase                           -> max of both
+      CZ    a ring step of the backward: the incoming K/V block (2u), the block's
+            travelling dK/dV partial and its successor (2 x 2u, bf16-equivalent), the
+            zigzag dO and O (2u) and the dQ partial (u); UZ's FC2 step in its own
+            phase                                                            -> max of both
       METP  one wave of TS's FC2 step: G [P w, F/P] and partial [P w, h], w = s/(P c)
             rows of each rank, plus the gathered wave input [P w, h]      -> (2P/c + F/(h c)) u
       METP-full  as METP plus the recomputed Q/K/V of the own heads [s, 3h/P] (3u)
@@ -90,7 +95,7 @@ def transient_floor(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
     if pi == UZ:
         return uz
     if pi == CZ:
-        return max(3 * P * u, uz)
+        return max(9 * u, uz)
     c = metp_chunks or P
     base = (2 * P * u + f * u) // c
     if pi == METP:

@@ -32,7 +32,7 @@ import copy
 import numpy as np
 
 from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
-                    rmsnorm, rmsnorm_bwd)
+                    rmsnorm, rmsnorm_bwd, rope_apply, rope_apply_t, rope_cos_sin)
 
 TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
 NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full"}
@@ -438,28 +438,165 @@ def _gather_qkv_parts(grid, W, h):
     return np.concatenate(parts, axis=0)                           # [3h, h], [Q all; K all; V all]
 
 
+# ------------------------------------------------------------------ MegatronCZ (ring, zigzag)
+# Reading R-CZ: Megatron-LM context parallelism + ZeRO3 weights.  Every
+# GEMM is local on the rank's boundary rows [r s/P, (r+1) s/P) (R-10, kept unchanged
+# so switching needs no redistribution).  Attention alone runs on a
+# causally balanced ("zigzag") placement: the s positions are cut into 2P half-chunks
+# of c = s/(2P); rank r computes the queries of half-chunks r and 2P-1-r, which it
+# receives (with their K, V) by point-to-point sends from their boundary owners, and
+# the keys / values travel around the ring in P steps (K/V of rank (r - k) mod P at
+# step k), so every rank holds O(u) of them at a time.  Each (query half-chunk, key
+# half-chunk) pair is a full block, a causal diagonal block, or empty; at every ring
+# step every rank has two full-block equivalents of work.  Partial results merge by
+# the log-sum-exp identity; the backward runs the same ring with each K/V block's fp32
+# dK / dV accumulator travelling with it (P passes: it comes home), using the merged
+# LSE.  Results return to the boundary layout by the reverse point-to-point exchange.
+
+def _zz(j, P):
+    """Zigzag owner of half-chunk j (of 2P)."""
+    return j if j < P else 2 * P - 1 - j
+
+
+def _zig(r, P):
+    """The half-chunks rank r computes, in position order."""
+    return (r, 2 * P - 1 - r)
+
+
+def _zig_positions(r, P, c):
+    a, b = _zig(r, P)
+    return np.concatenate([np.arange(a * c, (a + 1) * c), np.arange(b * c, (b + 1) * c)])
+
+
+def _to_zigzag(grid, X, bpe=2):
+    """Boundary rows [s/P, ...] per rank -> zigzag rows [half-chunk r ; half-chunk 2P-1-r]."""
+    P = grid.p
+    c = X[0].shape[0] // 2
+    recv = grid.permute([[X[r][:c], X[r][c:]] for r in range(P)],
+                        [[_zz(2 * r, P), _zz(2 * r + 1, P)] for r in range(P)], bpe)
+    out = []
+    for r in range(P):
+        ids = [hc for src in range(P) for hc in (2 * src, 2 * src + 1) if _zz(hc, P) == r]
+        byid = dict(zip(ids, recv[r]))
+        out.append(np.concatenate([byid[j] for j in _zig(r, P)], axis=0))
+    return out
+
+
+def _from_zigzag(grid, Z, bpe=2):
+    """Zigzag rows per rank -> boundary rows (the reverse exchange)."""
+    P = grid.p
+    c = Z[0].shape[0] // 2
+    recv = grid.permute([[Z[r][:c], Z[r][c:]] for r in range(P)],
+                        [[j // 2 for j in _zig(r, P)] for r in range(P)], bpe)
+    out = []
+    for q in range(P):
+        ids = [hc for src in range(P) for hc in _zig(src, P) if hc // 2 == q]
+        byid = dict(zip(ids, recv[q]))
+        out.append(np.concatenate([byid[2 * q], byid[2 * q + 1]], axis=0))
+    return out
+
+
+def _heads(x, n):
+    """[rows, b, n*d] -> [b, n, rows, d]"""
+    rows, b, hd = x.shape
+    return x.reshape(rows, b, n, hd // n).transpose(1, 2, 0, 3)
+
+
+def _unheads(x):
+    b, n, rows, d = x.shape
+    return x.transpose(2, 0, 1, 3).reshape(rows, b, n * d)
+
+
+def _pair_fwd(q, k, v, pq, pk, causal):
+    """Softmax attention of queries q [b, n, rq, d] over keys k / values v [b, n, rk, d]
+    alone (Eq. 2 restricted to these keys), causal by global position: (O, LSE); rows
+    with no visible key have O = 0, LSE = -inf."""
+    sc = np.einsum("bnqd,bnkd->bnqk", q, k) / np.sqrt(q.shape[-1])
+    if causal:
+        sc = np.where(pk[None, None, None, :] > pq[None, None, :, None], -np.inf, sc)
+    m = np.max(sc, axis=-1, keepdims=True)
+    m_safe = np.where(np.isfinite(m), m, 0.0)
+    e = np.exp(sc - m_safe)
+    l = np.sum(e, axis=-1, keepdims=True)
+    o = np.einsum("bnqk,bnkd->bnqd", e, v) / np.where(l > 0, l, 1.0)
+    lse = np.where(l[..., 0] > 0, m_safe[..., 0] + np.log(np.where(l[..., 0] > 0, l[..., 0], 1.0)), -np.inf)
+    return o, lse
+
+
+def _merge(o1, l1, o2, l2):
+    """log-sum-exp merge of two partial softmax results over disjoint key sets."""
+    lse = np.logaddexp(l1, l2)
+    fin = np.isfinite(lse)
+    w1 = np.where(fin, np.exp(np.where(fin, l1 - np.where(fin, lse, 0.0), -np.inf)), 0.0)
+    w2 = np.where(fin, np.exp(np.where(fin, l2 - np.where(fin, lse, 0.0), -np.inf)), 0.0)
+    return w1[..., None] * o1 + w2[..., None] * o2, lse
+
+
+def _pair_bwd(q, k, v, do, lse, D, pq, pk, causal):
+    """The pair's share of the attention backward given the MERGED row LSE and
+    D = rowsum(dO o O): P = exp(S - LSE) on the visible keys; dV = P^T dO;
+    dS = P o (dO V^T - D); dQ = dS K / sqrt(d); dK = dS^T Q / sqrt(d)."""
+    scale = 1.0 / np.sqrt(q.shape[-1])
+    sc = np.einsum("bnqd,bnkd->bnqk", q, k) * scale
+    p = np.exp(sc - lse[..., None])
+    if causal:
+        p = np.where(pk[None, None, None, :] > pq[None, None, :, None], 0.0, p)
+    dv = np.einsum("bnqk,bnqd->bnkd", p, do)
+    ds = p * (np.einsum("bnqd,bnkd->bnqk", do, v) - D[..., None])
+    return np.einsum("bnqk,bnkd->bnqd", ds, k) * scale, np.einsum("bnqk,bnqd->bnkd", ds, q) * scale, dv
+
+
 def cz_fwd(grid, xs, W, cfg):
     P = grid.p
     sl = xs[0].shape[0]
     s = sl * P
-    wq = _gather_qkv_parts(grid, W, cfg.h)
+    h, n = cfg.h, cfg.n
+    c = sl // 2
+    if sl % 2:
+        raise ValueError("MegatronCZ: s must be divisible by 2P (zigzag half-chunks)")
+    wq = _gather_qkv_parts(grid, W, h)
     wp = grid.all_gather(W["w_proj"])[0]
     wi = grid.all_gather(W["w_in_t"])[0]
     wo = grid.all_gather(W["w_out"])[0]
+    d = h // n
     saved = [dict() for _ in range(P)]
-    u, r1, qkv_loc = [], [], []
+    r1, qkv_b = [], []
     for r in range(P):
         ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
-        u.append(ur)
         r1.append(rr)
-        qkv_loc.append(ur @ wq.T)                                  # [s/P, b, 3h], [Q | K | V] all heads
-    qkv = grid.all_gather(qkv_loc)                                 # AG(QKV): the whole context
-    a_all, lse_all = mha_core_fwd(qkv[0], cfg.n, np.arange(s), cfg.causal, cfg.theta)
+        qkv = ur @ wq.T                                            # [s/P, b, 3h], [Q | K | V] all heads
+        cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
+        qr = _unheads(rope_apply(_heads(qkv[..., :h], n), cos, sin))
+        kr = _unheads(rope_apply(_heads(qkv[..., h:2 * h], n), cos, sin))
+        qkv_b.append(np.concatenate([qr, kr, qkv[..., 2 * h:]], axis=-1))   # RoPE at global positions
+    qkvz = _to_zigzag(grid, qkv_b)                                 # SendRecv(QKV): boundary -> zigzag
+    pos = [_zig_positions(r, P, c) for r in range(P)]
+    q = [_heads(qkvz[r][..., :h], n) for r in range(P)]
+    kv = [qkvz[r][..., h:] for r in range(P)]                      # travels around the ring
+    kv_pos = list(pos)
+    o_acc = [np.zeros_like(q[r]) for r in range(P)]
+    l_acc = [np.full(q[r].shape[:-1], -np.inf) for r in range(P)]
+    for k in range(P):
+        for r in range(P):
+            kk = _heads(kv[r][..., :h], n)
+            vv = _heads(kv[r][..., h:], n)
+            for ai in range(2):
+                qa = slice(ai * c, (ai + 1) * c)
+                for bi in range(2):
+                    kb = slice(bi * c, (bi + 1) * c)
+                    if cfg.causal and kv_pos[r][kb][0] > pos[r][qa][-1]:
+                        continue                                   # key half-chunk after every query
+                    o_p, l_p = _pair_fwd(q[r][:, :, qa], kk[:, :, kb], vv[:, :, kb], pos[r][qa],
+                                         kv_pos[r][kb], cfg.causal)
+                    o_acc[r][:, :, qa], l_acc[r][:, :, qa] = _merge(o_acc[r][:, :, qa], l_acc[r][:, :, qa],
+                                                                   o_p, l_p)
+        if k < P - 1:
+            kv = grid.ring_pass(kv, bpe=2)                         # K/V of rank r - k - 1 next
+            kv_pos = [kv_pos[(r - 1) % P] for r in range(P)]
+    a_all = _from_zigzag(grid, [_unheads(o_acc[r]) for r in range(P)])   # SendRecv(O): back to boundary
     y, o, z = [], [], []
     for r in range(P):
-        rows = slice(r * sl, (r + 1) * sl)
-        a_r = a_all[rows]                                          # this rank's query rows
-        lse_r = lse_all[..., rows]
+        a_r = a_all[r]
         o_r = a_r @ wp
         x1 = xs[r] + o_r
         vr, _, rr2 = rmsnorm(x1, W["g2"][r], cfg.eps)
@@ -471,9 +608,9 @@ def cz_fwd(grid, xs, W, cfg):
         sv = saved[r]
         _save(grid, r, sv, "x", xs[r], 2)
         _save(grid, r, sv, "r1", r1[r], 4)
-        _save(grid, r, sv, "qkv", qkv_loc[r], 2)
-        _save(grid, r, sv, "a", a_r, 2)
-        _save(grid, r, sv, "lse", lse_r, 4)
+        _save(grid, r, sv, "qkv", qkvz[r], 2)                      # zigzag rows, post-RoPE
+        _save(grid, r, sv, "a", a_r, 2)                            # boundary rows
+        _save(grid, r, sv, "lse", l_acc[r], 4)                     # zigzag rows
         _save(grid, r, sv, "x1", x1, 2)
         _save(grid, r, sv, "r2", rr2, 4)
         _save(grid, r, sv, "h", hp, 2)
@@ -483,9 +620,9 @@ def cz_fwd(grid, xs, W, cfg):
 def cz_bwd(grid, dys, saved, W, cfg, grads):
     P = grid.p
     sl = dys[0].shape[0]
-    s = sl * P
-    h = cfg.h
-    hl = h // P
+    h, n = cfg.h, cfg.n
+    d = h // n
+    c = sl // 2
     sv = saved
     wq = _gather_qkv_parts(grid, W, h)
     wp = grid.all_gather(W["w_proj"])[0]
@@ -501,34 +638,60 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
         dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
         dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
         xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
-        d, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
-        dx1.append(dys[r] + d)
+        dd, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
+        dx1.append(dys[r] + dd)
         dg2.append(dgr)
-        da.append(dx1[r] @ wp.T)                                   # dA, local rows
+        da.append(dx1[r] @ wp.T)                                   # dA, boundary rows
         dwp.append(np.tensordot(sv[r]["a"], dx1[r], axes=([0, 1], [0, 1])))
-    qkv = grid.all_gather([sv[r]["qkv"] for r in range(P)])        # AG(QKV) re-gather
-    # every rank: the gradients its own query rows induce on all of Q / K / V (the
-    # other rows' cotangents are zero), then RS sums the key / value parts over ranks
-    parts = []
+    oz = _to_zigzag(grid, [sv[r]["a"] for r in range(P)])          # SendRecv(O) -> zigzag
+    doz = _to_zigzag(grid, da)                                     # SendRecv(dO) -> zigzag
+    pos = [_zig_positions(r, P, c) for r in range(P)]
+    q = [_heads(sv[r]["qkv"][..., :h], n) for r in range(P)]
+    do_h = [_heads(doz[r], n) for r in range(P)]
+    D = [np.sum(do_h[r] * _heads(oz[r], n), axis=-1) for r in range(P)]
+    lse = [sv[r]["lse"] for r in range(P)]
+    kv = [sv[r]["qkv"][..., h:] for r in range(P)]
+    kv_pos = list(pos)
+    dkv = [np.zeros_like(kv[r]) for r in range(P)]                 # travels with its K/V block (fp32)
+    dq = [np.zeros_like(q[r]) for r in range(P)]
+    for k in range(P):
+        for r in range(P):
+            kk = _heads(kv[r][..., :h], n)
+            vv = _heads(kv[r][..., h:], n)
+            dk_h = np.zeros_like(kk)
+            dv_h = np.zeros_like(vv)
+            for ai in range(2):
+                qa = slice(ai * c, (ai + 1) * c)
+                for bi in range(2):
+                    kb = slice(bi * c, (bi + 1) * c)
+                    if cfg.causal and kv_pos[r][kb][0] > pos[r][qa][-1]:
+                        continue
+                    gq, gk, gv = _pair_bwd(q[r][:, :, qa], kk[:, :, kb], vv[:, :, kb], do_h[r][:, :, qa],
+                                           lse[r][:, :, qa], D[r][:, :, qa], pos[r][qa], kv_pos[r][kb],
+                                           cfg.causal)
+                    dq[r][:, :, qa] += gq
+                    dk_h[:, :, kb] += gk
+                    dv_h[:, :, kb] += gv
+            dkv[r] = dkv[r] + np.concatenate([_unheads(dk_h), _unheads(dv_h)], axis=-1)
+        if k < P - 1:
+            kv = grid.ring_pass(kv, bpe=2)
+            kv_pos = [kv_pos[(r - 1) % P] for r in range(P)]
+        dkv = grid.ring_pass(dkv, bpe=4)                           # P passes: home after the last
+    dqkvz = []
     for r in range(P):
-        rows = slice(r * sl, (r + 1) * sl)
-        da_full = np.zeros(qkv[r].shape[:-1] + (h,))
-        da_full[rows] = da[r]
-        a_full = np.zeros_like(da_full)
-        a_full[rows] = sv[r]["a"]
-        lse_full = np.zeros(sv[r]["lse"].shape[:-1] + (s,))
-        lse_full[..., rows] = sv[r]["lse"]
-        parts.append(mha_core_bwd(da_full, qkv[r], a_full, lse_full, cfg.n, np.arange(s), cfg.causal,
-                                  cfg.theta))
-    dqkv = grid.reduce_scatter(parts)                              # RS(dQKV)
+        cos, sin = rope_cos_sin(pos[r], d, cfg.theta)              # RoPE^T at the zigzag positions
+        dqr = _unheads(rope_apply_t(dq[r], cos, sin))
+        dkr = _unheads(rope_apply_t(_heads(dkv[r][..., :h], n), cos, sin))
+        dqkvz.append(np.concatenate([dqr, dkr, dkv[r][..., h:]], axis=-1))
+    dqkv = _from_zigzag(grid, dqkvz)                               # SendRecv(dQKV) -> boundary
     dx, dg1 = [], []
     for r in range(P):
         u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
         dwq.append(np.tensordot(dqkv[r], u, axes=([0, 1], [0, 1])))   # [3h, h], [Q; K; V] all
         du = dqkv[r] @ wq
         xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
-        d, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
-        dx.append(dx1[r] + d)
+        dd, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
+        dx.append(dx1[r] + dd)
         dg1.append(dgr)
     # ZeRO3 reduce-scatters (fp32): W_qkv^T part by part back into [Q_r; K_r; V_r]
     qparts = [grid.reduce_scatter([dwq[r][i * h:(i + 1) * h] for r in range(P)], axis=0, bpe=4)

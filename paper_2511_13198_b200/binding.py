@@ -145,6 +145,15 @@ _SIGS = {
     "pds_k_attn_bwd_rows": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
     "pds_set_attn_bwd": [C.c_int32],
+    "pds_k_attn_fwd_pair": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                            C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                            C.c_void_p],
+    "pds_k_attn_bwd_pair": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                            C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                            C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p],
+    "pds_k_attn_merge": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                         C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p],
+    "pds_k_attn_dot": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
     "pds_last_error": [],
     "pds_version": [],
 }
@@ -346,6 +355,26 @@ def k_attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, stream=0):
 
 def k_attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream=0):
     call("pds_k_attn_bwd", qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream)
+
+
+def k_attn_fwd_pair(q, ld_q, kv, ld_kv, kcol, vcol, sq, sk, heads, d, causal, out, ld_out, lse, stream=0):
+    call("pds_k_attn_fwd_pair", q, ld_q, kv, ld_kv, kcol, vcol, sq, sk, heads, d, causal, out, ld_out, lse, stream)
+
+
+def k_attn_bwd_pair(q, ld_q, kv, ld_kv, kcol, vcol, dout, ld_out, lse, dd, sq, sk, heads, d, causal, dq_acc, ld_dqa,
+                    dkv_acc, ld_dkva, stream=0):
+    call("pds_k_attn_bwd_pair", q, ld_q, kv, ld_kv, kcol, vcol, dout, ld_out, lse, dd, sq, sk, heads, d, causal,
+         dq_acc, ld_dqa, dkv_acc, ld_dkva, stream)
+
+
+def k_attn_merge(o_acc, ld_oacc, l_acc, lstride_acc, o_p, ld_op, l_p, lstride_p, rows, heads, d, first, out=None,
+                 ld_out=0, stream=0):
+    call("pds_k_attn_merge", o_acc, ld_oacc, l_acc, lstride_acc, o_p, ld_op, l_p, lstride_p, rows, heads, d, first,
+         out, ld_out, stream)
+
+
+def k_attn_dot(out, ld_out, dout, s, heads, d, dd, stream=0):
+    call("pds_k_attn_dot", out, ld_out, dout, s, heads, d, dd, stream)
 
 
 def set_attn_bwd(mode):

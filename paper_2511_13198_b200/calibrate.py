@@ -182,10 +182,24 @@ def comm_bytes_per_rank(pi, h, F, s, P):
     if pi == 4:              # METP-full: TS bytes + one more AG(u) for the Q/K/V recompute
         return 11 * fr * act + 2 * fr * 8 * h
     wb = 4 * h * h + 2 * h * F
-    if pi == 3:              # CZ: AG(QKV) fwd + re-gather bwd + RS(dQKV), ZeRO3 weights
-        return 3 * fr * 3 * act + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+    if pi == 3:              # CZ (R-CZ): zigzag exchanges + K/V ring (bf16) + dK/dV ring (fp32), ZeRO3 weights
+        return cz_zig_bytes(h, s, P) + cz_ring_bytes(h, s, P) + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
     a2a = 2 * fr * (s // P) * 4 * h * 2
     return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+
+
+def cz_zig_bytes(h, s, P):
+    """MegatronCZ's boundary <-> zigzag point-to-point exchanges per rank per layer (mean):
+    QKV and O (fwd), O, dO and dQKV (bwd); a half-chunk moves unless its zigzag owner is
+    its boundary owner (layer.cpp zig_exchange)."""
+    moved = sum(1 for j in range(2 * P) if (j if j < P else 2 * P - 1 - j) != j // 2)
+    return moved * (s // (2 * P)) * 9 * h * 2 / P
+
+
+def cz_ring_bytes(h, s, P):
+    """K/V ring passes (P - 1 fwd, P - 1 bwd, bf16) and the dK/dV accumulator ring (P, fp32)."""
+    kv = (s // P) * 2 * h
+    return 2 * (P - 1) * kv * 2 + P * kv * 4
 
 
 def class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, classes):
@@ -245,12 +259,13 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                 del w, gr, x, dy
             torch.cuda.empty_cache()
             for pi in ALL:
-                comp = t_unit[pi] / P
-                if pi == 3 and model.causal:
-                    # contiguous context chunks: the last rank's queries see every key, so
-                    # its causal attention share is (2P - 1) / P^2 instead of 1 / P
-                    comp += t_att * ((2 * P - 1) / (P * P) - 1.0 / P)
+                comp = t_unit[pi] / P              # CZ: zigzag placement, every rank 1/P of the attention
                 comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
+                if pi == 3:
+                    # the K/V ring passes run on the side stream under the ring step's
+                    # attention (P steps of 1/P^2 of it each); the rest stays exposed
+                    ring = 2 * (P - 1) * (s // P) * 2 * h * 2 / (link_gbs * 1e9)
+                    comm -= min(ring, t_att / P * (P - 1) / P)
                 if pi in (0, 2, 4):
                     # tile-overlapped AG / RS: each runs under the GEMM that
                     # consumes / produces it (those GEMMs carry 48h^2 of the 72h^2 GEMM
@@ -264,8 +279,9 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx_m.close()
         note = (f"modelled for P={P_target}: P=1 device time / P + comm bytes / {link_gbs} GB/s "
                 "(+ per-collective latency; TS / METP: minus the share hidden under the tile-overlapped "
-                "GEMMs, at least one chunk per collective exposed; CZ: + the causal imbalance of contiguous "
-                "chunks); replace with a measured profile on an 8xB200 box")
+                "GEMMs, at least one chunk per collective exposed; CZ: zigzag-balanced ring attention, its K/V "
+                "ring passes hidden under the ring steps' attention); replace with a measured profile on an "
+                "8xB200 box")
     os.makedirs(out_dir, exist_ok=True)
     path = os.path.join(out_dir, f"h{h}_n{n}_f{ffn}_P{P_target}.txt")
     cap = float(torch.cuda.get_device_properties(0).total_memory)

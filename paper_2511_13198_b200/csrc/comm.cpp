@@ -3,7 +3,9 @@
 #include <cuda.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 #include <cstring>
 #include <string>
 
@@ -48,8 +50,24 @@ pds_status stream_wait32_geq(cudaStream_t st, const uint32_t* addr, uint32_t v) 
   return PDS_OK;
 }
 
+// sends to this rank itself: device copies into the matching receives (same tag)
+static pds_status self_p2p(int rank, const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t st) {
+  for (int i = 0; i < ns; ++i) {
+    if (sends[i].peer != rank) continue;
+    int j = 0;
+    while (j < nr && !(recvs[j].peer == rank && recvs[j].tag == sends[i].tag)) ++j;
+    if (j == nr || recvs[j].bytes != sends[i].bytes) PDS_FAIL(PDS_EINVAL, "p2p: unmatched self transfer");
+    if (recvs[j].ptr != sends[i].ptr)
+      PDS_CUDA(cudaMemcpyAsync(recvs[j].ptr, sends[i].ptr, sends[i].bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return PDS_OK;
+}
+
 // ------------------------------------------------------------------ P = 1
 struct SelfComm : Comm {
+  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t st) override {
+    return self_p2p(0, sends, ns, recvs, nr, st);
+  }
   bool trivial() const override { return true; }
   pds_status all_gather(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     if (send != recv) PDS_CUDA(cudaMemcpyAsync(recv, send, count * dt_size(dt), cudaMemcpyDeviceToDevice, st));
@@ -123,6 +141,23 @@ struct NcclComm : Comm {
   }
   pds_status all_gather(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     PDS_NCCL(ncclAllGather(send, recv, (size_t)count, nt(dt), comm, st));
+    return PDS_OK;
+  }
+  // one NCCL group; between two ranks, sends and receives match in issue order, so
+  // both sides issue their transfers to / from each peer sorted by tag
+  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t st) override {
+    PDS_TRY(self_p2p(rank, sends, ns, recvs, nr, st));
+    std::vector<int> si, ri;
+    for (int i = 0; i < ns; ++i)
+      if (sends[i].peer != rank) si.push_back(i);
+    for (int i = 0; i < nr; ++i)
+      if (recvs[i].peer != rank) ri.push_back(i);
+    std::sort(si.begin(), si.end(), [&](int a, int b) { return sends[a].tag < sends[b].tag; });
+    std::sort(ri.begin(), ri.end(), [&](int a, int b) { return recvs[a].tag < recvs[b].tag; });
+    PDS_NCCL(ncclGroupStart());
+    for (int i : si) PDS_NCCL(ncclSend(sends[i].ptr, (size_t)sends[i].bytes, ncclUint8, sends[i].peer, comm, st));
+    for (int i : ri) PDS_NCCL(ncclRecv(recvs[i].ptr, (size_t)recvs[i].bytes, ncclUint8, recvs[i].peer, comm, st));
+    PDS_NCCL(ncclGroupEnd());
     return PDS_OK;
   }
   pds_status reduce_scatter(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
@@ -278,6 +313,27 @@ struct LoopComm : Comm {
   void wait_ready(cudaStream_t st) {
     for (int j = 0; j < P; ++j)
       if (j != rank) cudaStreamWaitEvent(st, g->ready[j], 0);
+  }
+  // every rank publishes its receive list (a host array); each rank then copies its
+  // sends into the matching peer receives once that peer's stream reached the call
+  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t st) override {
+    std::vector<P2P> mine(recvs, recvs + nr);
+    mine.push_back(P2P{-1, 0, nullptr, 0});            // terminator
+    publish(mine.data(), st);
+    for (int i = 0; i < ns; ++i) {
+      const P2P* theirs = static_cast<const P2P*>(g->ptr[sends[i].peer]);
+      const P2P* m = theirs;
+      while (m->peer >= 0 && !(m->peer == rank && m->tag == sends[i].tag)) ++m;
+      if (m->peer < 0 || m->bytes != sends[i].bytes) {
+        g->barrier();                                   // keep the peers' barrier count
+        PDS_FAIL(PDS_EINVAL, "p2p: unmatched loopback transfer");
+      }
+      if (sends[i].peer != rank) PDS_CUDA(cudaStreamWaitEvent(st, g->ready[sends[i].peer], 0));
+      if (m->ptr != sends[i].ptr)
+        PDS_CUDA(cudaMemcpyAsync(m->ptr, sends[i].ptr, sends[i].bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    finish(st);                                         // every peer's copy into our receives is done
+    return PDS_OK;
   }
   pds_status all_gather(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) override {
     const int64_t b = count * dt_size(dt);

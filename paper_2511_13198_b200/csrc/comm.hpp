@@ -16,9 +16,22 @@ namespace pds {
 
 enum DType { DT_BF16 = 0, DT_F32 = 1 };
 
+// one point-to-point transfer of a p2p() call: `bytes` from / to device memory `ptr`;
+// a send to `peer` is matched with that peer's receive from this rank of the same tag
+struct P2P {
+  int peer;
+  int tag;
+  void* ptr;
+  int64_t bytes;
+};
+
 struct Comm {
   int P = 1, rank = 0;
   virtual ~Comm() {}
+  // grouped point-to-point sends and receives (ring passes, the zigzag exchange of the
+  // context-parallel attention); a send to this rank itself is a device copy into the
+  // matching receive.  Every rank calls it at the same point of the program.
+  virtual pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t st) = 0;
   // recv [P][count] <- send [count] of every rank (rank order).  send may alias
   // recv + rank*count (in place).
   virtual pds_status all_gather(const void* send, void* recv, int64_t count, DType dt, cudaStream_t st) = 0;

@@ -169,6 +169,42 @@ extern "C" pds_status pds_k_attn_bwd_rows(const void* qkv, int64_t ld, const voi
   return r;
 }
 
+extern "C" pds_status pds_k_attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int32_t kcol,
+                                          int32_t vcol, int32_t sq, int32_t sk, int32_t heads, int32_t d,
+                                          int32_t causal, void* out, int64_t ld_out, void* lse, void* stream) {
+  if (!q || !kv || !out || !lse) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_fwd_pair(q, ld_q, kv, ld_kv, kcol, vcol, sq, sk, heads, d, causal, out, ld_out, lse,
+                            static_cast<cudaStream_t>(stream)), "pds_k_attn_fwd_pair");
+}
+
+extern "C" pds_status pds_k_attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int32_t kcol,
+                                          int32_t vcol, const void* dout, int64_t ld_out, const void* lse,
+                                          const void* Dd, int32_t sq, int32_t sk, int32_t heads, int32_t d,
+                                          int32_t causal, void* dq_acc, int64_t ld_dqa, void* dkv_acc,
+                                          int64_t ld_dkva, void* stream) {
+  if (!q || !kv || !dout || !lse || !Dd || !dq_acc || !dkv_acc) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_bwd_pair(q, ld_q, kv, ld_kv, kcol, vcol, dout, ld_out, lse, static_cast<const float*>(Dd), sq, sk,
+                            heads, d, causal, static_cast<float*>(dq_acc), ld_dqa, static_cast<float*>(dkv_acc),
+                            ld_dkva, static_cast<cudaStream_t>(stream)), "pds_k_attn_bwd_pair");
+}
+
+extern "C" pds_status pds_k_attn_merge(void* o_acc, int64_t ld_oacc, void* l_acc, int64_t lstride_acc,
+                                       const void* o_p, int64_t ld_op, const void* l_p, int64_t lstride_p,
+                                       int32_t rows, int32_t heads, int32_t d, int32_t first, void* out,
+                                       int64_t ld_out, void* stream) {
+  if (!o_acc || !l_acc || !o_p || !l_p) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_merge(static_cast<float*>(o_acc), ld_oacc, static_cast<float*>(l_acc), lstride_acc, o_p, ld_op,
+                         static_cast<const float*>(l_p), lstride_p, rows, heads, d, first, out, ld_out,
+                         static_cast<cudaStream_t>(stream)), "pds_k_attn_merge");
+}
+
+extern "C" pds_status pds_k_attn_dot(const void* out, int64_t ld_out, const void* dout, int32_t s, int32_t heads,
+                                     int32_t d, void* Dd, void* stream) {
+  if (!out || !dout || !Dd) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  return rc2s(attn_dot(out, ld_out, dout, s, heads, d, static_cast<float*>(Dd), static_cast<cudaStream_t>(stream)),
+              "pds_k_attn_dot");
+}
+
 extern "C" pds_status pds_set_attn_bwd(int32_t mode) {
   if (mode != 0 && mode != 1) PDS_FAIL(PDS_EINVAL, "attention backward mode must be 0 (split) or 1 (fused)");
   set_attn_bwd_mode(mode);

@@ -93,4 +93,113 @@ int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, 
   return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, qlo, qn);
 }
 
+// ------------------------------------------------------------------ ring attention helpers
+// Log-sum-exp merge of a pair's partial attention (o_p bf16 [rows][ld_op], l_p fp32
+// [heads][lstride_p]) into the running result (o_acc fp32 [rows][ld_oacc], l_acc fp32
+// [heads][lstride_acc]): L = log(e^La + e^Lp), O = e^(La-L) O_acc + e^(Lp-L) O_p.
+// first: the accumulator is empty (copy).  out (nullable): also write bf16 O.
+// Thread = (row, head, 8 columns); d / 8 threads per (row, head).
+__global__ void attn_merge_kernel(float* __restrict__ o_acc, int64_t ld_oacc, float* __restrict__ l_acc,
+                                  int64_t lstride_acc, const __nv_bfloat16* __restrict__ o_p, int64_t ld_op,
+                                  const float* __restrict__ l_p, int64_t lstride_p, int rows, int heads, int d,
+                                  int first, __nv_bfloat16* __restrict__ out, int64_t ld_out) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = d / 8;
+  if (gi >= (int64_t)rows * heads * per) return;
+  const int g = (int)(gi % per), head = (int)((gi / per) % heads), row = (int)(gi / ((int64_t)per * heads));
+  const float lp = l_p[(int64_t)head * lstride_p + row];
+  float* la_p = l_acc + (int64_t)head * lstride_acc + row;
+  const float la = first ? -INFINITY : *la_p;
+  const float m = fmaxf(la, lp);
+  float wa = 0.f, wp = 0.f, L = -INFINITY;
+  if (m > -INFINITY) {
+    const float ea = expf(la - m), ep = expf(lp - m);
+    L = m + logf(ea + ep);
+    wa = ea / (ea + ep);
+    wp = ep / (ea + ep);
+  }
+  float* oa = o_acc + (int64_t)row * ld_oacc + head * d + 8 * g;
+  const __nv_bfloat16* op = o_p + (int64_t)row * ld_op + head * d + 8 * g;
+  const uint4 pv = *reinterpret_cast<const uint4*>(op);
+  const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pv);
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(p2[i]);
+    v[2 * i] = f.x * wp;
+    v[2 * i + 1] = f.y * wp;
+  }
+  if (!first) {
+    const float4 a0 = reinterpret_cast<const float4*>(oa)[0], a1 = reinterpret_cast<const float4*>(oa)[1];
+    v[0] += a0.x * wa; v[1] += a0.y * wa; v[2] += a0.z * wa; v[3] += a0.w * wa;
+    v[4] += a1.x * wa; v[5] += a1.y * wa; v[6] += a1.z * wa; v[7] += a1.w * wa;
+  }
+  reinterpret_cast<float4*>(oa)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(oa)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  if (out) {
+    __nv_bfloat162 b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(out + (int64_t)row * ld_out + head * d + 8 * g) = *reinterpret_cast<const uint4*>(b);
+  }
+  if (g == 0) *la_p = L;
+}
+
+int attn_merge(float* o_acc, int64_t ld_oacc, float* l_acc, int64_t lstride_acc, const void* o_p, int64_t ld_op,
+               const float* l_p, int64_t lstride_p, int rows, int heads, int d, int first, void* out, int64_t ld_out,
+               cudaStream_t st) {
+  if (d % 8 || ld_oacc % 4 || ld_op % 8 || (out && ld_out % 8)) return (int)cudaErrorInvalidValue;
+  const int64_t n = (int64_t)rows * heads * (d / 8);
+  if (n == 0) return 0;
+  attn_merge_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      o_acc, ld_oacc, l_acc, lstride_acc, reinterpret_cast<const __nv_bfloat16*>(o_p), ld_op, l_p, lstride_p, rows,
+      heads, d, first, reinterpret_cast<__nv_bfloat16*>(out), ld_out);
+  return (int)cudaGetLastError();
+}
+
+// fp32 [rows][ld_src] -> bf16 [rows][ld_dst], `cols` columns; rope (nullable): RoPE^T on
+// every head's (k, k + d/2) pairs at position pos(row) = (row < half ? base0 : base1) +
+// (row % half) / b  (two position runs: a zigzag pair of half-chunks of b sequences).
+// Thread = (row, one pair column k of one head) -> columns k and k + d/2.
+__global__ void rope_t_f32_bf16_kernel(const float* __restrict__ src, int64_t ld_src, int rows, int cols, int d,
+                                       const float2* __restrict__ rope, int64_t base0, int64_t base1, int half,
+                                       int b, __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int pairs = cols / 2;
+  if (gi >= (int64_t)rows * pairs) return;
+  const int row = (int)(gi / pairs), pc = (int)(gi % pairs);
+  const int head = pc / (d / 2), k = pc % (d / 2);
+  const float* s = src + (int64_t)row * ld_src + head * d;
+  float x = s[k], y = s[k + d / 2];
+  if (rope) {
+    const int64_t pos = (row < half ? base0 : base1) + (row % half) / b;
+    const float2 cs = rope[pos * (d / 2) + k];
+    const float nx = x * cs.x + y * cs.y;
+    y = -x * cs.y + y * cs.x;
+    x = nx;
+  }
+  __nv_bfloat16* o = dst + (int64_t)row * ld_dst + head * d;
+  o[k] = __float2bfloat16_rn(x);
+  o[k + d / 2] = __float2bfloat16_rn(y);
+}
+
+int rope_t_f32_bf16(const float* src, int64_t ld_src, int rows, int cols, int d, const void* rope, int64_t base0,
+                    int64_t base1, int half, int b, void* dst, int64_t ld_dst, cudaStream_t st) {
+  if (cols % d || d % 2 || half <= 0 || b <= 0) return (int)cudaErrorInvalidValue;
+  const int64_t n = (int64_t)rows * (cols / 2);
+  if (n == 0) return 0;
+  rope_t_f32_bf16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      src, ld_src, rows, cols, d, reinterpret_cast<const float2*>(rope), base0, base1, half, b,
+      reinterpret_cast<__nv_bfloat16*>(dst), ld_dst);
+  return (int)cudaGetLastError();
+}
+
+// D = rowsum(dO o O) alone (ring attention: once per layer on the zigzag rows)
+int attn_dot(const void* out, int64_t ld_out, const void* dout, int s, int heads, int d, float* Dd, cudaStream_t st) {
+  attn_bwd_dot_kernel<<<(s * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,
+                                                          reinterpret_cast<const __nv_bfloat16*>(dout), s, heads, d,
+                                                          Dd, nullptr, 0);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace pds

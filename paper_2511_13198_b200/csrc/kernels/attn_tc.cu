@@ -171,9 +171,9 @@ struct Fwd2Cfg {
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int s, int heads, int causal,
-                       __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
-                       float scale_log2, int qlo, int qn) {
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmq, int s,
+                       int heads, int causal, __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
+                       float scale_log2, int qlo, int qn, int kcol, int vcol) {
   using C = Fwd2Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -193,12 +193,12 @@ __global__ void __launch_bounds__(384, 1)
   const int nqb = (qn + 255) / 256;
   const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int head = blockIdx.y;
-  const int hq = heads * D;
   const int q0 = qlo + qb * 256;
   const int nkv = causal ? min(s, q0 + 256) / BN : s / BN;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
+    tma_prefetch(&tmq);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
@@ -221,15 +221,14 @@ __global__ void __launch_bounds__(384, 1)
       mbar_arrive_expect_tx(q_full, 2 * C::TILE);
       for (int t = 0; t < 2; ++t)
         for (int a = 0; a < D / 64; ++a)
-          tma_load_2d(sm + C::Q_OFF + t * C::TILE + a * 16384, &tm, q_full, head * D + a * 64, q0 + 128 * t);
+          tma_load_2d(sm + C::Q_OFF + t * C::TILE + a * 16384, &tmq, q_full, head * D + a * 64, q0 + 128 * t);
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1;
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], hq + head * D + a * 64, j * BN);
-          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], 2 * hq + head * D + a * 64,
-                      j * BN);
+          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], kcol + head * D + a * 64, j * BN);
+          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], vcol + head * D + a * 64, j * BN);
         }
       }
     }
@@ -514,7 +513,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                           const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                           int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2, int qlo,
-                          int qn) {
+                          int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc) {
   using C = BwdKV4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -569,8 +568,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     if (elect_one()) {
       mbar_arrive_expect_tx(kv_full, 2 * C::T);
       for (int a = 0; a < D / 64; ++a) {
-        tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, hq + head * D + a * 64, k0);
-        tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, 2 * hq + head * D + a * 64, k0);
+        tma_load_2d(sm + C::K_OFF + a * 16384, &tkv, kv_full, kcol + head * D + a * 64, k0);
+        tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, vcol + head * D + a * 64, k0);
       }
       for (int i = 0; i < nq; ++i) {
         const int b = i % NST, q0 = (qstart + i) * 128;
@@ -763,6 +762,28 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     mbar_wait(fin, 0);
     tc_fence_after();
     const int key = k0 + t;
+    if (acc) {
+      // accumulate mode (ring attention): dK (scaled, no RoPE^T) at columns head*D and
+      // dV at heads*D + head*D of the fp32 row, added to what is there
+      float* arow = acc + (int64_t)key * ld_acc + head * D;
+      for (int task = wg; task < 2 * (D / 32); task += NWG) {
+        const int kv = task / (D / 32), c = task % (D / 32);
+        uint32_t r[32];
+        tmem_ld32(lb + (kv ? DV_COL : DK_COL) + c * 32, r);
+        tmem_ld_wait();
+        const float sc = kv ? 1.0f : scale;
+        float4* d4 = reinterpret_cast<float4*>(arow + kv * heads * D + c * 32);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float4 v = d4[e];
+          v.x += __uint_as_float(r[4 * e]) * sc;
+          v.y += __uint_as_float(r[4 * e + 1]) * sc;
+          v.z += __uint_as_float(r[4 * e + 2]) * sc;
+          v.w += __uint_as_float(r[4 * e + 3]) * sc;
+          d4[e] = v;
+        }
+      }
+    } else {
     __nv_bfloat16* rowp = dqkv + (int64_t)key * ld + head * D;
     // epilogue tasks: D/64 RoPE^T chunk pairs of dK, then D/32 chunks of dV
     for (int task = wg; task < D / 64 + D / 32; task += NWG) {
@@ -788,6 +809,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         store32_bf16(rowp + 2 * hq + c * 32, v);
       }
+    }
     }
   }
   tc_fence_before();
@@ -818,7 +840,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     attn_bwd_dq4_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld, const __nv_bfloat16* __restrict__ dout,
                         int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
                         const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
-                        const float2* __restrict__ rope, float scale, float scale_log2, int qlo, int qn) {
+                        const float2* __restrict__ rope, float scale, float scale_log2, int qlo, int qn, int kcol,
+                        int vcol, int64_t ld_dq, float* __restrict__ acc, int64_t ld_acc) {
   using C = BwdQ4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -838,7 +861,6 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   const int nqb = qn / 128;                 // local query blocks of [qlo, qlo + qn)
   const int qb = qlo / 128 + (causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x);
   const int head = blockIdx.y;
-  const int hq = heads * D;
   const int q0 = qb * 128;
   const int nkv = causal ? qb + 1 : s / 128;
   constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
@@ -871,8 +893,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[b], 2 * C::T);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], hq + head * D + a * 64, j * 128);
-          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], 2 * hq + head * D + a * 64, j * 128);
+          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], kcol + head * D + a * 64, j * 128);
+          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], vcol + head * D + a * 64, j * 128);
         }
       }
     }
@@ -1034,7 +1056,25 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     }
     mbar_wait(fin, 0);
     tc_fence_after();
-    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld + head * D;
+    if (acc) {                               // accumulate mode: dQ (scaled, no RoPE^T) into fp32
+      float* arow = acc + (int64_t)(row - qlo) * ld_acc + head * D;
+      for (int c = wg; c < D / 32; c += NWG) {
+        uint32_t r[32];
+        tmem_ld32(lb + DQ_COL + c * 32, r);
+        tmem_ld_wait();
+        float4* d4 = reinterpret_cast<float4*>(arow + c * 32);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float4 v = d4[e];
+          v.x += __uint_as_float(r[4 * e]) * scale;
+          v.y += __uint_as_float(r[4 * e + 1]) * scale;
+          v.z += __uint_as_float(r[4 * e + 2]) * scale;
+          v.w += __uint_as_float(r[4 * e + 3]) * scale;
+          d4[e] = v;
+        }
+      }
+    } else {
+    __nv_bfloat16* rowp = dqkv + (int64_t)row * ld_dq + head * D;
     for (int c = wg; c < D / 64; c += NWG) {
       uint32_t ra[32], rb[32];
       tmem_ld32(lb + DQ_COL + c * 32, ra);
@@ -1046,6 +1086,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
       store32_bf16(rowp + c * 32, a);
       store32_bf16(rowp + c * 32 + D / 2, bb);
+    }
     }
   }
   tc_fence_before();
@@ -1579,12 +1620,17 @@ int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// q: queries [rows of the q map][ld_q] (head i at column i*D); kv: keys at column kcol
+// and values at vcol (head i at + i*D) of [s][ld_kv]; q == kv with kcol = heads*D, vcol =
+// 2*heads*D is the packed [Q | K | V] buffer.  Query rows [qlo, qlo + qn) of the q map.
 template <int D>
-static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, void* out, int64_t ld_out,
-                    void* lse, int qlo, int qn, cudaStream_t st) {
-  CUtensorMap tm;
-  int rc = make_map_rows(&tm, qkv, (uint64_t)3 * heads * D, (uint64_t)s, (uint64_t)ld);
-  if (rc) return rc;
+static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
+                    int s, int heads, int causal, void* out, int64_t ld_out, void* lse, int qlo, int qn,
+                    cudaStream_t st) {
+  CUtensorMap tm, tmq;
+  int rc = make_map_rows(&tm, kv, (uint64_t)vcol + heads * D, (uint64_t)s, (uint64_t)ld_kv);
+  rc |= make_map_rows(&tmq, q, (uint64_t)heads * D, q_rows, (uint64_t)ld_q);
+  if (rc) return (int)cudaErrorInvalidValue;
   static bool once = false;
   if (!once) {
     cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
@@ -1592,8 +1638,8 @@ static int fwd_tc_t(const void* qkv, int64_t ld, int s, int heads, int causal, v
   }
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
   attn_fwd_tc_kernel<D><<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
-      tm, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
-      scale_log2, qlo, qn);
+      tm, tmq, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
+      scale_log2, qlo, qn, kcol, vcol);
   return (int)cudaGetLastError();
 }
 
@@ -1601,20 +1647,42 @@ int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal
                 void* lse, cudaStream_t st, int qlo, int qn) {
   if (qn < 0) qn = s;
   if (s % 128 || (ld % 8) || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s) return (int)cudaErrorInvalidValue;
-  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, heads, causal, out, ld_out, lse, qlo, qn, st);
-  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, heads, causal, out, ld_out, lse, qlo, qn, st);
+  const int hq = heads * d;
+  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, 2 * hq, s, heads, causal, out, ld_out, lse, qlo, qn, st);
+  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, 2 * hq, s, heads, causal, out, ld_out, lse, qlo, qn, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+// One (query block, key block) pair of ring attention: queries q [sq][ld_q] against keys /
+// values of kv [sk][ld_kv] (columns kcol / vcol); causal = the diagonal pair (sq == sk,
+// aligned positions), else every key is visible.  out / lse as attn_fwd_tc (the pair's
+// own softmax; pairs merge by log-sum-exp).
+int attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, int sq, int sk,
+                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st) {
+  if (sq % 128 || sk % 128 || sq <= 0 || sk <= 0 || ld_q % 8 || ld_kv % 8 || kcol % 8 || vcol % 8 ||
+      (causal && sq != sk))
+    return (int)cudaErrorInvalidValue;
+  if (d == 128)
+    return fwd_tc_t<128>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st);
+  if (d == 64) return fwd_tc_t<64>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st);
   return (int)cudaErrorInvalidValue;
 }
 
 }  // namespace pds
 
 namespace pds {
+// q / kv as fwd_tc_t.  dqkv != NULL: bf16 dQ (RoPE^T) into dqkv [q rows][ld] at columns
+// head*D and dK / dV into dqkv at kcol / vcol of the key rows (the packed-buffer layout:
+// q == kv == the QKV buffer).  dqkv == NULL: accumulate mode — dQ (scaled) added into
+// dq_acc [qn][heads*D] fp32, dK (scaled) / dV into dkv_acc [s][2*heads*D] fp32, no RoPE^T.
 template <int D>
-static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
-                    int s, int heads, int causal, void* dqkv, const void* rope, int qlo, int qn, cudaStream_t st) {
-  const uint64_t cols = (uint64_t)3 * heads * D;
-  CUtensorMap kv128, do128;
-  int rc = make_map_rows(&kv128, qkv, cols, s, ld, 128);
+static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
+                    const void* dout, int64_t ld_out, const void* lse, const float* Dd, int s, int heads, int causal,
+                    void* dqkv, int64_t ld, const void* rope, int qlo, int qn, float* dq_acc, int64_t ld_dqa,
+                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st) {
+  CUtensorMap kv128, q128, do128;
+  int rc = make_map_rows(&kv128, kv, (uint64_t)vcol + heads * D, s, ld_kv, 128);
+  rc |= make_map_rows(&q128, q, (uint64_t)heads * D, q_rows, ld_q, 128);
   rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, qn, ld_out, 128);
   if (rc) return (int)cudaErrorInvalidValue;
   // Elementwise warpgroups per CTA, measured under fixed clocks (ncu --clock-control
@@ -1640,16 +1708,16 @@ static int bwd_tc_t(const void* qkv, int64_t ld, const void* dout, int64_t ld_ou
     // causal: key blocks past the last local query get nothing (the caller zeroes them)
     const int nkb = causal ? (qlo + qn) / 128 : s / 128;
     attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
-        kv128, kv128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
+        kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
         reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2,
-        qlo, qn);
+        qlo, qn, kcol, vcol, dkv_acc, ld_dkva);
   };
   auto dq = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
     attn_bwd_dq4_kernel<D, NW><<<dim3(qn / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(qkv), ld, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
+        reinterpret_cast<const __nv_bfloat16*>(q), ld_q, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
         reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn);
+        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn, kcol, vcol, ld, dq_acc, ld_dqa);
   };
   if (force == 2) dkdv(std::integral_constant<int, 2>{});
   else dkdv(std::integral_constant<int, 4>{});
@@ -1689,8 +1757,31 @@ int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, c
   if (qn < 0) qn = s;
   if (s % 128 || ld % 8 || ld_out % 8 || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s)
     return (int)cudaErrorInvalidValue;
-  if (d == 128) return bwd_tc_t<128>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, qlo, qn, st);
-  if (d == 64) return bwd_tc_t<64>(qkv, ld, dout, ld_out, lse, Dd, s, heads, causal, dqkv, rope, qlo, qn, st);
+  const int hq = heads * d;
+  if (d == 128)
+    return bwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, 2 * hq, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope,
+                         qlo, qn, nullptr, 0, nullptr, 0, st);
+  if (d == 64)
+    return bwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, 2 * hq, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope, qlo,
+                        qn, nullptr, 0, nullptr, 0, st);
+  return (int)cudaErrorInvalidValue;
+}
+
+// Backward of one ring-attention pair (attn_fwd_pair): lse / Dd [heads][sq] are the
+// MERGED row statistics; dQ (scaled) accumulates into dq_acc [sq][heads*d] fp32, dK
+// (scaled) / dV into dkv_acc [sk][2*heads*d] fp32; RoPE^T is the caller's.
+int attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, const void* dout,
+                  int64_t ld_out, const void* lse, const float* Dd, int sq, int sk, int heads, int d, int causal,
+                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st) {
+  if (sq % 128 || sk % 128 || sq <= 0 || sk <= 0 || ld_q % 8 || ld_kv % 8 || ld_out % 8 || kcol % 8 || vcol % 8 ||
+      ld_dqa % 4 || ld_dkva % 4 || (causal && sq != sk) || !dq_acc || !dkv_acc)
+    return (int)cudaErrorInvalidValue;
+  if (d == 128)
+    return bwd_tc_t<128>(q, ld_q, sq, kv, ld_kv, kcol, vcol, dout, ld_out, lse, Dd, sk, heads, causal, nullptr, 0,
+                         nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st);
+  if (d == 64)
+    return bwd_tc_t<64>(q, ld_q, sq, kv, ld_kv, kcol, vcol, dout, ld_out, lse, Dd, sk, heads, causal, nullptr, 0,
+                        nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st);
   return (int)cudaErrorInvalidValue;
 }
 }  // namespace pds

@@ -21,6 +21,21 @@ int attn_fwd_rows(const void* qkv, int64_t ld, int s, int heads, int d, int caus
 int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
                   const void* dout, int s, int heads, int d, int causal, int qlo, int qn, void* dqkv,
                   const void* rope, float* Dd, cudaStream_t st);
+// ring attention (MegatronCZ, attn_tc.cu / attention.cu): one (query block, key block)
+// pair with separate query and key / value buffers, its backward in fp32-accumulate
+// mode, the log-sum-exp merge of pair results, the RoPE^T + bf16 conversion of the
+// accumulated gradients, and D = rowsum(dO o O)
+int attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, int sq, int sk,
+                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st);
+int attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, const void* dout,
+                  int64_t ld_out, const void* lse, const float* Dd, int sq, int sk, int heads, int d, int causal,
+                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st);
+int attn_merge(float* o_acc, int64_t ld_oacc, float* l_acc, int64_t lstride_acc, const void* o_p, int64_t ld_op,
+               const float* l_p, int64_t lstride_p, int rows, int heads, int d, int first, void* out, int64_t ld_out,
+               cudaStream_t st);
+int rope_t_f32_bf16(const float* src, int64_t ld_src, int rows, int cols, int d, const void* rope, int64_t base0,
+                    int64_t base1, int half, int b, void* dst, int64_t ld_dst, cudaStream_t st);
+int attn_dot(const void* out, int64_t ld_out, const void* dout, int s, int heads, int d, float* Dd, cudaStream_t st);
 int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps, void* x1_out,
                 void* u_out, void* rstd, cudaStream_t st);
 int rmsnorm_bwd_grid(int64_t rows);

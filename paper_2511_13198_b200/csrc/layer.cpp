@@ -453,6 +453,16 @@ struct Exec {
     Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
     return c->comm->reduce_scatter(send, recv, count, dt, st);
   }
+  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t on) {
+    pds_status rc = PDS_OK;
+    Comm* cm = on == st ? c->comm : c->comm->side(&rc);
+    if (!cm) return rc;
+    double bytes = 0;
+    for (int i = 0; i < ns; ++i)
+      if (sends[i].peer != r) bytes += (double)sends[i].bytes;
+    Prof p(c, on, K_COMM, 0, bytes);
+    return cm->p2p(sends, ns, recvs, nr, on);
+  }
   pds_status a2a(const void* send, void* recv, int64_t count) {
     Prof p(c, st, K_COMM, 0, (double)count * 2 * (P - 1));
     return c->comm->all_to_all(send, recv, count, DT_BF16, st);
@@ -778,56 +788,150 @@ pds_status cz_wqkv(Exec& e, const pds_weights* w, char* wqkv, cudaStream_t on) {
   return PDS_OK;
 }
 
+// ---------------------------------------------------------------- ring attention (R-CZ)
+// Zigzag placement of the attention (DESIGN.md R-CZ): the s positions are 2P half-chunks
+// of c = s/(2P); rank r computes the queries of half-chunks r and 2P-1-r ("zig rows":
+// [half-chunk r ; half-chunk 2P-1-r], c*b rows each, b sequences interleaved as in the
+// boundary layout).  Every other tensor of the layer stays on the boundary rows.
+struct Zig {
+  int P, r;
+  int64_t c, cb;                                      // positions / rows per half-chunk
+  int zz(int j) const { return j < P ? j : 2 * P - 1 - j; }
+  int hc(int i) const { return i == 0 ? r : 2 * P - 1 - r; }    // half-chunk of zig half i
+};
+
+// boundary rows X [2 cb][cols] -> zig rows Z (to_zig) or back (!to_zig), bf16
+pds_status zig_exchange(Exec& e, const Zig& z, char* X, char* Z, int64_t cols, bool to_zig) {
+  const int64_t bytes = z.cb * cols * 2;
+  P2P snd[2], rcv[2];
+  for (int i = 0; i < 2; ++i) {
+    const int own = 2 * z.r + i;                      // boundary half-chunks 2r, 2r+1
+    const int mine = z.hc(i);                         // zig half-chunks r, 2P-1-r
+    if (to_zig) {
+      snd[i] = P2P{z.zz(own), own, X + i * bytes, bytes};
+      rcv[i] = P2P{mine / 2, mine, Z + i * bytes, bytes};
+    } else {
+      snd[i] = P2P{mine / 2, mine, Z + i * bytes, bytes};
+      rcv[i] = P2P{z.zz(own), own, X + i * bytes, bytes};
+    }
+  }
+  return e.p2p(snd, 2, rcv, 2, e.st);
+}
+
+// the ring: send `cur` to rank r+1, receive rank r-1's block into `nxt`
+pds_status ring_pass(Exec& e, const char* cur, char* nxt, int64_t bytes, cudaStream_t on) {
+  P2P snd{(e.r + 1) % e.P, 0, const_cast<char*>(cur), bytes};
+  P2P rcv{(e.r - 1 + e.P) % e.P, 0, nxt, bytes};
+  return e.p2p(&snd, 1, &rcv, 1, on);
+}
+
 pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
+  const int64_t n = e.m.n_heads, h = e.h;
+  const Zig z{e.P, e.r, e.sp / 2, e.sl / 2};
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
   char* wout = ws + bp.ws_off("wout");
   char* u1 = ws + bp.ws_off("u1");
-  char* qkvg = ws + bp.ws_off("qkvg");
+  char* qkvb = ws + bp.ws_off("qkvb");
+  char* kvb[2] = {ws + bp.ws_off("kv0"), ws + bp.ws_off("kv1")};
+  float* oacc = reinterpret_cast<float*>(ws + bp.ws_off("acc"));
+  char* op = ws + bp.ws_off("op");
+  char* oz = ws + bp.ws_off("oz");
+  float* lp = reinterpret_cast<float*>(ws + bp.ws_off("lp"));
   char* v2 = ws + bp.ws_off("v2");
   char* f0 = ws + bp.ws_off("f0");
+  char* qkvz = sv->at("qkv");                        // saved: zig rows, post-RoPE [Q | K | V]
+  float* lse = reinterpret_cast<float*>(sv->at("lse"));   // saved: [b][2 zig halves][n][c]
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_TRY(e.link(e.st, cs));                 // gather buffers free (previous layer done with them)
   PDS_TRY(cz_wqkv(e, w, wqkv, e.st));
-  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * e.h));
-  PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * h));
   cudaEvent_t ev_ffn = e.mark(cs);
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
   // local Q/K/V of all heads ([Q | K | V] column blocks of h), RoPE at global positions
-  PDS_TRY(e.gemm(e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, 3 * e.h, e.h, sv->at("qkv"), 3 * e.h), e.h, 0, 0,
-                        e.r * e.sl)));
-  PDS_TRY(e.ag(sv->at("qkv"), qkvg, e.sl * 3 * e.h));                                   // AG(QKV)
-  PDS_TRY(e.attn_rows_f(qkvg, sv->at("a"), sv->at("lse")));                              // own queries
+  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, 3 * h, h, qkvb, 3 * h), h, 0, 0, e.r * e.sl)));
+  PDS_TRY(zig_exchange(e, z, qkvb, qkvz, 3 * h, true));                                  // -> zig rows
+  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * h * 2, qkvz + h * 2, 3 * h * 2, 2 * h * 2, e.sl, cudaMemcpyDeviceToDevice,
+                             e.st));
+  // P ring steps; step k holds the K/V of rank r - k (its zig half-chunks), the next
+  // block is received on the side stream while this one is computed
+  bool first[2] = {true, true};
+  for (int k = 0; k < e.P; ++k) {
+    const int src = (e.r - k + e.P) % e.P;
+    char* kv = kvb[k & 1];
+    cudaEvent_t ev_next = nullptr;
+    if (k + 1 < e.P) {
+      PDS_TRY(e.link(e.st, cs));
+      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * h * 2, cs));
+      ev_next = e.mark(cs);
+    }
+    const Zig zs{e.P, src, z.c, z.cb};
+    for (int ai = 0; ai < 2; ++ai)
+      for (int bi = 0; bi < 2; ++bi) {
+        const int qa = z.hc(ai), kb = zs.hc(bi);
+        if (e.m.causal && kb > qa) continue;          // every key after every query
+        const int diag = e.m.causal && kb == qa;
+        {
+          Prof p(e.c, e.st, K_ATTN_F, e.b * 4.0 * n * e.d * (diag ? 0.5 * z.c * z.c : (double)z.c * z.c), 0);
+          for (int64_t j = 0; j < e.b; ++j)
+            PDS_TRY(kerr(attn_fwd_pair(qkvz + ((ai * z.cb) + j) * 3 * h * 2, e.b * 3 * h,
+                                       kv + ((bi * z.cb) + j) * 2 * h * 2, e.b * 2 * h, 0, (int)h, (int)z.c, (int)z.c,
+                                       (int)n, (int)e.d, diag, op + j * h * 2, e.b * h, lp + j * n * z.c, e.st),
+                         "attn_fwd_pair"));
+        }
+        Prof p(e.c, e.st, K_NORM, 0, (double)z.cb * h * 10);
+        for (int64_t j = 0; j < e.b; ++j)
+          PDS_TRY(kerr(attn_merge(oacc + ((ai * z.cb) + j) * h, e.b * h, lse + (j * 2 + ai) * n * z.c, z.c,
+                                  op + j * h * 2, e.b * h, lp + j * n * z.c, z.c, (int)z.c, (int)n, (int)e.d,
+                                  first[ai], nullptr, 0, e.st), "attn_merge"));
+        first[ai] = false;
+      }
+    if (ev_next) PDS_TRY(e.wait(e.st, ev_next));
+  }
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 6);
+    PDS_TRY(kerr(rope_t_f32_bf16(oacc, h, (int)e.sl, (int)h, (int)e.d, nullptr, 0, 0, (int)z.cb, (int)e.b, oz, h,
+                                 e.st), "o convert"));
+  }
+  PDS_TRY(zig_exchange(e, z, sv->at("a"), oz, h, false));                               // -> boundary rows
   PDS_TRY(e.wait(e.st, ev_proj));
-  PDS_TRY(tn.xw(sv->at("a"), e.h, wproj, e.h, e.sl, e.h, e.h, u1, e.h));                // O
-  PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
+  PDS_TRY(tn.xw(sv->at("a"), h, wproj, h, e.sl, h, h, u1, h));                          // O
+  PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), v2, sv->at("rstd2")));
   PDS_TRY(e.wait(e.st, ev_ffn));
-  GemmArgs fc1 = Exec::G(v2, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
+  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.F, h, sv->at("h"), e.F, EPI_GELU);
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
-  PDS_TRY(tn.xw(f0, e.F, wout, e.h, e.sl, e.h, e.F, u1, e.h));                          // Z
-  PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * e.h));
-  return e.add(sv->at("x1"), u1, y, e.sl * e.h);
+  PDS_TRY(tn.xw(f0, e.F, wout, h, e.sl, h, e.F, u1, h));                                // Z
+  PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * h));
+  return e.add(sv->at("x1"), u1, y, e.sl * h);
 }
 
 pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
                   char* ws) {
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
+  const int64_t n = e.m.n_heads, h = e.h;
+  const Zig z{e.P, e.r, e.sp / 2, e.sl / 2};
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
   char* wout = ws + bp.ws_off("wout");
   char* dw = ws + bp.ws_off("dw");
   char* u1 = ws + bp.ws_off("u1");
-  char* qkvg = ws + bp.ws_off("qkvg");
-  char* dqkvf = ws + bp.ws_off("dqkvf");
+  char* qkvb = ws + bp.ws_off("qkvb");
+  char* kvb[2] = {ws + bp.ws_off("kv0"), ws + bp.ws_off("kv1")};
+  float* dkvb[2] = {reinterpret_cast<float*>(ws + bp.ws_off("dkv0")), reinterpret_cast<float*>(ws + bp.ws_off("dkv1"))};
+  float* dqacc = reinterpret_cast<float*>(ws + bp.ws_off("acc"));
+  char* doz = ws + bp.ws_off("op");
+  char* oz = ws + bp.ws_off("oz");
+  char* dqkvz = ws + bp.ws_off("dqkvz");
   char* f0 = ws + bp.ws_off("f0");
   char* f1 = ws + bp.ws_off("f1");
   char* v2 = ws + bp.ws_off("v2");
@@ -835,53 +939,108 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
   float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
   float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  const char* qkvz = sv->at("qkv");
+  const float* lse = reinterpret_cast<const float*>(sv->at("lse"));
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_TRY(e.link(e.st, cs));
-  PDS_TRY(e.ag(w->w_out, wout, e.Fl * e.h));
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * e.h));
+  PDS_TRY(e.ag(w->w_out, wout, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
   cudaEvent_t ev_in = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
   PDS_TRY(cz_wqkv(e, w, wqkv, cs));
   cudaEvent_t ev_qkv = e.mark(cs);
-  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * h * 4, e.st));
   // FFN: local with full weights (as UlyssesZ)
-  GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
+  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.F, EPI_DGELU);
   dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
   dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;                                 // G^T, dH^T
   PDS_TRY(e.gemm(dgel));
-  PDS_TRY(tn.tr(dy, e.h, e.sl, e.h, tn.tb));
-  PDS_TRY(tn.mm(tn.ta, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));           // dW_out (full, local)
+  PDS_TRY(tn.tr(dy, h, e.sl, h, tn.tb));
+  PDS_TRY(tn.mm(tn.ta, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));               // dW_out (full, local)
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
-  PDS_TRY(tn.tr(u1, e.h, e.sl, e.h, tn.tb));
-  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));              // dW_in^T (full, local)
+  PDS_TRY(tn.tr(u1, h, e.sl, h, tn.tb));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));                  // dW_in^T (full, local)
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
   PDS_TRY(e.wait(e.st, ev_in));
-  PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
-  PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
+  PDS_TRY(tn.xw(f1, e.F, win, h, e.sl, h, e.F, v2, h));
+  PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + h));
   PDS_TRY(e.wait(e.st, ev_proj));
-  PDS_TRY(e.gemm(Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, da, e.h)));        // dA = dX1 W_proj^T
-  PDS_TRY(tn.dw(sv->at("a"), e.h, dx, e.h, e.sl, e.h, e.h, dw, EPI_F32));
-  PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
-  // attention: re-gather the context's Q/K/V; this rank's queries give dQ of its rows
-  // and dK / dV contributions to every key row; RS sums those over ranks
-  PDS_TRY(e.ag(sv->at("qkv"), qkvg, e.sl * 3 * e.h));                                   // AG(QKV)
-  PDS_CUDA(cudaMemsetAsync(dqkvf, 0, e.s * 3 * e.h * 2, e.st));
-  PDS_TRY(e.attn_rows_b(qkvg, sv->at("a"), sv->at("lse"), da, dqkvf, dd));
-  char* dqkv = dqkvf + e.r * e.sl * 3 * e.h * 2;
-  PDS_TRY(e.rs(dqkvf, dqkv, e.sl * 3 * e.h));                                           // RS(dQKV)
+  PDS_TRY(e.gemm(Exec::G(dx, h, 0, wproj, h, 0, e.sl, h, h, da, h)));                  // dA = dX1 W_proj^T
+  PDS_TRY(tn.dw(sv->at("a"), h, dx, h, e.sl, h, h, dw, EPI_F32));
+  PDS_TRY(uz_dw(e, dw, h, g->dw_proj));
+  // ring attention backward on the zig rows: O and dO to zig rows, D = rowsum(dO o O)
+  PDS_TRY(zig_exchange(e, z, sv->at("a"), oz, h, true));
+  PDS_TRY(zig_exchange(e, z, da, doz, h, true));
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 4);
+    for (int64_t j = 0; j < e.b; ++j)
+      for (int ai = 0; ai < 2; ++ai)
+        PDS_TRY(kerr(attn_dot(oz + ((ai * z.cb) + j) * h * 2, e.b * h, doz + ((ai * z.cb) + j) * h * 2, (int)z.c,
+                              (int)n, (int)e.d, dd + (j * 2 + ai) * n * z.c, e.st), "attn_dot"));
+  }
+  PDS_CUDA(cudaMemsetAsync(dqacc, 0, e.sl * h * 4, e.st));
+  PDS_CUDA(cudaMemsetAsync(dkvb[0], 0, e.sl * 2 * h * 4, e.st));
+  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * h * 2, qkvz + h * 2, 3 * h * 2, 2 * h * 2, e.sl, cudaMemcpyDeviceToDevice,
+                             e.st));
+  int cur = 0;                                     // dK/dV accumulator of the block in hand
+  for (int k = 0; k < e.P; ++k) {
+    const int src = (e.r - k + e.P) % e.P;
+    char* kv = kvb[k & 1];
+    cudaEvent_t ev_next = nullptr;
+    if (k + 1 < e.P) {
+      PDS_TRY(e.link(e.st, cs));
+      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * h * 2, cs));
+      ev_next = e.mark(cs);
+    }
+    const Zig zs{e.P, src, z.c, z.cb};
+    for (int ai = 0; ai < 2; ++ai)
+      for (int bi = 0; bi < 2; ++bi) {
+        const int qa = z.hc(ai), kb = zs.hc(bi);
+        if (e.m.causal && kb > qa) continue;
+        const int diag = e.m.causal && kb == qa;
+        Prof p(e.c, e.st, K_ATTN_B, e.b * 10.0 * n * e.d * (diag ? 0.5 * z.c * z.c : (double)z.c * z.c), 0);
+        for (int64_t j = 0; j < e.b; ++j)
+          PDS_TRY(kerr(attn_bwd_pair(qkvz + ((ai * z.cb) + j) * 3 * h * 2, e.b * 3 * h,
+                                     kv + ((bi * z.cb) + j) * 2 * h * 2, e.b * 2 * h, 0, (int)h,
+                                     doz + ((ai * z.cb) + j) * h * 2, e.b * h, lse + (j * 2 + ai) * n * z.c,
+                                     dd + (j * 2 + ai) * n * z.c, (int)z.c, (int)z.c, (int)n, (int)e.d, diag,
+                                     dqacc + ((ai * z.cb) + j) * h, e.b * h,
+                                     dkvb[cur] + ((bi * z.cb) + j) * 2 * h, e.b * 2 * h, e.st), "attn_bwd_pair"));
+      }
+    // the accumulator travels with its block: P passes bring it home
+    if (e.P > 1) {
+      PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dkvb[cur]), reinterpret_cast<char*>(dkvb[cur ^ 1]),
+                        e.sl * 2 * h * 4, e.st));
+      cur ^= 1;
+    }
+    if (ev_next) PDS_TRY(e.wait(e.st, ev_next));
+  }
+  {
+    // RoPE^T at the zig positions, bf16, [dQ | dK | dV] zig rows
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 3 * h * 6);
+    const int64_t b0 = z.hc(0) * z.c, b1 = z.hc(1) * z.c;
+    PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)e.d, e.c->rope, b0, b1, (int)z.cb, (int)e.b,
+                                 dqkvz, 3 * h, e.st), "dq rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur], 2 * h, (int)e.sl, (int)h, (int)e.d, e.c->rope, b0, b1, (int)z.cb,
+                                 (int)e.b, dqkvz + h * 2, 3 * h, e.st), "dk rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur] + h, 2 * h, (int)e.sl, (int)h, (int)e.d, nullptr, 0, 0, (int)z.cb,
+                                 (int)e.b, dqkvz + 2 * h * 2, 3 * h, e.st), "dv convert"));
+  }
+  PDS_TRY(zig_exchange(e, z, qkvb, dqkvz, 3 * h, false));                               // dQKV -> boundary
+  char* dqkv = qkvb;
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
-  PDS_TRY(tn.dw(dqkv, 3 * e.h, u1, e.h, e.sl, 3 * e.h, e.h, dw, EPI_F32));              // [Q; K; V] all rows
+  PDS_TRY(tn.dw(dqkv, 3 * h, u1, h, e.sl, 3 * h, h, dw, EPI_F32));                      // [Q; K; V] all rows
   for (int i = 0; i < 3; ++i) {       // ZeRO3 RS part by part into the spec shard [Q_r; K_r; V_r]
-    char* part = dw + i * e.h * e.h * 4;
-    const int64_t cnt = e.hl * e.h;
+    char* part = dw + i * h * h * 4;
+    const int64_t cnt = e.hl * h;
     char* mine = part + e.r * cnt * 4;
     PDS_TRY(e.rs(part, mine, cnt, DT_F32));
     PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + i * cnt * 4, cnt, e.st), "add_f32"));
   }
   PDS_TRY(e.wait(e.st, ev_qkv));
-  PDS_TRY(tn.xw(dqkv, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));                // dU
+  PDS_TRY(tn.xw(dqkv, 3 * h, wqkv, h, e.sl, h, 3 * h, v2, h));                          // dU
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }

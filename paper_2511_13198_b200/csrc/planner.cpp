@@ -332,7 +332,11 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       break;
     }
     case PDS_MEGATRON_CZ: {
-      // saved: the local rows of TS's tensors (Q/K/V of all heads, A, LSE, H)
+      if ((sl / 2) % 128 || sl % 2)
+        PDS_FAIL(PDS_EDIVISIBILITY, "MegatronCZ: s/(2P)=" + std::to_string(sl / 2) +
+                                        " must be a multiple of 128 (zigzag half-chunks, R-CZ; caller pads)");
+      // saved: the local rows of TS's tensors (Q/K/V of all heads, A, LSE, H); Q/K/V and
+      // LSE on the zigzag rows
       push(p.saved, ts, "rstd1", ell);
       push(p.saved, ts, "qkv", SL * 3 * h * 2);
       push(p.saved, ts, "a", u);
@@ -346,8 +350,17 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "wout", F * h * 2);
       push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
       push(p.ws, tw, "u1", u);
-      push(p.ws, tw, "qkvg", S * 3 * h * 2);      // all-gathered Q/K/V of the context
-      push(p.ws, tw, "dqkvf", S * 3 * h * 2);     // dQ/dK/dV partials of all rows (RS in place)
+      // ring attention on the zigzag rows (R-CZ): O(u) per rank whatever P
+      push(p.ws, tw, "qkvb", 3 * u);              // QKV of the boundary rows (bwd: dQKV)
+      push(p.ws, tw, "kv0", 2 * u);               // the K/V block in hand / the next one
+      push(p.ws, tw, "kv1", 2 * u);
+      push(p.ws, tw, "acc", 2 * u);               // fp32 O accumulator (bwd: dQ)
+      push(p.ws, tw, "dkv0", 4 * u);              // fp32 dK/dV travelling with their block
+      push(p.ws, tw, "dkv1", 4 * u);
+      push(p.ws, tw, "op", u);                    // a pair's partial O (bwd: zigzag dO)
+      push(p.ws, tw, "oz", u);                    // zigzag O
+      push(p.ws, tw, "lp", lam);                  // a pair's partial LSE
+      push(p.ws, tw, "dqkvz", 3 * u);             // zigzag dQKV
       push(p.ws, tw, "f0", SL * F * 2);
       push(p.ws, tw, "f1", SL * F * 2);
       push(p.ws, tw, "v2", u);

@@ -389,3 +389,68 @@ def test_attention_query_rows(d, causal, s, qn):
         assert rel(g[:, hh * d:(hh + 1) * d], dqr) < 1e-2
         assert rel(g[:, hq + hh * d:hq + (hh + 1) * d], dkr) < 1e-2
         assert rel(g[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d], dvr) < 1e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [1, 0])
+def test_attention_ring_pairs(d, causal):
+    """Ring attention's pieces (MegatronCZ, R-CZ): the sequence cut into 4 blocks of c
+    rows, every query block's attention assembled from (query block, key block) pairs —
+    the diagonal pair causal, earlier key blocks full, later ones skipped when causal —
+    merged by log-sum-exp (pds_k_attn_merge), equals full attention (oracle); the pair
+    backwards accumulated in fp32 (pds_k_attn_bwd_pair, merged LSE, D from
+    pds_k_attn_dot) equal the full backward before RoPE^T."""
+    heads, c, nb = 2, 256, 4
+    s = c * nb
+    hq = heads * d
+    qkv = _mat(11 + d, 1, (s, 3 * hq))
+    dout = _mat(11 + d, 2, (s, hq))
+    tq, tdo = dev_bf16(qkv), dev_bf16(dout)
+    kv = tq[:, hq:].contiguous()                      # [K | V] of all rows
+    o_acc = torch.zeros(s, hq, dtype=torch.float32, device="cuda")
+    l_acc = torch.zeros(heads, s, dtype=torch.float32, device="cuda")
+    out = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+    op = torch.empty(c, hq, dtype=torch.bfloat16, device="cuda")
+    lp = torch.empty(heads, c, dtype=torch.float32, device="cuda")
+    st = stream()
+    for a in range(nb):
+        first = True
+        for bb in range(nb):
+            if causal and bb > a:
+                continue
+            B.k_attn_fwd_pair(tq[a * c:].data_ptr(), 3 * hq, kv[bb * c:].data_ptr(), 2 * hq, 0, hq, c, c, heads, d,
+                              int(causal and bb == a), op.data_ptr(), hq, lp.data_ptr(), st)
+            B.k_attn_merge(o_acc[a * c:].data_ptr(), hq, l_acc[:, a * c:].data_ptr(), s, op.data_ptr(), hq,
+                           lp.data_ptr(), c, c, heads, d, int(first), out[a * c:].data_ptr(), hq, st)
+            first = False
+    torch.cuda.synchronize()
+    o_gpu = host(out)
+    dd = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+    B.k_attn_dot(out.data_ptr(), hq, tdo.data_ptr(), s, heads, d, dd.data_ptr(), st)
+    dq_acc = torch.zeros(s, hq, dtype=torch.float32, device="cuda")
+    dkv_acc = torch.zeros(s, 2 * hq, dtype=torch.float32, device="cuda")
+    lse_blk = torch.empty(heads, c, dtype=torch.float32, device="cuda")
+    d_blk = torch.empty(heads, c, dtype=torch.float32, device="cuda")
+    for a in range(nb):
+        lse_blk.copy_(l_acc[:, a * c:(a + 1) * c])
+        d_blk.copy_(dd[:, a * c:(a + 1) * c])
+        for bb in range(nb):
+            if causal and bb > a:
+                continue
+            B.k_attn_bwd_pair(tq[a * c:].data_ptr(), 3 * hq, kv[bb * c:].data_ptr(), 2 * hq, 0, hq,
+                              tdo[a * c:].data_ptr(), hq, lse_blk.data_ptr(), d_blk.data_ptr(), c, c, heads, d,
+                              int(causal and bb == a), dq_acc[a * c:].data_ptr(), hq, dkv_acc[bb * c:].data_ptr(),
+                              2 * hq, st)
+    torch.cuda.synchronize()
+    for hh in range(heads):
+        q = qkv[:, hh * d:(hh + 1) * d]
+        k = qkv[:, hq + hh * d:hq + (hh + 1) * d]
+        v = qkv[:, 2 * hq + hh * d:2 * hq + (hh + 1) * d]
+        a_ref, l_ref = OL.attention_fwd(q, k, v, causal=bool(causal))
+        assert rel(o_gpu[:, hh * d:(hh + 1) * d], a_ref) < 1e-2
+        assert np.allclose(host(l_acc)[hh], l_ref, rtol=0, atol=2e-3)
+        dqr, dkr, dvr = OL.attention_bwd(q, k, v, o_gpu[:, hh * d:(hh + 1) * d], l_ref,
+                                         dout[:, hh * d:(hh + 1) * d], causal=bool(causal))
+        assert rel(host(dq_acc)[:, hh * d:(hh + 1) * d], dqr) < 1e-2
+        assert rel(host(dkv_acc)[:, hh * d:(hh + 1) * d], dkr) < 1e-2
+        assert rel(host(dkv_acc)[:, hq + hh * d:hq + (hh + 1) * d], dvr) < 1e-2

@@ -87,6 +87,58 @@ def _attn(qkv, nl, d, positions):
     return out
 
 
+def _rope_qk(qkv, n, d, positions):
+    """RoPE on the Q and K column blocks of [rows, 3 n d] at the given global positions."""
+    h = n * d
+    inv = 10000.0 ** (-2 * torch.arange(d // 2, dtype=torch.float64) / d)
+    ang = positions.double()[:, None] * inv[None, :]
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    out = qkv.clone()
+    for blk in (0, 1):
+        for hh in range(n):
+            t = qkv[:, blk * h + hh * d:blk * h + (hh + 1) * d]
+            a, b = t[:, :d // 2], t[:, d // 2:]
+            out[:, blk * h + hh * d:blk * h + (hh + 1) * d] = torch.cat([a * cos - b * sin, a * sin + b * cos], -1)
+    return out
+
+
+def _attn_keys(q, kv, pq, pk, n, d):
+    """Causal softmax attention of queries (post-RoPE, positions pq) over the keys of kv
+    [K | V] (positions pk) alone: (O [rows, n d], LSE [n, rows], -inf without keys)."""
+    h = n * d
+    o = torch.zeros(q.shape[0], h, dtype=q.dtype)
+    lse = torch.full((n, q.shape[0]), -float("inf"), dtype=q.dtype)
+    mask = pk[None, :] > pq[:, None]
+    for hh in range(n):
+        sc = q[:, hh * d:(hh + 1) * d] @ kv[:, hh * d:(hh + 1) * d].T / d ** 0.5
+        sc = sc.masked_fill(mask, -float("inf"))
+        l = torch.logsumexp(sc, dim=1)
+        p = torch.exp(sc - l[:, None]).nan_to_num(0.0)
+        o[:, hh * d:(hh + 1) * d] = p @ kv[:, h + hh * d:h + (hh + 1) * d]
+        lse[hh] = l
+    return o, lse
+
+
+def _exchange(blocks, sends, recvs):
+    """Point-to-point sends of blocks[i] to (peer, tag) = sends[i]; receives (peer, tag)
+    = recvs[j] into blocks of the same shape, concatenated in recvs order (comm.cpp p2p:
+    a transfer to this rank itself is a copy)."""
+    rank = dist.get_rank()
+    out = [torch.empty_like(blocks[0]) for _ in recvs]
+    reqs = []
+    for (peer, tag), blk in zip(sends, blocks):
+        if peer == rank:
+            out[[i for i, r in enumerate(recvs) if r == (rank, tag)][0]].copy_(blk)
+        else:
+            reqs.append(dist.isend(blk.contiguous(), peer, tag=tag))
+    for i, (peer, tag) in enumerate(recvs):
+        if peer != rank:
+            reqs.append(dist.irecv(out[i], peer, tag=tag))
+    for r in reqs:
+        r.wait()
+    return torch.cat(out, 0)
+
+
 def _worker(rank, P, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -120,11 +172,34 @@ def _worker(rank, P, port, q):
         afull = torch.cat(back, 1)                              # unpack: slot j = group j columns
         x1u = x + afull @ wpf
         y_uz = x1u + gelu(_rmsnorm(x1u, g2) @ wif.T) @ wof
-        # ---- MegatronCZ forward (csrc/layer.cpp cz_fwd): W_qkv^T gathered part by part
-        # into [Q all; K all; V all], local QKV, AG(QKV), own query rows vs every key
+        # ---- MegatronCZ forward (csrc/layer.cpp cz_fwd, reading R-CZ): W_qkv^T gathered
+        # part by part into [Q all; K all; V all], local QKV with RoPE at global positions,
+        # point-to-point exchange to the zigzag rows (half-chunks r, 2P-1-r), P ring steps
+        # of K/V with log-sum-exp merges, the reverse exchange of O
         wq_all = torch.cat([_ag(wq[i * hl:(i + 1) * hl].contiguous(), P) for i in range(3)], 0)
-        qkv_c = _ag(_rmsnorm(x, g1) @ wq_all.T, P)                # [s, 3h] of the whole context
-        a_c = _attn(qkv_c, N, d_, torch.arange(S))[rank * sl:(rank + 1) * sl]
+        qkv_b = _rope_qk(_rmsnorm(x, g1) @ wq_all.T, N, d_, torch.arange(rank * sl, (rank + 1) * sl))
+        c = sl // 2
+        zz = lambda j: j if j < P else 2 * P - 1 - j
+        zig = (rank, 2 * P - 1 - rank)
+        qkvz = _exchange([qkv_b[:c], qkv_b[c:]], [(zz(2 * rank), 2 * rank), (zz(2 * rank + 1), 2 * rank + 1)],
+                         [(j // 2, j) for j in zig])
+        pos = torch.cat([torch.arange(j * c, (j + 1) * c) for j in zig])
+        kv, kv_pos = qkvz[:, H:].contiguous(), pos
+        o_acc = torch.zeros(sl, H, dtype=torch.float64)
+        l_acc = torch.full((N, sl), -float("inf"), dtype=torch.float64)
+        for k in range(P):
+            o_p, l_p = _attn_keys(qkvz[:, :H], kv, pos, kv_pos, N, d_)
+            l_new = torch.logaddexp(l_acc, l_p)
+            wa = torch.exp(l_acc - l_new).nan_to_num(0.0)
+            wpr = torch.exp(l_p - l_new).nan_to_num(0.0)
+            o_acc = (o_acc.view(sl, N, d_) * wa.T[..., None] + o_p.view(sl, N, d_) * wpr.T[..., None]).view(sl, H)
+            l_acc = l_new
+            if k < P - 1:                                     # ring: K/V (and positions) to rank + 1
+                kv = _exchange([kv], [((rank + 1) % P, 0)], [((rank - 1) % P, 0)])
+                kv_pos = _exchange([kv_pos.double()[:, None]], [((rank + 1) % P, 1)],
+                                   [((rank - 1) % P, 1)])[:, 0].long()
+        a_c = _exchange([o_acc[:c], o_acc[c:]], [(j // 2, j) for j in zig],
+                        [(zz(2 * rank), 2 * rank), (zz(2 * rank + 1), 2 * rank + 1)])
         x1c = x + a_c @ wpf
         y_cz = x1c + gelu(_rmsnorm(x1c, g2) @ wif.T) @ wof
         # ---- tile-overlapped TS collectives (comm.cpp all_gather_flagged /

@@ -85,10 +85,12 @@ def test_comm_signatures_and_bytes_c1():
          {"AllGather": 8, "AllToAll": 4, "ReduceScatter": 4, "AllReduce": 1}),
         (S.METP, {"AllGather": 4, "ReduceScatter": 4},     # c = P = 2 waves
          {"AllGather": 12, "ReduceScatter": 8, "AllReduce": 1}),
-        # CZ: 6 weight AGs (W_qkv^T in its Q, K, V parts) + AG(QKV) per pass; bwd adds
-        # RS(dQKV) and the 6 fp32 dW reduce-scatters
-        (S.CZ, {"AllGather": 7},
-         {"AllGather": 14, "ReduceScatter": 7, "AllReduce": 1}),
+        # CZ (ring, zigzag): 6 weight AGs (W_qkv^T in its Q, K, V parts) per pass; fwd
+        # SendRecv(QKV -> zigzag), P - 1 K/V ring passes, SendRecv(O -> boundary); bwd
+        # SendRecv(O, dO -> zigzag), P - 1 K/V passes + P fp32 dK/dV passes,
+        # SendRecv(dQKV -> boundary), the 6 fp32 dW reduce-scatters, AR(dgamma)
+        (S.CZ, {"AllGather": 6, "SendRecv": 2, "RingPass": 1},
+         {"AllGather": 12, "SendRecv": 5, "RingPass": 4, "ReduceScatter": 6, "AllReduce": 1}),
     ]:
         g, _, _, _, _, flog = _run(pi, P, d, s)
         assert _signature(flog) == Counter(fwd_sig), pi
