@@ -338,7 +338,7 @@ def main():
             else:
                 hi = mid
         if lo:
-            frontier = {"s": lo, "layers": L_STACK, "plan": "".join("TUMCF"[q] for q in feasible(lo)[1]),
+            frontier = {"s": lo, "layers": L_STACK, "plan": "".join("TUMCFR"[q] for q in feasible(lo)[1]),
                         "source": "pds_plan (Algorithm 1, Eq. 6 on the exact memory plan, device capacity "
                                   "minus the bundle's reserve); measured frontiers in profiles/"}
     out = {

@@ -58,13 +58,16 @@ typedef enum {
   PDS_MEGATRON_TS = 0,     /* Megatron-LM TP+SP                    */
   PDS_ULYSSES_Z = 1,       /* DeepSpeed Ulysses + ZeRO3 weight gathering*/
   PDS_METP = 2,            /* METP-style chunked, memory-bounded (R-11)  */
-  PDS_MEGATRON_CZ = 3,     /* Megatron-LM CP + ZeRO3: context-parallel attention over
-                              the all-gathered Q/K/V (reading R-CZ)     */
-  PDS_METP_FULL = 4        /* METP with Q/K/V also recomputed in bwd (saved 3u + 2l +
+  PDS_MEGATRON_CZ = 3,     /* Megatron-LM CP + ZeRO3: zigzag-balanced ring attention
+                              (reading R-CZ)                            */
+  PDS_METP_FULL = 4,       /* METP with Q/K/V also recomputed in bwd (saved 3u + 2l +
                               lam instead of 6u + ..., SURVEY O-6): the planner's
                               deepest memory saver, chosen per layer   */
+  PDS_COLOSSAL_Z = 5       /* Colossal-AI SP (Ring Self-Attention) + ZeRO3 (PAPER.md:220,
+                              reading R-COL): the score matrix of the own rows is
+                              materialised, memory quadratic in s     */
 } pds_strategy;
-#define PDS_N_STRATEGIES 5
+#define PDS_N_STRATEGIES 6
 
 /* pds_plan flags */
 #define PDS_PLAN_INFEASIBLE 1u  /* no plan satisfies Eq. 6; least-memory fallback returned */

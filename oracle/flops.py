@@ -57,4 +57,9 @@ def comm_bytes(pi, h, s, P, ffn=None, b=1, metp_recompute="ffn"):
         kv = (s // P) * b * 2 * h                              # one rank's K/V block (elements)
         ring = 2 * (P - 1) * kv * 2 + P * kv * 4               # K/V fwd + bwd (bf16), dK/dV (fp32)
         return int(round(zig + ring + fr * wb * (2 + 2 + 4) + ar))
+    if pi == 5:              # ColossalZ (RSA), ZeRO3 weights as UZ
+        wb = 4 * h * h + 2 * h * f
+        kb = (s // P) * b * h                                  # one rank's K (or V) block (elements)
+        ring = 4 * (P - 1) * kb * 2 + 2 * P * kb * 4           # K, V fwd + V, K bwd (bf16); dV, dK (fp32)
+        return int(round(ring + fr * wb * (2 + 2 + 4) + ar))
     raise KeyError(pi)

@@ -10,6 +10,7 @@ this build reads M analytically (R-22, SURVEY O-6):
           UZ   = 7u + (F/h)u + 2l + lam   as TS + post-A2A attention output (1u)
           METP = 6u + 2l + lam            (metp_recompute = ffn: H recomputed)
           METP = 3u + 2l + lam            (metp_recompute = full, and METP-full: QKV recomputed too)
+          COL  = 6u + (F/h)u + 2l + n (s/P) s b 2   ColossalZ (RSA): the probabilities instead of LSE
   plan    sum_l (W + saved_{pi_l}) + max_{pi in plan} workspace_pi + reserve < capacity (R-22)
 
 Pins: the saved formula equals the simulated grid's ledger recount of the
@@ -22,7 +23,7 @@ library's exact workspace is pinned by measuring its device allocation
 """
 from __future__ import annotations
 
-TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
+TS, UZ, METP, CZ, METP_FULL, COL = 0, 1, 2, 3, 4, 5
 
 
 def units(h, n, s, P, b=1):
@@ -45,6 +46,8 @@ def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
         return (6 if metp_recompute == "ffn" else 3) * u + 2 * l + lam
     if pi == METP_FULL:
         return 3 * u + 2 * l + lam
+    if pi == COL:                      # ColossalZ (R-COL): TS's tensors minus LSE, plus the
+        return (6 + f) * u + 2 * l + n * (s // P) * s * b * 2     # softmax probabilities [n, s/P, s] bf16
     raise KeyError(pi)
 
 
@@ -96,6 +99,8 @@ def transient_floor(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
         return uz
     if pi == CZ:
         return max(9 * u, uz)
+    if pi == COL:                      # RSA: the fp32 score matrix of the own rows [n, s/P, s]
+        return max(n * (s // P) * s * b * 4, uz)
     c = metp_chunks or P
     base = (2 * P * u + f * u) // c
     if pi == METP:

@@ -34,8 +34,9 @@ import numpy as np
 from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
                     rmsnorm, rmsnorm_bwd, rope_apply, rope_apply_t, rope_cos_sin)
 
-TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
-NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full"}
+TS, UZ, METP, CZ, METP_FULL, COL = 0, 1, 2, 3, 4, 5
+NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full",
+         COL: "ColossalZ"}
 
 
 class Cfg:
@@ -708,6 +709,165 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
     return dx
 
 
+# ------------------------------------------------------------------ ColossalZ (RSA)
+# Reading R-COL: Colossal-AI sequence parallelism + ZeRO3 weights
+# (PAPER.md:220).  Weights and every GEMM as MegatronCZ (local boundary rows); the
+# attention is Ring Self-Attention on the contiguous boundary chunks: the keys pass
+# around the ring and every rank materialises its rows' full score matrix
+# [n, s/P, s] (quadratic memory, the paper's reason to exclude it),
+# a plain row softmax gives the probabilities (saved for the backward), then the
+# values pass around the ring for O = P V.  Backward: values again (dP = dO V^T,
+# dV partials travelling with their block), dS = P o (dP - D), keys again (dQ = dS K,
+# dK partials travelling with their block).
+
+def _ring_blocks(grid, blocks, bpe):
+    """P steps of the ring: yields (step, blocks held now) and passes after each step but
+    the last (P - 1 RingPass)."""
+    P = grid.p
+    for k in range(P):
+        yield k, blocks
+        if k < P - 1:
+            blocks = grid.ring_pass(blocks, bpe=bpe)
+
+
+def colossal_fwd(grid, xs, W, cfg):
+    P = grid.p
+    sl = xs[0].shape[0]
+    s = sl * P
+    h, n = cfg.h, cfg.n
+    d = h // n
+    wq = _gather_qkv_parts(grid, W, h)
+    wp = grid.all_gather(W["w_proj"])[0]
+    wi = grid.all_gather(W["w_in_t"])[0]
+    wo = grid.all_gather(W["w_out"])[0]
+    saved = [dict() for _ in range(P)]
+    r1, qkv_b = [], []
+    for r in range(P):
+        ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
+        r1.append(rr)
+        qkv = ur @ wq.T
+        cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
+        qr = _unheads(rope_apply(_heads(qkv[..., :h], n), cos, sin))
+        kr = _unheads(rope_apply(_heads(qkv[..., h:2 * h], n), cos, sin))
+        qkv_b.append(np.concatenate([qr, kr, qkv[..., 2 * h:]], axis=-1))
+    q = [_heads(qkv_b[r][..., :h], n) for r in range(P)]
+    b = xs[0].shape[1]
+    scores = [np.zeros((b, n, sl, s)) for _ in range(P)]
+    for k, kb in _ring_blocks(grid, [qkv_b[r][..., h:2 * h] for r in range(P)], 2):     # ring of K
+        for r in range(P):
+            j = (r - k) % P
+            scores[r][..., j * sl:(j + 1) * sl] = np.einsum("bnqd,bnkd->bnqk", q[r], _heads(kb[r], n)) / np.sqrt(d)
+    probs = []
+    for r in range(P):
+        sc = scores[r]
+        if cfg.causal:
+            pos_q = np.arange(r * sl, (r + 1) * sl)
+            sc = np.where(np.arange(s)[None, None, None, :] > pos_q[None, None, :, None], -np.inf, sc)
+        m = np.max(sc, axis=-1, keepdims=True)
+        e = np.exp(sc - m)
+        probs.append(e / np.sum(e, axis=-1, keepdims=True))
+    o = [np.zeros_like(q[r]) for r in range(P)]
+    for k, vb in _ring_blocks(grid, [qkv_b[r][..., 2 * h:] for r in range(P)], 2):      # ring of V
+        for r in range(P):
+            j = (r - k) % P
+            o[r] += np.einsum("bnqk,bnkd->bnqd", probs[r][..., j * sl:(j + 1) * sl], _heads(vb[r], n))
+    y, oo, z = [], [], []
+    for r in range(P):
+        a_r = _unheads(o[r])
+        o_r = a_r @ wp
+        x1 = xs[r] + o_r
+        vr, _, rr2 = rmsnorm(x1, W["g2"][r], cfg.eps)
+        hp = vr @ wi.T
+        z_r = gelu(hp) @ wo
+        oo.append(o_r)
+        z.append(z_r)
+        y.append(x1 + z_r)
+        sv = saved[r]
+        _save(grid, r, sv, "x", xs[r], 2)
+        _save(grid, r, sv, "r1", r1[r], 4)
+        _save(grid, r, sv, "qkv", qkv_b[r], 2)                     # boundary rows, post-RoPE
+        _save(grid, r, sv, "a", a_r, 2)
+        _save(grid, r, sv, "probs", probs[r], 2)                   # [b, n, s/P, s]: quadratic
+        _save(grid, r, sv, "x1", x1, 2)
+        _save(grid, r, sv, "r2", rr2, 4)
+        _save(grid, r, sv, "h", hp, 2)
+    return y, saved, dict(o=oo, z=z)
+
+
+def colossal_bwd(grid, dys, saved, W, cfg, grads):
+    P = grid.p
+    sl = dys[0].shape[0]
+    h, n = cfg.h, cfg.n
+    d = h // n
+    sv = saved
+    wq = _gather_qkv_parts(grid, W, h)
+    wp = grid.all_gather(W["w_proj"])[0]
+    wi = grid.all_gather(W["w_in_t"])[0]
+    wo = grid.all_gather(W["w_out"])[0]
+    dwo, dwi, dwp, dwq = [], [], [], []
+    dx1, dg2, da = [], [], []
+    for r in range(P):
+        hp = sv[r]["h"]
+        v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
+        dg = dys[r] @ wo.T
+        dh = dg * gelu_grad(hp)
+        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
+        xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
+        dd, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
+        dx1.append(dys[r] + dd)
+        dg2.append(dgr)
+        da.append(dx1[r] @ wp.T)
+        dwp.append(np.tensordot(sv[r]["a"], dx1[r], axes=([0, 1], [0, 1])))
+    do_h = [_heads(da[r], n) for r in range(P)]
+    D = [np.sum(do_h[r] * _heads(sv[r]["a"], n), axis=-1) for r in range(P)]
+    probs = [sv[r]["probs"] for r in range(P)]
+    dp = [np.zeros_like(probs[r]) for r in range(P)]
+    dvacc = [np.zeros_like(sv[r]["qkv"][..., 2 * h:]) for r in range(P)]
+    for k, vb in _ring_blocks(grid, [sv[r]["qkv"][..., 2 * h:] for r in range(P)], 2):  # ring of V
+        for r in range(P):
+            j = (r - k) % P
+            blk = slice(j * sl, (j + 1) * sl)
+            dp[r][..., blk] = np.einsum("bnqd,bnkd->bnqk", do_h[r], _heads(vb[r], n))
+            dvacc[r] = dvacc[r] + _unheads(np.einsum("bnqk,bnqd->bnkd", probs[r][..., blk], do_h[r]))
+        dvacc = grid.ring_pass(dvacc, bpe=4)                        # dV partials travel home (P passes)
+    ds = [probs[r] * (dp[r] - D[r][..., None]) / np.sqrt(d) for r in range(P)]
+    q = [_heads(sv[r]["qkv"][..., :h], n) for r in range(P)]
+    dq = [np.zeros_like(q[r]) for r in range(P)]
+    dkacc = [np.zeros_like(sv[r]["qkv"][..., h:2 * h]) for r in range(P)]
+    for k, kb in _ring_blocks(grid, [sv[r]["qkv"][..., h:2 * h] for r in range(P)], 2):  # ring of K
+        for r in range(P):
+            j = (r - k) % P
+            blk = slice(j * sl, (j + 1) * sl)
+            dq[r] += np.einsum("bnqk,bnkd->bnqd", ds[r][..., blk], _heads(kb[r], n))
+            dkacc[r] = dkacc[r] + _unheads(np.einsum("bnqk,bnqd->bnkd", ds[r][..., blk], q[r]))
+        dkacc = grid.ring_pass(dkacc, bpe=4)
+    dx, dg1 = [], []
+    for r in range(P):
+        cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
+        dqkv = np.concatenate([_unheads(rope_apply_t(dq[r], cos, sin)),
+                               _unheads(rope_apply_t(_heads(dkacc[r], n), cos, sin)), dvacc[r]], axis=-1)
+        u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
+        dwq.append(np.tensordot(dqkv, u, axes=([0, 1], [0, 1])))
+        du = dqkv @ wq
+        xhat1 = sv[r]["x"] * sv[r]["r1"][..., None]
+        dd, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
+        dx.append(dx1[r] + dd)
+        dg1.append(dgr)
+    qparts = [grid.reduce_scatter([dwq[r][i * h:(i + 1) * h] for r in range(P)], axis=0, bpe=4)
+              for i in range(3)]
+    for r in range(P):
+        grads["dw_qkv_t"][r] += np.concatenate([qparts[i][r] for i in range(3)], axis=0)
+    for key, full in (("dw_proj", dwp), ("dw_in_t", dwi), ("dw_out", dwo)):
+        part = grid.reduce_scatter(full, axis=0, bpe=4)
+        for r in range(P):
+            grads[key][r] += part[r]
+    _finish_dgamma(grid, grads, dg1, dg2)
+    for r in range(P):
+        _release(grid, sv[r])
+    return dx
+
+
 def _full(cfg):
     """METP-full (strategy 4) = R-METP with metp_recompute = 'full' (SURVEY O-5 / O-6),
     a strategy of its own so the planner can choose it per layer."""
@@ -725,7 +885,7 @@ def metp_full_bwd(grid, dys, saved, W, cfg, grads):
 
 
 REGISTRY = {TS: (ts_fwd, ts_bwd), UZ: (uz_fwd, uz_bwd), METP: (metp_fwd, metp_bwd), CZ: (cz_fwd, cz_bwd),
-            METP_FULL: (metp_full_fwd, metp_full_bwd)}
+            METP_FULL: (metp_full_fwd, metp_full_bwd), COL: (colossal_fwd, colossal_bwd)}
 
 
 def layer_fwd(pi, grid, xs, W, cfg):

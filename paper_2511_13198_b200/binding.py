@@ -13,9 +13,11 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDS_LIB") or os.path.join(HERE, "libparadyse.so")   # PDS_LIB: A/B builds
 
-TS, UZ, METP, CZ, METP_FULL = 0, 1, 2, 3, 4
-STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full"}
-N_STRATEGIES = 5
+TS, UZ, METP, CZ, METP_FULL, COLOSSAL_Z = 0, 1, 2, 3, 4, 5
+STRATEGIES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_FULL: "METP-full",
+              COLOSSAL_Z: "ColossalZ"}
+N_STRATEGIES = 6
+LETTERS = "TUMCFR"          # plan strings: T, U, M(ETP), C(Z), F(ull METP), R(ing self-attention: ColossalZ)
 
 STATUS = {0: "PDS_OK", -1: "PDS_EINVAL", -2: "PDS_EDIVISIBILITY", -3: "PDS_ESTRATEGY", -4: "PDS_ENOMEM",
           -5: "PDS_ECUDA", -6: "PDS_ENCCL", -7: "PDS_ESTATE", -8: "PDS_ENOCOSTS", -9: "PDS_ENOTIMPL"}

@@ -194,6 +194,74 @@ int rope_t_f32_bf16(const float* src, int64_t ld_src, int rows, int cols, int d,
   return (int)cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ Ring Self-Attention (ColossalZ)
+// Row softmax of materialised scores (R-COL): p[row][c] = exp(scale S - max) / sum over
+// the visible columns (causal: c <= pos(row), pos(row) = pos0 + row % rows_per_head),
+// bf16 out.  One warp per row.
+__global__ void rsa_softmax_kernel(const float* __restrict__ S, int64_t lds, int rows, int cols, int rows_per_head,
+                                   int64_t pos0, int causal, float scale, __nv_bfloat16* __restrict__ Pr,
+                                   int64_t ldp) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* srow = S + (int64_t)warp * lds;
+  __nv_bfloat16* prow = Pr + (int64_t)warp * ldp;
+  const int64_t last = causal ? pos0 + warp % rows_per_head : (int64_t)cols - 1;   // last visible column
+  const int nv = (int)(last + 1 < cols ? last + 1 : cols);
+  float m = -INFINITY;
+  for (int c = lane; c < nv; c += 32) m = fmaxf(m, srow[c] * scale);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffff, m, o));
+  float l = 0.f;
+  for (int c = lane; c < nv; c += 32) l += expf(srow[c] * scale - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffff, l, o);
+  const float inv = 1.0f / l;
+  for (int c = lane; c < cols; c += 32)
+    prow[c] = __float2bfloat16_rn(c < nv ? expf(srow[c] * scale - m) * inv : 0.f);
+}
+
+int rsa_softmax(const float* S, int64_t lds, int rows, int cols, int rows_per_head, int64_t pos0, int causal,
+                float scale, void* Pr, int64_t ldp, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0 || rows_per_head <= 0) return (int)cudaErrorInvalidValue;
+  rsa_softmax_kernel<<<(rows + 7) / 8, 256, 0, st>>>(S, lds, rows, cols, rows_per_head, pos0, causal, scale,
+                                                     reinterpret_cast<__nv_bfloat16*>(Pr), ldp);
+  return (int)cudaGetLastError();
+}
+
+// dS = scale * P o (dP - D[row]) (bf16), P bf16, dP fp32, D fp32 [rows]
+__global__ void rsa_dsoftmax_kernel(const __nv_bfloat16* __restrict__ Pr, int64_t ldp, const float* __restrict__ dP,
+                                    int64_t lddp, const float* __restrict__ D, int rows, int cols, float scale,
+                                    __nv_bfloat16* __restrict__ dS, int64_t ldds) {
+  const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = cols / 8;
+  if (gi >= (int64_t)rows * per) return;
+  const int row = (int)(gi / per), c = (int)(gi % per) * 8;
+  const uint4 pv = *reinterpret_cast<const uint4*>(Pr + (int64_t)row * ldp + c);
+  const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pv);
+  const float4 a = *reinterpret_cast<const float4*>(dP + (int64_t)row * lddp + c);
+  const float4 b = *reinterpret_cast<const float4*>(dP + (int64_t)row * lddp + c + 4);
+  const float dd = D[row];
+  const float dp[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  __nv_bfloat162 o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 p = __bfloat1622float2(p2[i]);
+    o[i] = __floats2bfloat162_rn(scale * p.x * (dp[2 * i] - dd), scale * p.y * (dp[2 * i + 1] - dd));
+  }
+  *reinterpret_cast<uint4*>(dS + (int64_t)row * ldds + c) = *reinterpret_cast<const uint4*>(o);
+}
+
+int rsa_dsoftmax(const void* Pr, int64_t ldp, const float* dP, int64_t lddp, const float* D, int rows, int cols,
+                 float scale, void* dS, int64_t ldds, cudaStream_t st) {
+  if (cols % 8 || ldp % 8 || lddp % 4 || ldds % 8) return (int)cudaErrorInvalidValue;
+  const int64_t n = (int64_t)rows * (cols / 8);
+  if (n == 0) return 0;
+  rsa_dsoftmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(Pr), ldp, dP, lddp, D, rows, cols, scale,
+      reinterpret_cast<__nv_bfloat16*>(dS), ldds);
+  return (int)cudaGetLastError();
+}
+
 // D = rowsum(dO o O) alone (ring attention: once per layer on the zigzag rows)
 int attn_dot(const void* out, int64_t ld_out, const void* dout, int s, int heads, int d, float* Dd, cudaStream_t st) {
   attn_bwd_dot_kernel<<<(s * heads + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(out), ld_out,

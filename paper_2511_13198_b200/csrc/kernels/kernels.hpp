@@ -36,6 +36,12 @@ int attn_merge(float* o_acc, int64_t ld_oacc, float* l_acc, int64_t lstride_acc,
 int rope_t_f32_bf16(const float* src, int64_t ld_src, int rows, int cols, int d, const void* rope, int64_t base0,
                     int64_t base1, int half, int b, void* dst, int64_t ld_dst, cudaStream_t st);
 int attn_dot(const void* out, int64_t ld_out, const void* dout, int s, int heads, int d, float* Dd, cudaStream_t st);
+// Ring Self-Attention (ColossalZ, attention.cu): row softmax of materialised fp32 scores
+// (causal by position pos0 + row % rows_per_head), and dS = scale * P o (dP - D)
+int rsa_softmax(const float* S, int64_t lds, int rows, int cols, int rows_per_head, int64_t pos0, int causal,
+                float scale, void* Pr, int64_t ldp, cudaStream_t st);
+int rsa_dsoftmax(const void* Pr, int64_t ldp, const float* dP, int64_t lddp, const float* D, int rows, int cols,
+                 float scale, void* dS, int64_t ldds, cudaStream_t st);
 int rmsnorm_fwd(const void* x, const void* res, const void* g, int64_t rows, int h, float eps, void* x1_out,
                 void* u_out, void* rstd, cudaStream_t st);
 int rmsnorm_bwd_grid(int64_t rows);

@@ -14,6 +14,8 @@
 //               remaps (no gather copies), FFN recomputed in bwd  (R-11)
 //
 // Readings R-1..R-36 of DESIGN.md; buffer plan in planner.cpp (make_plan).
+#include <cmath>
+#include <functional>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1045,6 +1047,232 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   return e.dgamma(dgl, g);
 }
 
+// ================================================================== ColossalZ (R-COL)
+// Colossal-AI sequence parallelism (Ring Self-Attention) + ZeRO3 weights:
+// weights and GEMMs as MegatronCZ on the boundary rows; the keys, then the values, pass
+// around the ring of contiguous chunks; every rank materialises the scores of its rows
+// against all s keys ([b][n][s/P][s] fp32, softmax -> bf16 probabilities saved for the
+// backward: the quadratic memory that makes the paper exclude it).
+// Per (sequence, head, key block) one tcgen05 GEMM for each product.
+struct ColBufs {
+  char* qkv;            // saved [s/P b][3h] post-RoPE
+  char* probs;          // saved [b][n][sp][s]
+  float* scores;        // ws [b][n][sp][s] fp32
+};
+
+// block j (the rank whose K / V is in hand) of the key axis: columns [j sp, (j+1) sp)
+pds_status col_ring(Exec& e, const char* first, int64_t col_off, char* kr[2],
+                    const std::function<pds_status(int k, int j, const char* blk)>& step) {
+  const int64_t h = e.h;
+  PDS_CUDA(cudaMemcpy2DAsync(kr[0], h * 2, first + col_off * 2, 3 * h * 2, h * 2, e.sl, cudaMemcpyDeviceToDevice,
+                             e.st));
+  for (int k = 0; k < e.P; ++k) {
+    const int j = (e.r - k + e.P) % e.P;
+    PDS_TRY(step(k, j, kr[k & 1]));
+    if (k + 1 < e.P) PDS_TRY(ring_pass(e, kr[k & 1], kr[(k + 1) & 1], e.sl * h * 2, e.st));
+  }
+  return PDS_OK;
+}
+
+pds_status col_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
+  const BufPlan& bp = sv->plan;
+  const cudaStream_t cs = e.side_stream();
+  const int64_t n = e.m.n_heads, h = e.h, d = e.d, sp = e.sp, sq = e.sq, b = e.b;
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* u1 = ws + bp.ws_off("u1");
+  float* scores = reinterpret_cast<float*>(ws + bp.ws_off("scores"));
+  char* kr[2] = {ws + bp.ws_off("kr0"), ws + bp.ws_off("kr1")};
+  float* oacc = reinterpret_cast<float*>(ws + bp.ws_off("acc"));
+  char* v2 = ws + bp.ws_off("v2");
+  char* f0 = ws + bp.ws_off("f0");
+  char* qkv = sv->at("qkv");
+  char* probs = sv->at("probs");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
+  PDS_TRY(e.link(e.st, cs));
+  PDS_TRY(cz_wqkv(e, w, wqkv, e.st));
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * h));
+  cudaEvent_t ev_ffn = e.mark(cs);
+  PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
+  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, 3 * h, h, qkv, 3 * h), h, 0, 0, e.r * e.sl)));
+  // ring of K: scores of the own rows against key block j, per sequence and head
+  PDS_TRY(col_ring(e, qkv, h, kr, [&](int, int j, const char* kb) -> pds_status {
+    for (int64_t q = 0; q < b; ++q)
+      for (int64_t hd = 0; hd < n; ++hd)
+        PDS_TRY(e.gemm(Exec::G(qkv + (q * 3 * h + hd * d) * 2, b * 3 * h, 0, kb + (q * h + hd * d) * 2, b * h, 0, sp,
+                               sp, d, scores + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
+    return PDS_OK;
+  }));
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)b * n * sp * sq * 6);
+    PDS_TRY(kerr(rsa_softmax(scores, sq, (int)(b * n * sp), (int)sq, (int)sp, e.r * sp, e.m.causal,
+                             1.0f / std::sqrt((float)d), probs, sq, e.st), "rsa_softmax"));
+  }
+  // ring of V: O += P_j V_j
+  PDS_CUDA(cudaMemsetAsync(oacc, 0, e.sl * h * 4, e.st));
+  PDS_TRY(col_ring(e, qkv, 2 * h, kr, [&](int, int j, const char* vb) -> pds_status {
+    for (int64_t q = 0; q < b; ++q)
+      for (int64_t hd = 0; hd < n; ++hd)
+        PDS_TRY(e.gemm(Exec::G(probs + ((q * n + hd) * sp * sq + j * sp) * 2, sq, 0, vb + (q * h + hd * d) * 2,
+                               b * h, 1, sp, d, sp, oacc + q * h + hd * d, b * h, EPI_F32_ACC)));
+    return PDS_OK;
+  }));
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 6);
+    PDS_TRY(kerr(rope_t_f32_bf16(oacc, h, (int)e.sl, (int)h, (int)d, nullptr, 0, 0, (int)e.sl, (int)b, sv->at("a"),
+                                 h, e.st), "o convert"));
+  }
+  PDS_TRY(e.wait(e.st, ev_proj));
+  PDS_TRY(tn.xw(sv->at("a"), h, wproj, h, e.sl, h, h, u1, h));                          // O
+  PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * h));
+  PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), v2, sv->at("rstd2")));
+  PDS_TRY(e.wait(e.st, ev_ffn));
+  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.F, h, sv->at("h"), e.F, EPI_GELU);
+  fc1.aux_out = f0; fc1.ld_aux = e.F;
+  PDS_TRY(e.gemm(fc1));
+  PDS_TRY(tn.xw(f0, e.F, wout, h, e.sl, h, e.F, u1, h));                                // Z
+  PDS_TRY(e.tap(e.c->tap_z, u1, e.sl * h));
+  return e.add(sv->at("x1"), u1, y, e.sl * h);
+}
+
+pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, const pds_grads* g, void* dx,
+                   char* ws) {
+  const BufPlan& bp = sv->plan;
+  const cudaStream_t cs = e.side_stream();
+  const int64_t n = e.m.n_heads, h = e.h, d = e.d, sp = e.sp, sq = e.sq, b = e.b;
+  char* wqkv = ws + bp.ws_off("wqkv");
+  char* wproj = ws + bp.ws_off("wproj");
+  char* win = ws + bp.ws_off("win");
+  char* wout = ws + bp.ws_off("wout");
+  char* dw = ws + bp.ws_off("dw");
+  char* u1 = ws + bp.ws_off("u1");
+  float* dp = reinterpret_cast<float*>(ws + bp.ws_off("scores"));
+  char* ds = ws + bp.ws_off("ds");
+  char* kr[2] = {ws + bp.ws_off("kr0"), ws + bp.ws_off("kr1")};
+  float* dqacc = reinterpret_cast<float*>(ws + bp.ws_off("acc"));
+  float* dacc[2] = {reinterpret_cast<float*>(ws + bp.ws_off("dacc0")), reinterpret_cast<float*>(ws + bp.ws_off("dacc1"))};
+  char* dqkv = ws + bp.ws_off("dqkv");
+  char* f0 = ws + bp.ws_off("f0");
+  char* f1 = ws + bp.ws_off("f1");
+  char* v2 = ws + bp.ws_off("v2");
+  char* da = ws + bp.ws_off("da");
+  float* dd = reinterpret_cast<float*>(ws + bp.ws_off("dd"));
+  float* dgp = reinterpret_cast<float*>(ws + bp.ws_off("dgp"));
+  float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
+  const char* qkv = sv->at("qkv");
+  const char* probs = sv->at("probs");
+  TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
+  PDS_TRY(e.link(e.st, cs));
+  PDS_TRY(e.ag(w->w_out, wout, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  cudaEvent_t ev_in = e.mark(cs);
+  PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
+  cudaEvent_t ev_proj = e.mark(cs);
+  PDS_TRY(cz_wqkv(e, w, wqkv, cs));
+  cudaEvent_t ev_qkv = e.mark(cs);
+  PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * h * 4, e.st));
+  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.F, EPI_DGELU);
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;
+  PDS_TRY(e.gemm(dgel));
+  PDS_TRY(tn.tr(dy, h, e.sl, h, tn.tb));
+  PDS_TRY(tn.mm(tn.ta, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));               // dW_out (full, local)
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
+  PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
+  PDS_TRY(tn.tr(u1, h, e.sl, h, tn.tb));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));                  // dW_in^T (full, local)
+  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(e.wait(e.st, ev_in));
+  PDS_TRY(tn.xw(f1, e.F, win, h, e.sl, h, e.F, v2, h));
+  PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + h));
+  PDS_TRY(e.wait(e.st, ev_proj));
+  PDS_TRY(e.gemm(Exec::G(dx, h, 0, wproj, h, 0, e.sl, h, h, da, h)));                  // dA = dO of attention
+  PDS_TRY(tn.dw(sv->at("a"), h, dx, h, e.sl, h, h, dw, EPI_F32));
+  PDS_TRY(uz_dw(e, dw, h, g->dw_proj));
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 4);
+    for (int64_t q = 0; q < b; ++q)
+      PDS_TRY(kerr(attn_dot(sv->at("a") + q * h * 2, b * h, da + q * h * 2, (int)sp, (int)n, (int)d, dd + q * n * sp,
+                            e.st), "attn_dot"));
+  }
+  // ring of V: dP_j = dO V_j^T, dV_j += P_j^T dO (the accumulator travels with V_j)
+  PDS_CUDA(cudaMemsetAsync(dacc[0], 0, e.sl * h * 4, e.st));
+  int cur = 0;
+  PDS_TRY(col_ring(e, qkv, 2 * h, kr, [&](int, int j, const char* vb) -> pds_status {
+    for (int64_t q = 0; q < b; ++q)
+      for (int64_t hd = 0; hd < n; ++hd) {
+        PDS_TRY(e.gemm(Exec::G(da + (q * h + hd * d) * 2, b * h, 0, vb + (q * h + hd * d) * 2, b * h, 0, sp, sp, d,
+                               dp + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
+        PDS_TRY(e.gemm(Exec::G(probs + ((q * n + hd) * sp * sq + j * sp) * 2, sq, 1, da + (q * h + hd * d) * 2,
+                               b * h, 1, sp, d, sp, dacc[cur] + q * h + hd * d, b * h, EPI_F32_ACC)));
+      }
+    if (e.P > 1) {
+      PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dacc[cur]), reinterpret_cast<char*>(dacc[cur ^ 1]),
+                        e.sl * h * 4, e.st));
+      cur ^= 1;
+    }
+    return PDS_OK;
+  }));
+  // dV (home after P passes) -> the V columns of dQKV
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 6);
+    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], h, (int)e.sl, (int)h, (int)d, nullptr, 0, 0, (int)e.sl, (int)b,
+                                 dqkv + 2 * h * 2, 3 * h, e.st), "dv convert"));
+  }
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)b * n * sp * sq * 8);
+    for (int64_t q = 0; q < b; ++q)
+      PDS_TRY(kerr(rsa_dsoftmax(probs + q * n * sp * sq * 2, sq, dp + q * n * sp * sq, sq, dd + q * n * sp,
+                                (int)(n * sp), (int)sq, 1.0f / std::sqrt((float)d), ds + q * n * sp * sq * 2, sq, e.st),
+                   "rsa_dsoftmax"));
+  }
+  // ring of K: dQ += dS_j K_j, dK_j += dS_j^T Q (the accumulator travels with K_j)
+  PDS_CUDA(cudaMemsetAsync(dqacc, 0, e.sl * h * 4, e.st));
+  PDS_CUDA(cudaMemsetAsync(dacc[cur], 0, e.sl * h * 4, e.st));
+  PDS_TRY(col_ring(e, qkv, h, kr, [&](int, int j, const char* kb) -> pds_status {
+    for (int64_t q = 0; q < b; ++q)
+      for (int64_t hd = 0; hd < n; ++hd) {
+        const char* dsb = ds + ((q * n + hd) * sp * sq + j * sp) * 2;
+        PDS_TRY(e.gemm(Exec::G(dsb, sq, 0, kb + (q * h + hd * d) * 2, b * h, 1, sp, d, sp, dqacc + q * h + hd * d,
+                               b * h, EPI_F32_ACC)));
+        PDS_TRY(e.gemm(Exec::G(dsb, sq, 1, qkv + (q * 3 * h + hd * d) * 2, b * 3 * h, 1, sp, d, sp,
+                               dacc[cur] + q * h + hd * d, b * h, EPI_F32_ACC)));
+      }
+    if (e.P > 1) {
+      PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dacc[cur]), reinterpret_cast<char*>(dacc[cur ^ 1]),
+                        e.sl * h * 4, e.st));
+      cur ^= 1;
+    }
+    return PDS_OK;
+  }));
+  {
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 2 * h * 6);
+    const int64_t b0 = e.r * sp;
+    PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b, dqkv,
+                                 3 * h, e.st), "dq rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], h, (int)e.sl, (int)h, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b,
+                                 dqkv + h * 2, 3 * h, e.st), "dk rope_t"));
+  }
+  PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
+  PDS_TRY(tn.dw(dqkv, 3 * h, u1, h, e.sl, 3 * h, h, dw, EPI_F32));
+  for (int i = 0; i < 3; ++i) {
+    char* part = dw + i * h * h * 4;
+    const int64_t cnt = e.hl * h;
+    char* mine = part + e.r * cnt * 4;
+    PDS_TRY(e.rs(part, mine, cnt, DT_F32));
+    PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + i * cnt * 4, cnt, e.st), "add_f32"));
+  }
+  PDS_TRY(e.wait(e.st, ev_qkv));
+  PDS_TRY(tn.xw(dqkv, 3 * h, wqkv, h, e.sl, h, 3 * h, v2, h));                          // dU
+  PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
+  return e.dgamma(dgl, g);
+}
+
 // ================================================================== METP (R-METP)
 int64_t metp_c(const Exec& e) { return e.m.metp_chunks > 0 ? e.m.metp_chunks : e.P; }
 
@@ -1441,6 +1669,7 @@ extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_le
     case PDS_MEGATRON_TS: rc = ts_fwd(e, x, w, y, sv.get(), c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_fwd(e, x, w, y, sv.get(), c->ws); break;
     case PDS_MEGATRON_CZ: rc = cz_fwd(e, x, w, y, sv.get(), c->ws); break;
+    case PDS_COLOSSAL_Z: rc = col_fwd(e, x, w, y, sv.get(), c->ws); break;
     default: rc = metp_fwd(e, x, w, y, sv.get(), c->ws); break;
   }
   c->tap_o = c->tap_z = nullptr;
@@ -1471,6 +1700,7 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
     case PDS_MEGATRON_TS: rc = ts_bwd(e, dy, saved, w, g, dx, c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_bwd(e, dy, saved, w, g, dx, c->ws); break;
     case PDS_MEGATRON_CZ: rc = cz_bwd(e, dy, saved, w, g, dx, c->ws); break;
+    case PDS_COLOSSAL_Z: rc = col_bwd(e, dy, saved, w, g, dx, c->ws); break;
     default: rc = metp_bwd(e, dy, saved, w, g, dx, c->ws); break;
   }
   c->saved_live -= saved->bytes;

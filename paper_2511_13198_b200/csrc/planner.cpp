@@ -373,6 +373,44 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
       break;
     }
+    case PDS_COLOSSAL_Z: {
+      // saved: TS's local-row tensors without LSE, plus the softmax probabilities of the
+      // own rows against every key, [b][n][s/P][s] bf16 (Ring Self-Attention, R-COL)
+      const int64_t n = m.n_heads;
+      const int64_t quad = n * sl * s * m.batch;       // elements of [b][n][s/P][s]
+      push(p.saved, ts, "rstd1", ell);
+      push(p.saved, ts, "qkv", SL * 3 * h * 2);
+      push(p.saved, ts, "a", u);
+      push(p.saved, ts, "probs", quad * 2);
+      push(p.saved, ts, "x1", u);
+      push(p.saved, ts, "rstd2", ell);
+      push(p.saved, ts, "h", SL * F * 2);
+      push(p.ws, tw, "wqkv", 3 * h * h * 2);
+      push(p.ws, tw, "wproj", h * h * 2);
+      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "wout", F * h * 2);
+      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "u1", u);
+      push(p.ws, tw, "scores", quad * 4);          // fp32 scores (bwd: dP)
+      push(p.ws, tw, "ds", quad * 2);              // bf16 dS (bwd)
+      push(p.ws, tw, "kr0", u);                    // the K (or V) block in hand / the next one
+      push(p.ws, tw, "kr1", u);
+      push(p.ws, tw, "acc", 2 * u);                // fp32 O (bwd: dQ)
+      push(p.ws, tw, "dacc0", 2 * u);              // fp32 dV / dK travelling with their block
+      push(p.ws, tw, "dacc1", 2 * u);
+      push(p.ws, tw, "dqkv", 3 * u);
+      push(p.ws, tw, "f0", SL * F * 2);
+      push(p.ws, tw, "f1", SL * F * 2);
+      push(p.ws, tw, "v2", u);
+      push(p.ws, tw, "da", u);
+      push(p.ws, tw, "dd", lam);
+      push(p.ws, tw, "dgp", dgp);
+      push(p.ws, tw, "dgl", 2 * h * 4);
+      push(p.ws, tw, "ta", std::max(3 * h, F) * SL * 2);
+      push(p.ws, tw, "tb", h * SL * 2);
+      push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
+      break;
+    }
     default:
       PDS_FAIL(PDS_ESTRATEGY, "unknown strategy id " + std::to_string(strategy));
   }

@@ -127,7 +127,7 @@ def main():
             best = (s, list(plan))
             s += a.step
         entry = {"predicted_max_s": best[0] if best else 0,
-                 "plan_at_max": "".join("TUMCF"[p] for p in best[1]) if best else None}
+                 "plan_at_max": "".join("TUMCFR"[p] for p in best[1]) if best else None}
         if best and not a.no_run:
             s_ok, plan = best
             try:

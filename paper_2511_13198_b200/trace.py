@@ -106,7 +106,7 @@ def run_trace(torch, B, ctx, model, lens, layers, L, fixed=None, memo=None):
             recs.append({"s": s, "oom": True})
             break
         cum += t
-        recs.append({"s": s, "plan": "".join("TUMCF"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
+        recs.append({"s": s, "plan": "".join("TUMCFR"[p] for p in plan), "seconds": t, "cum": cum, "flags": flags})
     per_bucket = {}
     for r in recs:
         if r.get("oom"):
@@ -158,9 +158,9 @@ def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
         per_layer[pi] = t / n_short
     t_mixed = measure(torch, B, ctx, model, plan, s, layers, memo)
     pred = sum(per_layer[p] for p in plan)
-    return {"s": s, "plan": "".join("TUMCF"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
+    return {"s": s, "plan": "".join("TUMCFR"[p] for p in plan), "measured_s": t_mixed, "sum_of_layers_s": pred,
             "overhead": t_mixed / pred - 1.0,
-            "per_layer_s": {"TUMCF"[k]: v for k, v in per_layer.items()}}
+            "per_layer_s": {"TUMCFR"[k]: v for k, v in per_layer.items()}}
 
 
 STATIC = (("MegatronTS", 0), ("UlyssesZ", 1), ("METP", 2), ("MegatronCZ", 3), ("METP-full", 4))
@@ -190,7 +190,7 @@ def predict_trace(B, model, bundle, lens, L, gamma, fixed=None, real=None):
         t = ctx.cost_eval(s)[0]
         sec = sum(t[p] for p in plan)
         cum += sec
-        recs.append({"s": s, "real": int(rs), "plan": "".join("TUMCF"[p] for p in plan), "seconds": sec, "cum": cum,
+        recs.append({"s": s, "real": int(rs), "plan": "".join("TUMCFR"[p] for p in plan), "seconds": sec, "cum": cum,
                      "flags": flags})
     ctx.close()
     per_bucket = {}
@@ -229,7 +229,7 @@ def predict_frontier(B, model, bundle, L, unit, fixed=None, s_max=1 << 20):
             lo = mid
         else:
             hi = mid
-    plan = "".join("TUMCF"[p] for p in ctx.plan(lo * unit, L)[0]) if lo else None
+    plan = "".join("TUMCFR"[p] for p in ctx.plan(lo * unit, L)[0]) if lo else None
     ctx.close()
     return {"s": lo * unit, "plan": plan}
 

@@ -49,6 +49,7 @@ CASES = [  # h, n, F, s, strategy, metp_chunks, metp_recompute, last sampled row
     (4096, 32, 16384, 4096, 2, 0, 0, 4095),
     (4096, 32, 16384, 4096, 3, 0, 0, 4095),
     (4096, 32, 16384, 4096, 4, 4, 0, 4095),
+    (4096, 32, 16384, 4096, 5, 0, 0, 4095),        # ColossalZ (Ring Self-Attention, quadratic)
     (4096, 32, 16384, 32768, 0, 0, 0, 32767),      # the bench's longest length
     (4096, 32, 16384, 32768, 4, 8, 0, 32767),      # METP-full, 8 waves (the 624K configuration)
     (4096, 32, 16384, 32768, 2, 4, 1, 20000),      # METP with the metp_recompute = full knob

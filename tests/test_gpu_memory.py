@@ -32,7 +32,7 @@ def _free():
     return torch.cuda.mem_get_info()[0]
 
 
-@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4, 5])
 def test_device_allocation_equals_mem_bytes(pi):
     s = 16384
     model = B.Model(h=H, n_heads=N, ffn=F, metp_chunks=4)

@@ -31,7 +31,7 @@ def _run(pi, P, d, s, causal=True, chunks=None):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4, 8])
-@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ])
+@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ, S.COL])
 def test_strategy_equals_unsharded(pi, P):
     s = 32
     d = layer_inputs(H, N, F, s, 1, seed=21)
@@ -64,7 +64,7 @@ def test_noncausal_and_batch(P):
     d = layer_inputs(H, N, F, s, 2, seed=5)
     y_ref, c = layer.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"],
                                d["g2"], n=N, causal=False)
-    for pi in (S.TS, S.UZ, S.METP, S.CZ):
+    for pi in (S.TS, S.UZ, S.METP, S.CZ, S.COL):
         _, ys, _, _, _, _ = _run(pi, P, d, s, causal=False)
         assert _rel(shard.unshard_act(ys), y_ref) < 1e-12
 
@@ -91,6 +91,10 @@ def test_comm_signatures_and_bytes_c1():
         # SendRecv(dQKV -> boundary), the 6 fp32 dW reduce-scatters, AR(dgamma)
         (S.CZ, {"AllGather": 6, "SendRecv": 2, "RingPass": 1},
          {"AllGather": 12, "SendRecv": 5, "RingPass": 4, "ReduceScatter": 6, "AllReduce": 1}),
+        # ColossalZ (RSA): weights as CZ; fwd K ring and V ring (P - 1 each); bwd V ring and
+        # K ring (P - 1 each) plus the fp32 dV and dK accumulators (P passes each)
+        (S.COL, {"AllGather": 6, "RingPass": 2},
+         {"AllGather": 12, "RingPass": 8, "ReduceScatter": 6, "AllReduce": 1}),
     ]:
         g, _, _, _, _, flog = _run(pi, P, d, s)
         assert _signature(flog) == Counter(fwd_sig), pi
@@ -111,7 +115,7 @@ def test_switched_chain_equals_stack(P):
     x = layers[0]["x"]
     dy = layers[0]["dy"]
     for trial in range(3):
-        plan = list(rng.integers(0, 4, size=Ln))
+        plan = list(rng.integers(0, 6, size=Ln))
         # dense stack
         yd = x
         caches = []
@@ -153,7 +157,7 @@ def test_switched_chain_equals_stack(P):
 
 
 @pytest.mark.parametrize("P", [1, 2, 4])
-@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ])
+@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.CZ, S.COL])
 def test_ledger_equals_memory_model(pi, P):
     # the ledger recount of saved tensors equals the analytic formula
     s = 32
