@@ -29,7 +29,15 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BUNDLES = os.path.join(HERE, "bundles")
-ALL = (0, 1, 2, 3, 4)       # TS, UZ, METP, CZ, METP-full (include/paradyse.h)
+ALL = (0, 1, 2, 3, 4, 5)    # TS, UZ, METP, CZ, METP-full, ColossalZ (include/paradyse.h)
+
+
+def fits(torch, B, model, pi, s, P=1):
+    """One layer of strategy pi at length s fits on this device (ColossalZ's quadratic
+    score matrix limits its profiled range; the other strategies fit the whole grid)."""
+    sv, ws, pers = B.mem_bytes(model, P, pi, s)
+    free, _ = torch.cuda.mem_get_info()
+    return sv + ws + pers < 0.85 * free
 
 
 S_EXTRAP_MAX = float(1 << 20)    # longest length the bundles extrapolate to (> 624K, Q-16)
@@ -81,7 +89,7 @@ def aic_poly(s, y, degrees=PR_DEGREES):
 def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
     """records: {strategy: [(s, seconds), ...]} -> bundle file."""
     from sklearn.ensemble import RandomForestRegressor
-    strategies = sorted(records)
+    strategies = sorted(k for k in records if len(records[k]) >= 2)   # profiled (fits the device)
     all_s = [s for st in strategies for s, _ in records[st]]
     norm = [(h, h), (n, n), (L, L), (float(min(all_s)), float(max(all_s)))]
 
@@ -184,6 +192,9 @@ def comm_bytes_per_rank(pi, h, F, s, P):
     wb = 4 * h * h + 2 * h * F
     if pi == 3:              # CZ (R-CZ): zigzag exchanges + K/V ring (bf16) + dK/dV ring (fp32), ZeRO3 weights
         return cz_zig_bytes(h, s, P) + cz_ring_bytes(h, s, P) + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+    if pi == 5:              # ColossalZ (RSA): K, V rings fwd + V, K rings bwd (bf16), dV, dK rings (fp32)
+        kb = (s // P) * h
+        return 4 * (P - 1) * kb * 2 + 2 * P * kb * 4 + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
     a2a = 2 * fr * (s // P) * 4 * h * 2
     return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
 
@@ -222,15 +233,17 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         ctx = B.Context(model)
         for s in grid:
             w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
+            run = [pi for pi in ALL if fits(torch, B, model, pi, s)]
             # strategies interleaved rep by rep (one warm-up pass each first), so slow drift
             # of the power-capped clock does not favour whichever strategy runs last
-            for pi in ALL:
+            for pi in run:
                 time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=1)
-            ts = {pi: [] for pi in ALL}
+                ctx.release_cache()
+            ts = {pi: [] for pi in run}
             for _ in range(reps):
-                for pi in ALL:
+                for pi in run:
                     ts[pi].append(time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0))
-            for pi in ALL:
+            for pi in run:
                 t = float(np.median(ts[pi]))
                 records[pi].append((int(s), t))
                 print(f"P=1 s={s} pi={pi} t={t * 1e3:.3f} ms", flush=True)
@@ -248,7 +261,7 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         for s in grid:
             t_unit, t_gemm = {}, {}
             t_att = 0.0
-            for pi in ALL:
+            for pi in [q for q in ALL if fits(torch, B, model, q, s)]:
                 w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
                 cx = ctx_m if pi in (2, 4) else ctx
                 t1 = time_layer(torch, B, cx, pi, s, w, gr, x, dy, reps=reps)
@@ -257,8 +270,9 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                 if pi == 3:
                     t_att = class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, (1, 2))
                 del w, gr, x, dy
+                cx.release_cache()
             torch.cuda.empty_cache()
-            for pi in ALL:
+            for pi in t_unit:
                 comp = t_unit[pi] / P              # CZ: zigzag placement, every rank 1/P of the attention
                 comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
                 if pi == 3:
@@ -272,7 +286,7 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                     # flops per token); at least one chunk per collective stays exposed
                     comm = max(comm / P, comm - (2.0 / 3.0) * t_gemm[pi] / P)
                 extra = (2 * P - 1) * 8e-6 * (P if pi in (2, 4) else 1)   # collective launch latency
-                if pi == 3:
+                if pi in (3, 5):
                     extra += 6 * 8e-6 * (P - 1)                           # part-wise weight AG / RS
                 records[pi].append((int(s), comp + comm + extra))
         ctx.close()
@@ -312,18 +326,22 @@ def profile_measured(h, n, ffn, L, grid, out_dir=BUNDLES, reps=3):
         if s % (P * 128) or (s // P) % (P * 128):
             continue                                  # METP waves need s/(P c) % 128 == 0, c = P
         w, gr, x, dy = make_layer_buffers(torch, model, P, s, seed=1 + rank)
-        for pi in ALL:
+        ok = torch.tensor([1.0 if fits(torch, B, model, pi, s, P) else 0.0 for pi in ALL], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)            # every rank runs the same set
+        run = [pi for i, pi in enumerate(ALL) if ok[i] > 0]
+        for pi in run:
             time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=1)
-        ts = {pi: [] for pi in ALL}
+            ctx.release_cache()
+        ts = {pi: [] for pi in run}
         for _ in range(reps):
-            for pi in ALL:
+            for pi in run:
                 ts[pi].append(time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=1, warm=0))
-        med = torch.tensor([float(np.median(ts[pi])) for pi in ALL], dtype=torch.float64, device="cuda")
+        med = torch.tensor([float(np.median(ts[pi])) for pi in run], dtype=torch.float64, device="cuda")
         dist.all_reduce(med, op=dist.ReduceOp.MAX)
-        for i, pi in enumerate(ALL):
+        for i, pi in enumerate(run):
             records[pi].append((int(s), float(med[i])))
         if rank == 0:
-            print(f"P={P} s={s} " + " ".join(f"pi{pi}={float(med[i]) * 1e3:.3f}ms" for i, pi in enumerate(ALL)),
+            print(f"P={P} s={s} " + " ".join(f"pi{pi}={float(med[i]) * 1e3:.3f}ms" for i, pi in enumerate(run)),
                   flush=True)
         del w, gr, x, dy
         torch.cuda.empty_cache()
