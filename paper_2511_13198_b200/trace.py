@@ -163,10 +163,10 @@ def switch_cost(torch, B, ctx, model, s, plan, layers, n_short=4):
             "per_layer_s": {"TUMCFR"[k]: v for k, v in per_layer.items()}}
 
 
-STATIC = (("MegatronTS", 0), ("UlyssesZ", 1), ("METP", 2), ("MegatronCZ", 3), ("METP-full", 4))
+STATIC = (("MegatronTS", 0), ("UlyssesZ", 1), ("METP", 2), ("MegatronCZ", 3), ("METP-full", 4), ("ColossalZ", 5))
 
 
-def predict_trace(B, model, bundle, lens, L, gamma, fixed=None, real=None):
+def predict_trace(B, model, bundle, lens, L, gamma, fixed=None, real=None, mask=None):
     """The trace protocol on a host-only context: plan (adaptive) or the uniform plan
     (static), time = sum over layers of the bundle's T_pi(s), OOM = Eq. 6 infeasible.
     real[i]: the unpadded length of lens[i] (tokens/s counts real tokens, Q-15)."""
@@ -175,6 +175,8 @@ def predict_trace(B, model, bundle, lens, L, gamma, fixed=None, real=None):
     ctx.load_costs(bundle)
     if fixed is not None:
         ctx.set_enabled(1 << fixed)
+    elif mask is not None:
+        ctx.set_enabled(mask)
     ctx.set_capacity(bundle_capacity(bundle), gamma if gamma > 0 else 1e-9)
     recs, cum, oom_at = [], 0.0, None
     for s, rs in zip(lens, real):
@@ -246,6 +248,34 @@ def bundle_capacity(path):
     return cap - (float(m.group(1)) if m else 0.0)
 
 
+def predict_ablation(B, model, bundle, lens, real, L):
+    """Table 5 on the cost model: ParaDySe (full, gamma = 0.05) and the
+    variants without one strategy, without RF (PR everywhere) and without smoothing."""
+    ALL = (1 << B.N_STRATEGIES) - 1
+    variants = [("ParaDySe (full)", dict(gamma=0.05)), ("w/o MegatronTS", dict(mask=ALL & ~1, gamma=0.05)),
+                ("w/o MegatronCZ", dict(mask=ALL & ~8, gamma=0.05)), ("w/o UlyssesZ", dict(mask=ALL & ~2, gamma=0.05)),
+                ("w/o ColossalZ", dict(mask=ALL & ~32, gamma=0.05)),
+                ("w/o METP", dict(mask=ALL & ~4 & ~16, gamma=0.05)), ("w/o RF", dict(gamma=0.05, pr_only=True)),
+                ("w/o Smoothing", dict(gamma=0.0))]
+    runs = {}
+    for name, kw in variants:
+        path = pr_only_bundle(bundle) if kw.get("pr_only") else bundle
+        if kw.get("pr_only"):
+            os.replace(path, path + f"_P{bundle_P(bundle)}.txt")
+            path = path + f"_P{bundle_P(bundle)}.txt"
+        runs[name] = predict_trace(B, model, path, lens, L, kw["gamma"], real=real, mask=kw.get("mask"))
+    full = runs["ParaDySe (full)"]
+    table = []
+    for name, _ in variants:
+        r = runs[name]
+        tf = time_full_at(full, r["max_s_trained"])
+        table.append({"framework": name, "seq_len": r["max_s_trained"], "time_s": r["cumulative_s"], "time_full_s": tf,
+                      "saving": None if name.endswith("(full)") or r["cumulative_s"] == 0
+                      else (r["cumulative_s"] - tf) / r["cumulative_s"],
+                      "switching": r["switching"]})
+    return table
+
+
 def predict_main(a):
     import sys
     sys.path.insert(0, ROOT)
@@ -275,6 +305,10 @@ def predict_main(a):
                  "bucket_common": common_bucket_table(runs, a.L),
                  "max_s_trained": {n: r["max_s_trained"] for n, r in runs.items()},
                  "frontier_L_stack": frontier}
+        if a.ablation:
+            entry["table5"] = predict_ablation(B, model, bundle, lens, real, a.L)
+            for row in entry["table5"]:
+                print("  ", {k: row[k] for k in ("framework", "seq_len", "time_s", "saving")}, flush=True)
         out["by_P"][str(P)] = entry
         print(f"P={P}", "max_s", entry["max_s_trained"], flush=True)
         print("  frontier", {n: v["s"] for n, v in frontier.items()}, flush=True)
@@ -297,6 +331,7 @@ def main():
         ap.add_argument("--L", type=int, default=32)
         ap.add_argument("--P", type=int, nargs="+", default=[1, 2, 4, 8])
         ap.add_argument("--gamma", type=float, default=0.0)
+        ap.add_argument("--ablation", action="store_true")
         ap.add_argument("--out", default=None)
         return predict_main(ap.parse_args())
     sys.path.insert(0, ROOT)
