@@ -16,9 +16,10 @@ def test_pr_only_bundle_takes_polynomial_everywhere():
         assert e["s_profile_max"] == 0.0
         f = full["strat"][sid]
         assert e["poly_coef"] == f["poly_coef"] and e["poly_scale"] == f["poly_scale"]
-        _, branch = OC.predict_time(e, [0.0] * 9, 1024)
+        nf = len(full["strat"]) + 4                 # one-hot over the bundle's strategies + (h, n, L, s)
+        _, branch = OC.predict_time(e, [0.0] * nf, 1024)
         assert branch == "pr"
-        _, branch = OC.predict_time(f, [0.0] * 9, 1024)
+        _, branch = OC.predict_time(f, [0.0] * nf, 1024)
         assert branch == "rf"
 
 
