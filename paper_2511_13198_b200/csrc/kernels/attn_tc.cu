@@ -28,6 +28,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <string>
 #include <type_traits>
 
 #include "ptx.cuh"
@@ -420,6 +421,306 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// ============================================================ forward, CTA pair
+// The forward above reads 192 KB of operands per 128-key block from shared memory
+// (S0 and S1 each stream Q_t and K, PV0 and PV1 each stream V) plus the 64 KB TMA
+// refill: ~125 B/clk at the tensor peak, the shared-memory limit.  Here a cluster of
+// two CTAs issues every MMA as cta_group::2 (M = 256: CTA c's 128 query rows of tile t
+// in its own TMEM), and each CTA stages only HALF of every B operand — K rows
+// [64c, 64c+64) of the key block for S = Q K^T, V columns [64c, 64c+64) for O += P V —
+// so per CTA the operand stream is 128 KB per key block and the refill 32 KB.
+// The pair covers 512 query rows: tile t of CTA c = rows base + 256 t + 128 c, so the
+// pair MMA t needs the key blocks up to (base + 256 t + 255) / 128 (per-tile nkv).
+// The leader (rank 0) issues all MMAs and owns q_full / kv_full / p_half / p_full
+// (both CTAs' TMA bytes and softmax arrivals land on the leader's barriers); the
+// commits multicast s_full / o_done / kv_empty to both CTAs.  Everything else (online
+// softmax, lazy rescale, P in TMEM, epilogue) is the single-CTA kernel's, per CTA.
+struct FwdPairCfg {
+  static constexpr int D = 128;
+  static constexpr int TILE = 128 * D * 2;        // one Q tile [128][128] bf16
+  static constexpr int KH = 64 * D * 2;           // K half [64 keys][128]
+  static constexpr int VH = 128 * 64 * 2;         // V half [128 keys][64]
+  static constexpr int NST = 3;
+  static constexpr int Q_OFF = 0;                 // Q0, Q1
+  static constexpr int K_OFF = 2 * TILE;          // [NST]
+  static constexpr int V_OFF = K_OFF + NST * KH;  // [NST]
+  static constexpr int BAR_OFF = V_OFF + NST * VH;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_fwd_pair_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                            const __grid_constant__ CUtensorMap tmv, int s, int heads, int causal,
+                            __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
+                            float scale_log2, int qlo, int qn, int kcol, int vcol) {
+  using C = FwdPairCfg;
+  constexpr int D = C::D, NST = C::NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;             // [NST] (leader)
+  uint64_t* kv_empty = bar + 1 + NST;      // [NST] (both, multicast commit)
+  uint64_t* s_full = bar + 1 + 2 * NST;    // [2] per tile (both)
+  uint64_t* p_full = bar + 3 + 2 * NST;    // [2] (leader, 8 arrivals)
+  uint64_t* o_done = bar + 5 + 2 * NST;    // [2] (both)
+  uint64_t* p_half = bar + 7 + 2 * NST;    // [2] (leader, 8 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9 + 2 * NST);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int npb = (qn + 511) / 512;
+  const int pb = causal ? (npb - 1 - (int)(blockIdx.x >> 1)) : (int)(blockIdx.x >> 1);
+  const int head = blockIdx.y;
+  const int base = qlo + pb * 512;
+  // per pair-MMA t: key blocks up to the last query row of tile t of CTA 1
+  int nkv_t[2];
+  for (int t = 0; t < 2; ++t)
+    nkv_t[t] = causal ? (min(s, base + 256 * t + 256) + BN - 1) / BN : s / BN;
+  const int nkv = max(nkv_t[0], nkv_t[1]);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmq);
+    tma_prefetch(&tmk);
+    tma_prefetch(&tmv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&p_half[i], 8);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t qf = mapa_u32(q_full, 0);
+      if (rank == 0) mbar_arrive_expect_tx(q_full, 2 * 2 * C::TILE);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < D / 64; ++a)
+          tma_load_2d_2sm(sm + C::Q_OFF + t * C::TILE + a * 16384, &tmq, qf, head * D + a * 64,
+                          base + 256 * t + 128 * rank);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[st], ((j / NST) - 1) & 1);
+        const uint32_t kf = mapa_u32(&kv_full[st], 0);
+        if (rank == 0) mbar_arrive_expect_tx(&kv_full[st], 2 * (C::KH + C::VH));
+        for (int a = 0; a < D / 64; ++a)
+          tma_load_2d_2sm(sm + C::K_OFF + st * C::KH + a * 8192, &tmk, kf, kcol + head * D + a * 64,
+                          j * BN + 64 * rank);
+        tma_load_2d_2sm(sm + C::V_OFF + st * C::VH, &tmv, kf, vcol + head * D + 64 * rank, j * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(256, BN, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(256, D, 0, 1);
+      const uint32_t sq = smem_u32(sm + C::Q_OFF);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int t, int j) {
+        if (elect_one()) {
+          const uint32_t sk = smem_u32(sm + C::K_OFF + (j % NST) * C::KH);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            umma_f16_2sm(tmem + t * 128, kmaj_desc(sq + t * C::TILE, kk), kmaj_desc(sk, kk, 8192), idesc_s, kk > 0);
+          umma_commit_2sm_mc(&s_full[t], 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t sv = smem_u32(sm + C::V_OFF + (j % NST) * C::VH);
+        mbar_wait(&p_half[t], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BN / 32; ++kk)
+            umma_f16_ts_2sm(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, (j | kk) != 0);
+        }
+        __syncwarp();
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = BN / 32; kk < BN / 16; ++kk)
+            umma_f16_ts_2sm(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj_desc(sv, kk), idesc_o, 1);
+        }
+        __syncwarp();
+      };
+      auto wait_kv = [&](int j) {
+        mbar_wait(&kv_full[j % NST], (j / NST) & 1);
+        tc_fence_after();
+      };
+      wait_kv(0);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool a0 = j < nkv_t[0];
+        if (a0) {
+          issue_pv(0, j);
+          if (j + 1 < nkv_t[0]) {
+            wait_kv(j + 1);
+            issue_s(0, j + 1);
+          } else if (elect_one()) {
+            umma_commit_2sm_mc(&o_done[0], 0x3);
+          }
+          __syncwarp();
+        }
+        issue_pv(1, j);
+        if (elect_one()) umma_commit_2sm_mc(&kv_empty[j % NST], 0x3);
+        __syncwarp();
+        if (j + 1 < nkv_t[1]) {
+          if (!(j + 1 < nkv_t[0])) wait_kv(j + 1);
+          issue_s(1, j + 1);
+        } else if (elect_one()) {
+          umma_commit_2sm_mc(&o_done[1], 0x3);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int tile = (warp - 4) >> 2;        // 0: warps 4-7, 1: warps 8-11
+    const int q = warp & 3;
+    const int tr = q * 32 + lane;            // row within the tile = TMEM lane
+    const int q0 = base + 256 * tile + 128 * (int)rank;   // this CTA's tile rows
+    const int row = q0 + tr;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t s_col = tile * 128, o_col = 256 + tile * 128;
+    const uint32_t ph_lead = mapa_u32(&p_half[tile], 0), pf_lead = mapa_u32(&p_full[tile], 0);
+    const int my_nkv = nkv_t[tile];
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < my_nkv; ++j) {
+      mbar_wait(&s_full[tile], j & 1);
+      tc_fence_after();
+      const int k0 = j * BN;
+      const bool mask = causal && (k0 + BN - 1 > q0);
+      auto block = [&](auto mask_c) {
+        constexpr bool MASK = decltype(mask_c)::value;
+        float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        {
+          uint32_t cur[16], nxt[16];
+          tmem_ld16(lb + s_col, cur);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < BN / 16; ++c) {
+            if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float v = __uint_as_float(cur[i]);
+              if (MASK && k0 + c * 16 + i > row) v = -INFINITY;
+              mxa[i & 3] = fmaxf(mxa[i & 3], v);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+          }
+        }
+        const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
+        const float m_new = mx * scale_log2;
+        const bool need = m_new > m_used + 8.0f;
+        if (j > 0 && __any_sync(0xffffffff, need)) {
+          const float f = need ? ex2(m_used - m_new) : 1.0f;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(lb + o_col + c * 32, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st16(lb + o_col + c * 32, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+            tmem_st16(lb + o_col + c * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+          }
+          if (need) l *= f;
+        }
+        if (need) m_used = m_new;
+        f2 rs2[2] = {f2{0.f, 0.f}, f2{0.f, 0.f}};
+        const f2 nm2{-m_used, -m_used}, sl2{scale_log2, scale_log2};
+        {
+          uint32_t cur[16], nxt[16];
+          tmem_ld16(lb + s_col, cur);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < BN / 16; ++c) {
+            if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const f2 x = fma2(f2{__uint_as_float(cur[i]), __uint_as_float(cur[i + 1])}, sl2, nm2);
+              f2 p;
+              if (emu_pair(i >> 1)) {
+                p = exp2_fma2(x);
+              } else {
+                p.x = ex2(x.x);
+                p.y = ex2(x.y);
+              }
+              if (MASK) {
+                if (k0 + c * 16 + i > row) p.x = 0.f;
+                if (k0 + c * 16 + i + 1 > row) p.y = 0.f;
+              }
+              rs2[(i >> 1) & 1] = add2(rs2[(i >> 1) & 1], p);
+              pk[i >> 1] = pack_bf16(p.x, p.y);
+            }
+            tmem_st8(lb + s_col + c * 8, pk);
+            if (c == BN / 32 - 1) {
+              tmem_st_wait();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive_cluster(ph_lead);
+            }
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+          }
+        }
+        const f2 rs = add2(rs2[0], rs2[1]);
+        l += rs.x + rs.y;
+      };
+      if (mask) block(std::true_type{});
+      else block(std::false_type{});
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(pf_lead);
+    }
+    mbar_wait(&o_done[tile], 0);
+    tc_fence_after();
+    const float inv = 1.0f / l;
+    const bool ok = row < qlo + qn;
+    __nv_bfloat16* o = out + (int64_t)(row - qlo) * ld_out + head * D;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(lb + o_col + c * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(o + c * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          d4[e] = make_uint4(pack_bf16(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
+                             pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+      }
+    }
+    if (ok) lse[(int64_t)head * qn + (row - qlo)] = (m_used + log2f(l)) * LN2;
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
   }
 }
 
@@ -1623,10 +1924,46 @@ int make_map_rows(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
 // q: queries [rows of the q map][ld_q] (head i at column i*D); kv: keys at column kcol
 // and values at vcol (head i at + i*D) of [s][ld_kv]; q == kv with kcol = heads*D, vcol =
 // 2*heads*D is the packed [Q | K | V] buffer.  Query rows [qlo, qlo + qn) of the q map.
+// PDS_ATTN_FWD=pair selects the CTA-pair forward (opt-in): measured slower than the
+// single-CTA kernel (s = 32K: 1010 vs 1341 TF/s; ncu at 16K: tensor pipe 47.5 %, the
+// softmax warps wait on S — every P half-release of either CTA reaches the leader's MMA
+// thread through a cluster-scope remote arrive, which lengthens the S -> softmax -> PV
+// -> S chain more than the halved operand traffic saves; profiles/r02_attn_fwd_pair.md)
+static int fwd_pair_mode() {
+  static const int v = [] {
+    const char* e = getenv("PDS_ATTN_FWD");
+    return (e && std::string(e) == "pair") ? 1 : 0;
+  }();
+  return v;
+}
+
+static int fwd_pair(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
+                    int s, int heads, int causal, void* out, int64_t ld_out, void* lse, int qlo, int qn,
+                    cudaStream_t st) {
+  constexpr int D = 128;
+  CUtensorMap tmq, tmk, tmv;
+  int rc = make_map_rows(&tmq, q, (uint64_t)heads * D, q_rows, (uint64_t)ld_q, 128);
+  rc |= make_map_rows(&tmk, kv, (uint64_t)vcol + heads * D, (uint64_t)s, (uint64_t)ld_kv, 64);
+  rc |= make_map_rows(&tmv, kv, (uint64_t)vcol + heads * D, (uint64_t)s, (uint64_t)ld_kv, 128);
+  if (rc) return (int)cudaErrorInvalidValue;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(attn_fwd_pair_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdPairCfg::SMEM);
+    once = true;
+  }
+  const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
+  attn_fwd_pair_tc_kernel<<<dim3(2 * ((qn + 511) / 512), heads), 384, FwdPairCfg::SMEM, st>>>(
+      tmq, tmk, tmv, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
+      scale_log2, qlo, qn, kcol, vcol);
+  return (int)cudaGetLastError();
+}
+
 template <int D>
 static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     int s, int heads, int causal, void* out, int64_t ld_out, void* lse, int qlo, int qn,
                     cudaStream_t st) {
+  if (D == 128 && fwd_pair_mode())
+    return fwd_pair(q, ld_q, q_rows, kv, ld_kv, kcol, vcol, s, heads, causal, out, ld_out, lse, qlo, qn, st);
   CUtensorMap tm, tmq;
   int rc = make_map_rows(&tm, kv, (uint64_t)vcol + heads * D, (uint64_t)s, (uint64_t)ld_kv);
   rc |= make_map_rows(&tmq, q, (uint64_t)heads * D, q_rows, (uint64_t)ld_q);
