@@ -454,3 +454,42 @@ def test_attention_ring_pairs(d, causal):
         assert rel(host(dq_acc)[:, hh * d:(hh + 1) * d], dqr) < 1e-2
         assert rel(host(dkv_acc)[:, hh * d:(hh + 1) * d], dkr) < 1e-2
         assert rel(host(dkv_acc)[:, hq + hh * d:hq + (hh + 1) * d], dvr) < 1e-2
+
+
+_FWD_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2511_13198_b200 import binding as B
+s, heads, d, causal = int(sys.argv[3]), 3, 128, int(sys.argv[4])
+hq = heads * d
+g = torch.Generator().manual_seed(5)
+qkv = (torch.randn(s, 3 * hq, generator=g) * 0.5).to(torch.bfloat16).cuda()
+out = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+B.k_attn_fwd(qkv.data_ptr(), 3 * hq, s, heads, d, causal, out.data_ptr(), hq, lse.data_ptr(), 0)
+torch.cuda.synchronize()
+np.savez(sys.argv[2], out=out.view(torch.int16).cpu().numpy(), lse=lse.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("s,causal", [(640, 1), (1536, 1), (1024, 0)])
+def test_attention_fwd_pair_kernel_matches(tmp_path, s, causal):
+    """The opt-in CTA-pair forward (PDS_ATTN_FWD=pair, cta_group::2) computes every row with
+    the same softmax code and the same MMA shapes per row as the default single-CTA
+    forward: outputs and LSE agree (ragged pair of 512 rows included)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("1cta", "pair"):
+        f = tmp_path / f"{mode}.npz"
+        env = dict(os.environ)
+        env["PDS_ATTN_FWD"] = mode
+        subprocess.run([sys.executable, "-c", _FWD_SCRIPT, root, str(f), str(s), str(causal)], check=True, env=env,
+                       timeout=300)
+        res[mode] = np.load(f)
+    a = (res["1cta"]["out"].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    b = (res["pair"]["out"].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    assert rel(b, a) < 1e-3
+    assert np.allclose(res["pair"]["lse"], res["1cta"]["lse"], rtol=0, atol=1e-4)
