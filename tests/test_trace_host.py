@@ -88,3 +88,28 @@ def test_predicted_trace_adaptive_never_slower_than_a_static_strategy():
             for r in st["records"]:
                 if "seconds" in r:
                     assert t_ad[r["s"]] <= r["seconds"] * (1 + 1e-12), (P, name, r["s"])
+
+
+def test_planner_crossovers_at_p8():
+    """The selector's value at P = 8 (host-only context, committed P = 8 bundle, the
+    bundle's per-GPU capacity): short sequences run uniformly on the fastest strategy,
+    the 624K sequence (north_star) gets a feasible plan that must mix in a
+    memory-saving strategy (no static time-optimal plan fits), and the L = 32 frontier
+    of the adaptive plan exceeds every static strategy's."""
+    from paper_2511_13198_b200 import binding as B
+    model = B.Model(h=4096, n_heads=32, ffn=16384, n_layers=32)
+    path = os.path.join(os.path.dirname(T.__file__), "bundles", "h4096_n32_f16384_P8.txt")
+    ctx = B.Context(model, P=8, device=-1)
+    ctx.load_costs(path)
+    t_short = ctx.cost_eval(8192)[0]
+    plan, flags = ctx.plan(8192, 32)
+    assert not flags & B.PLAN_INFEASIBLE
+    assert len(set(plan)) == 1 and t_short[plan[0]] == min(t for i, t in enumerate(t_short) if i in set(plan) | {0})
+    plan, flags = ctx.plan(638976, 32)
+    assert not flags & B.PLAN_INFEASIBLE
+    assert set(plan) & {B.METP, B.METP_FULL}
+    ctx.close()
+    unit = 128 * 64
+    fr = {pi: T.predict_frontier(B, model, path, 32, unit, fixed=pi)["s"] for pi in range(B.N_STRATEGIES)}
+    ad = T.predict_frontier(B, model, path, 32, unit)["s"]
+    assert ad >= 638976 and all(ad >= v for v in fr.values())
