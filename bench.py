@@ -198,7 +198,18 @@ def main():
     have_bundle = os.path.exists(bundle)
     if have_bundle:
         ctx.load_costs(bundle)
-    ctx.reserve(max(args.seqs), (1 << B.N_STRATEGIES) - 1 if args.strategy < 0 else (1 << args.strategy))
+    # workspace for the strategies the runs will use (the plan of every s; ColossalZ's
+    # quadratic workspace at 32K alone would exceed the device)
+    if args.strategy >= 0:
+        mask = 1 << args.strategy
+    elif have_bundle:
+        mask = 0
+        for s in args.seqs:
+            for q in ctx.plan(s, L_STACK)[0]:
+                mask |= 1 << q
+    else:
+        mask = 1
+    ctx.reserve(max(args.seqs), mask)
 
     st = torch.cuda.current_stream()
     bufs = {}

@@ -365,8 +365,11 @@ if __name__ == "__main__":
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--ffn", type=int, default=16384)
     ap.add_argument("--L", type=int, default=32)
+    # four lengths per octave, 1K..64K, multiples of 256 (every strategy valid at P = 1):
+    # the random forest interpolates between profiled lengths only (Eq. 9), and with one
+    # point per octave its piecewise-constant predictions misranked near-equal strategies
     ap.add_argument("--grid", type=int, nargs="+",
-                    default=[1024, 2048, 4096, 8192, 16384, 32768, 65536])
+                    default=sorted({int(round(1024 * 2 ** (i / 4) / 256)) * 256 for i in range(25)}))
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--measured", action="store_true", help="P = WORLD_SIZE ranks under torchrun, over NCCL")
     ap.add_argument("--refit", action="store_true", help="re-fit the committed bundles from their stored records (CPU)")

@@ -290,7 +290,7 @@ def predict_main(a):
         bundle = os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt")
         # pad to a multiple every strategy accepts (R-15; METP's c = P waves of 128 rows:
         # 128 P^2), curriculum order
-        unit = 128 * P * P
+        unit = max(128 * P * P, 256 * P)
         real = sorted(int(x) for x in raw)
         lens = [int(pad_to(x, unit)) for x in real]
         meta = json.load(open(bundle + ".json"))
@@ -364,7 +364,8 @@ def main():
     pers = a.L * B.mem_bytes(model, P, 0, 1024)[2]
     cap = float(free) - a.reserve_gb * 2 ** 30 + pers
     lens = sample_lengths(a.dataset, a.n, seed=42)
-    lens = sorted(min(int(pad_to(int(x), 128 * P)), a.cap_s) for x in lens)   # curriculum
+    # pad to what every strategy accepts (R-15: 128 | s/P; MegatronCZ's zigzag: 128 | s/(2P))
+    lens = sorted(min(int(pad_to(int(x), 256 * P)), a.cap_s) for x in lens)   # curriculum
     out = {"dataset": a.dataset, "n": a.n, "L": a.L, "P": P, "lengths": lens, "capacity_for_plan": cap, "runs": {}}
 
     ALL = (1 << B.N_STRATEGIES) - 1
