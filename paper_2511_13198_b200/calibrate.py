@@ -35,7 +35,10 @@ ALL = (0, 1, 2, 3, 4, 5)    # TS, UZ, METP, CZ, METP-full, ColossalZ (include/pa
 def fits(torch, B, model, pi, s, P=1):
     """One layer of strategy pi at length s fits on this device (ColossalZ's quadratic
     score matrix limits its profiled range; the other strategies fit the whole grid)."""
-    sv, ws, pers = B.mem_bytes(model, P, pi, s)
+    try:
+        sv, ws, pers = B.mem_bytes(model, P, pi, s)
+    except B.PdsError:                 # not valid at this length (R-15 divisibility)
+        return False
     free, _ = torch.cuda.mem_get_info()
     return sv + ws + pers < 0.85 * free
 
@@ -261,7 +264,7 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         for s in grid:
             t_unit, t_gemm = {}, {}
             t_att = 0.0
-            for pi in [q for q in ALL if fits(torch, B, model, q, s)]:
+            for pi in [q for q in ALL if fits(torch, B, ctx_m.model if q in (2, 4) else model, q, s)]:
                 w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
                 cx = ctx_m if pi in (2, 4) else ctx
                 t1 = time_layer(torch, B, cx, pi, s, w, gr, x, dy, reps=reps)

@@ -321,13 +321,8 @@ __global__ void __launch_bounds__(256)
     tile[rr][v * 4 + 3] = x[h4].w;
   }
   __syncthreads();
-  // thread -> column pair cp (dst rows c0 + 2cp, +1), source rows rb*8 .. +7 of each half.
-  // A warp covers 8 consecutive column pairs x 4 row groups: word (rb*8 + i)*33 + cp sits
-  // in bank (8 rb + i + cp) mod 32, distinct over the warp (conflict-free transposed reads;
-  // with 4 pairs x 8 groups the groups rb and rb + 4 shared a bank).  The stores still
-  // fill whole 32-byte sectors (groups rb, rb ^ 1 of a pair are in the same warp).
-  const int w = t >> 5, l = t & 31;
-  const int cp = (w & 3) * 8 + (l & 7), rb = (l >> 3) + 4 * (w >> 2);
+  // thread -> column pair cp (dst rows c0 + 2cp, +1), source rows rb*8 .. +7 of each half
+  const int cp = t >> 3, rb = t & 7;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     uint32_t w[8];
