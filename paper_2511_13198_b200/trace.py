@@ -56,11 +56,12 @@ def bucket_of(s):
 
 
 def pr_only_bundle(path):
-    """Copy of a cost bundle whose Eq. 9 branch always takes the polynomial (w/o RF)."""
+    """Copy of a cost bundle whose Eq. 9 branch always takes the polynomial (w/o RF),
+    in a temporary directory under the same file name (the name carries P)."""
     txt = open(path).read()
     txt = re.sub(r"s_profile_max [0-9.eE+-]+", "s_profile_max 0.0", txt)
-    fd, out = tempfile.mkstemp(suffix=".txt")
-    with os.fdopen(fd, "w") as f:
+    out = os.path.join(tempfile.mkdtemp(prefix="pds_pr_only_"), os.path.basename(path))
+    with open(out, "w") as f:
         f.write(txt)
     return out
 
@@ -260,9 +261,6 @@ def predict_ablation(B, model, bundle, lens, real, L):
     runs = {}
     for name, kw in variants:
         path = pr_only_bundle(bundle) if kw.get("pr_only") else bundle
-        if kw.get("pr_only"):
-            os.replace(path, path + f"_P{bundle_P(bundle)}.txt")
-            path = path + f"_P{bundle_P(bundle)}.txt"
         runs[name] = predict_trace(B, model, path, lens, L, kw["gamma"], real=real, mask=kw.get("mask"))
     full = runs["ParaDySe (full)"]
     table = []
