@@ -166,10 +166,10 @@ def test_plan_sequence_vs_oracle(B, path, gamma):
     cap = hd["capacity"] - hd["reserve"]
     rng = np.random.default_rng(7 + P)
     q = max(P * P * 128, P * 256)         # lengths every strategy accepts (R-15: METP waves, CZ zigzag)
-    base = [int(v) // q * q + q for v in np.exp(rng.uniform(np.log(q), np.log(1.2e6 if P > 1 else 2.4e5), 120))]
+    base = [int(v) // q * q + q for v in np.exp(rng.uniform(np.log(q), np.log(3e6 if P > 1 else 2.4e5), 120))]
     # ascending (curriculum), then repeats, then a fine sweep down and up again (plans
     # flip back and forth between neighbouring lengths: smoothing's case)
-    fine = sorted({int(v) // q * q + q for v in np.geomspace(q, 1.2e6 if P > 1 else 2.4e5, 90)})
+    fine = sorted({int(v) // q * q + q for v in np.geomspace(q, 3e6 if P > 1 else 2.4e5, 90)})
     seq = sorted(base) + list(rng.choice(base, 60)) + fine[::-1] + fine
     all_mask = (1 << B.N_STRATEGIES) - 1
     masks = {0: all_mask, 90: all_mask & ~(1 << B.TS), 130: all_mask & ~(1 << B.METP), 180: all_mask}
