@@ -307,7 +307,8 @@ pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads,
 pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
                           const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                           int32_t causal, void* dqkv, void* stream);
-/* Context-parallel attention (MegatronCZ): the query rows [qlo, qlo + qn) of the s
+/* Query-row-range attention (a rank's rows of an all-gathered context; the layer's
+ * MegatronCZ uses the ring pairs below instead): the query rows [qlo, qlo + qn) of the s
  * positions of qkv [s][ld] against every key (causal: keys <= the query position).
  * out [qn][ld_out] and lse fp32 [heads][qn] hold the local rows.  Backward: from the
  * local out / lse / dout, dQ of rows [qlo, qlo + qn) and the dK / dV contributions of

@@ -357,34 +357,6 @@ struct Exec {
                             static_cast<float*>(lse) + bi * nl * sq, st), "attn_fwd"));
     return PDS_OK;
   }
-  // context parallelism (CZ): this rank's query rows [r s/P, (r+1) s/P) of all n heads
-  // against every key of the all-gathered qkv [s][3h]
-  double cz_fl(double mult) const {
-    const double q0 = (double)r * sp;
-    return b * mult * m.h * (m.causal ? sp * (q0 + 0.5 * sp) : (double)sp * sq);
-  }
-  pds_status attn_rows_f(const void* qkvg, void* out, void* lse) {
-    Prof p(c, st, K_ATTN_F, cz_fl(4.0), 0);
-    const int64_t n = m.n_heads;
-    for (int64_t bi = 0; bi < b; ++bi)
-      PDS_TRY(kerr(attn_fwd_rows(static_cast<const char*>(qkvg) + bi * 3 * h * 2, 3 * h * b, (int)sq, (int)n, (int)d,
-                                 m.causal, (int)(r * sp), (int)sp, static_cast<char*>(out) + bi * h * 2, h * b,
-                                 static_cast<float*>(lse) + bi * n * sp, st), "attn_fwd_rows"));
-    return PDS_OK;
-  }
-  pds_status attn_rows_b(const void* qkvg, const void* out, const void* lse, const void* dout, void* dqkvf,
-                         float* dd) {
-    Prof p(c, st, K_ATTN_B, cz_fl(10.0), 0);
-    const int64_t n = m.n_heads;
-    for (int64_t bi = 0; bi < b; ++bi)
-      PDS_TRY(kerr(attn_bwd_rows(static_cast<const char*>(qkvg) + bi * 3 * h * 2, 3 * h * b,
-                                 static_cast<const char*>(out) + bi * h * 2, h * b,
-                                 static_cast<const float*>(lse) + bi * n * sp,
-                                 static_cast<const char*>(dout) + bi * h * 2, (int)sq, (int)n, (int)d, m.causal,
-                                 (int)(r * sp), (int)sp, static_cast<char*>(dqkvf) + bi * 3 * h * 2, c->rope,
-                                 dd + bi * n * sp, st), "attn_bwd_rows"));
-    return PDS_OK;
-  }
   // sc: the fused backward's scratch (an fp32 dQ accumulator of sc_bytes >= nl sq d 4,
   // a workspace region that is free during the attention backward) and its counters;
   // NULL selects the split kernels
@@ -776,11 +748,10 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
 
 // ================================================================== MegatronCZ
 // Megatron-LM CP + ZeRO3 (reading R-CZ): ZeRO3 weight gathers
-// as in UlyssesZ, every GEMM local on the rank's s/P rows, the context-parallel
-// attention over the all-gathered Q/K/V for the rank's own query rows, and in backward
-// a reduce-scatter of the dQ/dK/dV partials.  W_qkv^T is gathered part by part (the
-// Q, K, V rows of every spec shard) into [Q all; K all; V all], so one attention
-// launch covers all heads; its gradient is reduce-scattered part by part back into
+// as in UlyssesZ, every GEMM local on the rank's s/P rows, and the context-parallel
+// attention as zigzag-balanced ring attention (below).  W_qkv^T is gathered part by
+// part (the Q, K, V rows of every spec shard) into [Q all; K all; V all], so the local
+// QKV GEMM yields all heads; its gradient is reduce-scattered part by part back into
 // the spec layout.
 pds_status cz_wqkv(Exec& e, const pds_weights* w, char* wqkv, cudaStream_t on) {
   for (int i = 0; i < 3; ++i)
