@@ -10,11 +10,21 @@ with the north_star additions read as DESIGN.md R-1..R-7:
   Eq. 3  O = A W_proj
   Eq. 4  Z = GELU(V2 W_in) W_out, exact erf GELU   (R-4)
 
+Llama variant (SURVEY §8(f) NEXT-3, the paper's LLaMA of Table 4, PAPER.md:317;
+readings R-GQA / R-SWIGLU of DESIGN.md):
+  GQA     n_kv key/value heads (n_kv | n); query head i attends with key/value
+          head i // (n / n_kv); w_qkv [h, (n + 2 n_kv) d] columns [Q | K | V]
+  SwiGLU  FFN(v) = (SiLU(v W_gate) * (v W_up)) W_down, SiLU(x) = x sigma(x);
+          w_in [h, 2F] columns [W_gate | W_up], w_out [F, h]
+
 Shapes (b = batch, the boundary layout [s, b, h] of Table 2 / R-10):
   x [s, b, h]; w_qkv [h, 3h] columns [Q | K | V], head i at columns i*d;
   w_proj [h, h]; w_in [h, F]; w_out [F, h]; g1, g2 [h].
 
 Pins (tests/test_oracle_layer.py): s = 1 => attention = V (SPEC.md:221);
+GQA = MHA with every key/value head repeated over its query group (forward, dx,
+and dW_k / dW_v = the group sums of the repeated copies); SwiGLU with W_up = 0
+=> Z = 0, torch fp64 autograd (F.silu, SDPA with enable_gqa);
 W_in = 0 => Z = 0; RoPE at t = 0 is the identity; naive
 triple-loop attention on s <= 4; torch.float64 autograd (an independent
 library routine) for every gradient; central finite differences.
@@ -77,6 +87,58 @@ def gelu_grad(x):
     """d GELU / dx = Phi(x) + x phi(x)."""
     phi = np.exp(-0.5 * x * x) / math.sqrt(2.0 * math.pi)
     return 0.5 * (1.0 + erf(x / math.sqrt(2.0))) + x * phi
+
+
+def silu(x):
+    """SiLU(x) = x sigma(x) (R-SWIGLU)."""
+    return x / (1.0 + np.exp(-x))
+
+
+def silu_grad(x):
+    """d SiLU / dx = sigma(x) (1 + x (1 - sigma(x)))."""
+    sg = 1.0 / (1.0 + np.exp(-x))
+    return sg * (1.0 + x * (1.0 - sg))
+
+
+IL = 64   # SwiGLU interleave of the spec layout (R-SWIGLU): gate block j, then up block j
+
+
+def _gate_up(hpre, il):
+    """Views of the gate and up pre-activations.  il=False: plain [gate | up] halves
+    (the unsharded w_in); il=True: the spec layout's blocks of IL columns
+    [gate_0 | up_0 | gate_1 | up_1 | ...] (every rank shard and every gather of them)."""
+    F2 = hpre.shape[-1]
+    if not il:
+        return hpre[..., :F2 // 2], hpre[..., F2 // 2:]
+    blk = hpre.reshape(hpre.shape[:-1] + (F2 // (2 * IL), 2, IL))
+    return blk[..., 0, :], blk[..., 1, :]
+
+
+def ffn_act(hpre, act="gelu", il=False):
+    """G = GELU(H) (Eq. 4), or SwiGLU's G = SiLU(H_gate) * H_up."""
+    if act == "gelu":
+        return gelu(hpre)
+    if act != "swiglu":
+        raise ValueError(act)
+    gate, up = _gate_up(hpre, il)
+    g = silu(gate) * up
+    return g.reshape(hpre.shape[:-1] + (hpre.shape[-1] // 2,))
+
+
+def ffn_act_bwd(dg, hpre, act="gelu", il=False):
+    """dH from dG: GELU'(H) dG, or SwiGLU's dH_gate = dG H_up SiLU'(H_gate),
+    dH_up = dG SiLU(H_gate), in the layout of hpre."""
+    if act == "gelu":
+        return dg * gelu_grad(hpre)
+    if act != "swiglu":
+        raise ValueError(act)
+    gate, up = _gate_up(hpre, il)
+    dgv = dg.reshape(gate.shape)
+    dh = np.empty_like(hpre)
+    dgate, dup = _gate_up(dh, il)
+    dgate[...] = dgv * up * silu_grad(gate)
+    dup[...] = dgv * silu(gate)
+    return dh
 
 
 def attention_fwd(q, k, v, causal=True, block=256):
@@ -142,15 +204,21 @@ def _merge_heads(m):
     return m.transpose(2, 0, 1, 3).reshape(s, b, n * d)
 
 
-def mha_core_fwd(qkv, n, positions, causal=True, theta=ROPE_THETA):
-    """RoPE + Eq. 2 on a [s, b, 3*hl] tensor laid out [Q | K | V] (n heads per
-    block, head i at columns i*d of each block).  Returns (A [s, b, hl] with
-    head i at columns i*d, LSE [b, n, s])."""
-    hl = qkv.shape[-1] // 3
-    d = hl // n
-    q = _split_heads(qkv[..., :hl], n)
-    k = _split_heads(qkv[..., hl:2 * hl], n)
-    v = _split_heads(qkv[..., 2 * hl:], n)
+def _qkv_split(qkv, n, n_kv):
+    """[s, b, (n + 2 n_kv) d] laid out [Q | K | V] -> heads [b, n|n_kv, s, d]."""
+    nk = n if n_kv is None else n_kv
+    d = qkv.shape[-1] // (n + 2 * nk)
+    hq, hk = n * d, nk * d
+    return (_split_heads(qkv[..., :hq], n), _split_heads(qkv[..., hq:hq + hk], nk),
+            _split_heads(qkv[..., hq + hk:], nk), nk, d)
+
+
+def mha_core_fwd(qkv, n, positions, causal=True, theta=ROPE_THETA, n_kv=None):
+    """RoPE + Eq. 2 on a [s, b, (n + 2 n_kv) d] tensor laid out [Q | K | V] (head i
+    at columns i*d of each block; n_kv = None: n, MHA).  Query head i uses key /
+    value head i // (n / n_kv) (GQA).  Returns (A [s, b, n d], LSE [b, n, s])."""
+    q, k, v, nk, d = _qkv_split(qkv, n, n_kv)
+    grp = n // nk
     cos, sin = rope_cos_sin(positions, d, theta)
     qr = rope_apply(q, cos, sin)
     kr = rope_apply(k, cos, sin)
@@ -158,47 +226,51 @@ def mha_core_fwd(qkv, n, positions, causal=True, theta=ROPE_THETA):
     lse = np.empty(q.shape[:3])
     for bi in range(q.shape[0]):
         for hi in range(n):
-            a[bi, hi], lse[bi, hi] = attention_fwd(qr[bi, hi], kr[bi, hi], v[bi, hi], causal)
+            a[bi, hi], lse[bi, hi] = attention_fwd(qr[bi, hi], kr[bi, hi // grp], v[bi, hi // grp], causal)
     return _merge_heads(a), lse
 
 
-def mha_core_bwd(da_m, qkv, a_m, lse, n, positions, causal=True, theta=ROPE_THETA):
+def mha_core_bwd(da_m, qkv, a_m, lse, n, positions, causal=True, theta=ROPE_THETA, n_kv=None):
     """Backward of mha_core_fwd from its saved inputs only (pre-RoPE qkv, the
-    attention output A and LSE): returns d[Q|K|V] [s, b, 3*hl] (pre-RoPE)."""
-    hl = qkv.shape[-1] // 3
-    d = hl // n
+    attention output A and LSE): returns d[Q|K|V] (pre-RoPE), the layout of qkv;
+    a key / value head's gradient sums over its query group."""
+    q, k, v, nk, d = _qkv_split(qkv, n, n_kv)
+    grp = n // nk
     cos, sin = rope_cos_sin(positions, d, theta)
-    qr = rope_apply(_split_heads(qkv[..., :hl], n), cos, sin)
-    kr = rope_apply(_split_heads(qkv[..., hl:2 * hl], n), cos, sin)
-    v = _split_heads(qkv[..., 2 * hl:], n)
+    qr = rope_apply(q, cos, sin)
+    kr = rope_apply(k, cos, sin)
     a = _split_heads(a_m, n)
     da = _split_heads(da_m, n)
     dq = np.empty_like(qr)
-    dk = np.empty_like(kr)
-    dv = np.empty_like(v)
+    dk = np.zeros_like(kr)
+    dv = np.zeros_like(v)
     for bi in range(qr.shape[0]):
         for hi in range(n):
-            dq[bi, hi], dk[bi, hi], dv[bi, hi] = attention_bwd(
-                qr[bi, hi], kr[bi, hi], v[bi, hi], a[bi, hi], lse[bi, hi], da[bi, hi], causal)
+            j = hi // grp
+            gq, gk, gv = attention_bwd(qr[bi, hi], kr[bi, j], v[bi, j], a[bi, hi], lse[bi, hi], da[bi, hi], causal)
+            dq[bi, hi] = gq
+            dk[bi, j] += gk
+            dv[bi, j] += gv
     dq = rope_apply_t(dq, cos, sin)
     dk = rope_apply_t(dk, cos, sin)
     return np.concatenate([_merge_heads(dq), _merge_heads(dk), _merge_heads(dv)], axis=-1)
 
 
 def layer_fwd(x, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True, eps=EPS,
-              theta=ROPE_THETA):
+              theta=ROPE_THETA, n_kv=None, act="gelu"):
     """O-1: one unsharded layer forward.  Returns (y, cache) where cache holds
-    every intermediate named in O-1 (O and Z are the sublayer deltas, R-34)."""
+    every intermediate named in O-1 (O and Z are the sublayer deltas, R-34).
+    n_kv / act: the Llama variant (GQA, SwiGLU with w_in = [W_gate | W_up])."""
     s = x.shape[0]
     pos = np.arange(s)
     u, xhat1, r1 = rmsnorm(x, g1, eps)
     qkv = u @ w_qkv                                       # Eq. 1
-    a, lse = mha_core_fwd(qkv, n, pos, causal, theta)  # RoPE + Eq. 2
+    a, lse = mha_core_fwd(qkv, n, pos, causal, theta, n_kv)  # RoPE + Eq. 2
     o = a @ w_proj                                        # Eq. 3
     x1 = x + o
     v2, xhat2, r2 = rmsnorm(x1, g2, eps)
     hpre = v2 @ w_in                                      # Eq. 4
-    g = gelu(hpre)
+    g = ffn_act(hpre, act)
     z = g @ w_out
     y = x1 + z
     cache = dict(u=u, xhat1=xhat1, r1=r1, qkv=qkv, a=a, lse=lse, o=o, x1=x1,
@@ -207,14 +279,14 @@ def layer_fwd(x, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True, eps=EPS,
 
 
 def layer_bwd(dy, cache, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True,
-              theta=ROPE_THETA):
+              theta=ROPE_THETA, n_kv=None, act="gelu"):
     """O-2: analytic VJP of layer_fwd.  Returns dict of dx and all weight grads."""
     c = cache
     # FFN (O-2 step 1)
     dz = dy
     dw_out = np.tensordot(c["g"], dz, axes=([0, 1], [0, 1]))
     dg = dz @ w_out.T
-    dh = dg * gelu_grad(c["h"])
+    dh = ffn_act_bwd(dg, c["h"], act)
     dw_in = np.tensordot(c["v2"], dh, axes=([0, 1], [0, 1]))
     dv2 = dh @ w_in.T
     # RMSNorm2 (step 2)
@@ -224,7 +296,7 @@ def layer_bwd(dy, cache, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True,
     dw_proj = np.tensordot(c["a"], dx1, axes=([0, 1], [0, 1]))
     da = dx1 @ w_proj.T
     # attention + RoPE (steps 4-5)
-    dqkv = mha_core_bwd(da, c["qkv"], c["a"], c["lse"], n, c["pos"], causal, theta)
+    dqkv = mha_core_bwd(da, c["qkv"], c["a"], c["lse"], n, c["pos"], causal, theta, n_kv)
     # QKV (step 6)
     dw_qkv = np.tensordot(c["u"], dqkv, axes=([0, 1], [0, 1]))
     du = dqkv @ w_qkv.T

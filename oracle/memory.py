@@ -13,6 +13,11 @@ this build reads M analytically (R-22, SURVEY O-6):
           COL  = 6u + (F/h)u + 2l + n (s/P) s b 2   ColossalZ (RSA): the probabilities instead of LSE
   plan    sum_l (W + saved_{pi_l}) + max_{pi in plan} workspace_pi + reserve < capacity (R-22)
 
+Llama variant (NEXT-3, R-GQA / R-SWIGLU; TS, UZ, METP, METP-full): the saved Q/K/V
+is (n + 2 n_kv)/n x 3u/3 = q u with q = (n + 2 n_kv)/n instead of 3u, the saved FFN
+pre-activation H is (2F/h) u ([gate | up]) instead of (F/h) u, and the weights are
+W = (q h^2 + h^2 + 3hF)/P (2 + 4) + 2h (2 + 4).
+
 Pins: the saved formula equals the simulated grid's ledger recount of the
 tensors the sharded simulations keep for backward (tests/test_oracle_strategies.py,
 SPEC.md:99); the C1 worked example of SURVEY O-6.  The transient (workspace) term
@@ -31,33 +36,44 @@ def units(h, n, s, P, b=1):
     return sl * b * h * 2, sl * b * 4, (n // P) * s * b * 4
 
 
-def persistent(h, ffn, P):
-    return (4 * h * h + 2 * h * ffn) // P * 6 + 2 * h * 6
+def persistent(h, ffn, P, n=None, n_kv=None, act="gelu"):
+    qkv = 3 * h * h if n is None or n_kv is None else (n + 2 * n_kv) * (h // n) * h
+    fc = (3 if act == "swiglu" else 2) * h * ffn
+    return (qkv + h * h + fc) // P * 6 + 2 * h * 6
 
 
-def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
+def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn", n_kv=None, act="gelu"):
     u, l, lam = units(h, n, s, P, b)
-    f = ffn // h
+    nk = n if n_kv is None else n_kv
+    if (nk != n or act != "gelu") and pi in (CZ, COL):
+        raise NotImplementedError("MegatronCZ / ColossalZ: MHA + GELU only")
+    qkv = (s // P) * b * (n + 2 * nk) * (h // n) * 2       # local Q | K | V rows (3u for MHA)
+    hb = (s // P) * b * (2 if act == "swiglu" else 1) * ffn * 2   # FFN pre-activation H
     if pi == TS or pi == CZ:           # CZ saves its local rows of the same tensors
-        return (6 + f) * u + 2 * l + lam
+        return 3 * u + qkv + hb + 2 * l + lam
     if pi == UZ:
-        return (7 + f) * u + 2 * l + lam
+        return 4 * u + qkv + hb + 2 * l + lam
     if pi == METP:
-        return (6 if metp_recompute == "ffn" else 3) * u + 2 * l + lam
+        return (3 * u + qkv if metp_recompute == "ffn" else 3 * u) + 2 * l + lam
     if pi == METP_FULL:
         return 3 * u + 2 * l + lam
     if pi == COL:                      # ColossalZ (R-COL): TS's tensors minus LSE, plus the
-        return (6 + f) * u + 2 * l + n * (s // P) * s * b * 2     # softmax probabilities [n, s/P, s] bf16
+        return 3 * u + qkv + hb + 2 * l + n * (s // P) * s * b * 2     # softmax probabilities [n, s/P, s] bf16
     raise KeyError(pi)
 
 
-def valid(pi, h, n, ffn, s, P, metp_chunks=None):
+def valid(pi, h, n, ffn, s, P, metp_chunks=None, n_kv=None, act="gelu"):
     """Reading R-15: the library runs a strategy at (s, P) only when
     P | s, P | n, 128 | s/P (tile rows), 64 | F/P, for METP / METP-full also
     c | s/P and 128 | s/(P c) (c = metp_chunks, default P), and for MegatronCZ
-    128 | s/(2P) (its zigzag half-chunks, R-CZ).  Never padded."""
+    128 | s/(2P) (its zigzag half-chunks, R-CZ); the Llama variant (GQA n_kv, SwiGLU)
+    needs P | n_kv, n_kv | n and runs on TS / UZ / METP / METP-full.  Never padded."""
     if s <= 0 or s % P or n % P or (s // P) % 128 or ffn % P or (ffn // P) % 64:
         return False
+    nk = n if n_kv is None else n_kv
+    if nk != n or act != "gelu":       # Llama variant: P | n_kv, n_kv | n; TS / UZ / METP only
+        if nk % P or n % nk or pi in (CZ, COL):
+            return False
     if pi in (METP, METP_FULL):
         c = metp_chunks or P
         sl = s // P
@@ -110,6 +126,7 @@ def transient_floor(pi, h, n, ffn, s, P, b=1, metp_chunks=None):
     raise KeyError(pi)
 
 
-def layer_bytes(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn"):
+def layer_bytes(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn", n_kv=None, act="gelu"):
     """M_pi(s) of Eq. 6 for one layer: persistent + saved."""
-    return persistent(h, ffn, P) + saved(pi, h, n, ffn, s, P, b, metp_recompute)
+    return (persistent(h, ffn, P, n, n if n_kv is None else n_kv, act)
+            + saved(pi, h, n, ffn, s, P, b, metp_recompute, n_kv, act))

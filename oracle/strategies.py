@@ -31,7 +31,7 @@ import copy
 
 import numpy as np
 
-from .layer import (EPS, ROPE_THETA, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
+from .layer import (EPS, ROPE_THETA, ffn_act, ffn_act_bwd, gelu, gelu_grad, mha_core_bwd, mha_core_fwd,
                     rmsnorm, rmsnorm_bwd, rope_apply, rope_apply_t, rope_cos_sin)
 
 TS, UZ, METP, CZ, METP_FULL, COL = 0, 1, 2, 3, 4, 5
@@ -41,8 +41,12 @@ NAMES = {TS: "MegatronTS", UZ: "UlyssesZ", METP: "METP", CZ: "MegatronCZ", METP_
 
 class Cfg:
     def __init__(self, h, n, ffn, causal=True, eps=EPS, theta=ROPE_THETA, metp_chunks=None,
-                 metp_recompute="ffn"):
+                 metp_recompute="ffn", n_kv=None, act="gelu"):
         self.h, self.n, self.ffn = h, n, ffn
+        # Llama variant (NEXT-3, R-GQA / R-SWIGLU): MegatronTS, UlyssesZ, METP and
+        # METP-full run it; MegatronCZ / ColossalZ are MHA + GELU only
+        self.n_kv = n if n_kv is None else n_kv
+        self.act = act
         self.causal, self.eps, self.theta = causal, eps, theta
         self.metp_chunks = metp_chunks
         if metp_recompute not in ("ffn", "full"):
@@ -63,6 +67,24 @@ def _release(grid, saved):
 def _apply_norm(x, r, g):
     """Recompute u = x r g from the saved input and rstd (no new statistics)."""
     return x * r[..., None] * g
+
+
+def _nkv_local(cfg, P):
+    return cfg.n_kv // P
+
+
+def _act(h, cfg):
+    """G of a spec-layout (interleaved for SwiGLU) FC1 output."""
+    return ffn_act(h, cfg.act, il=True)
+
+
+def _act_bwd(dg, h, cfg):
+    return ffn_act_bwd(dg, h, cfg.act, il=True)
+
+
+def _mha_only(cfg, who):
+    if cfg.n_kv != cfg.n or cfg.act != "gelu":
+        raise NotImplementedError(f"{who}: MHA + GELU only (the Llama variant runs on TS, UZ, METP)")
 
 
 def _zero_grads(W):
@@ -86,7 +108,7 @@ def ts_fwd(grid, xs, W, cfg):
         r1.append(rr)
     U = grid.all_gather(u)                                         # AG(u)
     qkv = [U[r] @ W["w_qkv_t"][r].T for r in range(P)]             # column-parallel Eq. 1
-    att = [mha_core_fwd(qkv[r], nl, pos, cfg.causal, cfg.theta) for r in range(P)]
+    att = [mha_core_fwd(qkv[r], nl, pos, cfg.causal, cfg.theta, _nkv_local(cfg, P)) for r in range(P)]
     opart = [att[r][0] @ W["w_proj"][r] for r in range(P)]        # row-parallel Eq. 3
     o = grid.reduce_scatter(opart)                                 # RS(o)
     x1 = [xs[r] + o[r] for r in range(P)]
@@ -97,7 +119,7 @@ def ts_fwd(grid, xs, W, cfg):
         r2.append(rr)
     V = grid.all_gather(v)                                         # AG(v)
     hpre = [V[r] @ W["w_in_t"][r].T for r in range(P)]
-    zpart = [gelu(hpre[r]) @ W["w_out"][r] for r in range(P)]
+    zpart = [_act(hpre[r], cfg) @ W["w_out"][r] for r in range(P)]
     z = grid.reduce_scatter(zpart)                                 # RS(z)
     y = [x1[r] + z[r] for r in range(P)]
     for r in range(P):
@@ -126,8 +148,8 @@ def ts_bwd(grid, dys, saved, W, cfg, grads):
     for r in range(P):
         hp = sv[r]["h"]
         dg = dZ[r] @ W["w_out"][r].T
-        dh = dg * gelu_grad(hp)
-        grads["dw_out"][r] += np.tensordot(gelu(hp), dZ[r], axes=([0, 1], [0, 1]))
+        dh = _act_bwd(dg, hp, cfg)
+        grads["dw_out"][r] += np.tensordot(_act(hp, cfg), dZ[r], axes=([0, 1], [0, 1]))
         grads["dw_in_t"][r] += np.tensordot(dh, V[r], axes=([0, 1], [0, 1]))
         dvpart.append(dh @ W["w_in_t"][r])
     dv = grid.reduce_scatter(dvpart)                               # RS(dv)
@@ -144,7 +166,7 @@ def ts_bwd(grid, dys, saved, W, cfg, grads):
         da = dX1[r] @ W["w_proj"][r].T
         grads["dw_proj"][r] += np.tensordot(sv[r]["a"], dX1[r], axes=([0, 1], [0, 1]))
         dqkv.append(mha_core_bwd(da, sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, pos,
-                                 cfg.causal, cfg.theta))
+                                 cfg.causal, cfg.theta, _nkv_local(cfg, P)))
     U = grid.all_gather(u)                                         # AG(u) re-gather
     dupart = []
     for r in range(P):
@@ -197,7 +219,8 @@ def uz_fwd(grid, xs, W, cfg):
         qkv_loc.append(ur @ Wf["w_qkv_t"][r].T)     # [s/P, b, 3h], head-group-major columns
     # A2A seq -> heads: send column block j (3h/P wide) to rank j, concat along s
     qkv = grid.all_to_all(qkv_loc, split_axis=2, concat_axis=0)
-    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta) for r in range(P)]
+    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta, _nkv_local(cfg, P))
+           for r in range(P)]
     # A2A heads -> seq: send row block j (s/P rows) to rank j, concat along columns
     afull = grid.all_to_all([att[r][0] for r in range(P)], split_axis=0, concat_axis=2)
     o = [afull[r] @ Wf["w_proj"][r] for r in range(P)]
@@ -206,7 +229,7 @@ def uz_fwd(grid, xs, W, cfg):
     for r in range(P):
         vr, _, rr = rmsnorm(x1[r], W["g2"][r], cfg.eps)
         hp = vr @ Wf["w_in_t"][r].T
-        zr = gelu(hp) @ Wf["w_out"][r]
+        zr = _act(hp, cfg) @ Wf["w_out"][r]
         z.append(zr)
         y.append(x1[r] + zr)
         sv = saved[r]
@@ -235,8 +258,8 @@ def uz_bwd(grid, dys, saved, W, cfg, grads):
         hp = sv[r]["h"]
         v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
         dg = dys[r] @ Wf["w_out"][r].T
-        dh = dg * gelu_grad(hp)
-        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dh = _act_bwd(dg, hp, cfg)
+        dwo.append(np.tensordot(_act(hp, cfg), dys[r], axes=([0, 1], [0, 1])))
         dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
         dv = dh @ Wf["w_in_t"][r]
         xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
@@ -248,7 +271,7 @@ def uz_bwd(grid, dys, saved, W, cfg, grads):
     # A2A(dO): seq -> heads (column block j to rank j)
     da = grid.all_to_all(dafull, split_axis=2, concat_axis=0)
     dqkv = [mha_core_bwd(da[r], sv[r]["qkv"], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
-                         cfg.causal, cfg.theta) for r in range(P)]
+                         cfg.causal, cfg.theta, _nkv_local(cfg, P)) for r in range(P)]
     # A2A(dQKV): heads -> seq (row block j to rank j, concat along columns)
     dqkv_loc = grid.all_to_all(dqkv, split_axis=0, concat_axis=2)
     dx, dg1 = [], []
@@ -295,7 +318,7 @@ def metp_fwd(grid, xs, W, cfg):
     c = metp_chunks(cfg, P)
     if sl % c:
         raise ValueError(f"s/P={sl} not divisible by metp_chunks={c} (SPEC.md:184)")
-    hq = 3 * cfg.h // P
+    hq = (cfg.n + 2 * cfg.n_kv) * (cfg.h // cfg.n) // P     # local Q | K | V columns
     b = xs[0].shape[1]
     saved = [dict() for _ in range(P)]
     u, r1 = [], []
@@ -311,7 +334,8 @@ def metp_fwd(grid, xs, W, cfg):
         for r in range(P):
             qkv[r][posw] = Uw[r] @ W["w_qkv_t"][r].T
     # attention over the full sequence (query-chunk x KV-chunk two-level loop)
-    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta) for r in range(P)]
+    att = [mha_core_fwd(qkv[r], nl, np.arange(s), cfg.causal, cfg.theta, _nkv_local(cfg, P))
+           for r in range(P)]
     o = [np.zeros_like(xs[r]) for r in range(P)]
     for k in range(c):
         rows = _wave_rows(sl, c, k)
@@ -329,7 +353,7 @@ def metp_fwd(grid, xs, W, cfg):
     for k in range(c):
         rows = _wave_rows(sl, c, k)
         Vw = grid.all_gather([v[r][rows] for r in range(P)])       # AG(v) wave k
-        zw = grid.reduce_scatter([gelu(Vw[r] @ W["w_in_t"][r].T) @ W["w_out"][r]
+        zw = grid.reduce_scatter([_act(Vw[r] @ W["w_in_t"][r].T, cfg) @ W["w_out"][r]
                                   for r in range(P)])             # RS(z) wave k
         for r in range(P):
             z[r][rows] = zw[r]
@@ -365,8 +389,8 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
         for r in range(P):
             hp = Vw[r] @ W["w_in_t"][r].T
             dg = dZw[r] @ W["w_out"][r].T
-            dh = dg * gelu_grad(hp)
-            grads["dw_out"][r] += np.tensordot(gelu(hp), dZw[r], axes=([0, 1], [0, 1]))
+            dh = _act_bwd(dg, hp, cfg)
+            grads["dw_out"][r] += np.tensordot(_act(hp, cfg), dZw[r], axes=([0, 1], [0, 1]))
             grads["dw_in_t"][r] += np.tensordot(dh, Vw[r], axes=([0, 1], [0, 1]))
             dvpart.append(dh @ W["w_in_t"][r])
         dvw = grid.reduce_scatter(dvpart)                          # RS(dv) wave k
@@ -386,7 +410,7 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
             da[r][posw] = dX1w[r] @ W["w_proj"][r].T
             grads["dw_proj"][r] += np.tensordot(sv[r]["a"][posw], dX1w[r], axes=([0, 1], [0, 1]))
     if cfg.metp_recompute == "full":   # QKV recompute: per wave AG(u) and the QKV GEMM again
-        qkv = [np.zeros((s, b, 3 * hl)) for _ in range(P)]
+        qkv = [np.zeros((s, b, (cfg.n + 2 * cfg.n_kv) * (cfg.h // cfg.n) // P)) for _ in range(P)]
         for k in range(c):
             rows = _wave_rows(sl, c, k)
             posw = _wave_positions(P, sl, c, k)
@@ -397,7 +421,7 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
     else:
         qkv = [sv[r]["qkv"] for r in range(P)]
     dqkv = [mha_core_bwd(da[r], qkv[r], sv[r]["a"], sv[r]["lse"], nl, np.arange(s),
-                         cfg.causal, cfg.theta) for r in range(P)]
+                         cfg.causal, cfg.theta, _nkv_local(cfg, P)) for r in range(P)]
     dx = [np.zeros_like(d) for d in dys]
     dg1 = [np.zeros(cfg.h) for _ in range(P)]
     for k in range(c):   # QKV backward per wave
@@ -548,6 +572,7 @@ def _pair_bwd(q, k, v, do, lse, D, pq, pk, causal):
 
 
 def cz_fwd(grid, xs, W, cfg):
+    _mha_only(cfg, "MegatronCZ")
     P = grid.p
     sl = xs[0].shape[0]
     s = sl * P
@@ -619,6 +644,7 @@ def cz_fwd(grid, xs, W, cfg):
 
 
 def cz_bwd(grid, dys, saved, W, cfg, grads):
+    _mha_only(cfg, "MegatronCZ")
     P = grid.p
     sl = dys[0].shape[0]
     h, n = cfg.h, cfg.n
@@ -731,6 +757,7 @@ def _ring_blocks(grid, blocks, bpe):
 
 
 def colossal_fwd(grid, xs, W, cfg):
+    _mha_only(cfg, "ColossalZ")
     P = grid.p
     sl = xs[0].shape[0]
     s = sl * P
@@ -795,6 +822,7 @@ def colossal_fwd(grid, xs, W, cfg):
 
 
 def colossal_bwd(grid, dys, saved, W, cfg, grads):
+    _mha_only(cfg, "ColossalZ")
     P = grid.p
     sl = dys[0].shape[0]
     h, n = cfg.h, cfg.n

@@ -70,20 +70,24 @@ TID = dict(x=1, w_qkv=2, w_proj=3, w_in=4, w_out=5, g1=6, g2=7, dy=8)
 
 
 def layer_inputs(h: int, n_heads: int, ffn: int, s: int, b: int = 1, seed: int = 42,
-                 layer: int = 0):
+                 layer: int = 0, n_kv: int | None = None, act: str = "gelu"):
     """Dense (unsharded) inputs of one layer in the oracle's orientation.
 
     Returns a dict of bf16-exact float64 arrays:
-      x [s, b, h]; w_qkv [h, 3h] (columns [Q | K | V], head i at i*d);
-      w_proj [h, h]; w_in [h, ffn]; w_out [ffn, h]; g1, g2 [h]; dy [s, b, h].
+      x [s, b, h]; w_qkv [h, (n + 2 n_kv) d] (columns [Q | K | V], head i at i*d;
+      n_kv = n_heads unless given: GQA); w_proj [h, h]; w_in [h, ffn] (SwiGLU:
+      [h, 2 ffn] = [W_gate | W_up]); w_out [ffn, h]; g1, g2 [h]; dy [s, b, h].
     """
     off = 16 * layer
     std_w = 1.0 / np.sqrt(h)
+    nk = n_heads if n_kv is None else n_kv
+    wq = (n_heads + 2 * nk) * (h // n_heads)
+    fin = 2 * ffn if act == "swiglu" else ffn
     return dict(
         x=normal(seed, TID["x"] + off, (s, b, h)),
-        w_qkv=normal(seed, TID["w_qkv"] + off, (h, 3 * h), std=std_w),
+        w_qkv=normal(seed, TID["w_qkv"] + off, (h, wq), std=std_w),
         w_proj=normal(seed, TID["w_proj"] + off, (h, h), std=std_w),
-        w_in=normal(seed, TID["w_in"] + off, (h, ffn), std=std_w),
+        w_in=normal(seed, TID["w_in"] + off, (h, fin), std=std_w),
         w_out=normal(seed, TID["w_out"] + off, (ffn, h), std=1.0 / np.sqrt(ffn)),
         g1=normal(seed, TID["g1"] + off, (h,), std=0.1, mean=1.0),
         g2=normal(seed, TID["g2"] + off, (h,), std=0.1, mean=1.0),

@@ -173,3 +173,126 @@ def test_layer_bwd_finite_differences():
             fd = (loss(dp) - loss(dm)) / (2 * eps)
             an = g[gkey][idx]
             assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (key, idx, fd, an)
+
+
+# ---------------------------------------------------------------- Llama variant (NEXT-3)
+def _llama_inputs(h=16, n=4, n_kv=2, ffn=128, s=9, b=1, seed=5):
+    return layer_inputs(h, n, ffn, s, b, seed=seed, n_kv=n_kv, act="swiglu")
+
+
+def _torch_llama(x, w_qkv, w_proj, w_in, w_out, g1, g2, n, n_kv, causal=True, eps=1e-5):
+    """Independent torch fp64 Llama block from library routines: F.rms_norm,
+    F.scaled_dot_product_attention(enable_gqa=True), F.silu (SwiGLU with
+    w_in = [W_gate | W_up])."""
+    import torch.nn.functional as F
+    s, b, h = x.shape
+    d = h // n
+    u = F.rms_norm(x, (h,), g1, eps=eps)
+    q, k, v = (u @ w_qkv).split([n * d, n_kv * d, n_kv * d], dim=-1)
+    def heads(t, m):
+        return t.reshape(s, b, m, d).permute(1, 2, 0, 3)
+    q, k, v = heads(q, n), heads(k, n_kv), heads(v, n_kv)
+    pos = torch.arange(s, dtype=torch.float64)
+    inv = 10000.0 ** (-2 * torch.arange(d // 2, dtype=torch.float64) / d)
+    ang = pos[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], -1)
+    sin = torch.cat([ang.sin(), ang.sin()], -1)
+    def rot(t):
+        t1, t2 = t[..., : d // 2], t[..., d // 2:]
+        return t * cos + torch.cat([-t2, t1], -1) * sin
+    a = F.scaled_dot_product_attention(rot(q), rot(k), v, is_causal=causal, enable_gqa=True)
+    x1 = x + a.permute(2, 0, 1, 3).reshape(s, b, h) @ w_proj
+    gate, up = (F.rms_norm(x1, (h,), g2, eps=eps) @ w_in).chunk(2, dim=-1)
+    return x1 + (F.silu(gate) * up) @ w_out
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("n_kv", [1, 2, 4])
+def test_llama_layer_vs_torch_autograd(causal, n_kv):
+    d = _llama_inputs(n_kv=n_kv, b=2)
+    kw = dict(n=4, causal=causal, n_kv=n_kv, act="swiglu")
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    g = L.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    names = ["x", "w_qkv", "w_proj", "w_in", "w_out", "g1", "g2"]
+    tt = {k: torch.tensor(d[k], dtype=torch.float64, requires_grad=True) for k in names}
+    yt = _torch_llama(*(tt[k] for k in names), n=4, n_kv=n_kv, causal=causal)
+    assert np.allclose(yt.detach().numpy(), y, rtol=1e-12, atol=1e-12)
+    yt.backward(torch.tensor(d["dy"]))
+    for k, gk in [("x", "dx"), ("w_qkv", "dw_qkv"), ("w_proj", "dw_proj"), ("w_in", "dw_in"),
+                  ("w_out", "dw_out"), ("g1", "dg1"), ("g2", "dg2")]:
+        ref = tt[k].grad.numpy()
+        err = np.linalg.norm(ref - g[gk]) / np.linalg.norm(ref)
+        assert err < 1e-12, (k, err)
+
+
+def test_gqa_equals_mha_with_repeated_kv_heads():
+    """GQA is MHA whose key / value heads are copies within each query group: the
+    forward and dx agree, dW_q agrees, and dW_k / dW_v are the group sums of the
+    MHA gradients of the copies (a wrong head mapping breaks all three)."""
+    h, n, n_kv = 32, 8, 2
+    d = layer_inputs(h, n, 64, 11, 1, seed=9, n_kv=n_kv)
+    dh = h // n
+    grp = n // n_kv
+    wq, wk, wv = np.split(d["w_qkv"], [n * dh, (n + n_kv) * dh], axis=1)
+    rep = lambda w: np.concatenate([w[:, (i // grp) * dh:(i // grp + 1) * dh] for i in range(n)], axis=1)
+    w_mha = np.concatenate([wq, rep(wk), rep(wv)], axis=1)
+    args = (d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"])
+    y1, c1 = L.layer_fwd(d["x"], d["w_qkv"], *args, n=n, n_kv=n_kv)
+    y2, c2 = L.layer_fwd(d["x"], w_mha, *args, n=n)
+    assert np.allclose(y1, y2, rtol=1e-13, atol=1e-13)
+    g1 = L.layer_bwd(d["dy"], c1, d["w_qkv"], *args, n=n, n_kv=n_kv)
+    g2 = L.layer_bwd(d["dy"], c2, w_mha, *args, n=n)
+    assert np.allclose(g1["dx"], g2["dx"], rtol=1e-12, atol=1e-12)
+    gq, gk, gv = np.split(g1["dw_qkv"], [n * dh, (n + n_kv) * dh], axis=1)
+    mq, mk, mv = np.split(g2["dw_qkv"], [n * dh, 2 * n * dh], axis=1)
+    assert np.allclose(gq, mq, rtol=1e-12, atol=1e-12)
+    for gg, mm in ((gk, mk), (gv, mv)):
+        for j in range(n_kv):
+            ref = sum(mm[:, i * dh:(i + 1) * dh] for i in range(j * grp, (j + 1) * grp))
+            assert np.allclose(gg[:, j * dh:(j + 1) * dh], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_swiglu_closed_forms():
+    x = np.linspace(-6, 6, 97)
+    # SiLU = x sigma(x): sigma(0) = 1/2, odd part; SiLU' by central differences
+    assert L.silu(np.array([0.0]))[0] == 0.0
+    assert np.allclose(L.silu(x) - L.silu(-x), x, rtol=0, atol=1e-15)
+    e = 1e-6
+    assert np.allclose(L.silu_grad(x), (L.silu(x + e) - L.silu(x - e)) / (2 * e), rtol=0, atol=1e-8)
+    # W_up = 0 => Z = 0 (the gate cannot leak through)
+    d = _llama_inputs()
+    F = d["w_out"].shape[0]
+    d["w_in"][:, F:] = 0.0
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"],
+                       n=4, n_kv=2, act="swiglu")
+    assert np.array_equal(c["z"], np.zeros_like(c["z"]))
+    # the interleaved spec layout and the plain halves give the same G and dH
+    from oracle.shard import il_perm
+    hp = np.random.default_rng(1).standard_normal((5, 2 * 128))
+    pm = il_perm(128)
+    assert np.array_equal(L.ffn_act(hp[:, pm], "swiglu", il=True), L.ffn_act(hp, "swiglu"))
+    dg = np.random.default_rng(2).standard_normal((5, 128))
+    assert np.array_equal(L.ffn_act_bwd(dg, hp[:, pm], "swiglu", il=True), L.ffn_act_bwd(dg, hp, "swiglu")[:, pm])
+
+
+def test_llama_finite_differences():
+    d = _llama_inputs(h=8, n=2, n_kv=1, ffn=64, s=5, seed=13)
+    args = dict(n=2, n_kv=1, act="swiglu")
+    def loss(dd):
+        y, _ = L.layer_fwd(dd["x"], dd["w_qkv"], dd["w_proj"], dd["w_in"], dd["w_out"], dd["g1"],
+                           dd["g2"], **args)
+        return float(np.sum(y * d["dy"]))
+    y, c = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **args)
+    g = L.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **args)
+    rng = np.random.default_rng(0)
+    eps = 1e-6
+    for key, gkey in [("x", "dx"), ("w_qkv", "dw_qkv"), ("w_in", "dw_in"), ("w_out", "dw_out")]:
+        for _ in range(3):
+            idx = tuple(rng.integers(0, n) for n in d[key].shape)
+            dp = {k: v.copy() for k, v in d.items()}
+            dm = {k: v.copy() for k, v in d.items()}
+            dp[key][idx] += eps
+            dm[key][idx] -= eps
+            fd = (loss(dp) - loss(dm)) / (2 * eps)
+            an = g[gkey][idx]
+            assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (key, idx, fd, an)

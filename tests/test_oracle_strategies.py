@@ -232,3 +232,49 @@ def test_metp_full_recompute_halves_saved_bytes():
         assert ffn - full == 3 * u
     with pytest.raises(ValueError):
         S.Cfg(H, N, F, metp_recompute="qkv")
+
+
+# ---------------------------------------------------------------- Llama variant (NEXT-3)
+@pytest.mark.parametrize("P,n_kv", [(1, 2), (2, 2), (2, 4), (4, 4)])
+@pytest.mark.parametrize("pi", [S.TS, S.UZ, S.METP, S.METP_FULL])
+def test_llama_variant_equals_unsharded(pi, P, n_kv):
+    """GQA (n_kv key/value heads) + SwiGLU (interleaved spec layout, R-SWIGLU): every
+    strategy that runs the variant reproduces the unsharded Llama layer, per-rank
+    gradient shards included, and its ledger equals the memory formula."""
+    s, ffn = 32, 256
+    d = layer_inputs(H, N, ffn, s, 2, seed=23, n_kv=n_kv, act="swiglu")
+    kw = dict(n=N, n_kv=n_kv, act="swiglu")
+    y_ref, c = layer.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    g_ref = layer.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    g = Grid(P)
+    cfg = S.Cfg(H, N, ffn, metp_chunks=2 if pi in (S.METP, S.METP_FULL) else None, n_kv=n_kv, act="swiglu")
+    W = shard.shard_weights(d, N, P, n_kv=n_kv, act="swiglu")
+    ys, saved, taps = S.layer_fwd(pi, g, shard.shard_act(d["x"], P), W, cfg)
+    for r in range(P):
+        assert g.live_bytes(r, "saved") == memory.saved(pi, H, N, ffn, s, P, b=2, n_kv=n_kv, act="swiglu")
+    grads = S.new_grads(W)
+    dxs = S.layer_bwd(pi, g, shard.shard_act(d["dy"], P), saved, W, cfg, grads)
+    assert _rel(shard.unshard_act(ys), y_ref) < 1e-12
+    assert _rel(shard.unshard_act(taps["z"]), c["z"]) < 1e-12
+    assert _rel(shard.unshard_act(dxs), g_ref["dx"]) < 1e-12
+    dense = shard.unshard_grads(grads, N, n_kv=n_kv, act="swiglu")
+    for k in ("dw_qkv", "dw_proj", "dw_in", "dw_out", "dg1", "dg2"):
+        assert _rel(dense[k], g_ref[k]) < 1e-12, k
+    ref_sh = shard.shard_weights(dict(w_qkv=g_ref["dw_qkv"], w_proj=g_ref["dw_proj"], w_in=g_ref["dw_in"],
+                                      w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), N, P,
+                                 n_kv=n_kv, act="swiglu")
+    for r in range(P):
+        assert _rel(grads["dw_qkv_t"][r], ref_sh["w_qkv_t"][r]) < 1e-12
+        assert _rel(grads["dw_in_t"][r], ref_sh["w_in_t"][r]) < 1e-12
+
+
+def test_llama_variant_rejected_by_cz_and_colossal():
+    d = layer_inputs(H, N, 256, 32, 1, seed=3, n_kv=2, act="swiglu")
+    cfg = S.Cfg(H, N, 256, n_kv=2, act="swiglu")
+    W = shard.shard_weights(d, N, 2, n_kv=2, act="swiglu")
+    for pi in (S.CZ, S.COL):
+        with pytest.raises(NotImplementedError):
+            S.layer_fwd(pi, Grid(2), shard.shard_act(d["x"], 2), W, cfg)
+        assert not memory.valid(pi, H, N, 256, 256, 2, n_kv=2, act="swiglu")
+    assert memory.valid(S.TS, H, N, 256, 256, 2, n_kv=2, act="swiglu")
+    assert not memory.valid(S.TS, H, N, 256, 512, 4, n_kv=2, act="swiglu")      # P does not divide n_kv
