@@ -26,6 +26,11 @@
  *                          then its K rows, then its V rows  ((3h/p x h)^T of Table 2)
  *       w_proj  [h/P, h]   rows [r h/P, (r+1) h/P) of W_proj
  *       w_in_t  [F/P, h]   rows [r F/P, (r+1) F/P) of W_in^T   ((4h/p x h)^T)
+     Llama variant: w_qkv_t [(n + 2 n_kv) d / P, h] = the Q rows of head group r, then
+       the K rows of KV group r (n_kv/P heads), then its V rows; SwiGLU w_in_t [2F/P, h]
+       = rows [r 2F/P, (r+1) 2F/P) of [W_gate | W_up]^T with its rows interleaved in
+       blocks of 64 (gate rows 64j..64j+63, then up rows 64j..64j+63), so every shard
+       and every row-wise gather holds whole (gate, up) pairs; 64 | F/P.
  *       w_out   [F/P, h]   rows [r F/P, (r+1) F/P) of W_out
  *       g1, g2  [h]        RMSNorm gains, replicated
  *   - Divisibility (P | s, P | n, 128 | s/P, metp_chunks | s/P) is a hard error
@@ -90,6 +95,13 @@ typedef struct {
                               intermediates (R-11); 1 = also Q/K/V (then
                               PDS_METP behaves as PDS_METP_FULL); else EINVAL.
                               PDS_METP_FULL always recomputes Q/K/V.          */
+  /* Llama variant (the paper's LLaMA, Table 4, PAPER.md:317;
+   * readings R-GQA / R-SWIGLU).  Runs on MegatronTS, UlyssesZ, METP and METP-full;
+   * MegatronCZ / ColossalZ return PDS_ENOTIMPL for it (the planner skips them). */
+  int32_t n_kv_heads;     /* key/value heads (GQA): 0 -> n_heads (MHA); must
+                              divide n_heads and be divisible by P           */
+  int32_t ffn_act;        /* 0 = GELU (Eq. 4), 1 = SwiGLU: FFN(v) = (SiLU(v W_gate)
+                              * (v W_up)) W_down with ffn = the width of W_down  */
 } pds_model;
 
 typedef struct pds_ctx pds_ctx;     /* opaque: rank, P, comm, streams, arenas, costs, plan cache */
@@ -307,6 +319,33 @@ pds_status pds_k_attn_fwd(const void* qkv, int64_t ld, int32_t s, int32_t heads,
 pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
                           const void* lse, const void* dout, int32_t s, int32_t heads, int32_t d,
                           int32_t causal, void* dqkv, void* stream);
+/* Llama variant (readings R-GQA / R-SWIGLU).
+ * GQA attention: qkv [s][ld] laid out [Q (heads*d) | K (kv_heads*d) | V (kv_heads*d)];
+ * query head i attends with key / value head i / (heads / kv_heads).  out [s][ld_out],
+ * lse fp32 [heads][s] as pds_k_attn_fwd; the backward writes dqkv in qkv's layout, a
+ * key / value head's gradient summed over its query group (split kernels; the dK/dV
+ * kernel walks the group's query heads in one TMEM accumulation).  kv_heads must
+ * divide heads (PDS_EINVAL otherwise); kv_heads = heads is pds_k_attn_fwd/bwd. */
+pds_status pds_k_attn_fwd_gqa(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t kv_heads,
+                              int32_t d, int32_t causal, void* out, int64_t ld_out, void* lse, void* stream);
+pds_status pds_k_attn_bwd_gqa(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                              const void* lse, const void* dout, int32_t s, int32_t heads, int32_t kv_heads,
+                              int32_t d, int32_t causal, void* dqkv, void* stream);
+/* SwiGLU GEMM epilogues.  bwd = 0 (FC1): C [M, N] bf16 = H = A B^T, whose columns are
+ * interleaved in 64-blocks [gate_j | up_j] (N % 128 == 0), and g_out [M, N/2] (row
+ * stride ld_g) = SiLU(bf16 gate) * bf16 up.  bwd = 1 (dG GEMM): the accumulator is dG
+ * [M, N] (N % 64 == 0); h_in = H [M, 2N] (row stride ld_h); C [M, 2N] = dH in H's
+ * layout (dgate = dG up SiLU'(gate), dup = dG SiLU(gate)); optional g_out [M, N] = G,
+ * c_t [2N][ld_t] = dH^T, g_t [N][ld_t] = G^T (the dW GEMMs' K-major operands).
+ * Device pointers; PDS_EINVAL on a missing buffer or a misaligned N. */
+pds_status pds_k_gemm_swiglu(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N,
+                             int32_t K, int32_t bwd, void* C, int64_t ldc, const void* h_in, int64_t ld_h,
+                             void* g_out, int64_t ld_g, void* c_t, void* g_t, int64_t ld_t, void* stream);
+/* QKV GEMM + RoPE with GQA column groups [Q (hq) | K (hk) | V (hk)] repeated every
+ * hq + 2 hk columns; row r at position r. */
+pds_status pds_k_gemm_rope_gqa(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                               int32_t N, int32_t K, void* C, int64_t ldc, const void* rope, int32_t d,
+                               int32_t hq, int32_t hk, void* stream);
 /* Query-row-range attention (a rank's rows of an all-gathered context; the layer's
  * MegatronCZ uses the ring pairs below instead): the query rows [qlo, qlo + qn) of the s
  * positions of qkv [s][ld] against every key (causal: keys <= the query position).

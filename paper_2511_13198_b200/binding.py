@@ -33,7 +33,8 @@ class PdsError(RuntimeError):
 class _Model(C.Structure):
     _fields_ = [("h", C.c_int32), ("n_heads", C.c_int32), ("ffn", C.c_int32), ("n_layers", C.c_int32),
                 ("batch", C.c_int32), ("norm_eps", C.c_float), ("rope_theta", C.c_double),
-                ("causal", C.c_int32), ("metp_chunks", C.c_int32), ("metp_recompute", C.c_int32)]
+                ("causal", C.c_int32), ("metp_chunks", C.c_int32), ("metp_recompute", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("ffn_act", C.c_int32)]
 
 
 class _Weights(C.Structure):
@@ -56,10 +57,13 @@ class Model:
     causal: int = 1
     metp_chunks: int = 0
     metp_recompute: int = 0
+    n_kv_heads: int = 0          # GQA key/value heads (0: n_heads)
+    ffn_act: int = 0             # 0 GELU, 1 SwiGLU (Llama variant)
 
     def c(self):
         return _Model(self.h, self.n_heads, self.ffn, self.n_layers, self.batch, self.norm_eps,
-                      self.rope_theta, self.causal, self.metp_chunks, self.metp_recompute)
+                      self.rope_theta, self.causal, self.metp_chunks, self.metp_recompute,
+                      self.n_kv_heads, self.ffn_act)
 
 
 @dataclass
@@ -156,6 +160,15 @@ _SIGS = {
     "pds_k_attn_merge": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                          C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p],
     "pds_k_attn_dot": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
+    "pds_k_attn_fwd_gqa": [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
+    "pds_k_attn_bwd_gqa": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32,
+                           C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p],
+    "pds_k_gemm_swiglu": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                          C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                          C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p],
+    "pds_k_gemm_rope_gqa": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                            C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p],
     "pds_last_error": [],
     "pds_version": [],
 }
@@ -353,6 +366,23 @@ def k_rmsnorm_bwd(du, x, rstd, g, dres, rows, h, dx, dg, stream=0):
 
 def k_attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, stream=0):
     call("pds_k_attn_fwd", qkv, ld, s, heads, d, causal, out, ld_out, lse, stream)
+
+
+def k_attn_fwd_gqa(qkv, ld, s, heads, kv_heads, d, causal, out, ld_out, lse, stream=0):
+    call("pds_k_attn_fwd_gqa", qkv, ld, s, heads, kv_heads, d, causal, out, ld_out, lse, stream)
+
+
+def k_attn_bwd_gqa(qkv, ld, out, ld_out, lse, dout, s, heads, kv_heads, d, causal, dqkv, stream=0):
+    call("pds_k_attn_bwd_gqa", qkv, ld, out, ld_out, lse, dout, s, heads, kv_heads, d, causal, dqkv, stream)
+
+
+def k_gemm_swiglu(A, lda, B, ldb, M, N, K, bwd, Cp, ldc, h_in=None, ld_h=0, g_out=None, ld_g=0, c_t=None,
+                  g_t=None, ld_t=0, stream=0):
+    call("pds_k_gemm_swiglu", A, lda, B, ldb, M, N, K, bwd, Cp, ldc, h_in, ld_h, g_out, ld_g, c_t, g_t, ld_t, stream)
+
+
+def k_gemm_rope_gqa(A, lda, B, ldb, M, N, K, Cp, ldc, rope, d, hq, hk, stream=0):
+    call("pds_k_gemm_rope_gqa", A, lda, B, ldb, M, N, K, Cp, ldc, rope, d, hq, hk, stream)
 
 
 def k_attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, stream=0):

@@ -147,6 +147,55 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
   return r;
 }
 
+extern "C" pds_status pds_k_attn_fwd_gqa(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t kv_heads,
+                                         int32_t d, int32_t causal, void* out, int64_t ld_out, void* lse,
+                                         void* stream) {
+  if (!qkv || !out || !lse) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  if (kv_heads <= 0 || heads % kv_heads) PDS_FAIL(PDS_EINVAL, "kv_heads must divide heads");
+  return rc2s(attn_fwd(qkv, ld, s, heads, d, causal, out, ld_out, lse, static_cast<cudaStream_t>(stream), kv_heads),
+              "pds_k_attn_fwd_gqa");
+}
+
+extern "C" pds_status pds_k_attn_bwd_gqa(const void* qkv, int64_t ld, const void* out, int64_t ld_out,
+                                         const void* lse, const void* dout, int32_t s, int32_t heads,
+                                         int32_t kv_heads, int32_t d, int32_t causal, void* dqkv, void* stream) {
+  if (!qkv || !out || !lse || !dout || !dqkv) PDS_FAIL(PDS_EINVAL, "NULL argument");
+  if (kv_heads <= 0 || heads % kv_heads) PDS_FAIL(PDS_EINVAL, "kv_heads must divide heads");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* dd = nullptr;
+  PDS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dd), (size_t)heads * s * 4, st));
+  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st, nullptr,
+                               nullptr, kv_heads), "pds_k_attn_bwd_gqa");
+  cudaFreeAsync(dd, st);
+  return r;
+}
+
+extern "C" pds_status pds_k_gemm_swiglu(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N,
+                                        int32_t K, int32_t bwd, void* C, int64_t ldc, const void* h_in,
+                                        int64_t ld_h, void* g_out, int64_t ld_g, void* c_t, void* g_t, int64_t ld_t,
+                                        void* stream) {
+  if (!A || !B || !C) PDS_FAIL(PDS_EINVAL, "NULL operand");
+  if (!bwd && !g_out) PDS_FAIL(PDS_EINVAL, "SwiGLU forward needs g_out");
+  if (bwd && !h_in) PDS_FAIL(PDS_EINVAL, "SwiGLU backward needs h_in");
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.epi = bwd ? EPI_DSWIGLU : EPI_SWIGLU;
+  g.aux_in = h_in; g.ld_aux_in = ld_h; g.aux_out = g_out; g.ld_aux = ld_g;
+  g.c_t = c_t; g.aux_t = g_t; g.ld_t = ld_t;
+  return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm_swiglu");
+}
+
+extern "C" pds_status pds_k_gemm_rope_gqa(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M,
+                                          int32_t N, int32_t K, void* C, int64_t ldc, const void* rope, int32_t d,
+                                          int32_t hq, int32_t hk, void* stream) {
+  if (!A || !B || !C || !rope) PDS_FAIL(PDS_EINVAL, "NULL operand");
+  if (hq <= 0 || hk <= 0 || N % (hq + 2 * hk)) PDS_FAIL(PDS_EINVAL, "N must be a multiple of hq + 2 hk");
+  GemmArgs g;
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.M = M; g.N = N; g.K = K; g.C = C; g.ldc = ldc;
+  g.epi = EPI_ROPE; g.rope = reinterpret_cast<const float2*>(rope); g.rope_d = d; g.rope_hq = hq; g.rope_hk = hk;
+  return rc2s(gemm_launch(g, static_cast<cudaStream_t>(stream)), "pds_k_gemm_rope_gqa");
+}
+
 extern "C" pds_status pds_k_attn_fwd_rows(const void* qkv, int64_t ld, int32_t s, int32_t heads, int32_t d,
                                           int32_t causal, int32_t qlo, int32_t qn, void* out, int64_t ld_out,
                                           void* lse, void* stream) {

@@ -174,7 +174,7 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmq, int s,
                        int heads, int causal, __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
-                       float scale_log2, int qlo, int qn, int kcol, int vcol) {
+                       float scale_log2, int qlo, int qn, int kcol, int vcol, int grp) {
   using C = Fwd2Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(384, 1)
   const int nqb = (qn + 255) / 256;
   const int qb = causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int head = blockIdx.y;
+  const int kvh = head / grp;           // GQA: the key / value head of this query head
   const int q0 = qlo + qb * 256;
   const int nkv = causal ? min(s, q0 + 256) / BN : s / BN;
 
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(384, 1)
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], kcol + head * D + a * 64, j * BN);
-          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], vcol + head * D + a * 64, j * BN);
+          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], kcol + kvh * D + a * 64, j * BN);
+          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], vcol + kvh * D + a * 64, j * BN);
         }
       }
     }
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                           const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                           int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2, int qlo,
-                          int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc) {
+                          int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc, int grp) {
   using C = BwdKV4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -831,13 +832,16 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   uint64_t* p_half = bar + 2 * NST + 6;   // first half of every warpgroup's P^T columns written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NST + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // GQA: CTA = (key block, key / value head); its grp query heads run one after the
+  // other through the same loop (iteration i = query head g = i / nqh, query block
+  // qstart + i % nqh), so dK / dV accumulate over the group in TMEM
   const int kb = blockIdx.x, head = blockIdx.y;
-  const int hq = heads * D;
   const int k0 = kb * 128;
   // only the query blocks of [qlo, qlo + qn) contribute (dO, LSE, D are local to them);
   // the launch covers only key blocks that have at least one
   const int qstart = max(causal ? kb : 0, qlo / 128);
-  const int nq = (qlo + qn) / 128 - qstart;
+  const int nqh = (qlo + qn) / 128 - qstart;
+  const int nq = nqh * grp;
   constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
 
   if (warp == 0 && lane == 0) {
@@ -873,15 +877,15 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tma_load_2d(sm + C::V_OFF + a * 16384, &tkv, kv_full, vcol + head * D + a * 64, k0);
       }
       for (int i = 0; i < nq; ++i) {
-        const int b = i % NST, q0 = (qstart + i) * 128;
+        const int b = i % NST, q0 = (qstart + i % nqh) * 128, qh = head * grp + i / nqh;
         if (i >= NST) mbar_wait(&q_empty[b], ((i / NST) - 1) & 1);
         mbar_arrive_expect_tx(&q_full[b], 2 * C::T + 1024);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::Q_OFF + b * C::T + a * 16384, &tq, &q_full[b], head * D + a * 64, q0);
-          tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &q_full[b], head * D + a * 64, q0 - qlo);
+          tma_load_2d(sm + C::Q_OFF + b * C::T + a * 16384, &tq, &q_full[b], qh * D + a * 64, q0);
+          tma_load_2d(sm + C::O_OFF + b * C::T + a * 16384, &tdo, &q_full[b], qh * D + a * 64, q0 - qlo);
         }
-        bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)head * qn + (q0 - qlo), 512, &q_full[b]);
-        bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)head * qn + (q0 - qlo), 512, &q_full[b]);
+        bulk_load(sm + C::L_OFF + b * 512, lse + (int64_t)qh * qn + (q0 - qlo), 512, &q_full[b]);
+        bulk_load(sm + C::L_OFF + (NST + b) * 512, Dd + (int64_t)qh * qn + (q0 - qlo), 512, &q_full[b]);
       }
     }
   } else if (warp == 1) {
@@ -974,7 +978,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       const int b = i % NST;
       const uint32_t lsm = smem_u32(sm + C::L_OFF + b * 512) + wg * CW * 4;
       const uint32_t dsm = smem_u32(sm + C::L_OFF + (NST + b) * 512) + wg * CW * 4;
-      const bool diag = causal && qstart + i == kb;     // the query block on the key block's diagonal
+      const bool diag = causal && qstart + i % nqh == kb;   // the query block on the key block's diagonal
       float p[CW];
       {
         uint32_t sr[CW / 32][32];
@@ -1098,8 +1102,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
         rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
-        store32_bf16(rowp + hq + c * 32, a);
-        store32_bf16(rowp + hq + c * 32 + D / 2, bb);
+        store32_bf16(rowp + kcol + c * 32, a);          // dK at kcol + head * D
+        store32_bf16(rowp + kcol + c * 32 + D / 2, bb);
       } else {
         const int c = task - D / 64;
         uint32_t r[32];
@@ -1108,7 +1112,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        store32_bf16(rowp + 2 * hq + c * 32, v);
+        store32_bf16(rowp + vcol + c * 32, v);          // dV at vcol + head * D
       }
     }
     }
@@ -1142,7 +1146,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                         int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
                         const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                         const float2* __restrict__ rope, float scale, float scale_log2, int qlo, int qn, int kcol,
-                        int vcol, int64_t ld_dq, float* __restrict__ acc, int64_t ld_acc) {
+                        int vcol, int64_t ld_dq, float* __restrict__ acc, int64_t ld_acc, int grp) {
   using C = BwdQ4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1194,8 +1198,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[b], 2 * C::T);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], kcol + head * D + a * 64, j * 128);
-          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], vcol + head * D + a * 64, j * 128);
+          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], kcol + (head / grp) * D + a * 64, j * 128);
+          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], vcol + (head / grp) * D + a * 64, j * 128);
         }
       }
     }
@@ -1961,11 +1965,11 @@ static int fwd_pair(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
 template <int D>
 static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     int s, int heads, int causal, void* out, int64_t ld_out, void* lse, int qlo, int qn,
-                    cudaStream_t st) {
-  if (D == 128 && fwd_pair_mode())
+                    cudaStream_t st, int grp = 1) {
+  if (D == 128 && fwd_pair_mode() && grp == 1)
     return fwd_pair(q, ld_q, q_rows, kv, ld_kv, kcol, vcol, s, heads, causal, out, ld_out, lse, qlo, qn, st);
   CUtensorMap tm, tmq;
-  int rc = make_map_rows(&tm, kv, (uint64_t)vcol + heads * D, (uint64_t)s, (uint64_t)ld_kv);
+  int rc = make_map_rows(&tm, kv, (uint64_t)vcol + heads / grp * D, (uint64_t)s, (uint64_t)ld_kv);
   rc |= make_map_rows(&tmq, q, (uint64_t)heads * D, q_rows, (uint64_t)ld_q);
   if (rc) return (int)cudaErrorInvalidValue;
   static bool once = false;
@@ -1976,17 +1980,22 @@ static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
   attn_fwd_tc_kernel<D><<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
       tm, tmq, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
-      scale_log2, qlo, qn, kcol, vcol);
+      scale_log2, qlo, qn, kcol, vcol, grp);
   return (int)cudaGetLastError();
 }
 
+// packed [Q (heads) | K (kv_heads) | V (kv_heads)] rows; kv_heads = 0: heads (MHA)
 int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-                void* lse, cudaStream_t st, int qlo, int qn) {
+                void* lse, cudaStream_t st, int qlo, int qn, int kv_heads) {
   if (qn < 0) qn = s;
-  if (s % 128 || (ld % 8) || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s) return (int)cudaErrorInvalidValue;
-  const int hq = heads * d;
-  if (d == 128) return fwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, 2 * hq, s, heads, causal, out, ld_out, lse, qlo, qn, st);
-  if (d == 64) return fwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, 2 * hq, s, heads, causal, out, ld_out, lse, qlo, qn, st);
+  if (kv_heads <= 0) kv_heads = heads;
+  if (s % 128 || (ld % 8) || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s || heads % kv_heads)
+    return (int)cudaErrorInvalidValue;
+  const int hq = heads * d, hk = kv_heads * d, grp = heads / kv_heads;
+  if (d == 128)
+    return fwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp);
+  if (d == 64)
+    return fwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp);
   return (int)cudaErrorInvalidValue;
 }
 
@@ -2016,9 +2025,9 @@ template <int D>
 static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     const void* dout, int64_t ld_out, const void* lse, const float* Dd, int s, int heads, int causal,
                     void* dqkv, int64_t ld, const void* rope, int qlo, int qn, float* dq_acc, int64_t ld_dqa,
-                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st) {
+                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int grp = 1) {
   CUtensorMap kv128, q128, do128;
-  int rc = make_map_rows(&kv128, kv, (uint64_t)vcol + heads * D, s, ld_kv, 128);
+  int rc = make_map_rows(&kv128, kv, (uint64_t)vcol + heads / grp * D, s, ld_kv, 128);
   rc |= make_map_rows(&q128, q, (uint64_t)heads * D, q_rows, ld_q, 128);
   rc |= make_map_rows(&do128, dout, (uint64_t)heads * D, qn, ld_out, 128);
   if (rc) return (int)cudaErrorInvalidValue;
@@ -2044,17 +2053,17 @@ static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
     // the Q map is the K/V map (same buffer, same box): only the column offset differs
     // causal: key blocks past the last local query get nothing (the caller zeroes them)
     const int nkb = causal ? (qlo + qn) / 128 : s / 128;
-    attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
+    attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads / grp), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
         kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
         reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2,
-        qlo, qn, kcol, vcol, dkv_acc, ld_dkva);
+        qlo, qn, kcol, vcol, dkv_acc, ld_dkva, grp);
   };
   auto dq = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
     attn_bwd_dq4_kernel<D, NW><<<dim3(qn / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(q), ld_q, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
         reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn, kcol, vcol, ld, dq_acc, ld_dqa);
+        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn, kcol, vcol, ld, dq_acc, ld_dqa, grp);
   };
   if (force == 2) dkdv(std::integral_constant<int, 2>{});
   else dkdv(std::integral_constant<int, 4>{});
@@ -2090,17 +2099,19 @@ int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_
 
 // dQ, dK, dV into dqkv (same [s][ld] layout as qkv); Dd = rowsum(dO o O) precomputed
 int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
-                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo, int qn) {
+                int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo, int qn,
+                int kv_heads) {
   if (qn < 0) qn = s;
-  if (s % 128 || ld % 8 || ld_out % 8 || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s)
+  if (kv_heads <= 0) kv_heads = heads;
+  if (s % 128 || ld % 8 || ld_out % 8 || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s || heads % kv_heads)
     return (int)cudaErrorInvalidValue;
-  const int hq = heads * d;
+  const int hq = heads * d, hk = kv_heads * d, grp = heads / kv_heads;
   if (d == 128)
-    return bwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, 2 * hq, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope,
-                         qlo, qn, nullptr, 0, nullptr, 0, st);
+    return bwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope,
+                         qlo, qn, nullptr, 0, nullptr, 0, st, grp);
   if (d == 64)
-    return bwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, 2 * hq, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope, qlo,
-                        qn, nullptr, 0, nullptr, 0, st);
+    return bwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope, qlo,
+                        qn, nullptr, 0, nullptr, 0, st, grp);
   return (int)cudaErrorInvalidValue;
 }
 

@@ -56,9 +56,9 @@ struct EpiParams {
   int64_t blk_stride;
   const __nv_bfloat16* aux_in;
   __nv_bfloat16* aux_out;
-  int64_t ld_aux;
+  int64_t ld_aux, ld_aux_in;
   const float2* rope;
-  int rope_d, rope_hq, rope_b;
+  int rope_d, rope_hq, rope_hk, rope_b;
   int64_t seg, seg_stride, seg_base;
   int64_t c_seg, c_stride, c_base;
   __nv_bfloat16* c_t;      // transposed copies (dGELU epilogue): [N][ld_t]
@@ -150,6 +150,8 @@ __device__ __forceinline__ float gelu_f(float x) {
 __device__ __forceinline__ float bf16_round(float x) {
   return __bfloat162float(__float2bfloat16_rn(x));
 }
+// SiLU(x) = x sigma(x) and sigma(x) (R-SWIGLU)
+__device__ __forceinline__ float sigmoid_f(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 __device__ __forceinline__ int rot_block(int mb, int mt, int rot) {
   return rot ? (mb + rot) % mt : mb;
@@ -246,8 +248,8 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
         const int c1 = n0 + hs + j0;
         if (row_ok && c1 < N) {
         float v1[32], v2[32];
-        const int within = (n0 + hs) % (3 * ep.rope_hq);
-        if (within < 2 * ep.rope_hq) {
+        const int within = (n0 + hs) % (ep.rope_hq + 2 * ep.rope_hk);
+        if (within < ep.rope_hq + ep.rope_hk) {
           const float2* cs = ep.rope + pos * d2 + j0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
@@ -269,6 +271,66 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
         }
         __syncwarp();
       }
+    }
+  } else if (ep.epi == EPI_SWIGLU) {
+    // each 128-column group of the tile is one (gate_j | up_j) pair of 64-column blocks
+    for (int g0 = 0; g0 < BN; g0 += 128) {
+      for (int cc = 0; cc < 64; cc += 32) {
+        uint32_t rg[32], ru[32];
+        tmem_ld32(tbase + g0 + cc, rg);
+        tmem_ld32(tbase + g0 + 64 + cc, ru);
+        tmem_ld_wait();
+        const int col = n0 + g0 + cc;
+        if (row_ok && col < N) {
+          float vg[32], vu[32], g[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            vg[i] = __uint_as_float(rg[i]);
+            vu[i] = __uint_as_float(ru[i]);
+            const float x = bf16_round(vg[i]);
+            g[i] = x * sigmoid_f(x) * bf16_round(vu[i]);
+          }
+          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C);
+          store_row32_bf16(C + out_offset(ep, row, col), vg, 32);
+          store_row32_bf16(C + out_offset(ep, row, col + 64), vu, 32);
+          store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + (n0 + g0) / 2 + cc, g, 32);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (ep.epi == EPI_DSWIGLU) {
+    for (int cc = 0; cc < BN; cc += 32) {
+      uint32_t r[32];
+      tmem_ld32(tbase + cc, r);
+      tmem_ld_wait();
+      const int col = n0 + cc;                           // FFN column of dG
+      if (row_ok && col < N) {
+        const int valid = min(32, N - col);
+        const int hc = (col >> 6) * 128 + (col & 63);    // its gate column in H / dH
+        float gt[32], up[32], dgt[32], dup[32], g[32];
+        const __nv_bfloat16* hrow = ep.aux_in + (int64_t)row * ep.ld_aux_in;
+        load_row32_bf16(hrow + hc, gt, valid);
+        load_row32_bf16(hrow + hc + 64, up, valid);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float dg = __uint_as_float(r[i]);
+          const float sg = sigmoid_f(gt[i]);
+          const float si = gt[i] * sg;
+          g[i] = si * up[i];
+          dup[i] = dg * si;
+          dgt[i] = dg * up[i] * sg * fmaf(gt[i], 1.0f - sg, 1.0f);
+        }
+        __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C);
+        store_row32_bf16(C + out_offset(ep, row, hc), dgt, valid);
+        store_row32_bf16(C + out_offset(ep, row, hc + 64), dup, valid);
+        if (ep.aux_out) store_row32_bf16(ep.aux_out + (int64_t)row * ep.ld_aux + col, g, valid);
+        if (ep.c_t) {
+          store_col32_bf16(ep.c_t, ep.ld_t, row, hc, dgt, valid);
+          store_col32_bf16(ep.c_t, ep.ld_t, row, hc + 64, dup, valid);
+        }
+        if (ep.aux_t) store_col32_bf16(ep.aux_t, ep.ld_t, row, col, g, valid);
+      }
+      __syncwarp();
     }
   } else {
     for (int cc = 0; cc < BN; cc += 32) {
@@ -743,10 +805,12 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.aux_in = reinterpret_cast<const __nv_bfloat16*>(g.aux_in);
   ep.aux_out = reinterpret_cast<__nv_bfloat16*>(g.aux_out);
   ep.ld_aux = g.ld_aux;
+  ep.ld_aux_in = g.ld_aux_in > 0 ? g.ld_aux_in : g.ld_aux;
   ep.c_t = reinterpret_cast<__nv_bfloat16*>(g.c_t);
   ep.aux_t = reinterpret_cast<__nv_bfloat16*>(g.aux_t);
   ep.ld_t = g.ld_t;
   ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq; ep.rope_b = g.rope_b > 0 ? g.rope_b : 1;
+  ep.rope_hk = g.rope_hk > 0 ? g.rope_hk : g.rope_hq;
   ep.seg = g.seg > 0 ? g.seg : (int64_t)1 << 40;
   ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;
   ep.c_seg = g.c_seg > 0 ? g.c_seg : (int64_t)1 << 40;
@@ -769,6 +833,11 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   const int64_t tiles256 = (int64_t)((g.M + BM - 1) / BM) * ((g.N + 255) / 256);
   bool use256 = (g.N % 256 == 0 || g.N > 1024) && tiles256 >= gemm_num_sms();
   if (g.epi == EPI_ROPE && (g.rope_d % 64 || 128 % g.rope_d)) return (int)cudaErrorInvalidValue;
+  if (g.epi == EPI_ROPE && g.rope_hk > 0 && g.rope_hk % g.rope_d) return (int)cudaErrorInvalidValue;
+  // SwiGLU: whole (gate, up) 64-column pairs per 128 output columns; no column blocking
+  if ((g.epi == EPI_SWIGLU || g.epi == EPI_DSWIGLU) && (g.blk_w || g.chunk_cols)) return (int)cudaErrorInvalidValue;
+  if (g.epi == EPI_SWIGLU && (g.N % 128 || !g.aux_out)) return (int)cudaErrorInvalidValue;
+  if (g.epi == EPI_DSWIGLU && (g.N % 64 || !g.aux_in)) return (int)cudaErrorInvalidValue;
   const int64_t pair_tiles = (int64_t)((g.M + 255) / 256) * ((g.N + 255) / 256);
   const bool pair_ok = pair_mode() && g.M >= 256 && (g.N % 256 == 0 || g.N > 1024) &&
                        pair_tiles >= gemm_num_sms() / 2 && (g.a_seg == 0 || g.a_seg % 128 == 0) &&

@@ -17,6 +17,12 @@ enum GemmEpi : int {
   EPI_GELU = 3,      // C bf16 = H = acc ; aux_out bf16 = GELU(bf16(H))
   EPI_DGELU = 4,     // aux_in = H (bf16): C bf16 = acc * GELU'(H) ; aux_out bf16 = GELU(H)
   EPI_ROPE = 5,      // C bf16 = acc with RoPE applied to the Q/K columns
+  // SwiGLU (Llama variant, R-SWIGLU): the FC1 output's columns are interleaved in
+  // blocks of 64, [gate_j | up_j] per 128 (N % 128 == 0, every tile holds whole pairs)
+  EPI_SWIGLU = 6,    // C bf16 = H = acc [M, N] ; aux_out bf16 [M, N/2] = SiLU(bf16 gate) * bf16 up
+  EPI_DSWIGLU = 7,   // acc = dG [M, N]; aux_in = H [M, 2N] (row stride ld_aux_in): C bf16 [M, 2N]
+                     // = dH (dgate = dG up SiLU'(gate), dup = dG SiLU(gate)) in H's layout;
+                     // aux_out [M, N] = G; c_t = dH^T [2N][ld_t]; aux_t = G^T [N][ld_t]
 };
 
 struct GemmArgs {
@@ -38,11 +44,14 @@ struct GemmArgs {
   const void* aux_in = nullptr;
   void* aux_out = nullptr;
   int64_t ld_aux = 0;
-  // RoPE: columns laid out in groups of 3*hq = [Q | K | V] (hq = heads * d);
+  int64_t ld_aux_in = 0;          // EPI_DSWIGLU: row stride of aux_in (0: ld_aux)
+  // RoPE: columns laid out in groups of hq + 2 hk = [Q | K | V] (hq = q heads * d,
+  // hk = kv heads * d; rope_hk = 0: hk = hq, MHA); the Q and K columns are rotated;
   // position of row r: ((r / seg) * seg_stride + seg_base + (r % seg)) / rope_b
   const float2* rope = nullptr;   // [positions][d/2] (cos, sin)
   int rope_d = 0;
   int rope_hq = 0;
+  int rope_hk = 0;
   int rope_b = 1;                 // rows per position (batch b, layout [s, b, h]): pos = mapped row / b
   int64_t seg = 0, seg_stride = 0, seg_base = 0;
   // Row remaps of the STORED matrices (seg = 0: identity): logical row r lives at

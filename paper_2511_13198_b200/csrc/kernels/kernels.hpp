@@ -6,13 +6,15 @@
 namespace pds {
 // clock64 timeline of one dQ-kernel CTA (trace builds, -DPDS_TRACE); -1 otherwise
 int attn_debug_trace(long long* host_out, int rows);
+// qkv rows packed [Q (heads) | K (kv_heads) | V (kv_heads)]; kv_heads = 0: heads (MHA),
+// else GQA with query head i on key / value head i / (heads / kv_heads)
 int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-             void* lse, cudaStream_t st);
+             void* lse, cudaStream_t st, int kv_heads = 0);
 // dqacc (heads * s * d fp32) and ctr (heads * s / 128 + 1 ints) select the fused
-// one-kernel backward (d = 128, causal); NULL keeps the split dK/dV + dQ kernels
+// one-kernel backward (d = 128, causal, MHA); NULL keeps the split dK/dV + dQ kernels
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
              int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st,
-             float* dqacc = nullptr, int* ctr = nullptr);
+             float* dqacc = nullptr, int* ctr = nullptr, int kv_heads = 0);
 bool attn_bwd_fused_applies(int d, int causal);
 void set_attn_bwd_mode(int mode);
 // context parallelism: queries [qlo, qlo + qn) against all s keys (attention.cu)

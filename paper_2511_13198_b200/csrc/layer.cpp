@@ -168,10 +168,24 @@ struct Exec {
   // s, sl: TOKEN ROWS (all / this rank) of the [s, b, h] layout = positions x b; every
   // GEMM, norm and collective counts rows.  sq, sp: positions (attention, RoPE).
   int64_t b, sq, sp, s, sl, h, F, nl, d, hl, Fl;
+  // Llama variant (R-GQA / R-SWIGLU): nkl local key/value heads, qw / qwf the local /
+  // full Q|K|V widths (3 hl / 3 h for MHA), f1w / f1wf the local / full FC1 output
+  // widths (Fl / F; 2 Fl / 2 F with SwiGLU's interleaved [gate | up])
+  int64_t nkl, qw, qwf, f1w, f1wf;
+  bool swi;
   Exec(pds_ctx* c_, cudaStream_t st_, int64_t s_)
       : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), b(c_->m.batch), sq(s_), sp(s_ / c_->P),
         s(s_ * c_->m.batch), sl(s_ / c_->P * c_->m.batch), h(c_->m.h), F(c_->m.ffn),
-        nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {}
+        nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {
+    nkl = (c_->m.n_kv_heads > 0 ? c_->m.n_kv_heads : c_->m.n_heads) / c_->P;
+    qw = (nl + 2 * nkl) * d;
+    qwf = qw * c_->P;
+    swi = c_->m.ffn_act == 1;
+    f1w = swi ? 2 * Fl : Fl;
+    f1wf = swi ? 2 * F : F;
+  }
+  int fc1_epi() const { return swi ? EPI_SWIGLU : EPI_GELU; }
+  int dfc1_epi() const { return swi ? EPI_DSWIGLU : EPI_DGELU; }
 
   // overlap settings armed for the next gemm() (ag_next / rs_arm / a2a_arm); a store
   // counter's running host target advances only once that GEMM has been launched, so
@@ -187,7 +201,7 @@ struct Exec {
     // dGELU add the bf16 aux streams)
     const double mn = (double)g.M * g.N;
     const double cb = g.epi == EPI_F32_ACC ? 8.0 : g.epi == EPI_F32 ? 4.0 : g.epi == EPI_GELU ? 4.0
-                    : g.epi == EPI_DGELU ? 6.0 : 2.0;
+                    : g.epi == EPI_DGELU ? 6.0 : g.epi == EPI_SWIGLU ? 3.0 : g.epi == EPI_DSWIGLU ? 12.0 : 2.0;
     if (has_nxt) {
       g.wait_flags = nxt.wait_flags; g.flag_epoch = nxt.flag_epoch; g.done_ctr = nxt.done_ctr;
       g.chunk_rows = nxt.chunk_rows; g.m_rot_rows = nxt.m_rot_rows; g.sm_reserve = nxt.sm_reserve;
@@ -324,7 +338,8 @@ struct Exec {
     g.epi = EPI_ROPE;
     g.rope = reinterpret_cast<const float2*>(c->rope);
     g.rope_d = (int)d;
-    g.rope_hq = (int)hq;
+    g.rope_hq = (int)hq;                 // local Q width; K / V columns: nkl heads each
+    g.rope_hk = (int)(nkl * d);
     g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
     g.rope_b = (int)b;                 // row -> position: the mapped row / b
     return g;
@@ -352,9 +367,9 @@ struct Exec {
     const double fl = b * 4.0 * nl * d * (m.causal ? 0.5 * sq * sq : (double)sq * sq);
     Prof p(c, st, K_ATTN_F, fl, 0);
     for (int64_t bi = 0; bi < b; ++bi)
-      PDS_TRY(kerr(attn_fwd(static_cast<const char*>(qkv) + bi * 3 * hl * 2, 3 * hl * b, (int)sq, (int)nl, (int)d,
+      PDS_TRY(kerr(attn_fwd(static_cast<const char*>(qkv) + bi * qw * 2, qw * b, (int)sq, (int)nl, (int)d,
                             m.causal, static_cast<char*>(out) + bi * hl * 2, hl * b,
-                            static_cast<float*>(lse) + bi * nl * sq, st), "attn_fwd"));
+                            static_cast<float*>(lse) + bi * nl * sq, st, (int)nkl), "attn_fwd"));
     return PDS_OK;
   }
   // sc: the fused backward's scratch (an fp32 dQ accumulator of sc_bytes >= nl sq d 4,
@@ -366,11 +381,11 @@ struct Exec {
     Prof p(c, st, K_ATTN_B, fl, 0);
     float* acc = sc && ctr && sc_bytes >= nl * sq * d * 4 ? static_cast<float*>(sc) : nullptr;
     for (int64_t bi = 0; bi < b; ++bi)
-      PDS_TRY(kerr(attn_bwd(static_cast<const char*>(qkv) + bi * 3 * hl * 2, 3 * hl * b,
+      PDS_TRY(kerr(attn_bwd(static_cast<const char*>(qkv) + bi * qw * 2, qw * b,
                             static_cast<const char*>(out) + bi * hl * 2, hl * b,
                             static_cast<const float*>(lse) + bi * nl * sq, static_cast<const char*>(dout) + bi * hl * 2,
-                            (int)sq, (int)nl, (int)d, m.causal, static_cast<char*>(dqkv) + bi * 3 * hl * 2, c->rope,
-                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr), "attn_bwd"));
+                            (int)sq, (int)nl, (int)d, m.causal, static_cast<char*>(dqkv) + bi * qw * 2, c->rope,
+                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr, (int)nkl), "attn_bwd"));
     return PDS_OK;
   }
   // collectives
@@ -509,7 +524,7 @@ pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   const int64_t n = e.sl * e.h;
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, gather + slot, sv->at("rstd1")));
   PDS_TRY(ov ? e.ag_next(gather, n) : e.ag(gather + slot, gather, n));                // AG(u)
-  PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, 3 * e.hl, e.h, sv->at("qkv"), 3 * e.hl),
+  PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, e.qw, e.h, sv->at("qkv"), e.qw),
                         e.hl, 0, 0, 0)));                                                // Eq. 1 + RoPE
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));                          // Eq. 2
   if (ov) PDS_TRY(e.rs_arm(e.h));
@@ -518,9 +533,9 @@ pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.tap(e.c->tap_o, partial + slot, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, partial + slot, w->g2, e.sl, sv->at("x1"), gather + slot, sv->at("rstd2")));
   PDS_TRY(ov ? e.ag_next(gather, n) : e.ag(gather + slot, gather, n));                // AG(v)
-  GemmArgs fc1 = Exec::G(gather, e.h, 0, w->w_in_t, e.h, 0, e.s, e.Fl, e.h, sv->at("h"), e.Fl, EPI_GELU);
+  GemmArgs fc1 = Exec::G(gather, e.h, 0, w->w_in_t, e.h, 0, e.s, e.f1w, e.h, sv->at("h"), e.f1w, e.fc1_epi());
   fc1.aux_out = f0; fc1.ld_aux = e.Fl;
-  PDS_TRY(e.gemm(fc1));                                                                 // Eq. 4 (GELU)
+  PDS_TRY(e.gemm(fc1));                                                                 // Eq. 4 (GELU / SwiGLU)
   if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(f0, e.Fl, w->w_out, e.h, e.s, e.h, e.Fl, partial, e.h));
   PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(z)
@@ -565,8 +580,8 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   if (!ov) PDS_TRY(e.ag(dy, gather, n));                                                // AG(dz)
   // dH (row-major, for dV) plus the two operands the dW GEMMs need K-major, straight
   // from the epilogue: dH^T into f0, G^T into ta (G itself is never stored)
-  GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.Fl, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.Fl;
+  GemmArgs dgel = Exec::G(gather, e.h, 0, w->w_out, e.h, 0, e.s, e.Fl, e.h, f1, e.f1w, e.dfc1_epi());
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.Fl; dgel.ld_aux_in = e.f1w;
   dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.s;
   PDS_TRY(e.gemm(dgel));                                                                // dH, dH^T, G^T
   PDS_TRY(tn.tr(gather, e.h, e.s, e.h, tn.tb));
@@ -578,7 +593,7 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(v) re-gather
   }
   PDS_TRY(tn.tr(g2, e.h, e.s, e.h, tn.tb));
-  PDS_TRY(tn.mm(f0, e.s, tn.tb, e.s, e.Fl, e.h, e.s, g->dw_in_t, e.h, EPI_F32_ACC));      // dW_in^T += dH^T V
+  PDS_TRY(tn.mm(f0, e.s, tn.tb, e.s, e.f1w, e.h, e.s, g->dw_in_t, e.h, EPI_F32_ACC));     // dW_in^T += dH^T V
   if (pre) {
     PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, g2 + slot));
     PDS_TRY(e.link(e.st, cs));
@@ -586,7 +601,7 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     ev_u = e.mark(cs);
   }
   if (ov) PDS_TRY(e.rs_arm(e.h));
-  PDS_TRY(tn.xw(f1, e.Fl, w->w_in_t, e.h, e.s, e.h, e.Fl, partial, e.h));               // dV = dH W_in^T
+  PDS_TRY(tn.xw(f1, e.f1w, w->w_in_t, e.h, e.s, e.h, e.f1w, partial, e.h));             // dV = dH W_in^T
   PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(dv)
   PDS_TRY(e.norm_bwd(partial + slot, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
   if (ov) {
@@ -605,9 +620,9 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, gather + slot));
     PDS_TRY(e.ag(gather + slot, gather, e.sl * e.h));                                 // AG(u) re-gather
   }
-  PDS_TRY(tn.dw(f0, 3 * e.hl, g2, e.h, e.s, 3 * e.hl, e.h, g->dw_qkv_t));               // dW_qkv^T += dQKV^T U
+  PDS_TRY(tn.dw(f0, e.qw, g2, e.h, e.s, e.qw, e.h, g->dw_qkv_t));                       // dW_qkv^T += dQKV^T U
   if (ov) PDS_TRY(e.rs_arm(e.h));
-  PDS_TRY(tn.xw(f0, 3 * e.hl, w->w_qkv_t, e.h, e.s, e.h, 3 * e.hl, partial, e.h));      // dU = dQKV W_qkv^T
+  PDS_TRY(tn.xw(f0, e.qw, w->w_qkv_t, e.h, e.s, e.h, e.qw, partial, e.h));              // dU = dQKV W_qkv^T
   PDS_TRY(ov ? e.rs_run(partial, gather, n) : e.rs(partial, partial + slot, n));        // RS(du)
   PDS_TRY(e.norm_bwd(partial + slot, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
@@ -621,10 +636,10 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
   PDS_TRY(e.link(e.st, cs));                 // gather buffers free (previous layer done with them)
-  PDS_TRY(e.ag(w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));
+  PDS_TRY(e.ag(w->w_qkv_t, ws + bp.ws_off("wqkv"), e.qw * e.h));
   PDS_TRY(e.ag_on(cs, w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
   cudaEvent_t ev_proj = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.f1w * e.h));
   PDS_TRY(e.ag_on(cs, w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h));
   cudaEvent_t ev_ffn = e.mark(cs);
   char* wqkv = ws + bp.ws_off("wqkv");
@@ -639,15 +654,15 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
   // local QKV for all heads, head-group-major columns, written straight into the A2A
   // send layout [P][s/P][3h/P]; RoPE at global positions r*s/P + t
-  GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, 3 * e.h, e.h, s1, 3 * e.hl), e.hl, 0, 0, e.r * e.sl);
-  q.blk_w = (int)(3 * e.hl);
-  q.blk_stride = e.sl * 3 * e.hl;
+  GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, e.qwf, e.h, s1, e.qw), e.hl, 0, 0, e.r * e.sl);
+  q.blk_w = (int)e.qw;
+  q.blk_stride = e.sl * e.qw;
   // P > 1: block j of the packed output leaves for rank j as soon as its tiles are stored
   const bool ov = e.overlap();
-  if (ov) PDS_TRY(e.a2a_arm(3 * e.hl));
+  if (ov) PDS_TRY(e.a2a_arm(e.qw));
   PDS_TRY(e.gemm(q));
-  PDS_TRY(ov ? e.a2a_run(s1, sv->at("qkv"), e.sl * 3 * e.hl)
-             : e.a2a(s1, sv->at("qkv"), e.sl * 3 * e.hl));                               // A2A seq -> heads
+  PDS_TRY(ov ? e.a2a_run(s1, sv->at("qkv"), e.sl * e.qw)
+             : e.a2a(s1, sv->at("qkv"), e.sl * e.qw));                                   // A2A seq -> heads
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));
   PDS_TRY(e.a2a(sv->at("a"), r1, e.sl * e.hl));                                        // A2A heads -> seq
   {
@@ -659,7 +674,7 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * e.h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), s1, sv->at("rstd2")));
   PDS_TRY(e.wait(e.st, ev_ffn));
-  GemmArgs fc1 = Exec::G(s1, e.h, 0, win, e.h, 0, e.sl, e.F, e.h, sv->at("h"), e.F, EPI_GELU);
+  GemmArgs fc1 = Exec::G(s1, e.h, 0, win, e.h, 0, e.sl, e.f1wf, e.h, sv->at("h"), e.f1wf, e.fc1_epi());
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
   PDS_TRY(tn.xw(f0, e.F, wout, e.h, e.sl, e.h, e.F, u1, e.h));                          // Z
@@ -681,11 +696,11 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   const cudaStream_t cs = e.side_stream();
   PDS_TRY(e.link(e.st, cs));
   PDS_TRY(e.ag(w->w_out, ws + bp.ws_off("wout"), e.Fl * e.h));
-  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.Fl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, ws + bp.ws_off("win"), e.f1w * e.h));
   cudaEvent_t ev_in = e.mark(cs);
   PDS_TRY(e.ag_on(cs, w->w_proj, ws + bp.ws_off("wproj"), e.hl * e.h));
   cudaEvent_t ev_proj = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_qkv_t, ws + bp.ws_off("wqkv"), 3 * e.hl * e.h));
+  PDS_TRY(e.ag_on(cs, w->w_qkv_t, ws + bp.ws_off("wqkv"), e.qw * e.h));
   cudaEvent_t ev_qkv = e.mark(cs);
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
@@ -705,8 +720,8 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   float* dgl = reinterpret_cast<float*>(ws + bp.ws_off("dgl"));
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
-  GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.F, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  GemmArgs dgel = Exec::G(dy, e.h, 0, wout, e.h, 0, e.sl, e.F, e.h, f1, e.f1wf, e.dfc1_epi());
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F; dgel.ld_aux_in = e.f1wf;
   dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;                                 // G^T, dH^T
   PDS_TRY(e.gemm(dgel));
   PDS_TRY(tn.tr(dy, e.h, e.sl, e.h, tn.tb));
@@ -714,10 +729,10 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
   PDS_TRY(tn.tr(u1, e.h, e.sl, e.h, tn.tb));
-  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, e.h, e.sl, dw, e.h, EPI_F32));              // dW_in^T (full, local)
-  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.f1wf, e.h, e.sl, dw, e.h, EPI_F32));           // dW_in^T (full, local)
+  PDS_TRY(uz_dw(e, dw, e.f1wf, g->dw_in_t));
   PDS_TRY(e.wait(e.st, ev_in));
-  PDS_TRY(tn.xw(f1, e.F, win, e.h, e.sl, e.h, e.F, v2, e.h));
+  PDS_TRY(tn.xw(f1, e.f1wf, win, e.h, e.sl, e.h, e.f1wf, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + e.h));
   PDS_TRY(e.wait(e.st, ev_proj));
   GemmArgs dafull = Exec::G(dx, e.h, 0, wproj, e.h, 0, e.sl, e.h, e.h, s1, e.hl);
@@ -732,16 +747,16 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   if (!ov) PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                         // A2A(dO)
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), r1, x3, dd, tn.ta, bp.ws_size("ta"),
                    reinterpret_cast<int*>(ws + bp.ws_off("actr"))));
-  PDS_TRY(e.a2a(x3, r1, e.sl * 3 * e.hl));                                             // A2A(dQKV)
+  PDS_TRY(e.a2a(x3, r1, e.sl * e.qw));                                                 // A2A(dQKV)
   {
-    Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * 3 * e.h);
-    PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, 3 * e.hl, x4, 3 * e.h, e.st), "unpack"));
+    Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * e.qwf);
+    PDS_TRY(kerr(unpack_blocks(r1, e.P, e.sl, e.qw, x4, e.qwf, e.st), "unpack"));
   }
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
-  PDS_TRY(tn.dw(x4, 3 * e.h, u1, e.h, e.sl, 3 * e.h, e.h, dw, EPI_F32));
-  PDS_TRY(uz_dw(e, dw, 3 * e.h, g->dw_qkv_t));
+  PDS_TRY(tn.dw(x4, e.qwf, u1, e.h, e.sl, e.qwf, e.h, dw, EPI_F32));
+  PDS_TRY(uz_dw(e, dw, e.qwf, g->dw_qkv_t));
   PDS_TRY(e.wait(e.st, ev_qkv));
-  PDS_TRY(tn.xw(x4, 3 * e.h, wqkv, e.h, e.sl, e.h, 3 * e.h, v2, e.h));
+  PDS_TRY(tn.xw(x4, e.qwf, wqkv, e.h, e.sl, e.h, e.qwf, v2, e.h));
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -1281,7 +1296,7 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   };
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, ul, sv->at("rstd1")));
   PDS_TRY(waves(ul, [&](int64_t k, char* buf) -> pds_status {   // QKV waves: rows land at global positions
-    GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, qkv, 3 * e.hl),
+    GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, e.qw, e.h, qkv, e.qw),
                         e.hl, wr, e.sl, k * wr);
     q.c_seg = wr; q.c_stride = e.sl; q.c_base = k * wr;
     return e.gemm(q);
@@ -1303,7 +1318,7 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   }
   PDS_TRY(tn.tr(w->w_out, e.h, e.Fl, e.h, wt));                  // W_out^T, reused by every wave
   return waves(vl, [&](int64_t k, char* buf) -> pds_status {     // FFN waves
-    GemmArgs fc1 = Exec::G(buf, e.h, 0, w->w_in_t, e.h, 0, W, e.Fl, e.h, hw, e.Fl, EPI_GELU);
+    GemmArgs fc1 = Exec::G(buf, e.h, 0, w->w_in_t, e.h, 0, W, e.f1w, e.h, hw, e.f1w, e.fc1_epi());
     fc1.aux_out = gw; fc1.ld_aux = e.Fl;
     PDS_TRY(e.gemm(fc1));
     if (ov) PDS_TRY(e.rs_arm(e.h, wr));
@@ -1340,31 +1355,31 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
   char* dxb = static_cast<char*>(dx);
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * e.h * 4, e.st));
   const bool ov = e.overlap();       // P > 1: wave AG / RS overlapped with the wave GEMMs' tiles
-  PDS_TRY(tn.tr(w->w_in_t, e.h, e.Fl, e.h, wt));                 // W_in (= (W_in^T)^T) for dV, every wave
+  PDS_TRY(tn.tr(w->w_in_t, e.h, e.f1w, e.h, wt));                // W_in (= (W_in^T)^T) for dV, every wave
   for (int64_t k = 0; k < c; ++k) {   // FFN backward waves, recomputing v, H, G
     const int64_t o = k * wr;
     PDS_TRY(e.apply(sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, wr, vl));
     if (ov) {                          // tile-overlapped wave gathers (§7)
       PDS_CUDA(cudaMemcpyAsync(wg2 + slot, vl, wr * row, cudaMemcpyDeviceToDevice, e.st));
       PDS_TRY(e.ag_next(wg2, wr * e.h, wr));                                             // AG(v)
-      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                 // H recompute
+      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.f1w, e.h, hw, e.f1w));               // H recompute
       PDS_CUDA(cudaMemcpyAsync(wg + slot, dyb + o * row, wr * row, cudaMemcpyDeviceToDevice, e.st));
       PDS_TRY(e.ag_next(wg, wr * e.h, wr));                                              // AG(dz)
     } else {
       PDS_TRY(e.ag(dyb + o * row, wg, wr * e.h));                                       // AG(dz)
       PDS_TRY(e.ag(vl, wg2, wr * e.h));                                                  // AG(v)
-      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.Fl, e.h, hw, e.Fl));                 // H recompute
+      PDS_TRY(tn.mm(wg2, e.h, w->w_in_t, e.h, W, e.f1w, e.h, hw, e.f1w));               // H recompute
     }
-    GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.Fl, EPI_DGELU);
-    dgel.aux_in = hw; dgel.ld_aux = e.Fl;
+    GemmArgs dgel = Exec::G(wg, e.h, 0, w->w_out, e.h, 0, W, e.Fl, e.h, dhw, e.f1w, e.dfc1_epi());
+    dgel.aux_in = hw; dgel.ld_aux = e.Fl; dgel.ld_aux_in = e.f1w;
     dgel.aux_t = tn.ta; dgel.c_t = gw; dgel.ld_t = W;                                  // G^T, dH^T
     PDS_TRY(e.gemm(dgel));
     PDS_TRY(tn.tr(wg, e.h, W, e.h, tn.tb));
     PDS_TRY(tn.mm(tn.ta, W, tn.tb, W, e.Fl, e.h, W, g->dw_out, e.h, EPI_F32_ACC));      // dW_out += G^T dZ
     PDS_TRY(tn.tr(wg2, e.h, W, e.h, tn.tb));
-    PDS_TRY(tn.mm(gw, W, tn.tb, W, e.Fl, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC));        // dW_in^T += dH^T V
+    PDS_TRY(tn.mm(gw, W, tn.tb, W, e.f1w, e.h, W, g->dw_in_t, e.h, EPI_F32_ACC));       // dW_in^T += dH^T V
     if (ov) PDS_TRY(e.rs_arm(e.h, wr));
-    PDS_TRY(tn.mm(dhw, e.Fl, wt, e.Fl, W, e.h, e.Fl, pw, e.h));
+    PDS_TRY(tn.mm(dhw, e.f1w, wt, e.f1w, W, e.h, e.f1w, pw, e.h));
     PDS_TRY(ov ? e.rs_run(pw, wg, wr * e.h) : e.rs(pw, pw + slot, wr * e.h));            // RS(dv)
     PDS_TRY(e.norm_bwd(pw + slot, sv->at("x1") + o * row, sv->at("rstd2") + o * 4, w->g2, dyb + o * row, wr,
                        dxb + o * row, dgp, dgl + e.h));
@@ -1388,7 +1403,7 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
       const int64_t o = k * wr;
       PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
       PDS_TRY(e.ag(ul, wg, wr * e.h));                                                   // AG(u) recompute
-      GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, 3 * e.hl, e.h, qkv, 3 * e.hl),
+      GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, e.qw, e.h, qkv, e.qw),
                           e.hl, wr, e.sl, o);
       q.c_seg = wr; q.c_stride = e.sl; q.c_base = o;
       PDS_TRY(e.gemm(q));
@@ -1398,13 +1413,13 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
   const int64_t ulv = bp.ws_off("vl") == bp.ws_off("ul") + bp.ws_size("ul") ? 2 * bp.ws_size("ul") : bp.ws_size("ul");
   PDS_TRY(e.attn_b(qkv, sv->at("a"), sv->at("lse"), da, dqkv, dd, ul, ulv,
                    reinterpret_cast<int*>(ws + bp.ws_off("actr"))));
-  PDS_TRY(tn.tr(w->w_qkv_t, e.h, 3 * e.hl, e.h, wt));            // W_qkv for dU, every wave
+  PDS_TRY(tn.tr(w->w_qkv_t, e.h, e.qw, e.h, wt));                // W_qkv for dU, every wave
   for (int64_t k = 0; k < c; ++k) {   // QKV backward waves
     const int64_t o = k * wr;
     PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
     PDS_TRY(e.ag(ul, wg, wr * e.h));                                                     // AG(u)
-    PDS_TRY(tn.dw(dqkv, 3 * e.hl, wg, e.h, W, 3 * e.hl, e.h, g->dw_qkv_t, EPI_F32_ACC, wr, e.sl, o));
-    GemmArgs du = Exec::G(dqkv, 3 * e.hl, 0, wt, 3 * e.hl, 0, W, e.h, 3 * e.hl, pw, e.h);
+    PDS_TRY(tn.dw(dqkv, e.qw, wg, e.h, W, e.qw, e.h, g->dw_qkv_t, EPI_F32_ACC, wr, e.sl, o));
+    GemmArgs du = Exec::G(dqkv, e.qw, 0, wt, e.qw, 0, W, e.h, e.qw, pw, e.h);
     du.a_seg = wr; du.a_stride = e.sl; du.a_base = o; du.a_rows = e.s;
     if (ov) PDS_TRY(e.rs_arm(e.h, wr));
     PDS_TRY(e.gemm(du));

@@ -212,7 +212,10 @@ static void push(std::vector<Region>& v, int64_t& tot, const char* n, int64_t by
 
 int64_t persistent_bytes(const pds_model& m, int P) {
   const int64_t h = m.h, F = m.ffn;
-  return (4 * h * h + 2 * h * F) / P * (2 + 4) + 2 * h * (2 + 4);
+  const int64_t nk = m.n_kv_heads > 0 ? m.n_kv_heads : m.n_heads;
+  const int64_t qkv = (m.n_heads + 2 * nk) * (h / m.n_heads) * h;     // 3h^2 for MHA
+  const int64_t fc = (m.ffn_act == 1 ? 3 : 2) * h * F;                 // SwiGLU: gate, up, down
+  return (qkv + h * h + fc) / P * (2 + 4) + 2 * h * (2 + 4);
 }
 
 pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan* out) {
@@ -226,9 +229,21 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   if (s <= 0 || s % P) PDS_FAIL(PDS_EDIVISIBILITY, "seq_len=" + std::to_string(s) + " not divisible by P=" + std::to_string(P));
   if (m.n_heads % P) PDS_FAIL(PDS_EDIVISIBILITY, "n_heads=" + std::to_string(m.n_heads) + " not divisible by P=" + std::to_string(P));
   if (m.ffn % P || (m.ffn / P) % 64) PDS_FAIL(PDS_EDIVISIBILITY, "ffn/P must be a multiple of 64");
+  // Llama variant (R-GQA / R-SWIGLU)
+  const int64_t nk = m.n_kv_heads > 0 ? m.n_kv_heads : m.n_heads;
+  if (m.n_kv_heads < 0 || m.n_heads % nk) PDS_FAIL(PDS_EINVAL, "n_kv_heads must divide n_heads");
+  if (nk % P) PDS_FAIL(PDS_EDIVISIBILITY, "n_kv_heads=" + std::to_string(nk) + " not divisible by P=" + std::to_string(P));
+  if (m.ffn_act != 0 && m.ffn_act != 1) PDS_FAIL(PDS_EINVAL, "ffn_act must be 0 (GELU) or 1 (SwiGLU)");
+  const bool variant = nk != m.n_heads || m.ffn_act == 1;
+  if (variant && (strategy == PDS_MEGATRON_CZ || strategy == PDS_COLOSSAL_Z))
+    PDS_FAIL(PDS_ENOTIMPL, "GQA / SwiGLU run on MegatronTS, UlyssesZ, METP and METP-full only");
   const int64_t sl = s / P;
   if (sl % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/P=" + std::to_string(sl) + " must be a multiple of 128 (caller pads, R-15)");
   const int64_t h = m.h, F = m.ffn, nl = m.n_heads / P, hl = h / P, Fl = F / P;
+  // Q|K|V widths (local qw = 3 hl for MHA, full qwf = 3 h) and FC1 widths (f1w / f1wf =
+  // Fl / F, doubled by SwiGLU's [gate | up])
+  const int64_t qw = (nl + 2 * (nk / P)) * (h / m.n_heads), qwf = qw * P;
+  const int64_t f1w = (m.ffn_act == 1 ? 2 : 1) * Fl, f1wf = f1w * P;
   // token buffers hold rows = positions x b (layout [s, b, h], reading Q-35); the
   // divisibility checks above are on positions
   const int64_t S = s * m.batch, SL = sl * m.batch;
@@ -243,53 +258,54 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   switch (strategy) {
     case PDS_MEGATRON_TS:
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      push(p.saved, ts, "qkv", S * qw * 2);
       push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", S * Fl * 2);
+      push(p.saved, ts, "h", S * f1w * 2);
       push(p.ws, tw, "gather", S * h * 2);
       push(p.ws, tw, "partial", S * h * 2);
-      push(p.ws, tw, "f0", S * Fl * 2);
-      push(p.ws, tw, "f1", S * Fl * 2);
+      push(p.ws, tw, "f0", S * std::max(f1w, qw) * 2);       // G, dH^T, dQKV
+      push(p.ws, tw, "f1", S * f1w * 2);                     // dH, dA
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * S * 2);   // transposed operands (all GEMMs TN)
+      push(p.ws, tw, "ta", std::max(Fl, qw) * S * 2);       // transposed operands (all GEMMs TN)
       push(p.ws, tw, "tb", h * S * 2);
-      push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
       if (P > 1) push(p.ws, tw, "gather2", S * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
+      const int64_t uq = SL * qwf * 2;            // a [s/P, Q|K|V of all heads] buffer (3u for MHA)
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      push(p.saved, ts, "qkv", S * qw * 2);
       push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "afull", u);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", SL * F * 2);
-      push(p.ws, tw, "wqkv", 3 * h * h * 2);
+      push(p.saved, ts, "h", SL * f1wf * 2);
+      push(p.ws, tw, "wqkv", qwf * h * 2);
       push(p.ws, tw, "wproj", h * h * 2);
-      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "win", f1wf * h * 2);
       push(p.ws, tw, "wout", F * h * 2);
-      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "dw", std::max(qwf, f1wf) * h * 4);
       push(p.ws, tw, "u1", u);
-      push(p.ws, tw, "s1", 3 * u);
-      push(p.ws, tw, "r1", 3 * u);
-      push(p.ws, tw, "f0", SL * F * 2);
-      push(p.ws, tw, "f1", SL * F * 2);
-      push(p.ws, tw, "x3", 3 * u);
-      push(p.ws, tw, "x4", 3 * u);
+      push(p.ws, tw, "s1", std::max(uq, u));
+      push(p.ws, tw, "r1", std::max(uq, u));
+      push(p.ws, tw, "f0", SL * f1wf * 2);
+      push(p.ws, tw, "f1", SL * f1wf * 2);
+      push(p.ws, tw, "x3", uq);
+      push(p.ws, tw, "x4", uq);
       push(p.ws, tw, "v2", u);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(F, 3 * h) * SL * 2);
+      push(p.ws, tw, "ta", std::max(F, qwf) * SL * 2);
       push(p.ws, tw, "tb", h * SL * 2);
-      push(p.ws, tw, "wt", h * std::max(F, 3 * h) * 2);
+      push(p.ws, tw, "wt", h * std::max(f1wf, qwf) * 2);
       push(p.ws, tw, "actr", actr);
       break;
     }
@@ -306,7 +322,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       const int64_t W = w * m.batch;               // rows of one wave per rank
       const int64_t uw = W * h * 2;
       push(p.saved, ts, "rstd1", ell);
-      if (!full) push(p.saved, ts, "qkv", S * 3 * hl * 2);
+      if (!full) push(p.saved, ts, "qkv", S * qw * 2);
       push(p.saved, ts, "a", S * hl * 2);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
@@ -316,19 +332,19 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "wg", P * uw);
       push(p.ws, tw, "wg2", P * uw);
       push(p.ws, tw, "pw", P * uw);
-      push(p.ws, tw, "hw", P * W * Fl * 2);
-      push(p.ws, tw, "gw", P * W * Fl * 2);
-      push(p.ws, tw, "dhw", P * W * Fl * 2);
+      push(p.ws, tw, "hw", P * W * f1w * 2);
+      push(p.ws, tw, "gw", P * W * f1w * 2);              // G, dH^T
+      push(p.ws, tw, "dhw", P * W * f1w * 2);
       push(p.ws, tw, "da", S * hl * 2);
-      push(p.ws, tw, "dqkv", S * 3 * hl * 2);
+      push(p.ws, tw, "dqkv", S * qw * 2);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", (int64_t)rmsnorm_bwd_grid(W) * h * 4);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(Fl, 3 * hl) * P * W * 2);
+      push(p.ws, tw, "ta", std::max(Fl, qw) * P * W * 2);
       push(p.ws, tw, "tb", h * P * W * 2);
-      push(p.ws, tw, "wt", h * std::max(Fl, 3 * hl) * 2);
+      push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
-      if (full) push(p.ws, tw, "qkv", S * 3 * hl * 2);
+      if (full) push(p.ws, tw, "qkv", S * qw * 2);
       break;
     }
     case PDS_MEGATRON_CZ: {

@@ -493,3 +493,102 @@ def test_attention_fwd_pair_kernel_matches(tmp_path, s, causal):
     b = (res["pair"]["out"].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
     assert rel(b, a) < 1e-3
     assert np.allclose(res["pair"]["lse"], res["1cta"]["lse"], rtol=0, atol=1e-4)
+
+
+# ---------------------------------------------------------------- Llama variant (NEXT-3)
+@pytest.mark.parametrize("d,heads,kv_heads", [(128, 4, 1), (128, 4, 2), (64, 8, 2)])
+@pytest.mark.parametrize("causal", [1, 0])
+@pytest.mark.parametrize("s", [256, 640])
+def test_attention_gqa_vs_oracle(d, heads, kv_heads, causal, s):
+    """GQA attention (R-GQA): the kernels read key / value head i // grp for query head
+    i; the dK / dV kernel sums the group's query heads.  Oracle: oracle.layer's
+    per-head attention on the same bf16 inputs, dK / dV summed over the group."""
+    hq, hk, grp = heads * d, kv_heads * d, heads // kv_heads
+    W = hq + 2 * hk
+    qkv = _mat(31 + d, 1, (s, W))
+    dout = _mat(31 + d, 2, (s, hq))
+    tq, tdo = dev_bf16(qkv), dev_bf16(dout)
+    out = torch.empty(s, hq, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(heads, s, dtype=torch.float32, device="cuda")
+    B.k_attn_fwd_gqa(tq.data_ptr(), W, s, heads, kv_heads, d, causal, out.data_ptr(), hq, lse.data_ptr(), stream())
+    dqkv = torch.zeros(s, W, dtype=torch.bfloat16, device="cuda")
+    B.k_attn_bwd_gqa(tq.data_ptr(), W, out.data_ptr(), hq, lse.data_ptr(), tdo.data_ptr(), s, heads, kv_heads, d,
+                     causal, dqkv.data_ptr(), stream())
+    torch.cuda.synchronize()
+    o_gpu, g = host(out), host(dqkv)
+    dk_ref = np.zeros((s, hk))
+    dv_ref = np.zeros((s, hk))
+    for hh in range(heads):
+        j = hh // grp
+        q = qkv[:, hh * d:(hh + 1) * d]
+        k = qkv[:, hq + j * d:hq + (j + 1) * d]
+        v = qkv[:, hq + hk + j * d:hq + hk + (j + 1) * d]
+        a, l = OL.attention_fwd(q, k, v, causal=bool(causal))
+        assert rel(o_gpu[:, hh * d:(hh + 1) * d], a) < 1e-2
+        assert rel(host(lse)[hh], l) < 2e-3
+        dq, dk, dv = OL.attention_bwd(q, k, v, o_gpu[:, hh * d:(hh + 1) * d], l, dout[:, hh * d:(hh + 1) * d],
+                                      causal=bool(causal))
+        assert rel(g[:, hh * d:(hh + 1) * d], dq) < 1e-2
+        dk_ref[:, j * d:(j + 1) * d] += dk
+        dv_ref[:, j * d:(j + 1) * d] += dv
+    assert rel(g[:, hq:hq + hk], dk_ref) < 1e-2
+    assert rel(g[:, hq + hk:], dv_ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,F,K", [(384, 256, 256), (1024, 768, 512), (2048, 2048, 1024)])
+def test_gemm_swiglu_epilogues(M, F, K):
+    """SwiGLU epilogues (R-SWIGLU) against oracle.layer.ffn_act / ffn_act_bwd on the
+    interleaved layout: forward H and G = SiLU(bf16 gate) * bf16 up; backward dH (both
+    halves), G, and the transposed dH^T / G^T copies the dW GEMMs read."""
+    A = _mat(41, 1, (M, K), std=1 / math.sqrt(K))
+    Wt = _mat(41, 2, (2 * F, K))                           # W_in^T rows, interleaved
+    ta, tw = dev_bf16(A), dev_bf16(Wt)
+    hb = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    g = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm_swiglu(ta.data_ptr(), K, tw.data_ptr(), K, M, 2 * F, K, 0, hb.data_ptr(), 2 * F, g_out=g.data_ptr(),
+                    ld_g=F, stream=stream())
+    torch.cuda.synchronize()
+    H = host(hb)
+    assert rel(H, A @ Wt.T) < 1e-2
+    assert rel(host(g), OL.ffn_act(H, "swiglu", il=True)) < 1e-2
+    # backward: the accumulator is dG = dZ W_out^T (here any [M, F] product)
+    dZ = _mat(41, 3, (M, K))
+    Wo = _mat(41, 4, (F, K), std=1 / math.sqrt(K))
+    tz, to = dev_bf16(dZ), dev_bf16(Wo)
+    dh = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    g2 = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    dht = torch.empty(2 * F, M, dtype=torch.bfloat16, device="cuda")
+    gt = torch.empty(F, M, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm_swiglu(tz.data_ptr(), K, to.data_ptr(), K, M, F, K, 1, dh.data_ptr(), 2 * F, hb.data_ptr(), 2 * F,
+                    g2.data_ptr(), F, dht.data_ptr(), gt.data_ptr(), M, stream=stream())
+    torch.cuda.synchronize()
+    dg = dZ @ Wo.T
+    ref_dh = OL.ffn_act_bwd(dg, H, "swiglu", il=True)
+    ref_g = OL.ffn_act(H, "swiglu", il=True)
+    assert rel(host(dh), ref_dh) < 1e-2
+    assert rel(host(g2), ref_g) < 1e-2
+    assert rel(host(dht), ref_dh.T) < 1e-2
+    assert rel(host(gt), ref_g.T) < 1e-2
+
+
+def test_gemm_rope_gqa_groups():
+    """RoPE epilogue with GQA column groups [Q (hq) | K (hk) | V (hk)]: Q and K columns
+    rotated at their row's position, V untouched (oracle.layer.rope_apply)."""
+    d, hq, hk, M, K = 128, 512, 128, 256, 256
+    N = 2 * (hq + 2 * hk)                                  # two groups (two ranks' blocks)
+    A = _mat(43, 1, (M, K), std=1 / math.sqrt(K))
+    Wt = _mat(43, 2, (N, K))
+    rope = torch.empty(M, d // 2, 2, dtype=torch.float32, device="cuda")
+    B.k_rope_table(rope.data_ptr(), M, d, stream=stream())
+    ta, tw = dev_bf16(A), dev_bf16(Wt)
+    c = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm_rope_gqa(ta.data_ptr(), K, tw.data_ptr(), K, M, N, K, c.data_ptr(), N, rope.data_ptr(), d, hq, hk,
+                      stream=stream())
+    torch.cuda.synchronize()
+    raw = A @ Wt.T
+    cos, sin = OL.rope_cos_sin(np.arange(M), d)
+    ref = raw.copy()
+    for g0 in (0, hq + 2 * hk):
+        for c0 in range(g0, g0 + hq + hk, d):
+            ref[:, c0:c0 + d] = OL.rope_apply(raw[:, c0:c0 + d], cos, sin)
+    assert rel(host(c), ref) < 1e-2

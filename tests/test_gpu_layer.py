@@ -98,18 +98,18 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
     return outs
 
 
-def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, b=1):
-    d = layer_inputs(h, n, F, s, b, seed=seed)
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, b=1, n_kv=None, act="gelu"):
+    d = layer_inputs(h, n, F, s, b, seed=seed, n_kv=n_kv, act=act)
     y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
-                            causal=causal)
+                            causal=causal, n_kv=n_kv, act=act)
     g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
-                         causal=causal)
-    W = OS.shard_weights(d, n, P)
+                         causal=causal, n_kv=n_kv, act=act)
+    W = OS.shard_weights(d, n, P, n_kv=n_kv, act=act)
     xs = OS.shard_act(d["x"], P)
     dys = OS.shard_act(d["dy"], P)
     ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
     model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0,
-                    metp_recompute=recompute, batch=b)
+                    metp_recompute=recompute, batch=b, n_kv_heads=n_kv or 0, ffn_act=1 if act == "swiglu" else 0)
     outs = run_ranks(model, P, [pi], [ranks], xs, dys)
     y = np.concatenate([o[0] for o in outs]).reshape(s, b, h)
     dx = np.concatenate([o[1] for o in outs]).reshape(s, b, h)
@@ -118,12 +118,13 @@ def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, 
     res = dict(y=rel(y, y_ref), o=rel(o, c["o"]), z=rel(z, c["z"]), dx=rel(dx, g_ref["dx"]),
                dxmdy=rel(dx - d["dy"], g_ref["dx"] - d["dy"]))
     gsh = {k: [host(R.g[k]) for R in ranks] for k in ranks[0].g}
-    dense = OS.unshard_grads(gsh, n)
+    dense = OS.unshard_grads(gsh, n, n_kv=n_kv, act=act)
     for k in ("dw_qkv", "dw_proj", "dw_in", "dw_out", "dg1", "dg2"):
         res[k] = rel(dense[k], g_ref[k])
     # shard indexing: rank r's gradient shard vs the oracle's rank-r slice (O-4)
     ref_sh = OS.shard_weights(dict(w_qkv=g_ref["dw_qkv"], w_proj=g_ref["dw_proj"], w_in=g_ref["dw_in"],
-                                   w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P)
+                                   w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P,
+                              n_kv=n_kv, act=act)
     for r in range(P):
         res[f"qkv_shard{r}"] = rel(gsh["dw_qkv_t"][r], ref_sh["w_qkv_t"][r])
         res[f"y_shard{r}"] = rel(outs[r][0].reshape(s // P, b, h), y_ref[r * (s // P):(r + 1) * (s // P)])
@@ -380,3 +381,24 @@ def test_nccl_one_rank_equals_self(pi):
     assert torch.equal(a.y, b.y) and torch.equal(a.dx, b.dx)
     for k in a.g:
         assert torch.equal(a.g[k], b.g[k]), k
+
+
+# ---------------------------------------------------------------- Llama variant (NEXT-3)
+@pytest.mark.parametrize("pi", [0, 1, 2, 4])
+@pytest.mark.parametrize("P,h,n,n_kv,F,s", [
+    (1, 512, 8, 2, 768, 640),        # d = 64, grp 4, ragged query blocks
+    (2, 1024, 8, 2, 1536, 1024),     # d = 128, grp 4, one KV head per rank
+    (4, 1024, 8, 4, 1024, 2048),     # d = 128, grp 2
+])
+def test_llama_variant_layer(pi, P, h, n, n_kv, F, s):
+    """GQA + SwiGLU layer (R-GQA / R-SWIGLU) on every strategy that runs it, per-rank
+    shards included, against the fp64 oracle's Llama layer."""
+    chunks = 2 if pi in (2, 4) else 0
+    _check_layer(pi, P, h, n, F, s, seed=17, chunks=chunks, n_kv=n_kv, act="swiglu", b=2 if P == 2 else 1)
+
+
+@pytest.mark.parametrize("n_kv,act", [(2, "gelu"), (8, "swiglu")])
+def test_llama_variant_parts_separately(n_kv, act):
+    """GQA alone (GELU FFN) and SwiGLU alone (MHA) through MegatronTS at P = 2."""
+    _check_layer(0, 2, 1024, 8, 2048, 1024, seed=19, n_kv=n_kv, act=act)
+
