@@ -229,6 +229,19 @@ pds_status pds_layer_step_host(pds_ctx* ctx, uint8_t strategy, int64_t seq_len, 
 pds_status pds_host_drain(pds_ctx* ctx, void* stream);
 /* Release a saved set without running backward. */
 pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
+/* Varlen packing (reading R-VARLEN): the following layer calls of
+ * this context treat their seq_len tokens as n_seqs independent sequences packed back to
+ * back in the boundary layout (rank r holds tokens [r T/P, (r+1) T/P) of the packed
+ * stream, T = sum lens); attention never crosses a sequence boundary (causal or not) and
+ * RoPE positions restart at each sequence's first token.  lens: host int64[n_seqs], each
+ * a positive multiple of 256 (PDS_EDIVISIBILITY otherwise: the caller pads each
+ * sequence); the layer calls must pass seq_len = T (PDS_EINVAL otherwise).  n_seqs = 0
+ * restores one sequence.  Requires batch = 1 (PDS_EINVAL); MegatronTS, UlyssesZ, METP,
+ * METP-full (MegatronCZ / ColossalZ: PDS_ENOTIMPL).  A forward's setting is kept with
+ * its saved set, so the matching backward uses it whatever was set since.  Blocking
+ * (uploads a small table). */
+pds_status pds_set_varlen(pds_ctx* ctx, int32_t n_seqs, const int64_t* lens);
+
 /* Tile-level overlap of the MegatronTS collectives (P > 1): every
  * all-gather feeding a column-parallel GEMM (QKV, FC1; bwd dGELU, dA) runs chunk by
  * chunk on a side stream while the GEMM polls per tile for the chunks it needs, and

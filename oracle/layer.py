@@ -305,3 +305,40 @@ def layer_bwd(dy, cache, w_qkv, w_proj, w_in, w_out, g1, g2, n, causal=True,
     dx = dx1 + dxn
     return dict(dx=dx, dw_qkv=dw_qkv, dw_proj=dw_proj, dw_in=dw_in, dw_out=dw_out,
                 dg1=dg1, dg2=dg2, dx1=dx1, dqkv=dqkv)
+
+
+def layer_fwd_varlen(x, lens, w_qkv, w_proj, w_in, w_out, g1, g2, n, **kw):
+    """Varlen packing (reading R-VARLEN): the token axis of
+    x [T, 1, h] holds len(lens) independent sequences back to back.  By definition the
+    packed layer is the unsharded layer (O-1) applied to each sequence — attention
+    stays inside a sequence and its RoPE positions start at 0 — so this is that loop.
+    Returns (y [T, 1, h], per-sequence caches); o / z taps concatenated in the caches."""
+    ys, caches = [], []
+    o = 0
+    for L in lens:
+        y, c = layer_fwd(x[o:o + L], w_qkv, w_proj, w_in, w_out, g1, g2, n, **kw)
+        ys.append(y)
+        caches.append(c)
+        o += L
+    if o != x.shape[0]:
+        raise ValueError(f"sum(lens)={o} != tokens {x.shape[0]}")
+    return np.concatenate(ys, axis=0), caches
+
+
+def layer_bwd_varlen(dy, caches, lens, w_qkv, w_proj, w_in, w_out, g1, g2, n, **kw):
+    """Backward of layer_fwd_varlen: dx concatenated, weight and gain gradients summed
+    over the sequences (they share the weights)."""
+    out = None
+    dxs = []
+    o = 0
+    for L, c in zip(lens, caches):
+        g = layer_bwd(dy[o:o + L], c, w_qkv, w_proj, w_in, w_out, g1, g2, n, **kw)
+        dxs.append(g["dx"])
+        if out is None:
+            out = {k: v.copy() for k, v in g.items() if k.startswith("dw") or k.startswith("dg")}
+        else:
+            for k in out:
+                out[k] += g[k]
+        o += L
+    out["dx"] = np.concatenate(dxs, axis=0)
+    return out

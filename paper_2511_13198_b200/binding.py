@@ -128,6 +128,7 @@ _SIGS = {
     "pds_k_stream_write32": [C.c_void_p, C.c_void_p, C.c_uint32],
     "pds_k_stream_wait32": [C.c_void_p, C.c_void_p, C.c_uint32],
     "pds_set_overlap": [C.c_void_p, C.c_int32],
+    "pds_set_varlen": [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
     "pds_profile_read": [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                          C.POINTER(C.c_double), C.POINTER(C.c_double)],
@@ -313,6 +314,11 @@ class Context:
 
     def set_overlap(self, on):
         call("pds_set_overlap", self.h, 1 if on else 0)
+
+    def set_varlen(self, lens):
+        """Pack len(lens) sequences into the following layer calls (R-VARLEN); [] = one."""
+        arr = (C.c_int64 * max(1, len(lens)))(*[int(v) for v in lens])
+        call("pds_set_varlen", self.h, len(lens), arr)
 
     def debug_taps(self, o=None, z=None):
         call("pds_debug_taps", self.h, o, z)

@@ -37,16 +37,17 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ out, int64
 }
 
 int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-                void* lse, cudaStream_t st, int qlo = 0, int qn = -1, int kv_heads = 0);
+                void* lse, cudaStream_t st, int qlo = 0, int qn = -1, int kv_heads = 0,
+                const int* segs = nullptr);
 
 int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out,
-             int64_t ld_out, void* lse, cudaStream_t st, int kv_heads) {
-  return attn_fwd_tc(qkv, ld, s, heads, d, causal, out, ld_out, lse, st, 0, -1, kv_heads);
+             int64_t ld_out, void* lse, cudaStream_t st, int kv_heads, const int* segs) {
+  return attn_fwd_tc(qkv, ld, s, heads, d, causal, out, ld_out, lse, st, 0, -1, kv_heads, segs);
 }
 
 int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
                 int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo = 0,
-                int qn = -1, int kv_heads = 0);
+                int qn = -1, int kv_heads = 0, const int* segs = nullptr);
 
 int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
                       int s, int heads, void* dqkv, const void* rope, float* dqacc, int* ctr, cudaStream_t st);
@@ -61,10 +62,10 @@ bool attn_bwd_fused_applies(int d, int causal) { return g_bwd_mode == 1 && d == 
 
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
              const void* dout, int s, int heads, int d, int causal, void* dqkv, const void* rope,
-             float* Dd, cudaStream_t st, float* dqacc, int* ctr, int kv_heads) {
+             float* Dd, cudaStream_t st, float* dqacc, int* ctr, int kv_heads, const int* segs) {
   if (s % 128) return (int)cudaErrorInvalidValue;
   if (kv_heads <= 0) kv_heads = heads;
-  const bool fused = dqacc && ctr && attn_bwd_fused_applies(d, causal) && kv_heads == heads;
+  const bool fused = dqacc && ctr && attn_bwd_fused_applies(d, causal) && kv_heads == heads && !segs;
   const int nctr = fused ? heads * (s / 128) + 1 : 0;
   const int nblk = (s * heads + 7) / 8;
   if (nctr > nblk * 256) return (int)cudaErrorInvalidValue;
@@ -72,7 +73,7 @@ int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const
                                             reinterpret_cast<const __nv_bfloat16*>(dout), s, heads, d, Dd, ctr,
                                             nctr);
   if (fused) return attn_bwd_fused_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, dqkv, rope, dqacc, ctr, st);
-  return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, 0, -1, kv_heads);
+  return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, 0, -1, kv_heads, segs);
 }
 
 // Context parallelism (MegatronCZ): queries [qlo, qlo + qn) of the s positions against

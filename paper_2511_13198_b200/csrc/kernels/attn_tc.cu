@@ -174,7 +174,8 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmq, int s,
                        int heads, int causal, __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
-                       float scale_log2, int qlo, int qn, int kcol, int vcol, int grp) {
+                       float scale_log2, int qlo, int qn, int kcol, int vcol, int grp,
+                       const int* __restrict__ segs) {
   using C = Fwd2Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -196,7 +197,10 @@ __global__ void __launch_bounds__(384, 1)
   const int head = blockIdx.y;
   const int kvh = head / grp;           // GQA: the key / value head of this query head
   const int q0 = qlo + qb * 256;
-  const int nkv = causal ? min(s, q0 + 256) / BN : s / BN;
+  // varlen packing (R-VARLEN): the keys of this query block's own sequence only, key
+  // blocks [kb0, kb0 + nkv); segs[2 blk], segs[2 blk + 1] = its sequence's block range
+  const int kb0 = segs ? segs[2 * (q0 / 128)] : 0;
+  const int nkv = (causal ? min(s, q0 + 256) / BN : (segs ? segs[2 * (q0 / 128) + 1] : s / BN)) - kb0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
@@ -229,8 +233,10 @@ __global__ void __launch_bounds__(384, 1)
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], kcol + kvh * D + a * 64, j * BN);
-          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], vcol + kvh * D + a * 64, j * BN);
+          tma_load_2d(sm + C::K_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], kcol + kvh * D + a * 64,
+                      (kb0 + j) * BN);
+          tma_load_2d(sm + C::V_OFF + st * C::TILE + a * 16384, &tm, &kv_full[st], vcol + kvh * D + a * 64,
+                      (kb0 + j) * BN);
         }
       }
     }
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[tile], j & 1);
       tc_fence_after();
-      const int k0 = j * BN;
+      const int k0 = (kb0 + j) * BN;
       const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
       auto block = [&](auto mask_c) {
         constexpr bool MASK = decltype(mask_c)::value;
@@ -815,7 +821,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                           const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                           int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2, int qlo,
-                          int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc, int grp) {
+                          int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc, int grp,
+                          const int* __restrict__ segs) {
   using C = BwdKV4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -839,8 +846,9 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   const int k0 = kb * 128;
   // only the query blocks of [qlo, qlo + qn) contribute (dO, LSE, D are local to them);
   // the launch covers only key blocks that have at least one
-  const int qstart = max(causal ? kb : 0, qlo / 128);
-  const int nqh = (qlo + qn) / 128 - qstart;
+  // varlen packing: only the queries of the key block's own sequence
+  const int qstart = max(causal ? kb : (segs ? segs[2 * kb] : 0), qlo / 128);
+  const int nqh = (segs ? min((qlo + qn) / 128, segs[2 * kb + 1]) : (qlo + qn) / 128) - qstart;
   const int nq = nqh * grp;
   constexpr int ST_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 256 + D;
 
@@ -1101,7 +1109,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         float a[32], bb[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) { a[j] = __uint_as_float(ra[j]); bb[j] = __uint_as_float(rb[j]); }
-        rope_t_rows<D>(a, bb, rope, key, c * 32, scale);
+        rope_t_rows<D>(a, bb, rope, segs ? key - segs[2 * (key / 128)] * 128 : key, c * 32, scale);
         store32_bf16(rowp + kcol + c * 32, a);          // dK at kcol + head * D
         store32_bf16(rowp + kcol + c * 32 + D / 2, bb);
       } else {
@@ -1146,7 +1154,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                         int64_t ld_out, const __grid_constant__ CUtensorMap tkv, const float* __restrict__ lse,
                         const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                         const float2* __restrict__ rope, float scale, float scale_log2, int qlo, int qn, int kcol,
-                        int vcol, int64_t ld_dq, float* __restrict__ acc, int64_t ld_acc, int grp) {
+                        int vcol, int64_t ld_dq, float* __restrict__ acc, int64_t ld_acc, int grp,
+                        const int* __restrict__ segs) {
   using C = BwdQ4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1167,7 +1176,9 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   const int qb = qlo / 128 + (causal ? (nqb - 1 - (int)blockIdx.x) : (int)blockIdx.x);
   const int head = blockIdx.y;
   const int q0 = qb * 128;
-  const int nkv = causal ? qb + 1 : s / 128;
+  // varlen packing: key blocks [kb0, kb0 + nkv) of the query block's own sequence
+  const int kb0 = segs ? segs[2 * qb] : 0;
+  const int nkv = (causal ? qb + 1 : (segs ? segs[2 * qb + 1] : s / 128)) - kb0;
   constexpr int Q_COL = 0, O_COL = 64, S_COL = 128, DP_COL = 256, DQ_COL = 384;
 
   if (warp == 0 && lane == 0) {
@@ -1198,8 +1209,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         if (j >= NST) mbar_wait(&kv_empty[b], ((j / NST) - 1) & 1);
         mbar_arrive_expect_tx(&kv_full[b], 2 * C::T);
         for (int a = 0; a < D / 64; ++a) {
-          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], kcol + (head / grp) * D + a * 64, j * 128);
-          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], vcol + (head / grp) * D + a * 64, j * 128);
+          tma_load_2d(sm + C::K_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], kcol + (head / grp) * D + a * 64,
+                      (kb0 + j) * 128);
+          tma_load_2d(sm + C::V_OFF + b * C::T + a * 16384, &tkv, &kv_full[b], vcol + (head / grp) * D + a * 64,
+                      (kb0 + j) * 128);
         }
       }
     }
@@ -1388,7 +1401,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
       float a[32], bb[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) { a[i] = __uint_as_float(ra[i]); bb[i] = __uint_as_float(rb[i]); }
-      rope_t_rows<D>(a, bb, rope, row, c * 32, scale);
+      rope_t_rows<D>(a, bb, rope, segs ? row - kb0 * 128 : row, c * 32, scale);
       store32_bf16(rowp + c * 32, a);
       store32_bf16(rowp + c * 32 + D / 2, bb);
     }
@@ -1965,8 +1978,8 @@ static int fwd_pair(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
 template <int D>
 static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     int s, int heads, int causal, void* out, int64_t ld_out, void* lse, int qlo, int qn,
-                    cudaStream_t st, int grp = 1) {
-  if (D == 128 && fwd_pair_mode() && grp == 1)
+                    cudaStream_t st, int grp = 1, const int* segs = nullptr) {
+  if (D == 128 && fwd_pair_mode() && grp == 1 && !segs)
     return fwd_pair(q, ld_q, q_rows, kv, ld_kv, kcol, vcol, s, heads, causal, out, ld_out, lse, qlo, qn, st);
   CUtensorMap tm, tmq;
   int rc = make_map_rows(&tm, kv, (uint64_t)vcol + heads / grp * D, (uint64_t)s, (uint64_t)ld_kv);
@@ -1980,22 +1993,23 @@ static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
   attn_fwd_tc_kernel<D><<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
       tm, tmq, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
-      scale_log2, qlo, qn, kcol, vcol, grp);
+      scale_log2, qlo, qn, kcol, vcol, grp, segs);
   return (int)cudaGetLastError();
 }
 
 // packed [Q (heads) | K (kv_heads) | V (kv_heads)] rows; kv_heads = 0: heads (MHA)
 int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-                void* lse, cudaStream_t st, int qlo, int qn, int kv_heads) {
+                void* lse, cudaStream_t st, int qlo, int qn, int kv_heads, const int* segs) {
   if (qn < 0) qn = s;
+  if (segs && (qlo != 0 || qn != s)) return (int)cudaErrorInvalidValue;
   if (kv_heads <= 0) kv_heads = heads;
   if (s % 128 || (ld % 8) || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s || heads % kv_heads)
     return (int)cudaErrorInvalidValue;
   const int hq = heads * d, hk = kv_heads * d, grp = heads / kv_heads;
   if (d == 128)
-    return fwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp);
+    return fwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp, segs);
   if (d == 64)
-    return fwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp);
+    return fwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, s, heads, causal, out, ld_out, lse, qlo, qn, st, grp, segs);
   return (int)cudaErrorInvalidValue;
 }
 
@@ -2025,7 +2039,7 @@ template <int D>
 static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     const void* dout, int64_t ld_out, const void* lse, const float* Dd, int s, int heads, int causal,
                     void* dqkv, int64_t ld, const void* rope, int qlo, int qn, float* dq_acc, int64_t ld_dqa,
-                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int grp = 1) {
+                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int grp = 1, const int* segs = nullptr) {
   CUtensorMap kv128, q128, do128;
   int rc = make_map_rows(&kv128, kv, (uint64_t)vcol + heads / grp * D, s, ld_kv, 128);
   rc |= make_map_rows(&q128, q, (uint64_t)heads * D, q_rows, ld_q, 128);
@@ -2056,14 +2070,15 @@ static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
     attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads / grp), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
         kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
         reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2,
-        qlo, qn, kcol, vcol, dkv_acc, ld_dkva, grp);
+        qlo, qn, kcol, vcol, dkv_acc, ld_dkva, grp, segs);
   };
   auto dq = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
     attn_bwd_dq4_kernel<D, NW><<<dim3(qn / 128, heads), 128 + 128 * NW, BwdQ4Cfg<D>::SMEM, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(q), ld_q, reinterpret_cast<const __nv_bfloat16*>(dout), ld_out, kv128,
         reinterpret_cast<const float*>(lse), Dd, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(dqkv),
-        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn, kcol, vcol, ld, dq_acc, ld_dqa, grp);
+        reinterpret_cast<const float2*>(rope), scale, scale_log2, qlo, qn, kcol, vcol, ld, dq_acc, ld_dqa, grp,
+        segs);
   };
   if (force == 2) dkdv(std::integral_constant<int, 2>{});
   else dkdv(std::integral_constant<int, 4>{});
@@ -2100,18 +2115,19 @@ int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_
 // dQ, dK, dV into dqkv (same [s][ld] layout as qkv); Dd = rowsum(dO o O) precomputed
 int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
                 int s, int heads, int d, int causal, void* dqkv, const void* rope, cudaStream_t st, int qlo, int qn,
-                int kv_heads) {
+                int kv_heads, const int* segs) {
   if (qn < 0) qn = s;
   if (kv_heads <= 0) kv_heads = heads;
   if (s % 128 || ld % 8 || ld_out % 8 || qlo % 128 || qn % 128 || qn <= 0 || qlo + qn > s || heads % kv_heads)
     return (int)cudaErrorInvalidValue;
+  if (segs && (qlo != 0 || qn != s)) return (int)cudaErrorInvalidValue;
   const int hq = heads * d, hk = kv_heads * d, grp = heads / kv_heads;
   if (d == 128)
     return bwd_tc_t<128>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope,
-                         qlo, qn, nullptr, 0, nullptr, 0, st, grp);
+                         qlo, qn, nullptr, 0, nullptr, 0, st, grp, segs);
   if (d == 64)
     return bwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope, qlo,
-                        qn, nullptr, 0, nullptr, 0, st, grp);
+                        qn, nullptr, 0, nullptr, 0, st, grp, segs);
   return (int)cudaErrorInvalidValue;
 }
 

@@ -59,6 +59,7 @@ struct EpiParams {
   int64_t ld_aux, ld_aux_in;
   const float2* rope;
   int rope_d, rope_hq, rope_hk, rope_b;
+  const int* rope_segs;
   int64_t seg, seg_stride, seg_base;
   int64_t c_seg, c_stride, c_base;
   __nv_bfloat16* c_t;      // transposed copies (dGELU epilogue): [N][ld_t]
@@ -238,6 +239,7 @@ __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbas
     if (row_ok) {
       const int64_t r = row;
       pos = ((r / ep.seg) * ep.seg_stride + ep.seg_base + (r % ep.seg)) / ep.rope_b;
+      if (ep.rope_segs) pos -= (int64_t)ep.rope_segs[2 * (pos >> 7)] * 128;   // position in its sequence
     }
     for (int hs = 0; hs < BN; hs += d) {
       for (int j0 = 0; j0 < d2; j0 += 32) {
@@ -811,6 +813,7 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.ld_t = g.ld_t;
   ep.rope = g.rope; ep.rope_d = g.rope_d; ep.rope_hq = g.rope_hq; ep.rope_b = g.rope_b > 0 ? g.rope_b : 1;
   ep.rope_hk = g.rope_hk > 0 ? g.rope_hk : g.rope_hq;
+  ep.rope_segs = g.rope_segs;
   ep.seg = g.seg > 0 ? g.seg : (int64_t)1 << 40;
   ep.seg_stride = g.seg_stride; ep.seg_base = g.seg_base;
   ep.c_seg = g.c_seg > 0 ? g.c_seg : (int64_t)1 << 40;

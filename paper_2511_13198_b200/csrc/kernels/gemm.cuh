@@ -53,6 +53,7 @@ struct GemmArgs {
   int rope_hq = 0;
   int rope_hk = 0;
   int rope_b = 1;                 // rows per position (batch b, layout [s, b, h]): pos = mapped row / b
+  const int* rope_segs = nullptr; // varlen packing (R-VARLEN): pos -= rope_segs[2 (pos / 128)] * 128
   int64_t seg = 0, seg_stride = 0, seg_base = 0;
   // Row remaps of the STORED matrices (seg = 0: identity): logical row r lives at
   // storage row (r / seg) * stride + base + r % seg.  For A/B this is the TMA outer

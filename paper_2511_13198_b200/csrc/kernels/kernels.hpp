@@ -9,12 +9,16 @@ int attn_debug_trace(long long* host_out, int rows);
 // qkv rows packed [Q (heads) | K (kv_heads) | V (kv_heads)]; kv_heads = 0: heads (MHA),
 // else GQA with query head i on key / value head i / (heads / kv_heads)
 int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, void* out, int64_t ld_out,
-             void* lse, cudaStream_t st, int kv_heads = 0);
+             void* lse, cudaStream_t st, int kv_heads = 0, const int* segs = nullptr);
 // dqacc (heads * s * d fp32) and ctr (heads * s / 128 + 1 ints) select the fused
 // one-kernel backward (d = 128, causal, MHA); NULL keeps the split dK/dV + dQ kernels
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
              int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st,
-             float* dqacc = nullptr, int* ctr = nullptr, int kv_heads = 0);
+             float* dqacc = nullptr, int* ctr = nullptr, int kv_heads = 0, const int* segs = nullptr);
+// varlen packing (R-VARLEN): segs int32 [2 * s / 128] on the device, for every 128-row
+// block the [first, last + 1) block range of the sequence it belongs to (sequences are
+// 256-row aligned); attention stays inside each sequence and RoPE positions restart at
+// its first row; NULL = one sequence
 bool attn_bwd_fused_applies(int d, int causal);
 void set_attn_bwd_mode(int mode);
 // context parallelism: queries [qlo, qlo + qn) against all s keys (attention.cu)

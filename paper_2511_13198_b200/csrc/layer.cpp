@@ -43,6 +43,7 @@ struct ProfRec {
 struct pds_saved {
   int strategy;
   int64_t s;
+  const int* segs = nullptr;     // varlen table of the forward (R-VARLEN), reused by the backward
   const void* x;
   char* mem;
   int64_t bytes;
@@ -73,6 +74,12 @@ struct pds_ctx {
   uint32_t enabled = (1u << PDS_N_STRATEGIES) - 1;
   std::map<std::pair<int, int64_t>, std::pair<std::vector<uint8_t>, bool>> cache;
   std::vector<uint8_t> prev;
+  // varlen packing (R-VARLEN, pds_set_varlen): the device segment table of the current
+  // setting (NULL: one sequence) for seq_len = varlen_tokens; every table stays alive
+  // until the context is destroyed (a saved set may still point at an older one)
+  const int* segs = nullptr;
+  int64_t varlen_tokens = 0;
+  std::vector<int*> seg_tables;
   // debug taps
   void* tap_o = nullptr;
   void* tap_z = nullptr;
@@ -114,6 +121,7 @@ struct pds_ctx {
     if (down_st) cudaStreamDestroy(down_st);
     if (comm_st) cudaStreamDestroy(comm_st);
     if (sync) cudaFree(sync);
+    for (int* t : seg_tables) cudaFree(t);
     for (auto e : sync_pool) cudaEventDestroy(e);
     delete comm;
   }
@@ -173,10 +181,12 @@ struct Exec {
   // widths (Fl / F; 2 Fl / 2 F with SwiGLU's interleaved [gate | up])
   int64_t nkl, qw, qwf, f1w, f1wf;
   bool swi;
-  Exec(pds_ctx* c_, cudaStream_t st_, int64_t s_)
+  const int* segs;                   // varlen segment table (R-VARLEN) or NULL
+  Exec(pds_ctx* c_, cudaStream_t st_, int64_t s_, const int* segs_ = nullptr)
       : c(c_), st(st_), m(c_->m), P(c_->P), r(c_->rank), b(c_->m.batch), sq(s_), sp(s_ / c_->P),
         s(s_ * c_->m.batch), sl(s_ / c_->P * c_->m.batch), h(c_->m.h), F(c_->m.ffn),
         nl(c_->m.n_heads / c_->P), d(c_->m.h / c_->m.n_heads), hl(c_->m.h / c_->P), Fl(c_->m.ffn / c_->P) {
+    segs = segs_;
     nkl = (c_->m.n_kv_heads > 0 ? c_->m.n_kv_heads : c_->m.n_heads) / c_->P;
     qw = (nl + 2 * nkl) * d;
     qwf = qw * c_->P;
@@ -342,6 +352,7 @@ struct Exec {
     g.rope_hk = (int)(nkl * d);
     g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
     g.rope_b = (int)b;                 // row -> position: the mapped row / b
+    g.rope_segs = segs;                // varlen: positions restart at every sequence
     return g;
   }
   pds_status norm_fwd(const void* x, const void* res, const void* g, int64_t rows, void* x1, void* u, void* rstd) {
@@ -369,7 +380,7 @@ struct Exec {
     for (int64_t bi = 0; bi < b; ++bi)
       PDS_TRY(kerr(attn_fwd(static_cast<const char*>(qkv) + bi * qw * 2, qw * b, (int)sq, (int)nl, (int)d,
                             m.causal, static_cast<char*>(out) + bi * hl * 2, hl * b,
-                            static_cast<float*>(lse) + bi * nl * sq, st, (int)nkl), "attn_fwd"));
+                            static_cast<float*>(lse) + bi * nl * sq, st, (int)nkl, segs), "attn_fwd"));
     return PDS_OK;
   }
   // sc: the fused backward's scratch (an fp32 dQ accumulator of sc_bytes >= nl sq d 4,
@@ -385,7 +396,7 @@ struct Exec {
                             static_cast<const char*>(out) + bi * hl * 2, hl * b,
                             static_cast<const float*>(lse) + bi * nl * sq, static_cast<const char*>(dout) + bi * hl * 2,
                             (int)sq, (int)nl, (int)d, m.causal, static_cast<char*>(dqkv) + bi * qw * 2, c->rope,
-                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr, (int)nkl), "attn_bwd"));
+                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr, (int)nkl, segs), "attn_bwd"));
     return PDS_OK;
   }
   // collectives
@@ -1617,6 +1628,39 @@ extern "C" pds_status pds_release_cache(pds_ctx* c) {
   return PDS_OK;
 }
 
+extern "C" pds_status pds_set_varlen(pds_ctx* c, int32_t n_seqs, const int64_t* lens) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  if (n_seqs < 0 || (n_seqs > 0 && !lens)) PDS_FAIL(PDS_EINVAL, "pds_set_varlen: bad n_seqs / lens");
+  if (n_seqs == 0) {
+    c->segs = nullptr;
+    c->varlen_tokens = 0;
+    return PDS_OK;
+  }
+  if (c->m.batch != 1) PDS_FAIL(PDS_EINVAL, "varlen packing replaces the batch: batch must be 1");
+  if (c->device < 0) PDS_FAIL(PDS_ESTATE, "host-only planner context (device < 0)");
+  int64_t T = 0;
+  std::vector<int> tab;
+  for (int i = 0; i < n_seqs; ++i) {
+    if (lens[i] <= 0 || lens[i] % 256)
+      PDS_FAIL(PDS_EDIVISIBILITY, "varlen: sequence " + std::to_string(i) + " length " + std::to_string(lens[i]) +
+                                      " must be a positive multiple of 256 (caller pads, R-VARLEN)");
+    const int lo = (int)(T / 128), hi = (int)((T + lens[i]) / 128);
+    for (int blk = lo; blk < hi; ++blk) {
+      tab.push_back(lo);
+      tab.push_back(hi);
+    }
+    T += lens[i];
+  }
+  int* d = nullptr;
+  PDS_CUDA(cudaSetDevice(c->device));
+  PDS_CUDA(cudaMalloc(&d, tab.size() * sizeof(int)));
+  c->seg_tables.push_back(d);
+  PDS_CUDA(cudaMemcpy(d, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+  c->segs = d;
+  c->varlen_tokens = T;
+  return PDS_OK;
+}
+
 extern "C" pds_status pds_set_overlap(pds_ctx* c, int32_t on) {
   if (!c) PDS_FAIL(PDS_EINVAL, "pds_set_overlap: null ctx");
   c->overlap = on ? 1 : 0;
@@ -1639,17 +1683,25 @@ extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_le
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   BufPlan bp;
   PDS_TRY(make_plan(c->m, c->P, strategy, seq_len, &bp));
+  if (c->segs) {
+    if (seq_len != c->varlen_tokens)
+      PDS_FAIL(PDS_EINVAL, "varlen: seq_len=" + std::to_string(seq_len) + " != the packed total " +
+                               std::to_string(c->varlen_tokens) + " (pds_set_varlen)");
+    if (strategy == PDS_MEGATRON_CZ || strategy == PDS_COLOSSAL_Z)
+      PDS_FAIL(PDS_ENOTIMPL, "varlen packing runs on MegatronTS, UlyssesZ, METP and METP-full only");
+  }
   PDS_CUDA(cudaSetDevice(c->device));
   PDS_TRY(ensure_ws(c, bp.ws_bytes, st));
   PDS_TRY(ensure_rope(c, seq_len, st));
   std::unique_ptr<pds_saved> sv(new pds_saved());
   sv->strategy = strategy;
   sv->s = seq_len;
+  sv->segs = c->segs;
   sv->x = x;
   sv->plan = bp;
   sv->bytes = bp.saved_bytes;
   PDS_TRY(alloc_saved(c, bp.saved_bytes, &sv->mem));
-  Exec e(c, st, seq_len);
+  Exec e(c, st, seq_len, sv->segs);
   pds_status rc;
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_fwd(e, x, w, y, sv.get(), c->ws); break;
@@ -1680,7 +1732,7 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   PDS_CUDA(cudaSetDevice(c->device));
   PDS_TRY(ensure_ws(c, saved->plan.ws_bytes, st));
-  Exec e(c, st, saved->s);
+  Exec e(c, st, saved->s, saved->segs);
   pds_status rc;
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_bwd(e, dy, saved, w, g, dx, c->ws); break;

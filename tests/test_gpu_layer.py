@@ -47,7 +47,7 @@ class Rank:
         return B.Grads(*(self.g[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
 
 
-def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True, overlap=None):
+def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True, overlap=None, varlen=None):
     """Run an L-layer stack (plan pi_list) on P loopback ranks; returns per-rank outputs.
     overlap: None = library default, else pds_set_overlap(ctx, overlap)."""
     grp = B.Group(P)
@@ -62,6 +62,8 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
                 ctx = B.Context(model, group=grp, rank=r)
                 if overlap is not None:
                     ctx.set_overlap(overlap)
+                if varlen:
+                    ctx.set_varlen(varlen)
                 xs = dev_bf16(x_shards[r].reshape(x_shards[r].shape[0], -1))
                 acts = [xs]
                 saves = []
@@ -98,19 +100,25 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
     return outs
 
 
-def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, b=1, n_kv=None, act="gelu"):
+def _check_layer(pi, P, h, n, F, s, seed=1, chunks=0, causal=True, recompute=0, b=1, n_kv=None, act="gelu",
+                 varlen=None):
     d = layer_inputs(h, n, F, s, b, seed=seed, n_kv=n_kv, act=act)
-    y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
-                            causal=causal, n_kv=n_kv, act=act)
-    g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n,
-                         causal=causal, n_kv=n_kv, act=act)
+    wargs = (d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"])
+    kw = dict(n=n, causal=causal, n_kv=n_kv, act=act)
+    if varlen:                       # R-VARLEN: the oracle layer per packed sequence
+        y_ref, cs = OL.layer_fwd_varlen(d["x"], varlen, *wargs, **kw)
+        g_ref = OL.layer_bwd_varlen(d["dy"], cs, varlen, *wargs, **kw)
+        c = dict(o=np.concatenate([q["o"] for q in cs]), z=np.concatenate([q["z"] for q in cs]))
+    else:
+        y_ref, c = OL.layer_fwd(d["x"], *wargs, **kw)
+        g_ref = OL.layer_bwd(d["dy"], c, *wargs, **kw)
     W = OS.shard_weights(d, n, P, n_kv=n_kv, act=act)
     xs = OS.shard_act(d["x"], P)
     dys = OS.shard_act(d["dy"], P)
     ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
     model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, causal=1 if causal else 0,
                     metp_recompute=recompute, batch=b, n_kv_heads=n_kv or 0, ffn_act=1 if act == "swiglu" else 0)
-    outs = run_ranks(model, P, [pi], [ranks], xs, dys)
+    outs = run_ranks(model, P, [pi], [ranks], xs, dys, varlen=varlen)
     y = np.concatenate([o[0] for o in outs]).reshape(s, b, h)
     dx = np.concatenate([o[1] for o in outs]).reshape(s, b, h)
     o = np.concatenate([host(R.o) for R in ranks]).reshape(s, b, h)
@@ -402,3 +410,49 @@ def test_llama_variant_parts_separately(n_kv, act):
     """GQA alone (GELU FFN) and SwiGLU alone (MHA) through MegatronTS at P = 2."""
     _check_layer(0, 2, 1024, 8, 2048, 1024, seed=19, n_kv=n_kv, act=act)
 
+
+
+# ---------------------------------------------------------------- varlen packing (NEXT-3)
+@pytest.mark.parametrize("pi", [0, 1, 2, 4])
+@pytest.mark.parametrize("P,lens,causal", [
+    (1, [256, 768, 512], True),
+    (2, [256, 768, 512, 512], True),      # sequences straddle the rank boundary
+    (2, [512, 1024, 512], False),
+    (4, [1280, 256, 512], True),
+])
+def test_varlen_layer(pi, P, lens, causal):
+    """Packed sequences (R-VARLEN): attention block-diagonal per sequence, RoPE
+    positions restarting per sequence, against the oracle layer per sequence."""
+    chunks = 2 if pi in (2, 4) else 0
+    _check_layer(pi, P, 512, 4, 2048, sum(lens), seed=23, chunks=chunks, causal=causal, varlen=lens)
+
+
+def test_varlen_llama_variant():
+    """Packing together with GQA + SwiGLU (the Llama variant) through UlyssesZ at P = 2."""
+    _check_layer(1, 2, 1024, 8, 1536, 2048, seed=29, n_kv=2, act="swiglu", varlen=[768, 256, 1024])
+
+
+def test_varlen_argument_errors():
+    ctx = B.Context(B.Model(h=256, n_heads=4, ffn=1024))
+    with pytest.raises(B.PdsError) as e:
+        ctx.set_varlen([256, 300])
+    assert e.value.code == -2                             # every sequence a multiple of 256
+    ctx.set_varlen([256, 512])
+    d = layer_inputs(256, 4, 1024, 768, 1, seed=3)
+    W = OS.shard_weights(d, 4, 1)
+    R = Rank(W, 0, d["x"], d["dy"])
+    y = torch.empty_like(R.x)
+    with pytest.raises(B.PdsError) as e:                  # seq_len must be the packed total
+        ctx.layer_fwd(0, 1024, R.x.data_ptr(), R.weights(), y.data_ptr(), 0)
+    assert e.value.code == -1
+    for pi in (3, 5):
+        with pytest.raises(B.PdsError) as e:
+            ctx.layer_fwd(pi, 768, R.x.data_ptr(), R.weights(), y.data_ptr(), 0)
+        assert e.value.code == -9
+    ctx.set_varlen([])                                    # back to one sequence
+    sv = ctx.layer_fwd(0, 768, R.x.data_ptr(), R.weights(), y.data_ptr(), 0)
+    ctx.saved_release(sv)
+    ctx.close()
+    with pytest.raises(B.PdsError) as e:
+        B.Context(B.Model(h=256, n_heads=4, ffn=1024, batch=2)).set_varlen([256])
+    assert e.value.code == -1

@@ -296,3 +296,55 @@ def test_llama_finite_differences():
             fd = (loss(dp) - loss(dm)) / (2 * eps)
             an = g[gkey][idx]
             assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (key, idx, fd, an)
+
+
+# ---------------------------------------------------------------- varlen packing (NEXT-3)
+def _torch_packed(x, w_qkv, w_proj, w_in, w_out, g1, g2, n, lens, causal=True, eps=1e-5):
+    """Independent torch fp64 route for a PACKED stream: one SDPA call over all T tokens
+    with a block-diagonal (causal) boolean mask and RoPE positions that restart at every
+    sequence start (the packing semantics, written the other way round)."""
+    import torch.nn.functional as F
+    T, b, h = x.shape
+    d = h // n
+    u = F.rms_norm(x, (h,), g1, eps=eps)
+    q, k, v = (u @ w_qkv).split(h, dim=-1)
+    heads = lambda t: t.reshape(T, b, n, d).permute(1, 2, 0, 3)  # noqa: E731
+    q, k, v = heads(q), heads(k), heads(v)
+    seq = torch.repeat_interleave(torch.arange(len(lens)), torch.tensor(lens))
+    starts = torch.tensor(np.concatenate([[0], np.cumsum(lens)[:-1]]))
+    pos = (torch.arange(T) - starts[seq]).to(torch.float64)
+    inv = 10000.0 ** (-2 * torch.arange(d // 2, dtype=torch.float64) / d)
+    ang = pos[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], -1)
+    sin = torch.cat([ang.sin(), ang.sin()], -1)
+    def rot(t):
+        t1, t2 = t[..., : d // 2], t[..., d // 2:]
+        return t * cos + torch.cat([-t2, t1], -1) * sin
+    allowed = seq[:, None] == seq[None, :]
+    if causal:
+        allowed &= torch.arange(T)[None, :] <= torch.arange(T)[:, None]
+    a = F.scaled_dot_product_attention(rot(q), rot(k), v, attn_mask=allowed)
+    x1 = x + a.permute(2, 0, 1, 3).reshape(T, b, h) @ w_proj
+    return x1 + F.gelu(F.rms_norm(x1, (h,), g2, eps=eps) @ w_in) @ w_out
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_varlen_layer_vs_torch_packed(causal):
+    lens = [5, 1, 7, 3]
+    d = _inputs(h=16, n=4, ffn=48, s=sum(lens), b=1, seed=29)
+    kw = dict(n=4, causal=causal)
+    y, cs = L.layer_fwd_varlen(d["x"], lens, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    g = L.layer_bwd_varlen(d["dy"], cs, lens, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    names = ["x", "w_qkv", "w_proj", "w_in", "w_out", "g1", "g2"]
+    tt = {k: torch.tensor(d[k], dtype=torch.float64, requires_grad=True) for k in names}
+    yt = _torch_packed(*(tt[k] for k in names), n=4, lens=lens, causal=causal)
+    assert np.allclose(yt.detach().numpy(), y, rtol=1e-12, atol=1e-12)
+    yt.backward(torch.tensor(d["dy"]))
+    for k, gk in [("x", "dx"), ("w_qkv", "dw_qkv"), ("w_in", "dw_in"), ("w_out", "dw_out"), ("g1", "dg1")]:
+        ref = tt[k].grad.numpy()
+        assert np.linalg.norm(ref - g[gk]) / np.linalg.norm(ref) < 1e-12, k
+    # one sequence is the plain layer
+    y1, _ = L.layer_fwd_varlen(d["x"], [sum(lens)], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"],
+                               d["g2"], **kw)
+    y2, _ = L.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    assert np.array_equal(y1, y2)
