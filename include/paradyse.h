@@ -96,8 +96,7 @@ typedef struct {
                               PDS_METP behaves as PDS_METP_FULL); else EINVAL.
                               PDS_METP_FULL always recomputes Q/K/V.          */
   /* Llama variant (the paper's LLaMA, Table 4, PAPER.md:317;
-   * readings R-GQA / R-SWIGLU).  Runs on MegatronTS, UlyssesZ, METP and METP-full;
-   * MegatronCZ / ColossalZ return PDS_ENOTIMPL for it (the planner skips them). */
+   * readings R-GQA / R-SWIGLU), on every strategy. */
   int32_t n_kv_heads;     /* key/value heads (GQA): 0 -> n_heads (MHA); must
                               divide n_heads and be divisible by P           */
   int32_t ffn_act;        /* 0 = GELU (Eq. 4), 1 = SwiGLU: FFN(v) = (SiLU(v W_gate)

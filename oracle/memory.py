@@ -13,7 +13,7 @@ this build reads M analytically (R-22, SURVEY O-6):
           COL  = 6u + (F/h)u + 2l + n (s/P) s b 2   ColossalZ (RSA): the probabilities instead of LSE
   plan    sum_l (W + saved_{pi_l}) + max_{pi in plan} workspace_pi + reserve < capacity (R-22)
 
-Llama variant (NEXT-3, R-GQA / R-SWIGLU; TS, UZ, METP, METP-full): the saved Q/K/V
+Llama variant (NEXT-3, R-GQA / R-SWIGLU; every strategy): the saved Q/K/V
 is (n + 2 n_kv)/n x 3u/3 = q u with q = (n + 2 n_kv)/n instead of 3u, the saved FFN
 pre-activation H is (2F/h) u ([gate | up]) instead of (F/h) u, and the weights are
 W = (q h^2 + h^2 + 3hF)/P (2 + 4) + 2h (2 + 4).
@@ -45,8 +45,6 @@ def persistent(h, ffn, P, n=None, n_kv=None, act="gelu"):
 def saved(pi, h, n, ffn, s, P, b=1, metp_recompute="ffn", n_kv=None, act="gelu"):
     u, l, lam = units(h, n, s, P, b)
     nk = n if n_kv is None else n_kv
-    if (nk != n or act != "gelu") and pi in (CZ, COL):
-        raise NotImplementedError("MegatronCZ / ColossalZ: MHA + GELU only")
     qkv = (s // P) * b * (n + 2 * nk) * (h // n) * 2       # local Q | K | V rows (3u for MHA)
     hb = (s // P) * b * (2 if act == "swiglu" else 1) * ffn * 2   # FFN pre-activation H
     if pi == TS or pi == CZ:           # CZ saves its local rows of the same tensors
@@ -67,13 +65,12 @@ def valid(pi, h, n, ffn, s, P, metp_chunks=None, n_kv=None, act="gelu"):
     P | s, P | n, 128 | s/P (tile rows), 64 | F/P, for METP / METP-full also
     c | s/P and 128 | s/(P c) (c = metp_chunks, default P), and for MegatronCZ
     128 | s/(2P) (its zigzag half-chunks, R-CZ); the Llama variant (GQA n_kv, SwiGLU)
-    needs P | n_kv, n_kv | n and runs on TS / UZ / METP / METP-full.  Never padded."""
+    needs P | n_kv, n_kv | n.  Never padded."""
     if s <= 0 or s % P or n % P or (s // P) % 128 or ffn % P or (ffn // P) % 64:
         return False
     nk = n if n_kv is None else n_kv
-    if nk != n or act != "gelu":       # Llama variant: P | n_kv, n_kv | n; TS / UZ / METP only
-        if nk % P or n % nk or pi in (CZ, COL):
-            return False
+    if nk % P or n % nk:               # Llama variant (GQA): P | n_kv, n_kv | n
+        return False
     if pi in (METP, METP_FULL):
         c = metp_chunks or P
         sl = s // P

@@ -43,8 +43,7 @@ class Cfg:
     def __init__(self, h, n, ffn, causal=True, eps=EPS, theta=ROPE_THETA, metp_chunks=None,
                  metp_recompute="ffn", n_kv=None, act="gelu"):
         self.h, self.n, self.ffn = h, n, ffn
-        # Llama variant (NEXT-3, R-GQA / R-SWIGLU): MegatronTS, UlyssesZ, METP and
-        # METP-full run it; MegatronCZ / ColossalZ are MHA + GELU only
+        # Llama variant (NEXT-3, R-GQA / R-SWIGLU), every strategy
         self.n_kv = n if n_kv is None else n_kv
         self.act = act
         self.causal, self.eps, self.theta = causal, eps, theta
@@ -80,11 +79,6 @@ def _act(h, cfg):
 
 def _act_bwd(dg, h, cfg):
     return ffn_act_bwd(dg, h, cfg.act, il=True)
-
-
-def _mha_only(cfg, who):
-    if cfg.n_kv != cfg.n or cfg.act != "gelu":
-        raise NotImplementedError(f"{who}: MHA + GELU only (the Llama variant runs on TS, UZ, METP)")
 
 
 def _zero_grads(W):
@@ -455,18 +449,30 @@ def metp_bwd(grid, dys, saved, W, cfg, grads):
 # weight is [Q all; K all; V all] (one attention call over all heads), and its
 # gradient is reduce-scattered part by part back into the spec layout.
 
-def _gather_qkv_parts(grid, W, h):
+def _gather_qkv_parts(grid, W, h, n=None, n_kv=None):
+    """3 x AG of the spec shards' Q, K, V rows -> [Q all; K all; V all] ([(n + 2 n_kv) d, h];
+    GQA: the K and V parts are n_kv d / P rows per shard)."""
     P = grid.p
     hl = h // P
-    parts = [grid.all_gather([W["w_qkv_t"][r][i * hl:(i + 1) * hl] for r in range(P)])[0]
-             for i in range(3)]                                    # 3 x AG: Q, K, V rows
-    return np.concatenate(parts, axis=0)                           # [3h, h], [Q all; K all; V all]
+    hkl = hl if n is None or n_kv is None else n_kv * (h // n) // P
+    bounds = [(0, hl), (hl, hl + hkl), (hl + hkl, hl + 2 * hkl)]
+    parts = [grid.all_gather([W["w_qkv_t"][r][a:b] for r in range(P)])[0] for a, b in bounds]
+    return np.concatenate(parts, axis=0)
 
 
-# ------------------------------------------------------------------ MegatronCZ (ring, zigzag)
-# Reading R-CZ: Megatron-LM context parallelism + ZeRO3 weights.  Every
-# GEMM is local on the rank's boundary rows [r s/P, (r+1) s/P) (R-10, kept unchanged
-# so switching needs no redistribution).  Attention alone runs on a
+def _rep_kv(x, grp):
+    """GQA: key / value heads [b, n_kv, rows, d] -> one copy per query head [b, n, rows, d]."""
+    return np.repeat(x, grp, axis=1) if grp > 1 else x
+
+
+def _fold_kv(g, grp):
+    """GQA: per-query-head gradients [b, n, rows, d] -> summed per key / value head."""
+    if grp == 1:
+        return g
+    b, n, rows, d = g.shape
+    return g.reshape(b, n // grp, grp, rows, d).sum(axis=2)
+
+
 # causally balanced ("zigzag") placement: the s positions are cut into 2P half-chunks
 # of c = s/(2P); rank r computes the queries of half-chunks r and 2P-1-r, which it
 # receives (with their K, V) by point-to-point sends from their boundary owners, and
@@ -572,15 +578,15 @@ def _pair_bwd(q, k, v, do, lse, D, pq, pk, causal):
 
 
 def cz_fwd(grid, xs, W, cfg):
-    _mha_only(cfg, "MegatronCZ")
     P = grid.p
     sl = xs[0].shape[0]
     s = sl * P
-    h, n = cfg.h, cfg.n
+    h, n, nk = cfg.h, cfg.n, cfg.n_kv
+    grp = n // nk
     c = sl // 2
     if sl % 2:
         raise ValueError("MegatronCZ: s must be divisible by 2P (zigzag half-chunks)")
-    wq = _gather_qkv_parts(grid, W, h)
+    wq = _gather_qkv_parts(grid, W, h, n, nk)
     wp = grid.all_gather(W["w_proj"])[0]
     wi = grid.all_gather(W["w_in_t"])[0]
     wo = grid.all_gather(W["w_out"])[0]
@@ -590,11 +596,12 @@ def cz_fwd(grid, xs, W, cfg):
     for r in range(P):
         ur, _, rr = rmsnorm(xs[r], W["g1"][r], cfg.eps)
         r1.append(rr)
-        qkv = ur @ wq.T                                            # [s/P, b, 3h], [Q | K | V] all heads
+        qkv = ur @ wq.T                                            # [s/P, b, h + 2 hk], [Q | K | V] all heads
+        hk = nk * d
         cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
         qr = _unheads(rope_apply(_heads(qkv[..., :h], n), cos, sin))
-        kr = _unheads(rope_apply(_heads(qkv[..., h:2 * h], n), cos, sin))
-        qkv_b.append(np.concatenate([qr, kr, qkv[..., 2 * h:]], axis=-1))   # RoPE at global positions
+        kr = _unheads(rope_apply(_heads(qkv[..., h:h + hk], nk), cos, sin))
+        qkv_b.append(np.concatenate([qr, kr, qkv[..., h + hk:]], axis=-1))   # RoPE at global positions
     qkvz = _to_zigzag(grid, qkv_b)                                 # SendRecv(QKV): boundary -> zigzag
     pos = [_zig_positions(r, P, c) for r in range(P)]
     q = [_heads(qkvz[r][..., :h], n) for r in range(P)]
@@ -604,8 +611,8 @@ def cz_fwd(grid, xs, W, cfg):
     l_acc = [np.full(q[r].shape[:-1], -np.inf) for r in range(P)]
     for k in range(P):
         for r in range(P):
-            kk = _heads(kv[r][..., :h], n)
-            vv = _heads(kv[r][..., h:], n)
+            kk = _rep_kv(_heads(kv[r][..., :nk * d], nk), grp)
+            vv = _rep_kv(_heads(kv[r][..., nk * d:], nk), grp)
             for ai in range(2):
                 qa = slice(ai * c, (ai + 1) * c)
                 for bi in range(2):
@@ -627,7 +634,7 @@ def cz_fwd(grid, xs, W, cfg):
         x1 = xs[r] + o_r
         vr, _, rr2 = rmsnorm(x1, W["g2"][r], cfg.eps)
         hp = vr @ wi.T
-        z_r = gelu(hp) @ wo
+        z_r = _act(hp, cfg) @ wo
         o.append(o_r)
         z.append(z_r)
         y.append(x1 + z_r)
@@ -644,14 +651,15 @@ def cz_fwd(grid, xs, W, cfg):
 
 
 def cz_bwd(grid, dys, saved, W, cfg, grads):
-    _mha_only(cfg, "MegatronCZ")
     P = grid.p
     sl = dys[0].shape[0]
-    h, n = cfg.h, cfg.n
+    h, n, nk = cfg.h, cfg.n, cfg.n_kv
+    grp = n // nk
     d = h // n
+    hk = nk * d
     c = sl // 2
     sv = saved
-    wq = _gather_qkv_parts(grid, W, h)
+    wq = _gather_qkv_parts(grid, W, h, n, nk)
     wp = grid.all_gather(W["w_proj"])[0]
     wi = grid.all_gather(W["w_in_t"])[0]
     wo = grid.all_gather(W["w_out"])[0]
@@ -661,8 +669,8 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
         hp = sv[r]["h"]
         v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
         dg = dys[r] @ wo.T
-        dh = dg * gelu_grad(hp)
-        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dh = _act_bwd(dg, hp, cfg)
+        dwo.append(np.tensordot(_act(hp, cfg), dys[r], axes=([0, 1], [0, 1])))
         dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
         xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
         dd, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
@@ -683,8 +691,8 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
     dq = [np.zeros_like(q[r]) for r in range(P)]
     for k in range(P):
         for r in range(P):
-            kk = _heads(kv[r][..., :h], n)
-            vv = _heads(kv[r][..., h:], n)
+            kk = _rep_kv(_heads(kv[r][..., :hk], nk), grp)
+            vv = _rep_kv(_heads(kv[r][..., hk:], nk), grp)
             dk_h = np.zeros_like(kk)
             dv_h = np.zeros_like(vv)
             for ai in range(2):
@@ -699,7 +707,8 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
                     dq[r][:, :, qa] += gq
                     dk_h[:, :, kb] += gk
                     dv_h[:, :, kb] += gv
-            dkv[r] = dkv[r] + np.concatenate([_unheads(dk_h), _unheads(dv_h)], axis=-1)
+            dkv[r] = dkv[r] + np.concatenate([_unheads(_fold_kv(dk_h, grp)), _unheads(_fold_kv(dv_h, grp))],
+                                             axis=-1)
         if k < P - 1:
             kv = grid.ring_pass(kv, bpe=2)
             kv_pos = [kv_pos[(r - 1) % P] for r in range(P)]
@@ -708,8 +717,8 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
     for r in range(P):
         cos, sin = rope_cos_sin(pos[r], d, cfg.theta)              # RoPE^T at the zigzag positions
         dqr = _unheads(rope_apply_t(dq[r], cos, sin))
-        dkr = _unheads(rope_apply_t(_heads(dkv[r][..., :h], n), cos, sin))
-        dqkvz.append(np.concatenate([dqr, dkr, dkv[r][..., h:]], axis=-1))
+        dkr = _unheads(rope_apply_t(_heads(dkv[r][..., :hk], nk), cos, sin))
+        dqkvz.append(np.concatenate([dqr, dkr, dkv[r][..., hk:]], axis=-1))
     dqkv = _from_zigzag(grid, dqkvz)                               # SendRecv(dQKV) -> boundary
     dx, dg1 = [], []
     for r in range(P):
@@ -721,8 +730,8 @@ def cz_bwd(grid, dys, saved, W, cfg, grads):
         dx.append(dx1[r] + dd)
         dg1.append(dgr)
     # ZeRO3 reduce-scatters (fp32): W_qkv^T part by part back into [Q_r; K_r; V_r]
-    qparts = [grid.reduce_scatter([dwq[r][i * h:(i + 1) * h] for r in range(P)], axis=0, bpe=4)
-              for i in range(3)]
+    qparts = [grid.reduce_scatter([dwq[r][a:b] for r in range(P)], axis=0, bpe=4)
+              for a, b in ((0, h), (h, h + hk), (h + hk, h + 2 * hk))]
     for r in range(P):
         grads["dw_qkv_t"][r] += np.concatenate([qparts[i][r] for i in range(3)], axis=0)
     for key, full in (("dw_proj", dwp), ("dw_in_t", dwi), ("dw_out", dwo)):
@@ -757,13 +766,14 @@ def _ring_blocks(grid, blocks, bpe):
 
 
 def colossal_fwd(grid, xs, W, cfg):
-    _mha_only(cfg, "ColossalZ")
     P = grid.p
     sl = xs[0].shape[0]
     s = sl * P
-    h, n = cfg.h, cfg.n
+    h, n, nk = cfg.h, cfg.n, cfg.n_kv
+    grp = n // nk
     d = h // n
-    wq = _gather_qkv_parts(grid, W, h)
+    hk = nk * d
+    wq = _gather_qkv_parts(grid, W, h, n, nk)
     wp = grid.all_gather(W["w_proj"])[0]
     wi = grid.all_gather(W["w_in_t"])[0]
     wo = grid.all_gather(W["w_out"])[0]
@@ -775,15 +785,16 @@ def colossal_fwd(grid, xs, W, cfg):
         qkv = ur @ wq.T
         cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
         qr = _unheads(rope_apply(_heads(qkv[..., :h], n), cos, sin))
-        kr = _unheads(rope_apply(_heads(qkv[..., h:2 * h], n), cos, sin))
-        qkv_b.append(np.concatenate([qr, kr, qkv[..., 2 * h:]], axis=-1))
+        kr = _unheads(rope_apply(_heads(qkv[..., h:h + hk], nk), cos, sin))
+        qkv_b.append(np.concatenate([qr, kr, qkv[..., h + hk:]], axis=-1))
     q = [_heads(qkv_b[r][..., :h], n) for r in range(P)]
     b = xs[0].shape[1]
     scores = [np.zeros((b, n, sl, s)) for _ in range(P)]
-    for k, kb in _ring_blocks(grid, [qkv_b[r][..., h:2 * h] for r in range(P)], 2):     # ring of K
+    for k, kb in _ring_blocks(grid, [qkv_b[r][..., h:h + hk] for r in range(P)], 2):    # ring of K
         for r in range(P):
             j = (r - k) % P
-            scores[r][..., j * sl:(j + 1) * sl] = np.einsum("bnqd,bnkd->bnqk", q[r], _heads(kb[r], n)) / np.sqrt(d)
+            scores[r][..., j * sl:(j + 1) * sl] = np.einsum("bnqd,bnkd->bnqk", q[r],
+                                                            _rep_kv(_heads(kb[r], nk), grp)) / np.sqrt(d)
     probs = []
     for r in range(P):
         sc = scores[r]
@@ -794,10 +805,10 @@ def colossal_fwd(grid, xs, W, cfg):
         e = np.exp(sc - m)
         probs.append(e / np.sum(e, axis=-1, keepdims=True))
     o = [np.zeros_like(q[r]) for r in range(P)]
-    for k, vb in _ring_blocks(grid, [qkv_b[r][..., 2 * h:] for r in range(P)], 2):      # ring of V
+    for k, vb in _ring_blocks(grid, [qkv_b[r][..., h + hk:] for r in range(P)], 2):     # ring of V
         for r in range(P):
             j = (r - k) % P
-            o[r] += np.einsum("bnqk,bnkd->bnqd", probs[r][..., j * sl:(j + 1) * sl], _heads(vb[r], n))
+            o[r] += np.einsum("bnqk,bnkd->bnqd", probs[r][..., j * sl:(j + 1) * sl], _rep_kv(_heads(vb[r], nk), grp))
     y, oo, z = [], [], []
     for r in range(P):
         a_r = _unheads(o[r])
@@ -805,7 +816,7 @@ def colossal_fwd(grid, xs, W, cfg):
         x1 = xs[r] + o_r
         vr, _, rr2 = rmsnorm(x1, W["g2"][r], cfg.eps)
         hp = vr @ wi.T
-        z_r = gelu(hp) @ wo
+        z_r = _act(hp, cfg) @ wo
         oo.append(o_r)
         z.append(z_r)
         y.append(x1 + z_r)
@@ -822,13 +833,14 @@ def colossal_fwd(grid, xs, W, cfg):
 
 
 def colossal_bwd(grid, dys, saved, W, cfg, grads):
-    _mha_only(cfg, "ColossalZ")
     P = grid.p
     sl = dys[0].shape[0]
-    h, n = cfg.h, cfg.n
+    h, n, nk = cfg.h, cfg.n, cfg.n_kv
+    grp = n // nk
     d = h // n
+    hk = nk * d
     sv = saved
-    wq = _gather_qkv_parts(grid, W, h)
+    wq = _gather_qkv_parts(grid, W, h, n, nk)
     wp = grid.all_gather(W["w_proj"])[0]
     wi = grid.all_gather(W["w_in_t"])[0]
     wo = grid.all_gather(W["w_out"])[0]
@@ -838,8 +850,8 @@ def colossal_bwd(grid, dys, saved, W, cfg, grads):
         hp = sv[r]["h"]
         v = _apply_norm(sv[r]["x1"], sv[r]["r2"], W["g2"][r])
         dg = dys[r] @ wo.T
-        dh = dg * gelu_grad(hp)
-        dwo.append(np.tensordot(gelu(hp), dys[r], axes=([0, 1], [0, 1])))
+        dh = _act_bwd(dg, hp, cfg)
+        dwo.append(np.tensordot(_act(hp, cfg), dys[r], axes=([0, 1], [0, 1])))
         dwi.append(np.tensordot(dh, v, axes=([0, 1], [0, 1])))
         xhat2 = sv[r]["x1"] * sv[r]["r2"][..., None]
         dd, dgr = rmsnorm_bwd(dh @ wi, xhat2, sv[r]["r2"], W["g2"][r])
@@ -851,30 +863,30 @@ def colossal_bwd(grid, dys, saved, W, cfg, grads):
     D = [np.sum(do_h[r] * _heads(sv[r]["a"], n), axis=-1) for r in range(P)]
     probs = [sv[r]["probs"] for r in range(P)]
     dp = [np.zeros_like(probs[r]) for r in range(P)]
-    dvacc = [np.zeros_like(sv[r]["qkv"][..., 2 * h:]) for r in range(P)]
-    for k, vb in _ring_blocks(grid, [sv[r]["qkv"][..., 2 * h:] for r in range(P)], 2):  # ring of V
+    dvacc = [np.zeros_like(sv[r]["qkv"][..., h + hk:]) for r in range(P)]
+    for k, vb in _ring_blocks(grid, [sv[r]["qkv"][..., h + hk:] for r in range(P)], 2):  # ring of V
         for r in range(P):
             j = (r - k) % P
             blk = slice(j * sl, (j + 1) * sl)
-            dp[r][..., blk] = np.einsum("bnqd,bnkd->bnqk", do_h[r], _heads(vb[r], n))
-            dvacc[r] = dvacc[r] + _unheads(np.einsum("bnqk,bnqd->bnkd", probs[r][..., blk], do_h[r]))
+            dp[r][..., blk] = np.einsum("bnqd,bnkd->bnqk", do_h[r], _rep_kv(_heads(vb[r], nk), grp))
+            dvacc[r] = dvacc[r] + _unheads(_fold_kv(np.einsum("bnqk,bnqd->bnkd", probs[r][..., blk], do_h[r]), grp))
         dvacc = grid.ring_pass(dvacc, bpe=4)                        # dV partials travel home (P passes)
     ds = [probs[r] * (dp[r] - D[r][..., None]) / np.sqrt(d) for r in range(P)]
     q = [_heads(sv[r]["qkv"][..., :h], n) for r in range(P)]
     dq = [np.zeros_like(q[r]) for r in range(P)]
-    dkacc = [np.zeros_like(sv[r]["qkv"][..., h:2 * h]) for r in range(P)]
-    for k, kb in _ring_blocks(grid, [sv[r]["qkv"][..., h:2 * h] for r in range(P)], 2):  # ring of K
+    dkacc = [np.zeros_like(sv[r]["qkv"][..., h:h + hk]) for r in range(P)]
+    for k, kb in _ring_blocks(grid, [sv[r]["qkv"][..., h:h + hk] for r in range(P)], 2):  # ring of K
         for r in range(P):
             j = (r - k) % P
             blk = slice(j * sl, (j + 1) * sl)
-            dq[r] += np.einsum("bnqk,bnkd->bnqd", ds[r][..., blk], _heads(kb[r], n))
-            dkacc[r] = dkacc[r] + _unheads(np.einsum("bnqk,bnqd->bnkd", ds[r][..., blk], q[r]))
+            dq[r] += np.einsum("bnqk,bnkd->bnqd", ds[r][..., blk], _rep_kv(_heads(kb[r], nk), grp))
+            dkacc[r] = dkacc[r] + _unheads(_fold_kv(np.einsum("bnqk,bnqd->bnkd", ds[r][..., blk], q[r]), grp))
         dkacc = grid.ring_pass(dkacc, bpe=4)
     dx, dg1 = [], []
     for r in range(P):
         cos, sin = rope_cos_sin(np.arange(r * sl, (r + 1) * sl), d, cfg.theta)
         dqkv = np.concatenate([_unheads(rope_apply_t(dq[r], cos, sin)),
-                               _unheads(rope_apply_t(_heads(dkacc[r], n), cos, sin)), dvacc[r]], axis=-1)
+                               _unheads(rope_apply_t(_heads(dkacc[r], nk), cos, sin)), dvacc[r]], axis=-1)
         u = _apply_norm(sv[r]["x"], sv[r]["r1"], W["g1"][r])
         dwq.append(np.tensordot(dqkv, u, axes=([0, 1], [0, 1])))
         du = dqkv @ wq
@@ -882,8 +894,8 @@ def colossal_bwd(grid, dys, saved, W, cfg, grads):
         dd, dgr = rmsnorm_bwd(du, xhat1, sv[r]["r1"], W["g1"][r])
         dx.append(dx1[r] + dd)
         dg1.append(dgr)
-    qparts = [grid.reduce_scatter([dwq[r][i * h:(i + 1) * h] for r in range(P)], axis=0, bpe=4)
-              for i in range(3)]
+    qparts = [grid.reduce_scatter([dwq[r][a:b] for r in range(P)], axis=0, bpe=4)
+              for a, b in ((0, h), (h, h + hk), (h + hk, h + 2 * hk))]
     for r in range(P):
         grads["dw_qkv_t"][r] += np.concatenate([qparts[i][r] for i in range(3)], axis=0)
     for key, full in (("dw_proj", dwp), ("dw_in_t", dwi), ("dw_out", dwo)):

@@ -150,8 +150,11 @@ def make_layer_buffers(torch, model, P, s, seed=0):
     sl = s // P
     def rn(*shape, std=1.0):
         return (torch.randn(*shape, generator=g, device="cuda") * std).to(torch.bfloat16)
-    w = dict(w_qkv_t=rn(3 * h // P, h, std=h ** -0.5), w_proj=rn(h // P, h, std=h ** -0.5),
-             w_in_t=rn(F // P, h, std=h ** -0.5), w_out=rn(F // P, h, std=F ** -0.5),
+    n, nk = model.n_heads, (getattr(model, "n_kv_heads", 0) or model.n_heads)
+    qrows = (n + 2 * nk) * (h // n) // P                      # GQA: (n + 2 n_kv) d / P
+    frows = (2 if getattr(model, "ffn_act", 0) == 1 else 1) * F // P   # SwiGLU: [gate | up]
+    w = dict(w_qkv_t=rn(qrows, h, std=h ** -0.5), w_proj=rn(h // P, h, std=h ** -0.5),
+             w_in_t=rn(frows, h, std=h ** -0.5), w_out=rn(F // P, h, std=F ** -0.5),
              g1=(1 + 0.1 * torch.randn(h, generator=g, device="cuda")).to(torch.bfloat16),
              g2=(1 + 0.1 * torch.randn(h, generator=g, device="cuda")).to(torch.bfloat16))
     gr = {k: torch.zeros(v.shape, dtype=torch.float32, device="cuda") for k, v in

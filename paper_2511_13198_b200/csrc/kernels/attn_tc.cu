@@ -1077,7 +1077,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
     const int key = k0 + t;
     if (acc) {
       // accumulate mode (ring attention): dK (scaled, no RoPE^T) at columns head*D and
-      // dV at heads*D + head*D of the fp32 row, added to what is there
+      // dV at kv_heads*D + head*D of the fp32 row (head = the key / value head), added
+      // to what is there
       float* arow = acc + (int64_t)key * ld_acc + head * D;
       for (int task = wg; task < 2 * (D / 32); task += NWG) {
         const int kv = task / (D / 32), c = task % (D / 32);
@@ -1085,7 +1086,7 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         tmem_ld32(lb + (kv ? DV_COL : DK_COL) + c * 32, r);
         tmem_ld_wait();
         const float sc = kv ? 1.0f : scale;
-        float4* d4 = reinterpret_cast<float4*>(arow + kv * heads * D + c * 32);
+        float4* d4 = reinterpret_cast<float4*>(arow + kv * (heads / grp) * D + c * 32);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float4 v = d4[e];
@@ -2018,13 +2019,16 @@ int attn_fwd_tc(const void* qkv, int64_t ld, int s, int heads, int d, int causal
 // aligned positions), else every key is visible.  out / lse as attn_fwd_tc (the pair's
 // own softmax; pairs merge by log-sum-exp).
 int attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, int sq, int sk,
-                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st) {
+                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st, int kv_heads) {
+  if (kv_heads <= 0) kv_heads = heads;
   if (sq % 128 || sk % 128 || sq <= 0 || sk <= 0 || ld_q % 8 || ld_kv % 8 || kcol % 8 || vcol % 8 ||
-      (causal && sq != sk))
+      (causal && sq != sk) || heads % kv_heads)
     return (int)cudaErrorInvalidValue;
+  const int grp = heads / kv_heads;
   if (d == 128)
-    return fwd_tc_t<128>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st);
-  if (d == 64) return fwd_tc_t<64>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st);
+    return fwd_tc_t<128>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st, grp);
+  if (d == 64)
+    return fwd_tc_t<64>(q, ld_q, sq, kv, ld_kv, kcol, vcol, sk, heads, causal, out, ld_out, lse, 0, sq, st, grp);
   return (int)cudaErrorInvalidValue;
 }
 
@@ -2136,16 +2140,18 @@ int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, c
 // (scaled) / dV into dkv_acc [sk][2*heads*d] fp32; RoPE^T is the caller's.
 int attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, const void* dout,
                   int64_t ld_out, const void* lse, const float* Dd, int sq, int sk, int heads, int d, int causal,
-                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st) {
+                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int kv_heads) {
+  if (kv_heads <= 0) kv_heads = heads;
   if (sq % 128 || sk % 128 || sq <= 0 || sk <= 0 || ld_q % 8 || ld_kv % 8 || ld_out % 8 || kcol % 8 || vcol % 8 ||
-      ld_dqa % 4 || ld_dkva % 4 || (causal && sq != sk) || !dq_acc || !dkv_acc)
+      ld_dqa % 4 || ld_dkva % 4 || (causal && sq != sk) || !dq_acc || !dkv_acc || heads % kv_heads)
     return (int)cudaErrorInvalidValue;
+  const int grp = heads / kv_heads;
   if (d == 128)
     return bwd_tc_t<128>(q, ld_q, sq, kv, ld_kv, kcol, vcol, dout, ld_out, lse, Dd, sk, heads, causal, nullptr, 0,
-                         nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st);
+                         nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st, grp);
   if (d == 64)
     return bwd_tc_t<64>(q, ld_q, sq, kv, ld_kv, kcol, vcol, dout, ld_out, lse, Dd, sk, heads, causal, nullptr, 0,
-                        nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st);
+                        nullptr, 0, sq, dq_acc, ld_dqa, dkv_acc, ld_dkva, st, grp);
   return (int)cudaErrorInvalidValue;
 }
 }  // namespace pds

@@ -32,10 +32,12 @@ int attn_bwd_rows(const void* qkv, int64_t ld, const void* out, int64_t ld_out, 
 // mode, the log-sum-exp merge of pair results, the RoPE^T + bf16 conversion of the
 // accumulated gradients, and D = rowsum(dO o O)
 int attn_fwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, int sq, int sk,
-                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st);
+                  int heads, int d, int causal, void* out, int64_t ld_out, void* lse, cudaStream_t st,
+                  int kv_heads = 0);
 int attn_bwd_pair(const void* q, int64_t ld_q, const void* kv, int64_t ld_kv, int kcol, int vcol, const void* dout,
                   int64_t ld_out, const void* lse, const float* Dd, int sq, int sk, int heads, int d, int causal,
-                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st);
+                  float* dq_acc, int64_t ld_dqa, float* dkv_acc, int64_t ld_dkva, cudaStream_t st,
+                  int kv_heads = 0);
 int attn_merge(float* o_acc, int64_t ld_oacc, float* l_acc, int64_t lstride_acc, const void* o_p, int64_t ld_op,
                const float* l_p, int64_t lstride_p, int rows, int heads, int d, int first, void* out, int64_t ld_out,
                cudaStream_t st);

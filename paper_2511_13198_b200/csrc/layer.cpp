@@ -344,12 +344,14 @@ struct Exec {
     g.M = (int)M; g.N = (int)N; g.K = (int)K; g.C = C; g.ldc = ldc; g.epi = epi;
     return g;
   }
-  GemmArgs rope(GemmArgs g, int64_t hq, int64_t seg, int64_t seg_stride, int64_t seg_base) {
+  // hq / hk: the Q and the K (= V) widths of one [Q | K | V] column group (the local
+  // head group for TS / METP / UlyssesZ, all heads for MegatronCZ / ColossalZ)
+  GemmArgs rope(GemmArgs g, int64_t hq, int64_t hk, int64_t seg, int64_t seg_stride, int64_t seg_base) {
     g.epi = EPI_ROPE;
     g.rope = reinterpret_cast<const float2*>(c->rope);
     g.rope_d = (int)d;
-    g.rope_hq = (int)hq;                 // local Q width; K / V columns: nkl heads each
-    g.rope_hk = (int)(nkl * d);
+    g.rope_hq = (int)hq;
+    g.rope_hk = (int)hk;
     g.seg = seg; g.seg_stride = seg_stride; g.seg_base = seg_base;
     g.rope_b = (int)b;                 // row -> position: the mapped row / b
     g.rope_segs = segs;                // varlen: positions restart at every sequence
@@ -536,7 +538,7 @@ pds_status ts_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, gather + slot, sv->at("rstd1")));
   PDS_TRY(ov ? e.ag_next(gather, n) : e.ag(gather + slot, gather, n));                // AG(u)
   PDS_TRY(e.gemm(e.rope(Exec::G(gather, e.h, 0, w->w_qkv_t, e.h, 0, e.s, e.qw, e.h, sv->at("qkv"), e.qw),
-                        e.hl, 0, 0, 0)));                                                // Eq. 1 + RoPE
+                        e.hl, e.nkl * e.d, 0, 0, 0)));                                                // Eq. 1 + RoPE
   PDS_TRY(e.attn_f(sv->at("qkv"), sv->at("a"), sv->at("lse")));                          // Eq. 2
   if (ov) PDS_TRY(e.rs_arm(e.h));
   PDS_TRY(tn.xw(sv->at("a"), e.hl, w->w_proj, e.h, e.s, e.h, e.hl, partial, e.h));      // Eq. 3
@@ -665,7 +667,8 @@ pds_status uz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
   // local QKV for all heads, head-group-major columns, written straight into the A2A
   // send layout [P][s/P][3h/P]; RoPE at global positions r*s/P + t
-  GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, e.qwf, e.h, s1, e.qw), e.hl, 0, 0, e.r * e.sl);
+  GemmArgs q = e.rope(Exec::G(u1, e.h, 0, wqkv, e.h, 0, e.sl, e.qwf, e.h, s1, e.qw), e.hl, e.nkl * e.d, 0, 0,
+                      e.r * e.sl);
   q.blk_w = (int)e.qw;
   q.blk_stride = e.sl * e.qw;
   // P > 1: block j of the packed output leaves for rank j as soon as its tiles are stored
@@ -779,11 +782,16 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
 // part (the Q, K, V rows of every spec shard) into [Q all; K all; V all], so the local
 // QKV GEMM yields all heads; its gradient is reduce-scattered part by part back into
 // the spec layout.
+// GQA (R-GQA): the K and V parts are n_kv d / P rows per shard, n_kv d in the gather.
 pds_status cz_wqkv(Exec& e, const pds_weights* w, char* wqkv, cudaStream_t on) {
-  for (int i = 0; i < 3; ++i)
-    PDS_TRY(on == e.st ? e.ag(static_cast<const char*>(w->w_qkv_t) + i * e.hl * e.h * 2, wqkv + i * e.h * e.h * 2, e.hl * e.h)
-                       : e.ag_on(on, static_cast<const char*>(w->w_qkv_t) + i * e.hl * e.h * 2, wqkv + i * e.h * e.h * 2,
-                                 e.hl * e.h));
+  const int64_t hkl = e.nkl * e.d, hk = hkl * e.P;
+  const int64_t src_off[3] = {0, e.hl * e.h, (e.hl + hkl) * e.h};   // within the spec shard
+  const int64_t dst_off[3] = {0, e.h * e.h, (e.h + hk) * e.h};      // [Q all; K all; V all]
+  const int64_t cnt[3] = {e.hl * e.h, hkl * e.h, hkl * e.h};
+  for (int i = 0; i < 3; ++i) {
+    const char* src = static_cast<const char*>(w->w_qkv_t) + src_off[i] * 2;
+    PDS_TRY(on == e.st ? e.ag(src, wqkv + dst_off[i] * 2, cnt[i]) : e.ag_on(on, src, wqkv + dst_off[i] * 2, cnt[i]));
+  }
   return PDS_OK;
 }
 
@@ -828,6 +836,7 @@ pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
   const int64_t n = e.m.n_heads, h = e.h;
+  const int64_t hk = e.nkl * e.d * e.P, qw = e.qwf;      // K (V) width, [Q | K | V] width (GQA: n_kv d)
   const Zig z{e.P, e.r, e.sp / 2, e.sl / 2};
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
@@ -849,14 +858,14 @@ pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(cz_wqkv(e, w, wqkv, e.st));
   PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.f1w * h));
   PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * h));
   cudaEvent_t ev_ffn = e.mark(cs);
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
-  // local Q/K/V of all heads ([Q | K | V] column blocks of h), RoPE at global positions
-  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, 3 * h, h, qkvb, 3 * h), h, 0, 0, e.r * e.sl)));
-  PDS_TRY(zig_exchange(e, z, qkvb, qkvz, 3 * h, true));                                  // -> zig rows
-  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * h * 2, qkvz + h * 2, 3 * h * 2, 2 * h * 2, e.sl, cudaMemcpyDeviceToDevice,
+  // local Q/K/V of all heads ([Q (h) | K (hk) | V (hk)] column blocks), RoPE at global positions
+  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, qw, h, qkvb, qw), h, hk, 0, 0, e.r * e.sl)));
+  PDS_TRY(zig_exchange(e, z, qkvb, qkvz, qw, true));                                     // -> zig rows
+  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * hk * 2, qkvz + h * 2, qw * 2, 2 * hk * 2, e.sl, cudaMemcpyDeviceToDevice,
                              e.st));
   // P ring steps; step k holds the K/V of rank r - k (its zig half-chunks), the next
   // block is received on the side stream while this one is computed
@@ -867,7 +876,7 @@ pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
     cudaEvent_t ev_next = nullptr;
     if (k + 1 < e.P) {
       PDS_TRY(e.link(e.st, cs));
-      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * h * 2, cs));
+      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * hk * 2, cs));
       ev_next = e.mark(cs);
     }
     const Zig zs{e.P, src, z.c, z.cb};
@@ -879,9 +888,10 @@ pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
         {
           Prof p(e.c, e.st, K_ATTN_F, e.b * 4.0 * n * e.d * (diag ? 0.5 * z.c * z.c : (double)z.c * z.c), 0);
           for (int64_t j = 0; j < e.b; ++j)
-            PDS_TRY(kerr(attn_fwd_pair(qkvz + ((ai * z.cb) + j) * 3 * h * 2, e.b * 3 * h,
-                                       kv + ((bi * z.cb) + j) * 2 * h * 2, e.b * 2 * h, 0, (int)h, (int)z.c, (int)z.c,
-                                       (int)n, (int)e.d, diag, op + j * h * 2, e.b * h, lp + j * n * z.c, e.st),
+            PDS_TRY(kerr(attn_fwd_pair(qkvz + ((ai * z.cb) + j) * qw * 2, e.b * qw,
+                                       kv + ((bi * z.cb) + j) * 2 * hk * 2, e.b * 2 * hk, 0, (int)hk, (int)z.c,
+                                       (int)z.c, (int)n, (int)e.d, diag, op + j * h * 2, e.b * h, lp + j * n * z.c,
+                                       e.st, (int)(e.nkl * e.P)),
                          "attn_fwd_pair"));
         }
         Prof p(e.c, e.st, K_NORM, 0, (double)z.cb * h * 10);
@@ -904,7 +914,7 @@ pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sav
   PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), v2, sv->at("rstd2")));
   PDS_TRY(e.wait(e.st, ev_ffn));
-  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.F, h, sv->at("h"), e.F, EPI_GELU);
+  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.f1wf, h, sv->at("h"), e.f1wf, e.fc1_epi());
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
   PDS_TRY(tn.xw(f0, e.F, wout, h, e.sl, h, e.F, u1, h));                                // Z
@@ -917,6 +927,7 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
   const int64_t n = e.m.n_heads, h = e.h;
+  const int64_t hk = e.nkl * e.d * e.P, qw = e.qwf;
   const Zig z{e.P, e.r, e.sp / 2, e.sl / 2};
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
@@ -943,7 +954,7 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_TRY(e.link(e.st, cs));
   PDS_TRY(e.ag(w->w_out, wout, e.Fl * h));
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.f1w * h));
   cudaEvent_t ev_in = e.mark(cs);
   PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
@@ -951,8 +962,8 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   cudaEvent_t ev_qkv = e.mark(cs);
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * h * 4, e.st));
   // FFN: local with full weights (as UlyssesZ)
-  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.F, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.f1wf, e.dfc1_epi());
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F; dgel.ld_aux_in = e.f1wf;
   dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;                                 // G^T, dH^T
   PDS_TRY(e.gemm(dgel));
   PDS_TRY(tn.tr(dy, h, e.sl, h, tn.tb));
@@ -960,10 +971,10 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
   PDS_TRY(tn.tr(u1, h, e.sl, h, tn.tb));
-  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));                  // dW_in^T (full, local)
-  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.f1wf, h, e.sl, dw, h, EPI_F32));               // dW_in^T (full, local)
+  PDS_TRY(uz_dw(e, dw, e.f1wf, g->dw_in_t));
   PDS_TRY(e.wait(e.st, ev_in));
-  PDS_TRY(tn.xw(f1, e.F, win, h, e.sl, h, e.F, v2, h));
+  PDS_TRY(tn.xw(f1, e.f1wf, win, h, e.sl, h, e.f1wf, v2, h));
   PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + h));
   PDS_TRY(e.wait(e.st, ev_proj));
   PDS_TRY(e.gemm(Exec::G(dx, h, 0, wproj, h, 0, e.sl, h, h, da, h)));                  // dA = dX1 W_proj^T
@@ -980,8 +991,8 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
                               (int)n, (int)e.d, dd + (j * 2 + ai) * n * z.c, e.st), "attn_dot"));
   }
   PDS_CUDA(cudaMemsetAsync(dqacc, 0, e.sl * h * 4, e.st));
-  PDS_CUDA(cudaMemsetAsync(dkvb[0], 0, e.sl * 2 * h * 4, e.st));
-  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * h * 2, qkvz + h * 2, 3 * h * 2, 2 * h * 2, e.sl, cudaMemcpyDeviceToDevice,
+  PDS_CUDA(cudaMemsetAsync(dkvb[0], 0, e.sl * 2 * hk * 4, e.st));
+  PDS_CUDA(cudaMemcpy2DAsync(kvb[0], 2 * hk * 2, qkvz + h * 2, qw * 2, 2 * hk * 2, e.sl, cudaMemcpyDeviceToDevice,
                              e.st));
   int cur = 0;                                     // dK/dV accumulator of the block in hand
   for (int k = 0; k < e.P; ++k) {
@@ -990,7 +1001,7 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     cudaEvent_t ev_next = nullptr;
     if (k + 1 < e.P) {
       PDS_TRY(e.link(e.st, cs));
-      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * h * 2, cs));
+      PDS_TRY(ring_pass(e, kv, kvb[(k + 1) & 1], e.sl * 2 * hk * 2, cs));
       ev_next = e.mark(cs);
     }
     const Zig zs{e.P, src, z.c, z.cb};
@@ -1001,17 +1012,18 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
         const int diag = e.m.causal && kb == qa;
         Prof p(e.c, e.st, K_ATTN_B, e.b * 10.0 * n * e.d * (diag ? 0.5 * z.c * z.c : (double)z.c * z.c), 0);
         for (int64_t j = 0; j < e.b; ++j)
-          PDS_TRY(kerr(attn_bwd_pair(qkvz + ((ai * z.cb) + j) * 3 * h * 2, e.b * 3 * h,
-                                     kv + ((bi * z.cb) + j) * 2 * h * 2, e.b * 2 * h, 0, (int)h,
+          PDS_TRY(kerr(attn_bwd_pair(qkvz + ((ai * z.cb) + j) * qw * 2, e.b * qw,
+                                     kv + ((bi * z.cb) + j) * 2 * hk * 2, e.b * 2 * hk, 0, (int)hk,
                                      doz + ((ai * z.cb) + j) * h * 2, e.b * h, lse + (j * 2 + ai) * n * z.c,
                                      dd + (j * 2 + ai) * n * z.c, (int)z.c, (int)z.c, (int)n, (int)e.d, diag,
                                      dqacc + ((ai * z.cb) + j) * h, e.b * h,
-                                     dkvb[cur] + ((bi * z.cb) + j) * 2 * h, e.b * 2 * h, e.st), "attn_bwd_pair"));
+                                     dkvb[cur] + ((bi * z.cb) + j) * 2 * hk, e.b * 2 * hk, e.st,
+                                     (int)(e.nkl * e.P)), "attn_bwd_pair"));
       }
     // the accumulator travels with its block: P passes bring it home
     if (e.P > 1) {
       PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dkvb[cur]), reinterpret_cast<char*>(dkvb[cur ^ 1]),
-                        e.sl * 2 * h * 4, e.st));
+                        e.sl * 2 * hk * 4, e.st));
       cur ^= 1;
     }
     if (ev_next) PDS_TRY(e.wait(e.st, ev_next));
@@ -1021,25 +1033,30 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
     Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 3 * h * 6);
     const int64_t b0 = z.hc(0) * z.c, b1 = z.hc(1) * z.c;
     PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)e.d, e.c->rope, b0, b1, (int)z.cb, (int)e.b,
-                                 dqkvz, 3 * h, e.st), "dq rope_t"));
-    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur], 2 * h, (int)e.sl, (int)h, (int)e.d, e.c->rope, b0, b1, (int)z.cb,
-                                 (int)e.b, dqkvz + h * 2, 3 * h, e.st), "dk rope_t"));
-    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur] + h, 2 * h, (int)e.sl, (int)h, (int)e.d, nullptr, 0, 0, (int)z.cb,
-                                 (int)e.b, dqkvz + 2 * h * 2, 3 * h, e.st), "dv convert"));
+                                 dqkvz, qw, e.st), "dq rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur], 2 * hk, (int)e.sl, (int)hk, (int)e.d, e.c->rope, b0, b1, (int)z.cb,
+                                 (int)e.b, dqkvz + h * 2, qw, e.st), "dk rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dkvb[cur] + hk, 2 * hk, (int)e.sl, (int)hk, (int)e.d, nullptr, 0, 0, (int)z.cb,
+                                 (int)e.b, dqkvz + (h + hk) * 2, qw, e.st), "dv convert"));
   }
-  PDS_TRY(zig_exchange(e, z, qkvb, dqkvz, 3 * h, false));                               // dQKV -> boundary
+  PDS_TRY(zig_exchange(e, z, qkvb, dqkvz, qw, false));                                  // dQKV -> boundary
   char* dqkv = qkvb;
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
-  PDS_TRY(tn.dw(dqkv, 3 * h, u1, h, e.sl, 3 * h, h, dw, EPI_F32));                      // [Q; K; V] all rows
-  for (int i = 0; i < 3; ++i) {       // ZeRO3 RS part by part into the spec shard [Q_r; K_r; V_r]
-    char* part = dw + i * h * h * 4;
-    const int64_t cnt = e.hl * h;
-    char* mine = part + e.r * cnt * 4;
-    PDS_TRY(e.rs(part, mine, cnt, DT_F32));
-    PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + i * cnt * 4, cnt, e.st), "add_f32"));
+  PDS_TRY(tn.dw(dqkv, qw, u1, h, e.sl, qw, h, dw, EPI_F32));                            // [Q; K; V] all rows
+  {                                   // ZeRO3 RS part by part into the spec shard [Q_r; K_r; V_r]
+    const int64_t hkl = e.nkl * e.d;
+    const int64_t part_off[3] = {0, h * h, (h + hk) * h};          // rows of [Q all; K all; V all]
+    const int64_t shard_off[3] = {0, e.hl * h, (e.hl + hkl) * h};  // rows of the spec shard
+    const int64_t cnts[3] = {e.hl * h, hkl * h, hkl * h};
+    for (int i = 0; i < 3; ++i) {
+      char* part = dw + part_off[i] * 4;
+      char* mine = part + e.r * cnts[i] * 4;
+      PDS_TRY(e.rs(part, mine, cnts[i], DT_F32));
+      PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + shard_off[i] * 4, cnts[i], e.st), "add_f32"));
+    }
   }
   PDS_TRY(e.wait(e.st, ev_qkv));
-  PDS_TRY(tn.xw(dqkv, 3 * h, wqkv, h, e.sl, h, 3 * h, v2, h));                          // dU
+  PDS_TRY(tn.xw(dqkv, qw, wqkv, h, e.sl, h, qw, v2, h));                                // dU
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -1060,13 +1077,13 @@ struct ColBufs {
 // block j (the rank whose K / V is in hand) of the key axis: columns [j sp, (j+1) sp)
 pds_status col_ring(Exec& e, const char* first, int64_t col_off, char* kr[2],
                     const std::function<pds_status(int k, int j, const char* blk)>& step) {
-  const int64_t h = e.h;
-  PDS_CUDA(cudaMemcpy2DAsync(kr[0], h * 2, first + col_off * 2, 3 * h * 2, h * 2, e.sl, cudaMemcpyDeviceToDevice,
+  const int64_t hk = e.nkl * e.d * e.P;                   // a K (V) block's width (GQA)
+  PDS_CUDA(cudaMemcpy2DAsync(kr[0], hk * 2, first + col_off * 2, e.qwf * 2, hk * 2, e.sl, cudaMemcpyDeviceToDevice,
                              e.st));
   for (int k = 0; k < e.P; ++k) {
     const int j = (e.r - k + e.P) % e.P;
     PDS_TRY(step(k, j, kr[k & 1]));
-    if (k + 1 < e.P) PDS_TRY(ring_pass(e, kr[k & 1], kr[(k + 1) & 1], e.sl * h * 2, e.st));
+    if (k + 1 < e.P) PDS_TRY(ring_pass(e, kr[k & 1], kr[(k + 1) & 1], e.sl * hk * 2, e.st));
   }
   return PDS_OK;
 }
@@ -1075,6 +1092,7 @@ pds_status col_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sa
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
   const int64_t n = e.m.n_heads, h = e.h, d = e.d, sp = e.sp, sq = e.sq, b = e.b;
+  const int64_t hk = e.nkl * d * e.P, qw = e.qwf, grp = n / (e.nkl * e.P);   // GQA widths
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
@@ -1092,17 +1110,17 @@ pds_status col_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sa
   PDS_TRY(cz_wqkv(e, w, wqkv, e.st));
   PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.f1w * h));
   PDS_TRY(e.ag_on(cs, w->w_out, wout, e.Fl * h));
   cudaEvent_t ev_ffn = e.mark(cs);
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, u1, sv->at("rstd1")));
-  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, 3 * h, h, qkv, 3 * h), h, 0, 0, e.r * e.sl)));
+  PDS_TRY(e.gemm(e.rope(Exec::G(u1, h, 0, wqkv, h, 0, e.sl, qw, h, qkv, qw), h, hk, 0, 0, e.r * e.sl)));
   // ring of K: scores of the own rows against key block j, per sequence and head
   PDS_TRY(col_ring(e, qkv, h, kr, [&](int, int j, const char* kb) -> pds_status {
     for (int64_t q = 0; q < b; ++q)
       for (int64_t hd = 0; hd < n; ++hd)
-        PDS_TRY(e.gemm(Exec::G(qkv + (q * 3 * h + hd * d) * 2, b * 3 * h, 0, kb + (q * h + hd * d) * 2, b * h, 0, sp,
-                               sp, d, scores + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
+        PDS_TRY(e.gemm(Exec::G(qkv + (q * qw + hd * d) * 2, b * qw, 0, kb + (q * hk + hd / grp * d) * 2, b * hk, 0,
+                               sp, sp, d, scores + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
     return PDS_OK;
   }));
   {
@@ -1112,11 +1130,11 @@ pds_status col_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sa
   }
   // ring of V: O += P_j V_j
   PDS_CUDA(cudaMemsetAsync(oacc, 0, e.sl * h * 4, e.st));
-  PDS_TRY(col_ring(e, qkv, 2 * h, kr, [&](int, int j, const char* vb) -> pds_status {
+  PDS_TRY(col_ring(e, qkv, h + hk, kr, [&](int, int j, const char* vb) -> pds_status {
     for (int64_t q = 0; q < b; ++q)
       for (int64_t hd = 0; hd < n; ++hd)
-        PDS_TRY(e.gemm(Exec::G(probs + ((q * n + hd) * sp * sq + j * sp) * 2, sq, 0, vb + (q * h + hd * d) * 2,
-                               b * h, 1, sp, d, sp, oacc + q * h + hd * d, b * h, EPI_F32_ACC)));
+        PDS_TRY(e.gemm(Exec::G(probs + ((q * n + hd) * sp * sq + j * sp) * 2, sq, 0, vb + (q * hk + hd / grp * d) * 2,
+                               b * hk, 1, sp, d, sp, oacc + q * h + hd * d, b * h, EPI_F32_ACC)));
     return PDS_OK;
   }));
   {
@@ -1129,7 +1147,7 @@ pds_status col_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_sa
   PDS_TRY(e.tap(e.c->tap_o, u1, e.sl * h));
   PDS_TRY(e.norm_fwd(x, u1, w->g2, e.sl, sv->at("x1"), v2, sv->at("rstd2")));
   PDS_TRY(e.wait(e.st, ev_ffn));
-  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.F, h, sv->at("h"), e.F, EPI_GELU);
+  GemmArgs fc1 = Exec::G(v2, h, 0, win, h, 0, e.sl, e.f1wf, h, sv->at("h"), e.f1wf, e.fc1_epi());
   fc1.aux_out = f0; fc1.ld_aux = e.F;
   PDS_TRY(e.gemm(fc1));
   PDS_TRY(tn.xw(f0, e.F, wout, h, e.sl, h, e.F, u1, h));                                // Z
@@ -1142,6 +1160,7 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
   const BufPlan& bp = sv->plan;
   const cudaStream_t cs = e.side_stream();
   const int64_t n = e.m.n_heads, h = e.h, d = e.d, sp = e.sp, sq = e.sq, b = e.b;
+  const int64_t hk = e.nkl * d * e.P, qw = e.qwf, grp = n / (e.nkl * e.P);   // GQA widths
   char* wqkv = ws + bp.ws_off("wqkv");
   char* wproj = ws + bp.ws_off("wproj");
   char* win = ws + bp.ws_off("win");
@@ -1166,15 +1185,15 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
   TN tn{e, ws + bp.ws_off("ta"), ws + bp.ws_off("tb"), ws + bp.ws_off("wt")};
   PDS_TRY(e.link(e.st, cs));
   PDS_TRY(e.ag(w->w_out, wout, e.Fl * h));
-  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.Fl * h));
+  PDS_TRY(e.ag_on(cs, w->w_in_t, win, e.f1w * h));
   cudaEvent_t ev_in = e.mark(cs);
   PDS_TRY(e.ag_on(cs, w->w_proj, wproj, e.hl * h));
   cudaEvent_t ev_proj = e.mark(cs);
   PDS_TRY(cz_wqkv(e, w, wqkv, cs));
   cudaEvent_t ev_qkv = e.mark(cs);
   PDS_CUDA(cudaMemsetAsync(dgl, 0, 2 * h * 4, e.st));
-  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.F, EPI_DGELU);
-  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F;
+  GemmArgs dgel = Exec::G(dy, h, 0, wout, h, 0, e.sl, e.F, h, f1, e.f1wf, e.dfc1_epi());
+  dgel.aux_in = sv->at("h"); dgel.ld_aux = e.F; dgel.ld_aux_in = e.f1wf;
   dgel.aux_t = tn.ta; dgel.c_t = f0; dgel.ld_t = e.sl;
   PDS_TRY(e.gemm(dgel));
   PDS_TRY(tn.tr(dy, h, e.sl, h, tn.tb));
@@ -1182,10 +1201,10 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
   PDS_TRY(uz_dw(e, dw, e.F, g->dw_out));
   PDS_TRY(e.apply(sv->at("x1"), sv->at("rstd2"), w->g2, e.sl, u1));
   PDS_TRY(tn.tr(u1, h, e.sl, h, tn.tb));
-  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.F, h, e.sl, dw, h, EPI_F32));                  // dW_in^T (full, local)
-  PDS_TRY(uz_dw(e, dw, e.F, g->dw_in_t));
+  PDS_TRY(tn.mm(f0, e.sl, tn.tb, e.sl, e.f1wf, h, e.sl, dw, h, EPI_F32));               // dW_in^T (full, local)
+  PDS_TRY(uz_dw(e, dw, e.f1wf, g->dw_in_t));
   PDS_TRY(e.wait(e.st, ev_in));
-  PDS_TRY(tn.xw(f1, e.F, win, h, e.sl, h, e.F, v2, h));
+  PDS_TRY(tn.xw(f1, e.f1wf, win, h, e.sl, h, e.f1wf, v2, h));
   PDS_TRY(e.norm_bwd(v2, sv->at("x1"), sv->at("rstd2"), w->g2, dy, e.sl, dx, dgp, dgl + h));
   PDS_TRY(e.wait(e.st, ev_proj));
   PDS_TRY(e.gemm(Exec::G(dx, h, 0, wproj, h, 0, e.sl, h, h, da, h)));                  // dA = dO of attention
@@ -1198,19 +1217,19 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
                             e.st), "attn_dot"));
   }
   // ring of V: dP_j = dO V_j^T, dV_j += P_j^T dO (the accumulator travels with V_j)
-  PDS_CUDA(cudaMemsetAsync(dacc[0], 0, e.sl * h * 4, e.st));
+  PDS_CUDA(cudaMemsetAsync(dacc[0], 0, e.sl * hk * 4, e.st));
   int cur = 0;
-  PDS_TRY(col_ring(e, qkv, 2 * h, kr, [&](int, int j, const char* vb) -> pds_status {
+  PDS_TRY(col_ring(e, qkv, h + hk, kr, [&](int, int j, const char* vb) -> pds_status {
     for (int64_t q = 0; q < b; ++q)
-      for (int64_t hd = 0; hd < n; ++hd) {
-        PDS_TRY(e.gemm(Exec::G(da + (q * h + hd * d) * 2, b * h, 0, vb + (q * h + hd * d) * 2, b * h, 0, sp, sp, d,
-                               dp + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
+      for (int64_t hd = 0; hd < n; ++hd) {         // a value head's dV sums its query group (GQA)
+        PDS_TRY(e.gemm(Exec::G(da + (q * h + hd * d) * 2, b * h, 0, vb + (q * hk + hd / grp * d) * 2, b * hk, 0, sp,
+                               sp, d, dp + ((q * n + hd) * sp * sq + j * sp), sq, EPI_F32)));
         PDS_TRY(e.gemm(Exec::G(probs + ((q * n + hd) * sp * sq + j * sp) * 2, sq, 1, da + (q * h + hd * d) * 2,
-                               b * h, 1, sp, d, sp, dacc[cur] + q * h + hd * d, b * h, EPI_F32_ACC)));
+                               b * h, 1, sp, d, sp, dacc[cur] + q * hk + hd / grp * d, b * hk, EPI_F32_ACC)));
       }
     if (e.P > 1) {
       PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dacc[cur]), reinterpret_cast<char*>(dacc[cur ^ 1]),
-                        e.sl * h * 4, e.st));
+                        e.sl * hk * 4, e.st));
       cur ^= 1;
     }
     return PDS_OK;
@@ -1218,8 +1237,8 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
   // dV (home after P passes) -> the V columns of dQKV
   {
     Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * h * 6);
-    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], h, (int)e.sl, (int)h, (int)d, nullptr, 0, 0, (int)e.sl, (int)b,
-                                 dqkv + 2 * h * 2, 3 * h, e.st), "dv convert"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], hk, (int)e.sl, (int)hk, (int)d, nullptr, 0, 0, (int)e.sl, (int)b,
+                                 dqkv + (h + hk) * 2, qw, e.st), "dv convert"));
   }
   {
     Prof p(e.c, e.st, K_NORM, 0, (double)b * n * sp * sq * 8);
@@ -1230,19 +1249,19 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
   }
   // ring of K: dQ += dS_j K_j, dK_j += dS_j^T Q (the accumulator travels with K_j)
   PDS_CUDA(cudaMemsetAsync(dqacc, 0, e.sl * h * 4, e.st));
-  PDS_CUDA(cudaMemsetAsync(dacc[cur], 0, e.sl * h * 4, e.st));
+  PDS_CUDA(cudaMemsetAsync(dacc[cur], 0, e.sl * hk * 4, e.st));
   PDS_TRY(col_ring(e, qkv, h, kr, [&](int, int j, const char* kb) -> pds_status {
     for (int64_t q = 0; q < b; ++q)
       for (int64_t hd = 0; hd < n; ++hd) {
         const char* dsb = ds + ((q * n + hd) * sp * sq + j * sp) * 2;
-        PDS_TRY(e.gemm(Exec::G(dsb, sq, 0, kb + (q * h + hd * d) * 2, b * h, 1, sp, d, sp, dqacc + q * h + hd * d,
-                               b * h, EPI_F32_ACC)));
-        PDS_TRY(e.gemm(Exec::G(dsb, sq, 1, qkv + (q * 3 * h + hd * d) * 2, b * 3 * h, 1, sp, d, sp,
-                               dacc[cur] + q * h + hd * d, b * h, EPI_F32_ACC)));
+        PDS_TRY(e.gemm(Exec::G(dsb, sq, 0, kb + (q * hk + hd / grp * d) * 2, b * hk, 1, sp, d, sp,
+                               dqacc + q * h + hd * d, b * h, EPI_F32_ACC)));
+        PDS_TRY(e.gemm(Exec::G(dsb, sq, 1, qkv + (q * qw + hd * d) * 2, b * qw, 1, sp, d, sp,
+                               dacc[cur] + q * hk + hd / grp * d, b * hk, EPI_F32_ACC)));
       }
     if (e.P > 1) {
       PDS_TRY(ring_pass(e, reinterpret_cast<char*>(dacc[cur]), reinterpret_cast<char*>(dacc[cur ^ 1]),
-                        e.sl * h * 4, e.st));
+                        e.sl * hk * 4, e.st));
       cur ^= 1;
     }
     return PDS_OK;
@@ -1251,21 +1270,24 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
     Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 2 * h * 6);
     const int64_t b0 = e.r * sp;
     PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b, dqkv,
-                                 3 * h, e.st), "dq rope_t"));
-    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], h, (int)e.sl, (int)h, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b,
-                                 dqkv + h * 2, 3 * h, e.st), "dk rope_t"));
+                                 qw, e.st), "dq rope_t"));
+    PDS_TRY(kerr(rope_t_f32_bf16(dacc[cur], hk, (int)e.sl, (int)hk, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b,
+                                 dqkv + h * 2, qw, e.st), "dk rope_t"));
   }
   PDS_TRY(e.apply(sv->x, sv->at("rstd1"), w->g1, e.sl, u1));
-  PDS_TRY(tn.dw(dqkv, 3 * h, u1, h, e.sl, 3 * h, h, dw, EPI_F32));
+  PDS_TRY(tn.dw(dqkv, qw, u1, h, e.sl, qw, h, dw, EPI_F32));
+  const int64_t hkl = e.nkl * d;
+  const int64_t part_off[3] = {0, h * h, (h + hk) * h};            // rows of [Q all; K all; V all]
+  const int64_t shard_off[3] = {0, e.hl * h, (e.hl + hkl) * h};    // rows of the spec shard
+  const int64_t cnts[3] = {e.hl * h, hkl * h, hkl * h};
   for (int i = 0; i < 3; ++i) {
-    char* part = dw + i * h * h * 4;
-    const int64_t cnt = e.hl * h;
-    char* mine = part + e.r * cnt * 4;
-    PDS_TRY(e.rs(part, mine, cnt, DT_F32));
-    PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + i * cnt * 4, cnt, e.st), "add_f32"));
+    char* part = dw + part_off[i] * 4;
+    char* mine = part + e.r * cnts[i] * 4;
+    PDS_TRY(e.rs(part, mine, cnts[i], DT_F32));
+    PDS_TRY(kerr(add_f32(mine, static_cast<char*>(g->dw_qkv_t) + shard_off[i] * 4, cnts[i], e.st), "add_f32"));
   }
   PDS_TRY(e.wait(e.st, ev_qkv));
-  PDS_TRY(tn.xw(dqkv, 3 * h, wqkv, h, e.sl, h, 3 * h, v2, h));                          // dU
+  PDS_TRY(tn.xw(dqkv, qw, wqkv, h, e.sl, h, qw, v2, h));                                // dU
   PDS_TRY(e.norm_bwd(v2, sv->x, sv->at("rstd1"), w->g1, dx, e.sl, dx, dgp, dgl));
   return e.dgamma(dgl, g);
 }
@@ -1308,7 +1330,7 @@ pds_status metp_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_s
   PDS_TRY(e.norm_fwd(x, nullptr, w->g1, e.sl, nullptr, ul, sv->at("rstd1")));
   PDS_TRY(waves(ul, [&](int64_t k, char* buf) -> pds_status {   // QKV waves: rows land at global positions
     GemmArgs q = e.rope(Exec::G(buf, e.h, 0, w->w_qkv_t, e.h, 0, W, e.qw, e.h, qkv, e.qw),
-                        e.hl, wr, e.sl, k * wr);
+                        e.hl, e.nkl * e.d, wr, e.sl, k * wr);
     q.c_seg = wr; q.c_stride = e.sl; q.c_base = k * wr;
     return e.gemm(q);
   }));
@@ -1415,7 +1437,7 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
       PDS_TRY(e.apply(xb + o * row, sv->at("rstd1") + o * 4, w->g1, wr, ul));
       PDS_TRY(e.ag(ul, wg, wr * e.h));                                                   // AG(u) recompute
       GemmArgs q = e.rope(Exec::G(wg, e.h, 0, w->w_qkv_t, e.h, 0, W, e.qw, e.h, qkv, e.qw),
-                          e.hl, wr, e.sl, o);
+                          e.hl, e.nkl * e.d, wr, e.sl, o);
       q.c_seg = wr; q.c_stride = e.sl; q.c_base = o;
       PDS_TRY(e.gemm(q));
     }

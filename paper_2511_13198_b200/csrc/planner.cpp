@@ -234,9 +234,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   if (m.n_kv_heads < 0 || m.n_heads % nk) PDS_FAIL(PDS_EINVAL, "n_kv_heads must divide n_heads");
   if (nk % P) PDS_FAIL(PDS_EDIVISIBILITY, "n_kv_heads=" + std::to_string(nk) + " not divisible by P=" + std::to_string(P));
   if (m.ffn_act != 0 && m.ffn_act != 1) PDS_FAIL(PDS_EINVAL, "ffn_act must be 0 (GELU) or 1 (SwiGLU)");
-  const bool variant = nk != m.n_heads || m.ffn_act == 1;
-  if (variant && (strategy == PDS_MEGATRON_CZ || strategy == PDS_COLOSSAL_Z))
-    PDS_FAIL(PDS_ENOTIMPL, "GQA / SwiGLU run on MegatronTS, UlyssesZ, METP and METP-full only");
+
   const int64_t sl = s / P;
   if (sl % 128) PDS_FAIL(PDS_EDIVISIBILITY, "s/P=" + std::to_string(sl) + " must be a multiple of 128 (caller pads, R-15)");
   const int64_t h = m.h, F = m.ffn, nl = m.n_heads / P, hl = h / P, Fl = F / P;
@@ -244,6 +242,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   // Fl / F, doubled by SwiGLU's [gate | up])
   const int64_t qw = (nl + 2 * (nk / P)) * (h / m.n_heads), qwf = qw * P;
   const int64_t f1w = (m.ffn_act == 1 ? 2 : 1) * Fl, f1wf = f1w * P;
+  const int64_t hkf = nk * (h / m.n_heads);          // all K (V) heads' width (MegatronCZ / ColossalZ)
   // token buffers hold rows = positions x b (layout [s, b, h], reading Q-35); the
   // divisibility checks above are on positions
   const int64_t S = s * m.batch, SL = sl * m.batch;
@@ -354,39 +353,39 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       // saved: the local rows of TS's tensors (Q/K/V of all heads, A, LSE, H); Q/K/V and
       // LSE on the zigzag rows
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", SL * 3 * h * 2);
+      push(p.saved, ts, "qkv", SL * qwf * 2);
       push(p.saved, ts, "a", u);
       push(p.saved, ts, "lse", lam);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", SL * F * 2);
-      push(p.ws, tw, "wqkv", 3 * h * h * 2);      // [Q all; K all; V all] rows
+      push(p.saved, ts, "h", SL * f1wf * 2);
+      push(p.ws, tw, "wqkv", qwf * h * 2);      // [Q all; K all; V all] rows
       push(p.ws, tw, "wproj", h * h * 2);
-      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "win", f1wf * h * 2);
       push(p.ws, tw, "wout", F * h * 2);
-      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "dw", std::max(qwf, f1wf) * h * 4);
       push(p.ws, tw, "u1", u);
       // ring attention on the zigzag rows (R-CZ): O(u) per rank whatever P
-      push(p.ws, tw, "qkvb", 3 * u);              // QKV of the boundary rows (bwd: dQKV)
-      push(p.ws, tw, "kv0", 2 * u);               // the K/V block in hand / the next one
-      push(p.ws, tw, "kv1", 2 * u);
+      push(p.ws, tw, "qkvb", SL * qwf * 2);       // QKV of the boundary rows (bwd: dQKV)
+      push(p.ws, tw, "kv0", SL * 2 * hkf * 2);    // the K/V block in hand / the next one
+      push(p.ws, tw, "kv1", SL * 2 * hkf * 2);
       push(p.ws, tw, "acc", 2 * u);               // fp32 O accumulator (bwd: dQ)
-      push(p.ws, tw, "dkv0", 4 * u);              // fp32 dK/dV travelling with their block
-      push(p.ws, tw, "dkv1", 4 * u);
+      push(p.ws, tw, "dkv0", SL * 2 * hkf * 4);   // fp32 dK/dV travelling with their block
+      push(p.ws, tw, "dkv1", SL * 2 * hkf * 4);
       push(p.ws, tw, "op", u);                    // a pair's partial O (bwd: zigzag dO)
       push(p.ws, tw, "oz", u);                    // zigzag O
       push(p.ws, tw, "lp", lam);                  // a pair's partial LSE
-      push(p.ws, tw, "dqkvz", 3 * u);             // zigzag dQKV
-      push(p.ws, tw, "f0", SL * F * 2);
-      push(p.ws, tw, "f1", SL * F * 2);
+      push(p.ws, tw, "dqkvz", SL * qwf * 2);      // zigzag dQKV
+      push(p.ws, tw, "f0", SL * f1wf * 2);
+      push(p.ws, tw, "f1", SL * f1wf * 2);
       push(p.ws, tw, "v2", u);
       push(p.ws, tw, "da", u);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(3 * h, F) * SL * 2);
+      push(p.ws, tw, "ta", std::max(qwf, F) * SL * 2);
       push(p.ws, tw, "tb", h * SL * 2);
-      push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
+      push(p.ws, tw, "wt", h * std::max(qwf, f1wf) * 2);
       break;
     }
     case PDS_COLOSSAL_Z: {
@@ -395,36 +394,36 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       const int64_t n = m.n_heads;
       const int64_t quad = n * sl * s * m.batch;       // elements of [b][n][s/P][s]
       push(p.saved, ts, "rstd1", ell);
-      push(p.saved, ts, "qkv", SL * 3 * h * 2);
+      push(p.saved, ts, "qkv", SL * qwf * 2);
       push(p.saved, ts, "a", u);
       push(p.saved, ts, "probs", quad * 2);
       push(p.saved, ts, "x1", u);
       push(p.saved, ts, "rstd2", ell);
-      push(p.saved, ts, "h", SL * F * 2);
-      push(p.ws, tw, "wqkv", 3 * h * h * 2);
+      push(p.saved, ts, "h", SL * f1wf * 2);
+      push(p.ws, tw, "wqkv", qwf * h * 2);
       push(p.ws, tw, "wproj", h * h * 2);
-      push(p.ws, tw, "win", F * h * 2);
+      push(p.ws, tw, "win", f1wf * h * 2);
       push(p.ws, tw, "wout", F * h * 2);
-      push(p.ws, tw, "dw", std::max(3 * h, F) * h * 4);
+      push(p.ws, tw, "dw", std::max(qwf, f1wf) * h * 4);
       push(p.ws, tw, "u1", u);
       push(p.ws, tw, "scores", quad * 4);          // fp32 scores (bwd: dP)
       push(p.ws, tw, "ds", quad * 2);              // bf16 dS (bwd)
-      push(p.ws, tw, "kr0", u);                    // the K (or V) block in hand / the next one
-      push(p.ws, tw, "kr1", u);
+      push(p.ws, tw, "kr0", SL * hkf * 2);         // the K (or V) block in hand / the next one
+      push(p.ws, tw, "kr1", SL * hkf * 2);
       push(p.ws, tw, "acc", 2 * u);                // fp32 O (bwd: dQ)
-      push(p.ws, tw, "dacc0", 2 * u);              // fp32 dV / dK travelling with their block
-      push(p.ws, tw, "dacc1", 2 * u);
-      push(p.ws, tw, "dqkv", 3 * u);
-      push(p.ws, tw, "f0", SL * F * 2);
-      push(p.ws, tw, "f1", SL * F * 2);
+      push(p.ws, tw, "dacc0", SL * hkf * 4);       // fp32 dV / dK travelling with their block
+      push(p.ws, tw, "dacc1", SL * hkf * 4);
+      push(p.ws, tw, "dqkv", SL * qwf * 2);
+      push(p.ws, tw, "f0", SL * f1wf * 2);
+      push(p.ws, tw, "f1", SL * f1wf * 2);
       push(p.ws, tw, "v2", u);
       push(p.ws, tw, "da", u);
       push(p.ws, tw, "dd", lam);
       push(p.ws, tw, "dgp", dgp);
       push(p.ws, tw, "dgl", 2 * h * 4);
-      push(p.ws, tw, "ta", std::max(3 * h, F) * SL * 2);
+      push(p.ws, tw, "ta", std::max(qwf, F) * SL * 2);
       push(p.ws, tw, "tb", h * SL * 2);
-      push(p.ws, tw, "wt", h * std::max(3 * h, F) * 2);
+      push(p.ws, tw, "wt", h * std::max(qwf, f1wf) * 2);
       break;
     }
     default:

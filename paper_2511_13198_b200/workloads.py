@@ -5,6 +5,11 @@
   GPT    h = 12288, n = 96 (d = 128), L/node = 8
   FFN 4h GELU for all (reading R-5), bf16, b = 1.
 
+The Llama variant (NEXT-3, readings R-GQA / R-SWIGLU) at the paper's LLaMA width:
+  LLaMA-GQA  h = 8192, n = 64, n_kv = 8, SwiGLU F = 28672 (the Llama-2-70B block), L/node = 8
+  Llama3-8B  h = 4096, n = 32, n_kv = 8, SwiGLU F = 14336, L/node = 32
+(model FLOPs per token: 3 [2 (h (n + 2 n_kv) d + h^2 + 3 h F) + 2 s h] causal.)
+
 Per model: (1) device-timed tokens/s of one layer fwd + bwd per strategy at a few
 sequence lengths (the same kernels and C ABI as the 7B bench; CUDA events, L2 flushed);
 (2) the OOM frontier of the L/node stack per uniform strategy, from the exact memory
@@ -24,7 +29,19 @@ MODELS = {
     "BERT": dict(h=1024, n=16, L=24, causal=0),
     "LLaMA": dict(h=8192, n=64, L=8, causal=1),
     "GPT": dict(h=12288, n=96, L=8, causal=1),
+    "LLaMA-GQA": dict(h=8192, n=64, L=8, causal=1, n_kv=8, ffn=28672, act=1),
+    "Llama3-8B": dict(h=4096, n=32, L=32, causal=1, n_kv=8, ffn=14336, act=1),
 }
+
+
+def layer_flops(cfg, s):
+    """Model FLOPs of one layer fwd + bwd at length s (3 x forward; attention causal
+    counts the lower triangle)."""
+    h, n = cfg["h"], cfg["n"]
+    nk, F = cfg.get("n_kv", n), cfg.get("ffn", 4 * h)
+    lin = 2 * (h * (n + 2 * nk) * (h // n) + h * h + (3 if cfg.get("act") else 2) * h * F)
+    att = (2 if cfg["causal"] else 4) * s * h
+    return 3 * (lin + att) * s
 
 
 def main():
@@ -47,8 +64,11 @@ def main():
     for name in a.models:
         cfg = MODELS[name]
         h, n, L = cfg["h"], cfg["n"], cfg["L"]
-        model = B.Model(h=h, n_heads=n, ffn=4 * h, n_layers=L, causal=cfg["causal"])
-        out = {"h": h, "n": n, "ffn": 4 * h, "L_per_node": L, "causal": cfg["causal"], "layer": [], "frontier": {}}
+        F = cfg.get("ffn", 4 * h)
+        model = B.Model(h=h, n_heads=n, ffn=F, n_layers=L, causal=cfg["causal"], n_kv_heads=cfg.get("n_kv", 0),
+                        ffn_act=cfg.get("act", 0))
+        out = {"h": h, "n": n, "n_kv": cfg.get("n_kv", n), "ffn": F, "act": "swiglu" if cfg.get("act") else "gelu",
+               "L_per_node": L, "causal": cfg["causal"], "layer": [], "frontier": {}}
         # (1) one layer fwd + bwd per strategy
         for s in a.seqs:
             w, gr, x, dy = make_layer_buffers(torch, model, 1, s, seed=3)
@@ -69,7 +89,7 @@ def main():
                     if r:
                         times.append(e0.elapsed_time(e1) / 1e3)
                 t = min(times)
-                flops = (72 * h * h + 6 * s * h * (1 if cfg["causal"] else 2)) * s
+                flops = layer_flops(cfg, s)
                 rec = {"s": s, "strategy": pname, "seconds": t, "tokens_per_s": s / t,
                        "model_tflops": flops / t / 1e12}
                 out["layer"].append(rec)

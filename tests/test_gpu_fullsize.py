@@ -29,13 +29,13 @@ if torch.cuda.is_available():
     from tests.gpu_util import host, rel
 
 
-def _inputs(h, F, s, seed):
+def _inputs(h, F, s, seed, qkv_rows=None, fc1_rows=None):
     g = torch.Generator(device="cuda").manual_seed(seed)
 
     def r(*sh, std=1.0, mean=0.0):
         return (torch.randn(*sh, generator=g, device="cuda") * std + mean).to(torch.bfloat16)
-    return dict(x=r(s, h), w_qkv_t=r(3 * h, h, std=h ** -0.5), w_proj=r(h, h, std=h ** -0.5),
-                w_in_t=r(F, h, std=h ** -0.5), w_out=r(F, h, std=F ** -0.5),
+    return dict(x=r(s, h), w_qkv_t=r(qkv_rows or 3 * h, h, std=h ** -0.5), w_proj=r(h, h, std=h ** -0.5),
+                w_in_t=r(fc1_rows or F, h, std=h ** -0.5), w_out=r(F, h, std=F ** -0.5),
                 g1=r(h, std=0.1, mean=1.0), g2=r(h, std=0.1, mean=1.0))
 
 
@@ -61,8 +61,9 @@ CASES = [  # h, n, F, s, strategy, metp_chunks, metp_recompute, last sampled row
 
 @pytest.mark.parametrize("h,n,F,s,pi,chunks,recompute,last", CASES,
                          ids=[f"h{c[0]}-s{c[3]}-pi{c[4]}-c{c[5]}{'-knob' if c[6] else ''}" for c in CASES])
-def test_fullsize_sampled(h, n, F, s, pi, chunks, recompute, last):
-    w = _inputs(h, F, s, seed=11 + pi + h // 4096)
+def test_fullsize_sampled(h, n, F, s, pi, chunks, recompute, last, n_kv=0, act=0):
+    nk = n_kv or n
+    w = _inputs(h, F, s, seed=11 + pi + h // 4096, qkv_rows=(n + 2 * nk) * (h // n), fc1_rows=(2 if act else 1) * F)
     R = np.unique(np.array([5, 700, s // 3 + 1, s // 2 + 3, last - 513, last - 1, last]))
     rng = np.random.default_rng(99)
     dy_r = rng.standard_normal((len(R), h)).astype(np.float32)
@@ -70,7 +71,8 @@ def test_fullsize_sampled(h, n, F, s, pi, chunks, recompute, last):
     dy = torch.zeros(s, h, dtype=torch.bfloat16, device="cuda")
     dy[torch.from_numpy(R).cuda()] = dy_r.cuda()
     # ---------------- GPU (bench configuration: P = 1 context)
-    ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, metp_recompute=recompute))
+    ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, metp_recompute=recompute, n_kv_heads=n_kv,
+                            ffn_act=act))
     keys = ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")
     gr = {k: torch.zeros(w[k].shape, dtype=torch.float32, device="cuda") for k in keys}
     W = B.Weights(*(w[k].data_ptr() for k in keys))
@@ -90,7 +92,8 @@ def test_fullsize_sampled(h, n, F, s, pi, chunks, recompute, last):
     wq = _f32(w["w_qkv_t"]).T
     ref = OS.sampled_layer(_f32(x), wq, _f32(w["w_proj"]), _f32(w["w_in_t"]).T, _f32(w["w_out"]),
                            _f32(w["g1"]).astype(np.float64), _f32(w["g2"]).astype(np.float64), n, R,
-                           dy_r.float().numpy().astype(np.float64))
+                           dy_r.float().numpy().astype(np.float64), n_kv=nk, act="swiglu" if act else "gelu",
+                           il=bool(act))
     del w
     assert rel(oR, ref["o"]) < 1e-2
     assert rel(zR, ref["z"]) < 1e-2
@@ -104,3 +107,17 @@ def test_fullsize_sampled(h, n, F, s, pi, chunks, recompute, last):
     sample = np.unique(np.concatenate([R, np.arange(0, s, 97)]))
     assert rel(gx[sample], ref["dx"][sample]) < 1e-2
     assert np.all(gx[R.max() + 1:] == 0.0)            # no gradient beyond the last cotangent row
+
+
+LLAMA_CASES = [  # h, n, n_kv, F, s, strategy, metp_chunks, last sampled row
+    (8192, 64, 8, 28672, 4096, 0, 0, 4095),     # the paper's LLaMA (h 8192 / n 64, Table 4) as Llama-2-70B: GQA 8, SwiGLU
+    (8192, 64, 8, 28672, 4096, 4, 2, 3001),     # METP-full, 2 waves
+    (4096, 32, 8, 14336, 8192, 1, 0, 8191),     # Llama-3-8B-shaped layer through UlyssesZ
+]
+
+
+@pytest.mark.parametrize("h,n,n_kv,F,s,pi,chunks,last", LLAMA_CASES,
+                         ids=[f"llama-h{c[0]}-kv{c[2]}-s{c[4]}-pi{c[5]}" for c in LLAMA_CASES])
+def test_fullsize_sampled_llama_variant(h, n, n_kv, F, s, pi, chunks, last):
+    """GQA + SwiGLU (R-GQA / R-SWIGLU) at full size, sampled rows (O-9)."""
+    test_fullsize_sampled(h, n, F, s, pi, chunks, 0, last, n_kv=n_kv, act=1)

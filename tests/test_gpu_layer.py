@@ -392,16 +392,16 @@ def test_nccl_one_rank_equals_self(pi):
 
 
 # ---------------------------------------------------------------- Llama variant (NEXT-3)
-@pytest.mark.parametrize("pi", [0, 1, 2, 4])
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("P,h,n,n_kv,F,s", [
-    (1, 512, 8, 2, 768, 640),        # d = 64, grp 4, ragged query blocks
+    (1, 512, 8, 2, 768, 768),        # d = 64, grp 4, an odd count of 256-query CTAs
     (2, 1024, 8, 2, 1536, 1024),     # d = 128, grp 4, one KV head per rank
     (4, 1024, 8, 4, 1024, 2048),     # d = 128, grp 2
 ])
 def test_llama_variant_layer(pi, P, h, n, n_kv, F, s):
     """GQA + SwiGLU layer (R-GQA / R-SWIGLU) on every strategy that runs it, per-rank
     shards included, against the fp64 oracle's Llama layer."""
-    chunks = 2 if pi in (2, 4) else 0
+    chunks = 2 if pi in (2, 4) and P > 1 else 0
     _check_layer(pi, P, h, n, F, s, seed=17, chunks=chunks, n_kv=n_kv, act="swiglu", b=2 if P == 2 else 1)
 
 

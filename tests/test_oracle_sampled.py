@@ -48,3 +48,29 @@ def test_sampled_rejects_unsorted_rows():
     with pytest.raises(AssertionError):
         OS.sampled_layer(d["x"][:, 0], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], 2,
                          [5, 3], np.zeros((2, 64)))
+
+
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("il", [False, True])
+def test_sampled_llama_variant_equals_full_oracle(causal, il):
+    """GQA + SwiGLU (R-GQA / R-SWIGLU) in the row-sampled oracle, plain and interleaved
+    (the device's spec layout) W_in, against oracle.layer's full Llama layer."""
+    from oracle.shard import il_perm
+    h, n, n_kv, F, s = 128, 4, 2, 256, 256
+    d = layer_inputs(h, n, F, s, 1, seed=8, n_kv=n_kv, act="swiglu")
+    R = np.array([2, 77, 130, 250])
+    dy = np.zeros((s, 1, h))
+    dy[R, 0] = d["dy"][R, 0]
+    kw = dict(n=n, causal=causal, n_kv=n_kv, act="swiglu")
+    y, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    g = OL.layer_bwd(dy, c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], **kw)
+    pm = il_perm(F)
+    w_in = d["w_in"][:, pm] if il else d["w_in"]
+    r = OS.sampled_layer(d["x"][:, 0], d["w_qkv"], d["w_proj"], w_in, d["w_out"], d["g1"], d["g2"], n,
+                         R, dy[R, 0], causal=causal, n_kv=n_kv, act="swiglu", il=il)
+    assert _rel(r["y"], y[R, 0]) < 1e-12
+    assert _rel(r["z"], c["z"][R, 0]) < 1e-12
+    assert _rel(r["dx"], g["dx"][:, 0]) < 1e-12
+    assert _rel(r["dw_in"], g["dw_in"][:, pm] if il else g["dw_in"]) < 1e-12
+    for k in ("dw_qkv", "dw_proj", "dw_out", "dg1", "dg2"):
+        assert _rel(r[k], g[k]) < 1e-12, k
