@@ -228,6 +228,16 @@ pds_status pds_layer_step_host(pds_ctx* ctx, uint8_t strategy, int64_t seq_len, 
 pds_status pds_host_drain(pds_ctx* ctx, void* stream);
 /* Release a saved set without running backward. */
 pds_status pds_saved_release(pds_ctx* ctx, pds_saved* saved);
+/* Comm log: on = 1 clears and starts recording every collective of this
+ * rank's layer calls as a JSON line {"primitive": "AllGather" | "ReduceScatter" |
+ * "AllToAll" | "AllReduce" | "SendRecv" | "RingPass", "bytes": B, "participants": P}
+ * with B the bytes this rank sends (the oracle grid's payload convention, SPEC.md:109;
+ * nothing at P = 1); on = 0 stops.  pds_comm_log_read copies the log (NUL-terminated,
+ * truncated to cap - 1 bytes; buf may be NULL) and returns its full length in *len_out.
+ * Host-side bookkeeping only; every layer call also opens NVTX ranges
+ * ("pds_layer_fwd <strategy>", and "pds:gemm" / "pds:attn_fwd" / ... per launch). */
+pds_status pds_comm_log(pds_ctx* ctx, int32_t on);
+pds_status pds_comm_log_read(pds_ctx* ctx, char* buf, int64_t cap, int64_t* len_out);
 /* Varlen packing (reading R-VARLEN): the following layer calls of
  * this context treat their seq_len tokens as n_seqs independent sequences packed back to
  * back in the boundary layout (rank r holds tokens [r T/P, (r+1) T/P) of the packed

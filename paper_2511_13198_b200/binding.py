@@ -129,6 +129,8 @@ _SIGS = {
     "pds_k_stream_wait32": [C.c_void_p, C.c_void_p, C.c_uint32],
     "pds_set_overlap": [C.c_void_p, C.c_int32],
     "pds_set_varlen": [C.c_void_p, C.c_int32, C.POINTER(C.c_int64)],
+    "pds_comm_log": [C.c_void_p, C.c_int32],
+    "pds_comm_log_read": [C.c_void_p, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)],
     "pds_profile_enable": [C.c_void_p, C.c_int32],
     "pds_profile_read": [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                          C.POINTER(C.c_double), C.POINTER(C.c_double)],
@@ -314,6 +316,18 @@ class Context:
 
     def set_overlap(self, on):
         call("pds_set_overlap", self.h, 1 if on else 0)
+
+    def comm_log(self, on=True):
+        """Start (clearing) or stop the JSON-lines comm log of this rank."""
+        call("pds_comm_log", self.h, 1 if on else 0)
+
+    def read_comm_log(self):
+        import json
+        n = C.c_int64(0)
+        call("pds_comm_log_read", self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        call("pds_comm_log_read", self.h, buf, n.value + 1, C.byref(n))
+        return [json.loads(line) for line in buf.value.decode().splitlines() if line]
 
     def set_varlen(self, lens):
         """Pack len(lens) sequences into the following layer calls (R-VARLEN); [] = one."""

@@ -27,6 +27,9 @@
 #include <utility>
 #include <vector>
 
+#include <cstdio>
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.hpp"
 #include "internal.hpp"
 #include "kernels/gemm.cuh"
@@ -101,6 +104,10 @@ struct pds_ctx {
   uint32_t ag_epoch = 0, rs_count = 0, a2a_count = 0;
   int overlap = 1;
   std::vector<cudaEvent_t> sync_pool;
+  // comm log (JSON lines {"primitive", "bytes", "participants"}, the oracle
+  // grid's convention: bytes this rank sends), pds_comm_log / pds_comm_log_read
+  bool comm_log_on = false;
+  std::string comm_log;
   // profiling
   bool prof = false;
   std::vector<ProfRec> pending;
@@ -141,6 +148,14 @@ namespace {
 
 enum { K_GEMM = 0, K_ATTN_F = 1, K_ATTN_B = 2, K_NORM = 3, K_COMM = 4 };
 
+// NVTX range per launch class (SURVEY §5 tracing): visible in nsys / ncu --nvtx; a
+// no-op without an attached tool
+const char* const kProfName[5] = {"pds:gemm", "pds:attn_fwd", "pds:attn_bwd", "pds:elementwise", "pds:comm"};
+const char* const kLayerName[PDS_N_STRATEGIES][2] = {
+    {"pds_layer_fwd MegatronTS", "pds_layer_bwd MegatronTS"}, {"pds_layer_fwd UlyssesZ", "pds_layer_bwd UlyssesZ"},
+    {"pds_layer_fwd METP", "pds_layer_bwd METP"}, {"pds_layer_fwd MegatronCZ", "pds_layer_bwd MegatronCZ"},
+    {"pds_layer_fwd METP-full", "pds_layer_bwd METP-full"}, {"pds_layer_fwd ColossalZ", "pds_layer_bwd ColossalZ"}};
+
 struct Prof {
   pds_ctx* c;
   cudaStream_t st;
@@ -148,12 +163,14 @@ struct Prof {
   double fl, by;
   cudaEvent_t a = nullptr;
   Prof(pds_ctx* c_, cudaStream_t s_, int k_, double f_, double b_) : c(c_), st(s_), k(k_), fl(f_), by(b_) {
+    nvtxRangePushA(kProfName[k]);
     if (c->prof) {
       a = c->ev();
       cudaEventRecord(a, st);
     }
   }
   ~Prof() {
+    nvtxRangePop();
     if (a) {
       cudaEvent_t b = c->ev();
       cudaEventRecord(b, st);
@@ -254,6 +271,7 @@ struct Exec {
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
     const uint32_t epoch = ++c->ag_epoch;
+    log_comm("AllGather", (double)count * 2 * (P - 1));
     {
       Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
       PDS_TRY(cm->all_gather_flagged(buf, count, DT_BF16, st, cs, c->sync, epoch));
@@ -311,6 +329,7 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
+    log_comm("AllToAll", (double)count * 2 * (P - 1));
     {
       Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
       PDS_TRY(cm->all_to_all_gated(send, recv, count, DT_BF16, st, cs, c->sync + 16, a2a_target));
@@ -325,6 +344,7 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = c->comm->side(&rc);
     if (!cm) return rc;
+    log_comm("ReduceScatter", (double)count * 2 * (P - 1));
     {
       Prof p(c, cs, K_COMM, 0, (double)count * 2 * (P - 1));
       PDS_TRY(cm->reduce_scatter_gated(partial, recv, count, DT_BF16, st, cs, c->sync + 8, rs_target));
@@ -403,6 +423,7 @@ struct Exec {
   }
   // collectives
   pds_status ag(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
+    log_comm("AllGather", (double)count * dt_size(dt) * (P - 1));
     Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
     return c->comm->all_gather(send, recv, count, dt, st);
   }
@@ -411,6 +432,7 @@ struct Exec {
     pds_status rc = PDS_OK;
     Comm* cm = s2 == st ? c->comm : c->comm->side(&rc);
     if (!cm) return rc;
+    log_comm("AllGather", (double)count * 2 * (P - 1));
     Prof p(c, s2, K_COMM, 0, (double)count * 2 * (P - 1));
     return cm->all_gather(send, recv, count, DT_BF16, s2);
   }
@@ -452,24 +474,28 @@ struct Exec {
     return PDS_OK;
   }
   pds_status rs(const void* send, void* recv, int64_t count, DType dt = DT_BF16) {
+    log_comm("ReduceScatter", (double)count * dt_size(dt) * (P - 1));
     Prof p(c, st, K_COMM, 0, (double)count * dt_size(dt) * (P - 1));
     return c->comm->reduce_scatter(send, recv, count, dt, st);
   }
-  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t on) {
+  pds_status p2p(const P2P* sends, int ns, const P2P* recvs, int nr, cudaStream_t on, const char* prim = "SendRecv") {
     pds_status rc = PDS_OK;
     Comm* cm = on == st ? c->comm : c->comm->side(&rc);
     if (!cm) return rc;
     double bytes = 0;
     for (int i = 0; i < ns; ++i)
       if (sends[i].peer != r) bytes += (double)sends[i].bytes;
+    log_comm(prim, bytes);
     Prof p(c, on, K_COMM, 0, bytes);
     return cm->p2p(sends, ns, recvs, nr, on);
   }
   pds_status a2a(const void* send, void* recv, int64_t count) {
+    log_comm("AllToAll", (double)count * 2 * (P - 1));
     Prof p(c, st, K_COMM, 0, (double)count * 2 * (P - 1));
     return c->comm->all_to_all(send, recv, count, DT_BF16, st);
   }
   pds_status dgamma(float* dgl, const pds_grads* g) {
+    log_comm("AllReduce", 2.0 * (P - 1) / P * 2 * h * 4);       // ring all-reduce payload
     {
       Prof p(c, st, K_COMM, 0, 2.0 * h * 4 * 2 * (P - 1));
       PDS_TRY(c->comm->all_reduce(dgl, 2 * h, DT_F32, st));
@@ -481,6 +507,13 @@ struct Exec {
     if (!dst) return PDS_OK;
     PDS_CUDA(cudaMemcpyAsync(dst, src, n * 2, cudaMemcpyDeviceToDevice, st));
     return PDS_OK;
+  }
+  // one comm-log record: the bytes this rank sends (oracle/grid.py's payload convention)
+  void log_comm(const char* prim, double bytes) {
+    if (!c->comm_log_on || P == 1) return;
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "{\"primitive\": \"%s\", \"bytes\": %.0f, \"participants\": %d}\n", prim, bytes, P);
+    c->comm_log += buf;
   }
 };
 
@@ -829,7 +862,7 @@ pds_status zig_exchange(Exec& e, const Zig& z, char* X, char* Z, int64_t cols, b
 pds_status ring_pass(Exec& e, const char* cur, char* nxt, int64_t bytes, cudaStream_t on) {
   P2P snd{(e.r + 1) % e.P, 0, const_cast<char*>(cur), bytes};
   P2P rcv{(e.r - 1 + e.P) % e.P, 0, nxt, bytes};
-  return e.p2p(&snd, 1, &rcv, 1, on);
+  return e.p2p(&snd, 1, &rcv, 1, on, "RingPass");
 }
 
 pds_status cz_fwd(Exec& e, const void* x, const pds_weights* w, void* y, pds_saved* sv, char* ws) {
@@ -1650,6 +1683,24 @@ extern "C" pds_status pds_release_cache(pds_ctx* c) {
   return PDS_OK;
 }
 
+extern "C" pds_status pds_comm_log(pds_ctx* c, int32_t on) {
+  if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
+  c->comm_log_on = on != 0;
+  c->comm_log.clear();
+  return PDS_OK;
+}
+
+extern "C" pds_status pds_comm_log_read(pds_ctx* c, char* buf, int64_t cap, int64_t* len_out) {
+  if (!c || !len_out) PDS_FAIL(PDS_EINVAL, "NULL ctx / len_out");
+  *len_out = (int64_t)c->comm_log.size();
+  if (buf && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, (int64_t)c->comm_log.size());
+    std::memcpy(buf, c->comm_log.data(), (size_t)n);
+    buf[n] = 0;
+  }
+  return PDS_OK;
+}
+
 extern "C" pds_status pds_set_varlen(pds_ctx* c, int32_t n_seqs, const int64_t* lens) {
   if (!c) PDS_FAIL(PDS_EINVAL, "NULL ctx");
   if (n_seqs < 0 || (n_seqs > 0 && !lens)) PDS_FAIL(PDS_EINVAL, "pds_set_varlen: bad n_seqs / lens");
@@ -1725,6 +1776,7 @@ extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_le
   PDS_TRY(alloc_saved(c, bp.saved_bytes, &sv->mem));
   Exec e(c, st, seq_len, sv->segs);
   pds_status rc;
+  nvtxRangePushA(kLayerName[strategy][0]);
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_fwd(e, x, w, y, sv.get(), c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_fwd(e, x, w, y, sv.get(), c->ws); break;
@@ -1732,6 +1784,7 @@ extern "C" pds_status pds_layer_fwd(pds_ctx* c, uint8_t strategy, int64_t seq_le
     case PDS_COLOSSAL_Z: rc = col_fwd(e, x, w, y, sv.get(), c->ws); break;
     default: rc = metp_fwd(e, x, w, y, sv.get(), c->ws); break;
   }
+  nvtxRangePop();
   c->tap_o = c->tap_z = nullptr;
   if (rc != PDS_OK || !saved) {
     c->free_blocks.emplace(sv->bytes, sv->mem);
@@ -1756,6 +1809,7 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
   PDS_TRY(ensure_ws(c, saved->plan.ws_bytes, st));
   Exec e(c, st, saved->s, saved->segs);
   pds_status rc;
+  nvtxRangePushA(kLayerName[strategy][1]);
   switch (strategy) {
     case PDS_MEGATRON_TS: rc = ts_bwd(e, dy, saved, w, g, dx, c->ws); break;
     case PDS_ULYSSES_Z: rc = uz_bwd(e, dy, saved, w, g, dx, c->ws); break;
@@ -1763,6 +1817,7 @@ extern "C" pds_status pds_layer_bwd(pds_ctx* c, uint8_t strategy, const void* dy
     case PDS_COLOSSAL_Z: rc = col_bwd(e, dy, saved, w, g, dx, c->ws); break;
     default: rc = metp_bwd(e, dy, saved, w, g, dx, c->ws); break;
   }
+  nvtxRangePop();
   c->saved_live -= saved->bytes;
   c->free_blocks.emplace(saved->bytes, saved->mem);
   delete saved;

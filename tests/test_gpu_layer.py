@@ -47,7 +47,8 @@ class Rank:
         return B.Grads(*(self.g[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
 
 
-def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True, overlap=None, varlen=None):
+def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True, overlap=None, varlen=None,
+              logs=None):
     """Run an L-layer stack (plan pi_list) on P loopback ranks; returns per-rank outputs.
     overlap: None = library default, else pds_set_overlap(ctx, overlap)."""
     grp = B.Group(P)
@@ -64,6 +65,8 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
                     ctx.set_overlap(overlap)
                 if varlen:
                     ctx.set_varlen(varlen)
+                if logs is not None:
+                    ctx.comm_log(True)
                 xs = dev_bf16(x_shards[r].reshape(x_shards[r].shape[0], -1))
                 acts = [xs]
                 saves = []
@@ -85,6 +88,8 @@ def run_ranks(model, P, pi_list, ranks_per_layer, x_shards, dy_shards, taps=True
                     d = dx
                 st.synchronize()
                 outs[r] = (host(acts[-1]), host(d))
+                if logs is not None:
+                    logs[r] = ctx.read_comm_log()
                 ctx.close()
         except Exception as e:  # surfaced in the main thread
             errs.append(e)
@@ -456,3 +461,34 @@ def test_varlen_argument_errors():
     with pytest.raises(B.PdsError) as e:
         B.Context(B.Model(h=256, n_heads=4, ffn=1024, batch=2)).set_varlen([256])
     assert e.value.code == -1
+
+
+# ---------------------------------------------------------------- comm log
+@pytest.mark.parametrize("pi", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_comm_log_equals_oracle_dataflow(pi, overlap):
+    """The device path's collectives (pds_comm_log) at P = 2: the same primitive multiset
+    as the oracle simulation of that strategy, and the bytes every rank sends sum to the
+    oracle's formula (oracle/flops.comm_bytes, itself equal to the simulated comm log)."""
+    from collections import Counter
+    from oracle import flops as OF
+    from oracle import strategies as S
+    from oracle.grid import Grid
+    h, n, F, s, P = 256, 4, 1024, 1024, 2
+    d = layer_inputs(h, n, F, s, 1, seed=5)
+    W = OS.shard_weights(d, n, P)
+    xs, dys = OS.shard_act(d["x"], P), OS.shard_act(d["dy"], P)
+    ranks = [Rank(W, r, xs[r], dys[r]) for r in range(P)]
+    logs = [None] * P
+    run_ranks(B.Model(h=h, n_heads=n, ffn=F, metp_chunks=2), P, [pi], [ranks], xs, dys, taps=False,
+              overlap=overlap, logs=logs)
+    g = Grid(P)
+    cfg = S.Cfg(h, n, F, metp_chunks=2)
+    ys, saved, _ = S.layer_fwd(pi, g, xs, W, cfg)
+    S.layer_bwd(pi, g, dys, saved, W, cfg, S.new_grads(W))
+    for r in range(P):
+        assert Counter(e["primitive"] for e in logs[r]) == Counter(g.primitives()), (pi, r)
+        assert all(e["participants"] == P for e in logs[r])
+    total = sum(e["bytes"] for lg in logs for e in lg)
+    full = "full" if pi == 4 else "ffn"
+    assert total == P * OF.comm_bytes(pi, h, s, P, F, metp_recompute=full), (pi, total)
