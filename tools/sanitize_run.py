@@ -2,7 +2,9 @@
 shapes: every kernel family of libparadyse.so once — both tcgen05 GEMM kernels (CTA
 pair and 1-CTA) with every epilogue, the attention forward / backward (d = 64 and 128,
 causal and not, full and query-row-range), the norm / transpose / pack kernels — plus
-one whole layer fwd + bwd per strategy (P = 1 and a P = 2 loopback group).
+one whole layer fwd + bwd per strategy (P = 1 and a P = 2 loopback group); the Llama
+variant (GQA attention, SwiGLU epilogues, a GQA + SwiGLU layer per strategy) and varlen
+packing.
 
   compute-sanitizer --tool racecheck --print-limit 50 python tools/sanitize_run.py
 """
@@ -62,6 +64,31 @@ def kernels():
                           lse_r.data_ptr(), st)
         B.k_attn_bwd_rows(qkv.data_ptr(), 3 * heads * d, out_r.data_ptr(), heads * d, lse_r.data_ptr(),
                           dout[:qn].data_ptr(), s, heads, d, 1, 128, qn, dqkv.data_ptr(), st)
+    # GQA attention (4 query heads on 2 / 1 key-value heads) and the SwiGLU epilogues
+    for d, heads, kvh in ((128, 4, 2), (64, 4, 1)):
+        s = 384
+        W = (heads + 2 * kvh) * d
+        qkv = r(s, W, std=0.5)
+        out = torch.empty(s, heads * d, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(heads, s, device="cuda")
+        dout = r(s, heads * d)
+        dqkv = torch.zeros_like(qkv)
+        for causal in (1, 0):
+            B.k_attn_fwd_gqa(qkv.data_ptr(), W, s, heads, kvh, d, causal, out.data_ptr(), heads * d, lse.data_ptr(), st)
+            B.k_attn_bwd_gqa(qkv.data_ptr(), W, out.data_ptr(), heads * d, lse.data_ptr(), dout.data_ptr(), s, heads,
+                             kvh, d, causal, dqkv.data_ptr(), st)
+    M, F, K = 384, 256, 256
+    a, wt = r(M, K), r(2 * F, K)
+    hb = torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda")
+    g1 = torch.empty(M, F, dtype=torch.bfloat16, device="cuda")
+    B.k_gemm_swiglu(a.data_ptr(), K, wt.data_ptr(), K, M, 2 * F, K, 0, hb.data_ptr(), 2 * F, g_out=g1.data_ptr(),
+                    ld_g=F, stream=st)
+    wo = r(F, K)
+    dh, dht, gt = (torch.empty(M, 2 * F, dtype=torch.bfloat16, device="cuda"),
+                   torch.empty(2 * F, M, dtype=torch.bfloat16, device="cuda"),
+                   torch.empty(F, M, dtype=torch.bfloat16, device="cuda"))
+    B.k_gemm_swiglu(a.data_ptr(), K, wo.data_ptr(), K, M, F, K, 1, dh.data_ptr(), 2 * F, hb.data_ptr(), 2 * F,
+                    g1.data_ptr(), F, dht.data_ptr(), gt.data_ptr(), M, stream=st)
     h, rows = 512, 300
     x, res, gg = r(rows, h), r(rows, h), r(h)
     x1, u = torch.empty_like(x), torch.empty_like(x)
@@ -82,6 +109,22 @@ def layers():
     model = B.Model(h=h, n_heads=n, ffn=F, metp_chunks=2)
     ctx = B.Context(model)
     w, gr, x, dy = make_layer_buffers(torch, model, 1, s)
+    W = B.Weights(*(w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
+    G = B.Grads(*(gr[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    for pi in range(B.N_STRATEGIES):
+        sv = ctx.layer_fwd(pi, s, x.data_ptr(), W, y.data_ptr(), st)
+        ctx.layer_bwd(pi, dy.data_ptr(), sv, W, G, dx.data_ptr(), st)
+    ctx.set_varlen([256, 256])                       # varlen packing (TS / UZ / METP / METP-full)
+    for pi in (0, 1, 2, 4):
+        sv = ctx.layer_fwd(pi, s, x.data_ptr(), W, y.data_ptr(), st)
+        ctx.layer_bwd(pi, dy.data_ptr(), sv, W, G, dx.data_ptr(), st)
+    torch.cuda.synchronize()
+    ctx.close()
+    # the Llama variant (GQA 4 -> 2, SwiGLU), every strategy
+    lm = B.Model(h=h, n_heads=n, ffn=512, metp_chunks=2, n_kv_heads=2, ffn_act=1)
+    ctx = B.Context(lm)
+    w, gr, x, dy = make_layer_buffers(torch, lm, 1, s)
     W = B.Weights(*(w[k].data_ptr() for k in ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")))
     G = B.Grads(*(gr[k].data_ptr() for k in ("dw_qkv_t", "dw_proj", "dw_in_t", "dw_out", "dg1", "dg2")))
     y, dx = torch.empty_like(x), torch.empty_like(x)
