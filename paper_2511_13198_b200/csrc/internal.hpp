@@ -37,6 +37,11 @@ void set_error(const std::string& msg);
 // The exact per-rank byte plan of the CUDA path.  The
 // allocator and pds_mem_bytes both read it, so the model is exact by construction.
 constexpr int64_t kAlign = 256;
+// attention backward with dS through HBM: at most this many bytes of dS
+// workspace (kernel-level entry, pds_set_attn_bwd(2)); the layer plans use it up to
+// kDsMaxPos positions — 0: never (measured slower than the split kernels)
+constexpr int64_t kDsBudget = (int64_t)8 << 30;
+constexpr int64_t kDsMaxPos = 0;
 inline int64_t al(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Region {

@@ -127,9 +127,10 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
   static size_t scratch_bytes = 0;
   float* acc = nullptr;
   int* ctr = nullptr;
+  void* dsb = nullptr;
+  int64_t dsb_bytes = 0;
   std::lock_guard<std::mutex> lk(mu);
-  if (attn_bwd_fused_applies(d, causal) && s > 0) {
-    const size_t acc_b = (size_t)heads * s * d * 4, need = acc_b + ((size_t)heads * (s / 128) + 1) * 4;
+  auto grow = [&](size_t need) -> pds_status {
     if (need > scratch_bytes) {
       PDS_CUDA(cudaStreamSynchronize(st));
       if (scratch) cudaFree(scratch);
@@ -138,11 +139,19 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
       PDS_CUDA(cudaMalloc(&scratch, need));
       scratch_bytes = need;
     }
+    return PDS_OK;
+  };
+  if (attn_bwd_fused_applies(d, causal) && s > 0) {
+    const size_t acc_b = (size_t)heads * s * d * 4, need = acc_b + ((size_t)heads * (s / 128) + 1) * 4;
+    PDS_TRY(grow(need));
     acc = static_cast<float*>(scratch);
     ctr = reinterpret_cast<int*>(static_cast<char*>(scratch) + acc_b);
+  } else if (attn_bwd_mode() == 2 && (dsb_bytes = attn_ds_bytes(s, heads, heads, d, causal, kDsBudget)) > 0) {
+    PDS_TRY(grow((size_t)dsb_bytes));               // dS through HBM (reading R-DS)
+    dsb = scratch;
   }
-  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st, acc, ctr),
-                      "pds_k_attn_bwd");
+  pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st, acc, ctr,
+                               0, nullptr, dsb, dsb_bytes), "pds_k_attn_bwd");
   cudaFreeAsync(dd, st);
   return r;
 }
@@ -255,7 +264,8 @@ extern "C" pds_status pds_k_attn_dot(const void* out, int64_t ld_out, const void
 }
 
 extern "C" pds_status pds_set_attn_bwd(int32_t mode) {
-  if (mode != 0 && mode != 1) PDS_FAIL(PDS_EINVAL, "attention backward mode must be 0 (split) or 1 (fused)");
+  if (mode < 0 || mode > 2)
+    PDS_FAIL(PDS_EINVAL, "attention backward mode must be 0 (split), 1 (fused) or 2 (dS through HBM)");
   set_attn_bwd_mode(mode);
   return PDS_OK;
 }

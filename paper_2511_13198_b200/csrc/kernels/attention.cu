@@ -6,6 +6,7 @@
 // A/B baseline built separately, see its header).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -51,20 +52,37 @@ int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, c
 
 int attn_bwd_fused_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
                       int s, int heads, void* dqkv, const void* rope, float* dqacc, int* ctr, cudaStream_t st);
+int attn_bwd_ds_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                   int s, int heads, int kv_heads, void* dqkv, const void* rope, void* dsbuf, int64_t ds_bytes,
+                   cudaStream_t st);
 
-// 0: split dK/dV + dQ kernels (default), 1: fused kernel where it applies (pds_set_attn_bwd).
+int64_t attn_ds_bytes(int64_t s, int heads, int kv_heads, int d, int causal, int64_t budget) {
+  if (d != 128 || !causal || s <= 0 || s % 128) return 0;
+  if (kv_heads <= 0) kv_heads = heads;
+  const int grp = heads / kv_heads;
+  const int64_t per = s * s * 2;
+  int64_t G = std::min<int64_t>(heads, budget / per);
+  G -= G % grp;
+  return G >= 1 ? G * per : 0;
+}
+
+// 0: split dK/dV + dQ kernels (default), 1: fused kernel where it applies, 2: dS through HBM
+// for the kernel-level entry points (pds_set_attn_bwd; the layer path picks dS by its plan).
 // The fused kernel executes 5 matmuls instead of 7 but adds 64 KB of fp32 dQ reduction per
 // (key block, query block) pair through L2, which B200's L2 reduction throughput cannot
 // sustain at this tile shape: measured slower.
 static int g_bwd_mode = 0;
 void set_attn_bwd_mode(int mode) { g_bwd_mode = mode; }
 bool attn_bwd_fused_applies(int d, int causal) { return g_bwd_mode == 1 && d == 128 && causal; }
+int attn_bwd_mode() { return g_bwd_mode; }
 
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse,
              const void* dout, int s, int heads, int d, int causal, void* dqkv, const void* rope,
-             float* Dd, cudaStream_t st, float* dqacc, int* ctr, int kv_heads, const int* segs) {
+             float* Dd, cudaStream_t st, float* dqacc, int* ctr, int kv_heads, const int* segs, void* dsbuf,
+             int64_t ds_bytes) {
   if (s % 128) return (int)cudaErrorInvalidValue;
   if (kv_heads <= 0) kv_heads = heads;
+  const bool dspath = dsbuf && !segs && d == 128 && causal && ds_bytes >= (int64_t)s * s * 2 * (heads / kv_heads);
   const bool fused = dqacc && ctr && attn_bwd_fused_applies(d, causal) && kv_heads == heads && !segs;
   const int nctr = fused ? heads * (s / 128) + 1 : 0;
   const int nblk = (s * heads + 7) / 8;
@@ -73,6 +91,7 @@ int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const
                                             reinterpret_cast<const __nv_bfloat16*>(dout), s, heads, d, Dd, ctr,
                                             nctr);
   if (fused) return attn_bwd_fused_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, dqkv, rope, dqacc, ctr, st);
+  if (dspath) return attn_bwd_ds_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, kv_heads, dqkv, rope, dsbuf, ds_bytes, st);
   return attn_bwd_tc(qkv, ld, dout, ld_out, lse, Dd, s, heads, d, causal, dqkv, rope, st, 0, -1, kv_heads, segs);
 }
 

@@ -28,10 +28,12 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <string>
 #include <type_traits>
 
 #include "ptx.cuh"
+#include "gemm.cuh"
 
 namespace pds {
 
@@ -822,7 +824,8 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
                           const float* __restrict__ Dd, int s, int heads, int causal, __nv_bfloat16* __restrict__ dqkv,
                           int64_t ld, const float2* __restrict__ rope, float scale, float scale_log2, int qlo,
                           int qn, int kcol, int vcol, float* __restrict__ acc, int64_t ld_acc, int grp,
-                          const int* __restrict__ segs) {
+                          const int* __restrict__ segs, __nv_bfloat16* __restrict__ ds_out, int64_t ds_ld,
+                          int64_t ds_hstride, int head0) {
   using C = BwdKV4Cfg<D>;
   constexpr int NST = C::NST;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -842,7 +845,10 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
   // GQA: CTA = (key block, key / value head); its grp query heads run one after the
   // other through the same loop (iteration i = query head g = i / nqh, query block
   // qstart + i % nqh), so dK / dV accumulate over the group in TMEM
-  const int kb = blockIdx.x, head = blockIdx.y;
+  // ds_out (dS through HBM): also store dS^T = P^T o (dP^T - D) of every
+  // (key block, query block) as bf16 rows [query head - head0 * grp][key][query]; the dQ
+  // kernel is then replaced by one batched causal GEMM dQ = dS K
+  const int kb = blockIdx.x, head = head0 + blockIdx.y;
   const int k0 = kb * 128;
   // only the query blocks of [qlo, qlo + qn) contribute (dO, LSE, D are local to them);
   // the launch covers only key blocks that have at least one
@@ -1062,6 +1068,15 @@ __global__ void __launch_bounds__(128 + 128 * NWG, 1)
         }
         if (CW == 64) tmem_st32(c_d, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
         else tmem_st16(c_d, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        if (ds_out) {                          // this key row's CW dS values, one contiguous run
+          const int qh = i / nqh;               // query head within the group (launch-local)
+          const int qcol = (qstart + i % nqh) * 128 + CW * wg;
+          uint4* dst = reinterpret_cast<uint4*>(ds_out + ((int64_t)(blockIdx.y * grp + qh)) * ds_hstride +
+                                                (int64_t)(k0 + t) * ds_ld + qcol);
+#pragma unroll
+          for (int e = 0; e < CW / 8; ++e)
+            dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -2043,7 +2058,9 @@ template <int D>
 static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv, int64_t ld_kv, int kcol, int vcol,
                     const void* dout, int64_t ld_out, const void* lse, const float* Dd, int s, int heads, int causal,
                     void* dqkv, int64_t ld, const void* rope, int qlo, int qn, float* dq_acc, int64_t ld_dqa,
-                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int grp = 1, const int* segs = nullptr) {
+                    float* dkv_acc, int64_t ld_dkva, cudaStream_t st, int grp = 1, const int* segs = nullptr,
+                    __nv_bfloat16* ds_out = nullptr, int64_t ds_ld = 0, int64_t ds_hstride = 0, int head0 = 0,
+                    int kv_launch = 0) {
   CUtensorMap kv128, q128, do128;
   int rc = make_map_rows(&kv128, kv, (uint64_t)vcol + heads / grp * D, s, ld_kv, 128);
   rc |= make_map_rows(&q128, q, (uint64_t)heads * D, q_rows, ld_q, 128);
@@ -2071,10 +2088,11 @@ static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
     // the Q map is the K/V map (same buffer, same box): only the column offset differs
     // causal: key blocks past the last local query get nothing (the caller zeroes them)
     const int nkb = causal ? (qlo + qn) / 128 : s / 128;
-    attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, heads / grp), 128 + 128 * NW, BwdKV4Cfg<D>::SMEM, st>>>(
+    attn_bwd_dkdv4_kernel<D, NW><<<dim3(nkb, kv_launch > 0 ? kv_launch : heads / grp), 128 + 128 * NW,
+                                    BwdKV4Cfg<D>::SMEM, st>>>(
         kv128, q128, do128, reinterpret_cast<const float*>(lse), Dd, s, heads, causal,
         reinterpret_cast<__nv_bfloat16*>(dqkv), ld, reinterpret_cast<const float2*>(rope), scale, scale_log2,
-        qlo, qn, kcol, vcol, dkv_acc, ld_dkva, grp, segs);
+        qlo, qn, kcol, vcol, dkv_acc, ld_dkva, grp, segs, ds_out, ds_ld, ds_hstride, head0);
   };
   auto dq = [&](auto nw) {
     constexpr int NW = decltype(nw)::value;
@@ -2086,6 +2104,7 @@ static int bwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
   };
   if (force == 2) dkdv(std::integral_constant<int, 2>{});
   else dkdv(std::integral_constant<int, 4>{});
+  if (ds_out) return (int)cudaGetLastError();        // dQ by the caller's GEMM from dS
   if (force == 4) dq(std::integral_constant<int, 4>{});
   else dq(std::integral_constant<int, 2>{});
   return (int)cudaGetLastError();
@@ -2133,6 +2152,45 @@ int attn_bwd_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, c
     return bwd_tc_t<64>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, causal, dqkv, ld, rope, qlo,
                         qn, nullptr, 0, nullptr, 0, st, grp, segs);
   return (int)cudaErrorInvalidValue;
+}
+
+// dS through HBM (reading of the 5-matmul backward): per group of G query
+// heads, the dK/dV kernel also writes dS^T [G][s][s] (bf16, causal blocks only) into
+// dsbuf, and one batched causal tcgen05 GEMM dQ = scale * dS K (A = dS^T MN-major, B =
+// the K columns MN-major, K extent per query block = its causal prefix) applies RoPE^T
+// in its epilogue.  Executes 5 matmuls instead of 7; dS costs 2 s^2 B per head of HBM
+// traffic (written once, read once).  d = 128, causal, packed [Q | K | V] rows, no
+// varlen; G = ds_bytes / (2 s^2) rounded down to whole KV groups (>= 1 required).
+int attn_bwd_ds_tc(const void* qkv, int64_t ld, const void* dout, int64_t ld_out, const void* lse, const float* Dd,
+                   int s, int heads, int kv_heads, void* dqkv, const void* rope, void* dsbuf, int64_t ds_bytes,
+                   cudaStream_t st) {
+  constexpr int D = 128;
+  if (kv_heads <= 0) kv_heads = heads;
+  const int grp = heads / kv_heads;
+  const int64_t per = (int64_t)s * s * 2;
+  int G = (int)std::min<int64_t>(heads, ds_bytes / per);
+  G -= G % grp;
+  if (s % 128 || G < 1 || !dsbuf) return (int)cudaErrorInvalidValue;
+  const int hq = heads * D, hk = kv_heads * D;
+  for (int h0 = 0; h0 < heads; h0 += G) {
+    const int g = std::min(G, heads - h0);
+    int rc = bwd_tc_t<D>(qkv, ld, s, qkv, ld, hq, hq + hk, dout, ld_out, lse, Dd, s, heads, 1, dqkv, ld, rope, 0, s,
+                         nullptr, 0, nullptr, 0, st, grp, nullptr, static_cast<__nv_bfloat16*>(dsbuf), s,
+                         (int64_t)s * s, h0 / grp, g / grp);
+    if (rc) return rc;
+    GemmArgs ga;
+    ga.A = dsbuf; ga.lda = s; ga.a_mn = 1; ga.a_rows = (int64_t)g * s;
+    ga.B = static_cast<const __nv_bfloat16*>(qkv) + hq + (h0 / grp) * D; ga.ldb = ld; ga.b_mn = 1;
+    ga.b_rows = s; ga.b_cols = (int64_t)(kv_heads - h0 / grp) * D;
+    ga.M = s; ga.N = D; ga.K = s;
+    ga.C = static_cast<__nv_bfloat16*>(dqkv) + h0 * D; ga.ldc = ld;
+    ga.epi = EPI_ROPE_T; ga.rope = reinterpret_cast<const float2*>(rope); ga.rope_d = D;
+    ga.epi_scale = 1.0f / sqrtf((float)D);
+    ga.batch = g; ga.a_boff = s; ga.b_boff = D; ga.b_grp = grp; ga.c_boff = D; ga.k_causal = 1;
+    rc = gemm_launch(ga, st);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 // Backward of one ring-attention pair (attn_fwd_pair): lse / Dd [heads][sq] are the

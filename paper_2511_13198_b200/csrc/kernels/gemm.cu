@@ -73,6 +73,12 @@ struct EpiParams {
   int rot_mb;
   int chunk_cols;      // > 0: done_ctr counts per column block instead of per row chunk
   int rot_nb;
+  // batched / causal-K problems (gemm.cuh)
+  int batch;
+  int64_t a_boff, b_boff, c_boff;
+  int b_grp;
+  int k_causal;
+  float epi_scale;
 };
 
 // AG -> GEMM: wait until every chunk overlapping rows [r0, r0 + n) has landed.  The
@@ -232,8 +238,32 @@ __device__ __forceinline__ int64_t out_offset(const EpiParams& p, int row_l, int
 // tcgen05.ld, so every lane executes every load).
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const EpiParams& ep, uint32_t tbase, int row, bool row_ok,
-                                              int n0, int N) {
-  if (ep.epi == EPI_ROPE) {
+                                              int n0, int N, int bz = 0) {
+  if (ep.epi == EPI_ROPE_T) {
+    // RoPE^T (rotation by -angle) of the scaled accumulator, d = BN = 128 (one head per tile)
+    constexpr int D2 = BN / 2;
+    __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(ep.C) + (int64_t)bz * ep.c_boff;
+    for (int j0 = 0; j0 < D2; j0 += 32) {
+      uint32_t r1[32], r2[32];
+      tmem_ld32(tbase + j0, r1);
+      tmem_ld32(tbase + j0 + D2, r2);
+      tmem_ld_wait();
+      if (row_ok) {
+        const float2* cs = ep.rope ? ep.rope + (int64_t)row * D2 + j0 : nullptr;   // NULL: no rotation
+        float v1[32], v2[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float2 c = cs ? cs[i] : make_float2(1.0f, 0.0f);
+          const float a = __uint_as_float(r1[i]) * ep.epi_scale, b = __uint_as_float(r2[i]) * ep.epi_scale;
+          v1[i] = a * c.x + b * c.y;
+          v2[i] = -a * c.y + b * c.x;
+        }
+        store_row32_bf16(C + (int64_t)row * ep.ldc + j0, v1, 32);
+        store_row32_bf16(C + (int64_t)row * ep.ldc + j0 + D2, v2, 32);
+      }
+      __syncwarp();
+    }
+  } else if (ep.epi == EPI_ROPE) {
     const int d = ep.rope_d, d2 = d >> 1;
     int64_t pos = 0;
     if (row_ok) {
@@ -409,8 +439,26 @@ __global__ void __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM;
   const int nt = (N + BN - 1) / BN;
-  const int ntiles = mt * nt;
-  const int nkb = (K + BK - 1) / BK;
+  const int per = mt * nt;                       // tiles per problem (batch: ep.batch problems)
+  const int ntiles = per * ep.batch;
+  const int nkb_all = (K + BK - 1) / BK;
+  // tile t -> (problem z, m block, n block); a causal-K problem visits its heaviest
+  // (last) m blocks first so the persistent schedule ends balanced
+  auto coords = [&](int t, int& z, int& mb, int& nb) {
+    if (ep.batch > 1 || ep.k_causal) {
+      const int u = t % per;
+      z = t / per;
+      mb = mt - 1 - u / nt;                      // descending m: longest K first
+      nb = u % nt;
+      if (!ep.k_causal) mb = mt - 1 - mb;
+    } else {
+      z = 0;
+      tile_coords(t, mt, nt, mb, nb);
+      mb = rot_block(mb, mt, ep.rot_mb);
+      nb = rot_block(nb, nt, ep.rot_nb);
+    }
+  };
+  auto kblocks = [&](int mb) { return ep.k_causal ? min(nkb_all, (mb * BM + BM + BK - 1) / BK) : nkb_all; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -436,11 +484,10 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coords(t, mt, nt, mb, nb);
-        mb = rot_block(mb, mt, ep.rot_mb);
-        nb = rot_block(nb, nt, ep.rot_nb);
+        int z, mb, nb;
+        coords(t, z, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
+        const int nkb = kblocks(mb);
         wait_chunks(ep, m0, min(BM, M - m0));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -449,19 +496,20 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
           if (A_MN) {
-            const int kr = amap.map(k0);
+            const int kr = amap.map(k0) + (int)(z * ep.a_boff);
             tma_load_2d(sa, &tmA, &full_bar[stage], m0, kr);
             tma_load_2d(sa + 8192, &tmA, &full_bar[stage], m0 + 64, kr);
           } else {
-            tma_load_2d(sa, &tmA, &full_bar[stage], k0, amap.map(m0));
+            tma_load_2d(sa, &tmA, &full_bar[stage], k0, amap.map(m0) + (int)(z * ep.a_boff));
           }
           if (B_MN) {
             const int kr = bmap.map(k0);
+            const int nz = n0 + (int)((z / ep.b_grp) * ep.b_boff);
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(sb + i * 8192, &tmB, &full_bar[stage], n0 + 64 * i, kr);
+              tma_load_2d(sb + i * 8192, &tmB, &full_bar[stage], nz + 64 * i, kr);
           } else {
-            tma_load_2d(sb, &tmB, &full_bar[stage], k0, bmap.map(n0));
+            tma_load_2d(sb, &tmB, &full_bar[stage], k0, bmap.map(n0) + (int)((z / ep.b_grp) * ep.b_boff));
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -474,6 +522,9 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int z, mb, nb;
+      coords(t, z, mb, nb);
+      const int nkb = kblocks(mb);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
@@ -505,17 +556,15 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      int mb, nb;
-      tile_coords(t, mt, nt, mb, nb);
-      mb = rot_block(mb, mt, ep.rot_mb);
-      nb = rot_block(nb, nt, ep.rot_nb);
+      int z, mb, nb;
+      coords(t, z, mb, nb);
       const int m0 = mb * BM, n0 = nb * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      epilogue_tile<BN>(ep, tbase, row, row_ok, n0, N);
+      epilogue_tile<BN>(ep, tbase, row, row_ok, n0, N, z);
       count_stored(ep, m0 + q * 32, row_ok, n0, min(BN, N - n0));
       tc_fence_before();
       __syncwarp();
@@ -740,7 +789,7 @@ static int launch_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   if (A_MN) rc = make_map(&ta, g.A, g.M, a_rows, g.lda, 64, 64);
   else      rc = make_map(&ta, g.A, g.K, a_rows, g.lda, 64, BM);
   if (rc) return rc;
-  if (B_MN) rc = make_map(&tb, g.B, g.N, b_rows, g.ldb, 64, 64);
+  if (B_MN) rc = make_map(&tb, g.B, g.b_cols > 0 ? g.b_cols : g.N, b_rows, g.ldb, 64, 64);
   else      rc = make_map(&tb, g.B, g.K, b_rows, g.ldb, 64, BN);
   if (rc) return rc;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN>;
@@ -749,7 +798,7 @@ static int launch_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr_set = true;
   }
-  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * (g.batch > 0 ? g.batch : 1);
   const int sms = gemm_num_sms() - g.sm_reserve;
   const int grid = tiles < sms ? tiles : sms;
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
@@ -821,6 +870,15 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   ep.wait_flags = g.wait_flags; ep.flag_epoch = g.flag_epoch;
   ep.done_ctr = g.done_ctr; ep.chunk_rows = (int)g.chunk_rows; ep.rot_mb = 0;
   ep.chunk_cols = (int)g.chunk_cols; ep.rot_nb = 0;
+  ep.batch = g.batch > 0 ? g.batch : 1;
+  ep.a_boff = g.a_boff; ep.b_boff = g.b_boff; ep.c_boff = g.c_boff;
+  ep.b_grp = g.b_grp > 0 ? g.b_grp : 1;
+  ep.k_causal = g.k_causal; ep.epi_scale = g.epi_scale;
+  const bool plain1 = ep.batch > 1 || g.k_causal || g.epi == EPI_ROPE_T;   // 1-CTA kernel, BN = 128
+  if (plain1 && (g.wait_flags || g.done_ctr || g.blk_w || g.a_seg || g.b_seg || g.c_seg || g.m_rot_rows ||
+                 g.n_rot_cols))
+    return (int)cudaErrorInvalidValue;
+  if (g.epi == EPI_ROPE_T && g.N != 128) return (int)cudaErrorInvalidValue;
   if (g.wait_flags || (g.done_ctr && g.chunk_cols <= 0)) {
     if (g.chunk_rows <= 0 || g.chunk_rows % 32 || g.M % g.chunk_rows) return (int)cudaErrorInvalidValue;
     if (g.wait_flags && (g.a_mn || g.a_seg)) return (int)cudaErrorInvalidValue;
@@ -842,7 +900,8 @@ int gemm_launch(const GemmArgs& g, cudaStream_t st) {
   if (g.epi == EPI_SWIGLU && (g.N % 128 || !g.aux_out)) return (int)cudaErrorInvalidValue;
   if (g.epi == EPI_DSWIGLU && (g.N % 64 || !g.aux_in)) return (int)cudaErrorInvalidValue;
   const int64_t pair_tiles = (int64_t)((g.M + 255) / 256) * ((g.N + 255) / 256);
-  const bool pair_ok = pair_mode() && g.M >= 256 && (g.N % 256 == 0 || g.N > 1024) &&
+  if (plain1) use256 = false;
+  const bool pair_ok = !plain1 && pair_mode() && g.M >= 256 && (g.N % 256 == 0 || g.N > 1024) &&
                        pair_tiles >= gemm_num_sms() / 2 && (g.a_seg == 0 || g.a_seg % 128 == 0) &&
                        (!g.a_mn || g.M % 64 == 0) && (!g.b_mn || g.N % 64 == 0) &&
                        (g.b_seg == 0 || g.b_seg % 128 == 0);

@@ -20,6 +20,8 @@ enum GemmEpi : int {
   // SwiGLU (Llama variant, R-SWIGLU): the FC1 output's columns are interleaved in
   // blocks of 64, [gate_j | up_j] per 128 (N % 128 == 0, every tile holds whole pairs)
   EPI_SWIGLU = 6,    // C bf16 = H = acc [M, N] ; aux_out bf16 [M, N/2] = SiLU(bf16 gate) * bf16 up
+  EPI_ROPE_T = 8,    // C bf16 [M, d] = RoPE^T(epi_scale * acc) at position = row (the attention dQ
+                     // from dS K); N == d == 128
   EPI_DSWIGLU = 7,   // acc = dG [M, N]; aux_in = H [M, 2N] (row stride ld_aux_in): C bf16 [M, 2N]
                      // = dH (dgate = dG up SiLU'(gate), dup = dG SiLU(gate)) in H's layout;
                      // aux_out [M, N] = G; c_t = dH^T [2N][ld_t]; aux_t = G^T [N][ld_t]
@@ -93,6 +95,17 @@ struct GemmArgs {
   // column of the tile order (wraps).
   int64_t chunk_cols = 0;
   int64_t n_rot_cols = 0;
+  // Batched GEMM (1-CTA kernel only): `batch` independent problems of the same shape; problem
+  // z reads A rows shifted by z * a_boff (MN-major A: the stored K rows), B columns shifted by
+  // z * b_boff (MN-major B) and writes C columns shifted by z * c_boff.  k_causal: the tile of
+  // rows [m0, m0 + 128) only runs the K blocks below m0 + 128 (a causal contraction: K index
+  // <= M index).  epi_scale: EPI_ROPE_T's scale.
+  int batch = 1;
+  int64_t a_boff = 0, b_boff = 0, c_boff = 0;
+  int b_grp = 1;                  // B's shift is (z / b_grp) * b_boff (GQA: query heads per K head)
+  int64_t b_cols = 0;             // MN-major B: stored column extent (0: N)
+  int k_causal = 0;
+  float epi_scale = 1.0f;
 };
 
 // returns 0 on success, a cudaError_t value otherwise

@@ -14,12 +14,18 @@ int attn_fwd(const void* qkv, int64_t ld, int s, int heads, int d, int causal, v
 // one-kernel backward (d = 128, causal, MHA); NULL keeps the split dK/dV + dQ kernels
 int attn_bwd(const void* qkv, int64_t ld, const void* out, int64_t ld_out, const void* lse, const void* dout,
              int s, int heads, int d, int causal, void* dqkv, const void* rope, float* Dd, cudaStream_t st,
-             float* dqacc = nullptr, int* ctr = nullptr, int kv_heads = 0, const int* segs = nullptr);
+             float* dqacc = nullptr, int* ctr = nullptr, int kv_heads = 0, const int* segs = nullptr,
+             void* dsbuf = nullptr, int64_t ds_bytes = 0);
+// dS-through-HBM backward: the dsbuf bytes attn_bwd uses for a causal d = 128
+// attention over s positions with at most `budget` bytes (whole KV groups of heads, s^2 bf16
+// each); 0 when the path does not apply (then the split kernels run)
+int64_t attn_ds_bytes(int64_t s, int heads, int kv_heads, int d, int causal, int64_t budget);
 // varlen packing (R-VARLEN): segs int32 [2 * s / 128] on the device, for every 128-row
 // block the [first, last + 1) block range of the sequence it belongs to (sequences are
 // 256-row aligned); attention stays inside each sequence and RoPE positions restart at
 // its first row; NULL = one sequence
 bool attn_bwd_fused_applies(int d, int causal);
+int attn_bwd_mode();
 void set_attn_bwd_mode(int mode);
 // context parallelism: queries [qlo, qlo + qn) against all s keys (attention.cu)
 int attn_fwd_rows(const void* qkv, int64_t ld, int s, int heads, int d, int causal, int qlo, int qn, void* out,

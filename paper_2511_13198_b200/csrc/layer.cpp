@@ -409,7 +409,8 @@ struct Exec {
   // a workspace region that is free during the attention backward) and its counters;
   // NULL selects the split kernels
   pds_status attn_b(const void* qkv, const void* out, const void* lse, const void* dout, void* dqkv, float* dd,
-                    void* sc = nullptr, int64_t sc_bytes = 0, int* ctr = nullptr) {
+                    void* sc = nullptr, int64_t sc_bytes = 0, int* ctr = nullptr, void* dsb = nullptr,
+                    int64_t dsb_bytes = 0) {
     const double fl = b * 10.0 * nl * d * (m.causal ? 0.5 * sq * sq : (double)sq * sq);
     Prof p(c, st, K_ATTN_B, fl, 0);
     float* acc = sc && ctr && sc_bytes >= nl * sq * d * 4 ? static_cast<float*>(sc) : nullptr;
@@ -418,7 +419,8 @@ struct Exec {
                             static_cast<const char*>(out) + bi * hl * 2, hl * b,
                             static_cast<const float*>(lse) + bi * nl * sq, static_cast<const char*>(dout) + bi * hl * 2,
                             (int)sq, (int)nl, (int)d, m.causal, static_cast<char*>(dqkv) + bi * qw * 2, c->rope,
-                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr, (int)nkl, segs), "attn_bwd"));
+                            dd + bi * nl * sq, st, acc, acc ? ctr : nullptr, (int)nkl, segs, dsb, dsb_bytes),
+                   "attn_bwd"));
     return PDS_OK;
   }
   // collectives
@@ -659,7 +661,8 @@ pds_status ts_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(tn.mm(gather, e.h, w->w_proj, e.h, e.s, e.hl, e.h, f1, e.hl));                 // dA
   PDS_TRY(tn.dw(sv->at("a"), e.hl, gather, e.h, e.s, e.hl, e.h, g->dw_proj));            // dW_proj += A^T dX1
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), f1, f0, dd, tn.ta, bp.ws_size("ta"),
-                   reinterpret_cast<int*>(ws + bp.ws_off("actr"))));                     // dQKV (RoPE^T)
+                   reinterpret_cast<int*>(ws + bp.ws_off("actr")), bp.has_ws("dsb") ? ws + bp.ws_off("dsb") : nullptr,
+                   bp.ws_size("dsb")));                     // dQKV (RoPE^T)
   if (pre) {
     PDS_TRY(e.wait(e.st, ev_u));
   } else {
@@ -793,7 +796,8 @@ pds_status uz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   PDS_TRY(uz_dw(e, dw, e.h, g->dw_proj));
   if (!ov) PDS_TRY(e.a2a(s1, r1, e.sl * e.hl));                                         // A2A(dO)
   PDS_TRY(e.attn_b(sv->at("qkv"), sv->at("a"), sv->at("lse"), r1, x3, dd, tn.ta, bp.ws_size("ta"),
-                   reinterpret_cast<int*>(ws + bp.ws_off("actr"))));
+                   reinterpret_cast<int*>(ws + bp.ws_off("actr")), bp.has_ws("dsb") ? ws + bp.ws_off("dsb") : nullptr,
+                   bp.ws_size("dsb")));
   PDS_TRY(e.a2a(x3, r1, e.sl * e.qw));                                                 // A2A(dQKV)
   {
     Prof p(e.c, e.st, K_NORM, 0, 4.0 * e.sl * e.qwf);
@@ -1478,7 +1482,8 @@ pds_status metp_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w
   // the dQ accumulator borrows ul + vl (adjacent, 2u, free between the waves)
   const int64_t ulv = bp.ws_off("vl") == bp.ws_off("ul") + bp.ws_size("ul") ? 2 * bp.ws_size("ul") : bp.ws_size("ul");
   PDS_TRY(e.attn_b(qkv, sv->at("a"), sv->at("lse"), da, dqkv, dd, ul, ulv,
-                   reinterpret_cast<int*>(ws + bp.ws_off("actr"))));
+                   reinterpret_cast<int*>(ws + bp.ws_off("actr")), bp.has_ws("dsb") ? ws + bp.ws_off("dsb") : nullptr,
+                   bp.ws_size("dsb")));
   PDS_TRY(tn.tr(w->w_qkv_t, e.h, e.qw, e.h, wt));                // W_qkv for dU, every wave
   for (int64_t k = 0; k < c; ++k) {   // QKV backward waves
     const int64_t o = k * wr;

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "internal.hpp"
+#include "kernels/kernels.hpp"
 
 namespace pds {
 
@@ -254,6 +255,11 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
   // (its fp32 dQ accumulator borrows a region that is free during the attention
   // backward: ta for TS / UZ, ul + vl for METP)
   const int64_t actr = (nl * (s / 128) + 1) * 4;
+  // the attention backward's dS buffer (dS through HBM): measured slower than
+  // the split kernels on B200, so the layer plans never reserve it (kDsMaxPos = 0); the
+  // path stays selectable for the kernel-level entry point (pds_set_attn_bwd(2))
+  const int64_t dsb = s <= kDsMaxPos ? attn_ds_bytes(s, (int)nl, (int)(nk / P), (int)(h / m.n_heads), m.causal,
+                                                     kDsBudget) : 0;
   switch (strategy) {
     case PDS_MEGATRON_TS:
       push(p.saved, ts, "rstd1", ell);
@@ -274,6 +280,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * S * 2);
       push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
       if (P > 1) push(p.ws, tw, "gather2", S * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
@@ -306,6 +313,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * SL * 2);
       push(p.ws, tw, "wt", h * std::max(f1wf, qwf) * 2);
       push(p.ws, tw, "actr", actr);
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
       break;
     }
     case PDS_METP:
@@ -343,6 +351,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * P * W * 2);
       push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
       if (full) push(p.ws, tw, "qkv", S * qw * 2);
       break;
     }

@@ -592,3 +592,16 @@ def test_gemm_rope_gqa_groups():
         for c0 in range(g0, g0 + hq + hk, d):
             ref[:, c0:c0 + d] = OL.rope_apply(raw[:, c0:c0 + d], cos, sin)
     assert rel(host(c), ref) < 1e-2
+
+
+# ---------------------------------------------------------------- dS through HBM (R-DS)
+@pytest.mark.parametrize("s,heads", [(256, 2), (640, 3), (1152, 4)])
+def test_attention_bwd_ds_path_vs_oracle(s, heads):
+    """Backward with dS through HBM (pds_set_attn_bwd(2)): the dK/dV kernel also stores
+    dS^T, one batched causal GEMM forms dQ = scale dS K.  Same oracle check as the split
+    kernels (causal, d = 128, ragged block counts)."""
+    try:
+        B.set_attn_bwd(2)
+        _attention_fwd_bwd(128, 1, s, heads=heads)
+    finally:
+        B.set_attn_bwd(0)

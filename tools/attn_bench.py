@@ -22,8 +22,9 @@ def main():
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fused", action="store_true", help="fused backward kernel instead of the split dK/dV + dQ")
+    ap.add_argument("--ds", action="store_true", help="dS through HBM: dK/dV kernel + batched causal dQ GEMM")
     a = ap.parse_args()
-    B.set_attn_bwd(1 if a.fused else 0)
+    B.set_attn_bwd(1 if a.fused else 2 if a.ds else 0)
     s, H, d = a.s, a.heads, a.d
     hq = H * d
     qkv = (torch.randn(s, 3 * hq, device="cuda") * 0.5).to(torch.bfloat16)
@@ -47,7 +48,8 @@ def main():
             if r:
                 ts.append(e0.elapsed_time(e1))
         ms = min(ts)
-        print(f"{name}{' fused' if a.fused and name == 'bwd' else ''} s={s} {ms:.3f} ms {mult * fl / 2 / ms / 1e9:.1f} TF/s", flush=True)
+        tag = (" fused" if a.fused else " ds" if a.ds else "") if name == "bwd" else ""
+        print(f"{name}{tag} s={s} {ms:.3f} ms {mult * fl / 2 / ms / 1e9:.1f} TF/s", flush=True)
 
 
 if __name__ == "__main__":
