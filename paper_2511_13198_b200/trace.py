@@ -279,9 +279,10 @@ def predict_main(a):
     sys.path.insert(0, ROOT)
     from synth import pad_to, sample_lengths
     from . import binding as B
-    H, N, F = 4096, 32, 16384
-    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)
+    H, N, F = a.h, a.heads, a.ffn           # default configs[1]'s 7B layer; --h 12288 --heads 96 --ffn 49152 --L 8:
+    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)    # the paper's GPT of Table 4 / Table 5
     out = {"mode": "predicted (cost model + exact memory plan on host-only contexts; no device run)",
+           "model": {"h": H, "n_heads": N, "ffn": F, "L": a.L},
            "dataset": a.dataset, "n": a.n, "L": a.L, "gamma": a.gamma, "by_P": {}}
     raw = sample_lengths(a.dataset, a.n, seed=42)
     for P in a.P:
@@ -330,6 +331,9 @@ def main():
         ap.add_argument("--P", type=int, nargs="+", default=[1, 2, 4, 8])
         ap.add_argument("--gamma", type=float, default=0.0)
         ap.add_argument("--ablation", action="store_true")
+        ap.add_argument("--h", type=int, default=4096)
+        ap.add_argument("--heads", type=int, default=32)
+        ap.add_argument("--ffn", type=int, default=16384)
         ap.add_argument("--out", default=None)
         return predict_main(ap.parse_args())
     sys.path.insert(0, ROOT)
