@@ -266,6 +266,10 @@ def test_llama_variant_equals_unsharded(pi, P, n_kv):
     for r in range(P):
         assert _rel(grads["dw_qkv_t"][r], ref_sh["w_qkv_t"][r]) < 1e-12
         assert _rel(grads["dw_in_t"][r], ref_sh["w_in_t"][r]) < 1e-12
+    # the simulated comm log's bytes = the formula with the variant's widths
+    full = "full" if pi == S.METP_FULL else "ffn"
+    assert sum(e["bytes"] for e in g.comm_log) == flops.comm_bytes(pi, H, s, P, ffn, b=2, metp_recompute=full, n=N,
+                                                                 n_kv=n_kv, act="swiglu"), pi
 
 
 def test_llama_variant_validity():
