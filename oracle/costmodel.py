@@ -113,8 +113,14 @@ def read_bundle(path):
     for _ in range(7):
         k = nxt()
         hdr[k] = int(nxt()) if k not in ("capacity", "reserve") else float(nxt())
+    k = nxt()
+    if k == "kv":                     # optional Llama-variant fields (R-GQA / R-SWIGLU)
+        hdr["kv"] = int(nxt())
+        assert nxt() == "act"
+        hdr["act"] = int(nxt())
+        k = nxt()
     norm = []
-    assert nxt() == "norm"
+    assert k == "norm"
     for _ in range(4):
         norm.append((float(nxt()), float(nxt())))
     assert nxt() == "n_strat"

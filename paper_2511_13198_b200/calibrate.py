@@ -89,7 +89,7 @@ def aic_poly(s, y, degrees=PR_DEGREES):
     return best[1], best[2], scale
 
 
-def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
+def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note="", n_kv=0, act=0):
     """records: {strategy: [(s, seconds), ...]} -> bundle file."""
     from sklearn.ensemble import RandomForestRegressor
     strategies = sorted(k for k in records if len(records[k]) >= 2)   # profiled (fits the device)
@@ -102,8 +102,9 @@ def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
             return 0.0 if a == b else (v - a) / (b - a)
         return oh + [nz(h, *norm[0]), nz(n, *norm[1]), nz(L, *norm[2]), nz(s, *norm[3])]
 
+    variant = f" kv {n_kv} act {act}" if (n_kv and n_kv != n) or act else ""   # Llama variant only
     lines = ["pds_bundle 1",
-             f"P {P} h {h} n {n} ffn {ffn} L {L} capacity {capacity!r} reserve {reserve!r}",
+             f"P {P} h {h} n {n} ffn {ffn} L {L} capacity {capacity!r} reserve {reserve!r}{variant}",
              "norm " + " ".join(f"{float(a)!r} {float(b)!r}" for a, b in norm),
              f"n_strat {len(strategies)}"]
     for pi in strategies:
@@ -125,7 +126,7 @@ def fit_and_export(path, P, h, n, ffn, L, records, capacity, reserve, note=""):
     with open(path, "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(path + ".json", "w") as f:
-        json.dump({"P": P, "h": h, "n": n, "ffn": ffn, "L": L, "note": note,
+        json.dump({"P": P, "h": h, "n": n, "ffn": ffn, "L": L, "n_kv": n_kv, "act": act, "note": note,
                    "records": {str(k): v for k, v in records.items()}}, f, indent=1)
     return path
 
@@ -140,7 +141,7 @@ def refit(path):
     res = float(re.search(r"reserve ([0-9.eE+-]+)", hdr).group(1))
     records = {int(k): [tuple(r) for r in v] for k, v in meta["records"].items()}
     return fit_and_export(path, meta["P"], meta["h"], meta["n"], meta["ffn"], meta["L"], records, cap, res,
-                          note=meta.get("note", ""))
+                          note=meta.get("note", ""), n_kv=meta.get("n_kv", 0), act=meta.get("act", 0))
 
 
 # ------------------------------------------------------------------ profiling (GPU)
@@ -185,37 +186,42 @@ def time_layer(torch, B, ctx, pi, s, w, gr, x, dy, reps=5, warm=2):
     return float(np.median(ts))
 
 
-def comm_bytes_per_rank(pi, h, F, s, P):
-    """Bytes each rank moves per layer fwd+bwd (ring payload (P-1)/P x full)."""
+def comm_bytes_per_rank(pi, h, F, s, P, n=None, n_kv=None, act=0):
+    """Bytes each rank moves per layer fwd+bwd (ring payload (P-1)/P x full).  Llama variant:
+    GQA narrows the K / V blocks to n_kv d (Q|K|V width h + 2 n_kv d), SwiGLU weighs 3hF."""
     if P == 1:
         return 0.0
     fr = (P - 1) / P
-    act = s * h * 2
+    act_b = s * h * 2
+    hk = h if not n or not n_kv else n_kv * (h // n)
+    qw = h + 2 * hk
     if pi in (0, 2):
-        return 10 * fr * act + 2 * fr * 8 * h
+        return 10 * fr * act_b + 2 * fr * 8 * h
     if pi == 4:              # METP-full: TS bytes + one more AG(u) for the Q/K/V recompute
-        return 11 * fr * act + 2 * fr * 8 * h
-    wb = 4 * h * h + 2 * h * F
+        return 11 * fr * act_b + 2 * fr * 8 * h
+    wb = qw * h + h * h + (3 if act else 2) * h * F
     if pi == 3:              # CZ (R-CZ): zigzag exchanges + K/V ring (bf16) + dK/dV ring (fp32), ZeRO3 weights
-        return cz_zig_bytes(h, s, P) + cz_ring_bytes(h, s, P) + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
+        return cz_zig_bytes(h, s, P, qw) + cz_ring_bytes(hk, s, P) + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
     if pi == 5:              # ColossalZ (RSA): K, V rings fwd + V, K rings bwd (bf16), dV, dK rings (fp32)
-        kb = (s // P) * h
+        kb = (s // P) * hk
         return 4 * (P - 1) * kb * 2 + 2 * P * kb * 4 + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
-    a2a = 2 * fr * (s // P) * 4 * h * 2
+    a2a = 2 * fr * (s // P) * (qw + h) * 2
     return a2a + fr * wb * (2 + 2 + 4) + 2 * fr * 8 * h
 
 
-def cz_zig_bytes(h, s, P):
+def cz_zig_bytes(h, s, P, qw=None):
     """MegatronCZ's boundary <-> zigzag point-to-point exchanges per rank per layer (mean):
     QKV and O (fwd), O, dO and dQKV (bwd); a half-chunk moves unless its zigzag owner is
-    its boundary owner (layer.cpp zig_exchange)."""
+    its boundary owner (layer.cpp zig_exchange).  qw: the Q|K|V width (3h for MHA)."""
+    qw = 3 * h if qw is None else qw
     moved = sum(1 for j in range(2 * P) if (j if j < P else 2 * P - 1 - j) != j // 2)
-    return moved * (s // (2 * P)) * 9 * h * 2 / P
+    return moved * (s // (2 * P)) * (2 * qw + 3 * h) * 2 / P
 
 
-def cz_ring_bytes(h, s, P):
-    """K/V ring passes (P - 1 fwd, P - 1 bwd, bf16) and the dK/dV accumulator ring (P, fp32)."""
-    kv = (s // P) * 2 * h
+def cz_ring_bytes(hk, s, P):
+    """K/V ring passes (P - 1 fwd, P - 1 bwd, bf16) and the dK/dV accumulator ring (P, fp32);
+    hk = the K (V) width (h for MHA)."""
+    kv = (s // P) * 2 * hk
     return 2 * (P - 1) * kv * 2 + P * kv * 4
 
 
@@ -230,10 +236,15 @@ def class_seconds(torch, B, ctx, pi, s, w, gr, x, dy, classes):
     return ms / 1e3
 
 
-def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.0):
+def bundle_name(h, n, ffn, P, n_kv=0, act=0):
+    var = (f"_kv{n_kv}" if n_kv and n_kv != n else "") + ("_swiglu" if act else "")
+    return f"h{h}_n{n}{var}_f{ffn}_P{P}.txt"
+
+
+def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.0, n_kv=0, act=0):
     import torch
     from . import binding as B
-    model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L)
+    model = B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, n_kv_heads=n_kv, ffn_act=act)
     records = {pi: [] for pi in ALL}
     if P_target == 1:
         ctx = B.Context(model)
@@ -263,7 +274,8 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
         # n/P heads; METP: TS compute + waves) on a 1-rank context whose layer runs the
         # same kernels, then collective bytes / link bandwidth added.
         ctx = B.Context(model)
-        ctx_m = B.Context(B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, metp_chunks=P_target))
+        ctx_m = B.Context(B.Model(h=h, n_heads=n, ffn=ffn, n_layers=L, metp_chunks=P_target, n_kv_heads=n_kv,
+                                  ffn_act=act))
         for s in grid:
             t_unit, t_gemm = {}, {}
             t_att = 0.0
@@ -280,11 +292,12 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
             torch.cuda.empty_cache()
             for pi in t_unit:
                 comp = t_unit[pi] / P              # CZ: zigzag placement, every rank 1/P of the attention
-                comm = comm_bytes_per_rank(pi, h, ffn, s, P) / (link_gbs * 1e9)
+                comm = comm_bytes_per_rank(pi, h, ffn, s, P, n, n_kv, act) / (link_gbs * 1e9)
                 if pi == 3:
                     # the K/V ring passes run on the side stream under the ring step's
                     # attention (P steps of 1/P^2 of it each); the rest stays exposed
-                    ring = 2 * (P - 1) * (s // P) * 2 * h * 2 / (link_gbs * 1e9)
+                    hk = h if not n_kv else n_kv * (h // n)
+                    ring = 2 * (P - 1) * (s // P) * 2 * hk * 2 / (link_gbs * 1e9)
                     comm -= min(ring, t_att / P * (P - 1) / P)
                 if pi in (0, 2, 4):
                     # tile-overlapped AG / RS: each runs under the GEMM that
@@ -303,9 +316,10 @@ def profile(P_target, h, n, ffn, L, grid, out_dir=BUNDLES, reps=5, link_gbs=770.
                 "ring passes hidden under the ring steps' attention); replace with a measured profile on an "
                 "8xB200 box")
     os.makedirs(out_dir, exist_ok=True)
-    path = os.path.join(out_dir, f"h{h}_n{n}_f{ffn}_P{P_target}.txt")
+    path = os.path.join(out_dir, bundle_name(h, n, ffn, P_target, n_kv, act))
     cap = float(torch.cuda.get_device_properties(0).total_memory)
-    fit_and_export(path, P_target, h, n, ffn, L, records, capacity=cap, reserve=8.0 * 2 ** 30, note=note)
+    fit_and_export(path, P_target, h, n, ffn, L, records, capacity=cap, reserve=8.0 * 2 ** 30, note=note,
+                   n_kv=n_kv, act=act)
     return path
 
 
@@ -371,6 +385,8 @@ if __name__ == "__main__":
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--ffn", type=int, default=16384)
     ap.add_argument("--L", type=int, default=32)
+    ap.add_argument("--kv", type=int, default=0, help="GQA key/value heads (Llama variant; 0: MHA)")
+    ap.add_argument("--act", type=int, default=0, help="1: SwiGLU FFN (Llama variant)")
     # four lengths per octave, 1K..64K, multiples of 256 (every strategy valid at P = 1):
     # the random forest interpolates between profiled lengths only (Eq. 9), and with one
     # point per octave its piecewise-constant predictions misranked near-equal strategies
@@ -382,7 +398,7 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.refit:
         for P in a.P:
-            print(refit(os.path.join(BUNDLES, f"h{a.h}_n{a.n}_f{a.ffn}_P{P}.txt")))
+            print(refit(os.path.join(BUNDLES, bundle_name(a.h, a.n, a.ffn, P, a.kv, a.act))))
         raise SystemExit(0)
     if a.measured:
         grid = a.grid if a.grid != ap.get_default("grid") else [8192, 16384, 32768, 65536, 131072]
@@ -390,4 +406,4 @@ if __name__ == "__main__":
         raise SystemExit(0)
     for P in a.P:
         t0 = time.time()
-        print(profile(P, a.h, a.n, a.ffn, a.L, a.grid, reps=a.reps), f"{time.time() - t0:.1f}s")
+        print(profile(P, a.h, a.n, a.ffn, a.L, a.grid, reps=a.reps, n_kv=a.kv, act=a.act), f"{time.time() - t0:.1f}s")

@@ -104,6 +104,7 @@ struct StratCost {
 struct Bundle {
   bool loaded = false;
   int P = 0, h = 0, n = 0, ffn = 0, L = 0;
+  int n_kv = 0, act = 0;          // Llama variant (0 = n heads, GELU)
   double capacity = 0, reserve = 0;
   double norm[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
   StratCost strat[PDS_N_STRATEGIES];

@@ -1914,6 +1914,9 @@ extern "C" pds_status pds_load_costs(pds_ctx* c, const char* path) {
   PDS_TRY(load_bundle(path, &b));
   if (b.P != c->P || b.h != c->m.h || b.n != c->m.n_heads || b.ffn != c->m.ffn)
     PDS_FAIL(PDS_EINVAL, "bundle (P, h, n, ffn) does not match the context");
+  const int kv_b = b.n_kv > 0 ? b.n_kv : b.n, kv_c = c->m.n_kv_heads > 0 ? c->m.n_kv_heads : c->m.n_heads;
+  if (kv_b != kv_c || b.act != c->m.ffn_act)
+    PDS_FAIL(PDS_EINVAL, "bundle (n_kv, ffn_act) does not match the context");
   c->bundle = b;
   c->cache.clear();
   c->prev.clear();

@@ -130,7 +130,13 @@ pds_status load_bundle(const char* path, Bundle* b) {
       !expect("ffn") || !(f >> nb.ffn) || !expect("L") || !(f >> nb.L) || !expect("capacity") ||
       !(f >> nb.capacity) || !expect("reserve") || !(f >> nb.reserve))
     return PDS_EINVAL;
-  if (!expect("norm")) return PDS_EINVAL;
+  // optional (Llama variant, R-GQA / R-SWIGLU): "kv <n_kv> act <0|1>"; absent = MHA + GELU
+  if (!(f >> tok)) PDS_FAIL(PDS_EINVAL, "pds_load_costs: truncated header");
+  if (tok == "kv") {
+    if (!(f >> nb.n_kv) || !expect("act") || !(f >> nb.act)) PDS_FAIL(PDS_EINVAL, "pds_load_costs: bad kv / act");
+    if (!(f >> tok)) PDS_FAIL(PDS_EINVAL, "pds_load_costs: truncated header");
+  }
+  if (tok != "norm") PDS_FAIL(PDS_EINVAL, "pds_load_costs: expected 'norm', got '" + tok + "'");
   for (int i = 0; i < 4; ++i) f >> nb.norm[i][0] >> nb.norm[i][1];
   int ns = 0;
   if (!expect("n_strat") || !(f >> ns)) return PDS_EINVAL;

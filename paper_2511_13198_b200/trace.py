@@ -280,13 +280,16 @@ def predict_main(a):
     from synth import pad_to, sample_lengths
     from . import binding as B
     H, N, F = a.h, a.heads, a.ffn           # default configs[1]'s 7B layer; --h 12288 --heads 96 --ffn 49152 --L 8:
-    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L)    # the paper's GPT of Table 4 / Table 5
+    model = B.Model(h=H, n_heads=N, ffn=F, n_layers=a.L,    # the paper's GPT of Table 4 / Table 5; --kv / --act:
+                    n_kv_heads=a.kv, ffn_act=a.act)         # the Llama variant
     out = {"mode": "predicted (cost model + exact memory plan on host-only contexts; no device run)",
-           "model": {"h": H, "n_heads": N, "ffn": F, "L": a.L},
+           "model": {"h": H, "n_heads": N, "ffn": F, "L": a.L, "n_kv": a.kv or N,
+                     "act": "swiglu" if a.act else "gelu"},
            "dataset": a.dataset, "n": a.n, "L": a.L, "gamma": a.gamma, "by_P": {}}
     raw = sample_lengths(a.dataset, a.n, seed=42)
     for P in a.P:
-        bundle = os.path.join(HERE, "bundles", f"h{H}_n{N}_f{F}_P{P}.txt")
+        from .calibrate import bundle_name
+        bundle = os.path.join(HERE, "bundles", bundle_name(H, N, F, P, a.kv, a.act))
         # pad to a multiple every strategy accepts (R-15; METP's c = P waves of 128 rows:
         # 128 P^2), curriculum order
         unit = max(128 * P * P, 256 * P)
@@ -334,6 +337,8 @@ def main():
         ap.add_argument("--h", type=int, default=4096)
         ap.add_argument("--heads", type=int, default=32)
         ap.add_argument("--ffn", type=int, default=16384)
+        ap.add_argument("--kv", type=int, default=0)
+        ap.add_argument("--act", type=int, default=0)
         ap.add_argument("--out", default=None)
         return predict_main(ap.parse_args())
     sys.path.insert(0, ROOT)

@@ -76,7 +76,8 @@ def test_predict_time_branches():
 def _bundle_ctx(B, path):
     bd = CM.read_bundle(path)
     hd = bd["hdr"]
-    ctx = B.Context(B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=hd["L"]), P=hd["P"], device=-1)
+    ctx = B.Context(B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=hd["L"], n_kv_heads=hd.get("kv", 0),
+                            ffn_act=hd.get("act", 0)), P=hd["P"], device=-1)
     ctx.load_costs(path)
     return ctx, bd
 
@@ -121,8 +122,9 @@ def test_cost_eval_vs_oracle(B, path):
             assert br[pi] == (0 if bro[pi] == "rf" else 1), (s, pi)
             n_rf += bro[pi] == "rf"
             n_pr += bro[pi] == "pr"
-            if OM.valid(pi, h, n, F, s, P):
-                assert m[pi] == OM.layer_bytes(pi, h, n, F, s, P), (s, pi)
+            kv, act = hd.get("kv") or None, "swiglu" if hd.get("act") else "gelu"
+            if OM.valid(pi, h, n, F, s, P, n_kv=kv, act=act):
+                assert m[pi] == OM.layer_bytes(pi, h, n, F, s, P, n_kv=kv, act=act), (s, pi)
             else:
                 assert m[pi] == 1e300, (s, pi)
     assert n_rf > 100 and n_pr > 100

@@ -3,6 +3,8 @@ columns, switching statistics, and the "w/o RF" bundle (Eq. 9
 with every length on the polynomial branch)."""
 import os
 
+import pytest
+
 from oracle import costmodel as OC
 from paper_2511_13198_b200 import trace as T
 
@@ -113,3 +115,19 @@ def test_planner_crossovers_at_p8():
     fr = {pi: T.predict_frontier(B, model, path, 32, unit, fixed=pi)["s"] for pi in range(B.N_STRATEGIES)}
     ad = T.predict_frontier(B, model, path, 32, unit)["s"]
     assert ad >= 638976 and all(ad >= v for v in fr.values())
+
+
+@pytest.mark.parametrize("n_kv,act", [(None, 0), (8, 0), (8, 1), (32, 1)])
+def test_calibrate_comm_model_equals_oracle_formula(n_kv, act):
+    """The modelled bundles' collective bytes (calibrate.comm_bytes_per_rank) equal the
+    oracle's formula (oracle/flops.comm_bytes, itself pinned to the simulated comm logs),
+    MHA and the Llama variant, every strategy, P = 2 / 4 / 8."""
+    from oracle import flops as OF
+    from paper_2511_13198_b200 import calibrate as CAL
+    h, n, F = 4096, 32, 11264
+    for P in (2, 4, 8):
+        for s in (8192, 65536):
+            for pi in range(6):
+                got = CAL.comm_bytes_per_rank(pi, h, F, s, P, n, n_kv, act)
+                ref = OF.comm_bytes(pi, h, s, P, F, n=n, n_kv=n_kv, act="swiglu" if act else "gelu")
+                assert got == pytest.approx(ref, rel=1e-12, abs=1.0), (pi, P, s)
