@@ -172,7 +172,10 @@ struct Fwd2Cfg {
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
-template <int D>
+// RP (register pass, opt-in PDS_ATTN_FWD=regs): the producer / MMA warpgroup gives
+// registers up (setmaxnreg.dec 56) and each softmax warpgroup takes 224, so a thread
+// holds its whole 128-key S row in registers: one TMEM read per block instead of two.
+template <int D, bool RP = false>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmq, int s,
                        int heads, int causal, __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
@@ -224,7 +227,9 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp < 4) {
+   if (RP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+   if (warp == 0) {
     if (elect_one()) {
       mbar_arrive_expect_tx(q_full, 2 * C::TILE);
       for (int t = 0; t < 2; ++t)
@@ -299,7 +304,9 @@ __global__ void __launch_bounds__(384, 1)
       else if (elect_one()) umma_commit(&o_done[1]);
       __syncwarp();
     }
-  } else if (warp >= 4) {
+   }
+  } else {
+    if (RP) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
     const int tile = (warp - 4) >> 2;        // 0: warps 4-7, 1: warps 8-11
     const int q = warp & 3;
     const int tr = q * 32 + lane;            // row within the tile = TMEM lane
@@ -316,7 +323,19 @@ __global__ void __launch_bounds__(384, 1)
         constexpr bool MASK = decltype(mask_c)::value;
       // pass 1: row max; 16-column TMEM loads software-pipelined (next chunk in flight)
       float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      {
+      uint32_t srow[RP ? BN : 1];                // RP: the whole S row, read once
+      if constexpr (RP) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c)
+          tmem_ld32(lb + s_col + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&srow[c * 32]));
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          float v = __uint_as_float(srow[i]);
+          if (MASK && k0 + i > row) v = -INFINITY;
+          mxa[i & 3] = fmaxf(mxa[i & 3], v);
+        }
+      } else {
         uint32_t cur[16], nxt[16];
         tmem_ld16(lb + s_col, cur);
         tmem_ld_wait();
@@ -358,11 +377,18 @@ __global__ void __launch_bounds__(384, 1)
       const f2 nm2{-m_used, -m_used}, sl2{scale_log2, scale_log2};
       {
         uint32_t cur[16], nxt[16];
-        tmem_ld16(lb + s_col, cur);
-        tmem_ld_wait();
+        if constexpr (!RP) {
+          tmem_ld16(lb + s_col, cur);
+          tmem_ld_wait();
+        }
 #pragma unroll
         for (int c = 0; c < BN / 16; ++c) {
-          if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+          if constexpr (RP) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) cur[i] = srow[c * 16 + i];
+          } else {
+            if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+          }
           uint32_t pk[8];
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
@@ -388,9 +414,11 @@ __global__ void __launch_bounds__(384, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_half[tile]);
           }
-          tmem_ld_wait();
+          if constexpr (!RP) {
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+            for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
+          }
         }
       }
         const f2 rs = add2(rs2[0], rs2[1]);
@@ -2003,11 +2031,17 @@ static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
   if (rc) return (int)cudaErrorInvalidValue;
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
     once = true;
   }
+  static const bool rp = [] {
+    const char* e = getenv("PDS_ATTN_FWD");
+    return e && std::string(e) == "regs";
+  }();
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
-  attn_fwd_tc_kernel<D><<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
+  auto kern = rp ? attn_fwd_tc_kernel<D, true> : attn_fwd_tc_kernel<D, false>;
+  kern<<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
       tm, tmq, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
       scale_log2, qlo, qn, kcol, vcol, grp, segs);
   return (int)cudaGetLastError();

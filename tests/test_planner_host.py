@@ -136,10 +136,12 @@ def _plan_oracle(bd, B, s, L, mask, cap, gamma, cache, prev, wlib):
     h, n, F, P = hd["h"], hd["n"], hd["ffn"], hd["P"]
     present = sorted(bd["strat"])
     t, _ = _oracle_costs(bd, s, present)
-    en = [pi for pi in present if (mask >> pi) & 1 and OM.valid(pi, h, n, F, s, P)]
-    m = {pi: float(OM.layer_bytes(pi, h, n, F, s, P)) for pi in en}
+    kv, act = hd.get("kv") or None, "swiglu" if hd.get("act") else "gelu"
+    en = [pi for pi in present if (mask >> pi) & 1 and OM.valid(pi, h, n, F, s, P, n_kv=kv, act=act)]
+    m = {pi: float(OM.layer_bytes(pi, h, n, F, s, P, n_kv=kv, act=act)) for pi in en}
     w = {pi: float(wlib(pi, s)) for pi in en}
-    assert all(w[pi] >= OM.transient_floor(pi, h, n, F, s, P) for pi in en)
+    if kv is None and act == "gelu":      # the dataflow floor is stated for the MHA + GELU layer
+        assert all(w[pi] >= OM.transient_floor(pi, h, n, F, s, P) for pi in en)
     cached = (1, s) in cache
     plan, inf = OA.alg1(L, t, m, en, cap, cache=cache, key=(1, s), w=w)
     plan2, kept = OA.smooth(plan, prev, t, m, cap, gamma, en, w=w)
@@ -161,7 +163,8 @@ def test_plan_sequence_vs_oracle(B, path, gamma):
 
     def wlib(pi, s):
         if (pi, s) not in wl:
-            m = B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=L)
+            m = B.Model(h=hd["h"], n_heads=hd["n"], ffn=hd["ffn"], n_layers=L, n_kv_heads=hd.get("kv", 0),
+                        ffn_act=hd.get("act", 0))
             wl[(pi, s)] = B.mem_bytes(m, P, pi, s)[1]
         return wl[(pi, s)]
 
