@@ -497,23 +497,23 @@ def test_attention_fwd_pair_kernel_matches(tmp_path, s, causal):
 
 @pytest.mark.parametrize("s,causal", [(640, 1), (1024, 0), (2304, 1)])
 def test_attention_fwd_register_pass_matches(tmp_path, s, causal):
-    """The opt-in register-pass forward (PDS_ATTN_FWD=regs: setmaxnreg reallocation, the
-    S row read from TMEM once) runs the same arithmetic in the same order as the default
-    two-pass softmax: outputs and LSE are bit-identical."""
+    """The register-pass forward (default: setmaxnreg reallocation, the S row read from TMEM
+    once) runs the same arithmetic in the same order as the two-pass softmax
+    (PDS_ATTN_FWD=2pass): outputs and LSE are bit-identical."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for mode in ("1cta", "regs"):
+    for mode in ("2pass", "regs"):
         f = tmp_path / f"{mode}.npz"
         env = dict(os.environ)
         env["PDS_ATTN_FWD"] = mode
         subprocess.run([sys.executable, "-c", _FWD_SCRIPT, root, str(f), str(s), str(causal)], check=True, env=env,
                        timeout=300)
         res[mode] = np.load(f)
-    assert np.array_equal(res["regs"]["out"], res["1cta"]["out"])
-    assert np.array_equal(res["regs"]["lse"], res["1cta"]["lse"])
+    assert np.array_equal(res["regs"]["out"], res["2pass"]["out"])
+    assert np.array_equal(res["regs"]["lse"], res["2pass"]["lse"])
 
 
 # ---------------------------------------------------------------- Llama variant (NEXT-3)
