@@ -26,9 +26,12 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 TOL = 1e-2
-CASES = [  # h, n, F, s, metp_chunks: C1 and a d = 128 shape with 2 METP waves
-    (256, 4, 1024, 512, 0),
-    (1024, 8, 4096, 2048, 2),
+CASES = [  # h, n, F, s, metp_chunks, n_kv, act, varlen lens: C1, a d = 128 shape with 2 METP waves,
+           # the Llama variant (GQA 16 -> 8, SwiGLU) and varlen packing (TS / UZ / METP / METP-full)
+    (256, 4, 1024, 512, 0, None, "gelu", None),
+    (1024, 8, 4096, 2048, 2, None, "gelu", None),
+    (2048, 16, 2048, 2048, 2, 8, "swiglu", None),
+    (1024, 8, 2048, 2048, 2, None, "gelu", [512, 1024, 512]),
 ]
 
 
@@ -60,28 +63,40 @@ def run_rank():
         return t.float().cpu().numpy().astype(np.float64)
 
     failures = []
-    for (h, n, F, s, chunks) in CASES:
-        if n % P or (s // P) % 128 or (chunks and (s // P // chunks) % 128):
+    for (h, n, F, s, chunks, n_kv, act, lens) in CASES:
+        if n % P or (n_kv or n) % P or (s // P) % 128 or (chunks and (s // P // chunks) % 128):
             continue
-        d = layer_inputs(h, n, F, s, 1, seed=21)
-        y_ref, c = OL.layer_fwd(d["x"], d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
-        g_ref = OL.layer_bwd(d["dy"], c, d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"], n=n)
-        W = OS.shard_weights(d, n, P)
+        d = layer_inputs(h, n, F, s, 1, seed=21, n_kv=n_kv, act=act)
+        wargs = (d["w_qkv"], d["w_proj"], d["w_in"], d["w_out"], d["g1"], d["g2"])
+        kw = dict(n=n, n_kv=n_kv, act=act)
+        if lens:
+            y_ref, cs = OL.layer_fwd_varlen(d["x"], lens, *wargs, **kw)
+            g_ref = OL.layer_bwd_varlen(d["dy"], cs, lens, *wargs, **kw)
+            c = dict(o=np.concatenate([q["o"] for q in cs]), z=np.concatenate([q["z"] for q in cs]))
+        else:
+            y_ref, c = OL.layer_fwd(d["x"], *wargs, **kw)
+            g_ref = OL.layer_bwd(d["dy"], c, *wargs, **kw)
+        W = OS.shard_weights(d, n, P, n_kv=n_kv, act=act)
         ref_sh = OS.shard_weights(dict(w_qkv=g_ref["dw_qkv"], w_proj=g_ref["dw_proj"], w_in=g_ref["dw_in"],
-                                       w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P)
+                                       w_out=g_ref["dw_out"], g1=g_ref["dg1"], g2=g_ref["dg2"]), n, P,
+                                  n_kv=n_kv, act=act)
         sl = s // P
         rows = slice(rank * sl, (rank + 1) * sl)
         obj = [B.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks), P=P, rank=rank, device=local,
-                        uid=obj[0])
+        ctx = B.Context(B.Model(h=h, n_heads=n, ffn=F, metp_chunks=chunks, n_kv_heads=n_kv or 0,
+                                ffn_act=1 if act == "swiglu" else 0), P=P, rank=rank, device=local, uid=obj[0])
+        if lens:
+            ctx.set_varlen(lens)
         st = torch.cuda.current_stream().cuda_stream
         keys = ("w_qkv_t", "w_proj", "w_in_t", "w_out", "g1", "g2")
         w = {k: dev(W[k][rank]) for k in keys}
         Wp = B.Weights(*(w[k].data_ptr() for k in keys))
         x = dev(d["x"][rows, 0])
         dy = dev(d["dy"][rows, 0])
-        for pi in range(B.N_STRATEGIES):
+        for pi in ((0, 1, 2, 4) if lens else range(B.N_STRATEGIES)):
+            if pi == 3 and (s // P) % 256:
+                continue                       # MegatronCZ's zigzag half-chunks (R-CZ)
             res = []
             for ov in (0, 1):
                 ctx.set_overlap(ov)
@@ -101,7 +116,7 @@ def run_rank():
             bad = {k: v for k, v in chk.items() if not v < TOL}
             same = all(np.array_equal(a, b) for a, b in ((y0, y1), (dx0, dx1), (o0, o1), (z0, z1))) and \
                 all(np.array_equal(g0[k], g1[k]) for k in keys)
-            tag = f"P={P} rank={rank} h={h} s={s} pi={pi}"
+            tag = f"P={P} rank={rank} h={h} s={s} pi={pi} kv={n_kv} {act} varlen={lens}"
             if bad or not same:
                 failures.append(f"{tag}: bad={bad} overlap_bitwise={same}")
             elif rank == 0:
