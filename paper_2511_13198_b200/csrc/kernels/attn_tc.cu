@@ -169,14 +169,20 @@ struct Fwd2Cfg {
   static constexpr int K_OFF = 2 * TILE;          // [2 stages]
   static constexpr int V_OFF = K_OFF + 2 * TILE;  // [2 stages]
   static constexpr int BAR_OFF = V_OFF + 2 * TILE;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int RED_OFF = BAR_OFF + 256;           // NS = 2: row-max / row-sum exchange
+  static constexpr int SMEM = RED_OFF + 2 * 2 * 2 * 128 * 4 + 1024;
 };
 
 // RP (register pass, the default; PDS_ATTN_FWD=2pass: off): the producer / MMA warpgroup gives
 // registers up (setmaxnreg.dec 56) and each softmax warpgroup takes 224, so a thread
 // holds its whole 128-key S row in registers: one TMEM read per block instead of two.
-template <int D, bool RP = false>
-__global__ void __launch_bounds__(384, 1)
+// NS (softmax warpgroups per query tile, opt-in PDS_ATTN_FWD=split for NS = 2): with two,
+// each warpgroup owns half of the 128 keys of a block (threads of both hold the same rows,
+// TMEM lanes), the row max and the final row sum are exchanged through shared memory
+// under a named barrier per tile, and the half-0 warpgroup alone releases the first PV
+// half: a tile's softmax latency per block is halved.
+template <int D, bool RP = false, int NS = 1>
+__global__ void __launch_bounds__(128 + 256 * NS, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmq, int s,
                        int heads, int causal, __nv_bfloat16* __restrict__ out, int64_t ld_out, float* __restrict__ lse,
                        float scale_log2, int qlo, int qn, int kcol, int vcol, int grp,
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 4 * NS);
       mbar_init(&p_half[i], 4);
       mbar_init(&o_done[i], 1);
     }
@@ -306,31 +312,42 @@ __global__ void __launch_bounds__(384, 1)
     }
    }
   } else {
-    if (RP) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
-    const int tile = (warp - 4) >> 2;        // 0: warps 4-7, 1: warps 8-11
+    // the pool is the CTA's launch allocation (threads x compiled count: 384 x 168 / 640 x 96),
+    // so the increase is what WG0's decrease frees: 224 (NS = 1), 104 (NS = 2)
+    if (RP) {
+      if (NS == 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+      else asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    }
+    constexpr int KC = BN / NS;              // keys (S columns) per softmax warpgroup
+    constexpr int OC = D / NS;               // O columns per softmax warpgroup
+    const int wgi = (warp - 4) >> 2;
+    const int tile = wgi / NS;               // NS = 1: 0 = warps 4-7, 1 = warps 8-11
+    const int half = wgi % NS;               // NS = 2: keys [half KC, (half + 1) KC)
     const int q = warp & 3;
     const int tr = q * 32 + lane;            // row within the tile = TMEM lane
     const int row = q0 + tile * 128 + tr;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t s_col = tile * 128, o_col = 256 + tile * 128;
+    const uint32_t s_col = tile * 128 + half * KC, o_col = 256 + tile * 128 + half * OC;
+    float* red = reinterpret_cast<float*>(sm + C::RED_OFF);   // [2 parity][2 tiles][2 halves][128]
+    auto tile_sync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + tile) : "memory"); };
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[tile], j & 1);
       tc_fence_after();
-      const int k0 = (kb0 + j) * BN;
-      const bool mask = causal && (k0 + BN - 1 > q0 + tile * 128);
+      const int k0 = (kb0 + j) * BN + half * KC;      // this warpgroup's first key
+      const bool mask = causal && (k0 + KC - 1 > q0 + tile * 128);
       auto block = [&](auto mask_c) {
         constexpr bool MASK = decltype(mask_c)::value;
       // pass 1: row max; 16-column TMEM loads software-pipelined (next chunk in flight)
       float mxa[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      uint32_t srow[RP ? BN : 1];                // RP: the whole S row, read once
+      uint32_t srow[RP ? KC : 1];                // RP: the whole S row, read once
       if constexpr (RP) {
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c)
+        for (int c = 0; c < KC / 32; ++c)
           tmem_ld32(lb + s_col + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&srow[c * 32]));
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
+        for (int i = 0; i < KC; ++i) {
           float v = __uint_as_float(srow[i]);
           if (MASK && k0 + i > row) v = -INFINITY;
           mxa[i & 3] = fmaxf(mxa[i & 3], v);
@@ -340,8 +357,8 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld16(lb + s_col, cur);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < BN / 16; ++c) {
-          if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+        for (int c = 0; c < KC / 16; ++c) {
+          if (c + 1 < KC / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float v = __uint_as_float(cur[i]);
@@ -353,13 +370,19 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; ++i) cur[i] = nxt[i];
         }
       }
-      const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
+      float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
+      if constexpr (NS == 2) {                 // the row max over both halves of the keys
+        float* rb = red + ((j & 1) * 4 + tile * 2) * 128;
+        rb[half * 128 + tr] = mx;
+        tile_sync();
+        mx = fmaxf(mx, rb[(half ^ 1) * 128 + tr]);
+      }
       const float m_new = mx * scale_log2;
       const bool need = m_new > m_used + 8.0f;
       if (j > 0 && __any_sync(0xffffffff, need)) {
         const float f = need ? ex2(m_used - m_new) : 1.0f;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < OC / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(lb + o_col + c * 32, r);
           tmem_ld_wait();
@@ -382,12 +405,12 @@ __global__ void __launch_bounds__(384, 1)
           tmem_ld_wait();
         }
 #pragma unroll
-        for (int c = 0; c < BN / 16; ++c) {
+        for (int c = 0; c < KC / 16; ++c) {
           if constexpr (RP) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) cur[i] = srow[c * 16 + i];
           } else {
-            if (c + 1 < BN / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
+            if (c + 1 < KC / 16) tmem_ld16(lb + s_col + (c + 1) * 16, nxt);
           }
           uint32_t pk[8];
 #pragma unroll
@@ -407,8 +430,8 @@ __global__ void __launch_bounds__(384, 1)
             rs2[(i >> 1) & 1] = add2(rs2[(i >> 1) & 1], p);
             pk[i >> 1] = pack_bf16(p.x, p.y);
           }
-          tmem_st8(lb + s_col + c * 8, pk);
-          if (c == BN / 32 - 1) {             // P of keys 0..63 complete: release the first PV half
+          tmem_st8(lb + tile * 128 + (half * KC) / 2 + c * 8, pk);   // packed P of keys half KC + 16c..
+          if (half * KC + (c + 1) * 16 == BN / 2) {   // P of keys 0..63 complete: release the first PV half
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -433,11 +456,17 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_wait(&o_done[tile], 0);
     tc_fence_after();
+    if constexpr (NS == 2) {                   // the row sum over both halves of the keys
+      float* rb = red + ((nkv & 1) * 4 + tile * 2) * 128;   // the parity buffer block nkv - 2 used
+      rb[half * 128 + tr] = l;
+      tile_sync();
+      l += rb[(half ^ 1) * 128 + tr];
+    }
     const float inv = 1.0f / l;
     const bool ok = row < qlo + qn;
-    __nv_bfloat16* o = out + (int64_t)(row - qlo) * ld_out + head * D;
+    __nv_bfloat16* o = out + (int64_t)(row - qlo) * ld_out + head * D + half * OC;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < OC / 32; ++c) {
       uint32_t r[32];
       tmem_ld32(lb + o_col + c * 32, r);
       tmem_ld_wait();
@@ -451,7 +480,7 @@ __global__ void __launch_bounds__(384, 1)
                              pack_bf16(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
       }
     }
-    if (ok) lse[(int64_t)head * qn + (row - qlo)] = (m_used + log2f(l)) * LN2;
+    if (ok && half == 0) lse[(int64_t)head * qn + (row - qlo)] = (m_used + log2f(l)) * LN2;
   }
   tc_fence_before();
   __syncthreads();
@@ -2031,19 +2060,31 @@ static int fwd_tc_t(const void* q, int64_t ld_q, uint64_t q_rows, const void* kv
   if (rc) return (int)cudaErrorInvalidValue;
   static bool once = false;
   if (!once) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Fwd2Cfg<D>::SMEM);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Fwd2Cfg<D>::SMEM);
     once = true;
   }
   // register pass by default: bit-identical to the two-pass softmax, 0.3 % faster at fixed
   // clocks, ~1 % event-timed (profiles/raw_r02/ab_fwd_*); PDS_ATTN_FWD=2pass selects the latter
-  static const bool rp = [] {
+  static const int fmode = [] {               // 0: two-pass, 1: register pass, 2: split (NS = 2)
     const char* e = getenv("PDS_ATTN_FWD");
-    return !(e && std::string(e) == "2pass");
+    if (e && std::string(e) == "2pass") return 0;
+    if (e && std::string(e) == "split") return 2;
+    return 1;
   }();
+  static bool once2 = false;
+  if (!once2) {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<D, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Fwd2Cfg<D>::SMEM);
+    once2 = true;
+  }
   const float scale_log2 = (1.0f / sqrtf((float)D)) * LOG2E;
-  auto kern = rp ? attn_fwd_tc_kernel<D, true> : attn_fwd_tc_kernel<D, false>;
-  kern<<<dim3((qn + 255) / 256, heads), 384, Fwd2Cfg<D>::SMEM, st>>>(
+  auto kern = fmode == 2 ? attn_fwd_tc_kernel<D, true, 2>
+                         : fmode == 1 ? attn_fwd_tc_kernel<D, true, 1> : attn_fwd_tc_kernel<D, false, 1>;
+  const int nthr = fmode == 2 ? 128 + 512 : 384;
+  kern<<<dim3((qn + 255) / 256, heads), nthr, Fwd2Cfg<D>::SMEM, st>>>(
       tm, tmq, s, heads, causal, reinterpret_cast<__nv_bfloat16*>(out), ld_out, reinterpret_cast<float*>(lse),
       scale_log2, qlo, qn, kcol, vcol, grp, segs);
   return (int)cudaGetLastError();

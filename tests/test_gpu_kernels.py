@@ -516,6 +516,29 @@ def test_attention_fwd_register_pass_matches(tmp_path, s, causal):
     assert np.array_equal(res["regs"]["lse"], res["2pass"]["lse"])
 
 
+@pytest.mark.parametrize("s,causal", [(640, 1), (1024, 0), (2304, 1)])
+def test_attention_fwd_split_softmax_matches(tmp_path, s, causal):
+    """The opt-in split-softmax forward (PDS_ATTN_FWD=split: two warpgroups per query tile,
+    row max / row sum exchanged through shared memory) agrees with the default forward
+    (the row sum is added in two partial sums: rounding-level differences only)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode in ("regs", "split"):
+        f = tmp_path / f"{mode}.npz"
+        env = dict(os.environ)
+        env["PDS_ATTN_FWD"] = mode
+        subprocess.run([sys.executable, "-c", _FWD_SCRIPT, root, str(f), str(s), str(causal)], check=True, env=env,
+                       timeout=300)
+        res[mode] = np.load(f)
+    a = (res["regs"]["out"].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    b = (res["split"]["out"].view(np.uint16).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    assert rel(b, a) < 1e-3
+    assert np.allclose(res["split"]["lse"], res["regs"]["lse"], rtol=0, atol=1e-5)
+
+
 # ---------------------------------------------------------------- Llama variant (NEXT-3)
 @pytest.mark.parametrize("d,heads,kv_heads", [(128, 4, 1), (128, 4, 2), (64, 8, 2)])
 @pytest.mark.parametrize("causal", [1, 0])
