@@ -259,3 +259,20 @@ def test_host_only_context_rejects_layer_calls(B):
         ctx.reserve(512)
     assert e.value.code == -7
     ctx.close()
+
+
+def test_variant_bundle_checked_against_context(B):
+    """A Llama-variant bundle (header 'kv 8 act 1') loads only into a context of that
+    variant; an MHA / GELU context with the same (P, h, n, ffn) is refused."""
+    path = os.path.join(ROOT, "paper_2511_13198_b200", "bundles", "h8192_n64_kv8_swiglu_f28672_P1.txt")
+    assert os.path.exists(path)
+    ok = B.Context(B.Model(h=8192, n_heads=64, ffn=28672, n_layers=8, n_kv_heads=8, ffn_act=1), P=1, device=-1)
+    ok.load_costs(path)
+    ok.close()
+    for kv, act in ((0, 0), (8, 0), (0, 1), (16, 1)):
+        bad = B.Context(B.Model(h=8192, n_heads=64, ffn=28672, n_layers=8, n_kv_heads=kv, ffn_act=act), P=1,
+                        device=-1)
+        with pytest.raises(B.PdsError) as e:
+            bad.load_costs(path)
+        assert e.value.code == -1
+        bad.close()
