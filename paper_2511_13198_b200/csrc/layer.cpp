@@ -1067,7 +1067,7 @@ pds_status cz_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w, 
   }
   {
     // RoPE^T at the zig positions, bf16, [dQ | dK | dV] zig rows
-    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 3 * h * 6);
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * qw * 6);
     const int64_t b0 = z.hc(0) * z.c, b1 = z.hc(1) * z.c;
     PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)e.d, e.c->rope, b0, b1, (int)z.cb, (int)e.b,
                                  dqkvz, qw, e.st), "dq rope_t"));
@@ -1304,7 +1304,7 @@ pds_status col_bwd(Exec& e, const void* dy, pds_saved* sv, const pds_weights* w,
     return PDS_OK;
   }));
   {
-    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * 2 * h * 6);
+    Prof p(e.c, e.st, K_NORM, 0, (double)e.sl * (h + hk) * 6);
     const int64_t b0 = e.r * sp;
     PDS_TRY(kerr(rope_t_f32_bf16(dqacc, h, (int)e.sl, (int)h, (int)d, e.c->rope, b0, b0, (int)e.sl, (int)b, dqkv,
                                  qw, e.st), "dq rope_t"));
