@@ -831,10 +831,14 @@ static int launch2_t(const GemmArgs& g, const EpiParams& ep, cudaStream_t st) {
   RowMap am{g.a_seg > 0 ? g.a_seg : (int64_t)1 << 40, g.a_stride, g.a_base};
   RowMap bm{g.b_seg > 0 ? g.b_seg : (int64_t)1 << 40, g.b_stride, g.b_base};
   static const int env_gm = [] { const char* e = getenv("PDS_GEMM_GM"); return e ? atoi(e) : 0; }();
+  static const int env_short = [] { const char* e = getenv("PDS_GEMM_GM_SHORT"); return e ? atoi(e) : 0; }();
   // CTA-pair raster band: 8 m-blocks (2048 rows).  At fixed clocks 16 was best, but
   // under the 1000 W power cap 8 reads less DRAM and won 5 of 6 interleaved whole-bench
-  // rounds (+0.7 %, profiles/round1_ab_gemm_group_m*.txt); PDS_GEMM_GM overrides.
-  const int group_m = env_gm > 0 ? env_gm : 8;
+  // rounds (+0.7 %, profiles/round1_ab_gemm_group_m*.txt); 32 lost 4 % (raw_r02/gm_*).
+  // Short-K GEMMs (K <= 4096: QKV, proj, FC1, dG, dA) read the least DRAM with a band of
+  // 16 (fixed clocks, s = 16K FC1 shape: 1.68 GB vs 2.68 GB at 8, same time); long-K
+  // GEMMs keep 8.  PDS_GEMM_GM overrides both, PDS_GEMM_GM_SHORT the short-K band.
+  const int group_m = env_gm > 0 ? env_gm : (g.K <= 4096 ? (env_short > 0 ? env_short : 16) : 8);
   kern<<<2 * ncl, 384, SMEM, st>>>(ta, tb, g.M, g.N, g.K, am, bm, ep, group_m);
   return (int)cudaGetLastError();
 }
