@@ -147,7 +147,7 @@ extern "C" pds_status pds_k_attn_bwd(const void* qkv, int64_t ld, const void* ou
     acc = static_cast<float*>(scratch);
     ctr = reinterpret_cast<int*>(static_cast<char*>(scratch) + acc_b);
   } else if (attn_bwd_mode() == 2 && (dsb_bytes = attn_ds_bytes(s, heads, heads, d, causal, kDsBudget)) > 0) {
-    PDS_TRY(grow((size_t)dsb_bytes));               // dS through HBM (reading R-DS)
+    PDS_TRY(grow((size_t)dsb_bytes));               // dS through HBM
     dsb = scratch;
   }
   pds_status r = rc2s(attn_bwd(qkv, ld, out, ld_out, lse, dout, s, heads, d, causal, dqkv, nullptr, dd, st, acc, ctr,

@@ -286,7 +286,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * S * 2);
       push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
-      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd; never at kDsMaxPos = 0)
       if (P > 1) push(p.ws, tw, "gather2", S * h * 2);      // bwd re-gathers prefetched on the side stream
       break;
     case PDS_ULYSSES_Z: {
@@ -319,7 +319,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * SL * 2);
       push(p.ws, tw, "wt", h * std::max(f1wf, qwf) * 2);
       push(p.ws, tw, "actr", actr);
-      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd; never at kDsMaxPos = 0)
       break;
     }
     case PDS_METP:
@@ -357,7 +357,7 @@ pds_status make_plan(const pds_model& m, int P, int strategy, int64_t s, BufPlan
       push(p.ws, tw, "tb", h * P * W * 2);
       push(p.ws, tw, "wt", h * std::max(f1w, qw) * 2);
       push(p.ws, tw, "actr", actr);
-      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd, R-DS)
+      if (dsb) push(p.ws, tw, "dsb", dsb);                  // dS through HBM (attention bwd; never at kDsMaxPos = 0)
       if (full) push(p.ws, tw, "qkv", S * qw * 2);
       break;
     }

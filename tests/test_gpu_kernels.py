@@ -638,7 +638,7 @@ def test_gemm_rope_gqa_groups():
     assert rel(host(c), ref) < 1e-2
 
 
-# ---------------------------------------------------------------- dS through HBM (R-DS)
+# ---------------------------------------------------------------- dS through HBM
 @pytest.mark.parametrize("s,heads", [(256, 2), (640, 3), (1152, 4)])
 def test_attention_bwd_ds_path_vs_oracle(s, heads):
     """Backward with dS through HBM (pds_set_attn_bwd(2)): the dK/dV kernel also stores
